@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""Benchmark of the build stage (leaf elimination + hierarchical merges +
+root inverse) and the solve stage on B200.
+
+A step = one full build of the BASELINE workload (default configs[1]:
+Helmholtz kappa=40, n=512 interior, 16x16 leaves, dense FP64 merges) from a
+stencil resident in HBM, plus G applied to the config's Dirichlet vectors
+(16 for configs[1]). value = grid points/s over all ranks. e2e = the same
+metric through the public API with host buffers (stencil H2D, vectors H2D,
+DtN matrix S and the solution D2H inside the timed region).
+
+--impl reference: the reference's CPU path (restated C++ port of
+proj/src/dense_nd.cpp with OpenBLAS; the reference itself needs Eigen, which
+is not in this image) on all host cores, same metric and workload.
+
+Multi-GPU (torchrun): independent replicas, one per GPU (weak scaling);
+subtree sharding of one build is the next step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    1: dict(name="laplace", n_int=256, leaf=16, nvec=1, oracle=("laplace", 0.0)),
+    2: dict(name="helmholtz_k40", n_int=512, leaf=16, nvec=16, oracle=("helmholtz", 40.0)),
+}
+METRIC = "build grid-points/s"
+
+
+def fp64_peak():
+    """Measured FP64 peak (cuBLAS DGEMM 8192^3 on this pool, tools/probe/fp64_peak.py);
+    MEASURED_PEAKS.json carries no FP64 entry."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_fp64_peak.json")) as f:
+            d = json.load(f)
+        return float(d["dgemm_tflops"]), "measured (profiles/r01_fp64_peak.json, cuBLAS DGEMM burst)"
+    except Exception:
+        return 37.0, "fallback (DMMA instruction-rate probe)"
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.lines, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                pass
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def seeded_vectors(nb: int, nvec: int, seed: int = 1) -> np.ndarray:
+    rng = np.random.Generator(np.random.MT19937(seed))
+    return np.asfortranarray(rng.uniform(-1.0, 1.0, (nb, nvec)))
+
+
+# ------------------------------------------------------------------ reference arm
+def cpu_oracle_step(cfg, threads):
+    from oracle import oracle as O
+    n = cfg["n_int"] + 2
+    p = O.Problem(cfg["oracle"][0], n, cfg["oracle"][1])
+    t = O.Tree(n, uniform_side=cfg["leaf"])
+    t0 = time.perf_counter()
+    r = O.build_root_dense(p, t, threads=threads, mode=2)
+    X = seeded_vectors(len(r.boundary), cfg["nvec"])
+    Y = r.G @ X  # numpy/OpenBLAS DGEMM on the same cores
+    dt = time.perf_counter() - t0
+    return dt, float(np.linalg.norm(Y))
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_oracle_step(cfg, threads)
+    times = [cpu_oracle_step(cfg, threads)[0] for _ in range(args.steps)]
+    total = sum(times)
+    value = args.steps * cfg["n_int"] ** 2 / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "grid-points/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config{args.config}: {cfg['name']} n={cfg['n_int']} interior, "
+                               f"{cfg['leaf']}x{cfg['leaf']} leaves, dense, {cfg['nvec']} vectors"},
+        "cpu_baseline": {"value": value, "unit": "grid-points/s", "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} full builds + G*X ({cfg['nvec']} vectors), C++ restatement of "
+                                   "dense_nd.cpp with OpenBLAS (Eigen absent; reference not buildable)"},
+        "e2e": {"value": value, "unit": "grid-points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ B200 arm
+def run_b200(args, cfg, rank, world, local):
+    import torch
+    import paper_1302_5995_b200 as dtn
+
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    ctx = dtn.Context(local)
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+
+    n_int, nvec = cfg["n_int"], cfg["nvec"]
+    n = n_int + 2
+    spec = dtn.baseline_problem(args.config, n_int)
+    op = dtn.discretize(spec)
+    tree = dtn.build_tree_uniform(n, cfg["leaf"])
+    nb = 4 * n_int - 4
+    # inputs resident in HBM for the device-timed value
+    stencil_d = torch.from_numpy(op.stencil).to(dev)
+    X_h = seeded_vectors(nb, nvec)
+    X_d = torch.from_numpy(X_h).to(dev).t().contiguous().t()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+
+    def device_step():
+        sol = dtn.build_root_gpu(None, tree, ctx=ctx, stencil_device_ptr=stencil_d.data_ptr())
+        Y = dtn.apply_dtn(sol, X_d)
+        return sol, Y
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        sol, _ = device_step()
+        sol.free()
+    barrier()
+    events = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            sol, Y = device_step()
+            e1.record(stream)
+            stats = sol.build_stats
+            sol.free()
+            events.append((e0, e1))
+        barrier()
+    dev_ms = sum(a.elapsed_time(b) for a, b in events)
+    t_local = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t_local, op=torch.distributed.ReduceOp.MAX)
+    total_ms = float(t_local.item())
+    value = world * args.steps * n_int ** 2 / (total_ms * 1e-3)
+    launches_per_step = stats["launches"] + 1
+
+    # ---- e2e through the public API, host (pinned) buffers
+    pin_st = torch.empty(op.stencil.shape, dtype=torch.float64, pin_memory=True).numpy()
+    pin_st[...] = op.stencil
+    op_h = dtn.DiscreteOperator(op.n, op.h, op.mode, pin_st)
+    pin_x = torch.empty((nvec, nb), dtype=torch.float64, pin_memory=True).numpy().T
+    pin_x[...] = X_h
+    for _ in range(max(1, args.warmup // 2)):
+        s = dtn.build_root_gpu(op_h, tree, ctx=ctx)
+        dtn.apply_dtn(s, pin_x)
+        s.S_dense
+        s.free()
+    barrier()
+    e2e_times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        s = dtn.build_root_gpu(op_h, tree, ctx=ctx)
+        Yh = dtn.apply_dtn(s, pin_x)
+        Sh = s.S_dense
+        torch.cuda.synchronize(dev)
+        e2e_times.append(time.perf_counter() - t0)
+        s.free()
+    t_e2e = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t_e2e, op=torch.distributed.ReduceOp.MAX)
+    e2e_value = world * args.steps * n_int ** 2 / float(t_e2e.item())
+
+    # ---- per-kernel roofline from one profiled build (not timed above)
+    prof = dtn.build_root_gpu(None, tree, ctx=ctx, stencil_device_ptr=stencil_d.data_ptr(), profile=True)
+    ks = prof.kernel_stats
+    prof.free()
+    peak_tf, peak_src = fp64_peak()
+    hbm, hbm_src = hbm_peak()
+    dom_name, dom = max(ks.items(), key=lambda kv: kv[1]["ms"])
+    total_prof_ms = sum(v["ms"] for v in ks.values())
+    if dom["flops"] > 0:
+        achieved = dom["flops"] / (dom["ms"] * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                "frac": achieved / peak_tf, "traffic": None, "kernel": dom_name,
+                "share_of_build": dom["ms"] / total_prof_ms, "launches": dom["launches"],
+                "avg_launch_ms": dom["ms"] / max(1, dom["launches"]), "peak_source": peak_src + " (FP64 DMMA)"}
+    else:
+        achieved = dom["bytes"] / (dom["ms"] * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": None, "kernel": dom_name, "share_of_build": dom["ms"] / total_prof_ms,
+                "peak_source": hbm_src}
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+            roof["traffic"] = json.load(f).get(dom_name)
+    except Exception:
+        pass
+
+    merge_tf = stats["merge_flops"] / (stats["merge_ms"] * 1e-3) / 1e12 if stats["merge_ms"] > 0 else None
+    line = {
+        "metric": METRIC, "value": value, "unit": "grid-points/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE config shapes)",
+        "config": {"workload": f"config{args.config}: {cfg['name']} n={n_int} interior (ref n={n}), "
+                               f"{cfg['leaf']}x{cfg['leaf']} leaves, dense FP64 merges, G applied to "
+                               f"{nvec} uniform[-1,1] vectors",
+                   "parallelism": f"replicas x{world}", "l2": "flushed between timed steps (256 MB write)"},
+        "e2e": {"value": e2e_value, "unit": "grid-points/s",
+                "h2d_bytes_per_step": int(op.stencil.nbytes + X_h.nbytes),
+                "d2h_bytes_per_step": int(nb * nb * 8 + nb * nvec * 8)},
+        "gpu_launches": launches_per_step * args.steps,
+        "roofline": roof,
+        "clocks": clk.summary(),
+        "build": {"build_ms": stats["build_ms"], "leaf_ms": stats["leaf_ms"], "merge_ms": stats["merge_ms"],
+                  "inverse_ms": stats["inverse_ms"], "merge_gflop": stats["merge_flops"] / 1e9,
+                  "merge_tflops": merge_tf,
+                  "merge_frac_fp64_peak": merge_tf / peak_tf if merge_tf else None,
+                  "build_tflops_algorithmic": (stats["merge_flops"] + stats["inverse_flops"]) /
+                  (stats["build_ms"] * 1e-3) / 1e12,
+                  "solve_vectors_per_s": None},
+        "kernels": {k: {"ms": round(v["ms"], 4), "launches": v["launches"],
+                        "tflops": (v["flops"] / (v["ms"] * 1e-3) / 1e12) if v["ms"] > 0 and v["flops"] else None}
+                    for k, v in ks.items() if v["launches"]},
+    }
+    # solve throughput (device-resident, the configured batch)
+    sol = dtn.build_root_gpu(None, tree, ctx=ctx, stencil_device_ptr=stencil_d.data_ptr())
+    for _ in range(3):
+        dtn.apply_dtn(sol, X_d)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    reps = 20
+    for _ in range(reps):
+        dtn.apply_dtn(sol, X_d)
+    e1.record(stream)
+    e1.synchronize()
+    line["build"]["solve_vectors_per_s"] = reps * nvec / (e0.elapsed_time(e1) * 1e-3)
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            dts = [cpu_oracle_step(cfg, threads)[0] for _ in range(3)]
+            dt = statistics.median(dts)
+            line["cpu_baseline"] = {"value": n_int ** 2 / dt, "unit": "grid-points/s", "cores": threads,
+                                    "kind": "port", "sample": f"median of 3 full config{args.config} builds + G*X, "
+                                    "C++ restatement of dense_nd.cpp (OpenBLAS, all cores)"}
+            # parity of this run's operator against the oracle (not timed)
+            from oracle import oracle as O
+            ref = O.build_root_dense(O.Problem(cfg["oracle"][0], n, cfg["oracle"][1]),
+                                     O.Tree(n, uniform_side=cfg["leaf"]), threads=threads, mode=2)
+            line["parity"] = {"S_rel_fro": O.rel_fro(sol.S_dense, ref.S),
+                              "Sg_rel_fro": O.rel_fro(sol.S_dense @ X_h, ref.S @ X_h), "tol": 1e-10}
+        except Exception as e:  # pragma: no cover
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    sol.free()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+    else:
+        run_b200(args, cfg, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

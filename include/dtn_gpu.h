@@ -1,0 +1,125 @@
+/* dtn_gpu.h — C ABI of the B200-native build/solve engine for the
+ * Gillman–Martinsson nested-dissection DtN build (arXiv 1302.5995).
+ *
+ * Drop-in boundary for the reference's dense engine (/root/reference/proj):
+ *   dtn_gpu_build        replaces build_root_dense_op / build_with_loads(..., Engine::dense, ...)
+ *                        (proj/include/dtn/accel_nd.hpp:98-100, proj/src/bodyload.cpp:47-57,
+ *                         proj/src/dense_nd.cpp:196-225)
+ *   dtn_gpu_boundary     SolutionOperator::boundary / root_boundary (solution_operator.hpp:33,65)
+ *   dtn_gpu_export       SolutionOperator::S_dense, G_dense, cond_estimate (solution_operator.hpp:36,44)
+ *   dtn_gpu_apply        apply_dtn (which=0, G*g) / apply_schur (which=1, S*g)
+ *                        (solution_operator.hpp:55-59, solution_operator.cpp:36-52), batched
+ *   dtn_gpu_box_schur    SchurData::S of any box of the build tree (dense_nd.hpp:18-26)
+ *   dtn_gpu_level_stats  SolutionOperator::level_stats (solution_operator.hpp:18-23,46)
+ *   dtn_discretize_*     discretize (grid.hpp:111, grid.cpp:106-168) as 5-point stencil arrays
+ *
+ * All matrices are column-major FP64. The boundary is the canonical CCW ring
+ * of root unknowns starting at the south-west corner (grid.cpp:170-190), of
+ * size 4(n-2)-4 with n the reference grid size including the Dirichlet ring.
+ *
+ * Return codes (errors.hpp, harness.hpp:11-12): 0 ok, 2 invalid argument,
+ * 3 singular block (FactorizationError; dtn_gpu_last_error carries the
+ * "what [where]" text), 5 CUDA failure. There is no CPU fallback: without a
+ * usable sm_100a device every build returns 5.
+ */
+#ifndef DTN_GPU_H
+#define DTN_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dtn_ctx dtn_ctx;
+typedef struct dtn_op dtn_op;
+
+#define DTN_OK 0
+#define DTN_EINVAL 2
+#define DTN_ESINGULAR 3
+#define DTN_ECUDA 5
+
+typedef struct {
+  int32_t n;               /* grid side including the Dirichlet ring (grid.hpp:29-35) */
+  const double* stencil;   /* 5 x (n-2)^2 SoA: center, east, west, north, south, unknown_id order
+                              (grid.hpp:68-70); couplings to ring nodes are ignored */
+  int32_t stencil_on_device; /* 1: stencil is a device pointer on the context's device */
+} dtn_problem;
+
+typedef struct {
+  int32_t engine;      /* 0 = dense (Engine::dense, solution_operator.hpp:15) */
+  int32_t n_leaf;      /* build_tree leaf capacity (grid.hpp:159), used when leaf_side == 0 */
+  int32_t leaf_side;   /* > 0: uniform tree of leaf_side^2 leaves, requires n-2 = leaf_side*2^L */
+  int32_t want_G;      /* compute G = S^{-1} and cond_estimate (dense_nd.cpp:218-224) */
+  int32_t micro_max;   /* leaf elimination granularity (unknowns per one-CTA box); 0 = default */
+  int32_t profile;     /* 1: no graph, CUDA events around every launch (dtn_gpu_kernel_stats) */
+  double epsilon;      /* compressed engine tolerance (AccelOptions::epsilon) — reserved */
+  int64_t crossover;   /* AccelOptions::crossover — reserved */
+} dtn_opts;
+
+typedef struct {
+  int32_t level;       /* reference tree level (root = 0) */
+  int32_t boxes;       /* boxes merged at this level */
+  int64_t max_boundary;
+  double seconds;      /* device time of this level's waves */
+  double flops;        /* algorithmic merge flops of this level (SURVEY 8d formula) */
+} dtn_level_stats;
+
+typedef struct {
+  double build_ms;        /* device time of the whole build (leaf + merges + root inverse) */
+  double leaf_ms;         /* device time below the reference leaves */
+  double merge_ms;        /* device time of the reference-tree merges */
+  double inverse_ms;      /* device time of G = S^{-1} */
+  double merge_flops;     /* algorithmic flops of the reference-tree merges */
+  double leaf_flops;      /* flops of the in-leaf dense eliminations */
+  double inverse_flops;   /* 2 nb^3 */
+  int32_t waves;
+  int32_t launches;       /* kernels launched by one build */
+} dtn_build_stats;
+
+typedef struct {
+  char name[16];          /* kernel class */
+  int32_t launches;
+  double ms;              /* summed device time (profiled build) */
+  double max_ms;
+  double flops;           /* algorithmic flops of those launches */
+  double bytes;           /* algorithmic bytes (memory-bound classes) */
+} dtn_kernel_stats;
+
+int dtn_gpu_create(dtn_ctx** ctx, int device);
+void dtn_gpu_destroy(dtn_ctx* ctx);
+const char* dtn_gpu_last_error(const dtn_ctx* ctx);
+/* Run this context's work on an external CUDA stream (cudaStream_t); NULL restores its own. */
+int dtn_gpu_set_stream(dtn_ctx* ctx, void* stream);
+
+int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, dtn_op** out);
+void dtn_gpu_free(dtn_op* op);
+
+int dtn_gpu_boundary(const dtn_op* op, int64_t* ids, int64_t* nb);
+int dtn_gpu_export(const dtn_op* op, double* S, double* G, double* cond);
+int dtn_gpu_device_ptrs(const dtn_op* op, const double** S, const double** G, int64_t* ld);
+/* Y(nb x batch) = op(X), op = G (which 0, apply_dtn) or S (which 1, apply_schur).
+ * on_device: X and Y are device pointers (else host). */
+int dtn_gpu_apply(const dtn_op* op, int which, const double* X, int64_t ldx, int64_t batch, double* Y, int64_t ldy,
+                  int on_device);
+
+int dtn_gpu_num_boxes(const dtn_op* op, int32_t* count, int32_t* depth);
+/* info: level, parent, x0, x1, y0, y1, boundary size, children SW SE NW NE */
+int dtn_gpu_box_info(const dtn_op* op, int32_t box, int32_t* info);
+int dtn_gpu_box_schur(const dtn_op* op, int32_t box, double* S);
+int dtn_gpu_level_stats(const dtn_op* op, dtn_level_stats* out, int32_t max, int32_t* count);
+int dtn_gpu_build_stats(const dtn_op* op, dtn_build_stats* out);
+/* per-kernel-class timing of a build made with opts.profile = 1 (count 0 otherwise) */
+int dtn_gpu_kernel_stats(const dtn_op* op, dtn_kernel_stats* out, int32_t max, int32_t* count);
+
+/* discretize (grid.cpp:106-168) on the host: continuum mode from coefficient
+ * samples b, c, d at the unknowns (physical coordinates (x h, y h), h = 1/(n-1),
+ * unknown_id order; NULL = 0), network mode from the seeded link conductivities. */
+int dtn_discretize_continuum(int32_t n, const double* b, const double* c, const double* d, double* stencil);
+int dtn_discretize_network(int32_t n, double lo, double hi, uint64_t seed, double* stencil);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DTN_GPU_H */

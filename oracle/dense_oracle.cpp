@@ -176,6 +176,7 @@ double discrete_eigenvalue(int p, int q, int n) {
 }
 double discrete_eigenvalue_kth(int k, int n) {
   const int cap = std::min(n - 2, std::max(2 * k, 8));
+  if (int64_t(cap) * cap < k) throw std::invalid_argument("discrete_eigenvalue_kth: k exceeds spectrum");
   struct E { double l; int p, q; };
   std::vector<E> es;
   for (int p = 1; p <= cap; ++p)

@@ -1,0 +1,89 @@
+"""ctypes binding of libdtn_b200.so (include/dtn_gpu.h). The product path has
+no CPU fallback: a missing library or device raises."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libdtn_b200.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "dtn_gpu.h")
+
+DTN_OK, DTN_EINVAL, DTN_ESINGULAR, DTN_ECUDA = 0, 2, 3, 5
+
+
+class dtn_problem(C.Structure):
+    _fields_ = [("n", C.c_int32), ("stencil", C.c_void_p), ("stencil_on_device", C.c_int32)]
+
+
+class dtn_opts(C.Structure):
+    _fields_ = [("engine", C.c_int32), ("n_leaf", C.c_int32), ("leaf_side", C.c_int32), ("want_G", C.c_int32),
+                ("micro_max", C.c_int32), ("profile", C.c_int32), ("epsilon", C.c_double),
+                ("crossover", C.c_int64)]
+
+
+class dtn_level_stats(C.Structure):
+    _fields_ = [("level", C.c_int32), ("boxes", C.c_int32), ("max_boundary", C.c_int64), ("seconds", C.c_double),
+                ("flops", C.c_double)]
+
+
+class dtn_build_stats(C.Structure):
+    _fields_ = [("build_ms", C.c_double), ("leaf_ms", C.c_double), ("merge_ms", C.c_double),
+                ("inverse_ms", C.c_double), ("merge_flops", C.c_double), ("leaf_flops", C.c_double),
+                ("inverse_flops", C.c_double), ("waves", C.c_int32), ("launches", C.c_int32)]
+
+
+class dtn_kernel_stats(C.Structure):
+    _fields_ = [("name", C.c_char * 16), ("launches", C.c_int32), ("ms", C.c_double), ("max_ms", C.c_double),
+                ("flops", C.c_double), ("bytes", C.c_double)]
+
+
+EXPORTS = [
+    "dtn_gpu_create", "dtn_gpu_destroy", "dtn_gpu_last_error", "dtn_gpu_set_stream", "dtn_gpu_build",
+    "dtn_gpu_free", "dtn_gpu_boundary", "dtn_gpu_export", "dtn_gpu_device_ptrs", "dtn_gpu_apply",
+    "dtn_gpu_num_boxes", "dtn_gpu_box_info", "dtn_gpu_box_schur", "dtn_gpu_level_stats", "dtn_gpu_build_stats", "dtn_gpu_kernel_stats",
+    "dtn_discretize_continuum", "dtn_discretize_network",
+]
+
+_lib = None
+
+
+def build() -> str:
+    """Compile the extension in-tree (nvcc, sm_100a)."""
+    subprocess.run(["make", "-s", "-j8", "-C", _HERE], check=True)
+    return LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"libdtn_b200.so is not built ({LIB_PATH}); run paper_1302_5995_b200._lib.build()")
+    L = C.CDLL(LIB_PATH)
+    vp, i32, i64, f64 = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    P = C.POINTER
+    L.dtn_gpu_create.argtypes = [P(vp), C.c_int]
+    L.dtn_gpu_destroy.argtypes = [vp]
+    L.dtn_gpu_destroy.restype = None
+    L.dtn_gpu_last_error.argtypes = [vp]
+    L.dtn_gpu_last_error.restype = C.c_char_p
+    L.dtn_gpu_set_stream.argtypes = [vp, vp]
+    L.dtn_gpu_build.argtypes = [vp, P(dtn_problem), P(dtn_opts), P(vp)]
+    L.dtn_gpu_free.argtypes = [vp]
+    L.dtn_gpu_free.restype = None
+    L.dtn_gpu_boundary.argtypes = [vp, vp, P(i64)]
+    L.dtn_gpu_export.argtypes = [vp, vp, vp, P(f64)]
+    L.dtn_gpu_device_ptrs.argtypes = [vp, P(vp), P(vp), P(i64)]
+    L.dtn_gpu_apply.argtypes = [vp, C.c_int, vp, i64, i64, vp, i64, C.c_int]
+    L.dtn_gpu_num_boxes.argtypes = [vp, P(i32), P(i32)]
+    L.dtn_gpu_box_info.argtypes = [vp, i32, P(i32)]
+    L.dtn_gpu_box_schur.argtypes = [vp, i32, vp]
+    L.dtn_gpu_level_stats.argtypes = [vp, P(dtn_level_stats), i32, P(i32)]
+    L.dtn_gpu_build_stats.argtypes = [vp, P(dtn_build_stats)]
+    L.dtn_gpu_kernel_stats.argtypes = [vp, P(dtn_kernel_stats), i32, P(i32)]
+    L.dtn_discretize_continuum.argtypes = [i32, vp, vp, vp, vp]
+    L.dtn_discretize_network.argtypes = [i32, f64, f64, C.c_uint64, vp]
+    _lib = L
+    return L

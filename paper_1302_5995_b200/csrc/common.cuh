@@ -1,0 +1,66 @@
+// Shared device-side declarations for the B200 dense engine kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dtnb {
+
+// Device copy of a plan node (plan.hpp:Node) — only what kernels read.
+struct NodeDev {
+  int kind;   // 0 micro, 1 merge, 2 root-LU workspace
+  int nb, ni, total;
+  int a, b;   // child node indices (merge)
+  int ld;     // leading dimension of this node's S block
+  int ldm;    // blocked: leading dimension of the assembled system
+  long long s_off, m_off, pos_off, piv_off;
+};
+
+struct PosDev {  // == plan.hpp PosEntry
+  int src, partner, gid, dir;
+};
+
+struct GemmDesc {  // C(m x n) = beta*C + alpha*A(m x k)*B(k x n), column-major
+  const double* A;
+  const double* B;
+  double* C;
+  int m, n, k, lda, ldb, ldc;
+};
+
+struct KernelArgs {
+  const NodeDev* nodes;
+  const PosDev* pos;
+  const double* stencil;  // 5 x nu SoA: center, east, west, north, south
+  long long nu;
+  int side;               // n - 2
+  double* arena;
+  int* piv;
+  double* pivstat;        // 2 per node: min |pivot|, max |pivot|
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ void mma_f64_m16n8k4(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+// 16-byte async global->shared copy; bytes < 16 zero-fills the remainder.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+}  // namespace dtnb

@@ -1,0 +1,839 @@
+// Host orchestration of the B200 dense engine and the C ABI (include/dtn_gpu.h).
+//
+// One build = one CUDA-graph launch of: per wave, the batched one-CTA
+// eliminations (micro boxes and small merges, k_small.cu) and the blocked
+// merges (gather + panel/rowpanel/trailing per kb pivots, k_blocked.cu,
+// k_gemm.cu); then the root inverse G = S^{-1} (blocked LU of S with the same
+// kernels, then forward/backward blocked triangular sweeps on P*I). The plan
+// (tree, DAG, position tables, arena layout, graph) is cached per context.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/dtn_gpu.h"
+#include "common.cuh"
+#include "plan.hpp"
+
+namespace dtnb {
+cudaError_t launch_small_elim(const KernelArgs&, const int*, int, int, bool, cudaStream_t);
+cudaError_t launch_gather(const KernelArgs&, const int*, int, int, cudaStream_t);
+cudaError_t launch_panel(const KernelArgs&, const int*, int, int, int, int, cudaStream_t);
+cudaError_t launch_rowpanel(const KernelArgs&, const int*, int, int, int, int, int, int, cudaStream_t);
+cudaError_t launch_trailing_update(const KernelArgs&, const int*, int, int, int, int, cudaStream_t);
+cudaError_t launch_gemm_desc(const GemmDesc*, int, int, int, double, double, cudaStream_t);
+cudaError_t launch_perm_identity(const int*, int, int*, double*, int, cudaStream_t);
+cudaError_t launch_trsm_rows(const double*, int, double*, int, int, int, int, bool, cudaStream_t);
+cudaError_t launch_norm1(const double*, int, int, int, unsigned long long*, cudaStream_t);
+cudaError_t launch_copy2d(const double*, int, double*, int, int, int, cudaStream_t);
+cudaError_t gemm_init();
+cudaError_t blocked_init();
+int gemm_tiles(int, int);
+}  // namespace dtnb
+
+using namespace dtnb;
+
+namespace {
+
+struct CudaFail : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct Singular : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CK(x)                                                                                  \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess) throw CudaFail(std::string(#x) + ": " + cudaGetErrorString(e_));    \
+  } while (0)
+
+int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+constexpr int kSmallMax = 160;
+constexpr int kDefaultMicro = 128;
+constexpr size_t kPanelSmem = 220 * 1024;
+
+int panel_kb(int rows) {
+  for (int kb : {32, 16, 8})
+    if (size_t(kb) * size_t(rows | 1) * sizeof(double) <= kPanelSmem) return kb;
+  throw std::invalid_argument("dense merge interface too large for the one-CTA panel (ni > 3500)");
+}
+
+struct WaveLaunch {
+  int micro_off = 0, micro_cnt = 0, micro_max = 0;
+  int small_off = 0, small_cnt = 0, small_max = 0;
+  int blk_off = 0, blk_cnt = 0, blk_max_total = 0, blk_max_ni = 0, blk_max_nb = 0, kb = 32;
+  int level = -1;  // reference level of its tree merges, -1 for in-leaf waves
+  double flops = 0.0;
+};
+
+template <class T>
+T* dalloc(size_t count) {
+  T* p = nullptr;
+  CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+  return p;
+}
+
+struct PlanDev {
+  Plan P;
+  bool busy = false;
+  int device = 0;
+  std::vector<NodeDev> h_nodes;
+  NodeDev* d_nodes = nullptr;
+  PosDev* d_pos = nullptr;
+  double* d_arena = nullptr;
+  int* d_piv = nullptr;
+  double* d_pivstat = nullptr;
+  int* d_lists = nullptr;
+  std::vector<int> h_lists;
+  double* d_stencil = nullptr;
+  int64_t nu = 0;
+  std::vector<WaveLaunch> wl;
+  int root_list_off = 0, root_lu_node = 0;
+  int nb = 0;           // root boundary size
+  double* d_S = nullptr;  // compact root S (ld = lds)
+  int lds = 0;
+  double* d_G = nullptr;
+  int ldg = 0;
+  int64_t lu_off = 0;
+  int ldlu = 0, root_kb = 32;
+  int* d_perm = nullptr;
+  unsigned long long* d_norm = nullptr;
+  GemmDesc* d_inv_descs = nullptr;
+  std::vector<GemmDesc> h_inv_descs;
+  double* h_pivstat = nullptr;  // pinned
+  unsigned long long* h_norm = nullptr;
+  std::vector<cudaEvent_t> ev_wave;
+  cudaEvent_t ev_start = nullptr, ev_root = nullptr, ev_end = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  int graph_want_G = -1;
+  int launches = 0;
+
+  ~PlanDev() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    for (auto e : ev_wave) cudaEventDestroy(e);
+    for (auto e : {ev_start, ev_root, ev_end})
+      if (e) cudaEventDestroy(e);
+    for (void* p : std::initializer_list<void*>{d_nodes, d_pos, d_arena, d_piv, d_pivstat, d_lists, d_stencil, d_S, d_G,
+                                                d_perm, d_norm, d_inv_descs})
+      if (p) cudaFree(p);
+    if (h_pivstat) cudaFreeHost(h_pivstat);
+    if (h_norm) cudaFreeHost(h_norm);
+  }
+
+  KernelArgs args() const {
+    return KernelArgs{d_nodes, d_pos, d_stencil, (long long)nu, P.n - 2, d_arena, d_piv, d_pivstat};
+  }
+};
+
+std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
+  auto D = std::make_unique<PlanDev>();
+  D->device = device;
+  D->P = make_plan(key);
+  Plan& P = D->P;
+  D->nu = int64_t(P.n - 2) * (P.n - 2);
+  const Node& root = P.nodes[P.root];
+  D->nb = root.nb;
+  const int nb = D->nb;
+  // nodes (+ the root-LU pseudo node)
+  D->h_nodes.resize(P.nodes.size() + 1);
+  for (size_t i = 0; i < P.nodes.size(); ++i) {
+    const Node& s = P.nodes[i];
+    NodeDev& d = D->h_nodes[i];
+    d.kind = int(s.kind);
+    d.nb = s.nb;
+    d.ni = s.ni;
+    d.total = s.total;
+    d.a = s.a;
+    d.b = s.b;
+    d.ld = s.ld;
+    d.ldm = s.ldm;
+    d.s_off = s.s_off;
+    d.m_off = s.m_off;
+    d.pos_off = s.pos_off;
+    d.piv_off = s.piv_off;
+  }
+  D->ldlu = int(align_up(nb, 8));
+  D->lu_off = align_up(P.arena_doubles, 32);
+  D->root_lu_node = int(P.nodes.size());
+  {
+    NodeDev& r = D->h_nodes.back();
+    std::memset(&r, 0, sizeof(r));
+    r.kind = 2;
+    r.nb = 0;
+    r.ni = nb;
+    r.total = nb;
+    r.a = r.b = -1;
+    r.ldm = D->ldlu;
+    r.ld = D->ldlu;
+    r.m_off = D->lu_off;
+    r.s_off = D->lu_off;
+    r.piv_off = P.piv_ints;
+  }
+  D->root_kb = panel_kb(nb);
+  // launch lists
+  std::vector<int> lists;
+  D->wl.resize(P.waves.size());
+  for (size_t w = 0; w < P.waves.size(); ++w) {
+    const Wave& wv = P.waves[w];
+    WaveLaunch& L = D->wl[w];
+    L.micro_off = int(lists.size());
+    L.micro_cnt = int(wv.micro.size());
+    for (int id : wv.micro) {
+      lists.push_back(id);
+      L.micro_max = std::max(L.micro_max, P.nodes[id].total);
+    }
+    L.small_off = int(lists.size());
+    L.small_cnt = int(wv.small.size());
+    for (int id : wv.small) {
+      lists.push_back(id);
+      L.small_max = std::max(L.small_max, P.nodes[id].total);
+    }
+    L.blk_off = int(lists.size());
+    L.blk_cnt = int(wv.blocked.size());
+    for (int id : wv.blocked) {
+      lists.push_back(id);
+      const Node& nd = P.nodes[id];
+      L.blk_max_total = std::max(L.blk_max_total, nd.total);
+      L.blk_max_ni = std::max(L.blk_max_ni, nd.ni);
+      L.blk_max_nb = std::max(L.blk_max_nb, nd.nb);
+    }
+    if (L.blk_cnt) L.kb = panel_kb(L.blk_max_ni);
+    for (int id : wv.small) {
+      const Node& nd = P.nodes[id];
+      if (nd.label_level >= 0) L.level = L.level < 0 ? nd.label_level : std::min(L.level, nd.label_level);
+    }
+    for (int id : wv.blocked) {
+      const Node& nd = P.nodes[id];
+      if (nd.label_level >= 0) L.level = L.level < 0 ? nd.label_level : std::min(L.level, nd.label_level);
+    }
+    for (int id : wv.small) L.flops += merge_flop_count(P.nodes[id].ni, P.nodes[id].nb);
+    for (int id : wv.blocked) L.flops += merge_flop_count(P.nodes[id].ni, P.nodes[id].nb);
+    for (int id : wv.micro) L.flops += merge_flop_count(P.nodes[id].ni, P.nodes[id].nb);
+  }
+  D->root_list_off = int(lists.size());
+  lists.push_back(D->root_lu_node);
+  D->h_lists = lists;
+  // device buffers
+  D->d_nodes = dalloc<NodeDev>(D->h_nodes.size());
+  CK(cudaMemcpy(D->d_nodes, D->h_nodes.data(), D->h_nodes.size() * sizeof(NodeDev), cudaMemcpyHostToDevice));
+  static_assert(sizeof(PosDev) == sizeof(PosEntry), "PosDev/PosEntry layout");
+  D->d_pos = dalloc<PosDev>(P.pos.size());
+  CK(cudaMemcpy(D->d_pos, P.pos.data(), P.pos.size() * sizeof(PosDev), cudaMemcpyHostToDevice));
+  D->d_lists = dalloc<int>(lists.size());
+  CK(cudaMemcpy(D->d_lists, lists.data(), lists.size() * sizeof(int), cudaMemcpyHostToDevice));
+  D->d_arena = dalloc<double>(size_t(D->lu_off + int64_t(D->ldlu) * nb));
+  D->d_piv = dalloc<int>(size_t(P.piv_ints + nb));
+  D->d_pivstat = dalloc<double>(2 * D->h_nodes.size());
+  D->d_stencil = dalloc<double>(size_t(5 * D->nu));
+  D->lds = int(align_up(nb, 8));
+  D->d_S = dalloc<double>(size_t(D->lds) * nb);
+  D->ldg = int(align_up(nb, 8));
+  D->d_G = dalloc<double>(size_t(D->ldg) * nb);
+  D->d_perm = dalloc<int>(nb);
+  D->d_norm = dalloc<unsigned long long>(2);
+  CK(cudaMallocHost(&D->h_pivstat, 2 * D->h_nodes.size() * sizeof(double)));
+  CK(cudaMallocHost(&D->h_norm, 2 * sizeof(unsigned long long)));
+  // root inverse sweeps: forward X[k1:] -= L[k1:,k0:k1] X[k0:k1]; backward X[:k0] -= U[:k0,k0:k1] X[k0:k1]
+  const double* LU = D->d_arena + D->lu_off;
+  for (int k0 = 0; k0 < nb; k0 += 32) {
+    const int k1 = std::min(nb, k0 + 32);
+    D->h_inv_descs.push_back(GemmDesc{LU + k1 + int64_t(k0) * D->ldlu, D->d_G + k0, D->d_G + k1, nb - k1, nb,
+                                      k1 - k0, D->ldlu, D->ldg, D->ldg});
+  }
+  for (int k0 = 0; k0 < nb; k0 += 32) {
+    const int k1 = std::min(nb, k0 + 32);
+    D->h_inv_descs.push_back(
+        GemmDesc{LU + int64_t(k0) * D->ldlu, D->d_G + k0, D->d_G, k0, nb, k1 - k0, D->ldlu, D->ldg, D->ldg});
+  }
+  D->d_inv_descs = dalloc<GemmDesc>(D->h_inv_descs.size());
+  CK(cudaMemcpy(D->d_inv_descs, D->h_inv_descs.data(), D->h_inv_descs.size() * sizeof(GemmDesc),
+                cudaMemcpyHostToDevice));
+  D->ev_wave.resize(P.waves.size());
+  for (auto& e : D->ev_wave) CK(cudaEventCreate(&e));
+  CK(cudaEventCreate(&D->ev_start));
+  CK(cudaEventCreate(&D->ev_root));
+  CK(cudaEventCreate(&D->ev_end));
+  return D;
+}
+
+// Per-launch profiler (opts.profile): CUDA events around every launch,
+// aggregated per kernel class with the algorithmic work of each launch.
+enum KClass { K_SMALL = 0, K_GATHER, K_PANEL, K_ROWPANEL, K_TRAILING, K_COPY, K_INV_TRSM, K_INV_GEMM, K_MISC, K_COUNT };
+const char* kclass_name(int k) {
+  static const char* names[K_COUNT] = {"small_elim", "gather", "panel", "rowpanel", "trailing_gemm",
+                                       "copy",       "inv_trsm", "inv_gemm", "misc"};
+  return names[k];
+}
+struct Prof {
+  struct Rec {
+    int kclass;
+    cudaEvent_t a, b;
+    double flops, bytes;
+  };
+  std::vector<Rec> recs;
+  ~Prof() {
+    for (auto& r : recs) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+  }
+};
+
+// All device work of one build, in stream order (captured into a graph).
+void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullptr) {
+  const Plan& P = D.P;
+  const KernelArgs a = D.args();
+  int launches = 0;
+  auto run = [&](int kclass, double flops, double bytes, auto&& fn) {
+    Prof::Rec r{kclass, nullptr, nullptr, flops, bytes};
+    if (prof) {
+      CK(cudaEventCreate(&r.a));
+      CK(cudaEventCreate(&r.b));
+      CK(cudaEventRecord(r.a, st));
+    }
+    CK(fn());
+    ++launches;
+    if (prof) {
+      CK(cudaEventRecord(r.b, st));
+      prof->recs.push_back(r);
+    }
+  };
+  auto list_flops = [&](const int* ids, int cnt) {
+    double f = 0.0;
+    for (int i = 0; i < cnt; ++i) f += merge_flop_count(P.nodes[ids[i]].ni, P.nodes[ids[i]].nb);
+    return f;
+  };
+  const std::vector<int>& hl = D.h_lists;
+  CK(cudaEventRecord(D.ev_start, st));
+  for (size_t w = 0; w < D.wl.size(); ++w) {
+    const WaveLaunch& L = D.wl[w];
+    if (L.micro_cnt)
+      run(K_SMALL, list_flops(hl.data() + L.micro_off, L.micro_cnt), 0.0, [&] {
+        return launch_small_elim(a, D.d_lists + L.micro_off, L.micro_cnt, L.micro_max, true, st);
+      });
+    if (L.small_cnt)
+      run(K_SMALL, list_flops(hl.data() + L.small_off, L.small_cnt), 0.0, [&] {
+        return launch_small_elim(a, D.d_lists + L.small_off, L.small_cnt, L.small_max, false, st);
+      });
+    if (L.blk_cnt) {
+      const int* lst = D.d_lists + L.blk_off;
+      const int* hlst = hl.data() + L.blk_off;
+      double gb = 0.0;
+      for (int i = 0; i < L.blk_cnt; ++i) gb += 16.0 * double(P.nodes[hlst[i]].total) * P.nodes[hlst[i]].total;
+      run(K_GATHER, 0.0, gb, [&] { return launch_gather(a, lst, L.blk_cnt, L.blk_max_total, st); });
+      for (int k0 = 0; k0 < L.blk_max_ni; k0 += L.kb) {
+        double fp = 0.0, fr = 0.0, ft = 0.0;
+        for (int i = 0; i < L.blk_cnt; ++i) {
+          const Node& nd = P.nodes[hlst[i]];
+          if (k0 >= nd.ni) continue;
+          const double kbe = std::min(L.kb, nd.ni - k0), rows = nd.ni - k0, mn = nd.total - k0 - kbe;
+          fp += rows * kbe * kbe;
+          fr += kbe * kbe * mn;
+          ft += 2.0 * mn * mn * kbe;
+        }
+        run(K_PANEL, fp, 0.0, [&] { return launch_panel(a, lst, L.blk_cnt, L.blk_max_ni, k0, L.kb, st); });
+        run(K_ROWPANEL, fr, 0.0, [&] {
+          return launch_rowpanel(a, lst, L.blk_cnt, L.blk_max_total, 0, L.blk_max_nb, k0, L.kb, st);
+        });
+        run(K_TRAILING, ft, 0.0,
+            [&] { return launch_trailing_update(a, lst, L.blk_cnt, L.blk_max_total, k0, L.kb, st); });
+      }
+    }
+    CK(cudaEventRecord(D.ev_wave[w], st));
+  }
+  // compact copy of the root S
+  const Node& root = P.nodes[P.root];
+  const double* Sview = D.d_arena + root.s_off;
+  const double nb2 = double(D.nb) * D.nb;
+  run(K_COPY, 0.0, 16.0 * nb2, [&] { return launch_copy2d(Sview, root.ld, D.d_S, D.lds, D.nb, D.nb, st); });
+  CK(cudaEventRecord(D.ev_root, st));
+  if (want_G) {
+    const int nb = D.nb;
+    double* LU = D.d_arena + D.lu_off;
+    run(K_COPY, 0.0, 16.0 * nb2, [&] { return launch_copy2d(D.d_S, D.lds, LU, D.ldlu, nb, nb, st); });
+    const int* rl = D.d_lists + D.root_list_off;
+    for (int k0 = 0; k0 < nb; k0 += D.root_kb) {
+      const double kbe = std::min(D.root_kb, nb - k0), rows = nb - k0, mn = nb - k0 - kbe;
+      run(K_PANEL, rows * kbe * kbe, 0.0, [&] { return launch_panel(a, rl, 1, nb, k0, D.root_kb, st); });
+      run(K_ROWPANEL, kbe * kbe * mn, 0.0, [&] { return launch_rowpanel(a, rl, 1, nb, 0, 0, k0, D.root_kb, st); });
+      run(K_TRAILING, 2.0 * mn * mn * kbe, 0.0,
+          [&] { return launch_trailing_update(a, rl, 1, nb, k0, D.root_kb, st); });
+    }
+    run(K_MISC, 0.0, 8.0 * nb2, [&] {
+      return launch_perm_identity(D.d_piv + D.h_nodes[D.root_lu_node].piv_off, nb, D.d_perm, D.d_G, D.ldg, st);
+    });
+    ++launches;  // perm + scatter
+    int di = 0;
+    for (int k0 = 0; k0 < nb; k0 += 32, ++di) {
+      const int kbe = std::min(32, nb - k0);
+      run(K_INV_TRSM, double(kbe) * kbe * nb, 0.0,
+          [&] { return launch_trsm_rows(LU, D.ldlu, D.d_G, D.ldg, nb, k0, kbe, true, st); });
+      const GemmDesc& g = D.h_inv_descs[di];
+      if (g.m > 0)
+        run(K_INV_GEMM, 2.0 * g.m * g.n * g.k, 0.0, [&] {
+          return launch_gemm_desc(D.d_inv_descs + di, 1, gemm_tiles(g.m, g.n), g.k, -1.0, 1.0, st);
+        });
+    }
+    const int nblk = di;
+    for (int bi = nblk - 1; bi >= 0; --bi) {
+      const int k0 = bi * 32, kbe = std::min(32, nb - k0);
+      run(K_INV_TRSM, double(kbe) * kbe * nb, 0.0,
+          [&] { return launch_trsm_rows(LU, D.ldlu, D.d_G, D.ldg, nb, k0, kbe, false, st); });
+      const GemmDesc& g = D.h_inv_descs[nblk + bi];
+      if (g.m > 0)
+        run(K_INV_GEMM, 2.0 * g.m * g.n * g.k, 0.0, [&] {
+          return launch_gemm_desc(D.d_inv_descs + nblk + bi, 1, gemm_tiles(g.m, g.n), g.k, -1.0, 1.0, st);
+        });
+    }
+    CK(cudaMemsetAsync(D.d_norm, 0, 2 * sizeof(unsigned long long), st));
+    run(K_MISC, 0.0, 8.0 * nb2, [&] { return launch_norm1(D.d_S, D.lds, nb, nb, D.d_norm, st); });
+    run(K_MISC, 0.0, 8.0 * nb2, [&] { return launch_norm1(D.d_G, D.ldg, nb, nb, D.d_norm + 1, st); });
+  }
+  CK(cudaEventRecord(D.ev_end, st));
+  D.launches = launches;
+}
+
+bool use_graphs() {
+  const char* e = std::getenv("DTN_NO_GRAPH");
+  return !(e && e[0] == '1');
+}
+
+}  // namespace
+
+struct dtn_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  std::vector<std::unique_ptr<PlanDev>> plans;
+  std::string err;
+  // apply staging
+  double* d_x = nullptr;
+  double* d_y = nullptr;
+  size_t stage_cap = 0;
+  GemmDesc* d_desc = nullptr;
+};
+
+struct dtn_op {
+  std::vector<dtn_kernel_stats> kstats;
+  dtn_ctx* ctx = nullptr;
+  PlanDev* plan = nullptr;
+  int nb = 0;
+  bool has_G = false;
+  double cond = 0.0;
+  dtn_build_stats stats{};
+  std::vector<dtn_level_stats> levels;
+};
+
+namespace {
+
+thread_local std::string g_err;  // errors with no context (dtn_gpu_create)
+
+template <class F>
+int guarded(dtn_ctx* ctx, F&& f) {
+  std::string& err = ctx ? ctx->err : g_err;
+  try {
+    f();
+    err.clear();
+    return DTN_OK;
+  } catch (const Singular& e) {
+    err = e.what();
+    return DTN_ESINGULAR;
+  } catch (const std::invalid_argument& e) {
+    err = e.what();
+    return DTN_EINVAL;
+  } catch (const std::domain_error& e) {
+    err = e.what();
+    return DTN_EINVAL;
+  } catch (const std::exception& e) {
+    err = e.what();
+    return DTN_ECUDA;
+  }
+}
+
+std::string label_of(const Plan& P, const Node& nd) {
+  if (nd.label_level >= 0)
+    return "interface block is singular [level " + std::to_string(nd.label_level) + " box " +
+           std::to_string(nd.label_box) + "]";
+  return "interior block A_ii is singular [leaf box " + std::to_string(nd.label_box) + "]";
+}
+
+bool pivots_ok(double pmin, double pmax) { return (pmin > pmax * 1e-300) && std::isfinite(pmax); }
+
+}  // namespace
+
+extern "C" {
+
+int dtn_gpu_create(dtn_ctx** out, int device) {
+  return guarded(nullptr, [&] {
+    if (!out) throw std::invalid_argument("dtn_gpu_create: null output");
+    int count = 0;
+    CK(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) throw CudaFail("dtn_gpu_create: no such CUDA device");
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) throw CudaFail("dtn_gpu_create: sm_100a (B200) device required");
+    CK(cudaSetDevice(device));
+    CK(gemm_init());
+    CK(blocked_init());
+    auto* c = new dtn_ctx;
+    c->device = device;
+    CK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+    c->stream = c->own;
+    CK(cudaMalloc(&c->d_desc, sizeof(GemmDesc)));
+    *out = c;
+  });
+}
+
+void dtn_gpu_destroy(dtn_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  ctx->plans.clear();
+  if (ctx->d_x) cudaFree(ctx->d_x);
+  if (ctx->d_y) cudaFree(ctx->d_y);
+  if (ctx->d_desc) cudaFree(ctx->d_desc);
+  if (ctx->own) cudaStreamDestroy(ctx->own);
+  delete ctx;
+}
+
+const char* dtn_gpu_last_error(const dtn_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+int dtn_gpu_set_stream(dtn_ctx* ctx, void* stream) {
+  if (!ctx) return DTN_EINVAL;
+  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+  return DTN_OK;
+}
+
+int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, dtn_op** out) {
+  return guarded(ctx, [&] {
+    if (!ctx || !prob || !opts || !out) throw std::invalid_argument("dtn_gpu_build: null argument");
+    if (prob->n < 4) throw std::invalid_argument("discretize: n must be >= 4");
+    if (!prob->stencil) throw std::invalid_argument("dtn_gpu_build: null stencil");
+    if (opts->engine != 0) throw std::invalid_argument("dtn_gpu_build: only the dense engine is available");
+    CK(cudaSetDevice(ctx->device));
+    PlanKey key;
+    key.n = prob->n;
+    key.n_leaf = opts->n_leaf;
+    key.leaf_side = opts->leaf_side;
+    key.micro_max = opts->micro_max > 0 ? opts->micro_max : kDefaultMicro;
+    key.small_max = kSmallMax;
+    if (key.leaf_side <= 0 && key.n_leaf < 16) throw std::invalid_argument("build_tree: n_leaf must be >= 16");
+    PlanDev* D = nullptr;
+    for (auto& p : ctx->plans)
+      if (!p->busy && p->P.key == key) D = p.get();
+    if (!D) {
+      ctx->plans.push_back(make_plandev(key, ctx->device));
+      D = ctx->plans.back().get();
+    }
+    cudaStream_t st = ctx->stream;
+    const bool want_G = opts->want_G != 0;
+    const bool profile = opts->profile != 0;
+    std::unique_ptr<Prof> prof;
+    CK(cudaMemcpyAsync(D->d_stencil, prob->stencil, size_t(5 * D->nu) * sizeof(double),
+                       prob->stencil_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    if (profile) {
+      prof = std::make_unique<Prof>();
+      enqueue_build(*D, st, want_G, prof.get());
+    } else if (use_graphs()) {
+      if (!D->gexec || D->graph_want_G != int(want_G)) {
+        if (D->gexec) {
+          CK(cudaGraphExecDestroy(D->gexec));
+          D->gexec = nullptr;
+        }
+        cudaStream_t cap;
+        CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+        try {
+          enqueue_build(*D, cap, want_G);
+        } catch (...) {
+          cudaStreamEndCapture(cap, &g);
+          cudaStreamDestroy(cap);
+          throw;
+        }
+        CK(cudaStreamEndCapture(cap, &g));
+        CK(cudaGraphInstantiate(&D->gexec, g, 0));
+        CK(cudaGraphDestroy(g));
+        CK(cudaStreamDestroy(cap));
+        D->graph_want_G = int(want_G);
+      }
+      CK(cudaGraphLaunch(D->gexec, st));
+    } else {
+      enqueue_build(*D, st, want_G);
+    }
+    const size_t nstat = D->h_nodes.size();
+    CK(cudaMemcpyAsync(D->h_pivstat, D->d_pivstat, 2 * nstat * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (want_G) CK(cudaMemcpyAsync(D->h_norm, D->d_norm, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+    // singular blocks, first failing node in build order (dense_nd.cpp:93-96, 175-180)
+    const Plan& P = D->P;
+    for (const Wave& wv : P.waves)
+      for (const auto* lst : {&wv.micro, &wv.small, &wv.blocked})
+        for (int id : *lst) {
+          const Node& nd = P.nodes[id];
+          if (nd.ni > 0 && !pivots_ok(D->h_pivstat[2 * id], D->h_pivstat[2 * id + 1])) throw Singular(label_of(P, nd));
+        }
+    auto* op = new dtn_op;
+    op->ctx = ctx;
+    op->plan = D;
+    op->nb = D->nb;
+    op->has_G = want_G;
+    if (want_G) {
+      const int r = D->root_lu_node;
+      if (!pivots_ok(D->h_pivstat[2 * r], D->h_pivstat[2 * r + 1])) {
+        delete op;
+        throw Singular("root Schur complement is singular [root]");
+      }
+      double n1[2];
+      std::memcpy(n1, D->h_norm, sizeof(n1));
+      op->cond = n1[0] * n1[1];
+    }
+    // timings
+    auto ms = [](cudaEvent_t a, cudaEvent_t b) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, a, b);
+      return double(t);
+    };
+    dtn_build_stats& s = op->stats;
+    s.build_ms = ms(D->ev_start, D->ev_end);
+    s.inverse_ms = ms(D->ev_root, D->ev_end);
+    s.merge_flops = P.merge_flops;
+    s.leaf_flops = P.micro_flops;
+    s.inverse_flops = want_G ? 2.0 * double(D->nb) * D->nb * D->nb : 0.0;
+    s.waves = int(P.waves.size());
+    s.launches = D->launches;
+    std::vector<dtn_level_stats> lv(P.depth + 1);
+    for (int l = 0; l <= P.depth; ++l) {
+      lv[l].level = l;
+      lv[l].boxes = int(P.levels[l].size());
+      for (int id : P.levels[l])
+        lv[l].max_boundary = std::max<int64_t>(lv[l].max_boundary, perimeter_size(P.boxes[id].r));
+    }
+    cudaEvent_t prev = D->ev_start;
+    for (size_t w = 0; w < D->wl.size(); ++w) {
+      const double t = ms(prev, D->ev_wave[w]);
+      prev = D->ev_wave[w];
+      const int l = D->wl[w].level;
+      if (l < 0) {
+        s.leaf_ms += t;
+        lv[P.depth].seconds += t * 1e-3;
+        lv[P.depth].flops += D->wl[w].flops;
+      } else {
+        s.merge_ms += t;
+        lv[l].seconds += t * 1e-3;
+        lv[l].flops += D->wl[w].flops;
+      }
+    }
+    op->levels = std::move(lv);
+    if (prof) {
+      op->kstats.assign(K_COUNT, dtn_kernel_stats{});
+      for (int k = 0; k < K_COUNT; ++k) std::snprintf(op->kstats[k].name, sizeof(op->kstats[k].name), "%s", kclass_name(k));
+      for (auto& r : prof->recs) {
+        dtn_kernel_stats& ks = op->kstats[r.kclass];
+        const double t = ms(r.a, r.b);
+        ks.launches += 1;
+        ks.ms += t;
+        ks.max_ms = std::max(ks.max_ms, t);
+        ks.flops += r.flops;
+        ks.bytes += r.bytes;
+      }
+    }
+    D->busy = true;
+    *out = op;
+  });
+}
+
+void dtn_gpu_free(dtn_op* op) {
+  if (!op) return;
+  if (op->plan) op->plan->busy = false;
+  delete op;
+}
+
+int dtn_gpu_boundary(const dtn_op* op, int64_t* ids, int64_t* nb) {
+  if (!op || !nb) return DTN_EINVAL;
+  *nb = op->nb;
+  if (ids) {
+    const Plan& P = op->plan->P;
+    std::vector<std::pair<int, int>> per;
+    perimeter_ccw(P.nodes[P.root].r, per);
+    const int side = P.n - 2;
+    for (size_t i = 0; i < per.size(); ++i) ids[i] = int64_t(per[i].second - 1) * side + (per[i].first - 1);
+  }
+  return DTN_OK;
+}
+
+int dtn_gpu_export(const dtn_op* op, double* S, double* G, double* cond) {
+  if (!op) return DTN_EINVAL;
+  return guarded(op->ctx, [&] {
+    CK(cudaSetDevice(op->ctx->device));
+    const PlanDev& D = *op->plan;
+    const size_t nb = size_t(op->nb);
+    if (S) CK(cudaMemcpy2D(S, nb * 8, D.d_S, size_t(D.lds) * 8, nb * 8, nb, cudaMemcpyDeviceToHost));
+    if (G) {
+      if (!op->has_G) throw std::invalid_argument("dtn_gpu_export: G was not built (want_G = 0)");
+      CK(cudaMemcpy2D(G, nb * 8, D.d_G, size_t(D.ldg) * 8, nb * 8, nb, cudaMemcpyDeviceToHost));
+    }
+    if (cond) *cond = op->cond;
+  });
+}
+
+int dtn_gpu_device_ptrs(const dtn_op* op, const double** S, const double** G, int64_t* ld) {
+  if (!op) return DTN_EINVAL;
+  if (S) *S = op->plan->d_S;
+  if (G) *G = op->has_G ? op->plan->d_G : nullptr;
+  if (ld) *ld = op->plan->lds;
+  return DTN_OK;
+}
+
+int dtn_gpu_apply(const dtn_op* op, int which, const double* X, int64_t ldx, int64_t batch, double* Y, int64_t ldy,
+                  int on_device) {
+  if (!op) return DTN_EINVAL;
+  dtn_ctx* ctx = op->ctx;
+  return guarded(ctx, [&] {
+    const int nb = op->nb;
+    if (which != 0 && which != 1) throw std::invalid_argument("dtn_gpu_apply: which must be 0 (G) or 1 (S)");
+    if (which == 0 && !op->has_G) throw std::invalid_argument("apply_dtn: G was not built (want_G = 0)");
+    if (batch < 0 || ldx < nb || ldy < nb || (!X && batch) || (!Y && batch))
+      throw std::invalid_argument("apply: boundary vector size mismatch");
+    if (batch == 0) return;
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    const PlanDev& D = *op->plan;
+    const double* A = which == 0 ? D.d_G : D.d_S;
+    const int lda = which == 0 ? D.ldg : D.lds;
+    const bool aligned = on_device && (reinterpret_cast<uintptr_t>(X) % 16 == 0) && (ldx % 2 == 0) &&
+                         (reinterpret_cast<uintptr_t>(Y) % 16 == 0) && (ldy % 2 == 0);
+    const double* dX = X;
+    double* dY = Y;
+    int64_t ldX = ldx, ldY = ldy;
+    if (!aligned) {
+      const int64_t ldp = align_up(nb, 2);
+      const size_t need = size_t(ldp) * size_t(batch);
+      if (need > ctx->stage_cap) {
+        if (ctx->d_x) cudaFree(ctx->d_x);
+        if (ctx->d_y) cudaFree(ctx->d_y);
+        ctx->d_x = ctx->d_y = nullptr;
+        ctx->stage_cap = 0;
+        CK(cudaMalloc(&ctx->d_x, need * 8));
+        CK(cudaMalloc(&ctx->d_y, need * 8));
+        ctx->stage_cap = need;
+      }
+      CK(cudaMemcpy2DAsync(ctx->d_x, size_t(ldp) * 8, X, size_t(ldx) * 8, size_t(nb) * 8, size_t(batch),
+                           on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+      dX = ctx->d_x;
+      dY = ctx->d_y;
+      ldX = ldY = ldp;
+    }
+    GemmDesc d{A, dX, dY, nb, int(batch), nb, lda, int(ldX), int(ldY)};
+    CK(cudaMemcpyAsync(ctx->d_desc, &d, sizeof(d), cudaMemcpyHostToDevice, st));
+    CK(launch_gemm_desc(ctx->d_desc, 1, gemm_tiles(nb, int(batch)), nb, 1.0, 0.0, st));
+    if (!aligned)
+      CK(cudaMemcpy2DAsync(Y, size_t(ldy) * 8, dY, size_t(ldY) * 8, size_t(nb) * 8, size_t(batch),
+                           on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int dtn_gpu_num_boxes(const dtn_op* op, int32_t* count, int32_t* depth) {
+  if (!op) return DTN_EINVAL;
+  if (count) *count = int32_t(op->plan->P.boxes.size());
+  if (depth) *depth = op->plan->P.depth;
+  return DTN_OK;
+}
+
+int dtn_gpu_box_info(const dtn_op* op, int32_t box, int32_t* info) {
+  if (!op || !info || box < 0 || box >= int32_t(op->plan->P.boxes.size())) return DTN_EINVAL;
+  const RefBox& b = op->plan->P.boxes[box];
+  const int32_t v[11] = {b.level, b.parent, b.r.x0, b.r.x1, b.r.y0, b.r.y1, perimeter_size(b.r),
+                         b.children[0], b.children[1], b.children[2], b.children[3]};
+  std::copy(v, v + 11, info);
+  return DTN_OK;
+}
+
+int dtn_gpu_box_schur(const dtn_op* op, int32_t box, double* S) {
+  if (!op || box < 0 || box >= int32_t(op->plan->P.boxes.size())) return DTN_EINVAL;
+  return guarded(op->ctx, [&] {
+    const PlanDev& D = *op->plan;
+    const int node = D.P.boxes[box].node;
+    if (node < 0) throw std::invalid_argument("dtn_gpu_box_schur: empty box");
+    const Node& nd = D.P.nodes[node];
+    CK(cudaSetDevice(op->ctx->device));
+    CK(cudaMemcpy2D(S, size_t(nd.nb) * 8, D.d_arena + nd.s_off, size_t(nd.ld) * 8, size_t(nd.nb) * 8, nd.nb,
+                    cudaMemcpyDeviceToHost));
+  });
+}
+
+int dtn_gpu_level_stats(const dtn_op* op, dtn_level_stats* out, int32_t max, int32_t* count) {
+  if (!op || !count) return DTN_EINVAL;
+  *count = int32_t(op->levels.size());
+  if (out)
+    for (int32_t i = 0; i < std::min<int32_t>(max, *count); ++i) out[i] = op->levels[i];
+  return DTN_OK;
+}
+
+int dtn_gpu_kernel_stats(const dtn_op* op, dtn_kernel_stats* out, int32_t max, int32_t* count) {
+  if (!op || !count) return DTN_EINVAL;
+  *count = int32_t(op->kstats.size());
+  if (out)
+    for (int32_t i = 0; i < std::min<int32_t>(max, *count); ++i) out[i] = op->kstats[i];
+  return DTN_OK;
+}
+
+int dtn_gpu_build_stats(const dtn_op* op, dtn_build_stats* out) {
+  if (!op || !out) return DTN_EINVAL;
+  *out = op->stats;
+  return DTN_OK;
+}
+
+// discretize, continuum branch (grid.cpp:130-144): paper's 1/h convection scaling
+int dtn_discretize_continuum(int32_t n, const double* b, const double* c, const double* d, double* st) {
+  if (n < 4 || !st) return DTN_EINVAL;
+  const int64_t s = n - 2, nu = s * s;
+  const double h = 1.0 / (n - 1), ih2 = 1.0 / (h * h), ih = 1.0 / h;
+  for (int64_t k = 0; k < nu; ++k) {
+    const double bv = b ? b[k] : 0.0, cv = c ? c[k] : 0.0, dv = d ? d[k] : 0.0;
+    if (!std::isfinite(bv) || !std::isfinite(cv) || !std::isfinite(dv)) return DTN_EINVAL;
+    st[k] = 4.0 * ih2 + dv;
+    st[nu + k] = -ih2 + bv * ih;
+    st[2 * nu + k] = -ih2 - bv * ih;
+    st[3 * nu + k] = -ih2 + cv * ih;
+    st[4 * nu + k] = -ih2 - cv * ih;
+  }
+  return DTN_OK;
+}
+
+// discretize, network branch (grid.cpp:82-92, 145-150): std::mt19937_64,
+// u = (rng() >> 11) * 2^-53, horizontal links row-major then vertical links
+int dtn_discretize_network(int32_t n, double lo, double hi, uint64_t seed, double* st) {
+  if (n < 4 || !st) return DTN_EINVAL;
+  const int64_t s = n - 2, nu = s * s;
+  std::vector<double> sigma(size_t(2) * n * (n - 1));
+  std::mt19937_64 rng(seed);
+  for (auto& v : sigma) v = lo + (hi - lo) * (double(rng() >> 11) * 0x1.0p-53);
+  auto sh = [&](int x, int y) { return sigma[size_t(y) * (n - 1) + x]; };
+  auto sv = [&](int x, int y) { return sigma[size_t(n) * (n - 1) + size_t(y) * n + x]; };
+  for (int y = 1; y <= n - 2; ++y)
+    for (int x = 1; x <= n - 2; ++x) {
+      const int64_t k = int64_t(y - 1) * s + (x - 1);
+      const double se = sh(x, y), sw = sh(x - 1, y), sn = sv(x, y), ss = sv(x, y - 1);
+      st[k] = se + sw + sn + ss;
+      st[nu + k] = -se;
+      st[2 * nu + k] = -sw;
+      st[3 * nu + k] = -sn;
+      st[4 * nu + k] = -ss;
+    }
+  return DTN_OK;
+}
+
+}  // extern "C"

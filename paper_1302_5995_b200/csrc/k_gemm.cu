@@ -1,0 +1,202 @@
+// FP64 tensor-core GEMM (DMMA: mma.sync m16n8k4 .f64) for the merge
+// trailing updates, the root-inverse triangular sweeps and the batched solve.
+// CTA tile BM x BN, K staged through shared memory in BK chunks with a
+// two-stage cp.async pipeline; 8 warps, each owning a WM x WN accumulator
+// tile in registers (FP64 has no tcgen05/TMEM path on sm_100a).
+#include "common.cuh"
+
+namespace dtnb {
+
+constexpr int GBM = 128, GBN = 64, GWM = 32, GWN = 32;
+constexpr int GTHREADS = (GBM / GWM) * (GBN / GWN) * 32;  // 256
+constexpr int GPA = 4;                                    // A smem row pad (bank-conflict free frags)
+constexpr int GLDB = 20;                                  // B smem leading dim (== 4 mod 16)
+
+template <int BK>
+struct GemmSmem {
+  double a[2][BK][GBM + GPA];
+  double b[2][GBN][GLDB];
+};
+
+// One BM x BN tile of C = alpha*A*B + beta*C (beta == 0: C not read).
+// Requires 16-byte aligned columns (offsets and leading dimensions even).
+template <int BK, bool A16 = true>
+__device__ __forceinline__ void gemm_tile(const double* __restrict__ A, int lda, const double* __restrict__ B,
+                                          int ldb, double* C, int ldc, int m, int n, int k, int tm, int tn,
+                                          double alpha, double beta, GemmSmem<BK>& sm) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, tig = lane & 3;
+  const int wm0 = (warp % (GBM / GWM)) * GWM, wn0 = (warp / (GBM / GWM)) * GWN;
+  const int row0 = tm * GBM, col0 = tn * GBN;
+  const int KT = (k + BK - 1) / BK;
+
+  auto load = [&](int stage, int kt) {
+    const int kb0 = kt * BK;
+    // A: BK columns x GBM rows, 2-double chunks along rows (1-double chunks
+    // when A's columns are only 8-byte aligned)
+    if constexpr (A16) {
+      constexpr int ACH = BK * GBM / 2;
+#pragma unroll
+      for (int c = tid; c < ACH; c += GTHREADS) {
+        const int kk = c / (GBM / 2), rr = (c % (GBM / 2)) * 2;
+        const int gr = row0 + rr, gc = kb0 + kk;
+        int bytes = 0;
+        const double* src = A;
+        if (gc < k && gr < m) {
+          bytes = (m - gr) >= 2 ? 16 : 8;
+          src = A + gr + (long long)gc * lda;
+        }
+        cp_async16(&sm.a[stage][kk][rr], src, bytes);
+      }
+    } else {
+      constexpr int ACH = BK * GBM;
+#pragma unroll
+      for (int c = tid; c < ACH; c += GTHREADS) {
+        const int kk = c / GBM, rr = c % GBM;
+        const int gr = row0 + rr, gc = kb0 + kk;
+        const bool ok = gc < k && gr < m;
+        cp_async8(&sm.a[stage][kk][rr], ok ? A + gr + (long long)gc * lda : A, ok ? 8 : 0);
+      }
+    }
+    // B: GBN columns x BK rows, 2-double chunks along k
+    constexpr int BCH = GBN * BK / 2;
+#pragma unroll
+    for (int c = tid; c < BCH; c += GTHREADS) {
+      const int nn = c / (BK / 2), kp = (c % (BK / 2)) * 2;
+      const int gk = kb0 + kp, gc = col0 + nn;
+      int bytes = 0;
+      const double* src = B;
+      if (gc < n && gk < k) {
+        bytes = (k - gk) >= 2 ? 16 : 8;
+        src = B + gk + (long long)gc * ldb;
+      }
+      cp_async16(&sm.b[stage][nn][kp], src, bytes);
+    }
+    cp_async_commit();
+  };
+
+  double acc[GWM / 16][GWN / 8][4];
+#pragma unroll
+  for (int i = 0; i < GWM / 16; ++i)
+#pragma unroll
+    for (int j = 0; j < GWN / 8; ++j)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
+
+  if (KT > 0) load(0, 0);
+  for (int kt = 0; kt < KT; ++kt) {
+    if (kt + 1 < KT) {
+      load((kt + 1) & 1, kt + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const int s = kt & 1;
+#pragma unroll
+    for (int ks = 0; ks < BK / 4; ++ks) {
+      double af[GWM / 16][2], bf[GWN / 8];
+#pragma unroll
+      for (int i = 0; i < GWM / 16; ++i) {
+        af[i][0] = sm.a[s][ks * 4 + tig][wm0 + i * 16 + g];
+        af[i][1] = sm.a[s][ks * 4 + tig][wm0 + i * 16 + g + 8];
+      }
+#pragma unroll
+      for (int j = 0; j < GWN / 8; ++j) bf[j] = sm.b[s][wn0 + j * 8 + g][ks * 4 + tig];
+#pragma unroll
+      for (int i = 0; i < GWM / 16; ++i)
+#pragma unroll
+        for (int j = 0; j < GWN / 8; ++j) mma_f64_m16n8k4(acc[i][j], af[i][0], af[i][1], bf[j]);
+    }
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int i = 0; i < GWM / 16; ++i) {
+#pragma unroll
+    for (int j = 0; j < GWN / 8; ++j) {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int r = row0 + wm0 + i * 16 + g + 8 * (v >> 1);
+        const int c = col0 + wn0 + j * 8 + 2 * tig + (v & 1);
+        if (r < m && c < n) {
+          double* p = C + r + (long long)c * ldc;
+          *p = beta == 0.0 ? alpha * acc[i][j][v] : fma(alpha, acc[i][j][v], beta * *p);
+        }
+      }
+    }
+  }
+}
+
+template <int BK>
+__global__ void __launch_bounds__(GTHREADS) gemm_desc_kernel(const GemmDesc* __restrict__ descs, double alpha,
+                                                             double beta) {
+  extern __shared__ __align__(16) unsigned char gsm_raw[];
+  GemmSmem<BK>& sm = *reinterpret_cast<GemmSmem<BK>*>(gsm_raw);
+  const GemmDesc d = descs[blockIdx.y];
+  const int tiles_m = (d.m + GBM - 1) / GBM, tiles_n = (d.n + GBN - 1) / GBN;
+  const int t = blockIdx.x;
+  if (t >= tiles_m * tiles_n) return;
+  gemm_tile<BK>(d.A, d.lda, d.B, d.ldb, d.C, d.ldc, d.m, d.n, d.k, t % tiles_m, t / tiles_m, alpha, beta, sm);
+}
+
+// Trailing update of the blocked partial LU (right-looking, dense_nd.cpp:174-181
+// restated as a blocked elimination): for each merge in the list with
+// ni > k0, M[k1:, k1:] -= M[k1:, k0:k1] * M[k0:k1, k1:], k1 = k0 + min(kb, ni-k0).
+template <int BK>
+__global__ void __launch_bounds__(GTHREADS) trailing_update_kernel(KernelArgs args, const int* __restrict__ list,
+                                                                   int k0, int kb) {
+  extern __shared__ __align__(16) unsigned char gsm_raw[];
+  GemmSmem<BK>& sm = *reinterpret_cast<GemmSmem<BK>*>(gsm_raw);
+  const NodeDev nd = args.nodes[list[blockIdx.y]];
+  if (k0 >= nd.ni) return;
+  const int kbe = min(kb, nd.ni - k0), k1 = k0 + kbe;
+  const int mn = nd.total - k1;
+  const int tiles = (mn + GBM - 1) / GBM, tiles_n = (mn + GBN - 1) / GBN;
+  const int t = blockIdx.x;
+  if (t >= tiles * tiles_n) return;
+  double* M = args.arena + nd.m_off;
+  const long long ld = nd.ldm;
+  if ((k1 & 1) == 0)
+    gemm_tile<BK, true>(M + k1 + k0 * ld, nd.ldm, M + k0 + k1 * ld, nd.ldm, M + k1 + k1 * ld, nd.ldm, mn, mn, kbe,
+                        t % tiles, t / tiles, -1.0, 1.0, sm);
+  else
+    gemm_tile<BK, false>(M + k1 + k0 * ld, nd.ldm, M + k0 + k1 * ld, nd.ldm, M + k1 + k1 * ld, nd.ldm, mn, mn, kbe,
+                         t % tiles, t / tiles, -1.0, 1.0, sm);
+}
+
+cudaError_t gemm_init() {
+  cudaError_t e;
+  e = cudaFuncSetAttribute(gemm_desc_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(GemmSmem<16>));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(gemm_desc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(GemmSmem<8>));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(trailing_update_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           sizeof(GemmSmem<16>));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(trailing_update_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              sizeof(GemmSmem<8>));
+}
+
+int gemm_tiles(int m, int n) { return ((m + GBM - 1) / GBM) * ((n + GBN - 1) / GBN); }
+
+cudaError_t launch_gemm_desc(const GemmDesc* d_descs, int count, int max_tiles, int kmax, double alpha, double beta,
+                             cudaStream_t st) {
+  if (count <= 0 || max_tiles <= 0) return cudaSuccess;
+  dim3 grid(max_tiles, count);
+  if (kmax % 16 == 0 || kmax > 64) gemm_desc_kernel<16><<<grid, GTHREADS, sizeof(GemmSmem<16>), st>>>(d_descs, alpha, beta);
+  else gemm_desc_kernel<8><<<grid, GTHREADS, sizeof(GemmSmem<8>), st>>>(d_descs, alpha, beta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trailing_update(const KernelArgs& args, const int* d_list, int count, int max_total, int k0, int kb,
+                                   cudaStream_t st) {
+  const int mn = max_total - k0 - 1;
+  if (count <= 0 || mn <= 0) return cudaSuccess;
+  dim3 grid(gemm_tiles(mn, mn), count);
+  if (kb % 16 == 0) trailing_update_kernel<16><<<grid, GTHREADS, sizeof(GemmSmem<16>), st>>>(args, d_list, k0, kb);
+  else trailing_update_kernel<8><<<grid, GTHREADS, sizeof(GemmSmem<8>), st>>>(args, d_list, k0, kb);
+  return cudaGetLastError();
+}
+
+}  // namespace dtnb

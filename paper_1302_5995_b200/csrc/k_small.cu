@@ -1,0 +1,197 @@
+// Fused one-CTA elimination for small systems (total <= 160 unknowns):
+//  * micro boxes below a reference leaf: assemble A over the box's nodes
+//    ordered [interior row-major; boundary CCW] from the stencil and
+//    eliminate the interior — leaf_schur, dense_nd.cpp:37-103;
+//  * small pairwise merges: assemble the merge system from the two child
+//    Schur complements plus the cross-interface couplings and eliminate the
+//    interface — merge_two, dense_nd.cpp:135-181.
+// The system lives in registers, distributed over a TR x TC thread grid
+// (thread (tr,tc) owns rows tr+TR*a and columns tc+TC*b). Elimination is
+// Gaussian elimination with partial pivoting restricted to the eliminated
+// rows (PartialPivLU of M_ii, dense_nd.cpp:174) done without physical row
+// swaps: pivot rows are flagged instead of moved, so the boundary rows end up
+// holding S = M_bb - M_bi M_ii^{-1} M_ib in place. Two __syncthreads per pivot.
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace dtnb {
+
+template <int TR, int TC, int RPT, int CPT, bool MICRO>
+__global__ void __launch_bounds__(TR * TC) small_elim_kernel(KernelArgs args, const int* __restrict__ list) {
+  constexpr int MAXT = (TR * RPT > TC * CPT) ? TR * RPT : TC * CPT;
+  static_assert(TR <= 32 && (32 % TR) == 0, "column-owner group must sit inside one warp");
+  __shared__ PosDev spos[MAXT];
+  __shared__ double sst[MICRO ? 5 : 1][MICRO ? MAXT : 1];
+  __shared__ double colk[2][MAXT];
+  __shared__ double rowp[MAXT];
+  __shared__ int s_piv;
+
+  const int node_id = list[blockIdx.x];
+  const NodeDev nd = args.nodes[node_id];
+  const int total = nd.total, ni = nd.ni;
+  const int tid = threadIdx.x, tr = tid % TR, tc = tid / TR;
+
+  for (int p = tid; p < total; p += TR * TC) {
+    const PosDev e = args.pos[nd.pos_off + p];
+    spos[p] = e;
+    if constexpr (MICRO) {
+#pragma unroll
+      for (int r = 0; r < 5; ++r) sst[r][p] = args.stencil[r * args.nu + e.gid];
+    }
+  }
+  __syncthreads();
+
+  // ---- assemble the owned entries
+  double m[RPT][CPT];
+  const double* A = nullptr;
+  const double* B = nullptr;
+  int lda = 0, ldb = 0;
+  if constexpr (!MICRO) {
+    const NodeDev ca = args.nodes[nd.a], cb = args.nodes[nd.b];
+    A = args.arena + ca.s_off;
+    lda = ca.ld;
+    B = args.arena + cb.s_off;
+    ldb = cb.ld;
+  }
+#pragma unroll
+  for (int a = 0; a < RPT; ++a) {
+    const int i = tr + TR * a;
+#pragma unroll
+    for (int b = 0; b < CPT; ++b) {
+      const int j = tc + TC * b;
+      double v = 0.0;
+      if (i < total && j < total) {
+        const PosDev pi = spos[i], pj = spos[j];
+        if constexpr (MICRO) {
+          if (i == j) {
+            v = sst[0][i];
+          } else {
+            const int dx = (pj.gid % args.side) - (pi.gid % args.side);
+            const int dy = (pj.gid / args.side) - (pi.gid / args.side);
+            if (dy == 0 && dx == 1) v = sst[1][i];
+            else if (dy == 0 && dx == -1) v = sst[2][i];
+            else if (dx == 0 && dy == 1) v = sst[3][i];
+            else if (dx == 0 && dy == -1) v = sst[4][i];
+          }
+        } else {
+          if ((pi.src >= 0) == (pj.src >= 0)) {
+            v = pi.src >= 0 ? A[pi.src + (long long)pj.src * lda]
+                            : B[(-pi.src - 1) + (long long)(-pj.src - 1) * ldb];
+          } else if (pi.partner == j) {
+            v = args.stencil[pi.dir * args.nu + pi.gid];
+          }
+        }
+      }
+      m[a][b] = v;
+    }
+  }
+
+  // ---- elimination of rows/columns [0, ni)
+  unsigned elim = 0u;
+  double pmin = DBL_MAX, pmax = 0.0;
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned gmask = (TR == 32) ? 0xffffffffu : (((1u << TR) - 1u) << (lane & ~unsigned(TR - 1)));
+  for (int k = 0; k < ni; ++k) {
+    const int bk = k / TC, tck = k % TC;
+    double* ck = colk[k & 1];
+    if (tc == tck) {
+      double best = -1.0;
+      int bi = 0x7fffffff;
+#pragma unroll
+      for (int a = 0; a < RPT; ++a) {
+        const int i = tr + TR * a;
+        double v = m[a][0];
+#pragma unroll
+        for (int b = 1; b < CPT; ++b)
+          if (b == bk) v = m[a][b];
+        if (i < total) ck[i] = v;
+        if (i < ni && !((elim >> a) & 1u)) {
+          const double av = fabs(v);
+          if (av > best) { best = av; bi = i; }
+        }
+      }
+#pragma unroll
+      for (int off = TR / 2; off > 0; off >>= 1) {
+        const double ob = __shfl_xor_sync(gmask, best, off, TR);
+        const int oi = __shfl_xor_sync(gmask, bi, off, TR);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (tr == 0) s_piv = bi;
+    }
+    __syncthreads();
+    const int p = s_piv;
+    const double pv = ck[p];
+    if (tr == p % TR) {
+      const int ap = p / TR;
+#pragma unroll
+      for (int a = 0; a < RPT; ++a) {
+        if (a == ap) {
+          elim |= 1u << a;
+#pragma unroll
+          for (int b = 0; b < CPT; ++b) {
+            const int j = tc + TC * b;
+            if (j < MAXT) rowp[j] = m[a][b];
+          }
+        }
+      }
+    }
+    const double apv = fabs(pv);
+    pmin = fmin(pmin, apv);
+    pmax = fmax(pmax, apv);
+    __syncthreads();
+    const double rinv = 1.0 / pv;
+#pragma unroll
+    for (int a = 0; a < RPT; ++a) {
+      const int i = tr + TR * a;
+      if (i < total && !((elim >> a) & 1u)) {
+        const double l = ck[i] * rinv;
+#pragma unroll
+        for (int b = 0; b < CPT; ++b) {
+          const int j = tc + TC * b;
+          if (j > k && j < total) m[a][b] = fma(-l, rowp[j], m[a][b]);
+        }
+      }
+    }
+  }
+
+  // ---- S = trailing block, written compact (ld = nd.ld)
+  double* out = args.arena + nd.s_off;
+#pragma unroll
+  for (int b = 0; b < CPT; ++b) {
+    const int j = tc + TC * b;
+#pragma unroll
+    for (int a = 0; a < RPT; ++a) {
+      const int i = tr + TR * a;
+      if (i >= ni && i < total && j >= ni && j < total) out[(i - ni) + (long long)(j - ni) * nd.ld] = m[a][b];
+    }
+  }
+  if (tid == 0) {
+    args.pivstat[2 * node_id] = ni > 0 ? pmin : DBL_MAX;
+    args.pivstat[2 * node_id + 1] = pmax;
+  }
+}
+
+// Launch dispatch by the largest system in the batch.
+#define DTNB_SMALL_VARIANTS(X) \
+  X(32, 8, 8, 4, 4)            \
+  X(64, 16, 16, 4, 4)          \
+  X(96, 16, 16, 6, 6)          \
+  X(128, 16, 32, 8, 4)         \
+  X(160, 16, 32, 10, 5)
+
+cudaError_t launch_small_elim(const KernelArgs& args, const int* d_list, int count, int max_total, bool micro,
+                              cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+#define X(LIM, TR, TC, RPT, CPT)                                                         \
+  if (max_total <= LIM) {                                                                \
+    if (micro) small_elim_kernel<TR, TC, RPT, CPT, true><<<count, TR * TC, 0, st>>>(args, d_list); \
+    else small_elim_kernel<TR, TC, RPT, CPT, false><<<count, TR * TC, 0, st>>>(args, d_list);      \
+    return cudaGetLastError();                                                           \
+  }
+  DTNB_SMALL_VARIANTS(X)
+#undef X
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace dtnb

@@ -1,0 +1,286 @@
+// Build plan (see plan.hpp). Geometry follows the reference:
+//   unknown ids        grid.hpp:68-70   (y-1)(n-2) + (x-1)
+//   CCW perimeter      grid.cpp:170-190
+//   quadtree           grid.cpp:213-266 (halve the full grid, left/south take the extra point)
+//   box index sets     grid.cpp:194-209
+//   merge ordering     dense_nd.cpp:114-131 (union boundary CCW, then the remaining
+//                      child boundary nodes, child a first)
+//   merge_four order   dense_nd.cpp:188-194 (SW+NW, SE+NE, W|E)
+#include "plan.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <stdexcept>
+
+namespace dtnb {
+
+void perimeter_ccw(const Rect& r, std::vector<std::pair<int, int>>& p) {
+  p.clear();
+  if (r.empty()) return;
+  if (r.x0 == r.x1 && r.y0 == r.y1) { p.push_back({r.x0, r.y0}); return; }
+  if (r.x0 == r.x1) { for (int y = r.y0; y <= r.y1; ++y) p.push_back({r.x0, y}); return; }
+  if (r.y0 == r.y1) { for (int x = r.x0; x <= r.x1; ++x) p.push_back({x, r.y0}); return; }
+  for (int x = r.x0; x <= r.x1; ++x) p.push_back({x, r.y0});
+  for (int y = r.y0 + 1; y <= r.y1; ++y) p.push_back({r.x1, y});
+  for (int x = r.x1 - 1; x >= r.x0; --x) p.push_back({x, r.y1});
+  for (int y = r.y1 - 1; y >= r.y0 + 1; --y) p.push_back({r.x0, y});
+}
+
+int perimeter_size(const Rect& r) {
+  if (r.empty()) return 0;
+  if (r.w() == 1 || r.h() == 1) return int(r.nodes());
+  return 2 * (r.w() + r.h()) - 4;
+}
+
+namespace {
+
+// Closed-form position of (x,y) in perimeter_ccw(r); (x,y) must lie on it.
+int ccw_index(const Rect& r, int x, int y) {
+  const int w = r.w(), h = r.h();
+  if (w == 1) return y - r.y0;
+  if (h == 1) return x - r.x0;
+  if (y == r.y0) return x - r.x0;
+  if (x == r.x1) return (w - 1) + (y - r.y0);
+  if (y == r.y1) return (w - 1) + (h - 1) + (r.x1 - x);
+  return 2 * (w - 1) + (h - 1) + (r.y1 - y);
+}
+
+bool on_perimeter(const Rect& r, int x, int y) { return x == r.x0 || x == r.x1 || y == r.y0 || y == r.y1; }
+
+struct Builder {
+  const PlanKey& key;
+  Plan& P;
+  int side;  // n - 2
+  std::vector<std::pair<int, int>> tmp;
+
+  Builder(const PlanKey& k, Plan& p) : key(k), P(p), side(k.n - 2) {}
+
+  int32_t gid(int x, int y) const { return int32_t(int64_t(y - 1) * side + (x - 1)); }
+
+  int add_micro(const Rect& r, int leaf_box) {
+    Node nd;
+    nd.kind = NodeKind::micro;
+    nd.r = r;
+    nd.nb = perimeter_size(r);
+    nd.total = int(r.nodes());
+    nd.ni = nd.total - nd.nb;
+    nd.ref_box = -1;
+    nd.label_box = leaf_box;
+    nd.pos_off = int64_t(P.pos.size());
+    for (int y = r.y0 + 1; y <= r.y1 - 1; ++y)
+      for (int x = r.x0 + 1; x <= r.x1 - 1; ++x) P.pos.push_back({0, -1, gid(x, y), 0});
+    perimeter_ccw(r, tmp);
+    for (auto [x, y] : tmp) P.pos.push_back({0, -1, gid(x, y), 0});
+    P.micro_flops += merge_flop_count(nd.ni, nd.nb);
+    P.nodes.push_back(nd);
+    return int(P.nodes.size()) - 1;
+  }
+
+  // merge_two (dense_nd.cpp:105-186) as a DAG node
+  int add_merge(int ia, int ib, int label_level, int label_box, bool tree_merge) {
+    if (ia < 0) return ib;
+    if (ib < 0) return ia;
+    const Rect ra = P.nodes[ia].r, rb = P.nodes[ib].r;
+    Rect u{std::min(ra.x0, rb.x0), std::max(ra.x1, rb.x1), std::min(ra.y0, rb.y0), std::max(ra.y1, rb.y1)};
+    if (u.nodes() != ra.nodes() + rb.nodes())
+      throw std::invalid_argument("merge_two: children do not tile a rectangle");
+    Node nd;
+    nd.kind = NodeKind::merge;
+    nd.r = u;
+    nd.a = ia;
+    nd.b = ib;
+    nd.nb = perimeter_size(u);
+    const int na = P.nodes[ia].nb, nbb = P.nodes[ib].nb;
+    nd.total = na + nbb;
+    nd.ni = nd.total - nd.nb;
+    nd.label_level = label_level;
+    nd.label_box = label_box;
+    nd.ref_box = -1;
+    nd.pos_off = int64_t(P.pos.size());
+    P.pos.resize(P.pos.size() + nd.total, PosEntry{0, -1, 0, 0});
+    PosEntry* pe = P.pos.data() + nd.pos_off;
+    std::vector<int> posA(na), posB(nbb);
+    int next_int = 0;
+    for (int c = 0; c < 2; ++c) {
+      const Rect& rc = c == 0 ? ra : rb;
+      std::vector<int>& pm = c == 0 ? posA : posB;
+      perimeter_ccw(rc, tmp);
+      for (int i = 0; i < int(tmp.size()); ++i) {
+        const auto [x, y] = tmp[i];
+        const int p = on_perimeter(u, x, y) ? nd.ni + ccw_index(u, x, y) : next_int++;
+        pm[i] = p;
+        pe[p].src = c == 0 ? i : -i - 1;
+        pe[p].gid = gid(x, y);
+      }
+    }
+    if (next_int != nd.ni) throw std::logic_error("merge_two: interface bookkeeping");
+    // couplings across the shared edge (dense_nd.cpp:148-165); exactly one
+    // partner per interface node for the 5-point stencil
+    auto couple = [&](int xa, int ya, int xb, int yb, int dir_ab, int dir_ba) {
+      const int pa = posA[ccw_index(ra, xa, ya)], pb = posB[ccw_index(rb, xb, yb)];
+      pe[pa].partner = pb;
+      pe[pa].dir = dir_ab;
+      pe[pb].partner = pa;
+      pe[pb].dir = dir_ba;
+    };
+    if (ra.x1 + 1 == rb.x0 && ra.y0 == rb.y0 && ra.y1 == rb.y1) {
+      for (int y = ra.y0; y <= ra.y1; ++y) couple(ra.x1, y, rb.x0, y, 1, 2);
+    } else if (rb.x1 + 1 == ra.x0 && ra.y0 == rb.y0 && ra.y1 == rb.y1) {
+      for (int y = ra.y0; y <= ra.y1; ++y) couple(ra.x0, y, rb.x1, y, 2, 1);
+    } else if (ra.y1 + 1 == rb.y0 && ra.x0 == rb.x0 && ra.x1 == rb.x1) {
+      for (int x = ra.x0; x <= ra.x1; ++x) couple(x, ra.y1, x, rb.y0, 3, 4);
+    } else if (rb.y1 + 1 == ra.y0 && ra.x0 == rb.x0 && ra.x1 == rb.x1) {
+      for (int x = ra.x0; x <= ra.x1; ++x) couple(x, ra.y0, x, rb.y1, 4, 3);
+    } else {
+      throw std::invalid_argument("merge_two: children are not edge-adjacent");
+    }
+    nd.wave = 1 + std::max(P.nodes[ia].wave, P.nodes[ib].wave);
+    if (tree_merge) P.merge_flops += merge_flop_count(nd.ni, nd.nb);
+    else P.micro_flops += merge_flop_count(nd.ni, nd.nb);
+    P.nodes.push_back(nd);
+    return int(P.nodes.size()) - 1;
+  }
+
+  // Leaf elimination below a reference leaf: binary splits of the longer
+  // side until a box fits one CTA (micro_max unknowns).
+  int leaf_node(const Rect& r, int leaf_box) {
+    if (r.empty()) return -1;
+    if (r.nodes() <= key.micro_max) return add_micro(r, leaf_box);
+    Rect lo = r, hi = r;
+    if (r.w() >= r.h()) {
+      const int wl = r.w() / 2;
+      lo.x1 = r.x0 + wl - 1;
+      hi.x0 = r.x0 + wl;
+    } else {
+      const int hl = r.h() / 2;
+      lo.y1 = r.y0 + hl - 1;
+      hi.y0 = r.y0 + hl;
+    }
+    const int a = leaf_node(lo, leaf_box), b = leaf_node(hi, leaf_box);
+    return add_merge(a, b, -1, leaf_box, false);
+  }
+};
+
+void build_ref_tree(const PlanKey& key, Plan& P) {
+  const int n = key.n;
+  if (n < 4) throw std::invalid_argument("build_tree: n must be >= 4");
+  int depth = 0;
+  const bool uniform = key.leaf_side > 0;
+  if (uniform) {
+    int s = n - 2;
+    while (s > key.leaf_side) {
+      if (s % 2) throw std::invalid_argument("build_tree: n-2 is not leaf_side * 2^L");
+      s /= 2;
+      ++depth;
+    }
+    if (s != key.leaf_side) throw std::invalid_argument("build_tree: n-2 is not leaf_side * 2^L");
+  } else {
+    if (key.n_leaf < 16) throw std::invalid_argument("build_tree: n_leaf must be >= 16");
+    while (double(n) * n > double(key.n_leaf) * std::pow(4.0, depth)) ++depth;  // grid.cpp:217-218
+  }
+  P.depth = depth;
+  P.levels.assign(depth + 1, {});
+  auto fill = [&](RefBox& b) {  // grid.cpp:194-209
+    b.r.x0 = std::max(b.gx0, 1);
+    b.r.y0 = std::max(b.gy0, 1);
+    b.r.x1 = std::min(b.gx1, n - 1) - 1;
+    b.r.y1 = std::min(b.gy1, n - 1) - 1;
+  };
+  RefBox root;
+  root.id = 0;
+  root.gx0 = uniform ? 1 : 0;
+  root.gx1 = uniform ? n - 1 : n;
+  root.gy0 = root.gx0;
+  root.gy1 = root.gx1;
+  fill(root);
+  P.boxes.push_back(root);
+  P.levels[0].push_back(0);
+  for (int lev = 0; lev < depth; ++lev) {
+    for (int id : P.levels[lev]) {
+      const RefBox pb = P.boxes[id];
+      const int xm = uniform ? pb.gx0 + (pb.gx1 - pb.gx0) / 2 : pb.gx0 + (pb.gx1 - pb.gx0 + 1) / 2;
+      const int ym = uniform ? pb.gy0 + (pb.gy1 - pb.gy0) / 2 : pb.gy0 + (pb.gy1 - pb.gy0 + 1) / 2;
+      const int reg[4][4] = {{pb.gx0, xm, pb.gy0, ym}, {xm, pb.gx1, pb.gy0, ym},
+                             {pb.gx0, xm, ym, pb.gy1}, {xm, pb.gx1, ym, pb.gy1}};
+      for (int c = 0; c < 4; ++c) {
+        RefBox ch;
+        ch.id = int(P.boxes.size());
+        ch.level = lev + 1;
+        ch.parent = id;
+        ch.gx0 = reg[c][0]; ch.gx1 = reg[c][1]; ch.gy0 = reg[c][2]; ch.gy1 = reg[c][3];
+        fill(ch);
+        P.boxes[id].children[c] = ch.id;
+        P.levels[lev + 1].push_back(ch.id);
+        P.boxes.push_back(ch);
+      }
+    }
+  }
+}
+
+int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+Plan make_plan(const PlanKey& key) {
+  if (key.micro_max < 4 || key.micro_max > key.small_max)
+    throw std::invalid_argument("make_plan: bad micro/small thresholds");
+  Plan P;
+  P.key = key;
+  P.n = key.n;
+  build_ref_tree(key, P);
+  Builder B(key, P);
+  // bottom-up over the reference tree (build_root_dense, dense_nd.cpp:196-216)
+  for (int lev = P.depth; lev >= 0; --lev) {
+    for (int id : P.levels[lev]) {
+      RefBox& bx = P.boxes[id];
+      if (lev == P.depth) {
+        bx.node = B.leaf_node(bx.r, id);
+      } else {
+        const int sw = P.boxes[bx.children[0]].node, se = P.boxes[bx.children[1]].node;
+        const int nw = P.boxes[bx.children[2]].node, ne = P.boxes[bx.children[3]].node;
+        const int w = B.add_merge(sw, nw, lev, id, true);
+        const int e = B.add_merge(se, ne, lev, id, true);
+        bx.node = B.add_merge(w, e, lev, id, true);
+      }
+      if (bx.node >= 0 && P.nodes[bx.node].ref_box < 0) P.nodes[bx.node].ref_box = id;
+    }
+  }
+  P.root = P.boxes[0].node;
+  if (P.root < 0) throw std::invalid_argument("make_plan: empty domain");
+  // waves and storage
+  int nw = 0;
+  for (auto& nd : P.nodes) nw = std::max(nw, nd.wave + 1);
+  P.waves.assign(nw, {});
+  int64_t off = 0, poff = 0;
+  for (int i = 0; i < int(P.nodes.size()); ++i) {
+    Node& nd = P.nodes[i];
+    Wave& wv = P.waves[nd.wave];
+    if (nd.kind == NodeKind::micro) {
+      wv.micro.push_back(i);
+    } else if (nd.total <= key.small_max) {
+      wv.small.push_back(i);
+    } else {
+      nd.blocked = true;
+      wv.blocked.push_back(i);
+      wv.max_ni_blocked = std::max(wv.max_ni_blocked, nd.ni);
+    }
+    if (nd.blocked) {
+      nd.ldm = int(align_up(nd.total, 8));
+      nd.m_off = off;
+      off = align_up(off + int64_t(nd.ldm) * nd.total, 32);
+      nd.s_off = nd.m_off + nd.ni + int64_t(nd.ni) * nd.ldm;
+      nd.ld = nd.ldm;
+      nd.piv_off = poff;
+      poff += align_up(std::max(nd.ni, 1), 4);
+    } else {
+      nd.ld = std::max(nd.nb, 1);
+      nd.s_off = off;
+      off = align_up(off + int64_t(nd.ld) * nd.nb, 32);
+    }
+  }
+  P.arena_doubles = std::max<int64_t>(off, 32);
+  P.piv_ints = std::max<int64_t>(poff, 4);
+  return P;
+}
+
+}  // namespace dtnb

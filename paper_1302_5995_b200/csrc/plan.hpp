@@ -1,0 +1,109 @@
+// Build plan for the B200 dense engine: the quadtree of the reference
+// (proj/src/grid.cpp:213-266, or an exact-halving uniform variant), extended
+// below its leaves by binary splits down to "micro boxes" small enough to be
+// eliminated by one CTA, turned into a DAG of pairwise merges scheduled in
+// waves (all merges of a wave are independent and run as one batched launch).
+//
+// Everything here is coefficient-independent (it depends only on n and the
+// tree parameters), so a plan is built once and cached per context.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace dtnb {
+
+struct Rect {
+  int x0 = 0, x1 = -1, y0 = 0, y1 = -1;  // inclusive unknown rectangle
+  int w() const { return x1 - x0 + 1; }
+  int h() const { return y1 - y0 + 1; }
+  bool empty() const { return x0 > x1 || y0 > y1; }
+  int64_t nodes() const { return empty() ? 0 : int64_t(w()) * h(); }
+};
+
+// CCW perimeter from the SW corner (grid.cpp:170-190); degenerate 1-wide
+// rectangles are a single scan.
+void perimeter_ccw(const Rect& r, std::vector<std::pair<int, int>>& out);
+int perimeter_size(const Rect& r);
+
+// Reference quadtree box (grid.hpp:120-141); children SW, SE, NW, NE.
+struct RefBox {
+  int id = -1, level = 0, parent = -1;
+  int children[4] = {-1, -1, -1, -1};
+  int gx0 = 0, gx1 = 0, gy0 = 0, gy1 = 0;
+  Rect r;
+  int node = -1;  // DAG node holding this box's Schur complement
+};
+
+// A device-side position descriptor of a merge or micro box: one per row of
+// the assembled system, in the order [interior; boundary(CCW)].
+struct PosEntry {
+  int32_t src;      // merge: >=0 index in child a's boundary, <0: -(index in b)-1
+                    // micro: unused (0)
+  int32_t partner;  // merge: position of the node coupled across the interface, or -1
+  int32_t gid;      // unknown id of this node
+  int32_t dir;      // merge: stencil direction of the coupling (1=E,2=W,3=N,4=S), 0 if none
+};
+
+enum class NodeKind : int { micro = 0, merge = 1 };
+
+struct Node {
+  NodeKind kind = NodeKind::micro;
+  Rect r;
+  int nb = 0;        // boundary size = perimeter_size(r)
+  int ni = 0;        // eliminated unknowns (micro: interior; merge: interface)
+  int total = 0;     // ni + nb (rows of the assembled system)
+  int a = -1, b = -1;  // children (merge)
+  int wave = 0;
+  int ref_box = -1;    // reference box id when this node is one
+  int label_level = -1, label_box = -1;  // error label (dense_nd.cpp:16-18)
+  bool blocked = false;  // assembled in HBM and eliminated by the blocked kernels
+  // storage (offsets in doubles into the plan arena)
+  int64_t s_off = 0;   // S block (nb x nb, leading dimension ld)
+  int ld = 0;
+  int64_t m_off = 0;   // blocked: assembled system (total x total, leading dim ldm)
+  int ldm = 0;
+  int64_t pos_off = 0;  // offset into the PosEntry table
+  int64_t piv_off = 0;  // blocked: offset into the int pivot table
+};
+
+struct Wave {
+  std::vector<int> micro, small, blocked;  // node ids
+  int max_ni_blocked = 0;
+};
+
+struct PlanKey {
+  int n = 0, n_leaf = 0, leaf_side = 0, micro_max = 0, small_max = 0;
+  bool operator==(const PlanKey& o) const {
+    return n == o.n && n_leaf == o.n_leaf && leaf_side == o.leaf_side && micro_max == o.micro_max &&
+           small_max == o.small_max;
+  }
+};
+
+struct Plan {
+  PlanKey key;
+  int n = 0;
+  int depth = 0;
+  std::vector<RefBox> boxes;
+  std::vector<std::vector<int>> levels;
+  std::vector<Node> nodes;
+  std::vector<Wave> waves;
+  std::vector<PosEntry> pos;  // all position tables
+  int64_t arena_doubles = 0;
+  int64_t piv_ints = 0;
+  int root = -1;  // root node
+  // algorithmic work (reference formulation)
+  double merge_flops = 0.0;     // sum of (2/3)ni^3 + 2ni^2nb + 2nb^2ni over reference-tree merges
+  double micro_flops = 0.0;     // leaf-interior elimination executed (same formula)
+};
+
+// Builds the plan; leaf_side > 0 selects the uniform tree (n-2 = leaf_side*2^L),
+// else the reference rule with n_leaf. Throws std::invalid_argument.
+Plan make_plan(const PlanKey& key);
+
+inline double merge_flop_count(double ni, double nb) {
+  return (2.0 / 3.0) * ni * ni * ni + 2.0 * ni * ni * nb + 2.0 * nb * nb * ni;
+}
+
+}  // namespace dtnb

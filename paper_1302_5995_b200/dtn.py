@@ -1,0 +1,498 @@
+"""Host-side mirror of the reference's build/solve API for the hot path,
+backed by the B200 engine through the C ABI (include/dtn_gpu.h).
+
+Same names, argument meaning and error behaviour as namespace `dtn` in
+/root/reference/proj/include/dtn/:
+  ProblemSpec / catalog / discretize   grid.hpp:32-53,111; problems.hpp:20
+  build_tree                           grid.hpp:159 (plus build_tree_uniform)
+  build_root_dense_op                  accel_nd.hpp:98-100
+  build_with_loads(..., Engine, ...)   bodyload.hpp:31-34 (Engine.gpu = this engine)
+  SolutionOperator                     solution_operator.hpp:30-53
+  apply_dtn / apply_schur / densify_dtn  solution_operator.hpp:55-63 (batched: g may be nb x batch)
+  FactorizationError                   errors.hpp:11-21
+Size/argument errors raise ValueError (std::invalid_argument), singular
+blocks FactorizationError, device failures RuntimeError. There is no CPU
+fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _lib as L
+
+
+class FactorizationError(RuntimeError):
+    """A factorization step hit a (near-)singular block (errors.hpp:11-21)."""
+
+    def __init__(self, message: str):
+        super().__init__(message)
+        self.where = message[message.rfind("[") + 1:-1] if message.endswith("]") else ""
+
+
+class Engine(enum.IntEnum):
+    dense = 0   # reference dense engine (CPU)
+    accel = 1   # reference compressed engine (CPU)
+    gpu = 2     # this B200 engine (dense merges on sm_100a)
+
+
+class ProblemMode(enum.IntEnum):
+    continuum = 0
+    network = 1
+
+
+Field = Optional[Callable[[np.ndarray, np.ndarray], np.ndarray]]
+
+
+@dataclass
+class ProblemSpec:
+    """grid.hpp:32-53. Coefficient fields take vectorised (x, y) arrays."""
+    name: str
+    n: int
+    h: float
+    mode: ProblemMode = ProblemMode.continuum
+    b: Field = None
+    c: Field = None
+    d: Field = None
+    conductivity_lo: float = 1.0
+    conductivity_hi: float = 1.0
+    seed: int = 0
+
+    @staticmethod
+    def continuum(name: str, n: int, b: Field, c: Field, d: Field) -> "ProblemSpec":
+        return ProblemSpec(name, n, 1.0 / (n - 1), ProblemMode.continuum, b, c, d)
+
+    @staticmethod
+    def network(name: str, n: int, lo: float, hi: float, seed: int) -> "ProblemSpec":
+        return ProblemSpec(name, n, 1.0 / (n - 1), ProblemMode.network, conductivity_lo=lo, conductivity_hi=hi,
+                           seed=seed)
+
+
+def _const(v: float):
+    return lambda x, y: np.full(np.broadcast(x, y).shape, float(v))
+
+
+def discrete_eigenvalue(p: int, q: int, n: int) -> float:
+    """problems.cpp:75-84."""
+    if p < 1 or q < 1 or p > n - 2 or q > n - 2:
+        raise ValueError("discrete_eigenvalue: indices out of range")
+    h = 1.0 / (n - 1)
+    return (4.0 - 2.0 * (math.cos(p * math.pi / (n - 1)) + math.cos(q * math.pi / (n - 1)))) / (h * h)
+
+
+def discrete_eigenvalue_kth(k: int, n: int) -> float:
+    """problems.cpp:86-110 (ties broken by (p, q))."""
+    if k < 1:
+        raise ValueError("discrete_eigenvalue_kth: k >= 1")
+    cap = min(n - 2, max(2 * k, 8))
+    if cap * cap < k:
+        raise ValueError("discrete_eigenvalue_kth: k exceeds spectrum")
+    es = sorted((discrete_eigenvalue(p, q, n), p, q) for p in range(1, cap + 1) for q in range(1, cap + 1))
+    return es[k - 1][0]
+
+
+CATALOG_NAMES = ["laplace", "diffconv1", "diffconv2", "diffconv3", "diffconv4", "helmholtz1", "helmholtz2",
+                 "helmholtz3", "helmholtz4", "random1", "random2"]
+
+
+def catalog_names():
+    return list(CATALOG_NAMES)
+
+
+def catalog(name: str, n: int, seed: int = 0) -> ProblemSpec:
+    """problems.cpp:26-73."""
+    pi = math.pi
+    z = _const(0.0)
+    if name == "laplace":
+        return ProblemSpec.continuum(name, n, z, z, z)
+    if name == "diffconv1":
+        return ProblemSpec.continuum(name, n, _const(100.0), z, z)
+    if name == "diffconv2":
+        return ProblemSpec.continuum(name, n, _const(1000.0), z, z)
+    if name == "diffconv3":
+        return ProblemSpec.continuum(name, n, lambda x, y: 125.0 * np.cos(4 * pi * y) + 0 * x,
+                                     lambda x, y: 125.0 * np.sin(4 * pi * x) + 0 * y, z)
+    if name == "diffconv4":
+        return ProblemSpec.continuum(name, n, lambda x, y: 125.0 * np.cos(4 * pi * x) + 0 * y,
+                                     lambda x, y: 125.0 * np.sin(4 * pi * y) + 0 * x, z)
+    if name == "helmholtz1":
+        return ProblemSpec.continuum(name, n, z, z, _const(-100.0))
+    if name == "helmholtz2":
+        return ProblemSpec.continuum(name, n, z, z, _const(-4005.0))
+    if name == "helmholtz3":
+        return ProblemSpec.continuum(name, n, z, z, _const(-discrete_eigenvalue_kth(10, n) + 1e-5))
+    if name == "helmholtz4":
+        k = 2.0 * pi * n / 40.0
+        return ProblemSpec.continuum(name, n, z, z, _const(-k * k))
+    if name == "random1":
+        return ProblemSpec.network(name, n, 1.0, 2.0, seed)
+    if name == "random2":
+        return ProblemSpec.network(name, n, 1.0, 1000.0, seed)
+    raise ValueError(f"catalog: unknown problem '{name}'")
+
+
+def baseline_problem(config: int, n_int: int | None = None) -> ProblemSpec:
+    """BASELINE.json configs restated as ProblemSpecs (n_int = interior side,
+    reference n = n_int + 2)."""
+    pi = math.pi
+    z = _const(0.0)
+    if config == 1:
+        return ProblemSpec.continuum("laplace", (n_int or 256) + 2, z, z, z)
+    if config == 2:
+        return ProblemSpec.continuum("helmholtz_k40", (n_int or 512) + 2, z, z, _const(-1600.0))
+    if config == 3:
+        k2 = 60.0 ** 2
+        return ProblemSpec.continuum(
+            "varcoef_k60", (n_int or 1024) + 2,
+            lambda x, y: 50.0 * np.cos(4 * pi * y) + 0 * x,
+            lambda x, y: 50.0 * np.sin(4 * pi * x) + 0 * y,
+            lambda x, y: -k2 * (1.0 - 0.5 * np.exp(-((x - 0.5) ** 2 + (y - 0.5) ** 2) / 0.02)))
+    if config == 4:
+        return ProblemSpec.continuum("laplace", (n_int or 4096) + 2, z, z, z)
+    if config == 5:
+        return ProblemSpec.continuum("helmholtz_k100", (n_int or 2048) + 2, z, z, _const(-1.0e4))
+    raise ValueError("baseline_problem: config must be 1..5")
+
+
+@dataclass
+class Lattice:
+    """grid.hpp:56-78."""
+    n: int
+
+    def side(self) -> int:
+        return self.n - 2
+
+    def num_unknowns(self) -> int:
+        return self.side() ** 2
+
+    def unknown_id(self, x: int, y: int) -> int:
+        return (y - 1) * self.side() + (x - 1)
+
+    def point_of(self, i: int):
+        return (i % self.side() + 1, i // self.side() + 1)
+
+
+@dataclass
+class DiscreteOperator:
+    """grid.hpp:91-102, stored as the 5-point stencil: stencil[r, k] for
+    r = center, east, west, north, south of unknown k."""
+    n: int
+    h: float
+    mode: ProblemMode
+    stencil: np.ndarray
+
+    def lattice(self) -> Lattice:
+        return Lattice(self.n)
+
+    def coeff(self, row: int, col: int) -> float:
+        lat = self.lattice()
+        if row == col:
+            return float(self.stencil[0, row])
+        (px, py), (qx, qy) = lat.point_of(row), lat.point_of(col)
+        for r, (dx, dy) in enumerate([(1, 0), (-1, 0), (0, 1), (0, -1)], start=1):
+            if qx - px == dx and qy - py == dy:
+                return float(self.stencil[r, row])
+        return 0.0
+
+
+def discretize(spec: ProblemSpec) -> DiscreteOperator:
+    """grid.cpp:106-168 (host side; coefficient samples at (x h, y h))."""
+    if spec.n < 4:
+        raise ValueError("discretize: n must be >= 4")
+    n, s = spec.n, spec.n - 2
+    st = np.zeros((5, s * s))
+    if spec.mode == ProblemMode.network:
+        rc = L.lib().dtn_discretize_network(n, spec.conductivity_lo, spec.conductivity_hi, spec.seed,
+                                            st.ctypes.data)
+    else:
+        idx = np.arange(s * s)
+        px = (idx % s + 1) * spec.h
+        py = (idx // s + 1) * spec.h
+        arrs = []
+        for f in (spec.b, spec.c, spec.d):
+            v = np.zeros(s * s) if f is None else np.ascontiguousarray(np.broadcast_to(f(px, py), (s * s,)),
+                                                                         dtype=np.float64)
+            arrs.append(v)
+        rc = L.lib().dtn_discretize_continuum(n, arrs[0].ctypes.data, arrs[1].ctypes.data, arrs[2].ctypes.data,
+                                              st.ctypes.data)
+    if rc != 0:
+        raise ValueError("discretize: coefficient is not finite")
+    return DiscreteOperator(n, spec.h, spec.mode, st)
+
+
+@dataclass
+class BoxTree:
+    """Tree parameters (grid.hpp:143-153); the geometry itself is realised by
+    the engine (grid.cpp:213-266). leaf_side > 0: uniform power-of-two tree."""
+    n: int
+    n_leaf: int = 0
+    leaf_side: int = 0
+
+
+def build_tree(n: int, n_leaf: int) -> BoxTree:
+    """grid.hpp:159."""
+    if n < 4:
+        raise ValueError("build_tree: n must be >= 4")
+    if n_leaf < 16:
+        raise ValueError("build_tree: n_leaf must be >= 16")
+    return BoxTree(n, n_leaf, 0)
+
+
+def build_tree_uniform(n: int, leaf_side: int) -> BoxTree:
+    s = n - 2
+    while s > leaf_side and s % 2 == 0:
+        s //= 2
+    if s != leaf_side:
+        raise ValueError("build_tree: n-2 is not leaf_side * 2^L")
+    return BoxTree(n, leaf_side * leaf_side, leaf_side)
+
+
+@dataclass
+class AccelOptions:
+    """accel_nd.hpp:14-22 (the compressed engine is not available yet)."""
+    epsilon: float = 1e-7
+    crossover: int = 1024
+    hbs_leaf: int = 64
+    rank_warn_cap: int = 4096
+    threads: int = 1
+
+
+@dataclass
+class LevelStats:
+    level: int
+    max_rank: int
+    bytes: int
+    seconds: float
+    boxes: int = 0
+    flops: float = 0.0
+
+
+# ------------------------------------------------------------------ context
+class Context:
+    """One engine context (device, stream, cached build plans)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        rc = L.lib().dtn_gpu_create(C.byref(h), device)
+        if rc != 0:
+            raise RuntimeError(f"dtn_gpu_create failed ({rc}): {L.lib().dtn_gpu_last_error(None).decode()}")
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            L.lib().dtn_gpu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_handle: int | None):
+        L.lib().dtn_gpu_set_stream(self.h, C.c_void_p(stream_handle or 0) if stream_handle else None)
+
+    def check(self, rc: int):
+        if rc == 0:
+            return
+        msg = L.lib().dtn_gpu_last_error(self.h).decode()
+        if rc == L.DTN_ESINGULAR:
+            raise FactorizationError(msg)
+        if rc == L.DTN_EINVAL:
+            raise ValueError(msg)
+        raise RuntimeError(f"dtn_gpu error {rc}: {msg}")
+
+
+_contexts: dict[int, Context] = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _contexts:
+        _contexts[device] = Context(device)
+    return _contexts[device]
+
+
+class SolutionOperator:
+    """solution_operator.hpp:30-53 for Engine.gpu: S and G stay in HBM; the
+    dense copies S_dense / G_dense are fetched on first access."""
+
+    def __init__(self, ctx: Context, handle: C.c_void_p, n: int, want_G: bool):
+        self.ctx, self.h, self.n = ctx, handle, n
+        self.engine = Engine.gpu
+        nb = C.c_int64()
+        ctx.check(L.lib().dtn_gpu_boundary(handle, None, C.byref(nb)))
+        self.boundary = np.zeros(nb.value, dtype=np.int64)
+        ctx.check(L.lib().dtn_gpu_boundary(handle, self.boundary.ctypes.data, C.byref(nb)))
+        self._S = None
+        self._G = None
+        self.has_G = want_G
+        cond = C.c_double()
+        ctx.check(L.lib().dtn_gpu_export(handle, None, None, C.byref(cond)))
+        self.cond_estimate = cond.value
+        st = L.dtn_build_stats()
+        ctx.check(L.lib().dtn_gpu_build_stats(handle, C.byref(st)))
+        self.build_stats = {f: getattr(st, f) for f, _ in L.dtn_build_stats._fields_}
+        cnt = C.c_int32()
+        ctx.check(L.lib().dtn_gpu_level_stats(handle, None, 0, C.byref(cnt)))
+        arr = (L.dtn_level_stats * cnt.value)()
+        ctx.check(L.lib().dtn_gpu_level_stats(handle, arr, cnt.value, C.byref(cnt)))
+        self.level_stats = [LevelStats(a.level, 0, 8 * a.max_boundary ** 2, a.seconds, a.boxes, a.flops)
+                            for a in arr]
+        ctx.check(L.lib().dtn_gpu_kernel_stats(handle, None, 0, C.byref(cnt)))
+        karr = (L.dtn_kernel_stats * max(cnt.value, 1))()
+        ctx.check(L.lib().dtn_gpu_kernel_stats(handle, karr, cnt.value, C.byref(cnt)))
+        self.kernel_stats = {k.name.decode(): dict(launches=k.launches, ms=k.ms, max_ms=k.max_ms, flops=k.flops,
+                                                   bytes=k.bytes) for k in karr[:cnt.value]}
+
+    def free(self):
+        if getattr(self, "h", None):
+            L.lib().dtn_gpu_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def boundary_size(self) -> int:
+        return len(self.boundary)
+
+    @property
+    def S_dense(self) -> np.ndarray:
+        if self._S is None:
+            nb = self.boundary_size()
+            S = np.zeros((nb, nb), order="F")
+            self.ctx.check(L.lib().dtn_gpu_export(self.h, S.ctypes.data, None, None))
+            self._S = S
+        return self._S
+
+    @property
+    def G_dense(self) -> np.ndarray:
+        if self._G is None:
+            nb = self.boundary_size()
+            G = np.zeros((nb, nb), order="F")
+            self.ctx.check(L.lib().dtn_gpu_export(self.h, None, G.ctypes.data, None))
+            self._G = G
+        return self._G
+
+    def memory_bytes(self) -> int:
+        """solution_operator.cpp:5-18 (dense: S and G payloads)."""
+        nb = self.boundary_size()
+        return 8 * nb * nb * (2 if self.has_G else 1)
+
+    def device_ptrs(self):
+        s, g, ld = C.c_void_p(), C.c_void_p(), C.c_int64()
+        self.ctx.check(L.lib().dtn_gpu_device_ptrs(self.h, C.byref(s), C.byref(g), C.byref(ld)))
+        return s.value, g.value, ld.value
+
+    # per-box access to the build tree (testing aid)
+    def num_boxes(self):
+        cnt, depth = C.c_int32(), C.c_int32()
+        self.ctx.check(L.lib().dtn_gpu_num_boxes(self.h, C.byref(cnt), C.byref(depth)))
+        return cnt.value, depth.value
+
+    def box_info(self, box: int) -> dict:
+        info = (C.c_int32 * 11)()
+        self.ctx.check(L.lib().dtn_gpu_box_info(self.h, box, info))
+        v = list(info)
+        return dict(level=v[0], parent=v[1], x0=v[2], x1=v[3], y0=v[4], y1=v[5], nb=v[6], children=v[7:11])
+
+    def box_schur(self, box: int) -> np.ndarray:
+        nb = self.box_info(box)["nb"]
+        S = np.zeros((nb, nb), order="F")
+        self.ctx.check(L.lib().dtn_gpu_box_schur(self.h, box, S.ctypes.data))
+        return S
+
+
+def build_root_gpu(op: DiscreteOperator | None, tree: BoxTree, want_G: bool = True, micro_max: int = 0,
+                   ctx: Context | None = None, stencil_device_ptr: int | None = None,
+                   profile: bool = False) -> SolutionOperator:
+    """The B200 build: leaf elimination + merges + root inverse, through dtn_gpu_build."""
+    ctx = ctx or default_context()
+    if stencil_device_ptr:
+        prob = L.dtn_problem(tree.n, stencil_device_ptr, 1)
+    else:
+        if tree.n != op.n:
+            raise ValueError("build: tree and operator sizes differ")
+        st = np.ascontiguousarray(op.stencil, dtype=np.float64)
+        prob = L.dtn_problem(op.n, st.ctypes.data, 0)
+    opts = L.dtn_opts(0, tree.n_leaf, tree.leaf_side, 1 if want_G else 0, micro_max, 1 if profile else 0, 0.0, 0)
+    h = C.c_void_p()
+    ctx.check(L.lib().dtn_gpu_build(ctx.h, C.byref(prob), C.byref(opts), C.byref(h)))
+    return SolutionOperator(ctx, h, tree.n, want_G)
+
+
+def build_root_dense_op(op: DiscreteOperator, tree: BoxTree, loads=None) -> SolutionOperator:
+    """accel_nd.hpp:98-100, executed by the B200 engine."""
+    if loads:
+        raise NotImplementedError("body-load panels are not part of the B200 hot path yet")
+    return build_root_gpu(op, tree)
+
+
+def build_with_loads(op: DiscreteOperator, tree: BoxTree, loads, engine: Engine, opt: AccelOptions | None = None):
+    """bodyload.cpp:47-57 dispatcher; Engine.gpu (and Engine.dense, which the
+    B200 engine executes) build here."""
+    if engine == Engine.accel:
+        raise NotImplementedError("the compressed (accel) engine is not available in the B200 build yet")
+    return build_root_dense_op(op, tree, loads)
+
+
+def _apply(sol: SolutionOperator, which: int, g):
+    nb = sol.boundary_size()
+    try:
+        import torch
+        is_t = isinstance(g, torch.Tensor)
+    except ImportError:  # pragma: no cover
+        is_t = False
+    if is_t:
+        if g.dtype != torch.float64 or not g.is_cuda:
+            raise ValueError("apply: torch input must be a float64 CUDA tensor")
+        vec = g.dim() == 1
+        X = g.reshape(nb, -1) if vec else g
+        if X.shape[0] != nb:
+            raise ValueError("apply_dtn: boundary vector size mismatch")
+        Xf = X.t().contiguous().t() if X.stride(0) != 1 else X
+        Y = torch.empty((X.shape[1], nb), dtype=torch.float64, device=g.device).t()
+        sol.ctx.check(L.lib().dtn_gpu_apply(sol.h, which, Xf.data_ptr(), Xf.stride(1) if Xf.shape[1] > 1 else nb,
+                                            Xf.shape[1], Y.data_ptr(), nb, 1))
+        return Y.reshape(nb) if vec else Y
+    X = np.asarray(g, dtype=np.float64)
+    vec = X.ndim == 1
+    if X.shape[0] != nb:
+        raise ValueError(("apply_dtn" if which == 0 else "apply_schur") + ": boundary vector size mismatch")
+    X2 = np.asfortranarray(X.reshape(nb, -1))
+    Y = np.zeros_like(X2, order="F")
+    sol.ctx.check(L.lib().dtn_gpu_apply(sol.h, which, X2.ctypes.data, nb, X2.shape[1], Y.ctypes.data, nb, 0))
+    return Y[:, 0].copy() if vec else Y
+
+
+def apply_dtn(sol: SolutionOperator, g):
+    """v = G g (solution_operator.cpp:36-44); g may be (nb,) or (nb, batch)."""
+    return _apply(sol, 0, g)
+
+
+def apply_schur(sol: SolutionOperator, g):
+    """S g (solution_operator.cpp:46-52)."""
+    return _apply(sol, 1, g)
+
+
+def densify_dtn(sol: SolutionOperator) -> np.ndarray:
+    """solution_operator.cpp:54-66."""
+    return sol.G_dense
+
+
+def root_boundary(tree: BoxTree) -> np.ndarray:
+    """Canonical CCW ring of root unknowns (grid.cpp:185-188)."""
+    s = tree.n - 2
+    if s == 1:
+        return np.array([0], dtype=np.int64)
+    pts = [(x, 1) for x in range(1, s + 1)] + [(s, y) for y in range(2, s + 1)] + \
+          [(x, s) for x in range(s - 1, 0, -1)] + [(1, y) for y in range(s - 1, 1, -1)]
+    return np.array([(y - 1) * s + (x - 1) for x, y in pts], dtype=np.int64)

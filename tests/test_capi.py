@@ -1,0 +1,77 @@
+"""CPU-side checks of the product library: it loads, exports every symbol
+include/dtn_gpu.h declares, discretizes exactly like the oracle, and fails
+loudly (no CPU fallback) when no device is present."""
+import re
+
+import numpy as np
+import pytest
+
+import paper_1302_5995_b200 as dtn
+from paper_1302_5995_b200 import _lib as L
+from oracle import oracle as O
+
+
+def header_symbols():
+    src = open(L.HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+\*?(dtn_\w+)\(", src, re.M)))
+
+
+def test_library_exports_header_symbols():
+    lib = L.lib()
+    syms = header_symbols()
+    assert len(syms) >= 17
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(L.EXPORTS)
+
+
+@pytest.mark.parametrize("name", O.CATALOG)
+def test_discretize_matches_oracle(name):
+    if name == "helmholtz3":  # lambda_10 needs >= 10 eigenvalues (problems.cpp:88-93)
+        with pytest.raises(ValueError):
+            dtn.catalog(name, 5)
+        with pytest.raises(O.OracleError):
+            O.Problem(name, 5)
+    for n in ((12, 33) if name == "helmholtz3" else (5, 12, 33)):
+        a = dtn.discretize(dtn.catalog(name, n, seed=7)).stencil
+        b = O.Problem(name, n, seed=7).stencil()
+        assert np.array_equal(a, b), name
+
+
+def test_baseline_problems_match_oracle():
+    for cfg, oname, par in [(1, "laplace", 0.0), (2, "helmholtz", 40.0), (3, "varcoef", 60.0),
+                            (5, "helmholtz", 100.0)]:
+        a = dtn.discretize(dtn.baseline_problem(cfg, 30)).stencil
+        b = O.Problem(oname, 32, par).stencil()
+        np.testing.assert_allclose(a, b, rtol=1e-15, atol=0)
+
+
+def test_discretize_rejects_bad_input():
+    with pytest.raises(ValueError):
+        dtn.discretize(dtn.catalog("laplace", 3))
+    bad = dtn.ProblemSpec.continuum("bad", 8, lambda x, y: np.full_like(x, np.nan), None, None)
+    with pytest.raises(ValueError):
+        dtn.discretize(bad)
+
+
+def test_tree_argument_errors():
+    with pytest.raises(ValueError):
+        dtn.build_tree(3, 64)
+    with pytest.raises(ValueError):
+        dtn.build_tree(16, 8)
+    with pytest.raises(ValueError):
+        dtn.build_tree_uniform(100, 16)
+
+
+def test_root_boundary_ccw():
+    b = dtn.root_boundary(dtn.build_tree(16, 64))
+    t = O.Tree(16, 64)
+    assert np.array_equal(b, t.root()["boundary"])
+
+
+def test_no_cpu_fallback_without_device():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("device present")
+    with pytest.raises(RuntimeError):
+        dtn.Context(0)

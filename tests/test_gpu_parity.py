@@ -1,0 +1,163 @@
+"""GPU parity: the B200 engine (through the C ABI) against the CPU oracle
+(the restated reference dense engine) and the brute-force Schur complement.
+Tolerances follow BASELINE.json: relative Frobenius <= 1e-10 for S and the
+Neumann data S g (uncompressed merges)."""
+import numpy as np
+import pytest
+
+import paper_1302_5995_b200 as dtn
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def gpu_build(name, n, n_leaf=16, leaf_side=0, seed=0, param=None, micro_max=0, want_G=True):
+    if param is not None:
+        spec = dtn.baseline_problem({"helmholtz": 2, "varcoef": 3}[name], n - 2)
+        if name == "helmholtz":
+            spec = dtn.ProblemSpec.continuum("helmholtz", n, None, None,
+                                             lambda x, y: np.full_like(x, -param * param))
+    else:
+        spec = dtn.catalog(name, n, seed=seed)
+    op = dtn.discretize(spec)
+    tree = dtn.build_tree_uniform(n, leaf_side) if leaf_side else dtn.build_tree(n, n_leaf)
+    return dtn.build_root_gpu(op, tree, want_G=want_G, micro_max=micro_max)
+
+
+@pytest.mark.parametrize("n", [8, 16, 24, 32])
+@pytest.mark.parametrize("name", ["laplace", "diffconv1", "random1"])
+def test_root_S_vs_brute_and_oracle(n, name):  # test_dense_nd.cpp:123-132
+    sol = gpu_build(name, n, 16, seed=3)
+    p = O.Problem(name, n, seed=3)
+    t = O.Tree(n, 16)
+    rb = t.root()
+    assert np.array_equal(sol.boundary, rb["boundary"])
+    brute = O.brute_schur(p.dense_A(), rb["boundary"], rb["interior"])
+    assert O.rel_fro(sol.S_dense, brute) <= TOL
+    assert O.rel_fro(sol.S_dense, O.build_root_dense(p, t).S) <= TOL
+
+
+@pytest.mark.parametrize("n", [8, 16, 32])
+def test_acceptance_criterion1_all_catalog(n):  # acceptance.cpp:74-114
+    worst = 0.0
+    for name in O.CATALOG:
+        sol = gpu_build(name, n, 16, seed=1)
+        p = O.Problem(name, n, seed=1)
+        rb = O.Tree(n, 16).root()
+        worst = max(worst, O.rel_fro(sol.S_dense, O.brute_schur(p.dense_A(), rb["boundary"], rb["interior"])))
+    assert worst <= TOL
+
+
+@pytest.mark.parametrize("name,n,n_leaf", [("diffconv3", 66, 64), ("helmholtz2", 70, 100), ("random2", 45, 40)])
+def test_every_box_matches_oracle(name, n, n_leaf):
+    sol = gpu_build(name, n, n_leaf, seed=2)
+    p = O.Problem(name, n, seed=2)
+    t = O.Tree(n, n_leaf)
+    ref = O.build_root_dense(p, t, keep_all=True)
+    cnt, depth = sol.num_boxes()
+    assert cnt == len(t.boxes) and depth == t.depth
+    for bid in range(cnt):
+        info = sol.box_info(bid)
+        bx = t.boxes[bid]
+        assert (info["x0"], info["x1"], info["y0"], info["y1"]) == (bx["x0"], bx["x1"], bx["y0"], bx["y1"])
+        assert O.rel_fro(sol.box_schur(bid), ref.box_S(bid)) <= TOL, bid
+
+
+@pytest.mark.parametrize("micro_max", [16, 40, 64, 128, 160])
+def test_leaf_granularity_does_not_change_S(micro_max):
+    sol = gpu_build("diffconv4", 66, leaf_side=16, micro_max=micro_max)
+    ref = O.build_root_dense(O.Problem("diffconv4", 66), O.Tree(66, uniform_side=16))
+    assert O.rel_fro(sol.S_dense, ref.S) <= TOL
+
+
+def test_G_S_identity_and_solve():  # test_dense_nd.cpp:158-173
+    sol = gpu_build("laplace", 32, 64)
+    G, S = sol.G_dense, sol.S_dense
+    assert np.max(np.abs(G @ S - np.eye(len(S)))) <= 1e-10
+    p = O.Problem("laplace", 32)
+    A = p.dense_A()
+    rng = np.random.default_rng(17)
+    r = rng.standard_normal(len(sol.boundary))
+    r /= np.linalg.norm(r)
+    rhs = np.zeros(A.shape[0])
+    rhs[sol.boundary] = r
+    ref = np.linalg.solve(A, rhs)[sol.boundary]
+    assert np.linalg.norm(dtn.apply_dtn(sol, r) - ref) / np.linalg.norm(ref) <= 1e-10
+
+
+def test_near_resonant_condition():  # test_dense_nd.cpp:195-201
+    h3 = gpu_build("helmholtz3", 32, 64)
+    lap = gpu_build("laplace", 32, 64)
+    assert h3.cond_estimate > 100.0 * lap.cond_estimate
+    ref = O.build_root_dense(O.Problem("helmholtz3", 32), O.Tree(32, 64))
+    assert h3.cond_estimate == pytest.approx(ref.cond, rel=1e-6)
+
+
+def test_singular_block_raises_with_label():
+    op = dtn.discretize(dtn.ProblemSpec.network("zero", 20, 0.0, 0.0, 0))
+    with pytest.raises(dtn.FactorizationError) as e:
+        dtn.build_root_gpu(op, dtn.build_tree(20, 64))
+    assert "leaf box" in e.value.where
+
+
+def test_apply_argument_errors():
+    sol = gpu_build("laplace", 16, 16)
+    with pytest.raises(ValueError):
+        dtn.apply_dtn(sol, np.zeros(len(sol.boundary) + 1))
+    nog = gpu_build("laplace", 16, 16, want_G=False)
+    with pytest.raises(ValueError):
+        dtn.apply_dtn(nog, np.zeros(len(nog.boundary)))
+    assert np.allclose(dtn.apply_schur(nog, np.ones(len(nog.boundary))), nog.S_dense @ np.ones(len(nog.boundary)))
+
+
+def test_batched_apply_host_and_device():
+    import torch
+    sol = gpu_build("helmholtz1", 66, leaf_side=16)
+    nb = len(sol.boundary)
+    rng = np.random.default_rng(5)
+    X = rng.uniform(-1, 1, (nb, 37))
+    ref_G, ref_S = sol.G_dense @ X, sol.S_dense @ X
+    assert O.rel_fro(dtn.apply_dtn(sol, X), ref_G) <= 1e-13
+    assert O.rel_fro(dtn.apply_schur(sol, X), ref_S) <= 1e-13
+    Xd = torch.from_numpy(X).cuda()
+    assert O.rel_fro(dtn.apply_dtn(sol, Xd).cpu().numpy(), ref_G) <= 1e-13
+    assert O.rel_fro(dtn.apply_schur(sol, Xd[:, 3]).cpu().numpy(), ref_S[:, 3]) <= 1e-13
+
+
+def _cfg_case(cfg, n_int, seed_vectors, nvec):
+    name, par = {1: ("laplace", 0.0), 2: ("helmholtz", 40.0)}[cfg]
+    n = n_int + 2
+    sol = dtn.build_root_gpu(dtn.discretize(dtn.baseline_problem(cfg, n_int)), dtn.build_tree_uniform(n, 16))
+    ref = O.build_root_dense(O.Problem(name, n, par), O.Tree(n, uniform_side=16), threads=8, mode=2)
+    rng = np.random.Generator(np.random.MT19937(seed_vectors))
+    g = rng.uniform(-1.0, 1.0, (len(ref.boundary), nvec))
+    return sol, ref, g
+
+
+def test_baseline_config1_full_size():
+    sol, ref, g = _cfg_case(1, 256, 1, 1)
+    assert np.array_equal(sol.boundary, ref.boundary)
+    assert O.rel_fro(sol.S_dense, ref.S) <= TOL
+    assert O.rel_fro(dtn.apply_schur(sol, g), ref.S @ g) <= TOL          # Neumann data
+    assert O.rel_fro(sol.G_dense, ref.G) <= TOL
+    assert O.rel_fro(dtn.apply_dtn(sol, g), ref.G @ g) <= TOL
+    assert sol.cond_estimate == pytest.approx(ref.cond, rel=1e-8)
+
+
+def test_baseline_config2_full_size():
+    sol, ref, g = _cfg_case(2, 512, 1, 16)
+    assert O.rel_fro(sol.S_dense, ref.S) <= TOL
+    assert O.rel_fro(dtn.apply_schur(sol, g), ref.S @ g) <= TOL
+    # G is condition-limited: check it as an inverse of the oracle S
+    nb = len(ref.boundary)
+    assert np.linalg.norm(ref.S @ sol.G_dense - np.eye(nb)) / np.sqrt(nb) <= 1e-10 * max(1.0, sol.cond_estimate)
+    assert O.rel_fro(dtn.apply_dtn(sol, g), ref.G @ g) <= 1e-10 * max(1.0, sol.cond_estimate)
+
+
+def test_reference_tree_baseline_size():
+    # the reference's own 15/16/17-wide partition (build_tree(258, 289)) against the oracle
+    n = 258
+    sol = dtn.build_root_gpu(dtn.discretize(dtn.baseline_problem(1, 256)), dtn.build_tree(n, 289))
+    ref = O.build_root_dense(O.Problem("laplace", n), O.Tree(n, 289), threads=8, mode=2)
+    assert O.rel_fro(sol.S_dense, ref.S) <= TOL
