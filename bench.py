@@ -247,6 +247,7 @@ def run_b200(args, cfg, rank, world, local):
     # ---- per-kernel roofline from one profiled build (not timed above)
     prof = dtn.build_root_gpu(None, tree, ctx=ctx, stencil_device_ptr=stencil_d.data_ptr(), profile=True)
     ks = prof.kernel_stats
+    pst = prof.build_stats  # per-phase split (leaf / merges / inverse) from the profiled, event-timed build
     prof.free()
     peak_tf, peak_src = fp64_peak()
     hbm, hbm_src = hbm_peak()
@@ -269,7 +270,7 @@ def run_b200(args, cfg, rank, world, local):
     except Exception:
         pass
 
-    merge_tf = stats["merge_flops"] / (stats["merge_ms"] * 1e-3) / 1e12 if stats["merge_ms"] > 0 else None
+    merge_tf = pst["merge_flops"] / (pst["merge_ms"] * 1e-3) / 1e12 if pst["merge_ms"] > 0 else None
     line = {
         "metric": METRIC, "value": value, "unit": "grid-points/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -284,8 +285,9 @@ def run_b200(args, cfg, rank, world, local):
         "gpu_launches": launches_per_step * args.steps,
         "roofline": roof,
         "clocks": clk.summary(),
-        "build": {"build_ms": stats["build_ms"], "leaf_ms": stats["leaf_ms"], "merge_ms": stats["merge_ms"],
-                  "inverse_ms": stats["inverse_ms"], "merge_gflop": stats["merge_flops"] / 1e9,
+        "build": {"build_ms": stats["build_ms"], "profiled_build_ms": pst["build_ms"], "leaf_ms": pst["leaf_ms"],
+                  "merge_ms": pst["merge_ms"], "inverse_ms": pst["inverse_ms"],
+                  "merge_gflop": pst["merge_flops"] / 1e9,
                   "merge_tflops": merge_tf,
                   "merge_frac_fp64_peak": merge_tf / peak_tf if merge_tf else None,
                   "build_tflops_algorithmic": (stats["merge_flops"] + stats["inverse_flops"]) /

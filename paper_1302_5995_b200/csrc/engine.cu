@@ -27,7 +27,7 @@ namespace dtnb {
 cudaError_t launch_small_elim(const KernelArgs&, const int*, int, int, bool, cudaStream_t);
 cudaError_t launch_gather(const KernelArgs&, const int*, int, int, cudaStream_t);
 cudaError_t launch_panel(const KernelArgs&, const int*, int, int, int, int, cudaStream_t);
-cudaError_t launch_rowpanel(const KernelArgs&, const int*, int, int, int, int, int, int, cudaStream_t);
+cudaError_t launch_rowpanel(const KernelArgs&, const int*, int, int, int, int, bool, cudaStream_t);
 cudaError_t launch_trailing_update(const KernelArgs&, const int*, int, int, int, int, cudaStream_t);
 cudaError_t launch_gemm_desc(const GemmDesc*, int, int, int, double, double, cudaStream_t);
 cudaError_t launch_perm_identity(const int*, int, int*, double*, int, cudaStream_t);
@@ -60,12 +60,11 @@ int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
 constexpr int kSmallMax = 160;
 constexpr int kDefaultMicro = 128;
-constexpr size_t kPanelSmem = 220 * 1024;
 
+// Panel width; the register-resident panel spans up to 8 CTAs x 512 rows.
 int panel_kb(int rows) {
-  for (int kb : {32, 16, 8})
-    if (size_t(kb) * size_t(rows | 1) * sizeof(double) <= kPanelSmem) return kb;
-  throw std::invalid_argument("dense merge interface too large for the one-CTA panel (ni > 3500)");
+  if (rows > 8 * 512) throw std::invalid_argument("dense merge system too large for the cluster panel (> 4096 rows)");
+  return 32;
 }
 
 struct WaveLaunch {
@@ -207,7 +206,7 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
       L.blk_max_ni = std::max(L.blk_max_ni, nd.ni);
       L.blk_max_nb = std::max(L.blk_max_nb, nd.nb);
     }
-    if (L.blk_cnt) L.kb = panel_kb(L.blk_max_ni);
+    if (L.blk_cnt) L.kb = panel_kb(L.blk_max_total);
     for (int id : wv.small) {
       const Node& nd = P.nodes[id];
       if (nd.label_level >= 0) L.level = L.level < 0 ? nd.label_level : std::min(L.level, nd.label_level);
@@ -290,7 +289,7 @@ struct Prof {
 };
 
 // All device work of one build, in stream order (captured into a graph).
-void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullptr) {
+void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullptr, bool events = true) {
   const Plan& P = D.P;
   const KernelArgs a = D.args();
   int launches = 0;
@@ -314,7 +313,7 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
     return f;
   };
   const std::vector<int>& hl = D.h_lists;
-  CK(cudaEventRecord(D.ev_start, st));
+  if (events) CK(cudaEventRecord(D.ev_start, st));
   for (size_t w = 0; w < D.wl.size(); ++w) {
     const WaveLaunch& L = D.wl[w];
     if (L.micro_cnt)
@@ -337,26 +336,26 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
           const Node& nd = P.nodes[hlst[i]];
           if (k0 >= nd.ni) continue;
           const double kbe = std::min(L.kb, nd.ni - k0), rows = nd.ni - k0, mn = nd.total - k0 - kbe;
-          fp += rows * kbe * kbe;
+          fp += (nd.total - k0) * kbe * kbe;
           fr += kbe * kbe * mn;
           ft += 2.0 * mn * mn * kbe;
         }
-        run(K_PANEL, fp, 0.0, [&] { return launch_panel(a, lst, L.blk_cnt, L.blk_max_ni, k0, L.kb, st); });
-        run(K_ROWPANEL, fr, 0.0, [&] {
-          return launch_rowpanel(a, lst, L.blk_cnt, L.blk_max_total, 0, L.blk_max_nb, k0, L.kb, st);
-        });
+        run(K_PANEL, fp, 0.0,
+            [&] { return launch_panel(a, lst, L.blk_cnt, L.blk_max_total - k0, k0, L.kb, st); });
+        run(K_ROWPANEL, fr, 0.0,
+            [&] { return launch_rowpanel(a, lst, L.blk_cnt, L.blk_max_total, k0, L.kb, false, st); });
         run(K_TRAILING, ft, 0.0,
             [&] { return launch_trailing_update(a, lst, L.blk_cnt, L.blk_max_total, k0, L.kb, st); });
       }
     }
-    CK(cudaEventRecord(D.ev_wave[w], st));
+    if (events) CK(cudaEventRecord(D.ev_wave[w], st));
   }
   // compact copy of the root S
   const Node& root = P.nodes[P.root];
   const double* Sview = D.d_arena + root.s_off;
   const double nb2 = double(D.nb) * D.nb;
   run(K_COPY, 0.0, 16.0 * nb2, [&] { return launch_copy2d(Sview, root.ld, D.d_S, D.lds, D.nb, D.nb, st); });
-  CK(cudaEventRecord(D.ev_root, st));
+  if (events) CK(cudaEventRecord(D.ev_root, st));
   if (want_G) {
     const int nb = D.nb;
     double* LU = D.d_arena + D.lu_off;
@@ -364,8 +363,9 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
     const int* rl = D.d_lists + D.root_list_off;
     for (int k0 = 0; k0 < nb; k0 += D.root_kb) {
       const double kbe = std::min(D.root_kb, nb - k0), rows = nb - k0, mn = nb - k0 - kbe;
-      run(K_PANEL, rows * kbe * kbe, 0.0, [&] { return launch_panel(a, rl, 1, nb, k0, D.root_kb, st); });
-      run(K_ROWPANEL, kbe * kbe * mn, 0.0, [&] { return launch_rowpanel(a, rl, 1, nb, 0, 0, k0, D.root_kb, st); });
+      run(K_PANEL, rows * kbe * kbe, 0.0, [&] { return launch_panel(a, rl, 1, nb - k0, k0, D.root_kb, st); });
+      run(K_ROWPANEL, kbe * kbe * mn, 0.0,
+          [&] { return launch_rowpanel(a, rl, 1, nb, k0, D.root_kb, true, st); });
       run(K_TRAILING, 2.0 * mn * mn * kbe, 0.0,
           [&] { return launch_trailing_update(a, rl, 1, nb, k0, D.root_kb, st); });
     }
@@ -399,7 +399,7 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
     run(K_MISC, 0.0, 8.0 * nb2, [&] { return launch_norm1(D.d_S, D.lds, nb, nb, D.d_norm, st); });
     run(K_MISC, 0.0, 8.0 * nb2, [&] { return launch_norm1(D.d_G, D.ldg, nb, nb, D.d_norm + 1, st); });
   }
-  CK(cudaEventRecord(D.ev_end, st));
+  if (events) CK(cudaEventRecord(D.ev_end, st));
   D.launches = launches;
 }
 
@@ -441,6 +441,7 @@ thread_local std::string g_err;  // errors with no context (dtn_gpu_create)
 template <class F>
 int guarded(dtn_ctx* ctx, F&& f) {
   std::string& err = ctx ? ctx->err : g_err;
+  (void)cudaGetLastError();  // drop stale non-sticky errors from unrelated runtime calls
   try {
     f();
     err.clear();
@@ -555,7 +556,7 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
         try {
-          enqueue_build(*D, cap, want_G);
+          enqueue_build(*D, cap, want_G, nullptr, false);
         } catch (...) {
           cudaStreamEndCapture(cap, &g);
           cudaStreamDestroy(cap);
@@ -567,7 +568,9 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
         CK(cudaStreamDestroy(cap));
         D->graph_want_G = int(want_G);
       }
+      CK(cudaEventRecord(D->ev_start, st));
       CK(cudaGraphLaunch(D->gexec, st));
+      CK(cudaEventRecord(D->ev_end, st));
     } else {
       enqueue_build(*D, st, want_G);
     }
@@ -602,12 +605,16 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
     // timings
     auto ms = [](cudaEvent_t a, cudaEvent_t b) {
       float t = 0.f;
-      cudaEventElapsedTime(&t, a, b);
+      if (cudaEventElapsedTime(&t, a, b) != cudaSuccess) {
+        (void)cudaGetLastError();  // not a sticky error: do not poison later launches
+        return -1.0;
+      }
       return double(t);
     };
     dtn_build_stats& s = op->stats;
+    const bool graph_run = !profile && use_graphs();
     s.build_ms = ms(D->ev_start, D->ev_end);
-    s.inverse_ms = ms(D->ev_root, D->ev_end);
+    s.inverse_ms = graph_run ? 0.0 : ms(D->ev_root, D->ev_end);
     s.merge_flops = P.merge_flops;
     s.leaf_flops = P.micro_flops;
     s.inverse_flops = want_G ? 2.0 * double(D->nb) * D->nb * D->nb : 0.0;
@@ -622,7 +629,7 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
     }
     cudaEvent_t prev = D->ev_start;
     for (size_t w = 0; w < D->wl.size(); ++w) {
-      const double t = ms(prev, D->ev_wave[w]);
+      const double t = graph_run ? 0.0 : ms(prev, D->ev_wave[w]);
       prev = D->ev_wave[w];
       const int l = D->wl[w].level;
       if (l < 0) {

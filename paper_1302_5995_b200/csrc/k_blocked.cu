@@ -14,6 +14,8 @@
 // S = M_bb - M_bi M_ii^{-1} M_ib (dense_nd.cpp:181) in place.
 #include <cfloat>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace dtnb {
@@ -49,84 +51,198 @@ __global__ void __launch_bounds__(256) gather_kernel(KernelArgs args, const int*
   }
 }
 
-// GEPP of the interface rows [k0, ni) x panel columns [k0, k0+kbe), smem-resident.
-__global__ void __launch_bounds__(PANEL_THREADS) panel_kernel(KernelArgs args, const int* __restrict__ list, int k0,
-                                                              int kb, int node_slot) {
-  extern __shared__ double P[];
-  __shared__ double s_best[PANEL_THREADS / 32];
-  __shared__ int s_idx[PANEL_THREADS / 32];
+// Panel factorisation: GEPP of the panel columns [k0, k0+kbe) over ALL rows
+// [k0, total) of the system, pivot search restricted to the interface rows
+// [k0, ni) (boundary rows are eliminated but never chosen as pivots). The
+// panel lives in registers: a cluster of `csize` CTAs x PNT threads, thread
+// owning rows r = rank*PNT + tid + csize*PNT*a. One pivot step = warp argmax
+// -> CTA argmax -> (cluster barrier + DSMEM exchange of the candidate rows)
+// -> swap + rank-1 update in registers. Also writes ipiv (absolute rows).
+namespace cg = cooperative_groups;
+constexpr int PNT = 256, PKB = 32, PNW = PNT / 32;
+
+template <int RPT, bool CL>
+__global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* __restrict__ list, int k0, int kb,
+                                                   int csize) {
+  __shared__ double wrow[2][PNW][PKB];
+  __shared__ double wval[2][PNW];
+  __shared__ int wpos[2][PNW];
+  __shared__ double cval[2];
+  __shared__ int cpos[2], cwarp[2];
+  __shared__ double drow[2][PKB];
+  __shared__ double prow_s[PKB], jrow_s[PKB];
   __shared__ int s_p;
-  const int node_id = list[blockIdx.x + node_slot];
+  const int crank = CL ? int(cg::this_cluster().block_rank()) : 0;
+  const int node_id = list[blockIdx.x / csize];
   const NodeDev nd = args.nodes[node_id];
-  if (k0 >= nd.ni) return;
+  if (k0 >= nd.ni) return;  // uniform over the cluster
   const int kbe = min(kb, nd.ni - k0);
-  const int R = nd.ni - k0;
-  const int ldp = R | 1;
+  const int Ri = nd.ni - k0, Rall = nd.total - k0;
+  const int stride = csize * PNT;
   double* M = args.arena + nd.m_off + k0 + (long long)k0 * nd.ldm;
-  int* ipiv = args.piv + nd.piv_off;
+  const long long ldm = nd.ldm;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int c = 0; c < kbe; ++c)
-    for (int r = tid; r < R; r += PANEL_THREADS) P[c * ldp + r] = M[r + (long long)c * nd.ldm];
-  __syncthreads();
+  int* ipiv = args.piv + nd.piv_off;
+
+  double v[RPT][PKB];
+#pragma unroll
+  for (int a = 0; a < RPT; ++a) {
+    const int r = crank * PNT + tid + stride * a;
+#pragma unroll
+    for (int c = 0; c < PKB; ++c) v[a][c] = (r < Rall && c < kbe) ? M[r + c * ldm] : 0.0;
+  }
   double pmin = k0 == 0 ? DBL_MAX : args.pivstat[2 * node_id];
   double pmax = k0 == 0 ? 0.0 : args.pivstat[2 * node_id + 1];
-  for (int j = 0; j < kbe; ++j) {
+
+#pragma unroll
+  for (int j = 0; j < PKB; ++j) {
+    if (j >= kbe) break;
+    const int buf = j & 1;
+    // ---- thread / warp argmax over own candidate rows (NaN counts as +inf)
     double best = -1.0;
-    int bi = 0x7fffffff;
-    for (int r = j + tid; r < R; r += PANEL_THREADS) {
-      const double av = fabs(P[j * ldp + r]);
-      if (av > best) { best = av; bi = r; }
+    int bpos = 0x7fffffff, ba = 0;
+#pragma unroll
+    for (int a = 0; a < RPT; ++a) {
+      const int r = crank * PNT + tid + stride * a;
+      if (r >= j && r < Ri) {
+        double av = fabs(v[a][j]);
+        if (av != av) av = INFINITY;
+        if (av > best) { best = av; bpos = r; ba = a; }
+      }
     }
+    double wb = best;
+    int wp = bpos;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, off);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      const double ob = __shfl_xor_sync(0xffffffffu, wb, off);
+      const int op = __shfl_xor_sync(0xffffffffu, wp, off);
+      if (ob > wb || (ob == wb && op < wp)) { wb = ob; wp = op; }
     }
-    if (lane == 0) { s_best[warp] = best; s_idx[warp] = bi; }
+    if (wp == bpos && bpos != 0x7fffffff) {  // the owning lane publishes its row
+#pragma unroll
+      for (int a = 0; a < RPT; ++a)
+        if (a == ba) {
+#pragma unroll
+          for (int c = 0; c < PKB; ++c) wrow[buf][warp][c] = v[a][c];
+        }
+    }
+    if (lane == 0) { wval[buf][warp] = wb; wpos[buf][warp] = wp; }
+    {  // the owner of position j publishes row j
+      const int rj = j - crank * PNT;
+      if (rj >= 0 && (rj % stride) == tid && rj / stride < RPT) {
+        const int aj = rj / stride;
+#pragma unroll
+        for (int a = 0; a < RPT; ++a)
+          if (a == aj) {
+#pragma unroll
+            for (int c = 0; c < PKB; ++c) drow[buf][c] = v[a][c];
+          }
+      }
+    }
     __syncthreads();
     if (warp == 0) {
-      best = lane < PANEL_THREADS / 32 ? s_best[lane] : -1.0;
-      bi = lane < PANEL_THREADS / 32 ? s_idx[lane] : 0x7fffffff;
+      double b = lane < PNW ? wval[buf][lane] : -1.0;
+      int bp = lane < PNW ? wpos[buf][lane] : 0x7fffffff;
+      int bw = lane;
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, off);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        const double ob = __shfl_xor_sync(0xffffffffu, b, off);
+        const int op = __shfl_xor_sync(0xffffffffu, bp, off);
+        const int ow = __shfl_xor_sync(0xffffffffu, bw, off);
+        if (ob > b || (ob == b && op < bp)) { b = ob; bp = op; bw = ow; }
       }
-      if (lane == 0) s_p = bi;
+      if (lane == 0) { cval[buf] = b; cpos[buf] = bp; cwarp[buf] = bw; }
+    }
+    if constexpr (CL) {
+      cg::this_cluster().sync();
+    } else {
+      __syncthreads();
+    }
+    if (warp == 0) {
+      double b = -1.0;
+      int bp = 0x7fffffff, br = 0, bw = 0;
+      if (lane < csize) {
+        if constexpr (CL) {
+          cg::cluster_group cl = cg::this_cluster();
+          b = *cl.map_shared_rank(&cval[buf], lane);
+          bp = *cl.map_shared_rank(&cpos[buf], lane);
+          bw = *cl.map_shared_rank(&cwarp[buf], lane);
+        } else {
+          b = cval[buf];
+          bp = cpos[buf];
+          bw = cwarp[buf];
+        }
+        br = lane;
+      }
+#pragma unroll
+      for (int off = 4; off > 0; off >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, b, off);
+        const int op = __shfl_xor_sync(0xffffffffu, bp, off);
+        const int orr = __shfl_xor_sync(0xffffffffu, br, off);
+        const int ow = __shfl_xor_sync(0xffffffffu, bw, off);
+        if (ob > b || (ob == b && op < bp)) { b = ob; bp = op; br = orr; bw = ow; }
+      }
+      if (bp == 0x7fffffff) { bp = j; br = (j / PNT) % csize; bw = -1; }  // empty candidate set
+      const int rank_j = (j / PNT) % csize;
+      if (lane < kbe) {
+        if constexpr (CL) {
+          cg::cluster_group cl = cg::this_cluster();
+          prow_s[lane] = bw >= 0 ? *cl.map_shared_rank(&wrow[buf][bw][lane], br)
+                                 : *cl.map_shared_rank(&drow[buf][lane], rank_j);
+          jrow_s[lane] = *cl.map_shared_rank(&drow[buf][lane], rank_j);
+        } else {
+          prow_s[lane] = bw >= 0 ? wrow[buf][bw][lane] : drow[buf][lane];
+          jrow_s[lane] = drow[buf][lane];
+        }
+      }
+      if (lane == 0) s_p = bp;
     }
     __syncthreads();
     const int p = s_p;
-    if (p != j && tid < kbe) {
-      const double t = P[tid * ldp + j];
-      P[tid * ldp + j] = P[tid * ldp + p];
-      P[tid * ldp + p] = t;
+    const double piv = prow_s[j];
+    const double apiv = fabs(piv);
+    pmin = fmin(pmin, apiv);
+    pmax = (apiv != apiv) ? INFINITY : fmax(pmax, apiv);
+    const double rinv = 1.0 / piv;
+#pragma unroll
+    for (int a = 0; a < RPT; ++a) {
+      const int r = crank * PNT + tid + stride * a;
+      if (r == p && p != j) {
+#pragma unroll
+        for (int c = 0; c < PKB; ++c) v[a][c] = jrow_s[c];
+      }
+      if (r == j) {
+#pragma unroll
+        for (int c = 0; c < PKB; ++c) v[a][c] = prow_s[c];
+      }
+      if (r > j && r < Rall) {
+        const double l = v[a][j] * rinv;
+        v[a][j] = l;
+#pragma unroll
+        for (int c = j + 1; c < PKB; ++c) v[a][c] = fma(-l, prow_s[c], v[a][c]);
+      }
     }
-    if (tid == 0) ipiv[k0 + j] = k0 + p;
-    __syncthreads();
-    const double pv = P[j * ldp + j];
-    pmin = fmin(pmin, fabs(pv));
-    pmax = fmax(pmax, fabs(pv));
-    const double rinv = 1.0 / pv;
-    for (int r = j + 1 + tid; r < R; r += PANEL_THREADS) {
-      const double l = P[j * ldp + r] * rinv;
-      P[j * ldp + r] = l;
-      for (int c = j + 1; c < kbe; ++c) P[c * ldp + r] = fma(-l, P[c * ldp + j], P[c * ldp + r]);
-    }
-    __syncthreads();
+    if (crank == 0 && tid == 0) ipiv[k0 + j] = k0 + p;
   }
-  for (int c = 0; c < kbe; ++c)
-    for (int r = tid; r < R; r += PANEL_THREADS) M[r + (long long)c * nd.ldm] = P[c * ldp + r];
-  if (tid == 0) {
+#pragma unroll
+  for (int a = 0; a < RPT; ++a) {
+    const int r = crank * PNT + tid + stride * a;
+    if (r < Rall) {
+#pragma unroll
+      for (int c = 0; c < PKB; ++c)
+        if (c < kbe) M[r + c * ldm] = v[a][c];
+    }
+  }
+  if (crank == 0 && tid == 0) {
     args.pivstat[2 * node_id] = pmin;
     args.pivstat[2 * node_id + 1] = pmax;
   }
+  if constexpr (CL) cg::this_cluster().sync();  // keep smem alive for remote readers
 }
 
 // Net permutation of the rows touched by the kbe sequential swaps
 // (k0+i <-> ipiv[k0+i]): after the swaps, row dst[t] holds old row src[t].
-__device__ int panel_permutation(const int* ipiv, int k0, int kbe, int* dst, int* src) {
+__device__ int panel_permutation(const int* sp, int k0, int kbe, int* dst, int* src) {
   int nt = 0;
   auto find = [&](int row) {
     for (int t = 0; t < nt; ++t)
@@ -136,7 +252,7 @@ __device__ int panel_permutation(const int* ipiv, int k0, int kbe, int* dst, int
     return nt++;
   };
   for (int i = 0; i < kbe; ++i) {
-    const int a = find(k0 + i), b = find(ipiv[k0 + i]);
+    const int a = find(k0 + i), b = find(sp[i]);
     const int t = src[a];
     src[a] = src[b];
     src[b] = t;
@@ -144,66 +260,52 @@ __device__ int panel_permutation(const int* ipiv, int k0, int kbe, int* dst, int
   return nt;
 }
 
+// Row swaps + U12 = L11^{-1} (P A)[k0:k1, k1:total] for the trailing columns;
+// with swap_left, also the row swaps of the already factored columns [0, k0)
+// (needed only when L itself is reused: the root LU for G = S^{-1}).
 __global__ void __launch_bounds__(RP_THREADS) rowpanel_kernel(KernelArgs args, const int* __restrict__ list, int k0,
-                                                              int kb, int ncoltiles) {
+                                                              int kb, int ncoltiles, int swap_left) {
   __shared__ double T[32][33];
-  __shared__ int s_dst[64], s_src[64], s_nt;
+  __shared__ int s_dst[64], s_src[64], s_piv[32], s_nt;
   const NodeDev nd = args.nodes[list[blockIdx.y]];
   if (k0 >= nd.ni) return;
   const int kbe = min(kb, nd.ni - k0), k1 = k0 + kbe;
   double* M = args.arena + nd.m_off;
   const long long ld = nd.ldm;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (blockIdx.x < ncoltiles) {
-    const int jbase = k1 + blockIdx.x * RP_COLS;
-    if (jbase >= nd.total) return;
+  const bool left = blockIdx.x >= ncoltiles;
+  const int jbase = left ? (blockIdx.x - ncoltiles) * RP_COLS : k1 + blockIdx.x * RP_COLS;
+  const int jend = left ? k0 : nd.total;
+  if (left && !swap_left) return;
+  if (jbase >= jend) return;
+  if (tid < kbe) s_piv[tid] = args.piv[nd.piv_off + k0 + tid];
+  if (!left)
     for (int e = tid; e < kbe * kbe; e += RP_THREADS) T[e % kbe][e / kbe] = M[(k0 + e % kbe) + (k0 + e / kbe) * ld];
-    if (tid == 0) s_nt = panel_permutation(args.piv + nd.piv_off, k0, kbe, s_dst, s_src);
-    __syncthreads();
-    const int nt = s_nt;
-    for (int jj = warp; jj < RP_COLS; jj += RP_THREADS / 32) {
-      const int j = jbase + jj;
-      if (j >= nd.total) break;
-      double* col = M + (long long)j * ld;
-      const double v0 = lane < nt ? col[s_src[lane]] : 0.0;
-      const double v1 = lane + 32 < nt ? col[s_src[lane + 32]] : 0.0;
-      __syncwarp();
-      if (lane < nt) col[s_dst[lane]] = v0;
-      if (lane + 32 < nt) col[s_dst[lane + 32]] = v1;
-      __syncwarp();
-      double x = lane < kbe ? col[k0 + lane] : 0.0;
-      for (int c = 0; c < kbe; ++c) {  // unit lower L11
-        const double xc = __shfl_sync(0xffffffffu, x, c);
-        if (lane > c && lane < kbe) x = fma(-T[lane][c], xc, x);
-      }
-      if (lane < kbe) col[k0 + lane] = x;
+  __syncthreads();
+  if (tid == 0) s_nt = panel_permutation(s_piv, k0, kbe, s_dst, s_src);
+  __syncthreads();
+  const int nt = s_nt;
+  for (int jj = warp; jj < RP_COLS; jj += RP_THREADS / 32) {
+    const int j = jbase + jj;
+    if (j >= jend) break;
+    double* col = M + (long long)j * ld;
+    const double v0 = lane < nt ? col[s_src[lane]] : 0.0;
+    const double v1 = lane + 32 < nt ? col[s_src[lane + 32]] : 0.0;
+    __syncwarp();
+    if (lane < nt) col[s_dst[lane]] = v0;
+    if (lane + 32 < nt) col[s_dst[lane + 32]] = v1;
+    __syncwarp();
+    if (left) continue;
+    double x = lane < kbe ? col[k0 + lane] : 0.0;
+    for (int c = 0; c < kbe; ++c) {  // unit lower L11
+      const double xc = __shfl_sync(0xffffffffu, x, c);
+      if (lane > c && lane < kbe) x = fma(-T[lane][c], xc, x);
     }
-  } else {
-    const int i = nd.ni + (blockIdx.x - ncoltiles) * RP_THREADS + tid;
-    for (int e = tid; e < kbe * kbe; e += RP_THREADS) T[e % kbe][e / kbe] = M[(k0 + e % kbe) + (k0 + e / kbe) * ld];
-    __syncthreads();
-    if (i >= nd.total) return;
-    double x[32];
-#pragma unroll
-    for (int c = 0; c < 32; ++c) x[c] = c < kbe ? M[i + (k0 + c) * ld] : 0.0;
-#pragma unroll
-    for (int c = 0; c < 32; ++c) {  // x <- x U11^{-1}
-      if (c < kbe) {
-        double s = x[c];
-#pragma unroll
-        for (int l = 0; l < c; ++l) s = fma(-x[l], T[l][c], s);
-        x[c] = s / T[c][c];
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < 32; ++c)
-      if (c < kbe) M[i + (k0 + c) * ld] = x[c];
+    if (lane < kbe) col[k0 + lane] = x;
   }
 }
 
-cudaError_t blocked_init() {
-  return cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-}
+cudaError_t blocked_init() { return cudaSuccess; }
 
 cudaError_t launch_gather(const KernelArgs& args, const int* d_list, int count, int max_total, cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
@@ -212,24 +314,54 @@ cudaError_t launch_gather(const KernelArgs& args, const int* d_list, int count, 
   return cudaGetLastError();
 }
 
-// kb chosen by the caller so that kb * max_rows * 8 bytes fits in 220 KB.
-cudaError_t launch_panel(const KernelArgs& args, const int* d_list, int count, int max_ni, int k0, int kb,
-                         cudaStream_t st) {
-  if (count <= 0 || k0 >= max_ni) return cudaSuccess;
-  const int rows = (max_ni - k0) | 1;
-  const size_t smem = size_t(kb) * rows * sizeof(double);
-  panel_kernel<<<count, PANEL_THREADS, smem, st>>>(args, d_list, k0, kb, 0);
-  return cudaGetLastError();
+// Panel geometry for systems with up to max_rows rows below k0 (kb <= 32).
+void panel_shape(int max_rows, int* rpt, int* csize) {
+  if (max_rows <= PNT) { *rpt = 1; *csize = 1; return; }
+  *rpt = 2;
+  *csize = (max_rows + 2 * PNT - 1) / (2 * PNT);
 }
 
-cudaError_t launch_rowpanel(const KernelArgs& args, const int* d_list, int count, int max_total, int min_nb,
-                            int max_nb, int k0, int kb, cudaStream_t st) {
+template <int RPT, bool CL>
+cudaError_t launch_panel_t(const KernelArgs& args, const int* d_list, int count, int k0, int kb, int csize,
+                           cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(count * csize);
+  cfg.blockDim = dim3(PNT);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  if (CL) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = csize;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&cfg, panel_kernel<RPT, CL>, args, d_list, k0, kb, csize);
+}
+
+cudaError_t launch_panel(const KernelArgs& args, const int* d_list, int count, int max_rows, int k0, int kb,
+                         cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  if (kb > PKB) return cudaErrorInvalidValue;
+  int rpt, csize;
+  panel_shape(max_rows, &rpt, &csize);
+  if (csize > 8) return cudaErrorInvalidValue;
+  if (csize == 1) {
+    if (rpt == 1) return launch_panel_t<1, false>(args, d_list, count, k0, kb, 1, st);
+    return launch_panel_t<2, false>(args, d_list, count, k0, kb, 1, st);
+  }
+  return launch_panel_t<2, true>(args, d_list, count, k0, kb, csize, st);
+}
+
+cudaError_t launch_rowpanel(const KernelArgs& args, const int* d_list, int count, int max_total, int k0, int kb,
+                            bool swap_left, cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
   const int coltiles = (max_total - k0 + RP_COLS - 1) / RP_COLS;
-  const int rowtiles = (max_nb + RP_THREADS - 1) / RP_THREADS;
-  (void)min_nb;
-  dim3 grid(coltiles + rowtiles, count);
-  rowpanel_kernel<<<grid, RP_THREADS, 0, st>>>(args, d_list, k0, kb, coltiles);
+  const int lefttiles = swap_left ? (k0 + RP_COLS - 1) / RP_COLS : 0;
+  if (coltiles + lefttiles <= 0) return cudaSuccess;
+  dim3 grid(coltiles + lefttiles, count);
+  rowpanel_kernel<<<grid, RP_THREADS, 0, st>>>(args, d_list, k0, kb, coltiles, swap_left ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -107,7 +107,8 @@ __global__ void __launch_bounds__(TR * TC) small_elim_kernel(KernelArgs args, co
           if (b == bk) v = m[a][b];
         if (i < total) ck[i] = v;
         if (i < ni && !((elim >> a) & 1u)) {
-          const double av = fabs(v);
+          double av = fabs(v);
+          if (av != av) av = INFINITY;  // a NaN column still yields a (flagged) pivot
           if (av > best) { best = av; bi = i; }
         }
       }
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(TR * TC) small_elim_kernel(KernelArgs args, co
     }
     const double apv = fabs(pv);
     pmin = fmin(pmin, apv);
-    pmax = fmax(pmax, apv);
+    pmax = (apv != apv) ? INFINITY : fmax(pmax, apv);
     __syncthreads();
     const double rinv = 1.0 / pv;
 #pragma unroll
