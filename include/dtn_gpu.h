@@ -112,6 +112,10 @@ int dtn_gpu_build_stats(const dtn_op* op, dtn_build_stats* out);
 /* per-kernel-class timing of a build made with opts.profile = 1 (count 0 otherwise) */
 int dtn_gpu_kernel_stats(const dtn_op* op, dtn_kernel_stats* out, int32_t max, int32_t* count);
 
+/* Test hook: partial LU (pivots among the first ni rows) of a host n x n
+ * column-major matrix with the engine's blocked kernels; ni == n is a full LU. */
+int dtn_debug_partial_lu(int32_t n, int32_t ni, const double* A, double* out, int32_t* ipiv, double* pivstat);
+
 /* discretize (grid.cpp:106-168) on the host: continuum mode from coefficient
  * samples b, c, d at the unknowns (physical coordinates (x h, y h), h = 1/(n-1),
  * unknown_id order; NULL = 0), network mode from the seeded link conductivities. */

@@ -43,7 +43,7 @@ EXPORTS = [
     "dtn_gpu_create", "dtn_gpu_destroy", "dtn_gpu_last_error", "dtn_gpu_set_stream", "dtn_gpu_build",
     "dtn_gpu_free", "dtn_gpu_boundary", "dtn_gpu_export", "dtn_gpu_device_ptrs", "dtn_gpu_apply",
     "dtn_gpu_num_boxes", "dtn_gpu_box_info", "dtn_gpu_box_schur", "dtn_gpu_level_stats", "dtn_gpu_build_stats", "dtn_gpu_kernel_stats",
-    "dtn_discretize_continuum", "dtn_discretize_network",
+    "dtn_discretize_continuum", "dtn_discretize_network", "dtn_debug_partial_lu",
 ]
 
 _lib = None
@@ -85,5 +85,6 @@ def lib():
     L.dtn_gpu_kernel_stats.argtypes = [vp, P(dtn_kernel_stats), i32, P(i32)]
     L.dtn_discretize_continuum.argtypes = [i32, vp, vp, vp, vp]
     L.dtn_discretize_network.argtypes = [i32, f64, f64, C.c_uint64, vp]
+    L.dtn_debug_partial_lu.argtypes = [i32, i32, vp, vp, vp, vp]
     _lib = L
     return L

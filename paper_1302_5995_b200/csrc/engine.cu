@@ -59,7 +59,7 @@ struct Singular : std::runtime_error {
 int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
 constexpr int kSmallMax = 160;
-constexpr int kDefaultMicro = 128;
+constexpr int kDefaultMicro = 64;
 
 // Panel width; the register-resident panel spans up to 8 CTAs x 512 rows.
 int panel_kb(int rows) {
@@ -585,7 +585,13 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
       for (const auto* lst : {&wv.micro, &wv.small, &wv.blocked})
         for (int id : *lst) {
           const Node& nd = P.nodes[id];
-          if (nd.ni > 0 && !pivots_ok(D->h_pivstat[2 * id], D->h_pivstat[2 * id + 1])) throw Singular(label_of(P, nd));
+          if (nd.ni > 0 && !pivots_ok(D->h_pivstat[2 * id], D->h_pivstat[2 * id + 1])) {
+            if (std::getenv("DTN_DEBUG"))
+              std::fprintf(stderr, "dtn: node %d kind %d ni %d nb %d total %d blocked %d pmin %g pmax %g\n", id,
+                           int(nd.kind), nd.ni, nd.nb, nd.total, int(nd.blocked), D->h_pivstat[2 * id],
+                           D->h_pivstat[2 * id + 1]);
+            throw Singular(label_of(P, nd));
+          }
         }
     auto* op = new dtn_op;
     op->ctx = ctx;
@@ -801,6 +807,44 @@ int dtn_gpu_build_stats(const dtn_op* op, dtn_build_stats* out) {
   if (!op || !out) return DTN_EINVAL;
   *out = op->stats;
   return DTN_OK;
+}
+
+// Test hook: blocked partial LU of one dense n x n matrix with the engine's
+// panel / rowpanel / trailing kernels (pivots among the first ni rows;
+// ni == n is a full LU with left swaps, as for the root inverse).
+int dtn_debug_partial_lu(int32_t n, int32_t ni, const double* A, double* out, int32_t* ipiv, double* pivstat) {
+  return guarded(nullptr, [&] {
+    if (n <= 0 || ni <= 0 || ni > n) throw std::invalid_argument("dtn_debug_partial_lu: bad sizes");
+    CK(gemm_init());
+    const int ld = int(align_up(n, 8));
+    NodeDev nd{};
+    nd.kind = 2;
+    nd.nb = n - ni;
+    nd.ni = ni;
+    nd.total = n;
+    nd.a = nd.b = -1;
+    nd.ld = nd.ldm = ld;
+    NodeDev* d_node = dalloc<NodeDev>(1);
+    int* d_list = dalloc<int>(1);
+    double* d_a = dalloc<double>(size_t(ld) * n);
+    int* d_piv = dalloc<int>(n);
+    double* d_ps = dalloc<double>(2);
+    int zero = 0;
+    CK(cudaMemcpy(d_node, &nd, sizeof(nd), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_list, &zero, sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy2D(d_a, size_t(ld) * 8, A, size_t(n) * 8, size_t(n) * 8, n, cudaMemcpyHostToDevice));
+    KernelArgs a{d_node, nullptr, nullptr, 0, 0, d_a, d_piv, d_ps};
+    for (int k0 = 0; k0 < ni; k0 += 32) {
+      CK(launch_panel(a, d_list, 1, n - k0, k0, 32, 0));
+      CK(launch_rowpanel(a, d_list, 1, n, k0, 32, ni == n, 0));
+      CK(launch_trailing_update(a, d_list, 1, n, k0, 32, 0));
+    }
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy2D(out, size_t(n) * 8, d_a, size_t(ld) * 8, size_t(n) * 8, n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ipiv, d_piv, size_t(ni) * sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(pivstat, d_ps, 2 * sizeof(double), cudaMemcpyDeviceToHost));
+    for (void* p : std::initializer_list<void*>{d_node, d_list, d_a, d_piv, d_ps}) cudaFree(p);
+  });
 }
 
 // discretize, continuum branch (grid.cpp:130-144): paper's 1/h convection scaling

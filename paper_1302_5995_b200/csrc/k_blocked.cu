@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
         br = lane;
       }
 #pragma unroll
-      for (int off = 4; off > 0; off >>= 1) {
+      for (int off = 16; off > 0; off >>= 1) {  // all 32 lanes end with the winner
         const double ob = __shfl_xor_sync(0xffffffffu, b, off);
         const int op = __shfl_xor_sync(0xffffffffu, bp, off);
         const int orr = __shfl_xor_sync(0xffffffffu, br, off);
