@@ -61,9 +61,9 @@ int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 constexpr int kSmallMax = 160;
 constexpr int kDefaultMicro = 64;
 
-// Panel width; the register-resident panel spans up to 8 CTAs x 512 rows.
+// Panel width; the register-resident panel spans up to 16 CTAs x 256 rows.
 int panel_kb(int rows) {
-  if (rows > 8 * 512) throw std::invalid_argument("dense merge system too large for the cluster panel (> 4096 rows)");
+  if (rows > 16 * 256) throw std::invalid_argument("dense merge system too large for the cluster panel (> 4096 rows)");
   return 32;
 }
 
@@ -231,7 +231,7 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
   D->d_lists = dalloc<int>(lists.size());
   CK(cudaMemcpy(D->d_lists, lists.data(), lists.size() * sizeof(int), cudaMemcpyHostToDevice));
   D->d_arena = dalloc<double>(size_t(D->lu_off + int64_t(D->ldlu) * nb));
-  D->d_piv = dalloc<int>(size_t(P.piv_ints + nb));
+  D->d_piv = dalloc<int>(size_t(P.piv_ints + align_up(nb, 4) + 128));
   D->d_pivstat = dalloc<double>(2 * D->h_nodes.size());
   D->d_stencil = dalloc<double>(size_t(5 * D->nu));
   D->lds = int(align_up(nb, 8));
@@ -816,6 +816,7 @@ int dtn_debug_partial_lu(int32_t n, int32_t ni, const double* A, double* out, in
   return guarded(nullptr, [&] {
     if (n <= 0 || ni <= 0 || ni > n) throw std::invalid_argument("dtn_debug_partial_lu: bad sizes");
     CK(gemm_init());
+    CK(blocked_init());
     const int ld = int(align_up(n, 8));
     NodeDev nd{};
     nd.kind = 2;
@@ -827,7 +828,7 @@ int dtn_debug_partial_lu(int32_t n, int32_t ni, const double* A, double* out, in
     NodeDev* d_node = dalloc<NodeDev>(1);
     int* d_list = dalloc<int>(1);
     double* d_a = dalloc<double>(size_t(ld) * n);
-    int* d_piv = dalloc<int>(n);
+    int* d_piv = dalloc<int>(size_t(align_up(n, 4) + 128));
     double* d_ps = dalloc<double>(2);
     int zero = 0;
     CK(cudaMemcpy(d_node, &nd, sizeof(nd), cudaMemcpyHostToDevice));

@@ -55,209 +55,235 @@ __global__ void __launch_bounds__(256) gather_kernel(KernelArgs args, const int*
 // [k0, total) of the system, pivot search restricted to the interface rows
 // [k0, ni) (boundary rows are eliminated but never chosen as pivots). The
 // panel lives in registers: a cluster of `csize` CTAs x PNT threads, thread
-// owning rows r = rank*PNT + tid + csize*PNT*a. One pivot step = warp argmax
-// -> CTA argmax -> (cluster barrier + DSMEM exchange of the candidate rows)
-// -> swap + rank-1 update in registers. Also writes ipiv (absolute rows).
+// owning rows r = rank*PNT + tid + csize*PNT*a. One pivot step costs one CTA
+// barrier and one cluster barrier: each CTA pushes its best candidate row
+// (and the owner of row j pushes row j) into every CTA's shared memory with
+// remote DSMEM stores before the barrier, so after it the pivot decision and
+// the rank-1 update are purely local. Outputs: the factored panel, ipiv
+// (absolute rows) and the net row-move list consumed by rowpanel_kernel.
 namespace cg = cooperative_groups;
-constexpr int PNT = 256, PKB = 32, PNW = PNT / 32;
+constexpr int PNT = 256, PKB = 32, PNW = PNT / 32, PMAXC = 16;
 
-template <int RPT, bool CL>
+__device__ __forceinline__ int* move_list(const KernelArgs& args, const NodeDev& nd) {
+  return args.piv + nd.piv_off + ((nd.ni + 3) & ~3);
+}
+
+#ifdef DTN_PANEL_PROFILE
+__device__ long long g_panel_clk[4 * 32];
+#endif
+
+struct PanelCand {
+  double val;
+  int pos, lab;
+  double row[PKB];
+};
+
+// Registers hold one row per thread, rotated left by one after every pivot
+// step so the active column is always v[0] (no dynamic register indexing).
+template <bool CL>
 __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* __restrict__ list, int k0, int kb,
                                                    int csize) {
   __shared__ double wrow[2][PNW][PKB];
   __shared__ double wval[2][PNW];
-  __shared__ int wpos[2][PNW];
-  __shared__ double cval[2];
-  __shared__ int cpos[2], cwarp[2];
-  __shared__ double drow[2][PKB];
-  __shared__ double prow_s[PKB], jrow_s[PKB];
-  __shared__ int s_p;
+  __shared__ int wpos[2][PNW], wlab[2][PNW];
+  __shared__ double jrow[2][PKB];
+  __shared__ int jlab[2];
+  __shared__ PanelCand cand[2][CL ? PMAXC : 1];
+  __shared__ int sp[PKB];
   const int crank = CL ? int(cg::this_cluster().block_rank()) : 0;
   const int node_id = list[blockIdx.x / csize];
   const NodeDev nd = args.nodes[node_id];
   if (k0 >= nd.ni) return;  // uniform over the cluster
   const int kbe = min(kb, nd.ni - k0);
   const int Ri = nd.ni - k0, Rall = nd.total - k0;
-  const int stride = csize * PNT;
   double* M = args.arena + nd.m_off + k0 + (long long)k0 * nd.ldm;
   const long long ldm = nd.ldm;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int* ipiv = args.piv + nd.piv_off;
+  const int r = crank * PNT + tid;  // this thread's row (position) in the panel
 
-  double v[RPT][PKB];
+  double v[PKB];
 #pragma unroll
-  for (int a = 0; a < RPT; ++a) {
-    const int r = crank * PNT + tid + stride * a;
-#pragma unroll
-    for (int c = 0; c < PKB; ++c) v[a][c] = (r < Rall && c < kbe) ? M[r + c * ldm] : 0.0;
-  }
+  for (int c = 0; c < PKB; ++c) v[c] = (r < Rall && c < kbe) ? M[r + c * ldm] : 0.0;
+  int lab = r, first = -1;
   double pmin = k0 == 0 ? DBL_MAX : args.pivstat[2 * node_id];
   double pmax = k0 == 0 ? 0.0 : args.pivstat[2 * node_id + 1];
 
-#pragma unroll
-  for (int j = 0; j < PKB; ++j) {
-    if (j >= kbe) break;
+#pragma unroll 1
+  for (int j = 0; j < kbe; ++j) {
+#ifdef DTN_PANEL_PROFILE
+    if (blockIdx.x == 0 && tid == 0) g_panel_clk[j * 4 + 0] = clock64();
+#endif
     const int buf = j & 1;
-    // ---- thread / warp argmax over own candidate rows (NaN counts as +inf)
-    double best = -1.0;
-    int bpos = 0x7fffffff, ba = 0;
-#pragma unroll
-    for (int a = 0; a < RPT; ++a) {
-      const int r = crank * PNT + tid + stride * a;
-      if (r >= j && r < Ri) {
-        double av = fabs(v[a][j]);
-        if (av != av) av = INFINITY;
-        if (av > best) { best = av; bpos = r; ba = a; }
-      }
+    // ---- warp argmax of |column j| over candidate rows (NaN counts as +inf)
+    double val = -1.0;
+    if (r >= j && r < Ri) {
+      val = fabs(v[0]);
+      if (val != val) val = INFINITY;
     }
-    double wb = best;
-    int wp = bpos;
+    double wb = val;
+    int wp = val >= 0.0 ? r : 0x7fffffff;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
       const double ob = __shfl_xor_sync(0xffffffffu, wb, off);
       const int op = __shfl_xor_sync(0xffffffffu, wp, off);
       if (ob > wb || (ob == wb && op < wp)) { wb = ob; wp = op; }
     }
-    if (wp == bpos && bpos != 0x7fffffff) {  // the owning lane publishes its row
+    if (wp == r) {
 #pragma unroll
-      for (int a = 0; a < RPT; ++a)
-        if (a == ba) {
-#pragma unroll
-          for (int c = 0; c < PKB; ++c) wrow[buf][warp][c] = v[a][c];
-        }
+      for (int c = 0; c < PKB; ++c) wrow[buf][warp][c] = v[c];
+      wlab[buf][warp] = lab;
     }
     if (lane == 0) { wval[buf][warp] = wb; wpos[buf][warp] = wp; }
-    {  // the owner of position j publishes row j
-      const int rj = j - crank * PNT;
-      if (rj >= 0 && (rj % stride) == tid && rj / stride < RPT) {
-        const int aj = rj / stride;
+    if (r == j) {  // row j always sits in rank 0, warp 0
 #pragma unroll
-        for (int a = 0; a < RPT; ++a)
-          if (a == aj) {
-#pragma unroll
-            for (int c = 0; c < PKB; ++c) drow[buf][c] = v[a][c];
-          }
-      }
+      for (int c = 0; c < PKB; ++c) jrow[buf][c] = v[c];
+      jlab[buf] = lab;
     }
     __syncthreads();
-    if (warp == 0) {
-      double b = lane < PNW ? wval[buf][lane] : -1.0;
-      int bp = lane < PNW ? wpos[buf][lane] : 0x7fffffff;
-      int bw = lane;
+#ifdef DTN_PANEL_PROFILE
+    if (blockIdx.x == 0 && tid == 0) g_panel_clk[j * 4 + 1] = clock64();
+#endif
+    // ---- CTA argmax (every warp, redundantly)
+    double b = lane < PNW ? wval[buf][lane] : -1.0;
+    int bp = lane < PNW ? wpos[buf][lane] : 0x7fffffff;
+    int bw = lane;
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, b, off);
-        const int op = __shfl_xor_sync(0xffffffffu, bp, off);
-        const int ow = __shfl_xor_sync(0xffffffffu, bw, off);
-        if (ob > b || (ob == b && op < bp)) { b = ob; bp = op; bw = ow; }
-      }
-      if (lane == 0) { cval[buf] = b; cpos[buf] = bp; cwarp[buf] = bw; }
+    for (int off = PNW / 2; off > 0; off >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, b, off);
+      const int op = __shfl_xor_sync(0xffffffffu, bp, off);
+      const int ow = __shfl_xor_sync(0xffffffffu, bw, off);
+      if (ob > b || (ob == b && op < bp)) { b = ob; bp = op; bw = ow; }
     }
+    b = __shfl_sync(0xffffffffu, b, 0);
+    bp = __shfl_sync(0xffffffffu, bp, 0);
+    bw = __shfl_sync(0xffffffffu, bw, 0) & (PNW - 1);
+    const double* prow;
+    const double* jr;
+    int p, plab, jl;
     if constexpr (CL) {
+      // warp 0 pushes this CTA's candidate (and rank 0 row j) to every CTA
+      if (warp == 0) {
+        cg::cluster_group cl = cg::this_cluster();
+        const double rv = wrow[buf][bw][lane];
+        const int rl = wlab[buf][bw];
+        const double jv = jrow[buf][lane];
+        const int jlv = jlab[buf];
+        for (int d = 0; d < csize; ++d) {
+          PanelCand* dc = cl.map_shared_rank(&cand[buf][crank], d);
+          dc->row[lane] = rv;
+          if (lane == 0) {
+            dc->val = b;
+            dc->pos = bp;
+            dc->lab = rl;
+          }
+          if (crank == 0 && d != 0) {
+            cl.map_shared_rank(&jrow[buf][0], d)[lane] = jv;
+            if (lane == 0) *cl.map_shared_rank(&jlab[buf], d) = jlv;
+          }
+        }
+      }
       cg::this_cluster().sync();
-    } else {
-      __syncthreads();
-    }
-    if (warp == 0) {
-      double b = -1.0;
-      int bp = 0x7fffffff, br = 0, bw = 0;
-      if (lane < csize) {
-        if constexpr (CL) {
-          cg::cluster_group cl = cg::this_cluster();
-          b = *cl.map_shared_rank(&cval[buf], lane);
-          bp = *cl.map_shared_rank(&cpos[buf], lane);
-          bw = *cl.map_shared_rank(&cwarp[buf], lane);
-        } else {
-          b = cval[buf];
-          bp = cpos[buf];
-          bw = cwarp[buf];
-        }
-        br = lane;
-      }
+      double cb = lane < csize ? cand[buf][lane].val : -1.0;
+      int cp = lane < csize ? cand[buf][lane].pos : 0x7fffffff;
+      int cw = lane;
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {  // all 32 lanes end with the winner
-        const double ob = __shfl_xor_sync(0xffffffffu, b, off);
-        const int op = __shfl_xor_sync(0xffffffffu, bp, off);
-        const int orr = __shfl_xor_sync(0xffffffffu, br, off);
-        const int ow = __shfl_xor_sync(0xffffffffu, bw, off);
-        if (ob > b || (ob == b && op < bp)) { b = ob; bp = op; br = orr; bw = ow; }
+      for (int off = 8; off > 0; off >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, cb, off);
+        const int op = __shfl_xor_sync(0xffffffffu, cp, off);
+        const int ow = __shfl_xor_sync(0xffffffffu, cw, off);
+        if (ob > cb || (ob == cb && op < cp)) { cb = ob; cp = op; cw = ow; }
       }
-      if (bp == 0x7fffffff) { bp = j; br = (j / PNT) % csize; bw = -1; }  // empty candidate set
-      const int rank_j = (j / PNT) % csize;
-      if (lane < kbe) {
-        if constexpr (CL) {
-          cg::cluster_group cl = cg::this_cluster();
-          prow_s[lane] = bw >= 0 ? *cl.map_shared_rank(&wrow[buf][bw][lane], br)
-                                 : *cl.map_shared_rank(&drow[buf][lane], rank_j);
-          jrow_s[lane] = *cl.map_shared_rank(&drow[buf][lane], rank_j);
-        } else {
-          prow_s[lane] = bw >= 0 ? wrow[buf][bw][lane] : drow[buf][lane];
-          jrow_s[lane] = drow[buf][lane];
-        }
-      }
-      if (lane == 0) s_p = bp;
+      p = __shfl_sync(0xffffffffu, cp, 0);
+      cw = __shfl_sync(0xffffffffu, cw, 0) & (PMAXC - 1);
+      prow = cand[buf][cw].row;
+      plab = cand[buf][cw].lab;
+    } else {
+      p = bp;
+      prow = wrow[buf][bw];
+      plab = wlab[buf][bw];
     }
-    __syncthreads();
-    const int p = s_p;
-    const double piv = prow_s[j];
+    jr = jrow[buf];
+    jl = jlab[buf];
+#ifdef DTN_PANEL_PROFILE
+    if (blockIdx.x == 0 && tid == 0) g_panel_clk[j * 4 + 2] = clock64();
+#endif
+    const double piv = prow[0];
     const double apiv = fabs(piv);
     pmin = fmin(pmin, apiv);
     pmax = (apiv != apiv) ? INFINITY : fmax(pmax, apiv);
     const double rinv = 1.0 / piv;
+    if (r == p && p != j) {  // old row j moves down to position p
 #pragma unroll
-    for (int a = 0; a < RPT; ++a) {
-      const int r = crank * PNT + tid + stride * a;
-      if (r == p && p != j) {
-#pragma unroll
-        for (int c = 0; c < PKB; ++c) v[a][c] = jrow_s[c];
-      }
-      if (r == j) {
-#pragma unroll
-        for (int c = 0; c < PKB; ++c) v[a][c] = prow_s[c];
-      }
-      if (r > j && r < Rall) {
-        const double l = v[a][j] * rinv;
-        v[a][j] = l;
-#pragma unroll
-        for (int c = j + 1; c < PKB; ++c) v[a][c] = fma(-l, prow_s[c], v[a][c]);
-      }
+      for (int c = 0; c < PKB; ++c) v[c] = jr[c];
+      lab = jl;
+      if (first < 0) first = j;
     }
-    if (crank == 0 && tid == 0) ipiv[k0 + j] = k0 + p;
+    if (r == j) {  // pivot row moves up to position j
+#pragma unroll
+      for (int c = 0; c < PKB; ++c) v[c] = prow[c];
+      lab = plab;
+    }
+    if (r > j && r < Rall) {
+      const double l = v[0] * rinv;
+      v[0] = l;
+      const int lim = PKB - j;  // rotated indices >= lim hold the factored L columns
+#pragma unroll
+      for (int c = 1; c < PKB; ++c)
+        if (c < lim) v[c] = fma(-l, prow[c], v[c]);
+    }
+    {  // rotate left by one: the next column becomes v[0]
+      const double t0 = v[0];
+#pragma unroll
+      for (int c = 0; c < PKB - 1; ++c) v[c] = v[c + 1];
+      v[PKB - 1] = t0;
+    }
+    if (tid == 0) sp[j] = p;
+#ifdef DTN_PANEL_PROFILE
+    if (blockIdx.x == 0 && tid == 0) g_panel_clk[j * 4 + 3] = clock64();
+#endif
   }
+#pragma unroll 1
+  for (int t = kbe; t < PKB; ++t) {  // complete the rotation to the identity
+    const double t0 = v[0];
 #pragma unroll
-  for (int a = 0; a < RPT; ++a) {
-    const int r = crank * PNT + tid + stride * a;
-    if (r < Rall) {
+    for (int c = 0; c < PKB - 1; ++c) v[c] = v[c + 1];
+    v[PKB - 1] = t0;
+  }
+  // ---- write back; emit ipiv and the net row-move list
+  int* mv = move_list(args, nd);
+  if (r < Rall) {
 #pragma unroll
-      for (int c = 0; c < PKB; ++c)
-        if (c < kbe) M[r + c * ldm] = v[a][c];
+    for (int c = 0; c < PKB; ++c)
+      if (c < kbe) M[r + c * ldm] = v[c];
+    int slot = -1;
+    if (r < kbe) slot = r;
+    else if (first >= 0) slot = kbe + first;
+    if (slot >= 0) {
+      mv[slot] = k0 + r;
+      mv[2 * PKB + slot] = k0 + lab;
     }
   }
-  if (crank == 0 && tid == 0) {
-    args.pivstat[2 * node_id] = pmin;
-    args.pivstat[2 * node_id + 1] = pmax;
+  __syncthreads();
+  if (crank == 0) {
+    if (tid < kbe) {
+      args.piv[nd.piv_off + k0 + tid] = k0 + sp[tid];
+      bool used = sp[tid] >= kbe;  // slot kbe+tid: first displacement of a position >= kbe
+      for (int m = 0; m < tid; ++m)
+        if (sp[m] == sp[tid]) used = false;
+      if (!used) {
+        mv[kbe + tid] = -1;
+        mv[2 * PKB + kbe + tid] = -1;
+      }
+    } else if (tid >= 2 * kbe && tid < 2 * PKB) {
+      mv[tid] = -1;
+      mv[2 * PKB + tid] = -1;
+    }
+    if (tid == 0) {
+      args.pivstat[2 * node_id] = pmin;
+      args.pivstat[2 * node_id + 1] = pmax;
+    }
   }
-  if constexpr (CL) cg::this_cluster().sync();  // keep smem alive for remote readers
-}
-
-// Net permutation of the rows touched by the kbe sequential swaps
-// (k0+i <-> ipiv[k0+i]): after the swaps, row dst[t] holds old row src[t].
-__device__ int panel_permutation(const int* sp, int k0, int kbe, int* dst, int* src) {
-  int nt = 0;
-  auto find = [&](int row) {
-    for (int t = 0; t < nt; ++t)
-      if (dst[t] == row) return t;
-    dst[nt] = row;
-    src[nt] = row;
-    return nt++;
-  };
-  for (int i = 0; i < kbe; ++i) {
-    const int a = find(k0 + i), b = find(sp[i]);
-    const int t = src[a];
-    src[a] = src[b];
-    src[b] = t;
-  }
-  return nt;
+  if constexpr (CL) cg::this_cluster().sync();  // no CTA exits while others may still write its smem
 }
 
 // Row swaps + U12 = L11^{-1} (P A)[k0:k1, k1:total] for the trailing columns;
@@ -266,7 +292,7 @@ __device__ int panel_permutation(const int* sp, int k0, int kbe, int* dst, int* 
 __global__ void __launch_bounds__(RP_THREADS) rowpanel_kernel(KernelArgs args, const int* __restrict__ list, int k0,
                                                               int kb, int ncoltiles, int swap_left) {
   __shared__ double T[32][33];
-  __shared__ int s_dst[64], s_src[64], s_piv[32], s_nt;
+  __shared__ int s_dst[64], s_src[64];
   const NodeDev nd = args.nodes[list[blockIdx.y]];
   if (k0 >= nd.ni) return;
   const int kbe = min(kb, nd.ni - k0), k1 = k0 + kbe;
@@ -278,22 +304,24 @@ __global__ void __launch_bounds__(RP_THREADS) rowpanel_kernel(KernelArgs args, c
   const int jend = left ? k0 : nd.total;
   if (left && !swap_left) return;
   if (jbase >= jend) return;
-  if (tid < kbe) s_piv[tid] = args.piv[nd.piv_off + k0 + tid];
+  const int* mv = move_list(args, nd);
+  if (tid < 64) {
+    s_dst[tid] = mv[tid];
+    s_src[tid] = mv[64 + tid];
+  }
   if (!left)
     for (int e = tid; e < kbe * kbe; e += RP_THREADS) T[e % kbe][e / kbe] = M[(k0 + e % kbe) + (k0 + e / kbe) * ld];
   __syncthreads();
-  if (tid == 0) s_nt = panel_permutation(s_piv, k0, kbe, s_dst, s_src);
-  __syncthreads();
-  const int nt = s_nt;
   for (int jj = warp; jj < RP_COLS; jj += RP_THREADS / 32) {
     const int j = jbase + jj;
     if (j >= jend) break;
     double* col = M + (long long)j * ld;
-    const double v0 = lane < nt ? col[s_src[lane]] : 0.0;
-    const double v1 = lane + 32 < nt ? col[s_src[lane + 32]] : 0.0;
+    const int d0 = s_dst[lane], d1 = s_dst[lane + 32];
+    const double v0 = d0 >= 0 ? col[s_src[lane]] : 0.0;
+    const double v1 = d1 >= 0 ? col[s_src[lane + 32]] : 0.0;
     __syncwarp();
-    if (lane < nt) col[s_dst[lane]] = v0;
-    if (lane + 32 < nt) col[s_dst[lane + 32]] = v1;
+    if (d0 >= 0) col[d0] = v0;
+    if (d1 >= 0) col[d1] = v1;
     __syncwarp();
     if (left) continue;
     double x = lane < kbe ? col[k0 + lane] : 0.0;
@@ -305,7 +333,9 @@ __global__ void __launch_bounds__(RP_THREADS) rowpanel_kernel(KernelArgs args, c
   }
 }
 
-cudaError_t blocked_init() { return cudaSuccess; }
+cudaError_t blocked_init() {
+  return cudaFuncSetAttribute(panel_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+}
 
 cudaError_t launch_gather(const KernelArgs& args, const int* d_list, int count, int max_total, cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
@@ -314,14 +344,14 @@ cudaError_t launch_gather(const KernelArgs& args, const int* d_list, int count, 
   return cudaGetLastError();
 }
 
-// Panel geometry for systems with up to max_rows rows below k0 (kb <= 32).
+// Panel geometry for systems with up to max_rows rows below k0 (kb <= 32):
+// one row per thread (two would spill), clusters of up to 16 CTAs.
 void panel_shape(int max_rows, int* rpt, int* csize) {
-  if (max_rows <= PNT) { *rpt = 1; *csize = 1; return; }
-  *rpt = 2;
-  *csize = (max_rows + 2 * PNT - 1) / (2 * PNT);
+  *rpt = 1;
+  *csize = (max_rows + PNT - 1) / PNT;
 }
 
-template <int RPT, bool CL>
+template <bool CL>
 cudaError_t launch_panel_t(const KernelArgs& args, const int* d_list, int count, int k0, int kb, int csize,
                            cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
@@ -337,7 +367,7 @@ cudaError_t launch_panel_t(const KernelArgs& args, const int* d_list, int count,
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  return cudaLaunchKernelEx(&cfg, panel_kernel<RPT, CL>, args, d_list, k0, kb, csize);
+  return cudaLaunchKernelEx(&cfg, panel_kernel<CL>, args, d_list, k0, kb, csize);
 }
 
 cudaError_t launch_panel(const KernelArgs& args, const int* d_list, int count, int max_rows, int k0, int kb,
@@ -346,12 +376,9 @@ cudaError_t launch_panel(const KernelArgs& args, const int* d_list, int count, i
   if (kb > PKB) return cudaErrorInvalidValue;
   int rpt, csize;
   panel_shape(max_rows, &rpt, &csize);
-  if (csize > 8) return cudaErrorInvalidValue;
-  if (csize == 1) {
-    if (rpt == 1) return launch_panel_t<1, false>(args, d_list, count, k0, kb, 1, st);
-    return launch_panel_t<2, false>(args, d_list, count, k0, kb, 1, st);
-  }
-  return launch_panel_t<2, true>(args, d_list, count, k0, kb, csize, st);
+  if (csize > PMAXC || rpt != 1) return cudaErrorInvalidValue;
+  if (csize == 1) return launch_panel_t<false>(args, d_list, count, k0, kb, 1, st);
+  return launch_panel_t<true>(args, d_list, count, k0, kb, csize, st);
 }
 
 cudaError_t launch_rowpanel(const KernelArgs& args, const int* d_list, int count, int max_total, int k0, int kb,

@@ -271,7 +271,7 @@ Plan make_plan(const PlanKey& key) {
       nd.s_off = nd.m_off + nd.ni + int64_t(nd.ni) * nd.ldm;
       nd.ld = nd.ldm;
       nd.piv_off = poff;
-      poff += align_up(std::max(nd.ni, 1), 4);
+      poff += align_up(std::max(nd.ni, 1), 4) + 128;  // ipiv + per-panel row-move list
     } else {
       nd.ld = std::max(nd.nb, 1);
       nd.s_off = off;

@@ -1,0 +1,49 @@
+// Probe: device time of one panel launch (kb = 32) vs rows / cluster size.
+#define DTN_PANEL_PROFILE
+#include "../../paper_1302_5995_b200/csrc/k_blocked.cu"
+#include <cstdio>
+#include <vector>
+#include <random>
+using namespace dtnb;
+int main() {
+  blocked_init();
+  for (int kbv : {1, 2, 4, 8, 16, 32})
+  for (int rows : {64, 256, 2048}) {
+    const int n = rows, ld = (n + 7) / 8 * 8;
+    NodeDev nd{};
+    nd.kind = 2; nd.ni = n; nd.nb = 0; nd.total = n; nd.ld = nd.ldm = ld; nd.a = nd.b = -1;
+    NodeDev* dn; int* dl; double* da; double* db; int* dp; double* ds;
+    cudaMalloc(&dn, sizeof(nd)); cudaMalloc(&dl, 4); cudaMalloc(&da, sizeof(double) * ld * 32);
+    cudaMalloc(&db, sizeof(double) * ld * 32); cudaMalloc(&dp, 4 * (n + 200)); cudaMalloc(&ds, 16);
+    int zero = 0;
+    cudaMemcpy(dn, &nd, sizeof(nd), cudaMemcpyHostToDevice); cudaMemcpy(dl, &zero, 4, cudaMemcpyHostToDevice);
+    std::vector<double> h(size_t(ld) * 32);
+    std::mt19937_64 rng(1);
+    for (auto& x : h) x = double(rng() >> 11) * 0x1.0p-53 - 0.5;
+    cudaMemcpy(db, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+    KernelArgs a{dn, nullptr, nullptr, 0, 0, da, dp, ds};
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    float best = 1e9, tot = 0; int reps = 20;
+    for (int r = 0; r < reps + 2; ++r) {
+      cudaMemcpy(da, db, h.size() * 8, cudaMemcpyDeviceToDevice);
+      cudaEventRecord(e0);
+      cudaError_t err = launch_panel(a, dl, 1, n, 0, kbv, 0);
+      cudaEventRecord(e1); cudaEventSynchronize(e1);
+      if (err != cudaSuccess) { printf("err %s\n", cudaGetErrorString(err)); return 1; }
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      if (r >= 2) { best = ms < best ? ms : best; tot += ms; }
+    }
+    int rpt, cs; panel_shape(n, &rpt, &cs);
+    printf("kb %2d rows %5d csize %2d: best %.1f us, mean %.1f us (%.2f us/column)\n", kbv, n, cs, best * 1e3, tot / reps * 1e3,
+           best * 1e3 / kbv);
+  }
+  // empty-ish launch overhead reference
+  {
+    long long h[128];
+    cudaMemcpyFromSymbol(h, g_panel_clk, sizeof(h));
+    for (int j = 0; j < 32; j += 4)
+      printf("col %2d: argmax+publish %lld  warp0+push+sync %lld  update %lld  (next start %lld)\n", j, h[j*4+1]-h[j*4+0],
+             h[j*4+2]-h[j*4+1], h[j*4+3]-h[j*4+2], j < 31 ? h[(j+1)*4]-h[j*4+3] : 0LL);
+  }
+  printf("last error: %s\n", cudaGetErrorString(cudaGetLastError()));
+}
