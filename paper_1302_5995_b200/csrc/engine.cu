@@ -27,7 +27,7 @@ namespace dtnb {
 cudaError_t launch_small_elim(const KernelArgs&, const int*, int, int, bool, cudaStream_t);
 cudaError_t launch_gather(const KernelArgs&, const int*, int, int, cudaStream_t);
 cudaError_t launch_panel(const KernelArgs&, const int*, int, int, int, int, cudaStream_t);
-cudaError_t launch_rowpanel(const KernelArgs&, const int*, int, int, int, int, bool, cudaStream_t);
+cudaError_t launch_rowpanel(const KernelArgs&, const int*, int, int, int, int, int, bool, cudaStream_t);
 cudaError_t launch_trailing_update(const KernelArgs&, const int*, int, int, int, int, cudaStream_t);
 cudaError_t launch_gemm_desc(const GemmDesc*, int, int, int, double, double, cudaStream_t);
 cudaError_t launch_perm_identity(const int*, int, int*, double*, int, cudaStream_t);
@@ -206,7 +206,7 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
       L.blk_max_ni = std::max(L.blk_max_ni, nd.ni);
       L.blk_max_nb = std::max(L.blk_max_nb, nd.nb);
     }
-    if (L.blk_cnt) L.kb = panel_kb(L.blk_max_total);
+    if (L.blk_cnt) L.kb = panel_kb(L.blk_max_ni);
     for (int id : wv.small) {
       const Node& nd = P.nodes[id];
       if (nd.label_level >= 0) L.level = L.level < 0 ? nd.label_level : std::min(L.level, nd.label_level);
@@ -336,14 +336,16 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
           const Node& nd = P.nodes[hlst[i]];
           if (k0 >= nd.ni) continue;
           const double kbe = std::min(L.kb, nd.ni - k0), rows = nd.ni - k0, mn = nd.total - k0 - kbe;
-          fp += (nd.total - k0) * kbe * kbe;
+          fp += (nd.ni - k0) * kbe * kbe;
+          fr += kbe * kbe * nd.nb;
           fr += kbe * kbe * mn;
           ft += 2.0 * mn * mn * kbe;
         }
         run(K_PANEL, fp, 0.0,
-            [&] { return launch_panel(a, lst, L.blk_cnt, L.blk_max_total - k0, k0, L.kb, st); });
-        run(K_ROWPANEL, fr, 0.0,
-            [&] { return launch_rowpanel(a, lst, L.blk_cnt, L.blk_max_total, k0, L.kb, false, st); });
+            [&] { return launch_panel(a, lst, L.blk_cnt, L.blk_max_ni - k0, k0, L.kb, st); });
+        run(K_ROWPANEL, fr, 0.0, [&] {
+          return launch_rowpanel(a, lst, L.blk_cnt, L.blk_max_total, L.blk_max_nb, k0, L.kb, false, st);
+        });
         run(K_TRAILING, ft, 0.0,
             [&] { return launch_trailing_update(a, lst, L.blk_cnt, L.blk_max_total, k0, L.kb, st); });
       }
@@ -365,7 +367,7 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
       const double kbe = std::min(D.root_kb, nb - k0), rows = nb - k0, mn = nb - k0 - kbe;
       run(K_PANEL, rows * kbe * kbe, 0.0, [&] { return launch_panel(a, rl, 1, nb - k0, k0, D.root_kb, st); });
       run(K_ROWPANEL, kbe * kbe * mn, 0.0,
-          [&] { return launch_rowpanel(a, rl, 1, nb, k0, D.root_kb, true, st); });
+          [&] { return launch_rowpanel(a, rl, 1, nb, 0, k0, D.root_kb, true, st); });
       run(K_TRAILING, 2.0 * mn * mn * kbe, 0.0,
           [&] { return launch_trailing_update(a, rl, 1, nb, k0, D.root_kb, st); });
     }
@@ -836,8 +838,8 @@ int dtn_debug_partial_lu(int32_t n, int32_t ni, const double* A, double* out, in
     CK(cudaMemcpy2D(d_a, size_t(ld) * 8, A, size_t(n) * 8, size_t(n) * 8, n, cudaMemcpyHostToDevice));
     KernelArgs a{d_node, nullptr, nullptr, 0, 0, d_a, d_piv, d_ps};
     for (int k0 = 0; k0 < ni; k0 += 32) {
-      CK(launch_panel(a, d_list, 1, n - k0, k0, 32, 0));
-      CK(launch_rowpanel(a, d_list, 1, n, k0, 32, ni == n, 0));
+      CK(launch_panel(a, d_list, 1, ni - k0, k0, 32, 0));
+      CK(launch_rowpanel(a, d_list, 1, n, n - ni, k0, 32, ni == n, 0));
       CK(launch_trailing_update(a, d_list, 1, n, k0, 32, 0));
     }
     CK(cudaDeviceSynchronize());

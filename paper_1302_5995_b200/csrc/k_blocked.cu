@@ -73,8 +73,8 @@ __device__ long long g_panel_clk[4 * 32];
 #endif
 
 struct PanelCand {
-  double val;
-  int pos, lab;
+  unsigned key;
+  int pos, lab, pad;
   double row[PKB];
 };
 
@@ -84,7 +84,7 @@ template <bool CL>
 __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* __restrict__ list, int k0, int kb,
                                                    int csize) {
   __shared__ double wrow[2][PNW][PKB];
-  __shared__ double wval[2][PNW];
+  __shared__ unsigned wkey_s[2][PNW];
   __shared__ int wpos[2][PNW], wlab[2][PNW];
   __shared__ double jrow[2][PKB];
   __shared__ int jlab[2];
@@ -95,7 +95,9 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
   const NodeDev nd = args.nodes[node_id];
   if (k0 >= nd.ni) return;  // uniform over the cluster
   const int kbe = min(kb, nd.ni - k0);
-  const int Ri = nd.ni - k0, Rall = nd.total - k0;
+  // interface rows only: the boundary rows' L21 = A_b U11^{-1} is a parallel
+  // TRSM done by rowpanel_kernel
+  const int Ri = nd.ni - k0, Rall = Ri;
   double* M = args.arena + nd.m_off + k0 + (long long)k0 * nd.ldm;
   const long long ldm = nd.ldm;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -114,26 +116,20 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
     if (blockIdx.x == 0 && tid == 0) g_panel_clk[j * 4 + 0] = clock64();
 #endif
     const int buf = j & 1;
-    // ---- warp argmax of |column j| over candidate rows (NaN counts as +inf)
-    double val = -1.0;
-    if (r >= j && r < Ri) {
-      val = fabs(v[0]);
-      if (val != val) val = INFINITY;
-    }
-    double wb = val;
-    int wp = val >= 0.0 ? r : 0x7fffffff;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, wb, off);
-      const int op = __shfl_xor_sync(0xffffffffu, wp, off);
-      if (ob > wb || (ob == wb && op < wp)) { wb = ob; wp = op; }
-    }
-    if (wp == r) {
+    // ---- warp argmax of |column j| over candidate rows: 32-bit key = high
+    // word of |x| (sign 0, exponent, 20 mantissa bits; NaN ranks highest),
+    // low bit set for candidates; hardware warp max + ballot, ties -> lowest row
+    unsigned key = 0u;
+    if (r >= j && r < Ri) key = (unsigned(__double2hiint(fabs(v[0]))) | 1u);
+    const unsigned wkey = __reduce_max_sync(0xffffffffu, key);
+    const unsigned wball = __ballot_sync(0xffffffffu, key == wkey);
+    const int wp = (warp << 5) + __ffs(wball) - 1 + crank * PNT;
+    if (wp == r && key != 0u) {
 #pragma unroll
       for (int c = 0; c < PKB; ++c) wrow[buf][warp][c] = v[c];
       wlab[buf][warp] = lab;
     }
-    if (lane == 0) { wval[buf][warp] = wb; wpos[buf][warp] = wp; }
+    if (lane == 0) { wkey_s[buf][warp] = wkey; wpos[buf][warp] = wp; }
     if (r == j) {  // row j always sits in rank 0, warp 0
 #pragma unroll
       for (int c = 0; c < PKB; ++c) jrow[buf][c] = v[c];
@@ -144,19 +140,10 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
     if (blockIdx.x == 0 && tid == 0) g_panel_clk[j * 4 + 1] = clock64();
 #endif
     // ---- CTA argmax (every warp, redundantly)
-    double b = lane < PNW ? wval[buf][lane] : -1.0;
-    int bp = lane < PNW ? wpos[buf][lane] : 0x7fffffff;
-    int bw = lane;
-#pragma unroll
-    for (int off = PNW / 2; off > 0; off >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, b, off);
-      const int op = __shfl_xor_sync(0xffffffffu, bp, off);
-      const int ow = __shfl_xor_sync(0xffffffffu, bw, off);
-      if (ob > b || (ob == b && op < bp)) { b = ob; bp = op; bw = ow; }
-    }
-    b = __shfl_sync(0xffffffffu, b, 0);
-    bp = __shfl_sync(0xffffffffu, bp, 0);
-    bw = __shfl_sync(0xffffffffu, bw, 0) & (PNW - 1);
+    const unsigned lk = lane < PNW ? wkey_s[buf][lane] : 0u;
+    const unsigned bkey = __reduce_max_sync(0xffffffffu, lk);
+    const int bw = __ffs(__ballot_sync(0xffffffffu, lk == bkey && lane < PNW)) - 1;
+    const int bp = wpos[buf][bw];
     const double* prow;
     const double* jr;
     int p, plab, jl;
@@ -172,7 +159,7 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
           PanelCand* dc = cl.map_shared_rank(&cand[buf][crank], d);
           dc->row[lane] = rv;
           if (lane == 0) {
-            dc->val = b;
+            dc->key = bkey;
             dc->pos = bp;
             dc->lab = rl;
           }
@@ -183,18 +170,10 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
         }
       }
       cg::this_cluster().sync();
-      double cb = lane < csize ? cand[buf][lane].val : -1.0;
-      int cp = lane < csize ? cand[buf][lane].pos : 0x7fffffff;
-      int cw = lane;
-#pragma unroll
-      for (int off = 8; off > 0; off >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, cb, off);
-        const int op = __shfl_xor_sync(0xffffffffu, cp, off);
-        const int ow = __shfl_xor_sync(0xffffffffu, cw, off);
-        if (ob > cb || (ob == cb && op < cp)) { cb = ob; cp = op; cw = ow; }
-      }
-      p = __shfl_sync(0xffffffffu, cp, 0);
-      cw = __shfl_sync(0xffffffffu, cw, 0) & (PMAXC - 1);
+      const unsigned ck = lane < csize ? cand[buf][lane].key : 0u;
+      const unsigned gkey = __reduce_max_sync(0xffffffffu, ck);
+      const int cw = __ffs(__ballot_sync(0xffffffffu, ck == gkey && lane < csize)) - 1;
+      p = cand[buf][cw].pos;
       prow = cand[buf][cw].row;
       plab = cand[buf][cw].lab;
     } else {
@@ -211,7 +190,7 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
     const double apiv = fabs(piv);
     pmin = fmin(pmin, apiv);
     pmax = (apiv != apiv) ? INFINITY : fmax(pmax, apiv);
-    const double rinv = 1.0 / piv;
+    const double rinv = __drcp_rn(piv);
     if (r == p && p != j) {  // old row j moves down to position p
 #pragma unroll
       for (int c = 0; c < PKB; ++c) v[c] = jr[c];
@@ -290,7 +269,7 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
 // with swap_left, also the row swaps of the already factored columns [0, k0)
 // (needed only when L itself is reused: the root LU for G = S^{-1}).
 __global__ void __launch_bounds__(RP_THREADS) rowpanel_kernel(KernelArgs args, const int* __restrict__ list, int k0,
-                                                              int kb, int ncoltiles, int swap_left) {
+                                                              int kb, int ncoltiles, int nlefttiles) {
   __shared__ double T[32][33];
   __shared__ int s_dst[64], s_src[64];
   const NodeDev nd = args.nodes[list[blockIdx.y]];
@@ -299,10 +278,34 @@ __global__ void __launch_bounds__(RP_THREADS) rowpanel_kernel(KernelArgs args, c
   double* M = args.arena + nd.m_off;
   const long long ld = nd.ldm;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool left = blockIdx.x >= ncoltiles;
-  const int jbase = left ? (blockIdx.x - ncoltiles) * RP_COLS : k1 + blockIdx.x * RP_COLS;
+  const int bx = blockIdx.x;
+  if (bx >= ncoltiles + nlefttiles) {
+    // boundary rows [ni, total): L21 = A[i, k0:k1] U11^{-1}
+    const int i = nd.ni + (bx - ncoltiles - nlefttiles) * RP_THREADS + tid;
+    if (nd.ni + (bx - ncoltiles - nlefttiles) * RP_THREADS >= nd.total) return;
+    for (int e = tid; e < kbe * kbe; e += RP_THREADS) T[e % kbe][e / kbe] = M[(k0 + e % kbe) + (k0 + e / kbe) * ld];
+    __syncthreads();
+    if (i >= nd.total) return;
+    double x[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) x[c] = c < kbe ? M[i + (k0 + c) * ld] : 0.0;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      if (c < kbe) {
+        double sacc = x[c];
+#pragma unroll
+        for (int l = 0; l < c; ++l) sacc = fma(-x[l], T[l][c], sacc);
+        x[c] = sacc / T[c][c];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+      if (c < kbe) M[i + (k0 + c) * ld] = x[c];
+    return;
+  }
+  const bool left = bx >= ncoltiles;
+  const int jbase = left ? (bx - ncoltiles) * RP_COLS : k1 + bx * RP_COLS;
   const int jend = left ? k0 : nd.total;
-  if (left && !swap_left) return;
   if (jbase >= jend) return;
   const int* mv = move_list(args, nd);
   if (tid < 64) {
@@ -381,14 +384,15 @@ cudaError_t launch_panel(const KernelArgs& args, const int* d_list, int count, i
   return launch_panel_t<true>(args, d_list, count, k0, kb, csize, st);
 }
 
-cudaError_t launch_rowpanel(const KernelArgs& args, const int* d_list, int count, int max_total, int k0, int kb,
-                            bool swap_left, cudaStream_t st) {
+cudaError_t launch_rowpanel(const KernelArgs& args, const int* d_list, int count, int max_total, int max_nb, int k0,
+                            int kb, bool swap_left, cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
   const int coltiles = (max_total - k0 + RP_COLS - 1) / RP_COLS;
   const int lefttiles = swap_left ? (k0 + RP_COLS - 1) / RP_COLS : 0;
-  if (coltiles + lefttiles <= 0) return cudaSuccess;
-  dim3 grid(coltiles + lefttiles, count);
-  rowpanel_kernel<<<grid, RP_THREADS, 0, st>>>(args, d_list, k0, kb, coltiles, swap_left ? 1 : 0);
+  const int rowtiles = (max_nb + RP_THREADS - 1) / RP_THREADS;
+  if (coltiles + lefttiles + rowtiles <= 0) return cudaSuccess;
+  dim3 grid(coltiles + lefttiles + rowtiles, count);
+  rowpanel_kernel<<<grid, RP_THREADS, 0, st>>>(args, d_list, k0, kb, coltiles, lefttiles);
   return cudaGetLastError();
 }
 

@@ -27,10 +27,16 @@ def test_full_lu_matches_scipy(n):
     rng = np.random.default_rng(n)
     A = rng.standard_normal((n, n))
     out, ipiv, ps = gpu_partial_lu(A, n)
-    lu, piv = sla.lu_factor(A)
-    assert np.array_equal(ipiv, piv), (ipiv[:10], piv[:10])
-    assert np.max(np.abs(out - lu)) <= 1e-10 * np.max(np.abs(lu))
-    assert ps[0] == pytest.approx(np.min(np.abs(np.diag(lu))))
+    # P A = L U with the GPU's row-swap sequence (partial pivoting; near-ties may
+    # resolve differently from LAPACK, so compare the factorization, not ipiv)
+    PA = A.copy()
+    for i, p in enumerate(ipiv):
+        PA[[i, p]] = PA[[p, i]]
+    Lm = np.tril(out, -1) + np.eye(n)
+    Um = np.triu(out)
+    assert np.max(np.abs(Lm)) <= 1.0 + 1e-12          # partial pivoting bound |l_ij| <= 1
+    assert np.linalg.norm(Lm @ Um - PA) / np.linalg.norm(A) <= 1e-13
+    assert ps[0] == pytest.approx(np.min(np.abs(np.diag(Um))))
 
 
 @pytest.mark.parametrize("n,ni", [(40, 12), (184, 60), (376, 124), (1528, 508), (3064, 1020)])
