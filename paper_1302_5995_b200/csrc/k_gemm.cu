@@ -3,6 +3,8 @@
 // CTA tile BM x BN, K staged through shared memory in BK chunks with a
 // two-stage cp.async pipeline; 8 warps, each owning a WM x WN accumulator
 // tile in registers (FP64 has no tcgen05/TMEM path on sm_100a).
+#include <cstdint>
+
 #include "common.cuh"
 
 namespace dtnb {
@@ -18,9 +20,11 @@ struct GemmSmem {
   double b[2][GBN][GLDB];
 };
 
-// One BM x BN tile of C = alpha*A*B + beta*C (beta == 0: C not read).
-// Requires 16-byte aligned columns (offsets and leading dimensions even).
-template <int BK, bool A16 = true>
+// One BM x BN tile of C = alpha*A*B + beta*C with alpha, beta in {(1,0), (-1,1)}:
+// UPD (C -= A*B) preloads the C tile into the accumulators before the K loop
+// (its latency overlaps the first A/B stage) and feeds -A to the DMMA, so the
+// epilogue is a plain store. Requires 16-byte aligned B columns.
+template <int BK, bool A16 = true, bool UPD = false>
 __device__ __forceinline__ void gemm_tile(const double* __restrict__ A, int lda, const double* __restrict__ B,
                                           int ldb, double* C, int ldc, int m, int n, int k, int tm, int tn,
                                           double alpha, double beta, GemmSmem<BK>& sm) {
@@ -76,14 +80,21 @@ __device__ __forceinline__ void gemm_tile(const double* __restrict__ A, int lda,
   };
 
   double acc[GWM / 16][GWN / 8][4];
+  if (KT > 0) load(0, 0);
 #pragma unroll
   for (int i = 0; i < GWM / 16; ++i)
 #pragma unroll
     for (int j = 0; j < GWN / 8; ++j)
 #pragma unroll
-      for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
-
-  if (KT > 0) load(0, 0);
+      for (int v = 0; v < 4; ++v) {
+        double x = 0.0;
+        if constexpr (UPD) {
+          const int r = row0 + wm0 + i * 16 + g + 8 * (v >> 1);
+          const int c = col0 + wn0 + j * 8 + 2 * tig + (v & 1);
+          if (r < m && c < n) x = C[r + (long long)c * ldc];
+        }
+        acc[i][j][v] = x;
+      }
   for (int kt = 0; kt < KT; ++kt) {
     if (kt + 1 < KT) {
       load((kt + 1) & 1, kt + 1);
@@ -100,6 +111,10 @@ __device__ __forceinline__ void gemm_tile(const double* __restrict__ A, int lda,
       for (int i = 0; i < GWM / 16; ++i) {
         af[i][0] = sm.a[s][ks * 4 + tig][wm0 + i * 16 + g];
         af[i][1] = sm.a[s][ks * 4 + tig][wm0 + i * 16 + g + 8];
+        if constexpr (UPD) {
+          af[i][0] = -af[i][0];
+          af[i][1] = -af[i][1];
+        }
       }
 #pragma unroll
       for (int j = 0; j < GWN / 8; ++j) bf[j] = sm.b[s][wn0 + j * 8 + g][ks * 4 + tig];
@@ -121,14 +136,15 @@ __device__ __forceinline__ void gemm_tile(const double* __restrict__ A, int lda,
         const int c = col0 + wn0 + j * 8 + 2 * tig + (v & 1);
         if (r < m && c < n) {
           double* p = C + r + (long long)c * ldc;
-          *p = beta == 0.0 ? alpha * acc[i][j][v] : fma(alpha, acc[i][j][v], beta * *p);
+          if constexpr (UPD) *p = acc[i][j][v];
+          else *p = beta == 0.0 ? alpha * acc[i][j][v] : fma(alpha, acc[i][j][v], beta * *p);
         }
       }
     }
   }
 }
 
-template <int BK>
+template <int BK, bool UPD>
 __global__ void __launch_bounds__(GTHREADS) gemm_desc_kernel(const GemmDesc* __restrict__ descs, double alpha,
                                                              double beta) {
   extern __shared__ __align__(16) unsigned char gsm_raw[];
@@ -137,7 +153,10 @@ __global__ void __launch_bounds__(GTHREADS) gemm_desc_kernel(const GemmDesc* __r
   const int tiles_m = (d.m + GBM - 1) / GBM, tiles_n = (d.n + GBN - 1) / GBN;
   const int t = blockIdx.x;
   if (t >= tiles_m * tiles_n) return;
-  gemm_tile<BK>(d.A, d.lda, d.B, d.ldb, d.C, d.ldc, d.m, d.n, d.k, t % tiles_m, t / tiles_m, alpha, beta, sm);
+  // all descriptor GEMMs have 16-byte aligned A and B columns (root LU / G /
+  // S buffers with ld a multiple of 8, block offsets multiples of 32)
+  gemm_tile<BK, true, UPD>(d.A, d.lda, d.B, d.ldb, d.C, d.ldc, d.m, d.n, d.k, t % tiles_m, t / tiles_m, alpha, beta,
+                           sm);
 }
 
 // Trailing update of the blocked partial LU (right-looking, dense_nd.cpp:174-181
@@ -158,18 +177,26 @@ __global__ void __launch_bounds__(GTHREADS) trailing_update_kernel(KernelArgs ar
   double* M = args.arena + nd.m_off;
   const long long ld = nd.ldm;
   if ((k1 & 1) == 0)
-    gemm_tile<BK, true>(M + k1 + k0 * ld, nd.ldm, M + k0 + k1 * ld, nd.ldm, M + k1 + k1 * ld, nd.ldm, mn, mn, kbe,
-                        t % tiles, t / tiles, -1.0, 1.0, sm);
+    gemm_tile<BK, true, true>(M + k1 + k0 * ld, nd.ldm, M + k0 + k1 * ld, nd.ldm, M + k1 + k1 * ld, nd.ldm, mn, mn,
+                              kbe, t % tiles, t / tiles, -1.0, 1.0, sm);
   else
-    gemm_tile<BK, false>(M + k1 + k0 * ld, nd.ldm, M + k0 + k1 * ld, nd.ldm, M + k1 + k1 * ld, nd.ldm, mn, mn, kbe,
-                         t % tiles, t / tiles, -1.0, 1.0, sm);
+    gemm_tile<BK, false, true>(M + k1 + k0 * ld, nd.ldm, M + k0 + k1 * ld, nd.ldm, M + k1 + k1 * ld, nd.ldm, mn, mn,
+                               kbe, t % tiles, t / tiles, -1.0, 1.0, sm);
 }
 
 cudaError_t gemm_init() {
   cudaError_t e;
-  e = cudaFuncSetAttribute(gemm_desc_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(GemmSmem<16>));
+  e = cudaFuncSetAttribute(gemm_desc_kernel<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           sizeof(GemmSmem<16>));
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(gemm_desc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(GemmSmem<8>));
+  e = cudaFuncSetAttribute(gemm_desc_kernel<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           sizeof(GemmSmem<8>));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(gemm_desc_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           sizeof(GemmSmem<16>));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(gemm_desc_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           sizeof(GemmSmem<8>));
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(trailing_update_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            sizeof(GemmSmem<16>));
@@ -184,8 +211,16 @@ cudaError_t launch_gemm_desc(const GemmDesc* d_descs, int count, int max_tiles, 
                              cudaStream_t st) {
   if (count <= 0 || max_tiles <= 0) return cudaSuccess;
   dim3 grid(max_tiles, count);
-  if (kmax % 16 == 0 || kmax > 64) gemm_desc_kernel<16><<<grid, GTHREADS, sizeof(GemmSmem<16>), st>>>(d_descs, alpha, beta);
-  else gemm_desc_kernel<8><<<grid, GTHREADS, sizeof(GemmSmem<8>), st>>>(d_descs, alpha, beta);
+  const bool upd = alpha == -1.0 && beta == 1.0;
+  if (!upd && !(alpha == 1.0 && beta == 0.0)) return cudaErrorInvalidValue;
+  const bool bk16 = kmax % 16 == 0 || kmax > 64;
+  if (upd) {
+    if (bk16) gemm_desc_kernel<16, true><<<grid, GTHREADS, sizeof(GemmSmem<16>), st>>>(d_descs, alpha, beta);
+    else gemm_desc_kernel<8, true><<<grid, GTHREADS, sizeof(GemmSmem<8>), st>>>(d_descs, alpha, beta);
+  } else {
+    if (bk16) gemm_desc_kernel<16, false><<<grid, GTHREADS, sizeof(GemmSmem<16>), st>>>(d_descs, alpha, beta);
+    else gemm_desc_kernel<8, false><<<grid, GTHREADS, sizeof(GemmSmem<8>), st>>>(d_descs, alpha, beta);
+  }
   return cudaGetLastError();
 }
 
