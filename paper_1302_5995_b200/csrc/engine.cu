@@ -28,7 +28,7 @@ cudaError_t launch_small_elim(const KernelArgs&, const int*, int, int, bool, cud
 cudaError_t launch_gather(const KernelArgs&, const int*, int, int, cudaStream_t);
 cudaError_t launch_panel(const KernelArgs&, const int*, int, int, int, int, cudaStream_t);
 cudaError_t launch_rowpanel(const KernelArgs&, const int*, int, int, int, int, int, bool, cudaStream_t);
-cudaError_t launch_trailing_update(const KernelArgs&, const int*, int, int, int, int, cudaStream_t);
+cudaError_t launch_trailing_update(const KernelArgs&, const int*, int, int, int, int, int, int, cudaStream_t);
 cudaError_t launch_gemm_desc(const GemmDesc*, int, int, int, double, double, cudaStream_t);
 cudaError_t launch_perm_identity(const int*, int, int*, double*, int, cudaStream_t);
 cudaError_t launch_trsm_rows(const double*, int, double*, int, int, int, int, bool, cudaStream_t);
@@ -113,6 +113,8 @@ struct PlanDev {
   unsigned long long* h_norm = nullptr;
   std::vector<cudaEvent_t> ev_wave;
   cudaEvent_t ev_start = nullptr, ev_root = nullptr, ev_end = nullptr;
+  cudaEvent_t ev_rp = nullptr, ev_rest = nullptr;  // look-ahead dependencies
+  cudaStream_t side = nullptr;                      // low-priority stream for trailing updates
   cudaGraphExec_t gexec = nullptr;
   int graph_want_G = -1;
   int launches = 0;
@@ -120,8 +122,9 @@ struct PlanDev {
   ~PlanDev() {
     if (gexec) cudaGraphExecDestroy(gexec);
     for (auto e : ev_wave) cudaEventDestroy(e);
-    for (auto e : {ev_start, ev_root, ev_end})
+    for (auto e : {ev_start, ev_root, ev_end, ev_rp, ev_rest})
       if (e) cudaEventDestroy(e);
+    if (side) cudaStreamDestroy(side);
     for (void* p : std::initializer_list<void*>{d_nodes, d_pos, d_arena, d_piv, d_pivstat, d_lists, d_stencil, d_S, d_G,
                                                 d_perm, d_norm, d_inv_descs})
       if (p) cudaFree(p);
@@ -262,7 +265,17 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
   CK(cudaEventCreate(&D->ev_start));
   CK(cudaEventCreate(&D->ev_root));
   CK(cudaEventCreate(&D->ev_end));
+  CK(cudaEventCreateWithFlags(&D->ev_rp, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&D->ev_rest, cudaEventDisableTiming));
+  int lo = 0, hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  CK(cudaStreamCreateWithPriority(&D->side, cudaStreamNonBlocking, lo));
   return D;
+}
+
+bool use_lookahead() {
+  const char* e = std::getenv("DTN_NO_LOOKAHEAD");
+  return !(e && e[0] == '1');
 }
 
 // Per-launch profiler (opts.profile): CUDA events around every launch,
@@ -293,19 +306,63 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
   const Plan& P = D.P;
   const KernelArgs a = D.args();
   int launches = 0;
-  auto run = [&](int kclass, double flops, double bytes, auto&& fn) {
+  auto run_on = [&](cudaStream_t s_, int kclass, double flops, double bytes, auto&& fn) {
     Prof::Rec r{kclass, nullptr, nullptr, flops, bytes};
     if (prof) {
       CK(cudaEventCreate(&r.a));
       CK(cudaEventCreate(&r.b));
-      CK(cudaEventRecord(r.a, st));
+      CK(cudaEventRecord(r.a, s_));
     }
     CK(fn());
     ++launches;
     if (prof) {
-      CK(cudaEventRecord(r.b, st));
+      CK(cudaEventRecord(r.b, s_));
       prof->recs.push_back(r);
     }
+  };
+  auto run = [&](int kclass, double flops, double bytes, auto&& fn) { run_on(st, kclass, flops, bytes, fn); };
+  cudaStream_t st2 = D.side;
+  // Blocked partial LU of a batch of systems with one-step look-ahead: after
+  // panel(k) + rowpanel(k), the update of the next panel's columns runs on the
+  // main stream (so panel(k+1) starts at once) while the rest of the trailing
+  // update runs concurrently on the side stream; rowpanel(k+1) joins it.
+  auto blocked_lu = [&](const int* lst, const int* hlst, int cnt, int max_ni, int max_total, int max_nb, int kb,
+                        bool swap_left) {
+    bool pending = false;
+    for (int k0 = 0; k0 < max_ni; k0 += kb) {
+      double fp = 0.0, fr = 0.0, fn_ = 0.0, fr_ = 0.0;
+      for (int i = 0; i < cnt; ++i) {
+        const Node* ndp = hlst ? &P.nodes[hlst[i]] : nullptr;
+        const double ni = ndp ? ndp->ni : max_ni, nbn = ndp ? ndp->nb : max_nb, tot = ndp ? ndp->total : max_total;
+        if (k0 >= ni) continue;
+        const double kbe = std::min<double>(kb, ni - k0), mn = tot - k0 - kbe;
+        fp += (ni - k0) * kbe * kbe;
+        fr += kbe * kbe * (nbn + mn);
+        const double nn = std::min<double>(mn, kb);
+        fn_ += 2.0 * mn * nn * kbe;
+        fr_ += 2.0 * mn * (mn - nn) * kbe;
+      }
+      const bool more = k0 + kb < max_ni;
+      run(K_PANEL, fp, 0.0, [&] { return launch_panel(a, lst, cnt, max_ni - k0, k0, kb, st); });
+      if (pending) CK(cudaStreamWaitEvent(st, D.ev_rest, 0));
+      run(K_ROWPANEL, fr, 0.0,
+          [&] { return launch_rowpanel(a, lst, cnt, max_total, max_nb, k0, kb, swap_left, st); });
+      if (more && use_lookahead()) {
+        CK(cudaEventRecord(D.ev_rp, st));
+        CK(cudaStreamWaitEvent(st2, D.ev_rp, 0));
+        run(K_TRAILING, fn_, 0.0,
+            [&] { return launch_trailing_update(a, lst, cnt, max_total, k0, kb, 0, kb, st); });
+        run_on(st2, K_TRAILING, fr_, 0.0,
+               [&] { return launch_trailing_update(a, lst, cnt, max_total, k0, kb, kb, 1 << 30, st2); });
+        CK(cudaEventRecord(D.ev_rest, st2));
+        pending = true;
+      } else {
+        run(K_TRAILING, fn_ + fr_, 0.0,
+            [&] { return launch_trailing_update(a, lst, cnt, max_total, k0, kb, 0, 1 << 30, st); });
+        pending = false;
+      }
+    }
+    if (pending) CK(cudaStreamWaitEvent(st, D.ev_rest, 0));
   };
   auto list_flops = [&](const int* ids, int cnt) {
     double f = 0.0;
@@ -330,25 +387,7 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
       double gb = 0.0;
       for (int i = 0; i < L.blk_cnt; ++i) gb += 16.0 * double(P.nodes[hlst[i]].total) * P.nodes[hlst[i]].total;
       run(K_GATHER, 0.0, gb, [&] { return launch_gather(a, lst, L.blk_cnt, L.blk_max_total, st); });
-      for (int k0 = 0; k0 < L.blk_max_ni; k0 += L.kb) {
-        double fp = 0.0, fr = 0.0, ft = 0.0;
-        for (int i = 0; i < L.blk_cnt; ++i) {
-          const Node& nd = P.nodes[hlst[i]];
-          if (k0 >= nd.ni) continue;
-          const double kbe = std::min(L.kb, nd.ni - k0), rows = nd.ni - k0, mn = nd.total - k0 - kbe;
-          fp += (nd.ni - k0) * kbe * kbe;
-          fr += kbe * kbe * nd.nb;
-          fr += kbe * kbe * mn;
-          ft += 2.0 * mn * mn * kbe;
-        }
-        run(K_PANEL, fp, 0.0,
-            [&] { return launch_panel(a, lst, L.blk_cnt, L.blk_max_ni - k0, k0, L.kb, st); });
-        run(K_ROWPANEL, fr, 0.0, [&] {
-          return launch_rowpanel(a, lst, L.blk_cnt, L.blk_max_total, L.blk_max_nb, k0, L.kb, false, st);
-        });
-        run(K_TRAILING, ft, 0.0,
-            [&] { return launch_trailing_update(a, lst, L.blk_cnt, L.blk_max_total, k0, L.kb, st); });
-      }
+      blocked_lu(lst, hlst, L.blk_cnt, L.blk_max_ni, L.blk_max_total, L.blk_max_nb, L.kb, false);
     }
     if (events) CK(cudaEventRecord(D.ev_wave[w], st));
   }
@@ -363,14 +402,7 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
     double* LU = D.d_arena + D.lu_off;
     run(K_COPY, 0.0, 16.0 * nb2, [&] { return launch_copy2d(D.d_S, D.lds, LU, D.ldlu, nb, nb, st); });
     const int* rl = D.d_lists + D.root_list_off;
-    for (int k0 = 0; k0 < nb; k0 += D.root_kb) {
-      const double kbe = std::min(D.root_kb, nb - k0), rows = nb - k0, mn = nb - k0 - kbe;
-      run(K_PANEL, rows * kbe * kbe, 0.0, [&] { return launch_panel(a, rl, 1, nb - k0, k0, D.root_kb, st); });
-      run(K_ROWPANEL, kbe * kbe * mn, 0.0,
-          [&] { return launch_rowpanel(a, rl, 1, nb, 0, k0, D.root_kb, true, st); });
-      run(K_TRAILING, 2.0 * mn * mn * kbe, 0.0,
-          [&] { return launch_trailing_update(a, rl, 1, nb, k0, D.root_kb, st); });
-    }
+    blocked_lu(rl, nullptr, 1, nb, nb, 0, D.root_kb, true);
     run(K_MISC, 0.0, 8.0 * nb2, [&] {
       return launch_perm_identity(D.d_piv + D.h_nodes[D.root_lu_node].piv_off, nb, D.d_perm, D.d_G, D.ldg, st);
     });
@@ -554,7 +586,9 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
           D->gexec = nullptr;
         }
         cudaStream_t cap;
-        CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+        int lo = 0, hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CK(cudaStreamCreateWithPriority(&cap, cudaStreamNonBlocking, hi));
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
         try {
@@ -565,7 +599,7 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
           throw;
         }
         CK(cudaStreamEndCapture(cap, &g));
-        CK(cudaGraphInstantiate(&D->gexec, g, 0));
+        CK(cudaGraphInstantiateWithFlags(&D->gexec, g, cudaGraphInstantiateFlagUseNodePriority));
         CK(cudaGraphDestroy(g));
         CK(cudaStreamDestroy(cap));
         D->graph_want_G = int(want_G);
@@ -840,7 +874,7 @@ int dtn_debug_partial_lu(int32_t n, int32_t ni, const double* A, double* out, in
     for (int k0 = 0; k0 < ni; k0 += 32) {
       CK(launch_panel(a, d_list, 1, ni - k0, k0, 32, 0));
       CK(launch_rowpanel(a, d_list, 1, n, n - ni, k0, 32, ni == n, 0));
-      CK(launch_trailing_update(a, d_list, 1, n, k0, 32, 0));
+      CK(launch_trailing_update(a, d_list, 1, n, k0, 32, 0, 1 << 30, 0));
     }
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy2D(out, size_t(n) * 8, d_a, size_t(ld) * 8, size_t(n) * 8, n, cudaMemcpyDeviceToHost));

@@ -3,6 +3,7 @@
 // CTA tile BM x BN, K staged through shared memory in BK chunks with a
 // two-stage cp.async pipeline; 8 warps, each owning a WM x WN accumulator
 // tile in registers (FP64 has no tcgen05/TMEM path on sm_100a).
+#include <algorithm>
 #include <cstdint>
 
 #include "common.cuh"
@@ -164,25 +165,30 @@ __global__ void __launch_bounds__(GTHREADS) gemm_desc_kernel(const GemmDesc* __r
 // ni > k0, M[k1:, k1:] -= M[k1:, k0:k1] * M[k0:k1, k1:], k1 = k0 + min(kb, ni-k0).
 template <int BK>
 __global__ void __launch_bounds__(GTHREADS) trailing_update_kernel(KernelArgs args, const int* __restrict__ list,
-                                                                   int k0, int kb) {
+                                                                   int k0, int kb, int c0, int c1) {
   extern __shared__ __align__(16) unsigned char gsm_raw[];
   GemmSmem<BK>& sm = *reinterpret_cast<GemmSmem<BK>*>(gsm_raw);
   const NodeDev nd = args.nodes[list[blockIdx.y]];
   if (k0 >= nd.ni) return;
   const int kbe = min(kb, nd.ni - k0), k1 = k0 + kbe;
-  const int mn = nd.total - k1;
-  const int tiles = (mn + GBM - 1) / GBM, tiles_n = (mn + GBN - 1) / GBN;
+  // rows [k1, total); columns [k1 + c0, min(total, k1 + c1)) (look-ahead split)
+  const int m = nd.total - k1;
+  const int cb = k1 + c0, n = min(nd.total, k1 + c1) - cb;
+  if (m <= 0 || n <= 0) return;
+  const int tiles = (m + GBM - 1) / GBM, tiles_n = (n + GBN - 1) / GBN;
   const int t = blockIdx.x;
   if (t >= tiles * tiles_n) return;
   double* M = args.arena + nd.m_off;
   const long long ld = nd.ldm;
   if ((k1 & 1) == 0)
-    gemm_tile<BK, true, true>(M + k1 + k0 * ld, nd.ldm, M + k0 + k1 * ld, nd.ldm, M + k1 + k1 * ld, nd.ldm, mn, mn,
-                              kbe, t % tiles, t / tiles, -1.0, 1.0, sm);
+    gemm_tile<BK, true, true>(M + k1 + k0 * ld, nd.ldm, M + k0 + cb * ld, nd.ldm, M + k1 + cb * ld, nd.ldm, m, n, kbe,
+                              t % tiles, t / tiles, -1.0, 1.0, sm);
   else
-    gemm_tile<BK, false, true>(M + k1 + k0 * ld, nd.ldm, M + k0 + k1 * ld, nd.ldm, M + k1 + k1 * ld, nd.ldm, mn, mn,
+    gemm_tile<BK, false, true>(M + k1 + k0 * ld, nd.ldm, M + k0 + cb * ld, nd.ldm, M + k1 + cb * ld, nd.ldm, m, n,
                                kbe, t % tiles, t / tiles, -1.0, 1.0, sm);
 }
+
+int gemm_tiles(int m, int n);
 
 cudaError_t gemm_init() {
   cudaError_t e;
@@ -224,13 +230,17 @@ cudaError_t launch_gemm_desc(const GemmDesc* d_descs, int count, int max_tiles, 
   return cudaGetLastError();
 }
 
+// Columns [k1 + c0, k1 + c1) of the trailing block (c1 = INT_MAX: to the end).
 cudaError_t launch_trailing_update(const KernelArgs& args, const int* d_list, int count, int max_total, int k0, int kb,
-                                   cudaStream_t st) {
-  const int mn = max_total - k0 - 1;
-  if (count <= 0 || mn <= 0) return cudaSuccess;
-  dim3 grid(gemm_tiles(mn, mn), count);
-  if (kb % 16 == 0) trailing_update_kernel<16><<<grid, GTHREADS, sizeof(GemmSmem<16>), st>>>(args, d_list, k0, kb);
-  else trailing_update_kernel<8><<<grid, GTHREADS, sizeof(GemmSmem<8>), st>>>(args, d_list, k0, kb);
+                                   int c0, int c1, cudaStream_t st) {
+  const int m = max_total - k0 - 1;
+  const int n = std::min(m, c1) - c0;
+  if (count <= 0 || m <= 0 || n <= 0) return cudaSuccess;
+  dim3 grid(gemm_tiles(m, n), count);
+  if (kb % 16 == 0)
+    trailing_update_kernel<16><<<grid, GTHREADS, sizeof(GemmSmem<16>), st>>>(args, d_list, k0, kb, c0, c1);
+  else
+    trailing_update_kernel<8><<<grid, GTHREADS, sizeof(GemmSmem<8>), st>>>(args, d_list, k0, kb, c0, c1);
   return cudaGetLastError();
 }
 
