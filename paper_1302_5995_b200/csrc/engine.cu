@@ -35,6 +35,11 @@ cudaError_t launch_trsm_rows(const double*, int, double*, int, int, int, int, bo
 cudaError_t launch_norm1(const double*, int, int, int, unsigned long long*, cudaStream_t);
 cudaError_t launch_copy2d(const double*, int, double*, int, int, int, cudaStream_t);
 cudaError_t gemm_init();
+cudaError_t misc_init();
+cudaError_t launch_tri_inv_blocks(const double*, int, int, double*, cudaStream_t);
+cudaError_t launch_set_identity(double*, int, int, cudaStream_t);
+cudaError_t launch_permute_columns(const double*, int, const int*, int, double*, int, cudaStream_t);
+cudaError_t launch_perm_only(const int*, int, int*, cudaStream_t);
 cudaError_t blocked_init();
 int gemm_tiles(int, int);
 }  // namespace dtnb
@@ -109,6 +114,9 @@ struct PlanDev {
   unsigned long long* d_norm = nullptr;
   GemmDesc* d_inv_descs = nullptr;
   std::vector<GemmDesc> h_inv_descs;
+  double* d_W = nullptr;     // U^{-1} L^{-1} before the column permutation
+  double* d_T = nullptr;     // 128 x nb staging block of the triangular sweeps
+  double* d_tinv = nullptr;  // inverses of the 128 x 128 diagonal blocks of L and U
   double* h_pivstat = nullptr;  // pinned
   unsigned long long* h_norm = nullptr;
   std::vector<cudaEvent_t> ev_wave;
@@ -126,7 +134,7 @@ struct PlanDev {
       if (e) cudaEventDestroy(e);
     if (side) cudaStreamDestroy(side);
     for (void* p : std::initializer_list<void*>{d_nodes, d_pos, d_arena, d_piv, d_pivstat, d_lists, d_stencil, d_S, d_G,
-                                                d_perm, d_norm, d_inv_descs})
+                                                d_perm, d_norm, d_inv_descs, d_W, d_T, d_tinv})
       if (p) cudaFree(p);
     if (h_pivstat) cudaFreeHost(h_pivstat);
     if (h_norm) cudaFreeHost(h_norm);
@@ -245,17 +253,27 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
   D->d_norm = dalloc<unsigned long long>(2);
   CK(cudaMallocHost(&D->h_pivstat, 2 * D->h_nodes.size() * sizeof(double)));
   CK(cudaMallocHost(&D->h_norm, 2 * sizeof(unsigned long long)));
-  // root inverse sweeps: forward X[k1:] -= L[k1:,k0:k1] X[k0:k1]; backward X[:k0] -= U[:k0,k0:k1] X[k0:k1]
+  // Root inverse G = U^{-1} L^{-1} P (getri-style, 2 nb^3 flops): W = I; forward
+  // sweep over 128-row blocks using L_kk^{-1} (only the columns [0, k1) are
+  // nonzero), backward sweep with U_kk^{-1}; then G = W P (column permutation).
+  // Per block: T = Tinv_k W_k (GEMM), W_rest -= LU_block T (GEMM), W_k = T (copy).
   const double* LU = D->d_arena + D->lu_off;
-  for (int k0 = 0; k0 < nb; k0 += 32) {
-    const int k1 = std::min(nb, k0 + 32);
-    D->h_inv_descs.push_back(GemmDesc{LU + k1 + int64_t(k0) * D->ldlu, D->d_G + k0, D->d_G + k1, nb - k1, nb,
-                                      k1 - k0, D->ldlu, D->ldg, D->ldg});
+  D->d_W = dalloc<double>(size_t(D->ldg) * nb);
+  D->d_T = dalloc<double>(size_t(128) * nb);
+  const int nblk = (nb + 127) / 128;
+  D->d_tinv = dalloc<double>(size_t(nblk) * 2 * 128 * 128);
+  for (int kb_ = 0; kb_ < nblk; ++kb_) {  // forward
+    const int k0 = kb_ * 128, k1 = std::min(nb, k0 + 128), bk = k1 - k0;
+    const double* Linv = D->d_tinv + size_t(kb_) * 2 * 128 * 128;
+    D->h_inv_descs.push_back(GemmDesc{Linv, D->d_W + k0, D->d_T, bk, k1, bk, 128, D->ldg, 128});
+    D->h_inv_descs.push_back(GemmDesc{LU + k1 + int64_t(k0) * D->ldlu, D->d_T, D->d_W + k1, nb - k1, k1, bk, D->ldlu,
+                                      128, D->ldg});
   }
-  for (int k0 = 0; k0 < nb; k0 += 32) {
-    const int k1 = std::min(nb, k0 + 32);
-    D->h_inv_descs.push_back(
-        GemmDesc{LU + int64_t(k0) * D->ldlu, D->d_G + k0, D->d_G, k0, nb, k1 - k0, D->ldlu, D->ldg, D->ldg});
+  for (int kb_ = 0; kb_ < nblk; ++kb_) {  // backward (used in reverse order)
+    const int k0 = kb_ * 128, k1 = std::min(nb, k0 + 128), bk = k1 - k0;
+    const double* Uinv = D->d_tinv + size_t(kb_) * 2 * 128 * 128 + 128 * 128;
+    D->h_inv_descs.push_back(GemmDesc{Uinv, D->d_W + k0, D->d_T, bk, nb, bk, 128, D->ldg, 128});
+    D->h_inv_descs.push_back(GemmDesc{LU + int64_t(k0) * D->ldlu, D->d_T, D->d_W, k0, nb, bk, D->ldlu, 128, D->ldg});
   }
   D->d_inv_descs = dalloc<GemmDesc>(D->h_inv_descs.size());
   CK(cudaMemcpy(D->d_inv_descs, D->h_inv_descs.data(), D->h_inv_descs.size() * sizeof(GemmDesc),
@@ -403,32 +421,33 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
     run(K_COPY, 0.0, 16.0 * nb2, [&] { return launch_copy2d(D.d_S, D.lds, LU, D.ldlu, nb, nb, st); });
     const int* rl = D.d_lists + D.root_list_off;
     blocked_lu(rl, nullptr, 1, nb, nb, 0, D.root_kb, true);
-    run(K_MISC, 0.0, 8.0 * nb2, [&] {
-      return launch_perm_identity(D.d_piv + D.h_nodes[D.root_lu_node].piv_off, nb, D.d_perm, D.d_G, D.ldg, st);
-    });
-    ++launches;  // perm + scatter
-    int di = 0;
-    for (int k0 = 0; k0 < nb; k0 += 32, ++di) {
-      const int kbe = std::min(32, nb - k0);
-      run(K_INV_TRSM, double(kbe) * kbe * nb, 0.0,
-          [&] { return launch_trsm_rows(LU, D.ldlu, D.d_G, D.ldg, nb, k0, kbe, true, st); });
+    // the panels maintain perm[pos] = original row of the root LU (P A = L U)
+    const int* perm = D.d_piv + D.h_nodes[D.root_lu_node].piv_off;
+    run(K_INV_TRSM, double(nb) * 128 * 128, 0.0, [&] { return launch_tri_inv_blocks(LU, D.ldlu, nb, D.d_tinv, st); });
+    run(K_MISC, 0.0, 8.0 * nb2, [&] { return launch_set_identity(D.d_W, D.ldg, nb, st); });
+    const int nblk = (nb + 127) / 128;
+    auto gemm = [&](int di, double alpha, double beta) {
       const GemmDesc& g = D.h_inv_descs[di];
-      if (g.m > 0)
-        run(K_INV_GEMM, 2.0 * g.m * g.n * g.k, 0.0, [&] {
-          return launch_gemm_desc(D.d_inv_descs + di, 1, gemm_tiles(g.m, g.n), g.k, -1.0, 1.0, st);
-        });
+      if (g.m <= 0 || g.n <= 0) return;
+      run(K_INV_GEMM, 2.0 * g.m * g.n * g.k, 0.0, [&] {
+        return launch_gemm_desc(D.d_inv_descs + di, 1, gemm_tiles(g.m, g.n), g.k, alpha, beta, st);
+      });
+    };
+    for (int kb_ = 0; kb_ < nblk; ++kb_) {
+      const int k0 = kb_ * 128, k1 = std::min(nb, k0 + 128);
+      gemm(2 * kb_, 1.0, 0.0);       // T = L_kk^{-1} W[k0:k1, 0:k1]
+      gemm(2 * kb_ + 1, -1.0, 1.0);  // W[k1:, 0:k1] -= L[k1:, k0:k1] T
+      run(K_COPY, 0.0, 16.0 * (k1 - k0) * k1,
+          [&] { return launch_copy2d(D.d_T, 128, D.d_W + k0, D.ldg, k1 - k0, k1, st); });
     }
-    const int nblk = di;
-    for (int bi = nblk - 1; bi >= 0; --bi) {
-      const int k0 = bi * 32, kbe = std::min(32, nb - k0);
-      run(K_INV_TRSM, double(kbe) * kbe * nb, 0.0,
-          [&] { return launch_trsm_rows(LU, D.ldlu, D.d_G, D.ldg, nb, k0, kbe, false, st); });
-      const GemmDesc& g = D.h_inv_descs[nblk + bi];
-      if (g.m > 0)
-        run(K_INV_GEMM, 2.0 * g.m * g.n * g.k, 0.0, [&] {
-          return launch_gemm_desc(D.d_inv_descs + nblk + bi, 1, gemm_tiles(g.m, g.n), g.k, -1.0, 1.0, st);
-        });
+    for (int kb_ = nblk - 1; kb_ >= 0; --kb_) {
+      const int k0 = kb_ * 128, k1 = std::min(nb, k0 + 128);
+      gemm(2 * nblk + 2 * kb_, 1.0, 0.0);       // T = U_kk^{-1} W[k0:k1, :]
+      gemm(2 * nblk + 2 * kb_ + 1, -1.0, 1.0);  // W[:k0, :] -= U[:k0, k0:k1] T
+      run(K_COPY, 0.0, 16.0 * (k1 - k0) * nb,
+          [&] { return launch_copy2d(D.d_T, 128, D.d_W + k0, D.ldg, k1 - k0, nb, st); });
     }
+    run(K_COPY, 0.0, 16.0 * nb2, [&] { return launch_permute_columns(D.d_W, D.ldg, perm, nb, D.d_G, D.ldg, st); });
     CK(cudaMemsetAsync(D.d_norm, 0, 2 * sizeof(unsigned long long), st));
     run(K_MISC, 0.0, 8.0 * nb2, [&] { return launch_norm1(D.d_S, D.lds, nb, nb, D.d_norm, st); });
     run(K_MISC, 0.0, 8.0 * nb2, [&] { return launch_norm1(D.d_G, D.ldg, nb, nb, D.d_norm + 1, st); });
@@ -520,6 +539,7 @@ int dtn_gpu_create(dtn_ctx** out, int device) {
     CK(cudaSetDevice(device));
     CK(gemm_init());
     CK(blocked_init());
+    CK(misc_init());
     auto* c = new dtn_ctx;
     c->device = device;
     CK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));

@@ -69,7 +69,8 @@ __device__ __forceinline__ int* move_list(const KernelArgs& args, const NodeDev&
 }
 
 #ifdef DTN_PANEL_PROFILE
-__device__ long long g_panel_clk[4 * 32];
+__device__ long long g_panel_clk[8 * 32];
+#define PCLK(slot) do { if (blockIdx.x == 0 && tid == 0) g_panel_clk[j * 8 + (slot)] = clock64(); } while (0)
 #endif
 
 struct PanelCand {
@@ -78,18 +79,22 @@ struct PanelCand {
   double row[PKB];
 };
 
-// Registers hold one row per thread, rotated left by one after every pivot
-// step so the active column is always v[0] (no dynamic register indexing).
+// Registers hold one row per thread; the pivot loop is fully unrolled so all
+// register indices are compile-time. Rows are NOT swapped during the panel:
+// the pivot row of step j is flagged (elim = j) and stays in its thread, so a
+// pivot step moves no data except the per-warp candidate rows. The final row
+// order (pivot rows to positions [0, kbe), displaced top rows into the
+// vacated positions) is applied once at the end, and published as the net
+// row-move list + the node's running permutation perm[pos] = original row.
 template <bool CL>
 __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* __restrict__ list, int k0, int kb,
                                                    int csize) {
-  __shared__ double wrow[2][PNW][PKB];
-  __shared__ unsigned wkey_s[2][PNW];
-  __shared__ int wpos[2][PNW], wlab[2][PNW];
-  __shared__ double jrow[2][PKB];
-  __shared__ int jlab[2];
-  __shared__ PanelCand cand[2][CL ? PMAXC : 1];
-  __shared__ int sp[PKB];
+  // row slots: [0, PNW) warp candidates, PNW + q = candidate of cluster rank q
+  constexpr int SC = PNW, NSLOT = PNW + (CL ? PMAXC : 0);
+  __shared__ __align__(16) double rows[2][NSLOT][PKB];
+  __shared__ unsigned skey[2][NSLOT];
+  __shared__ int spos[2][NSLOT];
+  __shared__ int sp[PKB], vac[PKB];
   const int crank = CL ? int(cg::this_cluster().block_rank()) : 0;
   const int node_id = list[blockIdx.x / csize];
   const NodeDev nd = args.nodes[node_id];
@@ -97,170 +102,169 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
   const int kbe = min(kb, nd.ni - k0);
   // interface rows only: the boundary rows' L21 = A_b U11^{-1} is a parallel
   // TRSM done by rowpanel_kernel
-  const int Ri = nd.ni - k0, Rall = Ri;
+  const int Ri = nd.ni - k0;
   double* M = args.arena + nd.m_off + k0 + (long long)k0 * nd.ldm;
   const long long ldm = nd.ldm;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int r = crank * PNT + tid;  // this thread's row (position) in the panel
+  const int r = crank * PNT + tid;  // this thread's row in the panel (original position)
+  int* perm = args.piv + nd.piv_off;  // running permutation of the interface rows
 
   double v[PKB];
 #pragma unroll
-  for (int c = 0; c < PKB; ++c) v[c] = (r < Rall && c < kbe) ? M[r + c * ldm] : 0.0;
-  int lab = r, first = -1;
+  for (int c = 0; c < PKB; ++c) v[c] = (r < Ri && c < kbe) ? M[r + c * ldm] : 0.0;
+  int elim = (r < Ri) ? -1 : PKB;  // step at which this row became a pivot
   double pmin = k0 == 0 ? DBL_MAX : args.pivstat[2 * node_id];
   double pmax = k0 == 0 ? 0.0 : args.pivstat[2 * node_id + 1];
+  bool bad = false;
+  const int pperm0 = (k0 == 0 && r < Ri) ? r : 0;
+  if (k0 == 0 && r < Ri) perm[r] = pperm0;
 
-#pragma unroll 1
-  for (int j = 0; j < kbe; ++j) {
+#pragma unroll
+  for (int j = 0; j < PKB; ++j) {
+    if (j >= kbe) break;
 #ifdef DTN_PANEL_PROFILE
-    if (blockIdx.x == 0 && tid == 0) g_panel_clk[j * 4 + 0] = clock64();
+    PCLK(0);
 #endif
     const int buf = j & 1;
-    // ---- warp argmax of |column j| over candidate rows: 32-bit key = high
+    // ---- warp argmax of |column j| over the live rows: 32-bit key = high
     // word of |x| (sign 0, exponent, 20 mantissa bits; NaN ranks highest),
     // low bit set for candidates; hardware warp max + ballot, ties -> lowest row
     unsigned key = 0u;
-    if (r >= j && r < Ri) key = (unsigned(__double2hiint(fabs(v[0]))) | 1u);
+    if (elim < 0) key = (unsigned(__double2hiint(fabs(v[j]))) | 1u);
     const unsigned wkey = __reduce_max_sync(0xffffffffu, key);
-    const unsigned wball = __ballot_sync(0xffffffffu, key == wkey);
-    const int wp = (warp << 5) + __ffs(wball) - 1 + crank * PNT;
-    if (wp == r && key != 0u) {
+    const int wlane = __ffs(__ballot_sync(0xffffffffu, key == wkey)) - 1;
+#ifdef DTN_PANEL_PROFILE
+    PCLK(1);
+#endif
+    if (lane == wlane) {
 #pragma unroll
-      for (int c = 0; c < PKB; ++c) wrow[buf][warp][c] = v[c];
-      wlab[buf][warp] = lab;
+      for (int c = j; c < PKB; ++c) rows[buf][warp][c] = v[c];
+      skey[buf][warp] = wkey;
+      spos[buf][warp] = r;
     }
-    if (lane == 0) { wkey_s[buf][warp] = wkey; wpos[buf][warp] = wp; }
-    if (r == j) {  // row j always sits in rank 0, warp 0
-#pragma unroll
-      for (int c = 0; c < PKB; ++c) jrow[buf][c] = v[c];
-      jlab[buf] = lab;
-    }
+#ifdef DTN_PANEL_PROFILE
+    PCLK(2);
+#endif
     __syncthreads();
 #ifdef DTN_PANEL_PROFILE
-    if (blockIdx.x == 0 && tid == 0) g_panel_clk[j * 4 + 1] = clock64();
+    PCLK(3);
 #endif
     // ---- CTA argmax (every warp, redundantly)
-    const unsigned lk = lane < PNW ? wkey_s[buf][lane] : 0u;
+    const unsigned lk = lane < PNW ? skey[buf][lane] : 0u;
     const unsigned bkey = __reduce_max_sync(0xffffffffu, lk);
     const int bw = __ffs(__ballot_sync(0xffffffffu, lk == bkey && lane < PNW)) - 1;
-    const int bp = wpos[buf][bw];
-    const double* prow;
-    const double* jr;
-    int p, plab, jl;
+    int slot = bw, p = spos[buf][bw];
     if constexpr (CL) {
-      // warp 0 pushes this CTA's candidate (and rank 0 row j) to every CTA
+      // warp 0 pushes this CTA's candidate into every CTA of the cluster
       if (warp == 0) {
         cg::cluster_group cl = cg::this_cluster();
-        const double rv = wrow[buf][bw][lane];
-        const int rl = wlab[buf][bw];
-        const double jv = jrow[buf][lane];
-        const int jlv = jlab[buf];
+        const double rv = rows[buf][bw][lane];
         for (int d = 0; d < csize; ++d) {
-          PanelCand* dc = cl.map_shared_rank(&cand[buf][crank], d);
-          dc->row[lane] = rv;
+          if (lane >= j) cl.map_shared_rank(&rows[buf][SC + crank][0], d)[lane] = rv;
           if (lane == 0) {
-            dc->key = bkey;
-            dc->pos = bp;
-            dc->lab = rl;
-          }
-          if (crank == 0 && d != 0) {
-            cl.map_shared_rank(&jrow[buf][0], d)[lane] = jv;
-            if (lane == 0) *cl.map_shared_rank(&jlab[buf], d) = jlv;
+            *cl.map_shared_rank(&skey[buf][SC + crank], d) = bkey;
+            *cl.map_shared_rank(&spos[buf][SC + crank], d) = p;
           }
         }
       }
       cg::this_cluster().sync();
-      const unsigned ck = lane < csize ? cand[buf][lane].key : 0u;
+      const unsigned ck = lane < csize ? skey[buf][SC + lane] : 0u;
       const unsigned gkey = __reduce_max_sync(0xffffffffu, ck);
       const int cw = __ffs(__ballot_sync(0xffffffffu, ck == gkey && lane < csize)) - 1;
-      p = cand[buf][cw].pos;
-      prow = cand[buf][cw].row;
-      plab = cand[buf][cw].lab;
-    } else {
-      p = bp;
-      prow = wrow[buf][bw];
-      plab = wlab[buf][bw];
+      slot = SC + cw;
+      p = spos[buf][slot];
     }
-    jr = jrow[buf];
-    jl = jlab[buf];
 #ifdef DTN_PANEL_PROFILE
-    if (blockIdx.x == 0 && tid == 0) g_panel_clk[j * 4 + 2] = clock64();
+    PCLK(4);
 #endif
-    const double piv = prow[0];
+    double pr[PKB];
+#pragma unroll
+    for (int c = j; c < PKB; ++c) pr[c] = rows[buf][slot][c];
+    const double piv = pr[j];
     const double apiv = fabs(piv);
     pmin = fmin(pmin, apiv);
-    pmax = (apiv != apiv) ? INFINITY : fmax(pmax, apiv);
+    pmax = fmax(pmax, apiv);
+    bad |= !(apiv == apiv) || apiv == INFINITY;
     const double rinv = __drcp_rn(piv);
-    if (r == p && p != j) {  // old row j moves down to position p
+#ifdef DTN_PANEL_PROFILE
+    PCLK(5);
+#endif
+    if (r == p) elim = j;
+    if (elim < 0) {
+      const double l = v[j] * rinv;
+      v[j] = l;
 #pragma unroll
-      for (int c = 0; c < PKB; ++c) v[c] = jr[c];
-      lab = jl;
-      if (first < 0) first = j;
+      for (int c = j + 1; c < PKB; ++c) v[c] = fma(-l, pr[c], v[c]);
     }
-    if (r == j) {  // pivot row moves up to position j
-#pragma unroll
-      for (int c = 0; c < PKB; ++c) v[c] = prow[c];
-      lab = plab;
-    }
-    if (r > j && r < Rall) {
-      const double l = v[0] * rinv;
-      v[0] = l;
-      const int lim = PKB - j;  // rotated indices >= lim hold the factored L columns
-#pragma unroll
-      for (int c = 1; c < PKB; ++c)
-        if (c < lim) v[c] = fma(-l, prow[c], v[c]);
-    }
-    {  // rotate left by one: the next column becomes v[0]
-      const double t0 = v[0];
-#pragma unroll
-      for (int c = 0; c < PKB - 1; ++c) v[c] = v[c + 1];
-      v[PKB - 1] = t0;
-    }
+#ifdef DTN_PANEL_PROFILE
+    PCLK(6);
+#endif
     if (tid == 0) sp[j] = p;
 #ifdef DTN_PANEL_PROFILE
-    if (blockIdx.x == 0 && tid == 0) g_panel_clk[j * 4 + 3] = clock64();
+    PCLK(7);
 #endif
   }
-#pragma unroll 1
-  for (int t = kbe; t < PKB; ++t) {  // complete the rotation to the identity
-    const double t0 = v[0];
-#pragma unroll
-    for (int c = 0; c < PKB - 1; ++c) v[c] = v[c + 1];
-    v[PKB - 1] = t0;
+  __syncthreads();
+  // ---- final placement: pivot of step e -> position e; the top rows [0, kbe)
+  // that were not pivots fill, in order, the positions vacated by pivots that
+  // came from rows >= kbe (also in order)
+  if (warp == 0) {
+    const int x = lane < kbe ? sp[lane] : 0x7fffffff;
+    const int key2 = x >= kbe ? x : 0x7fffffff;
+    int rank = 0;
+    for (int e = 0; e < kbe; ++e) {
+      const int y = sp[e] >= kbe ? sp[e] : 0x7fffffff;
+      rank += (y < key2);
+    }
+    if (lane < kbe && key2 != 0x7fffffff) vac[rank] = key2;
   }
-  // ---- write back; emit ipiv and the net row-move list
+  unsigned topmask = 0u;  // top rows [0, kbe) that became pivots
+#pragma unroll
+  for (int e = 0; e < PKB; ++e)
+    if (e < kbe && sp[e] < kbe) topmask |= 1u << sp[e];
+  __syncthreads();
+  int fp = r;
+  if (elim >= 0 && elim < PKB) {
+    fp = elim;
+  } else if (r < kbe) {  // displaced top row (r < kbe < Ri, never a pivot)
+    fp = vac[__popc(~topmask & ((1u << r) - 1u))];
+  }
   int* mv = move_list(args, nd);
-  if (r < Rall) {
+  if (r < Ri) {
 #pragma unroll
     for (int c = 0; c < PKB; ++c)
-      if (c < kbe) M[r + c * ldm] = v[c];
+      if (c < kbe) M[fp + c * ldm] = v[c];
     int slot = -1;
-    if (r < kbe) slot = r;
-    else if (first >= 0) slot = kbe + first;
+    if (fp < kbe) slot = fp;
+    else if (fp != r) {  // fp is a vacated position: its rank among them
+      int rk = 0;
+      for (int e = 0; e < kbe; ++e) rk += (sp[e] >= kbe && sp[e] < fp);
+      slot = kbe + rk;
+    }
     if (slot >= 0) {
-      mv[slot] = k0 + r;
-      mv[2 * PKB + slot] = k0 + lab;
+      mv[slot] = k0 + fp;
+      mv[2 * PKB + slot] = k0 + r;
     }
   }
-  __syncthreads();
   if (crank == 0) {
-    if (tid < kbe) {
-      args.piv[nd.piv_off + k0 + tid] = k0 + sp[tid];
-      bool used = sp[tid] >= kbe;  // slot kbe+tid: first displacement of a position >= kbe
-      for (int m = 0; m < tid; ++m)
-        if (sp[m] == sp[tid]) used = false;
-      if (!used) {
-        mv[kbe + tid] = -1;
-        mv[2 * PKB + kbe + tid] = -1;
-      }
-    } else if (tid >= 2 * kbe && tid < 2 * PKB) {
+    const int nvac = __popc(~topmask & ((kbe < 32) ? ((1u << kbe) - 1u) : 0xffffffffu));
+    if (tid >= kbe + nvac && tid < 2 * PKB) {
       mv[tid] = -1;
       mv[2 * PKB + tid] = -1;
     }
-    if (tid == 0) {
-      args.pivstat[2 * node_id] = pmin;
-      args.pivstat[2 * node_id + 1] = pmax;
-    }
+  }
+  // running permutation: perm[k0 + fp] = old perm[k0 + r] for the moved rows
+  if constexpr (CL) cg::this_cluster().sync();
+  else __syncthreads();
+  int oldp = 0;
+  const bool moved = r < Ri && fp != r;
+  if (moved) oldp = perm[k0 + r];
+  if constexpr (CL) cg::this_cluster().sync();
+  else __syncthreads();
+  if (moved) perm[k0 + fp] = oldp;
+  if (crank == 0 && tid == 0) {
+    args.pivstat[2 * node_id] = pmin;
+    args.pivstat[2 * node_id + 1] = bad ? INFINITY : pmax;
   }
   if constexpr (CL) cg::this_cluster().sync();  // no CTA exits while others may still write its smem
 }

@@ -1,4 +1,5 @@
 // Root inverse helpers (G = S^{-1}, dense_nd.cpp:218-224) and small utilities.
+#include <algorithm>
 #include <cfloat>
 
 #include "common.cuh"
@@ -72,6 +73,96 @@ __global__ void copy2d_kernel(const double* __restrict__ src, int lds, double* d
     const int r = int(e % m), c = int(e / m);
     dst[r + (long long)c * ldd] = src[r + (long long)c * lds];
   }
+}
+
+// Inverses of the diagonal TB x TB blocks of the LU factors: Linv_k = L_kk^{-1}
+// (unit lower) and Uinv_k = U_kk^{-1}, one CTA per block, one thread per
+// column, block staged in shared memory. Output: full TB x TB blocks (zero
+// outside the triangle; identity padding for a partial last block).
+constexpr int TB = 128;
+__global__ void __launch_bounds__(TB) tri_inv_blocks_kernel(const double* __restrict__ LU, int ldlu, int n,
+                                                            double* __restrict__ out) {
+  extern __shared__ double blk[];  // TB x (TB+1)
+  const int kb = blockIdx.x, k0 = kb * TB, bk = min(TB, n - k0);
+  const int j = threadIdx.x;
+  for (int c = 0; c < TB; ++c) {
+    const int r = j;
+    blk[c * (TB + 1) + r] = (r < bk && c < bk) ? LU[(k0 + r) + (long long)(k0 + c) * ldlu] : (r == c ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  double* Li = out + (long long)kb * 2 * TB * TB;
+  double* Ui = Li + TB * TB;
+  // column j of L^{-1}: forward substitution with the unit lower triangle
+  {
+    double x[TB];
+#pragma unroll 1
+    for (int i = 0; i < TB; ++i) x[i] = 0.0;
+    // (register array with dynamic indexing lives in local memory; bounded by TB)
+    x[j] = 1.0;
+    for (int i = j + 1; i < TB; ++i) {
+      double s = 0.0;
+      for (int m = j; m < i; ++m) s = fma(blk[m * (TB + 1) + i], x[m], s);
+      x[i] = -s;
+    }
+    for (int i = 0; i < TB; ++i) Li[i + (long long)j * TB] = x[i];
+  }
+  // column j of U^{-1}: back substitution
+  {
+    double x[TB];
+    for (int i = 0; i < TB; ++i) x[i] = 0.0;
+    x[j] = 1.0 / blk[j * (TB + 1) + j];
+    for (int i = j - 1; i >= 0; --i) {
+      double s = 0.0;
+      for (int m = i + 1; m <= j; ++m) s = fma(blk[m * (TB + 1) + i], x[m], s);
+      x[i] = -s / blk[i * (TB + 1) + i];
+    }
+    for (int i = 0; i < TB; ++i) Ui[i + (long long)j * TB] = x[i];
+  }
+}
+
+__global__ void set_identity_kernel(double* X, int ldx, int n) {
+  const long long total = (long long)n * ldx;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int r = int(e % ldx), c = int(e / ldx);
+    X[e] = (r == c && r < n) ? 1.0 : 0.0;
+  }
+}
+
+// G[:, perm[i]] = W[:, i]  (A^{-1} = U^{-1} L^{-1} P)
+__global__ void permute_columns_kernel(const double* __restrict__ W, int ldw, const int* __restrict__ perm, int n,
+                                       double* __restrict__ G, int ldg) {
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    const double* src = W + (long long)i * ldw;
+    double* dst = G + (long long)perm[i] * ldg;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) dst[r] = src[r];
+  }
+}
+
+cudaError_t misc_init() {
+  return cudaFuncSetAttribute(tri_inv_blocks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              TB * (TB + 1) * sizeof(double));
+}
+
+cudaError_t launch_tri_inv_blocks(const double* LU, int ldlu, int n, double* out, cudaStream_t st) {
+  const int nblk = (n + TB - 1) / TB;
+  tri_inv_blocks_kernel<<<nblk, TB, TB * (TB + 1) * sizeof(double), st>>>(LU, ldlu, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_set_identity(double* X, int ldx, int n, cudaStream_t st) {
+  set_identity_kernel<<<1184, 256, 0, st>>>(X, ldx, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_permute_columns(const double* W, int ldw, const int* perm, int n, double* G, int ldg,
+                                   cudaStream_t st) {
+  permute_columns_kernel<<<std::min(n, 2048), 256, 0, st>>>(W, ldw, perm, n, G, ldg);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_perm_only(const int* d_ipiv, int n, int* d_perm, cudaStream_t st) {
+  perm_identity_kernel<<<1, 32, 0, st>>>(d_ipiv, n, d_perm, nullptr, 0);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_perm_identity(const int* d_ipiv, int n, int* d_perm, double* X, int ldx, cudaStream_t st) {

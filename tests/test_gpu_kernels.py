@@ -27,11 +27,11 @@ def test_full_lu_matches_scipy(n):
     rng = np.random.default_rng(n)
     A = rng.standard_normal((n, n))
     out, ipiv, ps = gpu_partial_lu(A, n)
-    # P A = L U with the GPU's row-swap sequence (partial pivoting; near-ties may
-    # resolve differently from LAPACK, so compare the factorization, not ipiv)
-    PA = A.copy()
-    for i, p in enumerate(ipiv):
-        PA[[i, p]] = PA[[p, i]]
+    # P A = L U with the GPU's row permutation perm[pos] = original row (partial
+    # pivoting; near-ties may resolve differently from LAPACK, so compare the
+    # factorization, not the pivot sequence)
+    assert sorted(ipiv.tolist()) == list(range(n))
+    PA = A[ipiv]
     Lm = np.tril(out, -1) + np.eye(n)
     Um = np.triu(out)
     assert np.max(np.abs(Lm)) <= 1.0 + 1e-12          # partial pivoting bound |l_ij| <= 1

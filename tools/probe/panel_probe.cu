@@ -7,8 +7,8 @@
 using namespace dtnb;
 int main() {
   blocked_init();
-  for (int kbv : {1, 2, 4, 8, 16, 32})
-  for (int rows : {64, 256, 2048}) {
+  for (int kbv : {32})
+  for (int rows : {2048, 256}) {
     const int n = rows, ld = (n + 7) / 8 * 8;
     NodeDev nd{};
     nd.kind = 2; nd.ni = n; nd.nb = 0; nd.total = n; nd.ld = nd.ldm = ld; nd.a = nd.b = -1;
@@ -39,11 +39,14 @@ int main() {
   }
   // empty-ish launch overhead reference
   {
-    long long h[128];
+    long long h[256];
     cudaMemcpyFromSymbol(h, g_panel_clk, sizeof(h));
-    for (int j = 0; j < 32; j += 4)
-      printf("col %2d: argmax+publish %lld  warp0+push+sync %lld  update %lld  (next start %lld)\n", j, h[j*4+1]-h[j*4+0],
-             h[j*4+2]-h[j*4+1], h[j*4+3]-h[j*4+2], j < 31 ? h[(j+1)*4]-h[j*4+3] : 0LL);
+    printf("phases: redux | publish | barrier | pivot-decide | rcp | update | rotate | next\n");
+    for (int j = 0; j < 32; j += 4) {
+      printf("col %2d:", j);
+      for (int q = 1; q < 8; ++q) printf(" %5lld", h[j*8+q]-h[j*8+q-1]);
+      printf(" %5lld\n", j < 31 ? h[(j+1)*8]-h[j*8+7] : 0LL);
+    }
   }
   printf("last error: %s\n", cudaGetErrorString(cudaGetLastError()));
 }
