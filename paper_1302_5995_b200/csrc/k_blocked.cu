@@ -319,19 +319,32 @@ __global__ void __launch_bounds__(RP_THREADS) rowpanel_kernel(KernelArgs args, c
   if (!left)
     for (int e = tid; e < kbe * kbe; e += RP_THREADS) T[e % kbe][e / kbe] = M[(k0 + e % kbe) + (k0 + e / kbe) * ld];
   __syncthreads();
-  for (int jj = warp; jj < RP_COLS; jj += RP_THREADS / 32) {
-    const int j = jbase + jj;
+  // a warp owns 4 columns: all gathers are issued first (one L2 round trip);
+  // slot i < kbe always moves a row into k0+i, so the top block is solved
+  // from registers (no store -> reload)
+  constexpr int CPW = RP_COLS / (RP_THREADS / 32);
+  const int d0 = s_dst[lane], d1 = s_dst[lane + 32];
+  const int s0 = s_src[lane], s1 = s_src[lane + 32];
+  double g0[CPW], g1[CPW];
+#pragma unroll
+  for (int q = 0; q < CPW; ++q) {
+    const int j = jbase + warp * CPW + q;
+    const double* col = M + (long long)j * ld;
+    g0[q] = (j < jend && d0 >= 0) ? col[s0] : 0.0;
+    g1[q] = (j < jend && d1 >= 0) ? col[s1] : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < CPW; ++q) {
+    const int j = jbase + warp * CPW + q;
     if (j >= jend) break;
     double* col = M + (long long)j * ld;
-    const int d0 = s_dst[lane], d1 = s_dst[lane + 32];
-    const double v0 = d0 >= 0 ? col[s_src[lane]] : 0.0;
-    const double v1 = d1 >= 0 ? col[s_src[lane + 32]] : 0.0;
-    __syncwarp();
-    if (d0 >= 0) col[d0] = v0;
-    if (d1 >= 0) col[d1] = v1;
-    __syncwarp();
-    if (left) continue;
-    double x = lane < kbe ? col[k0 + lane] : 0.0;
+    if (d1 >= 0) col[d1] = g1[q];
+    if (left) {
+      if (d0 >= 0) col[d0] = g0[q];
+      continue;
+    }
+    if (d0 >= 0 && lane >= kbe) col[d0] = g0[q];
+    double x = lane < kbe ? g0[q] : 0.0;
     for (int c = 0; c < kbe; ++c) {  // unit lower L11
       const double xc = __shfl_sync(0xffffffffu, x, c);
       if (lane > c && lane < kbe) x = fma(-T[lane][c], xc, x);
