@@ -23,6 +23,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <numbers>
@@ -47,6 +48,11 @@ void scipy_dgemm_64_(const char* ta, const char* tb, const int64_t* m, const int
                      const int64_t* k, const double* alpha, const double* a, const int64_t* lda,
                      const double* b, const int64_t* ldb, const double* beta, double* c,
                      const int64_t* ldc, size_t, size_t);
+void scipy_dtrsm_64_(const char* side, const char* uplo, const char* transa, const char* diag, const int64_t* m,
+                     const int64_t* n, const double* alpha, const double* a, const int64_t* lda, double* b,
+                     const int64_t* ldb, size_t, size_t, size_t, size_t);
+void scipy_dlaswp_64_(const int64_t* n, double* a, const int64_t* lda, const int64_t* k1, const int64_t* k2,
+                      const int64_t* ipiv, const int64_t* incx);
 void scipy_openblas_set_num_threads64_(int);
 int scipy_openblas_get_num_threads64_(void);
 }
@@ -450,8 +456,18 @@ SchurData merge_two(const SchurData& a, const SchurData& b, const Operator& op, 
   }
   if (!(pmin > pmax * 1e-300) || !std::isfinite(pmax))  // dense_nd.cpp:175-180
     throw FactorizationError("interface block is singular", box_label(level, box));
-  scipy_dgetrs_64_("N", &n64, &nrhs, mii.a.data(), &n64, ipiv.data(), mib.a.data(), &n64, &info, 1);
-  gemm_sub(mbi, mib, mbb);
+  static const bool left_assoc = std::getenv("ORC_RIGHT_LOOKING_ASSOC") != nullptr;
+  if (!left_assoc) {  // reference association: S = M_bb - M_bi (U^-1 L^-1 P M_ib)
+    scipy_dgetrs_64_("N", &n64, &nrhs, mii.a.data(), &n64, ipiv.data(), mib.a.data(), &n64, &info, 1);
+    gemm_sub(mbi, mib, mbb);
+  } else {  // diagnostic: S = M_bb - (M_bi U^-1)(L^-1 P M_ib), the right-looking association
+    const int64_t one = 1, nb64 = nb;
+    const double alpha = 1.0;
+    scipy_dlaswp_64_(&nrhs, mib.a.data(), &n64, &one, &n64, ipiv.data(), &one);
+    scipy_dtrsm_64_("L", "L", "N", "U", &n64, &nrhs, &alpha, mii.a.data(), &n64, mib.a.data(), &n64, 1, 1, 1, 1);
+    scipy_dtrsm_64_("R", "U", "N", "N", &nb64, &n64, &alpha, mii.a.data(), &n64, mbi.a.data(), &nb64, 1, 1, 1, 1);
+    gemm_sub(mbi, mib, mbb);
+  }
   out.S = std::move(mbb);
   return out;
 }

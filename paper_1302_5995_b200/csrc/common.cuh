@@ -27,6 +27,24 @@ struct GemmDesc {  // C(m x n) = beta*C + alpha*A(m x k)*B(k x n), column-major
   int m, n, k, lda, ldb, ldc;
 };
 
+struct TriDesc {  // inverses of the 128 x 128 diagonal blocks of U of an n x n LU
+  const double* LU;
+  double* out;
+  int ld, n;
+};
+
+struct TrsmDesc {  // Y(bk x ncols) <- U^{-1} Y, U a bk x bk upper triangle (bk <= 128)
+  const double* U;
+  double* Y;
+  int ldu, ldy, bk, ncols;
+};
+
+struct CopyDesc {
+  const double* src;
+  double* dst;
+  int lds, ldd, m, n;
+};
+
 struct KernelArgs {
   const NodeDev* nodes;
   const PosDev* pos;

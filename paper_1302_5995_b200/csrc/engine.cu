@@ -28,8 +28,11 @@ cudaError_t launch_small_elim(const KernelArgs&, const int*, int, int, bool, cud
 cudaError_t launch_gather(const KernelArgs&, const int*, int, int, cudaStream_t);
 cudaError_t launch_panel(const KernelArgs&, const int*, int, int, int, int, cudaStream_t);
 cudaError_t launch_rowpanel(const KernelArgs&, const int*, int, int, int, int, int, bool, cudaStream_t);
-cudaError_t launch_trailing_update(const KernelArgs&, const int*, int, int, int, int, int, int, cudaStream_t);
-cudaError_t launch_gemm_desc(const GemmDesc*, int, int, int, double, double, cudaStream_t);
+cudaError_t launch_trailing_update(const KernelArgs&, const int*, int, int, int, int, int, int, cudaStream_t, int);
+cudaError_t launch_tri_inv_u_batched(const void*, int, int, cudaStream_t);
+cudaError_t launch_copy2d_batched(const void*, int, cudaStream_t);
+cudaError_t launch_trsm_upper_batched(const void*, int, int, cudaStream_t);
+cudaError_t launch_gemm_desc(const GemmDesc*, int, int, int, double, double, cudaStream_t, bool);
 cudaError_t launch_perm_identity(const int*, int, int*, double*, int, cudaStream_t);
 cudaError_t launch_trsm_rows(const double*, int, double*, int, int, int, int, bool, cudaStream_t);
 cudaError_t launch_norm1(const double*, int, int, int, unsigned long long*, cudaStream_t);
@@ -66,9 +69,9 @@ int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 constexpr int kSmallMax = 160;
 constexpr int kDefaultMicro = 64;
 
-// Panel width; the register-resident panel spans up to 16 CTAs x 256 rows.
+// Panel width; the register-resident panel spans up to 16 CTAs x 512 rows.
 int panel_kb(int rows) {
-  if (rows > 16 * 256) throw std::invalid_argument("dense merge system too large for the cluster panel (> 4096 rows)");
+  if (rows > 16 * 512) throw std::invalid_argument("dense merge system too large for the cluster panel (> 8192 rows)");
   return 32;
 }
 
@@ -78,6 +81,15 @@ struct WaveLaunch {
   int blk_off = 0, blk_cnt = 0, blk_max_total = 0, blk_max_ni = 0, blk_max_nb = 0, kb = 32;
   int level = -1;  // reference level of its tree merges, -1 for in-leaf waves
   double flops = 0.0;
+  // Schur-form back substitution X = U^{-1} Y and S -= M_bi X (descriptor ranges)
+  int tri_off = 0, tri_blocks = 0;                 // TriDesc range (one per blocked merge)
+  std::vector<int> bs_off, bs_cnt;                 // per back-substitution step: GemmDesc pairs / CopyDesc
+  std::vector<int> bs_toff, bs_soff, bs_tiles1, bs_tiles2, bs_k, bs_cols;  // launch geometry per step
+  std::vector<double> bs_flops;
+  int copy_base = 0;                               // first CopyDesc of this wave
+  int fin_off = 0, fin_tiles = 0, fin_k = 0;       // final GEMM S -= M_bi X
+  bool fin_aligned = true;
+  double fin_flops = 0.0;
 };
 
 template <class T>
@@ -114,6 +126,15 @@ struct PlanDev {
   unsigned long long* d_norm = nullptr;
   GemmDesc* d_inv_descs = nullptr;
   std::vector<GemmDesc> h_inv_descs;
+  std::vector<GemmDesc> h_bs_gemm;  // arena offsets until relocated
+  std::vector<CopyDesc> h_bs_copy;
+  std::vector<TriDesc> h_tri;
+  std::vector<TrsmDesc> h_trs;
+  int subst_base = 0;
+  TrsmDesc* d_trs = nullptr;
+  GemmDesc* d_bs_gemm = nullptr;  // back-substitution / final GEMM descriptors (all waves)
+  CopyDesc* d_bs_copy = nullptr;
+  TriDesc* d_tri = nullptr;
   double* d_W = nullptr;     // U^{-1} L^{-1} before the column permutation
   double* d_T = nullptr;     // 128 x nb staging block of the triangular sweeps
   double* d_tinv = nullptr;  // inverses of the 128 x 128 diagonal blocks of L and U
@@ -134,7 +155,8 @@ struct PlanDev {
       if (e) cudaEventDestroy(e);
     if (side) cudaStreamDestroy(side);
     for (void* p : std::initializer_list<void*>{d_nodes, d_pos, d_arena, d_piv, d_pivstat, d_lists, d_stencil, d_S, d_G,
-                                                d_perm, d_norm, d_inv_descs, d_W, d_T, d_tinv})
+                                                d_perm, d_norm, d_inv_descs, d_W, d_T, d_tinv, d_bs_gemm,
+                                                d_bs_copy, d_tri, d_trs})
       if (p) cudaFree(p);
     if (h_pivstat) cudaFreeHost(h_pivstat);
     if (h_norm) cudaFreeHost(h_norm);
@@ -230,6 +252,96 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
     for (int id : wv.blocked) L.flops += merge_flop_count(P.nodes[id].ni, P.nodes[id].nb);
     for (int id : wv.micro) L.flops += merge_flop_count(P.nodes[id].ni, P.nodes[id].nb);
   }
+  // Schur-form descriptors: X = U^{-1} Y by 128-row blocks from the bottom
+  // (T = Uinv_k Y_k; Y_top -= U_top,k T; Y_k = T), then S -= M_bi X.
+  {
+    std::vector<GemmDesc> gd;
+    std::vector<CopyDesc> cd;
+    std::vector<TriDesc> td;
+    std::vector<TrsmDesc> trs;
+    std::vector<GemmDesc> gs;  // substitution variant's updates (appended after gd)
+    double* A0 = nullptr;  // descriptors hold absolute pointers into the arena (allocated below)
+    (void)A0;
+    for (size_t w = 0; w < P.waves.size(); ++w) {
+      WaveLaunch& L = D->wl[w];
+      const Wave& wv = P.waves[w];
+      if (wv.blocked.empty()) continue;
+      L.tri_off = int(td.size());
+      int maxblk = 0;
+      for (int id : wv.blocked) {
+        const Node& nd = P.nodes[id];
+        td.push_back(TriDesc{reinterpret_cast<const double*>(nd.m_off), reinterpret_cast<double*>(nd.uinv_off), nd.ldm,
+                             nd.ni});
+        maxblk = std::max(maxblk, (nd.ni + 127) / 128);
+      }
+      L.tri_blocks = maxblk;
+      L.copy_base = int(cd.size());
+      for (int t = 0; t < maxblk; ++t) {
+        const int off = int(gd.size()), toff = int(trs.size()), soff = int(gs.size());
+        int cnt = 0, t1 = 0, t2 = 0, kk = 0, mc = 0;
+        double fl = 0.0;
+        std::vector<GemmDesc> g2;
+        for (int id : wv.blocked) {
+          const Node& nd = P.nodes[id];
+          const int nblk = (nd.ni + 127) / 128;
+          const int sblk = nblk - 1 - t;
+          if (sblk < 0) continue;
+          const int64_t M = nd.m_off, ldm = nd.ldm;
+          const int k0 = sblk * 128, k1 = std::min(nd.ni, k0 + 128), bk = k1 - k0;
+          // substitution variant: Y_k <- U_kk^{-1} Y_k in place, Y[0:k0] -= U[0:k0, k0:k1] Y_k
+          trs.push_back(TrsmDesc{reinterpret_cast<const double*>(M + k0 + int64_t(k0) * ldm),
+                                 reinterpret_cast<double*>(M + k0 + nd.ni * ldm), int(ldm), int(ldm), bk, nd.nb});
+          gs.push_back(GemmDesc{reinterpret_cast<const double*>(M + int64_t(k0) * ldm),
+                                reinterpret_cast<const double*>(M + k0 + nd.ni * ldm),
+                                reinterpret_cast<double*>(M + nd.ni * ldm), k0, nd.nb, bk, int(ldm), int(ldm), int(ldm)});
+          // default (explicit block inverse): T = Uinv_k Y_k; Y[0:k0] -= U[0:k0, k0:k1] T; Y_k = T
+          const int64_t uinv = nd.uinv_off + int64_t(sblk) * 2 * 128 * 128 + 128 * 128;
+          gd.push_back(GemmDesc{reinterpret_cast<const double*>(uinv),
+                                reinterpret_cast<const double*>(M + k0 + nd.ni * ldm),
+                                reinterpret_cast<double*>(nd.t_off), bk, nd.nb, bk, 128, int(ldm), 128});
+          g2.push_back(GemmDesc{reinterpret_cast<const double*>(M + int64_t(k0) * ldm),
+                                reinterpret_cast<const double*>(nd.t_off), reinterpret_cast<double*>(M + nd.ni * ldm), k0,
+                                nd.nb, bk, int(ldm), 128, int(ldm)});
+          cd.push_back(CopyDesc{reinterpret_cast<const double*>(nd.t_off),
+                                reinterpret_cast<double*>(M + k0 + nd.ni * ldm), 128, int(ldm), bk, nd.nb});
+          t1 = std::max(t1, gemm_tiles(bk, nd.nb));
+          t2 = std::max(t2, gemm_tiles(std::max(k0, 1), nd.nb));
+          kk = std::max(kk, bk);
+          mc = std::max(mc, nd.nb);
+          fl += double(bk) * bk * nd.nb + 2.0 * k0 * double(nd.nb) * bk;
+          ++cnt;
+        }
+        gd.insert(gd.end(), g2.begin(), g2.end());
+        L.bs_off.push_back(off);
+        L.bs_soff.push_back(soff);
+        L.bs_tiles1.push_back(t1);
+        L.bs_toff.push_back(toff);
+        L.bs_cnt.push_back(cnt);
+        L.bs_tiles2.push_back(t2);
+        L.bs_k.push_back(kk);
+        L.bs_cols.push_back(mc);
+        L.bs_flops.push_back(fl);
+      }
+      L.fin_off = int(gd.size());
+      for (int id : wv.blocked) {
+        const Node& nd = P.nodes[id];
+        const int64_t M = nd.m_off, ldm = nd.ldm;
+        gd.push_back(GemmDesc{reinterpret_cast<const double*>(M + nd.ni), reinterpret_cast<const double*>(M + nd.ni * ldm),
+                              reinterpret_cast<double*>(M + nd.ni + nd.ni * ldm), nd.nb, nd.nb, nd.ni, int(ldm), int(ldm),
+                              int(ldm)});
+        L.fin_tiles = std::max(L.fin_tiles, gemm_tiles(nd.nb, nd.nb));
+        L.fin_k = std::max(L.fin_k, nd.ni);
+        L.fin_aligned = L.fin_aligned && (nd.ni % 2 == 0);
+        L.fin_flops += 2.0 * nd.nb * double(nd.nb) * nd.ni;
+      }
+    }
+    D->h_trs = std::move(trs);
+    D->subst_base = int(gd.size());
+    gd.insert(gd.end(), gs.begin(), gs.end());
+    D->h_bs_gemm = std::move(gd);
+    D->h_bs_copy = std::move(cd);
+    D->h_tri = std::move(td);
+  }
   D->root_list_off = int(lists.size());
   lists.push_back(D->root_lu_node);
   D->h_lists = lists;
@@ -243,6 +355,26 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
   CK(cudaMemcpy(D->d_lists, lists.data(), lists.size() * sizeof(int), cudaMemcpyHostToDevice));
   D->d_arena = dalloc<double>(size_t(D->lu_off + int64_t(D->ldlu) * nb));
   D->d_piv = dalloc<int>(size_t(P.piv_ints + align_up(nb, 4) + 128));
+  {  // relocate the Schur-form descriptors (stored as arena offsets) and upload
+    double* base = D->d_arena;
+    auto rel = [&](auto* p) { return reinterpret_cast<decltype(p)>(base + reinterpret_cast<int64_t>(p)); };
+    for (auto& g : D->h_bs_gemm) { g.A = rel(g.A); g.B = rel(g.B); g.C = rel(g.C); }
+    for (auto& c : D->h_bs_copy) { c.src = rel(c.src); c.dst = rel(c.dst); }
+    for (auto& t : D->h_tri) { t.LU = rel(t.LU); t.out = rel(t.out); }
+    for (auto& t : D->h_trs) { t.U = rel(t.U); t.Y = rel(t.Y); }
+    D->d_trs = dalloc<TrsmDesc>(D->h_trs.size());
+    if (!D->h_trs.empty())
+      CK(cudaMemcpy(D->d_trs, D->h_trs.data(), D->h_trs.size() * sizeof(TrsmDesc), cudaMemcpyHostToDevice));
+    D->d_bs_gemm = dalloc<GemmDesc>(D->h_bs_gemm.size());
+    D->d_bs_copy = dalloc<CopyDesc>(D->h_bs_copy.size());
+    D->d_tri = dalloc<TriDesc>(D->h_tri.size());
+    if (!D->h_bs_gemm.empty())
+      CK(cudaMemcpy(D->d_bs_gemm, D->h_bs_gemm.data(), D->h_bs_gemm.size() * sizeof(GemmDesc), cudaMemcpyHostToDevice));
+    if (!D->h_bs_copy.empty())
+      CK(cudaMemcpy(D->d_bs_copy, D->h_bs_copy.data(), D->h_bs_copy.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
+    if (!D->h_tri.empty())
+      CK(cudaMemcpy(D->d_tri, D->h_tri.data(), D->h_tri.size() * sizeof(TriDesc), cudaMemcpyHostToDevice));
+  }
   D->d_pivstat = dalloc<double>(2 * D->h_nodes.size());
   D->d_stencil = dalloc<double>(size_t(5 * D->nu));
   D->lds = int(align_up(nb, 8));
@@ -291,6 +423,11 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
   return D;
 }
 
+bool use_subst() {  // default: substitution (DTN_BACKSUB_SUBST=0 selects the explicit block inverses)
+  const char* e = std::getenv("DTN_BACKSUB_SUBST");
+  return !(e && e[0] == '0');
+}
+
 bool use_lookahead() {
   const char* e = std::getenv("DTN_NO_LOOKAHEAD");
   return !(e && e[0] == '1');
@@ -298,10 +435,13 @@ bool use_lookahead() {
 
 // Per-launch profiler (opts.profile): CUDA events around every launch,
 // aggregated per kernel class with the algorithmic work of each launch.
-enum KClass { K_SMALL = 0, K_GATHER, K_PANEL, K_ROWPANEL, K_TRAILING, K_COPY, K_INV_TRSM, K_INV_GEMM, K_MISC, K_COUNT };
+enum KClass {
+  K_SMALL = 0, K_GATHER, K_PANEL, K_ROWPANEL, K_TRAILING, K_BACKSUB, K_SCHUR, K_COPY, K_INV_TRSM, K_INV_GEMM, K_MISC,
+  K_COUNT
+};
 const char* kclass_name(int k) {
-  static const char* names[K_COUNT] = {"small_elim", "gather", "panel", "rowpanel", "trailing_gemm",
-                                       "copy",       "inv_trsm", "inv_gemm", "misc"};
+  static const char* names[K_COUNT] = {"small_elim", "gather",   "panel",    "rowpanel", "trailing_gemm", "backsub_gemm",
+                                       "schur_gemm", "copy",     "inv_trsm", "inv_gemm", "misc"};
   return names[k];
 }
 struct Prof {
@@ -344,8 +484,16 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
   // panel(k) + rowpanel(k), the update of the next panel's columns runs on the
   // main stream (so panel(k+1) starts at once) while the rest of the trailing
   // update runs concurrently on the side stream; rowpanel(k+1) joins it.
+  // schur: eliminate the interface rows only (trailing updates restricted to
+  // rows [k1, ni), no boundary-row multipliers): leaves L\U of M_ii and
+  // Y = L^{-1} P M_ib; the Schur complement is formed afterwards as
+  // S = M_bb - M_bi (U^{-1} Y), the reference's association (dense_nd.cpp:181),
+  // which is markedly more accurate than (M_bi U^{-1}) Y for the near-resonant
+  // interface blocks of the Helmholtz configurations.
   auto blocked_lu = [&](const int* lst, const int* hlst, int cnt, int max_ni, int max_total, int max_nb, int kb,
-                        bool swap_left) {
+                        bool swap_left, bool schur) {
+    const int rows_lim = schur ? max_ni : 0;
+    const int nb_rows = schur ? 0 : max_nb;
     bool pending = false;
     for (int k0 = 0; k0 < max_ni; k0 += kb) {
       double fp = 0.0, fr = 0.0, fn_ = 0.0, fr_ = 0.0;
@@ -354,29 +502,31 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
         const double ni = ndp ? ndp->ni : max_ni, nbn = ndp ? ndp->nb : max_nb, tot = ndp ? ndp->total : max_total;
         if (k0 >= ni) continue;
         const double kbe = std::min<double>(kb, ni - k0), mn = tot - k0 - kbe;
+        const double mr = schur ? ni - k0 - kbe : mn;  // rows of the trailing update
         fp += (ni - k0) * kbe * kbe;
-        fr += kbe * kbe * (nbn + mn);
+        fr += kbe * kbe * ((schur ? 0.0 : nbn) + mn);
         const double nn = std::min<double>(mn, kb);
-        fn_ += 2.0 * mn * nn * kbe;
-        fr_ += 2.0 * mn * (mn - nn) * kbe;
+        fn_ += 2.0 * mr * nn * kbe;
+        fr_ += 2.0 * mr * (mn - nn) * kbe;
       }
       const bool more = k0 + kb < max_ni;
       run(K_PANEL, fp, 0.0, [&] { return launch_panel(a, lst, cnt, max_ni - k0, k0, kb, st); });
       if (pending) CK(cudaStreamWaitEvent(st, D.ev_rest, 0));
       run(K_ROWPANEL, fr, 0.0,
-          [&] { return launch_rowpanel(a, lst, cnt, max_total, max_nb, k0, kb, swap_left, st); });
+          [&] { return launch_rowpanel(a, lst, cnt, max_total, nb_rows, k0, kb, swap_left, st); });
       if (more && use_lookahead()) {
         CK(cudaEventRecord(D.ev_rp, st));
         CK(cudaStreamWaitEvent(st2, D.ev_rp, 0));
         run(K_TRAILING, fn_, 0.0,
-            [&] { return launch_trailing_update(a, lst, cnt, max_total, k0, kb, 0, kb, st); });
-        run_on(st2, K_TRAILING, fr_, 0.0,
-               [&] { return launch_trailing_update(a, lst, cnt, max_total, k0, kb, kb, 1 << 30, st2); });
+            [&] { return launch_trailing_update(a, lst, cnt, max_total, k0, kb, 0, kb, st, rows_lim); });
+        run_on(st2, K_TRAILING, fr_, 0.0, [&] {
+          return launch_trailing_update(a, lst, cnt, max_total, k0, kb, kb, 1 << 30, st2, rows_lim);
+        });
         CK(cudaEventRecord(D.ev_rest, st2));
         pending = true;
       } else {
         run(K_TRAILING, fn_ + fr_, 0.0,
-            [&] { return launch_trailing_update(a, lst, cnt, max_total, k0, kb, 0, 1 << 30, st); });
+            [&] { return launch_trailing_update(a, lst, cnt, max_total, k0, kb, 0, 1 << 30, st, rows_lim); });
         pending = false;
       }
     }
@@ -405,7 +555,40 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
       double gb = 0.0;
       for (int i = 0; i < L.blk_cnt; ++i) gb += 16.0 * double(P.nodes[hlst[i]].total) * P.nodes[hlst[i]].total;
       run(K_GATHER, 0.0, gb, [&] { return launch_gather(a, lst, L.blk_cnt, L.blk_max_total, st); });
-      blocked_lu(lst, hlst, L.blk_cnt, L.blk_max_ni, L.blk_max_total, L.blk_max_nb, L.kb, false);
+      blocked_lu(lst, hlst, L.blk_cnt, L.blk_max_ni, L.blk_max_total, L.blk_max_nb, L.kb, false, true);
+      // X = U^{-1} Y by 128-row blocks from the bottom: dtrsm-style
+      // substitution on the diagonal blocks (default; as accurate as the
+      // reference on the near-resonant configurations) or explicit block
+      // inverses (DTN_BACKSUB_SUBST=0; GEMM only), then S = M_bb - M_bi X
+      if (!use_subst()) {
+        run(K_INV_TRSM, 0.0, 0.0,
+            [&] { return launch_tri_inv_u_batched(D.d_tri + L.tri_off, L.blk_cnt, L.tri_blocks, st); });
+      }
+      int coff = L.copy_base;
+      for (size_t t = 0; t < L.bs_off.size(); ++t) {
+        const int off = L.bs_off[t], cnt = L.bs_cnt[t];
+        if (use_subst()) {
+          run(K_BACKSUB, 0.0, 0.0,
+              [&] { return launch_trsm_upper_batched(D.d_trs + L.bs_toff[t], cnt, L.bs_cols[t], st); });
+          run(K_BACKSUB, L.bs_flops[t], 0.0, [&] {
+            return launch_gemm_desc(D.d_bs_gemm + D.subst_base + L.bs_soff[t], cnt, L.bs_tiles2[t], L.bs_k[t], -1.0,
+                                    1.0, st, true);
+          });
+        } else {
+          run(K_BACKSUB, 0.0, 0.0, [&] {
+            return launch_gemm_desc(D.d_bs_gemm + off, cnt, L.bs_tiles1[t], L.bs_k[t], 1.0, 0.0, st, true);
+          });
+          run(K_BACKSUB, L.bs_flops[t], 0.0, [&] {
+            return launch_gemm_desc(D.d_bs_gemm + off + cnt, cnt, L.bs_tiles2[t], L.bs_k[t], -1.0, 1.0, st, true);
+          });
+          run(K_COPY, 0.0, 0.0, [&] { return launch_copy2d_batched(D.d_bs_copy + coff, cnt, st); });
+        }
+        coff += cnt;
+      }
+      run(K_SCHUR, L.fin_flops, 0.0, [&] {
+        return launch_gemm_desc(D.d_bs_gemm + L.fin_off, L.blk_cnt, L.fin_tiles, L.fin_k, -1.0, 1.0, st,
+                                L.fin_aligned);
+      });
     }
     if (events) CK(cudaEventRecord(D.ev_wave[w], st));
   }
@@ -420,7 +603,7 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
     double* LU = D.d_arena + D.lu_off;
     run(K_COPY, 0.0, 16.0 * nb2, [&] { return launch_copy2d(D.d_S, D.lds, LU, D.ldlu, nb, nb, st); });
     const int* rl = D.d_lists + D.root_list_off;
-    blocked_lu(rl, nullptr, 1, nb, nb, 0, D.root_kb, true);
+    blocked_lu(rl, nullptr, 1, nb, nb, 0, D.root_kb, true, false);
     // the panels maintain perm[pos] = original row of the root LU (P A = L U)
     const int* perm = D.d_piv + D.h_nodes[D.root_lu_node].piv_off;
     run(K_INV_TRSM, double(nb) * 128 * 128, 0.0, [&] { return launch_tri_inv_blocks(LU, D.ldlu, nb, D.d_tinv, st); });
@@ -430,7 +613,7 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
       const GemmDesc& g = D.h_inv_descs[di];
       if (g.m <= 0 || g.n <= 0) return;
       run(K_INV_GEMM, 2.0 * g.m * g.n * g.k, 0.0, [&] {
-        return launch_gemm_desc(D.d_inv_descs + di, 1, gemm_tiles(g.m, g.n), g.k, alpha, beta, st);
+        return launch_gemm_desc(D.d_inv_descs + di, 1, gemm_tiles(g.m, g.n), g.k, alpha, beta, st, true);
       });
     };
     for (int kb_ = 0; kb_ < nblk; ++kb_) {
@@ -806,7 +989,7 @@ int dtn_gpu_apply(const dtn_op* op, int which, const double* X, int64_t ldx, int
     }
     GemmDesc d{A, dX, dY, nb, int(batch), nb, lda, int(ldX), int(ldY)};
     CK(cudaMemcpyAsync(ctx->d_desc, &d, sizeof(d), cudaMemcpyHostToDevice, st));
-    CK(launch_gemm_desc(ctx->d_desc, 1, gemm_tiles(nb, int(batch)), nb, 1.0, 0.0, st));
+    CK(launch_gemm_desc(ctx->d_desc, 1, gemm_tiles(nb, int(batch)), nb, 1.0, 0.0, st, true));
     if (!aligned)
       CK(cudaMemcpy2DAsync(Y, size_t(ldy) * 8, dY, size_t(ldY) * 8, size_t(nb) * 8, size_t(batch),
                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
@@ -894,7 +1077,7 @@ int dtn_debug_partial_lu(int32_t n, int32_t ni, const double* A, double* out, in
     for (int k0 = 0; k0 < ni; k0 += 32) {
       CK(launch_panel(a, d_list, 1, ni - k0, k0, 32, 0));
       CK(launch_rowpanel(a, d_list, 1, n, n - ni, k0, 32, ni == n, 0));
-      CK(launch_trailing_update(a, d_list, 1, n, k0, 32, 0, 1 << 30, 0));
+      CK(launch_trailing_update(a, d_list, 1, n, k0, 32, 0, 1 << 30, 0, 0));
     }
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy2D(out, size_t(n) * 8, d_a, size_t(ld) * 8, size_t(n) * 8, n, cudaMemcpyDeviceToHost));

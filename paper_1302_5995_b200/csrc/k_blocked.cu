@@ -86,13 +86,13 @@ struct PanelCand {
 // order (pivot rows to positions [0, kbe), displaced top rows into the
 // vacated positions) is applied once at the end, and published as the net
 // row-move list + the node's running permutation perm[pos] = original row.
-template <bool CL>
+template <bool CL, int RPT>
 __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* __restrict__ list, int k0, int kb,
                                                    int csize) {
   // row slots: [0, PNW) warp candidates, PNW + q = candidate of cluster rank q
   constexpr int SC = PNW, NSLOT = PNW + (CL ? PMAXC : 0);
   __shared__ __align__(16) double rows[2][NSLOT][PKB];
-  __shared__ unsigned skey[2][NSLOT];
+  __shared__ unsigned skey[2][NSLOT], sklo[2][NSLOT];
   __shared__ int spos[2][NSLOT];
   __shared__ int sp[PKB], vac[PKB];
   const int crank = CL ? int(cg::this_cluster().block_rank()) : 0;
@@ -106,18 +106,22 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
   double* M = args.arena + nd.m_off + k0 + (long long)k0 * nd.ldm;
   const long long ldm = nd.ldm;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int r = crank * PNT + tid;  // this thread's row in the panel (original position)
+  const int stride = csize * PNT;
   int* perm = args.piv + nd.piv_off;  // running permutation of the interface rows
 
-  double v[PKB];
+  double v[RPT][PKB];
+  int elim[RPT];
 #pragma unroll
-  for (int c = 0; c < PKB; ++c) v[c] = (r < Ri && c < kbe) ? M[r + c * ldm] : 0.0;
-  int elim = (r < Ri) ? -1 : PKB;  // step at which this row became a pivot
+  for (int a = 0; a < RPT; ++a) {
+    const int r = crank * PNT + tid + stride * a;  // original panel row
+#pragma unroll
+    for (int c = 0; c < PKB; ++c) v[a][c] = (r < Ri && c < kbe) ? M[r + c * ldm] : 0.0;
+    elim[a] = (r < Ri) ? -1 : PKB;  // step at which this row became a pivot
+    if (k0 == 0 && r < Ri) perm[r] = r;
+  }
   double pmin = k0 == 0 ? DBL_MAX : args.pivstat[2 * node_id];
   double pmax = k0 == 0 ? 0.0 : args.pivstat[2 * node_id + 1];
   bool bad = false;
-  const int pperm0 = (k0 == 0 && r < Ri) ? r : 0;
-  if (k0 == 0 && r < Ri) perm[r] = pperm0;
 
 #pragma unroll
   for (int j = 0; j < PKB; ++j) {
@@ -126,21 +130,37 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
     PCLK(0);
 #endif
     const int buf = j & 1;
-    // ---- warp argmax of |column j| over the live rows: 32-bit key = high
-    // word of |x| (sign 0, exponent, 20 mantissa bits; NaN ranks highest),
-    // low bit set for candidates; hardware warp max + ballot, ties -> lowest row
-    unsigned key = 0u;
-    if (elim < 0) key = (unsigned(__double2hiint(fabs(v[j]))) | 1u);
-    const unsigned wkey = __reduce_max_sync(0xffffffffu, key);
-    const int wlane = __ffs(__ballot_sync(0xffffffffu, key == wkey)) - 1;
+    // ---- argmax of |column j| over the live rows: 32-bit key = high word of
+    // |x| (sign 0, exponent, 20 mantissa bits; NaN ranks highest), low bit
+    // set for candidates; hardware warp max + ballot, ties -> lowest lane
+    // exact argmax: max of the high words, then of the low words among the
+    // lanes holding that high word (|x| >= 0 orders like its bit pattern)
+    unsigned key = 0u, klo = 0u;
+    int ba = 0;
+#pragma unroll
+    for (int a = 0; a < RPT; ++a) {
+      const double ax = fabs(v[a][j]);
+      const unsigned ka = elim[a] < 0 ? (unsigned(__double2hiint(ax)) | 0x80000000u) : 0u;
+      const unsigned kl = unsigned(__double2loint(ax));
+      if (ka > key || (ka == key && kl > klo)) { key = ka; klo = kl; ba = a; }
+    }
+    const unsigned whi = __reduce_max_sync(0xffffffffu, key);
+    const unsigned wlo = __reduce_max_sync(0xffffffffu, key == whi ? klo : 0u);
+    const int wlane = __ffs(__ballot_sync(0xffffffffu, key == whi && klo == wlo)) - 1;
+    const unsigned wkey = whi;
 #ifdef DTN_PANEL_PROFILE
     PCLK(1);
 #endif
     if (lane == wlane) {
 #pragma unroll
-      for (int c = j; c < PKB; ++c) rows[buf][warp][c] = v[c];
+      for (int a = 0; a < RPT; ++a)
+        if (a == ba) {
+#pragma unroll
+          for (int c = j; c < PKB; ++c) rows[buf][warp][c] = v[a][c];
+        }
       skey[buf][warp] = wkey;
-      spos[buf][warp] = r;
+      sklo[buf][warp] = wlo;
+      spos[buf][warp] = crank * PNT + tid + stride * ba;
     }
 #ifdef DTN_PANEL_PROFILE
     PCLK(2);
@@ -151,8 +171,10 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
 #endif
     // ---- CTA argmax (every warp, redundantly)
     const unsigned lk = lane < PNW ? skey[buf][lane] : 0u;
+    const unsigned ll = lane < PNW ? sklo[buf][lane] : 0u;
     const unsigned bkey = __reduce_max_sync(0xffffffffu, lk);
-    const int bw = __ffs(__ballot_sync(0xffffffffu, lk == bkey && lane < PNW)) - 1;
+    const unsigned blo = __reduce_max_sync(0xffffffffu, lk == bkey ? ll : 0u);
+    const int bw = __ffs(__ballot_sync(0xffffffffu, lk == bkey && ll == blo && lane < PNW)) - 1;
     int slot = bw, p = spos[buf][bw];
     if constexpr (CL) {
       // warp 0 pushes this CTA's candidate into every CTA of the cluster
@@ -163,14 +185,17 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
           if (lane >= j) cl.map_shared_rank(&rows[buf][SC + crank][0], d)[lane] = rv;
           if (lane == 0) {
             *cl.map_shared_rank(&skey[buf][SC + crank], d) = bkey;
+            *cl.map_shared_rank(&sklo[buf][SC + crank], d) = blo;
             *cl.map_shared_rank(&spos[buf][SC + crank], d) = p;
           }
         }
       }
       cg::this_cluster().sync();
       const unsigned ck = lane < csize ? skey[buf][SC + lane] : 0u;
+      const unsigned cl_ = lane < csize ? sklo[buf][SC + lane] : 0u;
       const unsigned gkey = __reduce_max_sync(0xffffffffu, ck);
-      const int cw = __ffs(__ballot_sync(0xffffffffu, ck == gkey && lane < csize)) - 1;
+      const unsigned glo = __reduce_max_sync(0xffffffffu, ck == gkey ? cl_ : 0u);
+      const int cw = __ffs(__ballot_sync(0xffffffffu, ck == gkey && cl_ == glo && lane < csize)) - 1;
       slot = SC + cw;
       p = spos[buf][slot];
     }
@@ -189,12 +214,16 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
 #ifdef DTN_PANEL_PROFILE
     PCLK(5);
 #endif
-    if (r == p) elim = j;
-    if (elim < 0) {
-      const double l = v[j] * rinv;
-      v[j] = l;
 #pragma unroll
-      for (int c = j + 1; c < PKB; ++c) v[c] = fma(-l, pr[c], v[c]);
+    for (int a = 0; a < RPT; ++a) {
+      const int r = crank * PNT + tid + stride * a;
+      if (r == p) elim[a] = j;
+      if (elim[a] < 0) {
+        const double l = v[a][j] * rinv;
+        v[a][j] = l;
+#pragma unroll
+        for (int c = j + 1; c < PKB; ++c) v[a][c] = fma(-l, pr[c], v[a][c]);
+      }
     }
 #ifdef DTN_PANEL_PROFILE
     PCLK(6);
@@ -223,27 +252,29 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
   for (int e = 0; e < PKB; ++e)
     if (e < kbe && sp[e] < kbe) topmask |= 1u << sp[e];
   __syncthreads();
-  int fp = r;
-  if (elim >= 0 && elim < PKB) {
-    fp = elim;
-  } else if (r < kbe) {  // displaced top row (r < kbe < Ri, never a pivot)
-    fp = vac[__popc(~topmask & ((1u << r) - 1u))];
-  }
   int* mv = move_list(args, nd);
-  if (r < Ri) {
+  int fp[RPT];
 #pragma unroll
-    for (int c = 0; c < PKB; ++c)
-      if (c < kbe) M[fp + c * ldm] = v[c];
-    int slot = -1;
-    if (fp < kbe) slot = fp;
-    else if (fp != r) {  // fp is a vacated position: its rank among them
-      int rk = 0;
-      for (int e = 0; e < kbe; ++e) rk += (sp[e] >= kbe && sp[e] < fp);
-      slot = kbe + rk;
-    }
-    if (slot >= 0) {
-      mv[slot] = k0 + fp;
-      mv[2 * PKB + slot] = k0 + r;
+  for (int a = 0; a < RPT; ++a) {
+    const int r = crank * PNT + tid + stride * a;
+    fp[a] = r;
+    if (elim[a] >= 0 && elim[a] < PKB) fp[a] = elim[a];
+    else if (r < kbe) fp[a] = vac[__popc(~topmask & ((1u << r) - 1u))];  // displaced top row
+    if (r < Ri) {
+#pragma unroll
+      for (int c = 0; c < PKB; ++c)
+        if (c < kbe) M[fp[a] + c * ldm] = v[a][c];
+      int slot = -1;
+      if (fp[a] < kbe) slot = fp[a];
+      else if (fp[a] != r) {  // a vacated position: its rank among them
+        int rk = 0;
+        for (int e = 0; e < kbe; ++e) rk += (sp[e] >= kbe && sp[e] < fp[a]);
+        slot = kbe + rk;
+      }
+      if (slot >= 0) {
+        mv[slot] = k0 + fp[a];
+        mv[2 * PKB + slot] = k0 + r;
+      }
     }
   }
   if (crank == 0) {
@@ -256,12 +287,19 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
   // running permutation: perm[k0 + fp] = old perm[k0 + r] for the moved rows
   if constexpr (CL) cg::this_cluster().sync();
   else __syncthreads();
-  int oldp = 0;
-  const bool moved = r < Ri && fp != r;
-  if (moved) oldp = perm[k0 + r];
+  int oldp[RPT];
+#pragma unroll
+  for (int a = 0; a < RPT; ++a) {
+    const int r = crank * PNT + tid + stride * a;
+    oldp[a] = (r < Ri && fp[a] != r) ? perm[k0 + r] : 0;
+  }
   if constexpr (CL) cg::this_cluster().sync();
   else __syncthreads();
-  if (moved) perm[k0 + fp] = oldp;
+#pragma unroll
+  for (int a = 0; a < RPT; ++a) {
+    const int r = crank * PNT + tid + stride * a;
+    if (r < Ri && fp[a] != r) perm[k0 + fp[a]] = oldp[a];
+  }
   if (crank == 0 && tid == 0) {
     args.pivstat[2 * node_id] = pmin;
     args.pivstat[2 * node_id + 1] = bad ? INFINITY : pmax;
@@ -354,7 +392,9 @@ __global__ void __launch_bounds__(RP_THREADS) rowpanel_kernel(KernelArgs args, c
 }
 
 cudaError_t blocked_init() {
-  return cudaFuncSetAttribute(panel_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaError_t e = cudaFuncSetAttribute(panel_kernel<true, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(panel_kernel<true, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
 }
 
 cudaError_t launch_gather(const KernelArgs& args, const int* d_list, int count, int max_total, cudaStream_t st) {
@@ -365,13 +405,14 @@ cudaError_t launch_gather(const KernelArgs& args, const int* d_list, int count, 
 }
 
 // Panel geometry for systems with up to max_rows rows below k0 (kb <= 32):
-// one row per thread (two would spill), clusters of up to 16 CTAs.
+// one row per thread up to 16 CTAs x 256 rows, two rows per thread beyond
+// (clusters of up to 16 CTAs, 8192 rows).
 void panel_shape(int max_rows, int* rpt, int* csize) {
-  *rpt = 1;
-  *csize = (max_rows + PNT - 1) / PNT;
+  *rpt = max_rows <= PMAXC * PNT ? 1 : 2;
+  *csize = (max_rows + *rpt * PNT - 1) / (*rpt * PNT);
 }
 
-template <bool CL>
+template <bool CL, int RPT>
 cudaError_t launch_panel_t(const KernelArgs& args, const int* d_list, int count, int k0, int kb, int csize,
                            cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
@@ -387,7 +428,7 @@ cudaError_t launch_panel_t(const KernelArgs& args, const int* d_list, int count,
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  return cudaLaunchKernelEx(&cfg, panel_kernel<CL>, args, d_list, k0, kb, csize);
+  return cudaLaunchKernelEx(&cfg, panel_kernel<CL, RPT>, args, d_list, k0, kb, csize);
 }
 
 cudaError_t launch_panel(const KernelArgs& args, const int* d_list, int count, int max_rows, int k0, int kb,
@@ -396,9 +437,10 @@ cudaError_t launch_panel(const KernelArgs& args, const int* d_list, int count, i
   if (kb > PKB) return cudaErrorInvalidValue;
   int rpt, csize;
   panel_shape(max_rows, &rpt, &csize);
-  if (csize > PMAXC || rpt != 1) return cudaErrorInvalidValue;
-  if (csize == 1) return launch_panel_t<false>(args, d_list, count, k0, kb, 1, st);
-  return launch_panel_t<true>(args, d_list, count, k0, kb, csize, st);
+  if (csize > PMAXC) return cudaErrorInvalidValue;
+  if (csize == 1) return launch_panel_t<false, 1>(args, d_list, count, k0, kb, 1, st);
+  if (rpt == 1) return launch_panel_t<true, 1>(args, d_list, count, k0, kb, csize, st);
+  return launch_panel_t<true, 2>(args, d_list, count, k0, kb, csize, st);
 }
 
 cudaError_t launch_rowpanel(const KernelArgs& args, const int* d_list, int count, int max_total, int max_nb, int k0,

@@ -145,7 +145,7 @@ __device__ __forceinline__ void gemm_tile(const double* __restrict__ A, int lda,
   }
 }
 
-template <int BK, bool UPD>
+template <int BK, bool UPD, bool A16>
 __global__ void __launch_bounds__(GTHREADS) gemm_desc_kernel(const GemmDesc* __restrict__ descs, double alpha,
                                                              double beta) {
   extern __shared__ __align__(16) unsigned char gsm_raw[];
@@ -154,10 +154,9 @@ __global__ void __launch_bounds__(GTHREADS) gemm_desc_kernel(const GemmDesc* __r
   const int tiles_m = (d.m + GBM - 1) / GBM, tiles_n = (d.n + GBN - 1) / GBN;
   const int t = blockIdx.x;
   if (t >= tiles_m * tiles_n) return;
-  // all descriptor GEMMs have 16-byte aligned A and B columns (root LU / G /
-  // S buffers with ld a multiple of 8, block offsets multiples of 32)
-  gemm_tile<BK, true, UPD>(d.A, d.lda, d.B, d.ldb, d.C, d.ldc, d.m, d.n, d.k, t % tiles_m, t / tiles_m, alpha, beta,
-                           sm);
+  // B columns are always 16-byte aligned; A only when the launcher says so
+  gemm_tile<BK, A16, UPD>(d.A, d.lda, d.B, d.ldb, d.C, d.ldc, d.m, d.n, d.k, t % tiles_m, t / tiles_m, alpha, beta,
+                          sm);
 }
 
 // Trailing update of the blocked partial LU (right-looking, dense_nd.cpp:174-181
@@ -165,14 +164,15 @@ __global__ void __launch_bounds__(GTHREADS) gemm_desc_kernel(const GemmDesc* __r
 // ni > k0, M[k1:, k1:] -= M[k1:, k0:k1] * M[k0:k1, k1:], k1 = k0 + min(kb, ni-k0).
 template <int BK>
 __global__ void __launch_bounds__(GTHREADS) trailing_update_kernel(KernelArgs args, const int* __restrict__ list,
-                                                                   int k0, int kb, int c0, int c1) {
+                                                                   int k0, int kb, int c0, int c1, int iface_rows) {
   extern __shared__ __align__(16) unsigned char gsm_raw[];
   GemmSmem<BK>& sm = *reinterpret_cast<GemmSmem<BK>*>(gsm_raw);
   const NodeDev nd = args.nodes[list[blockIdx.y]];
   if (k0 >= nd.ni) return;
   const int kbe = min(kb, nd.ni - k0), k1 = k0 + kbe;
-  // rows [k1, total); columns [k1 + c0, min(total, k1 + c1)) (look-ahead split)
-  const int m = nd.total - k1;
+  // rows [k1, total) (or [k1, ni): interface rows only, Schur form);
+  // columns [k1 + c0, min(total, k1 + c1)) (look-ahead split)
+  const int m = (iface_rows ? nd.ni : nd.total) - k1;
   const int cb = k1 + c0, n = min(nd.total, k1 + c1) - cb;
   if (m <= 0 || n <= 0) return;
   const int tiles = (m + GBM - 1) / GBM, tiles_n = (n + GBN - 1) / GBN;
@@ -190,20 +190,19 @@ __global__ void __launch_bounds__(GTHREADS) trailing_update_kernel(KernelArgs ar
 
 int gemm_tiles(int m, int n);
 
+template <int BK, bool UPD, bool A16>
+cudaError_t set_desc_attr() {
+  return cudaFuncSetAttribute(gemm_desc_kernel<BK, UPD, A16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              sizeof(GemmSmem<BK>));
+}
+
 cudaError_t gemm_init() {
   cudaError_t e;
-  e = cudaFuncSetAttribute(gemm_desc_kernel<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           sizeof(GemmSmem<16>));
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(gemm_desc_kernel<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           sizeof(GemmSmem<8>));
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(gemm_desc_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           sizeof(GemmSmem<16>));
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(gemm_desc_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           sizeof(GemmSmem<8>));
-  if (e != cudaSuccess) return e;
+  for (cudaError_t x : {set_desc_attr<16, false, true>(), set_desc_attr<8, false, true>(), set_desc_attr<16, true, true>(),
+                        set_desc_attr<8, true, true>(), set_desc_attr<16, false, false>(),
+                        set_desc_attr<8, false, false>(), set_desc_attr<16, true, false>(),
+                        set_desc_attr<8, true, false>()})
+    if (x != cudaSuccess) return x;
   e = cudaFuncSetAttribute(trailing_update_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            sizeof(GemmSmem<16>));
   if (e != cudaSuccess) return e;
@@ -214,33 +213,38 @@ cudaError_t gemm_init() {
 int gemm_tiles(int m, int n) { return ((m + GBM - 1) / GBM) * ((n + GBN - 1) / GBN); }
 
 cudaError_t launch_gemm_desc(const GemmDesc* d_descs, int count, int max_tiles, int kmax, double alpha, double beta,
-                             cudaStream_t st) {
+                             cudaStream_t st, bool a_aligned) {
   if (count <= 0 || max_tiles <= 0) return cudaSuccess;
   dim3 grid(max_tiles, count);
   const bool upd = alpha == -1.0 && beta == 1.0;
   if (!upd && !(alpha == 1.0 && beta == 0.0)) return cudaErrorInvalidValue;
   const bool bk16 = kmax % 16 == 0 || kmax > 64;
-  if (upd) {
-    if (bk16) gemm_desc_kernel<16, true><<<grid, GTHREADS, sizeof(GemmSmem<16>), st>>>(d_descs, alpha, beta);
-    else gemm_desc_kernel<8, true><<<grid, GTHREADS, sizeof(GemmSmem<8>), st>>>(d_descs, alpha, beta);
+#define DTNB_DESC_LAUNCH(BK, U, AL) \
+  gemm_desc_kernel<BK, U, AL><<<grid, GTHREADS, sizeof(GemmSmem<BK>), st>>>(d_descs, alpha, beta)
+  if (a_aligned) {
+    if (upd) { if (bk16) DTNB_DESC_LAUNCH(16, true, true); else DTNB_DESC_LAUNCH(8, true, true); }
+    else { if (bk16) DTNB_DESC_LAUNCH(16, false, true); else DTNB_DESC_LAUNCH(8, false, true); }
   } else {
-    if (bk16) gemm_desc_kernel<16, false><<<grid, GTHREADS, sizeof(GemmSmem<16>), st>>>(d_descs, alpha, beta);
-    else gemm_desc_kernel<8, false><<<grid, GTHREADS, sizeof(GemmSmem<8>), st>>>(d_descs, alpha, beta);
+    if (upd) { if (bk16) DTNB_DESC_LAUNCH(16, true, false); else DTNB_DESC_LAUNCH(8, true, false); }
+    else { if (bk16) DTNB_DESC_LAUNCH(16, false, false); else DTNB_DESC_LAUNCH(8, false, false); }
   }
+#undef DTNB_DESC_LAUNCH
   return cudaGetLastError();
 }
 
 // Columns [k1 + c0, k1 + c1) of the trailing block (c1 = INT_MAX: to the end).
 cudaError_t launch_trailing_update(const KernelArgs& args, const int* d_list, int count, int max_total, int k0, int kb,
-                                   int c0, int c1, cudaStream_t st) {
-  const int m = max_total - k0 - 1;
-  const int n = std::min(m, c1) - c0;
+                                   int c0, int c1, cudaStream_t st, int max_rows) {
+  const int m = (max_rows > 0 ? max_rows : max_total) - k0 - 1;
+  const int n = std::min(max_total - k0 - 1, c1) - c0;
   if (count <= 0 || m <= 0 || n <= 0) return cudaSuccess;
   dim3 grid(gemm_tiles(m, n), count);
   if (kb % 16 == 0)
-    trailing_update_kernel<16><<<grid, GTHREADS, sizeof(GemmSmem<16>), st>>>(args, d_list, k0, kb, c0, c1);
+    trailing_update_kernel<16><<<grid, GTHREADS, sizeof(GemmSmem<16>), st>>>(args, d_list, k0, kb, c0, c1,
+                                                                             max_rows > 0 ? 1 : 0);
   else
-    trailing_update_kernel<8><<<grid, GTHREADS, sizeof(GemmSmem<8>), st>>>(args, d_list, k0, kb, c0, c1);
+    trailing_update_kernel<8><<<grid, GTHREADS, sizeof(GemmSmem<8>), st>>>(args, d_list, k0, kb, c0, c1,
+                                                                           max_rows > 0 ? 1 : 0);
   return cudaGetLastError();
 }
 

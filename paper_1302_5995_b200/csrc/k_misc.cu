@@ -120,6 +120,117 @@ __global__ void __launch_bounds__(TB) tri_inv_blocks_kernel(const double* __rest
   }
 }
 
+// Batched: inverses of the 128 x 128 diagonal blocks of U for several LU
+// factors (back substitution of the merge systems); out layout as above.
+__global__ void __launch_bounds__(TB) tri_inv_u_batched_kernel(const TriDesc* __restrict__ descs) {
+  extern __shared__ double blk[];
+  const TriDesc d = descs[blockIdx.y];
+  const int kb = blockIdx.x, k0 = kb * TB;
+  if (k0 >= d.n) return;
+  const int bk = min(TB, d.n - k0);
+  const int j = threadIdx.x;
+  for (int c = 0; c < TB; ++c)
+    blk[c * (TB + 1) + j] = (j < bk && c < bk) ? d.LU[(k0 + j) + (long long)(k0 + c) * d.ld] : (j == c ? 1.0 : 0.0);
+  __syncthreads();
+  double* Ui = d.out + (long long)kb * 2 * TB * TB + TB * TB;
+  double x[TB];
+  for (int i = 0; i < TB; ++i) x[i] = 0.0;
+  x[j] = 1.0 / blk[j * (TB + 1) + j];
+  for (int i = j - 1; i >= 0; --i) {
+    double s = 0.0;
+    for (int m = i + 1; m <= j; ++m) s = fma(blk[m * (TB + 1) + i], x[m], s);
+    x[i] = -s / blk[i * (TB + 1) + i];
+  }
+  for (int i = 0; i < TB; ++i) Ui[i + (long long)j * TB] = x[i];
+}
+
+__global__ void copy2d_batched_kernel(const CopyDesc* __restrict__ descs) {
+  const CopyDesc d = descs[blockIdx.y];
+  const long long total = (long long)d.m * d.n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int r = int(e % d.m), c = int(e / d.m);
+    d.dst[r + (long long)c * d.ldd] = d.src[r + (long long)c * d.lds];
+  }
+}
+
+cudaError_t launch_tri_inv_u_batched(const void* d_descs, int count, int max_blocks, cudaStream_t st) {
+  if (count <= 0 || max_blocks <= 0) return cudaSuccess;
+  tri_inv_u_batched_kernel<<<dim3(max_blocks, count), TB, TB * (TB + 1) * sizeof(double), st>>>(
+      static_cast<const TriDesc*>(d_descs));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy2d_batched(const void* d_descs, int count, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  copy2d_batched_kernel<<<dim3(64, count), 256, 0, st>>>(static_cast<const CopyDesc*>(d_descs));
+  return cudaGetLastError();
+}
+
+// Batched block back substitution by rows (as dtrsm, no explicit inverse):
+// one warp per column, lane l holds rows l, l+32, l+64, l+96.
+__global__ void __launch_bounds__(256) trsm_upper_block_kernel(const TrsmDesc* __restrict__ descs) {
+  extern __shared__ double trsm_smem[];
+  double (*Us)[TB + 1] = reinterpret_cast<double (*)[TB + 1]>(trsm_smem);
+  double* rd = trsm_smem + TB * (TB + 1);
+  const TrsmDesc d = descs[blockIdx.y];
+  const int bk = d.bk;
+  if (blockIdx.x * 8 >= d.ncols) return;
+  for (int e = threadIdx.x; e < bk * bk; e += blockDim.x) {
+    const int r = e % bk, c = e / bk;
+    Us[r][c] = d.U[r + (long long)c * d.ldu];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < bk; c += blockDim.x) rd[c] = 1.0 / Us[c][c];
+  __syncthreads();
+  // each warp runs TCW independent columns interleaved (ILP over the
+  // 128-step dependent substitution chain)
+  constexpr int TCW = 4;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j0 = (blockIdx.x * 8 + warp) * TCW; j0 < d.ncols; j0 += gridDim.x * 8 * TCW) {
+    double x[TCW][4];
+#pragma unroll
+    for (int u = 0; u < TCW; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        x[u][q] = (j0 + u < d.ncols && lane + 32 * q < bk) ? d.Y[lane + 32 * q + (long long)(j0 + u) * d.ldy] : 0.0;
+    for (int c = bk - 1; c >= 0; --c) {
+      const int owner = c & 31, qc = c >> 5;
+      const double rdc = rd[c];
+      double xc[TCW];
+#pragma unroll
+      for (int u = 0; u < TCW; ++u) {
+        double t = x[u][0];
+#pragma unroll
+        for (int q = 1; q < 4; ++q) t = (q == qc) ? x[u][q] : t;
+        xc[u] = __shfl_sync(0xffffffffu, t * rdc, owner);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = lane + 32 * q;
+        const double urc = (r < c) ? Us[r][c] : 0.0;
+#pragma unroll
+        for (int u = 0; u < TCW; ++u) {
+          if (r == c) x[u][q] = xc[u];
+          else x[u][q] = fma(-urc, xc[u], x[u][q]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < TCW; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (j0 + u < d.ncols && lane + 32 * q < bk) d.Y[lane + 32 * q + (long long)(j0 + u) * d.ldy] = x[u][q];
+  }
+}
+
+cudaError_t launch_trsm_upper_batched(const void* d_descs, int count, int max_cols, cudaStream_t st) {
+  if (count <= 0 || max_cols <= 0) return cudaSuccess;
+  const int bx = std::min((max_cols + 31) / 32, 1184);
+  trsm_upper_block_kernel<<<dim3(bx, count), 256, (TB * (TB + 1) + TB) * sizeof(double), st>>>(
+      static_cast<const TrsmDesc*>(d_descs));
+  return cudaGetLastError();
+}
+
 __global__ void set_identity_kernel(double* X, int ldx, int n) {
   const long long total = (long long)n * ldx;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
@@ -139,8 +250,14 @@ __global__ void permute_columns_kernel(const double* __restrict__ W, int ldw, co
 }
 
 cudaError_t misc_init() {
-  return cudaFuncSetAttribute(tri_inv_blocks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              TB * (TB + 1) * sizeof(double));
+  cudaError_t e = cudaFuncSetAttribute(tri_inv_blocks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       TB * (TB + 1) * sizeof(double));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(tri_inv_u_batched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           TB * (TB + 1) * sizeof(double));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(trsm_upper_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (TB * (TB + 1) + TB) * sizeof(double));
 }
 
 cudaError_t launch_tri_inv_blocks(const double* LU, int ldlu, int n, double* out, cudaStream_t st) {

@@ -272,6 +272,11 @@ Plan make_plan(const PlanKey& key) {
       nd.ld = nd.ldm;
       nd.piv_off = poff;
       poff += align_up(std::max(nd.ni, 1), 4) + 128;  // ipiv + per-panel row-move list
+      const int64_t nblk = (nd.ni + 127) / 128;
+      nd.uinv_off = off;
+      off = align_up(off + nblk * 2 * 128 * 128, 32);
+      nd.t_off = off;
+      off = align_up(off + int64_t(128) * std::max(nd.nb, 1), 32);
     } else {
       nd.ld = std::max(nd.nb, 1);
       nd.s_off = off;

@@ -66,6 +66,8 @@ struct Node {
   int ldm = 0;
   int64_t pos_off = 0;  // offset into the PosEntry table
   int64_t piv_off = 0;  // blocked: offset into the int pivot table
+  int64_t uinv_off = 0;  // blocked: inverses of the 128 x 128 diagonal blocks of U (back substitution)
+  int64_t t_off = 0;     // blocked: 128 x nb staging block of the back substitution
 };
 
 struct Wave {

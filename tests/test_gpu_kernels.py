@@ -22,7 +22,7 @@ def gpu_partial_lu(A, ni):
     return out, ipiv, ps
 
 
-@pytest.mark.parametrize("n", [5, 20, 33, 64, 100, 257, 600, 1100, 2100])
+@pytest.mark.parametrize("n", [5, 20, 33, 64, 100, 257, 600, 1100, 2100, 4100, 8190])
 def test_full_lu_matches_scipy(n):
     rng = np.random.default_rng(n)
     A = rng.standard_normal((n, n))
@@ -39,7 +39,7 @@ def test_full_lu_matches_scipy(n):
     assert ps[0] == pytest.approx(np.min(np.abs(np.diag(Um))))
 
 
-@pytest.mark.parametrize("n,ni", [(40, 12), (184, 60), (376, 124), (1528, 508), (3064, 1020)])
+@pytest.mark.parametrize("n,ni", [(40, 12), (184, 60), (376, 124), (1528, 508), (3064, 1020), (6136, 2044)])
 def test_partial_lu_schur(n, ni):
     rng = np.random.default_rng(ni)
     A = rng.standard_normal((n, n))
