@@ -44,6 +44,10 @@ typedef struct {
   const double* stencil;   /* 5 x (n-2)^2 SoA: center, east, west, north, south, unknown_id order
                               (grid.hpp:68-70); couplings to ring nodes are ignored */
   int32_t stencil_on_device; /* 1: stencil is a device pointer on the context's device */
+  /* top-of-tree build only (opts.nshards > 1, opts.shard == -1): the Schur
+   * complements of the shards (column-major nb x nb, dtn_gpu_shard_info order) */
+  const double* const* shard_S;
+  int32_t shard_S_on_device;
 } dtn_problem;
 
 typedef struct {
@@ -55,6 +59,9 @@ typedef struct {
   int32_t profile;     /* 1: no graph, CUDA events around every launch (dtn_gpu_kernel_stats) */
   double epsilon;      /* compressed engine tolerance (AccelOptions::epsilon) — reserved */
   int64_t crossover;   /* AccelOptions::crossover — reserved */
+  int32_t nshards;     /* subtree sharding: 1, 2 (W|E), 4 (quadrants), 8 (quadrant halves) */
+  int32_t shard;       /* >= 0: build only this shard's S; -1: full build (nshards == 1) or the top of
+                          the tree from prob.shard_S (nshards > 1) */
 } dtn_opts;
 
 typedef struct {
@@ -98,6 +105,8 @@ void dtn_gpu_free(dtn_op* op);
 int dtn_gpu_boundary(const dtn_op* op, int64_t* ids, int64_t* nb);
 int dtn_gpu_export(const dtn_op* op, double* S, double* G, double* cond);
 int dtn_gpu_device_ptrs(const dtn_op* op, const double** S, const double** G, int64_t* ld);
+/* Device-to-device export into caller buffers (leading dimensions lds, ldg); NULL skips. */
+int dtn_gpu_export_device(const dtn_op* op, double* S, int64_t lds, double* G, int64_t ldg);
 /* Y(nb x batch) = op(X), op = G (which 0, apply_dtn) or S (which 1, apply_schur).
  * on_device: X and Y are device pointers (else host). */
 int dtn_gpu_apply(const dtn_op* op, int which, const double* X, int64_t ldx, int64_t batch, double* Y, int64_t ldy,
@@ -111,6 +120,11 @@ int dtn_gpu_level_stats(const dtn_op* op, dtn_level_stats* out, int32_t max, int
 int dtn_gpu_build_stats(const dtn_op* op, dtn_build_stats* out);
 /* per-kernel-class timing of a build made with opts.profile = 1 (count 0 otherwise) */
 int dtn_gpu_kernel_stats(const dtn_op* op, dtn_kernel_stats* out, int32_t max, int32_t* count);
+
+/* Geometry of shard `shard` of `nshards` (host only, no device needed):
+ * rect = x0, x1, y0, y1 of its unknown rectangle; nb = its boundary size. */
+int dtn_gpu_shard_info(int32_t n, int32_t n_leaf, int32_t leaf_side, int32_t nshards, int32_t shard, int32_t* rect,
+                       int64_t* nb);
 
 /* Test hook: partial LU (pivots among the first ni rows) of a host n x n
  * column-major matrix with the engine's blocked kernels; ni == n is a full LU. */

@@ -696,5 +696,27 @@ int orc_merge_rects(void* p, const int* ra, const int* rb, double* S, int64_t* n
     if (S) std::copy(s.S.a.begin(), s.S.a.end(), S);
   });
 }
+// merge_two of two given Schur complements on rectangles ra, rb (x0,x1,y0,y1)
+// (column-major, CCW boundary order) — the top-of-tree merges of a sharded build.
+int orc_merge_given(void* p, const int* ra, const double* Sa, const int* rb, const double* Sb, double* S,
+                    int64_t* nb_out) {
+  return guarded([&] {
+    auto* op = static_cast<orc::Operator*>(p);
+    orc::SchurData ch[2];
+    const int* rr[2] = {ra, rb};
+    const double* ss[2] = {Sa, Sb};
+    for (int c = 0; c < 2; ++c) {
+      ch[c].x0 = rr[c][0]; ch[c].x1 = rr[c][1]; ch[c].y0 = rr[c][2]; ch[c].y1 = rr[c][3];
+      for (const auto& gp : orc::rect_perimeter_ccw(ch[c].x0, ch[c].x1, ch[c].y0, ch[c].y1))
+        ch[c].boundary.push_back(op->lat.unknown_id(gp.x, gp.y));
+      const int64_t nb = int64_t(ch[c].boundary.size());
+      ch[c].S = orc::Mat(nb, nb);
+      std::copy(ss[c], ss[c] + nb * nb, ch[c].S.a.begin());
+    }
+    const auto out = orc::merge_two(ch[0], ch[1], *op, -1, -1);
+    *nb_out = int64_t(out.boundary.size());
+    if (S) std::copy(out.S.a.begin(), out.S.a.end(), S);
+  });
+}
 int orc_blas_threads() { return scipy_openblas_get_num_threads64_(); }
 }

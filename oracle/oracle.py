@@ -56,6 +56,7 @@ def lib():
         L.orc_result_box.restype = i64
         L.orc_leaf_rect.argtypes = [vp, i32, i32, i32, i32, P(f64), P(i64)]
         L.orc_merge_rects.argtypes = [vp, P(i32), P(i32), P(f64), P(i64)]
+        L.orc_merge_given.argtypes = [vp, P(i32), P(f64), P(i32), P(f64), P(f64), P(i64)]
         _lib = L
     return _lib
 
@@ -210,6 +211,21 @@ def merge_rects(problem: Problem, ra, rb) -> np.ndarray:
     S = np.zeros((nb.value, nb.value), order="F")
     _check(lib().orc_merge_rects(problem.h, _ip(a, C.c_int), _ip(b, C.c_int), _dp(S), C.byref(nb)))
     return S
+
+
+def merge_given(problem: Problem, ra, Sa, rb, Sb):
+    """merge_two (dense_nd.cpp:105-186) of two given Schur complements on
+    rectangles ra, rb = (x0, x1, y0, y1); returns (rect, S)."""
+    a = np.asarray(ra, dtype=np.int32)
+    b = np.asarray(rb, dtype=np.int32)
+    Sa = np.asfortranarray(Sa, dtype=np.float64)
+    Sb = np.asfortranarray(Sb, dtype=np.float64)
+    nb = C.c_int64()
+    _check(lib().orc_merge_given(problem.h, _ip(a, C.c_int), _dp(Sa), _ip(b, C.c_int), _dp(Sb), None, C.byref(nb)))
+    S = np.zeros((nb.value, nb.value), order="F")
+    _check(lib().orc_merge_given(problem.h, _ip(a, C.c_int), _dp(Sa), _ip(b, C.c_int), _dp(Sb), _dp(S), C.byref(nb)))
+    rect = (min(a[0], b[0]), max(a[1], b[1]), min(a[2], b[2]), max(a[3], b[3]))
+    return rect, S
 
 
 # ----------------------------------------------------------------- checkers

@@ -3,6 +3,6 @@ DtN build (arXiv 1302.5995): leaf elimination, batched FP64 merges and the
 batched solve on sm_100a, behind the C ABI in include/dtn_gpu.h."""
 from .dtn import (AccelOptions, BoxTree, Context, DiscreteOperator, Engine, FactorizationError, Lattice,  # noqa: F401
                   ProblemMode, ProblemSpec, SolutionOperator, apply_dtn, apply_schur, baseline_problem,
-                  build_root_dense_op, build_root_gpu, build_tree, build_tree_uniform, build_with_loads, catalog,
+                  build_root_dense_op, build_root_gpu, build_tree, build_tree_uniform, build_with_loads, catalog, shard_info,
                   catalog_names, default_context, densify_dtn, discrete_eigenvalue, discrete_eigenvalue_kth,
                   discretize, root_boundary)

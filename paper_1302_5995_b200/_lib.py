@@ -14,13 +14,14 @@ DTN_OK, DTN_EINVAL, DTN_ESINGULAR, DTN_ECUDA = 0, 2, 3, 5
 
 
 class dtn_problem(C.Structure):
-    _fields_ = [("n", C.c_int32), ("stencil", C.c_void_p), ("stencil_on_device", C.c_int32)]
+    _fields_ = [("n", C.c_int32), ("stencil", C.c_void_p), ("stencil_on_device", C.c_int32),
+                ("shard_S", C.POINTER(C.c_void_p)), ("shard_S_on_device", C.c_int32)]
 
 
 class dtn_opts(C.Structure):
     _fields_ = [("engine", C.c_int32), ("n_leaf", C.c_int32), ("leaf_side", C.c_int32), ("want_G", C.c_int32),
                 ("micro_max", C.c_int32), ("profile", C.c_int32), ("epsilon", C.c_double),
-                ("crossover", C.c_int64)]
+                ("crossover", C.c_int64), ("nshards", C.c_int32), ("shard", C.c_int32)]
 
 
 class dtn_level_stats(C.Structure):
@@ -41,9 +42,10 @@ class dtn_kernel_stats(C.Structure):
 
 EXPORTS = [
     "dtn_gpu_create", "dtn_gpu_destroy", "dtn_gpu_last_error", "dtn_gpu_set_stream", "dtn_gpu_build",
-    "dtn_gpu_free", "dtn_gpu_boundary", "dtn_gpu_export", "dtn_gpu_device_ptrs", "dtn_gpu_apply",
+    "dtn_gpu_free", "dtn_gpu_boundary", "dtn_gpu_export", "dtn_gpu_export_device", "dtn_gpu_device_ptrs",
+    "dtn_gpu_apply",
     "dtn_gpu_num_boxes", "dtn_gpu_box_info", "dtn_gpu_box_schur", "dtn_gpu_level_stats", "dtn_gpu_build_stats", "dtn_gpu_kernel_stats",
-    "dtn_discretize_continuum", "dtn_discretize_network", "dtn_debug_partial_lu",
+    "dtn_discretize_continuum", "dtn_discretize_network", "dtn_debug_partial_lu", "dtn_gpu_shard_info",
 ]
 
 _lib = None
@@ -76,6 +78,7 @@ def lib():
     L.dtn_gpu_boundary.argtypes = [vp, vp, P(i64)]
     L.dtn_gpu_export.argtypes = [vp, vp, vp, P(f64)]
     L.dtn_gpu_device_ptrs.argtypes = [vp, P(vp), P(vp), P(i64)]
+    L.dtn_gpu_export_device.argtypes = [vp, vp, i64, vp, i64]
     L.dtn_gpu_apply.argtypes = [vp, C.c_int, vp, i64, i64, vp, i64, C.c_int]
     L.dtn_gpu_num_boxes.argtypes = [vp, P(i32), P(i32)]
     L.dtn_gpu_box_info.argtypes = [vp, i32, P(i32)]
@@ -86,5 +89,6 @@ def lib():
     L.dtn_discretize_continuum.argtypes = [i32, vp, vp, vp, vp]
     L.dtn_discretize_network.argtypes = [i32, f64, f64, C.c_uint64, vp]
     L.dtn_debug_partial_lu.argtypes = [i32, i32, vp, vp, vp, vp]
+    L.dtn_gpu_shard_info.argtypes = [i32, i32, i32, i32, i32, P(i32), P(i64)]
     _lib = L
     return L

@@ -765,6 +765,11 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
     key.leaf_side = opts->leaf_side;
     key.micro_max = opts->micro_max > 0 ? opts->micro_max : kDefaultMicro;
     key.small_max = kSmallMax;
+    key.nshards = opts->nshards > 0 ? opts->nshards : 1;
+    key.shard = opts->shard;
+    if (key.nshards == 1) key.shard = -1;
+    const bool top_mode = key.nshards > 1 && key.shard < 0;
+    if (top_mode && !prob->shard_S) throw std::invalid_argument("dtn_gpu_build: top build needs the shard S blocks");
     if (key.leaf_side <= 0 && key.n_leaf < 16) throw std::invalid_argument("build_tree: n_leaf must be >= 16");
     PlanDev* D = nullptr;
     for (auto& p : ctx->plans)
@@ -774,7 +779,17 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
       D = ctx->plans.back().get();
     }
     cudaStream_t st = ctx->stream;
-    const bool want_G = opts->want_G != 0;
+    const bool want_G = opts->want_G != 0 && key.shard < 0;  // a shard's S is not inverted
+    if (top_mode) {
+      const Plan& P0 = D->P;
+      for (size_t i = 0; i < P0.inputs.size(); ++i) {
+        const Node& nd = P0.nodes[P0.inputs[i]];
+        if (!prob->shard_S[i]) throw std::invalid_argument("dtn_gpu_build: null shard S");
+        CK(cudaMemcpy2DAsync(D->d_arena + nd.s_off, size_t(nd.ld) * 8, prob->shard_S[i], size_t(nd.nb) * 8,
+                             size_t(nd.nb) * 8, size_t(nd.nb),
+                             prob->shard_S_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+      }
+    }
     const bool profile = opts->profile != 0;
     std::unique_ptr<Prof> prof;
     CK(cudaMemcpyAsync(D->d_stencil, prob->stencil, size_t(5 * D->nu) * sizeof(double),
@@ -940,6 +955,26 @@ int dtn_gpu_export(const dtn_op* op, double* S, double* G, double* cond) {
   });
 }
 
+int dtn_gpu_export_device(const dtn_op* op, double* S, int64_t lds, double* G, int64_t ldg) {
+  if (!op) return DTN_EINVAL;
+  return guarded(op->ctx, [&] {
+    CK(cudaSetDevice(op->ctx->device));
+    const PlanDev& D = *op->plan;
+    const size_t nb = size_t(op->nb);
+    cudaStream_t st = op->ctx->stream;
+    if (S) {
+      if (lds < int64_t(nb)) throw std::invalid_argument("dtn_gpu_export_device: lds < nb");
+      CK(cudaMemcpy2DAsync(S, size_t(lds) * 8, D.d_S, size_t(D.lds) * 8, nb * 8, nb, cudaMemcpyDeviceToDevice, st));
+    }
+    if (G) {
+      if (!op->has_G) throw std::invalid_argument("dtn_gpu_export_device: G was not built (want_G = 0)");
+      if (ldg < int64_t(nb)) throw std::invalid_argument("dtn_gpu_export_device: ldg < nb");
+      CK(cudaMemcpy2DAsync(G, size_t(ldg) * 8, D.d_G, size_t(D.ldg) * 8, nb * 8, nb, cudaMemcpyDeviceToDevice, st));
+    }
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
 int dtn_gpu_device_ptrs(const dtn_op* op, const double** S, const double** G, int64_t* ld) {
   if (!op) return DTN_EINVAL;
   if (S) *S = op->plan->d_S;
@@ -1019,6 +1054,7 @@ int dtn_gpu_box_schur(const dtn_op* op, int32_t box, double* S) {
     const PlanDev& D = *op->plan;
     const int node = D.P.boxes[box].node;
     if (node < 0) throw std::invalid_argument("dtn_gpu_box_schur: empty box");
+    if (!D.P.active[node]) throw std::invalid_argument("dtn_gpu_box_schur: box not computed by this (sharded) build");
     const Node& nd = D.P.nodes[node];
     CK(cudaSetDevice(op->ctx->device));
     CK(cudaMemcpy2D(S, size_t(nd.nb) * 8, D.d_arena + nd.s_off, size_t(nd.ld) * 8, size_t(nd.nb) * 8, nd.nb,
@@ -1046,6 +1082,29 @@ int dtn_gpu_build_stats(const dtn_op* op, dtn_build_stats* out) {
   if (!op || !out) return DTN_EINVAL;
   *out = op->stats;
   return DTN_OK;
+}
+
+int dtn_gpu_shard_info(int32_t n, int32_t n_leaf, int32_t leaf_side, int32_t nshards, int32_t shard, int32_t* rect,
+                       int64_t* nb) {
+  return guarded(nullptr, [&] {
+    PlanKey key;
+    key.n = n;
+    key.n_leaf = n_leaf;
+    key.leaf_side = leaf_side;
+    key.micro_max = kDefaultMicro;
+    key.small_max = kSmallMax;
+    const Plan P = make_plan(key);
+    const std::vector<int> sh = shard_nodes(P, nshards);
+    if (shard < 0 || shard >= int(sh.size())) throw std::invalid_argument("shards: shard index out of range");
+    const Node& nd = P.nodes[sh[shard]];
+    if (rect) {
+      rect[0] = nd.r.x0;
+      rect[1] = nd.r.x1;
+      rect[2] = nd.r.y0;
+      rect[3] = nd.r.y1;
+    }
+    if (nb) *nb = nd.nb;
+  });
 }
 
 // Test hook: blocked partial LU of one dense n x n matrix with the engine's

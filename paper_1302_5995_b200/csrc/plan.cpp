@@ -221,6 +221,39 @@ int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
 }  // namespace
 
+std::vector<int> shard_nodes(const Plan& P, int nshards) {
+  auto need = [&](bool ok) {
+    if (!ok) throw std::invalid_argument("shards: the tree is too shallow for this shard count");
+  };
+  const Node& root = P.nodes[P.root];
+  switch (nshards) {
+    case 1:
+      return {P.root};
+    case 2:  // W | E halves of the root's merge_four (dense_nd.cpp:188-194)
+      need(root.kind == NodeKind::merge && P.depth >= 1);
+      return {root.a, root.b};
+    case 4: {  // quadrants SW, SE, NW, NE
+      need(P.depth >= 1);
+      std::vector<int> out;
+      for (int c = 0; c < 4; ++c) out.push_back(P.boxes[P.boxes[0].children[c]].node);
+      return out;
+    }
+    case 8: {  // W | E halves of every quadrant
+      need(P.depth >= 2);
+      std::vector<int> out;
+      for (int c = 0; c < 4; ++c) {
+        const Node& q = P.nodes[P.boxes[P.boxes[0].children[c]].node];
+        need(q.kind == NodeKind::merge);
+        out.push_back(q.a);
+        out.push_back(q.b);
+      }
+      return out;
+    }
+    default:
+      throw std::invalid_argument("shards: nshards must be 1, 2, 4 or 8");
+  }
+}
+
 Plan make_plan(const PlanKey& key) {
   if (key.micro_max < 4 || key.micro_max > key.small_max)
     throw std::invalid_argument("make_plan: bad micro/small thresholds");
@@ -247,14 +280,68 @@ Plan make_plan(const PlanKey& key) {
   }
   P.root = P.boxes[0].node;
   if (P.root < 0) throw std::invalid_argument("make_plan: empty domain");
+  P.active.assign(P.nodes.size(), 1);
+  if (key.nshards > 1 || key.shard >= 0) {
+    const std::vector<int> sh = shard_nodes(P, key.nshards);
+    std::vector<char> below(P.nodes.size(), 0);  // inside some shard's subtree (inclusive)
+    std::vector<int> stack;
+    for (int s0 : sh) {
+      stack.push_back(s0);
+      while (!stack.empty()) {
+        const int v = stack.back();
+        stack.pop_back();
+        if (v < 0 || below[v]) continue;
+        below[v] = 1;
+        if (P.nodes[v].kind == NodeKind::merge) {
+          stack.push_back(P.nodes[v].a);
+          stack.push_back(P.nodes[v].b);
+        }
+      }
+    }
+    if (key.shard >= 0) {
+      if (key.shard >= int(sh.size())) throw std::invalid_argument("shards: shard index out of range");
+      std::vector<char> mine(P.nodes.size(), 0);
+      stack.push_back(sh[key.shard]);
+      while (!stack.empty()) {
+        const int v = stack.back();
+        stack.pop_back();
+        if (v < 0 || mine[v]) continue;
+        mine[v] = 1;
+        if (P.nodes[v].kind == NodeKind::merge) {
+          stack.push_back(P.nodes[v].a);
+          stack.push_back(P.nodes[v].b);
+        }
+      }
+      P.active = mine;
+      P.root = sh[key.shard];
+    } else {
+      for (size_t v = 0; v < P.nodes.size(); ++v) P.active[v] = !below[v];
+      P.inputs = sh;
+    }
+    P.merge_flops = P.micro_flops = 0.0;
+    for (size_t v = 0; v < P.nodes.size(); ++v) {
+      if (!P.active[v]) continue;
+      const Node& nd = P.nodes[v];
+      (nd.label_level >= 0 ? P.merge_flops : P.micro_flops) += merge_flop_count(nd.ni, nd.nb);
+    }
+  }
   // waves and storage
   int nw = 0;
   for (auto& nd : P.nodes) nw = std::max(nw, nd.wave + 1);
   P.waves.assign(nw, {});
   int64_t off = 0, poff = 0;
+  std::vector<char> is_input(P.nodes.size(), 0);
+  for (int v : P.inputs) is_input[v] = 1;
   for (int i = 0; i < int(P.nodes.size()); ++i) {
     Node& nd = P.nodes[i];
+    if (!P.active[i] && !is_input[i]) continue;  // not computed, not read: no storage
     Wave& wv = P.waves[nd.wave];
+    if (is_input[i]) {  // provided by the caller: compact S storage only
+      nd.ld = std::max(nd.nb, 1);
+      nd.s_off = off;
+      off = align_up(off + int64_t(nd.ld) * nd.nb, 32);
+      continue;
+    }
     if (nd.kind == NodeKind::micro) {
       wv.micro.push_back(i);
     } else if (nd.total <= key.small_max) {

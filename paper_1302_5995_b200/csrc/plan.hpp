@@ -75,11 +75,17 @@ struct Wave {
   int max_ni_blocked = 0;
 };
 
+// Subtree sharding: nshards in {1, 2, 4, 8} splits the tree into
+// the root's W|E halves, its quadrants, or the quadrants' W|E halves.
+// shard >= 0: build only that shard's subtree (its S is the result);
+// shard == -1 with nshards > 1: the top of the tree above the shards, whose
+// S blocks are inputs.
 struct PlanKey {
   int n = 0, n_leaf = 0, leaf_side = 0, micro_max = 0, small_max = 0;
+  int nshards = 1, shard = -1;
   bool operator==(const PlanKey& o) const {
     return n == o.n && n_leaf == o.n_leaf && leaf_side == o.leaf_side && micro_max == o.micro_max &&
-           small_max == o.small_max;
+           small_max == o.small_max && nshards == o.nshards && shard == o.shard;
   }
 };
 
@@ -94,7 +100,9 @@ struct Plan {
   std::vector<PosEntry> pos;  // all position tables
   int64_t arena_doubles = 0;
   int64_t piv_ints = 0;
-  int root = -1;  // root node
+  int root = -1;  // root node (the shard's node in shard mode)
+  std::vector<int> inputs;  // top mode: shard nodes whose S is provided by the caller
+  std::vector<char> active;  // nodes computed by this plan
   // algorithmic work (reference formulation)
   double merge_flops = 0.0;     // sum of (2/3)ni^3 + 2ni^2nb + 2nb^2ni over reference-tree merges
   double micro_flops = 0.0;     // leaf-interior elimination executed (same formula)
@@ -103,6 +111,9 @@ struct Plan {
 // Builds the plan; leaf_side > 0 selects the uniform tree (n-2 = leaf_side*2^L),
 // else the reference rule with n_leaf. Throws std::invalid_argument.
 Plan make_plan(const PlanKey& key);
+
+// DAG nodes of the shards of a full plan (see PlanKey), in shard order.
+std::vector<int> shard_nodes(const Plan& P, int nshards);
 
 inline double merge_flop_count(double ni, double nb) {
   return (2.0 / 3.0) * ni * ni * ni + 2.0 * ni * ni * nb + 2.0 * nb * nb * ni;

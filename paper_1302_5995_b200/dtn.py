@@ -387,6 +387,10 @@ class SolutionOperator:
         nb = self.boundary_size()
         return 8 * nb * nb * (2 if self.has_G else 1)
 
+    def export_device(self, S_ptr: int | None = None, lds: int = 0, G_ptr: int | None = None, ldg: int = 0):
+        """Device-to-device export of S and/or G (column-major, leading dims)."""
+        self.ctx.check(L.lib().dtn_gpu_export_device(self.h, S_ptr, lds, G_ptr, ldg))
+
     def device_ptrs(self):
         s, g, ld = C.c_void_p(), C.c_void_p(), C.c_int64()
         self.ctx.check(L.lib().dtn_gpu_device_ptrs(self.h, C.byref(s), C.byref(g), C.byref(ld)))
@@ -411,9 +415,20 @@ class SolutionOperator:
         return S
 
 
+def shard_info(tree: BoxTree, nshards: int, shard: int) -> dict:
+    """Rectangle and boundary size of shard `shard` of `nshards` (SURVEY 8e:
+    2 = W|E halves, 4 = quadrants, 8 = quadrant halves). Host only."""
+    rect = (C.c_int32 * 4)()
+    nb = C.c_int64()
+    rc = L.lib().dtn_gpu_shard_info(tree.n, tree.n_leaf, tree.leaf_side, nshards, shard, rect, C.byref(nb))
+    if rc != 0:
+        raise ValueError(L.lib().dtn_gpu_last_error(None).decode())
+    return dict(rect=tuple(rect), nb=nb.value)
+
+
 def build_root_gpu(op: DiscreteOperator | None, tree: BoxTree, want_G: bool = True, micro_max: int = 0,
                    ctx: Context | None = None, stencil_device_ptr: int | None = None,
-                   profile: bool = False) -> SolutionOperator:
+                   profile: bool = False, nshards: int = 1, shard: int = -1, shard_S=None) -> SolutionOperator:
     """The B200 build: leaf elimination + merges + root inverse, through dtn_gpu_build."""
     ctx = ctx or default_context()
     if stencil_device_ptr:
@@ -423,7 +438,33 @@ def build_root_gpu(op: DiscreteOperator | None, tree: BoxTree, want_G: bool = Tr
             raise ValueError("build: tree and operator sizes differ")
         st = np.ascontiguousarray(op.stencil, dtype=np.float64)
         prob = L.dtn_problem(op.n, st.ctypes.data, 0)
-    opts = L.dtn_opts(0, tree.n_leaf, tree.leaf_side, 1 if want_G else 0, micro_max, 1 if profile else 0, 0.0, 0)
+    keep = []
+    if shard_S is not None:  # top of a sharded build: the shards' S blocks
+        ptrs = (C.c_void_p * len(shard_S))()
+        on_dev = None
+        for i, S in enumerate(shard_S):
+            try:
+                import torch
+                is_t = isinstance(S, torch.Tensor)
+            except ImportError:  # pragma: no cover
+                is_t = False
+            if is_t:
+                S = S.t().contiguous().t() if S.stride(0) != 1 else S  # column-major
+                dev = bool(S.is_cuda)
+                ptrs[i] = S.data_ptr()
+            else:
+                S = np.asfortranarray(S, dtype=np.float64)
+                dev = False
+                ptrs[i] = S.ctypes.data
+            if on_dev is None:
+                on_dev = dev
+            elif on_dev != dev:
+                raise ValueError("build: shard S blocks must all be host or all device arrays")
+            keep.append(S)
+        prob.shard_S = ptrs
+        prob.shard_S_on_device = 1 if on_dev else 0
+    opts = L.dtn_opts(0, tree.n_leaf, tree.leaf_side, 1 if want_G else 0, micro_max, 1 if profile else 0, 0.0, 0,
+                      nshards, shard)
     h = C.c_void_p()
     ctx.check(L.lib().dtn_gpu_build(ctx.h, C.byref(prob), C.byref(opts), C.byref(h)))
     return SolutionOperator(ctx, h, tree.n, want_G)
