@@ -13,8 +13,8 @@ DtN matrix S and the solution D2H inside the timed region).
 proj/src/dense_nd.cpp with OpenBLAS; the reference itself needs Eigen, which
 is not in this image) on all host cores, same metric and workload.
 
-Multi-GPU (torchrun): independent replicas, one per GPU (weak scaling);
-subtree sharding of one build is the next step.
+Multi-GPU (torchrun): one build per step, subtree-sharded over the GPUs
+(paper_1302_5995_b200/shard.py) — strong scaling.
 """
 from __future__ import annotations
 
@@ -183,9 +183,15 @@ def run_b200(args, cfg, rank, world, local):
     X_d = torch.from_numpy(X_h).to(dev).t().contiguous().t()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
 
+    from paper_1302_5995_b200 import shard as SH
+    eng_dev = SH.GpuShardEngine(None, tree, ctx=ctx, stencil_device_ptr=stencil_d.data_ptr(), device=dev)
+
     def device_step():
-        sol = dtn.build_root_gpu(None, tree, ctx=ctx, stencil_device_ptr=stencil_d.data_ptr())
-        Y = dtn.apply_dtn(sol, X_d)
+        if world == 1:
+            sol = dtn.build_root_gpu(None, tree, ctx=ctx, stencil_device_ptr=stencil_d.data_ptr())
+        else:  # subtree-sharded build: shards on every GPU, top merges + inverse on rank 0
+            sol = SH.build_distributed(eng_dev, rank, world)
+        Y = dtn.apply_dtn(sol, X_d) if sol is not None else None
         return sol, Y
 
     def barrier():
@@ -195,7 +201,8 @@ def run_b200(args, cfg, rank, world, local):
 
     for _ in range(args.warmup):
         sol, _ = device_step()
-        sol.free()
+        if sol is not None:
+            sol.free()
     barrier()
     events = []
     with ClockSampler(local) as clk:
@@ -206,8 +213,9 @@ def run_b200(args, cfg, rank, world, local):
             e0.record(stream)
             sol, Y = device_step()
             e1.record(stream)
-            stats = sol.build_stats
-            sol.free()
+            if sol is not None:
+                stats = sol.build_stats
+                sol.free()
             events.append((e0, e1))
         barrier()
     dev_ms = sum(a.elapsed_time(b) for a, b in events)
@@ -215,7 +223,11 @@ def run_b200(args, cfg, rank, world, local):
     if world > 1:
         torch.distributed.all_reduce(t_local, op=torch.distributed.ReduceOp.MAX)
     total_ms = float(t_local.item())
-    value = world * args.steps * n_int ** 2 / (total_ms * 1e-3)
+    # world == 1: one build per step; world > 1: ONE sharded build of the same
+    # problem per step over all GPUs (strong scaling)
+    value = args.steps * n_int ** 2 / (total_ms * 1e-3)
+    if rank != 0:
+        stats = {"launches": 0}
     launches_per_step = stats["launches"] + 1
 
     # ---- e2e through the public API, host (pinned) buffers
@@ -224,25 +236,31 @@ def run_b200(args, cfg, rank, world, local):
     op_h = dtn.DiscreteOperator(op.n, op.h, op.mode, pin_st)
     pin_x = torch.empty((nvec, nb), dtype=torch.float64, pin_memory=True).numpy().T
     pin_x[...] = X_h
+    eng_host = SH.GpuShardEngine(op_h, tree, ctx=ctx, device=dev)
+
+    def e2e_step():
+        if world == 1:
+            s = dtn.build_root_gpu(op_h, tree, ctx=ctx)
+        else:
+            s = SH.build_distributed(eng_host, rank, world)
+        if s is not None:
+            dtn.apply_dtn(s, pin_x)
+            s.S_dense
+            s.free()
+
     for _ in range(max(1, args.warmup // 2)):
-        s = dtn.build_root_gpu(op_h, tree, ctx=ctx)
-        dtn.apply_dtn(s, pin_x)
-        s.S_dense
-        s.free()
+        e2e_step()
     barrier()
     e2e_times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        s = dtn.build_root_gpu(op_h, tree, ctx=ctx)
-        Yh = dtn.apply_dtn(s, pin_x)
-        Sh = s.S_dense
+        e2e_step()
         torch.cuda.synchronize(dev)
         e2e_times.append(time.perf_counter() - t0)
-        s.free()
     t_e2e = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(t_e2e, op=torch.distributed.ReduceOp.MAX)
-    e2e_value = world * args.steps * n_int ** 2 / float(t_e2e.item())
+    e2e_value = args.steps * n_int ** 2 / float(t_e2e.item())
 
     # ---- per-kernel roofline from one profiled build (not timed above)
     prof = dtn.build_root_gpu(None, tree, ctx=ctx, stencil_device_ptr=stencil_d.data_ptr(), profile=True)
@@ -273,12 +291,15 @@ def run_b200(args, cfg, rank, world, local):
     merge_tf = pst["merge_flops"] / (pst["merge_ms"] * 1e-3) / 1e12 if pst["merge_ms"] > 0 else None
     line = {
         "metric": METRIC, "value": value, "unit": "grid-points/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE config shapes)",
         "config": {"workload": f"config{args.config}: {cfg['name']} n={n_int} interior (ref n={n}), "
                                f"{cfg['leaf']}x{cfg['leaf']} leaves, dense FP64 merges, G applied to "
                                f"{nvec} uniform[-1,1] vectors",
-                   "parallelism": f"replicas x{world}", "l2": "flushed between timed steps (256 MB write)"},
+                   "parallelism": (f"subtree shards x{world} (NCCL gather of shard S to rank 0, top merges + "
+                                   f"root inverse on rank 0)" if world > 1 else "single GPU"),
+                   "l2": "flushed between timed steps (256 MB write)"},
         "e2e": {"value": e2e_value, "unit": "grid-points/s",
                 "h2d_bytes_per_step": int(op.stencil.nbytes + X_h.nbytes),
                 "d2h_bytes_per_step": int(nb * nb * 8 + nb * nvec * 8)},
