@@ -13,6 +13,7 @@
 // After the last panel the boundary block M[ni:, ni:] holds
 // S = M_bb - M_bi M_ii^{-1} M_ib (dense_nd.cpp:181) in place.
 #include <cfloat>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 
@@ -64,6 +65,40 @@ __global__ void __launch_bounds__(256) gather_kernel(KernelArgs args, const int*
 namespace cg = cooperative_groups;
 constexpr int PNT = 256, PKB = 32, PNW = PNT / 32, PMAXC = 16;
 
+// ---- DSMEM push with mbarrier completion (no cluster-wide barrier per pivot)
+__device__ __forceinline__ unsigned cluster_map(const void* p, int rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_b64(unsigned addr, unsigned long long v, unsigned mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(addr), "l"(v),
+               "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_b32(unsigned addr, unsigned v, unsigned mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(addr), "r"(v),
+               "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arm(unsigned long long* b, unsigned tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+
 __device__ __forceinline__ int* move_list(const KernelArgs& args, const NodeDev& nd) {
   return args.piv + nd.piv_off + ((nd.ni + 3) & ~3);
 }
@@ -95,6 +130,7 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
   __shared__ unsigned skey[2][NSLOT], sklo[2][NSLOT];
   __shared__ int spos[2][NSLOT];
   __shared__ int sp[PKB], vac[PKB];
+  __shared__ __align__(8) unsigned long long mbar[2];
   const int crank = CL ? int(cg::this_cluster().block_rank()) : 0;
   const int node_id = list[blockIdx.x / csize];
   const NodeDev nd = args.nodes[node_id];
@@ -122,6 +158,18 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
   double pmin = k0 == 0 ? DBL_MAX : args.pivstat[2 * node_id];
   double pmax = k0 == 0 ? 0.0 : args.pivstat[2 * node_id + 1];
   bool bad = false;
+  // every CTA receives csize candidates per pivot: 32 row doubles + key, lo, pos
+  const unsigned tx_bytes = unsigned(csize) * (PKB * 8 + 12);
+  if constexpr (CL) {
+    if (tid == 0) {
+      mbar_init(&mbar[0], 1);
+      mbar_init(&mbar[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_arm(&mbar[0], tx_bytes);
+      mbar_arm(&mbar[1], tx_bytes);
+    }
+    cg::this_cluster().sync();  // all barriers armed before any push
+  }
 
 #pragma unroll
   for (int j = 0; j < PKB; ++j) {
@@ -177,20 +225,22 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
     const int bw = __ffs(__ballot_sync(0xffffffffu, lk == bkey && ll == blo && lane < PNW)) - 1;
     int slot = bw, p = spos[buf][bw];
     if constexpr (CL) {
-      // warp 0 pushes this CTA's candidate into every CTA of the cluster
+      // warp 0 pushes this CTA's candidate into slot SC+crank of every CTA
+      // with st.async; each CTA waits on its own mbarrier for all csize
+      // candidates (no cluster-wide barrier on the critical path)
       if (warp == 0) {
-        cg::cluster_group cl = cg::this_cluster();
         const double rv = rows[buf][bw][lane];
         for (int d = 0; d < csize; ++d) {
-          if (lane >= j) cl.map_shared_rank(&rows[buf][SC + crank][0], d)[lane] = rv;
+          const unsigned mb = cluster_map(&mbar[buf], d);
+          st_async_b64(cluster_map(&rows[buf][SC + crank][lane], d), __double_as_longlong(rv), mb);
           if (lane == 0) {
-            *cl.map_shared_rank(&skey[buf][SC + crank], d) = bkey;
-            *cl.map_shared_rank(&sklo[buf][SC + crank], d) = blo;
-            *cl.map_shared_rank(&spos[buf][SC + crank], d) = p;
+            st_async_b32(cluster_map(&skey[buf][SC + crank], d), bkey, mb);
+            st_async_b32(cluster_map(&sklo[buf][SC + crank], d), blo, mb);
+            st_async_b32(cluster_map(&spos[buf][SC + crank], d), unsigned(p), mb);
           }
         }
       }
-      cg::this_cluster().sync();
+      mbar_wait(&mbar[buf], unsigned(j >> 1) & 1u);
       const unsigned ck = lane < csize ? skey[buf][SC + lane] : 0u;
       const unsigned cl_ = lane < csize ? sklo[buf][SC + lane] : 0u;
       const unsigned gkey = __reduce_max_sync(0xffffffffu, ck);
@@ -205,6 +255,11 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
     double pr[PKB];
 #pragma unroll
     for (int c = j; c < PKB; ++c) pr[c] = rows[buf][slot][c];
+    if constexpr (CL) {
+      // re-arm for column j + 2: remote pushes for j + 2 can only start after
+      // this CTA's own column j + 1 push, i.e. after this column is consumed
+      if (tid == 0) mbar_arm(&mbar[buf], tx_bytes);
+    }
     const double piv = pr[j];
     const double apiv = fabs(piv);
     pmin = fmin(pmin, apiv);
@@ -408,8 +463,13 @@ cudaError_t launch_gather(const KernelArgs& args, const int* d_list, int count, 
 // one row per thread up to 16 CTAs x 256 rows, two rows per thread beyond
 // (clusters of up to 16 CTAs, 8192 rows).
 void panel_shape(int max_rows, int* rpt, int* csize) {
-  *rpt = max_rows <= PMAXC * PNT ? 1 : 2;
-  *csize = (max_rows + *rpt * PNT - 1) / (*rpt * PNT);
+  // measured per-pivot cost (tools/probe/panel_probe): one CTA 0.9 us (<= 256
+  // rows), one CTA with 2 rows/thread 1.14 us (<= 512), clusters with the
+  // st.async exchange 1.3-1.6 us (2-16 CTAs x 256 rows), 2 rows/thread beyond
+  if (max_rows <= PNT) { *rpt = 1; *csize = 1; }
+  else if (max_rows <= 2 * PNT) { *rpt = 2; *csize = 1; }
+  else if (max_rows <= PMAXC * PNT) { *rpt = 1; *csize = (max_rows + PNT - 1) / PNT; }
+  else { *rpt = 2; *csize = (max_rows + 2 * PNT - 1) / (2 * PNT); }
 }
 
 template <bool CL, int RPT>
@@ -438,6 +498,7 @@ cudaError_t launch_panel(const KernelArgs& args, const int* d_list, int count, i
   int rpt, csize;
   panel_shape(max_rows, &rpt, &csize);
   if (csize > PMAXC) return cudaErrorInvalidValue;
+  if (csize == 1 && rpt == 2) return launch_panel_t<false, 2>(args, d_list, count, k0, kb, 1, st);
   if (csize == 1) return launch_panel_t<false, 1>(args, d_list, count, k0, kb, 1, st);
   if (rpt == 1) return launch_panel_t<true, 1>(args, d_list, count, k0, kb, csize, st);
   return launch_panel_t<true, 2>(args, d_list, count, k0, kb, csize, st);

@@ -8,7 +8,7 @@ using namespace dtnb;
 int main() {
   blocked_init();
   for (int kbv : {32})
-  for (int rows : {2048, 256}) {
+  for (int rows : {256, 512, 1024, 2048, 4096}) {
     const int n = rows, ld = (n + 7) / 8 * 8;
     NodeDev nd{};
     nd.kind = 2; nd.ni = n; nd.nb = 0; nd.total = n; nd.ld = nd.ldm = ld; nd.a = nd.b = -1;
@@ -34,7 +34,7 @@ int main() {
       if (r >= 2) { best = ms < best ? ms : best; tot += ms; }
     }
     int rpt, cs; panel_shape(n, &rpt, &cs);
-    printf("kb %2d rows %5d csize %2d: best %.1f us, mean %.1f us (%.2f us/column)\n", kbv, n, cs, best * 1e3, tot / reps * 1e3,
+    printf("rpt %d kb %2d rows %5d csize %2d: best %.1f us, mean %.1f us (%.2f us/column)\n", rpt, kbv, n, cs, best * 1e3, tot / reps * 1e3,
            best * 1e3 / kbv);
   }
   // empty-ish launch overhead reference
