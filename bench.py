@@ -158,6 +158,43 @@ def run_reference(args, cfg, rank, world):
 
 
 # ------------------------------------------------------------------ B200 arm
+def solve_cfg5(dtn, torch, ctx, dev, stream, rank, world, steps, warmup):
+    """configs[4]: the DtN operator of the Helmholtz kappa=100, n=2048 build
+    (dense FP64 here; the compressed engine is the next step) applied to 4096
+    seeded uniform[-1,1] Dirichlet vectors of length 4n-4, batch-sharded over
+    the ranks. Build untimed; the timed region is the batched apply (G X) from
+    HBM-resident vectors."""
+    n_int, batch = 2048, 4096
+    n = n_int + 2
+    op = dtn.discretize(dtn.baseline_problem(5, n_int))
+    st = torch.from_numpy(op.stencil).to(dev)
+    sol = dtn.build_root_gpu(None, dtn.build_tree_uniform(n, 32), ctx=ctx, stencil_device_ptr=st.data_ptr())
+    build_ms = sol.build_stats["build_ms"]
+    nb = len(sol.boundary)
+    mine = batch // world
+    X = torch.from_numpy(seeded_vectors(nb, batch)[:, rank * mine:(rank + 1) * mine]).to(dev).t().contiguous().t()
+    for _ in range(warmup):
+        dtn.apply_dtn(sol, X)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        Y = dtn.apply_dtn(sol, X)
+    e1.record(stream)
+    e1.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t.item())
+    flops = 2.0 * nb * nb * batch
+    sol.free()
+    return {"workload": f"config5: Helmholtz kappa=100 n={n_int} (dense FP64 root operator {nb}x{nb}, build "
+                        f"{build_ms:.1f} ms untimed), G applied to {batch} uniform[-1,1] vectors, batch-sharded x{world}",
+            "vectors_per_s": batch / (ms * 1e-3), "ms_per_batch": ms, "tflops": flops / (ms * 1e-3) / 1e12}
+
+
 def run_b200(args, cfg, rank, world, local):
     import torch
     import paper_1302_5995_b200 as dtn
@@ -332,6 +369,14 @@ def run_b200(args, cfg, rank, world, local):
     e1.synchronize()
     line["build"]["solve_vectors_per_s"] = reps * nvec / (e0.elapsed_time(e1) * 1e-3)
 
+    if not args.no_solve:
+        try:
+            peak_tf, _ = fp64_peak()
+            sv = solve_cfg5(dtn, torch, ctx, dev, stream, rank, world, steps=max(3, args.steps // 2), warmup=2)
+            sv["frac_fp64_peak"] = sv["tflops"] / peak_tf
+            line["solve"] = sv
+        except Exception as e:  # pragma: no cover
+            line["solve"] = {"error": str(e)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
@@ -363,6 +408,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-solve", action="store_true", help="skip the config-5 solve measurement")
     args = ap.parse_args()
     rank, world, local = dist_env()
     cfg = CONFIGS[args.config]
