@@ -26,8 +26,8 @@
 namespace dtnb {
 cudaError_t launch_small_elim(const KernelArgs&, const int*, int, int, bool, cudaStream_t);
 cudaError_t launch_gather(const KernelArgs&, const int*, int, int, cudaStream_t);
-cudaError_t launch_panel(const KernelArgs&, const int*, int, int, int, int, cudaStream_t);
-cudaError_t launch_rowpanel(const KernelArgs&, const int*, int, int, int, int, int, bool, cudaStream_t);
+cudaError_t launch_panel(const KernelArgs&, const int*, int, int, int, int, cudaStream_t, bool);
+cudaError_t launch_rowpanel(const KernelArgs&, const int*, int, int, int, int, int, bool, cudaStream_t, bool);
 cudaError_t launch_trailing_update(const KernelArgs&, const int*, int, int, int, int, int, int, cudaStream_t, int);
 cudaError_t launch_tri_inv_u_batched(const void*, int, int, cudaStream_t);
 cudaError_t launch_copy2d_batched(const void*, int, cudaStream_t);
@@ -136,13 +136,15 @@ struct PlanDev {
   CopyDesc* d_bs_copy = nullptr;
   TriDesc* d_tri = nullptr;
   double* d_W = nullptr;     // U^{-1} L^{-1} before the column permutation
-  double* d_T = nullptr;     // 128 x nb staging block of the triangular sweeps
+  double* d_LUp = nullptr;   // L_ik Linv_kk (below) and U_ik Uinv_kk (above the diagonal blocks)
+  int inv_pre = 0;           // pre-product descriptors at the front of h_inv_descs
   double* d_tinv = nullptr;  // inverses of the 128 x 128 diagonal blocks of L and U
   double* h_pivstat = nullptr;  // pinned
   unsigned long long* h_norm = nullptr;
   std::vector<cudaEvent_t> ev_wave;
   cudaEvent_t ev_start = nullptr, ev_root = nullptr, ev_end = nullptr;
   cudaEvent_t ev_rp = nullptr, ev_rest = nullptr;  // look-ahead dependencies
+  cudaEvent_t ev_rest2[2] = {nullptr, nullptr};       // fused look-ahead: side-stream step parity
   cudaStream_t side = nullptr;                      // low-priority stream for trailing updates
   cudaGraphExec_t gexec = nullptr;
   int graph_want_G = -1;
@@ -151,11 +153,11 @@ struct PlanDev {
   ~PlanDev() {
     if (gexec) cudaGraphExecDestroy(gexec);
     for (auto e : ev_wave) cudaEventDestroy(e);
-    for (auto e : {ev_start, ev_root, ev_end, ev_rp, ev_rest})
+    for (auto e : {ev_start, ev_root, ev_end, ev_rp, ev_rest, ev_rest2[0], ev_rest2[1]})
       if (e) cudaEventDestroy(e);
     if (side) cudaStreamDestroy(side);
     for (void* p : std::initializer_list<void*>{d_nodes, d_pos, d_arena, d_piv, d_pivstat, d_lists, d_stencil, d_S, d_G,
-                                                d_perm, d_norm, d_inv_descs, d_W, d_T, d_tinv, d_bs_gemm,
+                                                d_perm, d_norm, d_inv_descs, d_W, d_LUp, d_tinv, d_bs_gemm,
                                                 d_bs_copy, d_tri, d_trs})
       if (p) cudaFree(p);
     if (h_pivstat) cudaFreeHost(h_pivstat);
@@ -354,7 +356,7 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
   D->d_lists = dalloc<int>(lists.size());
   CK(cudaMemcpy(D->d_lists, lists.data(), lists.size() * sizeof(int), cudaMemcpyHostToDevice));
   D->d_arena = dalloc<double>(size_t(D->lu_off + int64_t(D->ldlu) * nb));
-  D->d_piv = dalloc<int>(size_t(P.piv_ints + align_up(nb, 4) + 128));
+  D->d_piv = dalloc<int>(size_t(P.piv_ints + align_up(nb, 4) + 256));
   {  // relocate the Schur-form descriptors (stored as arena offsets) and upload
     double* base = D->d_arena;
     auto rel = [&](auto* p) { return reinterpret_cast<decltype(p)>(base + reinterpret_cast<int64_t>(p)); };
@@ -385,27 +387,49 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
   D->d_norm = dalloc<unsigned long long>(2);
   CK(cudaMallocHost(&D->h_pivstat, 2 * D->h_nodes.size() * sizeof(double)));
   CK(cudaMallocHost(&D->h_norm, 2 * sizeof(unsigned long long)));
-  // Root inverse G = U^{-1} L^{-1} P (getri-style, 2 nb^3 flops): W = I; forward
-  // sweep over 128-row blocks using L_kk^{-1} (only the columns [0, k1) are
-  // nonzero), backward sweep with U_kk^{-1}; then G = W P (column permutation).
-  // Per block: T = Tinv_k W_k (GEMM), W_rest -= LU_block T (GEMM), W_k = T (copy).
+  // Root inverse G = U^{-1} L^{-1} P (getri-style, 2 nb^3 flops) over 128-row
+  // blocks with the diagonal-block solves deferred, so each sweep is a chain of
+  // large GEMMs only: with L'_ik = L_ik Linv_kk and U'_ik = U_ik Uinv_kk
+  // (one batched launch), the forward sweep on W = I is
+  //   W[k1:, :k1] -= L'[k1:, k] W[k, :k1]      (W_k stays unsolved),
+  // then Z_k = Linv_kk W_k for all k (batched), the backward sweep
+  //   Z[:k0, :] -= U'[:k0, k] Z[k, :],
+  // then W_k = Uinv_kk Z_k for all k (batched) and G = W P.
+  // Descriptor ranges in h_inv_descs: [0, inv_pre) pre-products, then nblk - 1
+  // forward, nblk Z solves, nblk - 1 backward, nblk final solves.
   const double* LU = D->d_arena + D->lu_off;
   D->d_W = dalloc<double>(size_t(D->ldg) * nb);
-  D->d_T = dalloc<double>(size_t(128) * nb);
+  D->d_LUp = dalloc<double>(size_t(D->ldlu) * nb);
   const int nblk = (nb + 127) / 128;
   D->d_tinv = dalloc<double>(size_t(nblk) * 2 * 128 * 128);
-  for (int kb_ = 0; kb_ < nblk; ++kb_) {  // forward
+  auto tinv = [&](int kb_, int u) { return D->d_tinv + size_t(kb_) * 2 * 128 * 128 + (u ? 128 * 128 : 0); };
+  for (int kb_ = 0; kb_ < nblk; ++kb_) {
     const int k0 = kb_ * 128, k1 = std::min(nb, k0 + 128), bk = k1 - k0;
-    const double* Linv = D->d_tinv + size_t(kb_) * 2 * 128 * 128;
-    D->h_inv_descs.push_back(GemmDesc{Linv, D->d_W + k0, D->d_T, bk, k1, bk, 128, D->ldg, 128});
-    D->h_inv_descs.push_back(GemmDesc{LU + k1 + int64_t(k0) * D->ldlu, D->d_T, D->d_W + k1, nb - k1, k1, bk, D->ldlu,
-                                      128, D->ldg});
+    if (nb - k1 > 0)
+      D->h_inv_descs.push_back(GemmDesc{LU + k1 + int64_t(k0) * D->ldlu, tinv(kb_, 0),
+                                        D->d_LUp + k1 + int64_t(k0) * D->ldlu, nb - k1, bk, bk, D->ldlu, 128, D->ldlu});
+    if (k0 > 0)
+      D->h_inv_descs.push_back(GemmDesc{LU + int64_t(k0) * D->ldlu, tinv(kb_, 1), D->d_LUp + int64_t(k0) * D->ldlu,
+                                        k0, bk, bk, D->ldlu, 128, D->ldlu});
   }
-  for (int kb_ = 0; kb_ < nblk; ++kb_) {  // backward (used in reverse order)
+  D->inv_pre = int(D->h_inv_descs.size());
+  for (int kb_ = 0; kb_ + 1 < nblk; ++kb_) {  // forward
     const int k0 = kb_ * 128, k1 = std::min(nb, k0 + 128), bk = k1 - k0;
-    const double* Uinv = D->d_tinv + size_t(kb_) * 2 * 128 * 128 + 128 * 128;
-    D->h_inv_descs.push_back(GemmDesc{Uinv, D->d_W + k0, D->d_T, bk, nb, bk, 128, D->ldg, 128});
-    D->h_inv_descs.push_back(GemmDesc{LU + int64_t(k0) * D->ldlu, D->d_T, D->d_W, k0, nb, bk, D->ldlu, 128, D->ldg});
+    D->h_inv_descs.push_back(GemmDesc{D->d_LUp + k1 + int64_t(k0) * D->ldlu, D->d_W + k0, D->d_W + k1, nb - k1, k1,
+                                      bk, D->ldlu, D->ldg, D->ldg});
+  }
+  for (int kb_ = 0; kb_ < nblk; ++kb_) {  // Z_k = Linv_kk W_k (Z in the G buffer, zero beyond column k1)
+    const int k0 = kb_ * 128, k1 = std::min(nb, k0 + 128), bk = k1 - k0;
+    D->h_inv_descs.push_back(GemmDesc{tinv(kb_, 0), D->d_W + k0, D->d_G + k0, bk, k1, bk, 128, D->ldg, D->ldg});
+  }
+  for (int kb_ = 1; kb_ < nblk; ++kb_) {  // backward (used in reverse order)
+    const int k0 = kb_ * 128, k1 = std::min(nb, k0 + 128), bk = k1 - k0;
+    D->h_inv_descs.push_back(GemmDesc{D->d_LUp + int64_t(k0) * D->ldlu, D->d_G + k0, D->d_G, k0, nb, bk, D->ldlu,
+                                      D->ldg, D->ldg});
+  }
+  for (int kb_ = 0; kb_ < nblk; ++kb_) {  // W_k = Uinv_kk Z_k
+    const int k0 = kb_ * 128, k1 = std::min(nb, k0 + 128), bk = k1 - k0;
+    D->h_inv_descs.push_back(GemmDesc{tinv(kb_, 1), D->d_G + k0, D->d_W + k0, bk, nb, bk, 128, D->ldg, D->ldg});
   }
   D->d_inv_descs = dalloc<GemmDesc>(D->h_inv_descs.size());
   CK(cudaMemcpy(D->d_inv_descs, D->h_inv_descs.data(), D->h_inv_descs.size() * sizeof(GemmDesc),
@@ -417,6 +441,8 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
   CK(cudaEventCreate(&D->ev_end));
   CK(cudaEventCreateWithFlags(&D->ev_rp, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&D->ev_rest, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&D->ev_rest2[0], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&D->ev_rest2[1], cudaEventDisableTiming));
   int lo = 0, hi = 0;
   CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   CK(cudaStreamCreateWithPriority(&D->side, cudaStreamNonBlocking, lo));
@@ -431,6 +457,11 @@ bool use_subst() {  // default: substitution (DTN_BACKSUB_SUBST=0 selects the ex
 bool use_lookahead() {
   const char* e = std::getenv("DTN_NO_LOOKAHEAD");
   return !(e && e[0] == '1');
+}
+
+bool use_fused() {  // DTN_NO_FUSED=1: the unfused look-ahead (next-panel update on the main stream)
+  const char* e = std::getenv("DTN_NO_FUSED");
+  return use_lookahead() && !(e && e[0] == '1');
 }
 
 // Per-launch profiler (opts.profile): CUDA events around every launch,
@@ -494,6 +525,39 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
                         bool swap_left, bool schur) {
     const int rows_lim = schur ? max_ni : 0;
     const int nb_rows = schur ? 0 : max_nb;
+    // Fused look-ahead (no boundary rows in the panel columns: Schur merges
+    // and the root LU): panel(s) applies step s-1 to its own columns in its
+    // prologue, so the main stream runs only the panel chain; rowpanel(s) and
+    // the trailing update of the remaining columns run on the side stream.
+    // panel(s) waits for the side stream's step s-2 (its columns' updates).
+    if (nb_rows == 0 && use_fused()) {
+      int s = 0;
+      for (int k0 = 0; k0 < max_ni; k0 += kb, ++s) {
+        double fp = 0.0, fr = 0.0, ft = 0.0;
+        for (int i = 0; i < cnt; ++i) {
+          const Node* ndp = hlst ? &P.nodes[hlst[i]] : nullptr;
+          const double ni = ndp ? ndp->ni : max_ni, tot = ndp ? ndp->total : max_total;
+          if (k0 >= ni) continue;
+          const double kbe = std::min<double>(kb, ni - k0), mn = tot - k0 - kbe, mr = ni - k0 - kbe;
+          fp += (ni - k0) * kbe * kbe;
+          if (k0 > 0) fp += 2.0 * (ni - k0) * kb * kbe + kb * kb * kbe;  // prologue
+          const double nn = std::min<double>(mr, kb);
+          fr += kbe * kbe * (mn - nn);
+          ft += 2.0 * mr * (mn - nn) * kbe;
+        }
+        if (s >= 2) CK(cudaStreamWaitEvent(st, D.ev_rest2[s & 1], 0));
+        run(K_PANEL, fp, 0.0, [&] { return launch_panel(a, lst, cnt, max_ni - k0, k0, kb, st, true); });
+        CK(cudaEventRecord(D.ev_rp, st));
+        CK(cudaStreamWaitEvent(st2, D.ev_rp, 0));
+        run_on(st2, K_ROWPANEL, fr, 0.0,
+               [&] { return launch_rowpanel(a, lst, cnt, max_total, 0, k0, kb, swap_left, st2, true); });
+        run_on(st2, K_TRAILING, ft, 0.0,
+               [&] { return launch_trailing_update(a, lst, cnt, max_total, k0, kb, -1, 1 << 30, st2, max_ni); });
+        CK(cudaEventRecord(D.ev_rest2[s & 1], st2));
+      }
+      if (s > 0) CK(cudaStreamWaitEvent(st, D.ev_rest2[(s - 1) & 1], 0));
+      return;
+    }
     bool pending = false;
     for (int k0 = 0; k0 < max_ni; k0 += kb) {
       double fp = 0.0, fr = 0.0, fn_ = 0.0, fr_ = 0.0;
@@ -510,10 +574,10 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
         fr_ += 2.0 * mr * (mn - nn) * kbe;
       }
       const bool more = k0 + kb < max_ni;
-      run(K_PANEL, fp, 0.0, [&] { return launch_panel(a, lst, cnt, max_ni - k0, k0, kb, st); });
+      run(K_PANEL, fp, 0.0, [&] { return launch_panel(a, lst, cnt, max_ni - k0, k0, kb, st, false); });
       if (pending) CK(cudaStreamWaitEvent(st, D.ev_rest, 0));
       run(K_ROWPANEL, fr, 0.0,
-          [&] { return launch_rowpanel(a, lst, cnt, max_total, nb_rows, k0, kb, swap_left, st); });
+          [&] { return launch_rowpanel(a, lst, cnt, max_total, nb_rows, k0, kb, swap_left, st, false); });
       if (more && use_lookahead()) {
         CK(cudaEventRecord(D.ev_rp, st));
         CK(cudaStreamWaitEvent(st2, D.ev_rp, 0));
@@ -609,27 +673,30 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
     run(K_INV_TRSM, double(nb) * 128 * 128, 0.0, [&] { return launch_tri_inv_blocks(LU, D.ldlu, nb, D.d_tinv, st); });
     run(K_MISC, 0.0, 8.0 * nb2, [&] { return launch_set_identity(D.d_W, D.ldg, nb, st); });
     const int nblk = (nb + 127) / 128;
-    auto gemm = [&](int di, double alpha, double beta) {
-      const GemmDesc& g = D.h_inv_descs[di];
-      if (g.m <= 0 || g.n <= 0) return;
-      run(K_INV_GEMM, 2.0 * g.m * g.n * g.k, 0.0, [&] {
-        return launch_gemm_desc(D.d_inv_descs + di, 1, gemm_tiles(g.m, g.n), g.k, alpha, beta, st, true);
+    // a batch of descriptors [d0, d0 + cnt) in one launch
+    auto gemm = [&](int d0, int cnt, double alpha, double beta) {
+      if (cnt <= 0) return;
+      int tiles = 0;
+      double f = 0.0;
+      for (int i = d0; i < d0 + cnt; ++i) {
+        const GemmDesc& g = D.h_inv_descs[i];
+        tiles = std::max(tiles, gemm_tiles(g.m, g.n));
+        f += 2.0 * g.m * g.n * g.k;
+      }
+      run(K_INV_GEMM, f, 0.0, [&] {
+        return launch_gemm_desc(D.d_inv_descs + d0, cnt, tiles, 128, alpha, beta, st, true);
       });
     };
-    for (int kb_ = 0; kb_ < nblk; ++kb_) {
-      const int k0 = kb_ * 128, k1 = std::min(nb, k0 + 128);
-      gemm(2 * kb_, 1.0, 0.0);       // T = L_kk^{-1} W[k0:k1, 0:k1]
-      gemm(2 * kb_ + 1, -1.0, 1.0);  // W[k1:, 0:k1] -= L[k1:, k0:k1] T
-      run(K_COPY, 0.0, 16.0 * (k1 - k0) * k1,
-          [&] { return launch_copy2d(D.d_T, 128, D.d_W + k0, D.ldg, k1 - k0, k1, st); });
-    }
-    for (int kb_ = nblk - 1; kb_ >= 0; --kb_) {
-      const int k0 = kb_ * 128, k1 = std::min(nb, k0 + 128);
-      gemm(2 * nblk + 2 * kb_, 1.0, 0.0);       // T = U_kk^{-1} W[k0:k1, :]
-      gemm(2 * nblk + 2 * kb_ + 1, -1.0, 1.0);  // W[:k0, :] -= U[:k0, k0:k1] T
-      run(K_COPY, 0.0, 16.0 * (k1 - k0) * nb,
-          [&] { return launch_copy2d(D.d_T, 128, D.d_W + k0, D.ldg, k1 - k0, nb, st); });
-    }
+    gemm(0, D.inv_pre, 1.0, 0.0);  // L' and U'
+    int d = D.inv_pre;
+    for (int kb_ = 0; kb_ + 1 < nblk; ++kb_) gemm(d + kb_, 1, -1.0, 1.0);  // forward sweep
+    d += nblk - 1;
+    CK(cudaMemsetAsync(D.d_G, 0, size_t(D.ldg) * nb * sizeof(double), st));
+    gemm(d, nblk, 1.0, 0.0);  // Z_k = Linv_kk W_k
+    d += nblk;
+    for (int kb_ = nblk - 1; kb_ >= 1; --kb_) gemm(d + kb_ - 1, 1, -1.0, 1.0);  // backward sweep
+    d += nblk - 1;
+    gemm(d, nblk, 1.0, 0.0);  // W_k = Uinv_kk Z_k
     run(K_COPY, 0.0, 16.0 * nb2, [&] { return launch_permute_columns(D.d_W, D.ldg, perm, nb, D.d_G, D.ldg, st); });
     CK(cudaMemsetAsync(D.d_norm, 0, 2 * sizeof(unsigned long long), st));
     run(K_MISC, 0.0, 8.0 * nb2, [&] { return launch_norm1(D.d_S, D.lds, nb, nb, D.d_norm, st); });
@@ -1126,17 +1193,21 @@ int dtn_debug_partial_lu(int32_t n, int32_t ni, const double* A, double* out, in
     NodeDev* d_node = dalloc<NodeDev>(1);
     int* d_list = dalloc<int>(1);
     double* d_a = dalloc<double>(size_t(ld) * n);
-    int* d_piv = dalloc<int>(size_t(align_up(n, 4) + 128));
+    int* d_piv = dalloc<int>(size_t(align_up(n, 4) + 256));
     double* d_ps = dalloc<double>(2);
     int zero = 0;
     CK(cudaMemcpy(d_node, &nd, sizeof(nd), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(d_list, &zero, sizeof(int), cudaMemcpyHostToDevice));
     CK(cudaMemcpy2D(d_a, size_t(ld) * 8, A, size_t(n) * 8, size_t(n) * 8, n, cudaMemcpyHostToDevice));
     KernelArgs a{d_node, nullptr, nullptr, 0, 0, d_a, d_piv, d_ps};
+    // DTN_DEBUG_LU_FUSED=1 (full LU only): the fused look-ahead sequence of
+    // the root LU, serialised on one stream
+    const char* fe = std::getenv("DTN_DEBUG_LU_FUSED");
+    const bool fused = ni == n && fe && fe[0] == '1';
     for (int k0 = 0; k0 < ni; k0 += 32) {
-      CK(launch_panel(a, d_list, 1, ni - k0, k0, 32, 0));
-      CK(launch_rowpanel(a, d_list, 1, n, n - ni, k0, 32, ni == n, 0));
-      CK(launch_trailing_update(a, d_list, 1, n, k0, 32, 0, 1 << 30, 0, 0));
+      CK(launch_panel(a, d_list, 1, ni - k0, k0, 32, 0, fused));
+      CK(launch_rowpanel(a, d_list, 1, n, n - ni, k0, 32, ni == n, 0, fused));
+      CK(launch_trailing_update(a, d_list, 1, n, k0, 32, fused ? -1 : 0, 1 << 30, 0, fused ? n : 0));
     }
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy2D(out, size_t(n) * 8, d_a, size_t(ld) * 8, size_t(n) * 8, n, cudaMemcpyDeviceToHost));

@@ -64,6 +64,10 @@ __global__ void __launch_bounds__(256) gather_kernel(KernelArgs args, const int*
 // (absolute rows) and the net row-move list consumed by rowpanel_kernel.
 namespace cg = cooperative_groups;
 constexpr int PNT = 256, PKB = 32, PNW = PNT / 32, PMAXC = 16;
+#ifndef DTN_PG
+#define DTN_PG 32
+#endif
+constexpr int PG = DTN_PG;  // pivots per unrolled group (see the pivot loop)
 
 // ---- DSMEM push with mbarrier completion (no cluster-wide barrier per pivot)
 __device__ __forceinline__ unsigned cluster_map(const void* p, int rank) {
@@ -79,6 +83,12 @@ __device__ __forceinline__ void st_async_b64(unsigned addr, unsigned long long v
 __device__ __forceinline__ void st_async_b32(unsigned addr, unsigned v, unsigned mbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(addr), "r"(v),
                "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_v4_b32(unsigned addr, unsigned a, unsigned b, unsigned c, unsigned d,
+                                                unsigned mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(addr),
+               "r"(a), "r"(b), "r"(c), "r"(d), "r"(mbar)
                : "memory");
 }
 __device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
@@ -99,13 +109,20 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
       : "memory");
 }
 
-__device__ __forceinline__ int* move_list(const KernelArgs& args, const NodeDev& nd) {
-  return args.piv + nd.piv_off + ((nd.ni + 3) & ~3);
+// Net row moves of the panel at k0 (64 dst + 64 src slots), double-buffered
+// by step parity: the next panel's prologue reads step k0's list while the
+// side stream's rowpanel(k0) may still be reading it.
+__device__ __forceinline__ int* move_list(const KernelArgs& args, const NodeDev& nd, int k0) {
+  return args.piv + nd.piv_off + ((nd.ni + 3) & ~3) + ((k0 / PKB) & 1) * 4 * PKB;
 }
 
 #ifdef DTN_PANEL_PROFILE
 __device__ long long g_panel_clk[8 * 32];
 #define PCLK(slot) do { if (blockIdx.x == 0 && tid == 0) g_panel_clk[j * 8 + (slot)] = clock64(); } while (0)
+__device__ long long g_pro_clk[8];
+#define PROCLK(slot) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_pro_clk[slot] = clock64(); } while (0)
+#else
+#define PROCLK(slot) do { } while (0)
 #endif
 
 struct PanelCand {
@@ -123,14 +140,18 @@ struct PanelCand {
 // row-move list + the node's running permutation perm[pos] = original row.
 template <bool CL, int RPT>
 __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* __restrict__ list, int k0, int kb,
-                                                   int csize) {
+                                                   int csize, int fused) {
   // row slots: [0, PNW) warp candidates, PNW + q = candidate of cluster rank q
   constexpr int SC = PNW, NSLOT = PNW + (CL ? PMAXC : 0);
   __shared__ __align__(16) double rows[2][NSLOT][PKB];
   __shared__ unsigned skey[2][NSLOT], sklo[2][NSLOT];
   __shared__ int spos[2][NSLOT];
   __shared__ int sp[PKB], vac[PKB];
+  __shared__ __align__(16) unsigned cinfo[2][CL ? PMAXC : 1][4];  // cluster candidates: key, lo, pos
   __shared__ __align__(8) unsigned long long mbar[2];
+  constexpr int PLD = PKB + 2;  // 16-byte aligned rows
+  __shared__ __align__(16) double pro[PKB * PLD];  // prologue: L11 of step k0 - kb, then U12
+  __shared__ int m_dst[2 * PKB], m_src[2 * PKB];
   const int crank = CL ? int(cg::this_cluster().block_rank()) : 0;
   const int node_id = list[blockIdx.x / csize];
   const NodeDev nd = args.nodes[node_id];
@@ -147,19 +168,94 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
 
   double v[RPT][PKB];
   int elim[RPT];
+  if (k0 == 0 || !fused) {
+#pragma unroll
+    for (int a = 0; a < RPT; ++a) {
+      const int r = crank * PNT + tid + stride * a;  // original panel row
+#pragma unroll
+      for (int c = 0; c < PKB; ++c) v[a][c] = (r < Ri && c < kbe) ? M[r + c * ldm] : 0.0;
+      if (k0 == 0 && r < Ri) perm[r] = r;
+    }
+  } else {
+    // ---- fused prologue: step kp = k0 - kb is applied to this panel's
+    // columns here -- its row moves, U12 = L11^{-1} (P A)[kp:k0, cols] and the
+    // rank-kb update with L21 -- so the panel chain never waits for the
+    // rowpanel / trailing kernels, which handle the other columns of step kp
+    // on the side stream concurrently with this panel.
+    const int kp = k0 - kb;  // step kp was a full-width step (k0 < ni)
+    PROCLK(0);
+    const int* mvp = move_list(args, nd, kp);
+    if (tid < 2 * PKB) {
+      m_dst[tid] = mvp[tid];
+      m_src[tid] = mvp[2 * PKB + tid];
+    }
+    double* Mg = args.arena + nd.m_off;  // absolute indexing
+    for (int e = tid; e < PKB * PKB; e += PNT) {
+      const int i = e % PKB, m = e / PKB;
+      pro[i * PLD + m] = (m < i && i < kb) ? Mg[(kp + i) + (long long)(kp + m) * ldm] : 0.0;
+    }
+    __syncthreads();
+    PROCLK(1);
+    if (warp == 0) {  // lane = column: U12 = L11^{-1} (moved top rows); slot i moves a row into kp + i
+      const bool live = lane < kbe;
+      double x[PKB];
+#pragma unroll
+      for (int i = 0; i < PKB; ++i)
+        x[i] = (live && i < kb) ? Mg[m_src[i] + (long long)(k0 + lane) * ldm] : 0.0;
+#pragma unroll
+      for (int m = 0; m < PKB - 1; ++m)
+#pragma unroll
+        for (int i = m + 1; i < PKB; ++i) x[i] = fma(-pro[i * PLD + m], x[m], x[i]);
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < PKB; ++i) pro[i * PLD + lane] = x[i];  // U12[i][c]; written to M after the loop
+    }
+    __syncthreads();
+    PROCLK(2);
+#pragma unroll
+    for (int a = 0; a < RPT; ++a) {
+      const int r = crank * PNT + tid + stride * a;
+      if (r < Ri) {
+        const long long R = k0 + r;
+        int src = int(R);
+#pragma unroll 4
+        for (int t = PKB; t < 2 * PKB; ++t)  // vacated positions (>= kp + kb)
+          if (m_dst[t] == R) src = m_src[t];
+        double lrow[PKB];
+#pragma unroll
+        for (int m = 0; m < PKB; ++m) lrow[m] = m < kb ? Mg[R + (long long)(kp + m) * ldm] : 0.0;
+#pragma unroll
+        for (int c = 0; c < PKB; ++c) v[a][c] = c < kbe ? Mg[src + (long long)(k0 + c) * ldm] : 0.0;
+#pragma unroll
+        for (int m = 0; m < PKB; ++m) {
+          const double2* u2 = reinterpret_cast<const double2*>(pro + m * PLD);
+#pragma unroll
+          for (int c2 = 0; c2 < PKB / 2; ++c2) {
+            const double2 u = u2[c2];
+            v[a][2 * c2] = fma(-lrow[m], u.x, v[a][2 * c2]);
+            v[a][2 * c2 + 1] = fma(-lrow[m], u.y, v[a][2 * c2 + 1]);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < PKB; ++c)
+          if (c >= kbe) v[a][c] = 0.0;
+      } else {
+#pragma unroll
+        for (int c = 0; c < PKB; ++c) v[a][c] = 0.0;
+      }
+    }
+  }
 #pragma unroll
   for (int a = 0; a < RPT; ++a) {
-    const int r = crank * PNT + tid + stride * a;  // original panel row
-#pragma unroll
-    for (int c = 0; c < PKB; ++c) v[a][c] = (r < Ri && c < kbe) ? M[r + c * ldm] : 0.0;
+    const int r = crank * PNT + tid + stride * a;
     elim[a] = (r < Ri) ? -1 : PKB;  // step at which this row became a pivot
-    if (k0 == 0 && r < Ri) perm[r] = r;
   }
+  PROCLK(3);
   double pmin = k0 == 0 ? DBL_MAX : args.pivstat[2 * node_id];
   double pmax = k0 == 0 ? 0.0 : args.pivstat[2 * node_id + 1];
   bool bad = false;
   // every CTA receives csize candidates per pivot: 32 row doubles + key, lo, pos
-  const unsigned tx_bytes = unsigned(csize) * (PKB * 8 + 12);
+  const unsigned tx_bytes = unsigned(csize) * (PKB * 8 + 16);
   if constexpr (CL) {
     if (tid == 0) {
       mbar_init(&mbar[0], 1);
@@ -171,9 +267,20 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
     cg::this_cluster().sync();  // all barriers armed before any push
   }
 
+  // Columns are processed in PKB / PG groups of PG pivots. The group body is
+  // unrolled over t (compile-time register slots) but the group loop is not:
+  // after each group the row registers rotate left by PG, so logical column
+  // PG*g + t always sits in slot t and finished columns collect at the tail
+  // (slots >= lim, masked out of the updates). This keeps the loop body small
+  // enough for the instruction cache; a fully unrolled 32-step loop stalled
+  // on instruction fetch (stall_no_inst) for most of each step.
+#pragma unroll 1
+  for (int g = 0; g < PKB / PG; ++g) {
+  const int lim = PKB - PG * g;
 #pragma unroll
-  for (int j = 0; j < PKB; ++j) {
-    if (j >= kbe) break;
+  for (int t = 0; t < PG; ++t) {
+    const int j = PG * g + t;
+    if (j < kbe) {
 #ifdef DTN_PANEL_PROFILE
     PCLK(0);
 #endif
@@ -187,7 +294,7 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
     int ba = 0;
 #pragma unroll
     for (int a = 0; a < RPT; ++a) {
-      const double ax = fabs(v[a][j]);
+      const double ax = fabs(v[a][t]);
       const unsigned ka = elim[a] < 0 ? (unsigned(__double2hiint(ax)) | 0x80000000u) : 0u;
       const unsigned kl = unsigned(__double2loint(ax));
       if (ka > key || (ka == key && kl > klo)) { key = ka; klo = kl; ba = a; }
@@ -204,7 +311,7 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
       for (int a = 0; a < RPT; ++a)
         if (a == ba) {
 #pragma unroll
-          for (int c = j; c < PKB; ++c) rows[buf][warp][c] = v[a][c];
+          for (int c = t; c < PKB; ++c) rows[buf][warp][c] = v[a][c];
         }
       skey[buf][warp] = wkey;
       sklo[buf][warp] = wlo;
@@ -228,39 +335,37 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
       // warp 0 pushes this CTA's candidate into slot SC+crank of every CTA
       // with st.async; each CTA waits on its own mbarrier for all csize
       // candidates (no cluster-wide barrier on the critical path)
-      if (warp == 0) {
+      // (warp w serves destinations w, w + PNW: the push is not serialised
+      // in one warp; key, lo and pos travel as one 16-byte store)
+      {
         const double rv = rows[buf][bw][lane];
-        for (int d = 0; d < csize; ++d) {
+        for (int d = warp; d < csize; d += PNW) {
           const unsigned mb = cluster_map(&mbar[buf], d);
           st_async_b64(cluster_map(&rows[buf][SC + crank][lane], d), __double_as_longlong(rv), mb);
-          if (lane == 0) {
-            st_async_b32(cluster_map(&skey[buf][SC + crank], d), bkey, mb);
-            st_async_b32(cluster_map(&sklo[buf][SC + crank], d), blo, mb);
-            st_async_b32(cluster_map(&spos[buf][SC + crank], d), unsigned(p), mb);
-          }
+          if (lane == 0) st_async_v4_b32(cluster_map(&cinfo[buf][crank][0], d), bkey, blo, unsigned(p), 0u, mb);
         }
       }
       mbar_wait(&mbar[buf], unsigned(j >> 1) & 1u);
-      const unsigned ck = lane < csize ? skey[buf][SC + lane] : 0u;
-      const unsigned cl_ = lane < csize ? sklo[buf][SC + lane] : 0u;
+      const unsigned ck = lane < csize ? cinfo[buf][lane][0] : 0u;
+      const unsigned cl_ = lane < csize ? cinfo[buf][lane][1] : 0u;
       const unsigned gkey = __reduce_max_sync(0xffffffffu, ck);
       const unsigned glo = __reduce_max_sync(0xffffffffu, ck == gkey ? cl_ : 0u);
       const int cw = __ffs(__ballot_sync(0xffffffffu, ck == gkey && cl_ == glo && lane < csize)) - 1;
       slot = SC + cw;
-      p = spos[buf][slot];
+      p = int(cinfo[buf][cw][2]);
     }
 #ifdef DTN_PANEL_PROFILE
     PCLK(4);
 #endif
     double pr[PKB];
 #pragma unroll
-    for (int c = j; c < PKB; ++c) pr[c] = rows[buf][slot][c];
+    for (int c = t; c < PKB; ++c) pr[c] = c < lim ? rows[buf][slot][c] : 0.0;
     if constexpr (CL) {
       // re-arm for column j + 2: remote pushes for j + 2 can only start after
       // this CTA's own column j + 1 push, i.e. after this column is consumed
       if (tid == 0) mbar_arm(&mbar[buf], tx_bytes);
     }
-    const double piv = pr[j];
+    const double piv = pr[t];
     const double apiv = fabs(piv);
     pmin = fmin(pmin, apiv);
     pmax = fmax(pmax, apiv);
@@ -274,10 +379,10 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
       const int r = crank * PNT + tid + stride * a;
       if (r == p) elim[a] = j;
       if (elim[a] < 0) {
-        const double l = v[a][j] * rinv;
-        v[a][j] = l;
+        const double l = v[a][t] * rinv;
+        v[a][t] = l;
 #pragma unroll
-        for (int c = j + 1; c < PKB; ++c) v[a][c] = fma(-l, pr[c], v[a][c]);
+        for (int c = t + 1; c < PKB; ++c) v[a][c] = fma(-l, pr[c], v[a][c]);
       }
     }
 #ifdef DTN_PANEL_PROFILE
@@ -287,8 +392,28 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
 #ifdef DTN_PANEL_PROFILE
     PCLK(7);
 #endif
+    }
+  }
+  // rotate: the finished group moves to the tail
+#pragma unroll
+  for (int a = 0; a < RPT; ++a) {
+    double tmp[PG];
+#pragma unroll
+    for (int q = 0; q < PG; ++q) tmp[q] = v[a][q];
+#pragma unroll
+    for (int q = 0; q < PKB - PG; ++q) v[a][q] = v[a][q + PG];
+#pragma unroll
+    for (int q = 0; q < PG; ++q) v[a][PKB - PG + q] = tmp[q];
+  }
   }
   __syncthreads();
+  if (fused && k0 > 0 && crank == 0) {  // U12 of the prologue into rows [k0 - kb, k0)
+    double* Mg = args.arena + nd.m_off;
+    for (int e = tid; e < PKB * PKB; e += PNT) {
+      const int i = e % PKB, c = e / PKB;
+      if (i < kb && c < kbe) Mg[(k0 - kb + i) + (long long)(k0 + c) * ldm] = pro[i * PLD + c];
+    }
+  }
   // ---- final placement: pivot of step e -> position e; the top rows [0, kbe)
   // that were not pivots fill, in order, the positions vacated by pivots that
   // came from rows >= kbe (also in order)
@@ -307,7 +432,7 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
   for (int e = 0; e < PKB; ++e)
     if (e < kbe && sp[e] < kbe) topmask |= 1u << sp[e];
   __syncthreads();
-  int* mv = move_list(args, nd);
+  int* mv = move_list(args, nd, k0);
   int fp[RPT];
 #pragma unroll
   for (int a = 0; a < RPT; ++a) {
@@ -366,7 +491,7 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
 // with swap_left, also the row swaps of the already factored columns [0, k0)
 // (needed only when L itself is reused: the root LU for G = S^{-1}).
 __global__ void __launch_bounds__(RP_THREADS) rowpanel_kernel(KernelArgs args, const int* __restrict__ list, int k0,
-                                                              int kb, int ncoltiles, int nlefttiles) {
+                                                              int kb, int ncoltiles, int nlefttiles, int skip_next) {
   __shared__ double T[32][33];
   __shared__ int s_dst[64], s_src[64];
   const NodeDev nd = args.nodes[list[blockIdx.y]];
@@ -401,10 +526,12 @@ __global__ void __launch_bounds__(RP_THREADS) rowpanel_kernel(KernelArgs args, c
     return;
   }
   const bool left = bx >= ncoltiles;
-  const int jbase = left ? (bx - ncoltiles) * RP_COLS : k1 + bx * RP_COLS;
+  // skip_next: the next panel (fused prologue) owns columns [k1, k1 + min(kb, ni - k1))
+  const int cs = k1 + (skip_next ? min(kb, max(nd.ni - k1, 0)) : 0);
+  const int jbase = left ? (bx - ncoltiles) * RP_COLS : cs + bx * RP_COLS;
   const int jend = left ? k0 : nd.total;
   if (jbase >= jend) return;
-  const int* mv = move_list(args, nd);
+  const int* mv = move_list(args, nd, k0);
   if (tid < 64) {
     s_dst[tid] = mv[tid];
     s_src[tid] = mv[64 + tid];
@@ -474,7 +601,7 @@ void panel_shape(int max_rows, int* rpt, int* csize) {
 
 template <bool CL, int RPT>
 cudaError_t launch_panel_t(const KernelArgs& args, const int* d_list, int count, int k0, int kb, int csize,
-                           cudaStream_t st) {
+                           cudaStream_t st, bool fused) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(count * csize);
   cfg.blockDim = dim3(PNT);
@@ -488,31 +615,33 @@ cudaError_t launch_panel_t(const KernelArgs& args, const int* d_list, int count,
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  return cudaLaunchKernelEx(&cfg, panel_kernel<CL, RPT>, args, d_list, k0, kb, csize);
+  return cudaLaunchKernelEx(&cfg, panel_kernel<CL, RPT>, args, d_list, k0, kb, csize, fused ? 1 : 0);
 }
 
+// fused: apply step k0 - kb to this panel's columns first (the look-ahead
+// prologue); the matching rowpanel / trailing launches skip those columns.
 cudaError_t launch_panel(const KernelArgs& args, const int* d_list, int count, int max_rows, int k0, int kb,
-                         cudaStream_t st) {
+                         cudaStream_t st, bool fused) {
   if (count <= 0) return cudaSuccess;
   if (kb > PKB) return cudaErrorInvalidValue;
   int rpt, csize;
   panel_shape(max_rows, &rpt, &csize);
   if (csize > PMAXC) return cudaErrorInvalidValue;
-  if (csize == 1 && rpt == 2) return launch_panel_t<false, 2>(args, d_list, count, k0, kb, 1, st);
-  if (csize == 1) return launch_panel_t<false, 1>(args, d_list, count, k0, kb, 1, st);
-  if (rpt == 1) return launch_panel_t<true, 1>(args, d_list, count, k0, kb, csize, st);
-  return launch_panel_t<true, 2>(args, d_list, count, k0, kb, csize, st);
+  if (csize == 1 && rpt == 2) return launch_panel_t<false, 2>(args, d_list, count, k0, kb, 1, st, fused);
+  if (csize == 1) return launch_panel_t<false, 1>(args, d_list, count, k0, kb, 1, st, fused);
+  if (rpt == 1) return launch_panel_t<true, 1>(args, d_list, count, k0, kb, csize, st, fused);
+  return launch_panel_t<true, 2>(args, d_list, count, k0, kb, csize, st, fused);
 }
 
 cudaError_t launch_rowpanel(const KernelArgs& args, const int* d_list, int count, int max_total, int max_nb, int k0,
-                            int kb, bool swap_left, cudaStream_t st) {
+                            int kb, bool swap_left, cudaStream_t st, bool skip_next) {
   if (count <= 0) return cudaSuccess;
   const int coltiles = (max_total - k0 + RP_COLS - 1) / RP_COLS;
   const int lefttiles = swap_left ? (k0 + RP_COLS - 1) / RP_COLS : 0;
   const int rowtiles = (max_nb + RP_THREADS - 1) / RP_THREADS;
   if (coltiles + lefttiles + rowtiles <= 0) return cudaSuccess;
   dim3 grid(coltiles + lefttiles + rowtiles, count);
-  rowpanel_kernel<<<grid, RP_THREADS, 0, st>>>(args, d_list, k0, kb, coltiles, lefttiles);
+  rowpanel_kernel<<<grid, RP_THREADS, 0, st>>>(args, d_list, k0, kb, coltiles, lefttiles, skip_next ? 1 : 0);
   return cudaGetLastError();
 }
 

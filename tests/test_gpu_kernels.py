@@ -39,6 +39,22 @@ def test_full_lu_matches_scipy(n):
     assert ps[0] == pytest.approx(np.min(np.abs(np.diag(Um))))
 
 
+@pytest.mark.parametrize("n", [33, 64, 100, 600, 2100, 4100, 8190])
+def test_full_lu_fused_lookahead(n, monkeypatch):
+    """The fused look-ahead sequence (panel prologue applies the previous step
+    to its own columns; rowpanel / trailing skip them) gives a valid P A = L U."""
+    monkeypatch.setenv("DTN_DEBUG_LU_FUSED", "1")
+    rng = np.random.default_rng(n + 7)
+    A = rng.standard_normal((n, n))
+    out, ipiv, ps = gpu_partial_lu(A, n)
+    assert sorted(ipiv.tolist()) == list(range(n))
+    Lm = np.tril(out, -1) + np.eye(n)
+    Um = np.triu(out)
+    assert np.max(np.abs(Lm)) <= 1.0 + 1e-12
+    assert np.linalg.norm(Lm @ Um - A[ipiv]) / np.linalg.norm(A) <= 1e-13
+    assert ps[0] == pytest.approx(np.min(np.abs(np.diag(Um))))
+
+
 @pytest.mark.parametrize("n,ni", [(40, 12), (184, 60), (376, 124), (1528, 508), (3064, 1020), (6136, 2044)])
 def test_partial_lu_schur(n, ni):
     rng = np.random.default_rng(ni)

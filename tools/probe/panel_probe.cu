@@ -13,11 +13,11 @@ int main() {
     NodeDev nd{};
     nd.kind = 2; nd.ni = n; nd.nb = 0; nd.total = n; nd.ld = nd.ldm = ld; nd.a = nd.b = -1;
     NodeDev* dn; int* dl; double* da; double* db; int* dp; double* ds;
-    cudaMalloc(&dn, sizeof(nd)); cudaMalloc(&dl, 4); cudaMalloc(&da, sizeof(double) * ld * 32);
-    cudaMalloc(&db, sizeof(double) * ld * 32); cudaMalloc(&dp, 4 * (n + 200)); cudaMalloc(&ds, 16);
+    cudaMalloc(&dn, sizeof(nd)); cudaMalloc(&dl, 4); cudaMalloc(&da, sizeof(double) * ld * 64);
+    cudaMalloc(&db, sizeof(double) * ld * 64); cudaMalloc(&dp, 4 * (n + 200)); cudaMalloc(&ds, 16);
     int zero = 0;
     cudaMemcpy(dn, &nd, sizeof(nd), cudaMemcpyHostToDevice); cudaMemcpy(dl, &zero, 4, cudaMemcpyHostToDevice);
-    std::vector<double> h(size_t(ld) * 32);
+    std::vector<double> h(size_t(ld) * 64);
     std::mt19937_64 rng(1);
     for (auto& x : h) x = double(rng() >> 11) * 0x1.0p-53 - 0.5;
     cudaMemcpy(db, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
@@ -27,7 +27,7 @@ int main() {
     for (int r = 0; r < reps + 2; ++r) {
       cudaMemcpy(da, db, h.size() * 8, cudaMemcpyDeviceToDevice);
       cudaEventRecord(e0);
-      cudaError_t err = launch_panel(a, dl, 1, n, 0, kbv, 0);
+      cudaError_t err = launch_panel(a, dl, 1, n, 0, kbv, 0, false);
       cudaEventRecord(e1); cudaEventSynchronize(e1);
       if (err != cudaSuccess) { printf("err %s\n", cudaGetErrorString(err)); return 1; }
       float ms; cudaEventElapsedTime(&ms, e0, e1);
@@ -36,17 +36,52 @@ int main() {
     int rpt, cs; panel_shape(n, &rpt, &cs);
     printf("rpt %d kb %2d rows %5d csize %2d: best %.1f us, mean %.1f us (%.2f us/column)\n", rpt, kbv, n, cs, best * 1e3, tot / reps * 1e3,
            best * 1e3 / kbv);
-  }
-  // empty-ish launch overhead reference
   {
-    long long h[256];
-    cudaMemcpyFromSymbol(h, g_panel_clk, sizeof(h));
-    printf("phases: redux | publish | barrier | pivot-decide | rcp | update | rotate | next\n");
-    for (int j = 0; j < 32; j += 4) {
-      printf("col %2d:", j);
-      for (int q = 1; q < 8; ++q) printf(" %5lld", h[j*8+q]-h[j*8+q-1]);
-      printf(" %5lld\n", j < 31 ? h[(j+1)*8]-h[j*8+7] : 0LL);
+      long long h[256];
+      cudaMemcpyFromSymbol(h, g_panel_clk, sizeof(h));
+      printf("phases: redux | publish | barrier | pivot-decide | rcp | update | rotate | next\n");
+      for (int j = 0; j < 32; j += 4) {
+        printf("col %2d:", j);
+        for (int q = 1; q < 8; ++q) printf(" %5lld", h[j*8+q]-h[j*8+q-1]);
+        printf(" %5lld\n", j < 31 ? h[(j+1)*8]-h[j*8+7] : 0LL);
+      }
+    }
+  
+  }
+  // fused prologue: panel(32) after panel(0), with and without the prologue
+  for (int rows : {256, 512, 1024, 2048, 4096}) {
+    const int n = rows, ld = (n + 7) / 8 * 8;
+    NodeDev nd{};
+    nd.kind = 2; nd.ni = n; nd.nb = 0; nd.total = n; nd.ld = nd.ldm = ld; nd.a = nd.b = -1;
+    NodeDev* dn; int* dl; double* da; double* db; int* dp; double* ds;
+    cudaMalloc(&dn, sizeof(nd)); cudaMalloc(&dl, 4); cudaMalloc(&da, sizeof(double) * ld * 64);
+    cudaMalloc(&db, sizeof(double) * ld * 64); cudaMalloc(&dp, 4 * (n + 300)); cudaMalloc(&ds, 16);
+    int zero = 0;
+    cudaMemcpy(dn, &nd, sizeof(nd), cudaMemcpyHostToDevice); cudaMemcpy(dl, &zero, 4, cudaMemcpyHostToDevice);
+    std::vector<double> h(size_t(ld) * 64);
+    std::mt19937_64 rng(1);
+    for (auto& x : h) x = double(rng() >> 11) * 0x1.0p-53 - 0.5;
+    cudaMemcpy(db, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+    KernelArgs a{dn, nullptr, nullptr, 0, 0, da, dp, ds};
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    for (int fused = 0; fused < 2; ++fused) {
+      float best = 1e9;
+      for (int r = 0; r < 12; ++r) {
+        cudaMemcpy(da, db, h.size() * 8, cudaMemcpyDeviceToDevice);
+        launch_panel(a, dl, 1, n, 0, 32, 0, false);
+        cudaEventRecord(e0);
+        cudaError_t err = launch_panel(a, dl, 1, n - 32, 32, 32, 0, fused);
+        cudaEventRecord(e1); cudaEventSynchronize(e1);
+        if (err != cudaSuccess) { printf("err %s\n", cudaGetErrorString(err)); return 1; }
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        if (r >= 2) best = ms < best ? ms : best;
+      }
+      long long pc[8];
+      cudaMemcpyFromSymbol(pc, g_pro_clk, sizeof(pc));
+      printf("rows %5d panel(k0=32) fused=%d: best %.1f us  prologue clk: movelist+L11 %lld solve %lld update %lld\n", n,
+             fused, best * 1e3, pc[1] - pc[0], pc[2] - pc[1], pc[3] - pc[2]);
     }
   }
+  // empty-ish launch overhead reference
   printf("last error: %s\n", cudaGetErrorString(cudaGetLastError()));
 }
