@@ -32,6 +32,9 @@ cudaError_t launch_trailing_update(const KernelArgs&, const int*, int, int, int,
 cudaError_t launch_tri_inv_u_batched(const void*, int, int, cudaStream_t);
 cudaError_t launch_copy2d_batched(const void*, int, cudaStream_t);
 cudaError_t launch_trsm_upper_batched(const void*, int, int, cudaStream_t);
+cudaError_t launch_trsm_batched(const void*, int, int, int, bool, cudaStream_t);
+cudaError_t launch_block_identity(double*, int, cudaStream_t);
+cudaError_t launch_trsm_upper_ref(const void*, int, int, cudaStream_t);
 cudaError_t launch_gemm_desc(const GemmDesc*, int, int, int, double, double, cudaStream_t, bool);
 cudaError_t launch_perm_identity(const int*, int, int*, double*, int, cudaStream_t);
 cudaError_t launch_trsm_rows(const double*, int, double*, int, int, int, int, bool, cudaStream_t);
@@ -138,6 +141,8 @@ struct PlanDev {
   double* d_W = nullptr;     // U^{-1} L^{-1} before the column permutation
   double* d_LUp = nullptr;   // L_ik Linv_kk (below) and U_ik Uinv_kk (above the diagonal blocks)
   int inv_pre = 0;           // pre-product descriptors at the front of h_inv_descs
+  std::vector<TrsmDesc> h_root_trs;
+  TrsmDesc* d_root_trs = nullptr;
   double* d_tinv = nullptr;  // inverses of the 128 x 128 diagonal blocks of L and U
   double* h_pivstat = nullptr;  // pinned
   unsigned long long* h_norm = nullptr;
@@ -157,7 +162,7 @@ struct PlanDev {
       if (e) cudaEventDestroy(e);
     if (side) cudaStreamDestroy(side);
     for (void* p : std::initializer_list<void*>{d_nodes, d_pos, d_arena, d_piv, d_pivstat, d_lists, d_stencil, d_S, d_G,
-                                                d_perm, d_norm, d_inv_descs, d_W, d_LUp, d_tinv, d_bs_gemm,
+                                                d_perm, d_norm, d_inv_descs, d_W, d_LUp, d_tinv, d_root_trs, d_bs_gemm,
                                                 d_bs_copy, d_tri, d_trs})
       if (p) cudaFree(p);
     if (h_pivstat) cudaFreeHost(h_pivstat);
@@ -413,6 +418,15 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
                                         k0, bk, bk, D->ldlu, 128, D->ldlu});
   }
   D->inv_pre = int(D->h_inv_descs.size());
+  // diagonal-block inverses by substitution on identity blocks: Linv (unit
+  // lower, forward) for every block, then Uinv (backward)
+  for (int u = 0; u < 2; ++u)
+    for (int kb_ = 0; kb_ < nblk; ++kb_) {
+      const int k0 = kb_ * 128, bk = std::min(nb, k0 + 128) - k0;
+      D->h_root_trs.push_back(TrsmDesc{LU + k0 + int64_t(k0) * D->ldlu, tinv(kb_, u), D->ldlu, 128, bk, bk});
+    }
+  D->d_root_trs = dalloc<TrsmDesc>(D->h_root_trs.size());
+  CK(cudaMemcpy(D->d_root_trs, D->h_root_trs.data(), D->h_root_trs.size() * sizeof(TrsmDesc), cudaMemcpyHostToDevice));
   for (int kb_ = 0; kb_ + 1 < nblk; ++kb_) {  // forward
     const int k0 = kb_ * 128, k1 = std::min(nb, k0 + 128), bk = k1 - k0;
     D->h_inv_descs.push_back(GemmDesc{D->d_LUp + k1 + int64_t(k0) * D->ldlu, D->d_W + k0, D->d_W + k1, nb - k1, k1,
@@ -454,6 +468,11 @@ bool use_subst() {  // default: substitution (DTN_BACKSUB_SUBST=0 selects the ex
   return !(e && e[0] == '0');
 }
 
+bool env_flag(const char* name) {
+  const char* e = std::getenv(name);
+  return e && e[0] == '1';
+}
+
 bool use_lookahead() {
   const char* e = std::getenv("DTN_NO_LOOKAHEAD");
   return !(e && e[0] == '1');
@@ -468,11 +487,11 @@ bool use_fused() {  // DTN_NO_FUSED=1: the unfused look-ahead (next-panel update
 // aggregated per kernel class with the algorithmic work of each launch.
 enum KClass {
   K_SMALL = 0, K_GATHER, K_PANEL, K_ROWPANEL, K_TRAILING, K_BACKSUB, K_SCHUR, K_COPY, K_INV_TRSM, K_INV_GEMM, K_MISC,
-  K_COUNT
+  K_SUBST, K_COUNT
 };
 const char* kclass_name(int k) {
   static const char* names[K_COUNT] = {"small_elim", "gather",   "panel",    "rowpanel", "trailing_gemm", "backsub_gemm",
-                                       "schur_gemm", "copy",     "inv_trsm", "inv_gemm", "misc"};
+                                       "schur_gemm", "copy",     "inv_trsm", "inv_gemm", "misc", "backsub_subst"};
   return names[k];
 }
 struct Prof {
@@ -480,8 +499,10 @@ struct Prof {
     int kclass;
     cudaEvent_t a, b;
     double flops, bytes;
+    int wave;
   };
   std::vector<Rec> recs;
+  int wave = -1;  // current wave (root inverse: number of waves)
   ~Prof() {
     for (auto& r : recs) {
       cudaEventDestroy(r.a);
@@ -496,7 +517,7 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
   const KernelArgs a = D.args();
   int launches = 0;
   auto run_on = [&](cudaStream_t s_, int kclass, double flops, double bytes, auto&& fn) {
-    Prof::Rec r{kclass, nullptr, nullptr, flops, bytes};
+    Prof::Rec r{kclass, nullptr, nullptr, flops, bytes, prof ? prof->wave : -1};
     if (prof) {
       CK(cudaEventCreate(&r.a));
       CK(cudaEventCreate(&r.b));
@@ -604,6 +625,7 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
   const std::vector<int>& hl = D.h_lists;
   if (events) CK(cudaEventRecord(D.ev_start, st));
   for (size_t w = 0; w < D.wl.size(); ++w) {
+    if (prof) prof->wave = int(w);
     const WaveLaunch& L = D.wl[w];
     if (L.micro_cnt)
       run(K_SMALL, list_flops(hl.data() + L.micro_off, L.micro_cnt), 0.0, [&] {
@@ -632,8 +654,12 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
       for (size_t t = 0; t < L.bs_off.size(); ++t) {
         const int off = L.bs_off[t], cnt = L.bs_cnt[t];
         if (use_subst()) {
-          run(K_BACKSUB, 0.0, 0.0,
-              [&] { return launch_trsm_upper_batched(D.d_trs + L.bs_toff[t], cnt, L.bs_cols[t], st); });
+          run(K_SUBST, 0.0, 0.0,
+              [&] {
+                return env_flag("DTN_SUBST_REF")
+                           ? launch_trsm_upper_ref(D.d_trs + L.bs_toff[t], cnt, L.bs_cols[t], st)
+                           : launch_trsm_batched(D.d_trs + L.bs_toff[t], cnt, L.bs_cols[t], L.bs_k[t], false, st);
+              });
           run(K_BACKSUB, L.bs_flops[t], 0.0, [&] {
             return launch_gemm_desc(D.d_bs_gemm + D.subst_base + L.bs_soff[t], cnt, L.bs_tiles2[t], L.bs_k[t], -1.0,
                                     1.0, st, true);
@@ -662,6 +688,7 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
   const double nb2 = double(D.nb) * D.nb;
   run(K_COPY, 0.0, 16.0 * nb2, [&] { return launch_copy2d(Sview, root.ld, D.d_S, D.lds, D.nb, D.nb, st); });
   if (events) CK(cudaEventRecord(D.ev_root, st));
+  if (prof) prof->wave = int(D.wl.size());
   if (want_G) {
     const int nb = D.nb;
     double* LU = D.d_arena + D.lu_off;
@@ -670,7 +697,16 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
     blocked_lu(rl, nullptr, 1, nb, nb, 0, D.root_kb, true, false);
     // the panels maintain perm[pos] = original row of the root LU (P A = L U)
     const int* perm = D.d_piv + D.h_nodes[D.root_lu_node].piv_off;
-    run(K_INV_TRSM, double(nb) * 128 * 128, 0.0, [&] { return launch_tri_inv_blocks(LU, D.ldlu, nb, D.d_tinv, st); });
+    if (env_flag("DTN_TRIINV_REF")) {
+      run(K_INV_TRSM, 0.0, 0.0, [&] { return launch_tri_inv_blocks(LU, D.ldlu, nb, D.d_tinv, st); });
+    } else {
+      const int nblk = (nb + 127) / 128, mb = std::min(nb, 128);
+      run(K_MISC, 0.0, 0.0, [&] { return launch_block_identity(D.d_tinv, 2 * nblk, st); });
+      run(K_INV_TRSM, double(nb) * 128 * 128 / 3.0, 0.0,
+          [&] { return launch_trsm_batched(D.d_root_trs, nblk, mb, mb, true, st); });
+      run(K_INV_TRSM, double(nb) * 128 * 128 / 3.0, 0.0,
+          [&] { return launch_trsm_batched(D.d_root_trs + nblk, nblk, mb, mb, false, st); });
+    }
     run(K_MISC, 0.0, 8.0 * nb2, [&] { return launch_set_identity(D.d_W, D.ldg, nb, st); });
     const int nblk = (nb + 127) / 128;
     // a batch of descriptors [d0, d0 + cnt) in one launch
@@ -973,6 +1009,12 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
     if (prof) {
       op->kstats.assign(K_COUNT, dtn_kernel_stats{});
       for (int k = 0; k < K_COUNT; ++k) std::snprintf(op->kstats[k].name, sizeof(op->kstats[k].name), "%s", kclass_name(k));
+      // DTN_PROF_DUMP=1: the launch timeline on stderr (wave, class, start, duration)
+      const char* dump = std::getenv("DTN_PROF_DUMP");
+      if (dump && dump[0] == '1' && !prof->recs.empty())
+        for (auto& r : prof->recs)
+          std::fprintf(stderr, "prof wave %3d %-14s start %9.4f ms dur %8.4f ms gflop %8.4f\n", r.wave,
+                       kclass_name(r.kclass), ms(prof->recs.front().a, r.a), ms(r.a, r.b), r.flops * 1e-9);
       for (auto& r : prof->recs) {
         dtn_kernel_stats& ks = op->kstats[r.kclass];
         const double t = ms(r.a, r.b);

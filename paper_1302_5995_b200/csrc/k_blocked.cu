@@ -91,6 +91,18 @@ __device__ __forceinline__ void st_async_v4_b32(unsigned addr, unsigned a, unsig
                "r"(a), "r"(b), "r"(c), "r"(d), "r"(mbar)
                : "memory");
 }
+__device__ __forceinline__ void st_shared_v2_pred(double* p, double a, double b, bool pred) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n @q st.shared.v2.f64 [%0], {%1, %2};\n}" ::"r"(smem_u32(p)),
+               "d"(a), "d"(b), "r"(int(pred))
+               : "memory");
+}
+__device__ __forceinline__ void st_shared_v4u_pred(unsigned* p, unsigned a, unsigned b, unsigned c, unsigned d,
+                                                   bool pred) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n @q st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n}" ::"r"(
+                   smem_u32(p)),
+               "r"(a), "r"(b), "r"(c), "r"(d), "r"(int(pred))
+               : "memory");
+}
 __device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
 }
@@ -144,8 +156,7 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
   // row slots: [0, PNW) warp candidates, PNW + q = candidate of cluster rank q
   constexpr int SC = PNW, NSLOT = PNW + (CL ? PMAXC : 0);
   __shared__ __align__(16) double rows[2][NSLOT][PKB];
-  __shared__ unsigned skey[2][NSLOT], sklo[2][NSLOT];
-  __shared__ int spos[2][NSLOT];
+  __shared__ __align__(16) unsigned sinfo[2][PNW][4];  // warp candidates: key, lo, pos
   __shared__ int sp[PKB], vac[PKB];
   __shared__ __align__(16) unsigned cinfo[2][CL ? PMAXC : 1][4];  // cluster candidates: key, lo, pos
   __shared__ __align__(8) unsigned long long mbar[2];
@@ -306,6 +317,7 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
 #ifdef DTN_PANEL_PROFILE
     PCLK(1);
 #endif
+#ifdef DTN_PUBLISH_BRANCH
     if (lane == wlane) {
 #pragma unroll
       for (int a = 0; a < RPT; ++a)
@@ -313,10 +325,24 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
 #pragma unroll
           for (int c = t; c < PKB; ++c) rows[buf][warp][c] = v[a][c];
         }
-      skey[buf][warp] = wkey;
-      sklo[buf][warp] = wlo;
-      spos[buf][warp] = crank * PNT + tid + stride * ba;
+      sinfo[buf][warp][0] = wkey;
+      sinfo[buf][warp][1] = wlo;
+      sinfo[buf][warp][2] = unsigned(crank * PNT + tid + stride * ba);
     }
+#else
+    // branch-free publish: predicated shared stores by the winning lane (a
+    // divergent branch here cost several hundred cycles per pivot)
+    {
+      const bool win = lane == wlane;
+#pragma unroll
+      for (int a = 0; a < RPT; ++a) {
+        const bool wa = win && a == ba;
+#pragma unroll
+        for (int c = t & ~1; c < PKB; c += 2) st_shared_v2_pred(&rows[buf][warp][c], v[a][c], v[a][c + 1], wa);
+      }
+      st_shared_v4u_pred(&sinfo[buf][warp][0], wkey, wlo, unsigned(crank * PNT + tid + stride * ba), 0u, win);
+    }
+#endif
 #ifdef DTN_PANEL_PROFILE
     PCLK(2);
 #endif
@@ -325,12 +351,12 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
     PCLK(3);
 #endif
     // ---- CTA argmax (every warp, redundantly)
-    const unsigned lk = lane < PNW ? skey[buf][lane] : 0u;
-    const unsigned ll = lane < PNW ? sklo[buf][lane] : 0u;
+    const unsigned lk = lane < PNW ? sinfo[buf][lane][0] : 0u;
+    const unsigned ll = lane < PNW ? sinfo[buf][lane][1] : 0u;
     const unsigned bkey = __reduce_max_sync(0xffffffffu, lk);
     const unsigned blo = __reduce_max_sync(0xffffffffu, lk == bkey ? ll : 0u);
     const int bw = __ffs(__ballot_sync(0xffffffffu, lk == bkey && ll == blo && lane < PNW)) - 1;
-    int slot = bw, p = spos[buf][bw];
+    int slot = bw, p = int(sinfo[buf][bw][2]);
     if constexpr (CL) {
       // warp 0 pushes this CTA's candidate into slot SC+crank of every CTA
       // with st.async; each CTA waits on its own mbarrier for all csize
@@ -381,8 +407,12 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
       if (elim[a] < 0) {
         const double l = v[a][t] * rinv;
         v[a][t] = l;
+#if defined(DTN_ABL) && DTN_ABL == 1
+        v[a][t + 1 < PKB ? t + 1 : t] = fma(-l, pr[t + 1 < PKB ? t + 1 : t], v[a][t + 1 < PKB ? t + 1 : t]);
+#else
 #pragma unroll
         for (int c = t + 1; c < PKB; ++c) v[a][c] = fma(-l, pr[c], v[a][c]);
+#endif
       }
     }
 #ifdef DTN_PANEL_PROFILE

@@ -29,8 +29,12 @@ if __name__ == "__main__":
         nint, micro, cfg = map(int, sys.argv[1:4])
         print(json.dumps(run(nint, micro, cfg)))
         sys.exit(0)
-    for env, nint, micro, cfg in [({}, 512, 0, 3), ({"DTN_NO_LOOKAHEAD": "1", "DTN_NO_GRAPH": "1"}, 512, 0, 3),
-                                   ({}, 512, 16, 3), ({}, 512, 160, 3), ({}, 512, 0, 2), ({}, 256, 0, 3)]:
+    exps = [({}, 512, 0, 3), ({"DTN_NO_LOOKAHEAD": "1", "DTN_NO_GRAPH": "1"}, 512, 0, 3),
+            ({}, 512, 16, 3), ({}, 512, 160, 3), ({}, 512, 0, 2), ({}, 256, 0, 3)]
+    if os.environ.get("AB_SET") == "backsub":
+        exps = [(e, nint, 0, cfg) for nint, cfg in ((512, 2), (512, 3), (1024, 3))
+                for e in ({}, {"DTN_BACKSUB_SUBST": "0"}, {"DTN_NO_FUSED": "1"})]
+    for env, nint, micro, cfg in exps:
         e = dict(os.environ); e.update(env)
         out = subprocess.run([sys.executable, __file__, str(nint), str(micro), str(cfg)], env=e, capture_output=True, text=True)
         print(env, nint, micro, cfg, out.stdout.strip() or out.stderr[-300:], flush=True)
