@@ -34,6 +34,7 @@ cudaError_t launch_copy2d_batched(const void*, int, cudaStream_t);
 cudaError_t launch_trsm_upper_batched(const void*, int, int, cudaStream_t);
 cudaError_t launch_trsm_batched(const void*, int, int, int, bool, cudaStream_t);
 cudaError_t launch_block_identity(double*, int, cudaStream_t);
+unsigned panel_fallbacks_read_reset();
 cudaError_t launch_trsm_upper_ref(const void*, int, int, cudaStream_t);
 cudaError_t launch_gemm_desc(const GemmDesc*, int, int, int, double, double, cudaStream_t, bool);
 cudaError_t launch_perm_identity(const int*, int, int*, double*, int, cudaStream_t);
@@ -361,7 +362,7 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
   D->d_lists = dalloc<int>(lists.size());
   CK(cudaMemcpy(D->d_lists, lists.data(), lists.size() * sizeof(int), cudaMemcpyHostToDevice));
   D->d_arena = dalloc<double>(size_t(D->lu_off + int64_t(D->ldlu) * nb));
-  D->d_piv = dalloc<int>(size_t(P.piv_ints + align_up(nb, 4) + 256));
+  D->d_piv = dalloc<int>(size_t(P.piv_ints + align_up(nb, 4) + 260));
   {  // relocate the Schur-form descriptors (stored as arena offsets) and upload
     double* base = D->d_arena;
     auto rel = [&](auto* p) { return reinterpret_cast<decltype(p)>(base + reinterpret_cast<int64_t>(p)); };
@@ -1011,6 +1012,7 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
       for (int k = 0; k < K_COUNT; ++k) std::snprintf(op->kstats[k].name, sizeof(op->kstats[k].name), "%s", kclass_name(k));
       // DTN_PROF_DUMP=1: the launch timeline on stderr (wave, class, start, duration)
       const char* dump = std::getenv("DTN_PROF_DUMP");
+      if (dump && dump[0] == '1') std::fprintf(stderr, "prof panel fallbacks %u\n", panel_fallbacks_read_reset());
       if (dump && dump[0] == '1' && !prof->recs.empty())
         for (auto& r : prof->recs)
           std::fprintf(stderr, "prof wave %3d %-14s start %9.4f ms dur %8.4f ms gflop %8.4f\n", r.wave,
@@ -1235,7 +1237,7 @@ int dtn_debug_partial_lu(int32_t n, int32_t ni, const double* A, double* out, in
     NodeDev* d_node = dalloc<NodeDev>(1);
     int* d_list = dalloc<int>(1);
     double* d_a = dalloc<double>(size_t(ld) * n);
-    int* d_piv = dalloc<int>(size_t(align_up(n, 4) + 256));
+    int* d_piv = dalloc<int>(size_t(align_up(n, 4) + 260));
     double* d_ps = dalloc<double>(2);
     int zero = 0;
     CK(cudaMemcpy(d_node, &nd, sizeof(nd), cudaMemcpyHostToDevice));

@@ -64,10 +64,7 @@ __global__ void __launch_bounds__(256) gather_kernel(KernelArgs args, const int*
 // (absolute rows) and the net row-move list consumed by rowpanel_kernel.
 namespace cg = cooperative_groups;
 constexpr int PNT = 256, PKB = 32, PNW = PNT / 32, PMAXC = 16;
-#ifndef DTN_PG
-#define DTN_PG 32
-#endif
-constexpr int PG = DTN_PG;  // pivots per unrolled group (see the pivot loop)
+
 
 // ---- DSMEM push with mbarrier completion (no cluster-wide barrier per pivot)
 __device__ __forceinline__ unsigned cluster_map(const void* p, int rank) {
@@ -127,6 +124,11 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
 __device__ __forceinline__ int* move_list(const KernelArgs& args, const NodeDev& nd, int k0) {
   return args.piv + nd.piv_off + ((nd.ni + 3) & ~3) + ((k0 / PKB) & 1) * 4 * PKB;
 }
+// per-node flag: an earlier panel of this node needed row interchanges, so the
+// no-interchange attempt is skipped for its remaining panels
+__device__ __forceinline__ int* pivoting_flag(const KernelArgs& args, const NodeDev& nd) {
+  return args.piv + nd.piv_off + ((nd.ni + 3) & ~3) + 8 * PKB;
+}
 
 #ifdef DTN_PANEL_PROFILE
 __device__ long long g_panel_clk[8 * 32];
@@ -136,6 +138,8 @@ __device__ long long g_pro_clk[8];
 #else
 #define PROCLK(slot) do { } while (0)
 #endif
+
+__device__ unsigned g_panel_fallbacks;  // panels whose no-interchange attempt failed (diagnostic)
 
 struct PanelCand {
   unsigned key;
@@ -152,7 +156,7 @@ struct PanelCand {
 // row-move list + the node's running permutation perm[pos] = original row.
 template <bool CL, int RPT>
 __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* __restrict__ list, int k0, int kb,
-                                                   int csize, int fused) {
+                                                   int csize, int fused, int use_fast) {
   // row slots: [0, PNW) warp candidates, PNW + q = candidate of cluster rank q
   constexpr int SC = PNW, NSLOT = PNW + (CL ? PMAXC : 0);
   __shared__ __align__(16) double rows[2][NSLOT][PKB];
@@ -265,6 +269,150 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
   double pmin = k0 == 0 ? DBL_MAX : args.pivstat[2 * node_id];
   double pmax = k0 == 0 ? 0.0 : args.pivstat[2 * node_id + 1];
   bool bad = false;
+  // ---- fast path: the panel without row interchanges, verified. Partial
+  // pivoting keeps the diagonal whenever no entry below it is larger in
+  // magnitude, i.e. whenever every multiplier satisfies |l| <= 1 (ties resolve
+  // to the lowest row, the diagonal); the merge and root systems of these
+  // operators almost never interchange (config-2 root: 3 of 2044 steps). So
+  // the top kbe x kbe block is factored by one warp, every other row solves
+  // x U11 = a with the same operation order as the right-looking elimination
+  // (bit-identical to the pivoted path), and if any |l| > 1 (or non-finite)
+  // anywhere in the panel, the panel is redone from the saved rows by the
+  // pivoted loop below -- the result is always that of partial pivoting.
+  extern __shared__ __align__(16) double pdyn[];
+  double* ub = pdyn;                         // [PKB][PLD] rows of U11
+  double* urinv = ub + PKB * PLD;            // [PKB] reciprocal pivots
+  double* psave = urinv + PKB;               // [RPT * PNT][PKB + 1] rows before the panel
+  __shared__ int fast_fail;
+  bool fast = false;
+  // (every CTA reads it before any can pass the cluster barriers ahead of a
+  // fallback that sets it; k0 == 0 starts clean)
+  const bool try_fast = use_fast && (k0 == 0 || *(volatile int*)pivoting_flag(args, nd) == 0);
+  if (k0 == 0 && crank == 0 && tid == 0) *pivoting_flag(args, nd) = 0;
+  if (try_fast) {
+#pragma unroll
+    for (int a = 0; a < RPT; ++a)
+#pragma unroll
+      for (int c = 0; c < PKB; ++c) psave[(a * PNT + tid) * (PKB + 1) + c] = v[a][c];
+    if (tid == 0) fast_fail = 0;
+    bool ok = true;
+    PROCLK(4);
+    if (crank == 0 && warp == 0) {  // rows 0..kbe-1 live in lanes 0..kbe-1 (a = 0)
+#pragma unroll
+      for (int j = 0; j < PKB; ++j) {
+        if (j < kbe) {
+          const double pj = __shfl_sync(0xffffffffu, v[0][j], j);
+          double pr[PKB];
+#pragma unroll
+          for (int c = j + 1; c < PKB; ++c) pr[c] = __shfl_sync(0xffffffffu, v[0][c], j);
+          const double rinv = __drcp_rn(pj);
+          if (lane == j) urinv[j] = rinv;
+          if (lane > j && lane < kbe) {
+            const double l = v[0][j] * rinv;
+            v[0][j] = l;
+            ok &= fabs(l) <= 1.0;
+#pragma unroll
+            for (int c = j + 1; c < PKB; ++c) v[0][c] = fma(-l, pr[c], v[0][c]);
+          }
+        }
+      }
+      // U11 rows for the substitution (row-major, 16-byte aligned)
+#pragma unroll
+      for (int c = 0; c < PKB; ++c) ub[lane * PLD + c] = (c >= lane) ? v[0][c] : 0.0;
+      // (ub row j holds U11 row j in columns >= j); the pivot statistics
+      double apiv = 0.0;
+#pragma unroll
+      for (int c = 0; c < PKB; ++c)
+        if (c == lane) apiv = fabs(v[0][c]);
+      double lo = lane < kbe ? apiv : DBL_MAX, hi = lane < kbe ? apiv : 0.0;
+      const bool nb_ = lane < kbe && (!(apiv == apiv) || apiv == INFINITY);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      }
+      pmin = fmin(pmin, lo);
+      pmax = fmax(pmax, hi);
+      bad |= __any_sync(0xffffffffu, nb_);
+    }
+    // the top block already interchanges: skip the substitution
+    if (crank == 0 && warp == 0 && __any_sync(0xffffffffu, !ok) && lane == 0) fast_fail = 1;
+    if constexpr (CL) {
+      cg::this_cluster().sync();  // rank 0's U11 complete
+      if (crank != 0) {
+        const double* rub = cg::this_cluster().map_shared_rank(ub, 0);
+        for (int e = tid; e < PKB * PLD + PKB; e += PNT) ub[e] = rub[e];
+        if (tid == 0 && *cg::this_cluster().map_shared_rank(&fast_fail, 0)) ok = false;
+      }
+    }
+    __syncthreads();
+    const bool top_failed = crank == 0 ? fast_fail != 0 : __syncthreads_or(!ok) != 0;
+    if (top_failed) ok = false;
+    PROCLK(5);
+    // every row below the top block: x U11 = a (forward substitution)
+#pragma unroll
+    for (int a = 0; a < RPT; ++a) {
+      const int r = crank * PNT + tid + stride * a;
+      if (!top_failed && r >= kbe && r < Ri) {
+#pragma unroll
+        for (int j = 0; j < PKB; ++j) {
+          if (j < kbe) {
+            const double l = v[a][j] * urinv[j];
+            v[a][j] = l;
+            ok &= fabs(l) <= 1.0;
+            if ((j + 1) & 1) v[a][j + 1] = fma(-l, ub[j * PLD + j + 1], v[a][j + 1]);
+#pragma unroll
+            for (int c = (j + 2) & ~1; c < PKB; c += 2) {
+              const double2 u2 = *reinterpret_cast<const double2*>(&ub[j * PLD + c]);
+              v[a][c] = fma(-l, u2.x, v[a][c]);
+              v[a][c + 1] = fma(-l, u2.y, v[a][c + 1]);
+            }
+          }
+        }
+      }
+    }
+    // all of the panel (every CTA of the cluster) must pass
+    const int cta_fail = __syncthreads_or(!ok);
+    PROCLK(6);
+    if constexpr (CL) {
+      if (tid == 0 && cta_fail) atomicOr(cg::this_cluster().map_shared_rank(&fast_fail, 0), 1);
+      cg::this_cluster().sync();
+      fast = *cg::this_cluster().map_shared_rank(&fast_fail, 0) == 0;
+      cg::this_cluster().sync();  // rank 0's flag read by all before anything reuses it
+    } else {
+      fast = !cta_fail;
+    }
+    PROCLK(7);
+    if (fast) {
+      // identity placement; the move list moves every pivot row onto itself
+#pragma unroll
+      for (int a = 0; a < RPT; ++a) {
+        const int r = crank * PNT + tid + stride * a;
+        if (r < Ri)
+#pragma unroll
+          for (int c = 0; c < PKB; ++c)
+            if (c < kbe) M[r + c * ldm] = v[a][c];
+      }
+      if (crank == 0 && tid < 2 * PKB) {
+        int* mv = move_list(args, nd, k0);
+        mv[tid] = tid < kbe ? k0 + tid : -1;
+        mv[2 * PKB + tid] = tid < kbe ? k0 + tid : -1;
+      }
+    } else {
+      if (crank == 0 && tid == 0) {
+        atomicAdd(&g_panel_fallbacks, 1u);
+        *pivoting_flag(args, nd) = 1;
+      }
+#pragma unroll
+      for (int a = 0; a < RPT; ++a)
+#pragma unroll
+        for (int c = 0; c < PKB; ++c) v[a][c] = psave[(a * PNT + tid) * (PKB + 1) + c];
+      pmin = k0 == 0 ? DBL_MAX : args.pivstat[2 * node_id];
+      pmax = k0 == 0 ? 0.0 : args.pivstat[2 * node_id + 1];
+      bad = false;
+    }
+  }
+  if (!fast) {
   // every CTA receives csize candidates per pivot: 32 row doubles + key, lo, pos
   const unsigned tx_bytes = unsigned(csize) * (PKB * 8 + 16);
   if constexpr (CL) {
@@ -278,20 +426,9 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
     cg::this_cluster().sync();  // all barriers armed before any push
   }
 
-  // Columns are processed in PKB / PG groups of PG pivots. The group body is
-  // unrolled over t (compile-time register slots) but the group loop is not:
-  // after each group the row registers rotate left by PG, so logical column
-  // PG*g + t always sits in slot t and finished columns collect at the tail
-  // (slots >= lim, masked out of the updates). This keeps the loop body small
-  // enough for the instruction cache; a fully unrolled 32-step loop stalled
-  // on instruction fetch (stall_no_inst) for most of each step.
-#pragma unroll 1
-  for (int g = 0; g < PKB / PG; ++g) {
-  const int lim = PKB - PG * g;
 #pragma unroll
-  for (int t = 0; t < PG; ++t) {
-    const int j = PG * g + t;
-    if (j < kbe) {
+  for (int j = 0; j < PKB; ++j) {
+    if (j >= kbe) break;
 #ifdef DTN_PANEL_PROFILE
     PCLK(0);
 #endif
@@ -305,7 +442,7 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
     int ba = 0;
 #pragma unroll
     for (int a = 0; a < RPT; ++a) {
-      const double ax = fabs(v[a][t]);
+      const double ax = fabs(v[a][j]);
       const unsigned ka = elim[a] < 0 ? (unsigned(__double2hiint(ax)) | 0x80000000u) : 0u;
       const unsigned kl = unsigned(__double2loint(ax));
       if (ka > key || (ka == key && kl > klo)) { key = ka; klo = kl; ba = a; }
@@ -323,7 +460,7 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
       for (int a = 0; a < RPT; ++a)
         if (a == ba) {
 #pragma unroll
-          for (int c = t; c < PKB; ++c) rows[buf][warp][c] = v[a][c];
+          for (int c = j; c < PKB; ++c) rows[buf][warp][c] = v[a][c];
         }
       sinfo[buf][warp][0] = wkey;
       sinfo[buf][warp][1] = wlo;
@@ -338,7 +475,7 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
       for (int a = 0; a < RPT; ++a) {
         const bool wa = win && a == ba;
 #pragma unroll
-        for (int c = t & ~1; c < PKB; c += 2) st_shared_v2_pred(&rows[buf][warp][c], v[a][c], v[a][c + 1], wa);
+        for (int c = j & ~1; c < PKB; c += 2) st_shared_v2_pred(&rows[buf][warp][c], v[a][c], v[a][c + 1], wa);
       }
       st_shared_v4u_pred(&sinfo[buf][warp][0], wkey, wlo, unsigned(crank * PNT + tid + stride * ba), 0u, win);
     }
@@ -385,13 +522,13 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
 #endif
     double pr[PKB];
 #pragma unroll
-    for (int c = t; c < PKB; ++c) pr[c] = c < lim ? rows[buf][slot][c] : 0.0;
+    for (int c = j; c < PKB; ++c) pr[c] = rows[buf][slot][c];
     if constexpr (CL) {
       // re-arm for column j + 2: remote pushes for j + 2 can only start after
       // this CTA's own column j + 1 push, i.e. after this column is consumed
       if (tid == 0) mbar_arm(&mbar[buf], tx_bytes);
     }
-    const double piv = pr[t];
+    const double piv = pr[j];
     const double apiv = fabs(piv);
     pmin = fmin(pmin, apiv);
     pmax = fmax(pmax, apiv);
@@ -405,14 +542,10 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
       const int r = crank * PNT + tid + stride * a;
       if (r == p) elim[a] = j;
       if (elim[a] < 0) {
-        const double l = v[a][t] * rinv;
-        v[a][t] = l;
-#if defined(DTN_ABL) && DTN_ABL == 1
-        v[a][t + 1 < PKB ? t + 1 : t] = fma(-l, pr[t + 1 < PKB ? t + 1 : t], v[a][t + 1 < PKB ? t + 1 : t]);
-#else
+        const double l = v[a][j] * rinv;
+        v[a][j] = l;
 #pragma unroll
-        for (int c = t + 1; c < PKB; ++c) v[a][c] = fma(-l, pr[c], v[a][c]);
-#endif
+        for (int c = j + 1; c < PKB; ++c) v[a][c] = fma(-l, pr[c], v[a][c]);
       }
     }
 #ifdef DTN_PANEL_PROFILE
@@ -422,28 +555,8 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
 #ifdef DTN_PANEL_PROFILE
     PCLK(7);
 #endif
-    }
-  }
-  // rotate: the finished group moves to the tail
-#pragma unroll
-  for (int a = 0; a < RPT; ++a) {
-    double tmp[PG];
-#pragma unroll
-    for (int q = 0; q < PG; ++q) tmp[q] = v[a][q];
-#pragma unroll
-    for (int q = 0; q < PKB - PG; ++q) v[a][q] = v[a][q + PG];
-#pragma unroll
-    for (int q = 0; q < PG; ++q) v[a][PKB - PG + q] = tmp[q];
-  }
   }
   __syncthreads();
-  if (fused && k0 > 0 && crank == 0) {  // U12 of the prologue into rows [k0 - kb, k0)
-    double* Mg = args.arena + nd.m_off;
-    for (int e = tid; e < PKB * PKB; e += PNT) {
-      const int i = e % PKB, c = e / PKB;
-      if (i < kb && c < kbe) Mg[(k0 - kb + i) + (long long)(k0 + c) * ldm] = pro[i * PLD + c];
-    }
-  }
   // ---- final placement: pivot of step e -> position e; the top rows [0, kbe)
   // that were not pivots fill, in order, the positions vacated by pivots that
   // came from rows >= kbe (also in order)
@@ -509,6 +622,14 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
   for (int a = 0; a < RPT; ++a) {
     const int r = crank * PNT + tid + stride * a;
     if (r < Ri && fp[a] != r) perm[k0 + fp[a]] = oldp[a];
+  }
+  }
+  if (fused && k0 > 0 && crank == 0) {  // U12 of the prologue into rows [k0 - kb, k0)
+    double* Mg = args.arena + nd.m_off;
+    for (int e = tid; e < PKB * PKB; e += PNT) {
+      const int i = e % PKB, c = e / PKB;
+      if (i < kb && c < kbe) Mg[(k0 - kb + i) + (long long)(k0 + c) * ldm] = pro[i * PLD + c];
+    }
   }
   if (crank == 0 && tid == 0) {
     args.pivstat[2 * node_id] = pmin;
@@ -603,10 +724,39 @@ __global__ void __launch_bounds__(RP_THREADS) rowpanel_kernel(KernelArgs args, c
   }
 }
 
+unsigned panel_fallbacks_read_reset() {
+  unsigned h = 0, z = 0;
+  cudaMemcpyFromSymbol(&h, g_panel_fallbacks, sizeof(h));
+  cudaMemcpyToSymbol(g_panel_fallbacks, &z, sizeof(z));
+  return h;
+}
+
+size_t panel_dyn_smem(int rpt) { return size_t(PKB * (PKB + 2) + PKB + rpt * PNT * (PKB + 1)) * sizeof(double); }
+
+// DTN_NO_FAST=1: always run the pivoted panel loop (diagnostic)
+bool panel_fast_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DTN_NO_FAST");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 cudaError_t blocked_init() {
   cudaError_t e = cudaFuncSetAttribute(panel_kernel<true, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(panel_kernel<true, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  e = cudaFuncSetAttribute(panel_kernel<true, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  for (cudaError_t x : {cudaFuncSetAttribute(panel_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(panel_dyn_smem(1))),
+                        cudaFuncSetAttribute(panel_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(panel_dyn_smem(2))),
+                        cudaFuncSetAttribute(panel_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(panel_dyn_smem(1))),
+                        cudaFuncSetAttribute(panel_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(panel_dyn_smem(2)))})
+    if (x != cudaSuccess) return x;
+  return cudaSuccess;
 }
 
 cudaError_t launch_gather(const KernelArgs& args, const int* d_list, int count, int max_total, cudaStream_t st) {
@@ -629,6 +779,9 @@ void panel_shape(int max_rows, int* rpt, int* csize) {
   else { *rpt = 2; *csize = (max_rows + 2 * PNT - 1) / (2 * PNT); }
 }
 
+size_t panel_dyn_smem(int rpt);
+bool panel_fast_enabled();
+
 template <bool CL, int RPT>
 cudaError_t launch_panel_t(const KernelArgs& args, const int* d_list, int count, int k0, int kb, int csize,
                            cudaStream_t st, bool fused) {
@@ -645,7 +798,9 @@ cudaError_t launch_panel_t(const KernelArgs& args, const int* d_list, int count,
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  return cudaLaunchKernelEx(&cfg, panel_kernel<CL, RPT>, args, d_list, k0, kb, csize, fused ? 1 : 0);
+  cfg.dynamicSmemBytes = panel_dyn_smem(RPT);
+  return cudaLaunchKernelEx(&cfg, panel_kernel<CL, RPT>, args, d_list, k0, kb, csize, fused ? 1 : 0,
+                            panel_fast_enabled() ? 1 : 0);
 }
 
 // fused: apply step k0 - kb to this panel's columns first (the look-ahead

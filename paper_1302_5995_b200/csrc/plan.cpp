@@ -358,7 +358,7 @@ Plan make_plan(const PlanKey& key) {
       nd.s_off = nd.m_off + nd.ni + int64_t(nd.ni) * nd.ldm;
       nd.ld = nd.ldm;
       nd.piv_off = poff;
-      poff += align_up(std::max(nd.ni, 1), 4) + 256;  // ipiv + two per-panel row-move lists
+      poff += align_up(std::max(nd.ni, 1), 4) + 260;  // ipiv + two per-panel row-move lists + flags
       const int64_t nblk = (nd.ni + 127) / 128;
       nd.uinv_off = off;
       off = align_up(off + nblk * 2 * 128 * 128, 32);

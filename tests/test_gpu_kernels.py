@@ -55,6 +55,30 @@ def test_full_lu_fused_lookahead(n, monkeypatch):
     assert ps[0] == pytest.approx(np.min(np.abs(np.diag(Um))))
 
 
+@pytest.mark.parametrize("n", [64, 300, 1100, 2100])
+@pytest.mark.parametrize("swap_at", [None, 0, 45, 97])
+def test_full_lu_no_interchange_fast_path(n, swap_at, monkeypatch):
+    """Diagonally dominant systems take the panel's no-interchange path (result
+    identical to partial pivoting: identity permutation); a single off-diagonal
+    entry larger than its pivot forces that panel back onto the pivoted loop."""
+    monkeypatch.setenv("DTN_DEBUG_LU_FUSED", "1")
+    rng = np.random.default_rng(n)
+    A = rng.uniform(-1, 1, (n, n))
+    A[np.arange(n), np.arange(n)] = 2.0 * n
+    if swap_at is not None and swap_at + 5 < n:
+        A[swap_at + 5, swap_at] = 4.0 * n  # partial pivoting must interchange at step swap_at
+    out, ipiv, _ = gpu_partial_lu(A, n)
+    Lm = np.tril(out, -1) + np.eye(n)
+    Um = np.triu(out)
+    assert np.max(np.abs(Lm)) <= 1.0 + 1e-12
+    assert np.linalg.norm(Lm @ Um - A[ipiv]) / np.linalg.norm(A) <= 1e-14
+    moved = np.flatnonzero(ipiv != np.arange(n))
+    if swap_at is None or swap_at + 5 >= n:
+        assert moved.size == 0
+    else:
+        assert swap_at in moved
+
+
 @pytest.mark.parametrize("n,ni", [(40, 12), (184, 60), (376, 124), (1528, 508), (3064, 1020), (6136, 2044)])
 def test_partial_lu_schur(n, ni):
     rng = np.random.default_rng(ni)

@@ -48,6 +48,38 @@ int main() {
     }
   
   }
+  // diagonally dominant panels: the no-interchange fast path succeeds
+  for (int rows : {256, 512, 1024, 2048, 4096}) {
+    const int n = rows, ld = (n + 7) / 8 * 8;
+    NodeDev nd{};
+    nd.kind = 2; nd.ni = n; nd.nb = 0; nd.total = n; nd.ld = nd.ldm = ld; nd.a = nd.b = -1;
+    NodeDev* dn; int* dl; double* da; double* db; int* dp; double* ds;
+    cudaMalloc(&dn, sizeof(nd)); cudaMalloc(&dl, 4); cudaMalloc(&da, sizeof(double) * ld * 32);
+    cudaMalloc(&db, sizeof(double) * ld * 32); cudaMalloc(&dp, 4 * (n + 300)); cudaMalloc(&ds, 16);
+    int zero = 0;
+    cudaMemcpy(dn, &nd, sizeof(nd), cudaMemcpyHostToDevice); cudaMemcpy(dl, &zero, 4, cudaMemcpyHostToDevice);
+    std::vector<double> h(size_t(ld) * 32);
+    std::mt19937_64 rng(1);
+    for (auto& x : h) x = double(rng() >> 11) * 0x1.0p-53 - 0.5;
+    for (int i = 0; i < 32; ++i) h[i + size_t(i) * ld] = 4.0 * n;
+    cudaMemcpy(db, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+    KernelArgs a{dn, nullptr, nullptr, 0, 0, da, dp, ds};
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    float best = 1e9;
+    for (int r = 0; r < 12; ++r) {
+      cudaMemcpy(da, db, h.size() * 8, cudaMemcpyDeviceToDevice);
+      cudaEventRecord(e0);
+      launch_panel(a, dl, 1, n, 0, 32, 0, false);
+      cudaEventRecord(e1); cudaEventSynchronize(e1);
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      if (r >= 2) best = ms < best ? ms : best;
+    }
+    int piv[32]; cudaMemcpy(piv, dp, sizeof(piv), cudaMemcpyDeviceToHost);
+    int moved = 0; for (int i = 0; i < 32; ++i) moved += piv[i] != i;
+    long long pc[8]; cudaMemcpyFromSymbol(pc, g_pro_clk, sizeof(pc));
+    printf("diag-dominant rows %5d: best %.1f us (rows moved %d) %s | start->save %lld topLU %lld subst %lld check %lld\n", n, best * 1e3, moved,
+           cudaGetErrorString(cudaGetLastError()), pc[4] - pc[3], pc[5] - pc[4], pc[6] - pc[5], pc[7] - pc[6]);
+  }
   // fused prologue: panel(32) after panel(0), with and without the prologue
   for (int rows : {256, 512, 1024, 2048, 4096}) {
     const int n = rows, ld = (n + 7) / 8 * 8;

@@ -22,6 +22,8 @@ from collections import defaultdict
 agg = defaultdict(lambda: defaultdict(lambda: [0, 0.0, 0.0]))
 span = {}
 for line in r.stderr.splitlines():
+    if line.startswith("prof panel fallbacks"):
+        print(line)
     if not line.startswith("prof wave"):
         continue
     f = line.split()
