@@ -1012,7 +1012,22 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
       for (int k = 0; k < K_COUNT; ++k) std::snprintf(op->kstats[k].name, sizeof(op->kstats[k].name), "%s", kclass_name(k));
       // DTN_PROF_DUMP=1: the launch timeline on stderr (wave, class, start, duration)
       const char* dump = std::getenv("DTN_PROF_DUMP");
-      if (dump && dump[0] == '1') std::fprintf(stderr, "prof panel fallbacks %u\n", panel_fallbacks_read_reset());
+      if (dump && dump[0] == '1') {
+        std::fprintf(stderr, "prof panel fallbacks %u\n", panel_fallbacks_read_reset());
+        // per wave: blocked merges whose panels needed row interchanges
+        for (size_t w = 0; w < P.waves.size(); ++w) {
+          int cnt = 0, tot = 0;
+          for (int id : P.waves[w].blocked) {
+            const Node& nd = P.nodes[id];
+            int flag = 0;
+            cudaMemcpy(&flag, D->d_piv + nd.piv_off + align_up(std::max(nd.ni, 1), 4) + 256, sizeof(int),
+                       cudaMemcpyDeviceToHost);
+            cnt += flag;
+            ++tot;
+          }
+          if (tot) std::fprintf(stderr, "prof wave %zu pivoting panels %d in %d merges\n", w, cnt, tot);
+        }
+      }
       if (dump && dump[0] == '1' && !prof->recs.empty())
         for (auto& r : prof->recs)
           std::fprintf(stderr, "prof wave %3d %-14s start %9.4f ms dur %8.4f ms gflop %8.4f\n", r.wave,

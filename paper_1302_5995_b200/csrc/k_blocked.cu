@@ -124,8 +124,9 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
 __device__ __forceinline__ int* move_list(const KernelArgs& args, const NodeDev& nd, int k0) {
   return args.piv + nd.piv_off + ((nd.ni + 3) & ~3) + ((k0 / PKB) & 1) * 4 * PKB;
 }
-// per-node flag: an earlier panel of this node needed row interchanges, so the
-// no-interchange attempt is skipped for its remaining panels
+// per-node count of panels that needed row interchanges; once it reaches the
+// launch's use_fast threshold the no-interchange attempt is skipped for the
+// node's remaining panels
 __device__ __forceinline__ int* pivoting_flag(const KernelArgs& args, const NodeDev& nd) {
   return args.piv + nd.piv_off + ((nd.ni + 3) & ~3) + 8 * PKB;
 }
@@ -167,6 +168,12 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
   constexpr int PLD = PKB + 2;  // 16-byte aligned rows
   __shared__ __align__(16) double pro[PKB * PLD];  // prologue: L11 of step k0 - kb, then U12
   __shared__ int m_dst[2 * PKB], m_src[2 * PKB];
+  // dynamic: the fast path's U11 rows and reciprocals, and per-thread row
+  // storage (the prologue's L21 rows, then the rows saved for a fallback)
+  extern __shared__ __align__(16) double pdyn[];
+  double* ub = pdyn;                         // [PKB][PLD] rows of U11
+  double* urinv = ub + PKB * PLD;            // [PKB] reciprocal pivots
+  double* psave = urinv + PKB;               // [RPT * PNT][PKB + 1] rows before the panel
   const int crank = CL ? int(cg::this_cluster().block_rank()) : 0;
   const int node_id = list[blockIdx.x / csize];
   const NodeDev nd = args.nodes[node_id];
@@ -183,6 +190,11 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
 
   double v[RPT][PKB];
   int elim[RPT];
+  // no-interchange attempt for this panel? (every CTA reads the node's count
+  // before any can pass the cluster barriers ahead of a fallback that bumps
+  // it; k0 == 0 starts clean)
+  const bool try_fast = use_fast && (k0 == 0 || *(volatile int*)pivoting_flag(args, nd) < use_fast);
+  if (k0 == 0 && crank == 0 && tid == 0) *pivoting_flag(args, nd) = 0;
   if (k0 == 0 || !fused) {
 #pragma unroll
     for (int a = 0; a < RPT; ++a) {
@@ -199,65 +211,105 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
     // on the side stream concurrently with this panel.
     const int kp = k0 - kb;  // step kp was a full-width step (k0 < ni)
     PROCLK(0);
+    double* Mg = args.arena + nd.m_off;  // absolute indexing
+    // issue every load up front: this thread's L21 rows (into its row
+    // storage) and L11 (into ub, free until the fast path) by cp.async, its
+    // rows of the panel columns speculatively from the unmoved position, the
+    // move list
+    double* l11 = ub;  // [PKB][PLD], L11[i][m] at i * PLD + m
+#pragma unroll
+    for (int a = 0; a < RPT; ++a) {
+      const int r = crank * PNT + tid + stride * a;
+      double* lr = psave + (a * PNT + tid) * (PKB + 1);
+      if (r < Ri) {
+        const long long R = k0 + r;
+        for (int m = 0; m < kb; ++m) cp_async8(lr + m, Mg + R + (long long)(kp + m) * ldm, 8);
+#pragma unroll
+        for (int c = 0; c < PKB; ++c) v[a][c] = c < kbe ? Mg[R + (long long)(k0 + c) * ldm] : 0.0;
+      } else {
+#pragma unroll
+        for (int c = 0; c < PKB; ++c) v[a][c] = 0.0;
+      }
+    }
+    for (int e = tid; e < PKB * PKB; e += PNT) {
+      const int i = e % PKB, m = e / PKB;
+      if (m < i && i < kb) cp_async8(l11 + i * PLD + m, Mg + (kp + i) + (long long)(kp + m) * ldm, 8);
+      else l11[i * PLD + m] = 0.0;
+    }
+    cp_async_commit();
     const int* mvp = move_list(args, nd, kp);
     if (tid < 2 * PKB) {
       m_dst[tid] = mvp[tid];
       m_src[tid] = mvp[2 * PKB + tid];
     }
-    double* Mg = args.arena + nd.m_off;  // absolute indexing
-    for (int e = tid; e < PKB * PKB; e += PNT) {
-      const int i = e % PKB, m = e / PKB;
-      pro[i * PLD + m] = (m < i && i < kb) ? Mg[(kp + i) + (long long)(kp + m) * ldm] : 0.0;
-    }
+    cp_async_wait<0>();
     __syncthreads();
     PROCLK(1);
-    if (warp == 0) {  // lane = column: U12 = L11^{-1} (moved top rows); slot i moves a row into kp + i
-      const bool live = lane < kbe;
-      double x[PKB];
+    // U12 = L11^{-1} (moved top rows) by all warps: warp w solves columns
+    // 4w..4w+3 with lane = row (slot i moves a row into kp + i), the solved
+    // entry of row m broadcast by shuffle at step m
+    {
+      constexpr int QC = PKB / PNW;  // columns per warp
+      const int i = lane, c0 = warp * QC;
+      const int srow = m_src[i];
+      double x[QC];
 #pragma unroll
-      for (int i = 0; i < PKB; ++i)
-        x[i] = (live && i < kb) ? Mg[m_src[i] + (long long)(k0 + lane) * ldm] : 0.0;
+      for (int q = 0; q < QC; ++q) x[q] = (i < kb && c0 + q < kbe) ? Mg[srow + (long long)(k0 + c0 + q) * ldm] : 0.0;
+#pragma unroll 4
+      for (int m = 0; m < kb - 1; ++m) {
+        const double lim = (i > m) ? l11[i * PLD + m] : 0.0;
 #pragma unroll
-      for (int m = 0; m < PKB - 1; ++m)
+        for (int q = 0; q < QC; ++q) x[q] = fma(-lim, __shfl_sync(0xffffffffu, x[q], m), x[q]);
+      }
 #pragma unroll
-        for (int i = m + 1; i < PKB; ++i) x[i] = fma(-pro[i * PLD + m], x[m], x[i]);
-      __syncwarp();
-#pragma unroll
-      for (int i = 0; i < PKB; ++i) pro[i * PLD + lane] = x[i];  // U12[i][c]; written to M after the loop
+      for (int q = 0; q < QC; ++q) pro[i * PLD + c0 + q] = x[q];  // U12[i][c]; written to M after the loop
     }
-    __syncthreads();
-    PROCLK(2);
+    // rows displaced by step kp's interchanges (rare) reload from their source
 #pragma unroll
     for (int a = 0; a < RPT; ++a) {
       const int r = crank * PNT + tid + stride * a;
       if (r < Ri) {
-        const long long R = k0 + r;
-        int src = int(R);
+        const int R = k0 + r;
+        int src = R;
 #pragma unroll 4
         for (int t = PKB; t < 2 * PKB; ++t)  // vacated positions (>= kp + kb)
           if (m_dst[t] == R) src = m_src[t];
-        double lrow[PKB];
+        if (src != R)
 #pragma unroll
-        for (int m = 0; m < PKB; ++m) lrow[m] = m < kb ? Mg[R + (long long)(kp + m) * ldm] : 0.0;
-#pragma unroll
-        for (int c = 0; c < PKB; ++c) v[a][c] = c < kbe ? Mg[src + (long long)(k0 + c) * ldm] : 0.0;
-#pragma unroll
-        for (int m = 0; m < PKB; ++m) {
-          const double2* u2 = reinterpret_cast<const double2*>(pro + m * PLD);
-#pragma unroll
-          for (int c2 = 0; c2 < PKB / 2; ++c2) {
-            const double2 u = u2[c2];
-            v[a][2 * c2] = fma(-lrow[m], u.x, v[a][2 * c2]);
-            v[a][2 * c2 + 1] = fma(-lrow[m], u.y, v[a][2 * c2 + 1]);
-          }
-        }
-#pragma unroll
-        for (int c = 0; c < PKB; ++c)
-          if (c >= kbe) v[a][c] = 0.0;
-      } else {
-#pragma unroll
-        for (int c = 0; c < PKB; ++c) v[a][c] = 0.0;
+          for (int c = 0; c < PKB; ++c) v[a][c] = c < kbe ? Mg[src + (long long)(k0 + c) * ldm] : 0.0;
       }
+    }
+    __syncthreads();
+    PROCLK(2);
+    // the fast path's top-block LU (warp 0 of rank 0) waits only for warp 0's
+    // own rows: the other warps of that CTA update theirs while it factors
+    const bool lead = try_fast && crank == 0;
+    if (lead && warp != 0) asm volatile("bar.sync 1, %0;" ::"r"(PNT) : "memory");
+    // rank-kb update with L21, rolled over m (the unrolled 1024-FMA form ran
+    // at the instruction-fetch rate)
+#pragma unroll 2
+    for (int m = 0; m < kb; ++m) {
+      double lm[RPT];
+#pragma unroll
+      for (int a = 0; a < RPT; ++a) lm[a] = psave[(a * PNT + tid) * (PKB + 1) + m];
+      const double2* u2 = reinterpret_cast<const double2*>(pro + m * PLD);
+#pragma unroll
+      for (int c2 = 0; c2 < PKB / 2; ++c2) {
+        const double2 u = u2[c2];
+#pragma unroll
+        for (int a = 0; a < RPT; ++a) {
+          v[a][2 * c2] = fma(-lm[a], u.x, v[a][2 * c2]);
+          v[a][2 * c2 + 1] = fma(-lm[a], u.y, v[a][2 * c2 + 1]);
+        }
+      }
+    }
+    if (lead && warp == 0) asm volatile("bar.arrive 1, %0;" ::"r"(PNT) : "memory");
+#pragma unroll
+    for (int a = 0; a < RPT; ++a) {
+      const int r = crank * PNT + tid + stride * a;
+#pragma unroll
+      for (int c = 0; c < PKB; ++c)
+        if (c >= kbe || r >= Ri) v[a][c] = 0.0;
     }
   }
 #pragma unroll
@@ -279,16 +331,8 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
   // (bit-identical to the pivoted path), and if any |l| > 1 (or non-finite)
   // anywhere in the panel, the panel is redone from the saved rows by the
   // pivoted loop below -- the result is always that of partial pivoting.
-  extern __shared__ __align__(16) double pdyn[];
-  double* ub = pdyn;                         // [PKB][PLD] rows of U11
-  double* urinv = ub + PKB * PLD;            // [PKB] reciprocal pivots
-  double* psave = urinv + PKB;               // [RPT * PNT][PKB + 1] rows before the panel
   __shared__ int fast_fail;
   bool fast = false;
-  // (every CTA reads it before any can pass the cluster barriers ahead of a
-  // fallback that sets it; k0 == 0 starts clean)
-  const bool try_fast = use_fast && (k0 == 0 || *(volatile int*)pivoting_flag(args, nd) == 0);
-  if (k0 == 0 && crank == 0 && tid == 0) *pivoting_flag(args, nd) = 0;
   if (try_fast) {
 #pragma unroll
     for (int a = 0; a < RPT; ++a)
@@ -401,7 +445,7 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
     } else {
       if (crank == 0 && tid == 0) {
         atomicAdd(&g_panel_fallbacks, 1u);
-        *pivoting_flag(args, nd) = 1;
+        *pivoting_flag(args, nd) += 1;
       }
 #pragma unroll
       for (int a = 0; a < RPT; ++a)
@@ -733,13 +777,14 @@ unsigned panel_fallbacks_read_reset() {
 
 size_t panel_dyn_smem(int rpt) { return size_t(PKB * (PKB + 2) + PKB + rpt * PNT * (PKB + 1)) * sizeof(double); }
 
-// DTN_NO_FAST=1: always run the pivoted panel loop (diagnostic)
-bool panel_fast_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("DTN_NO_FAST");
-    return !(e && e[0] == '1');
+// no-interchange attempts stop for a node after this many of its panels
+// needed interchanges (DTN_FAST_THRESHOLD; 0 = always run the pivoted loop)
+int panel_fast_threshold() {
+  static const int th = [] {
+    const char* e = std::getenv("DTN_FAST_THRESHOLD");
+    return e ? std::atoi(e) : 1;
   }();
-  return on;
+  return th;
 }
 
 cudaError_t blocked_init() {
@@ -780,7 +825,7 @@ void panel_shape(int max_rows, int* rpt, int* csize) {
 }
 
 size_t panel_dyn_smem(int rpt);
-bool panel_fast_enabled();
+int panel_fast_threshold();
 
 template <bool CL, int RPT>
 cudaError_t launch_panel_t(const KernelArgs& args, const int* d_list, int count, int k0, int kb, int csize,
@@ -800,7 +845,7 @@ cudaError_t launch_panel_t(const KernelArgs& args, const int* d_list, int count,
   }
   cfg.dynamicSmemBytes = panel_dyn_smem(RPT);
   return cudaLaunchKernelEx(&cfg, panel_kernel<CL, RPT>, args, d_list, k0, kb, csize, fused ? 1 : 0,
-                            panel_fast_enabled() ? 1 : 0);
+                            panel_fast_threshold());
 }
 
 // fused: apply step k0 - kb to this panel's columns first (the look-ahead

@@ -22,8 +22,9 @@ from collections import defaultdict
 agg = defaultdict(lambda: defaultdict(lambda: [0, 0.0, 0.0]))
 span = {}
 for line in r.stderr.splitlines():
-    if line.startswith("prof panel fallbacks"):
+    if line.startswith("prof panel fallbacks") or "pivoting panels" in line:
         print(line)
+        continue
     if not line.startswith("prof wave"):
         continue
     f = line.split()
