@@ -109,6 +109,15 @@ int dtn_gpu_device_ptrs(const dtn_op* op, const double** S, const double** G, in
 int dtn_gpu_export_device(const dtn_op* op, double* S, int64_t lds, double* G, int64_t ldg);
 /* Y(nb x batch) = op(X), op = G (which 0, apply_dtn) or S (which 1, apply_schur).
  * on_device: X and Y are device pointers (else host). */
+/* Dirichlet-ring DtN adapter (SURVEY f-1; not in the reference, derived from
+ * A u = -D g, grid.hpp:88-90, grid.cpp:151-166): T = (1/h)(I + P G D_b), the
+ * m x m map from Dirichlet data on the m = 4 n_int non-corner ring nodes to
+ * the one-sided normal derivative there. adj[i] = boundary position of the
+ * unknown adjacent to ring node i, coef[i] = its stencil coefficient toward
+ * the ring node. T column-major (leading dimension ldt) on the host or, with
+ * on_device, in device memory. Requires G (want_G). */
+int dtn_gpu_ring_dtn(const dtn_op* op, const int64_t* adj, const double* coef, int64_t m, double h, double* T,
+                     int64_t ldt, int on_device);
 int dtn_gpu_apply(const dtn_op* op, int which, const double* X, int64_t ldx, int64_t batch, double* Y, int64_t ldy,
                   int on_device);
 

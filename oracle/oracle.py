@@ -270,3 +270,27 @@ def rel_fro(a, b) -> float:
 
 CATALOG = ["laplace", "diffconv1", "diffconv2", "diffconv3", "diffconv4", "helmholtz1",
            "helmholtz2", "helmholtz3", "helmholtz4", "random1", "random2"]
+
+
+def ring_dtn(problem: Problem, result: DenseResult) -> np.ndarray:
+    """Dirichlet-ring DtN map on the 4 n_int non-corner ring nodes (ring_id
+    order, grid.cpp:40-47): T = (1/h)(I + P G D_b) (SURVEY f-1; follows from
+    A u = -D g, grid.hpp:88-90, with D's couplings from grid.cpp:151-157).
+    Test infrastructure: restated independently of the product's adapter."""
+    n = problem.n
+    m, s, h = n - 1, n - 2, 1.0 / (n - 1)
+    st = problem.stencil()
+    pos = {int(b): i for i, b in enumerate(result.boundary)}
+    adj, coef = [], []
+    for rid in range(4 * m):
+        side, off = divmod(rid, m)
+        if off == 0:
+            continue
+        # (unknown adjacent to the ring node, stencil row toward the ring)
+        ux, uy, r = [(off, 1, 4), (m - 1, off, 1), (m - off, m - 1, 3), (1, m - off, 2)][side]
+        uid = (uy - 1) * s + (ux - 1)
+        adj.append(pos[uid])
+        coef.append(st[r, uid])
+    adj = np.array(adj)
+    coef = np.array(coef)
+    return (np.eye(len(adj)) + result.G[np.ix_(adj, adj)] * coef[None, :]) / h

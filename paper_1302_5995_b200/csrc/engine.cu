@@ -35,6 +35,7 @@ cudaError_t launch_trsm_upper_batched(const void*, int, int, cudaStream_t);
 cudaError_t launch_trsm_batched(const void*, int, int, int, bool, cudaStream_t);
 cudaError_t launch_block_identity(double*, int, cudaStream_t);
 unsigned panel_fallbacks_read_reset();
+cudaError_t launch_ring_dtn(const double*, int, const int*, const double*, int, double, double*, long long, cudaStream_t);
 cudaError_t launch_trsm_upper_ref(const void*, int, int, cudaStream_t);
 cudaError_t launch_gemm_desc(const GemmDesc*, int, int, int, double, double, cudaStream_t, bool);
 cudaError_t launch_perm_identity(const int*, int, int*, double*, int, cudaStream_t);
@@ -1107,6 +1108,48 @@ int dtn_gpu_device_ptrs(const dtn_op* op, const double** S, const double** G, in
   if (G) *G = op->has_G ? op->plan->d_G : nullptr;
   if (ld) *ld = op->plan->lds;
   return DTN_OK;
+}
+
+int dtn_gpu_ring_dtn(const dtn_op* op, const int64_t* adj, const double* coef, int64_t m, double h, double* T,
+                     int64_t ldt, int on_device) {
+  if (!op) return DTN_EINVAL;
+  dtn_ctx* ctx = op->ctx;
+  return guarded(ctx, [&] {
+    const int nb = op->nb;
+    if (!op->has_G) throw std::invalid_argument("dtn_gpu_ring_dtn: G was not built (want_G = 0)");
+    if (m < 0 || m > (int64_t(1) << 30) || ldt < m || (m && (!adj || !coef || !T)) || !(h > 0.0))
+      throw std::invalid_argument("dtn_gpu_ring_dtn: bad arguments");
+    std::vector<int> a32(static_cast<size_t>(m));
+    for (int64_t i = 0; i < m; ++i) {
+      if (adj[i] < 0 || adj[i] >= nb) throw std::invalid_argument("dtn_gpu_ring_dtn: adjacency outside the boundary");
+      a32[size_t(i)] = int(adj[i]);
+    }
+    if (m == 0) return;
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    const PlanDev& D = *op->plan;
+    int* d_adj = nullptr;
+    double *d_coef = nullptr, *d_T = nullptr;
+    CK(cudaMallocAsync(&d_adj, size_t(m) * sizeof(int), st));
+    CK(cudaMallocAsync(&d_coef, size_t(m) * sizeof(double), st));
+    CK(cudaMemcpyAsync(d_adj, a32.data(), size_t(m) * sizeof(int), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_coef, coef, size_t(m) * sizeof(double), cudaMemcpyHostToDevice, st));
+    double* out = T;
+    int64_t ldo = ldt;
+    if (!on_device) {
+      CK(cudaMallocAsync(&d_T, size_t(m) * size_t(m) * sizeof(double), st));
+      out = d_T;
+      ldo = m;
+    }
+    CK(launch_ring_dtn(D.d_G, D.ldg, d_adj, d_coef, int(m), h, out, ldo, st));
+    if (!on_device)
+      CK(cudaMemcpy2DAsync(T, size_t(ldt) * 8, d_T, size_t(m) * 8, size_t(m) * 8, size_t(m), cudaMemcpyDeviceToHost,
+                           st));
+    CK(cudaFreeAsync(d_adj, st));
+    CK(cudaFreeAsync(d_coef, st));
+    if (d_T) CK(cudaFreeAsync(d_T, st));
+    CK(cudaStreamSynchronize(st));
+  });
 }
 
 int dtn_gpu_apply(const dtn_op* op, int which, const double* X, int64_t ldx, int64_t batch, double* Y, int64_t ldy,

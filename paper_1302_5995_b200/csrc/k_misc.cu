@@ -314,6 +314,27 @@ __global__ void __launch_bounds__(256) trsm_block_kernel(const TrsmDesc* __restr
   TSCLK(15);
 }
 
+// Dirichlet-ring DtN (SURVEY f-1): T[i][j] = (delta_ij + coef[j] G[adj[i]][adj[j]]) / h
+// for the non-corner ring nodes, T = (1/h)(I + P G D_b).
+__global__ void ring_dtn_kernel(const double* __restrict__ G, int ldg, const int* __restrict__ adj,
+                                const double* __restrict__ coef, int m, double inv_h, double* __restrict__ T, long long ldt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // consecutive threads: consecutive rows of T
+  if (i >= m) return;
+  const int ai = adj[i];
+  for (int j = blockIdx.y; j < m; j += gridDim.y) {
+    const double g = G[ai + (long long)adj[j] * ldg];
+    T[i + (long long)j * ldt] = ((i == j ? 1.0 : 0.0) + coef[j] * g) * inv_h;
+  }
+}
+
+cudaError_t launch_ring_dtn(const double* G, int ldg, const int* adj, const double* coef, int m, double h, double* T,
+                            long long ldt, cudaStream_t st) {
+  if (m <= 0) return cudaSuccess;
+  dim3 grid((m + 127) / 128, std::min(m, 2048));
+  ring_dtn_kernel<<<grid, 128, 0, st>>>(G, ldg, adj, coef, m, 1.0 / h, T, ldt);
+  return cudaGetLastError();
+}
+
 // nblk consecutive TB x TB column-major identity blocks
 __global__ void block_identity_kernel(double* out, long long total) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x)

@@ -537,6 +537,76 @@ def densify_dtn(sol: SolutionOperator) -> np.ndarray:
     return sol.G_dense
 
 
+def ring_nodes(n: int):
+    """Non-corner nodes of the Dirichlet ring in ring_id order (grid.cpp:40-47:
+    counterclockwise from (0, 0)): ids, positions, the adjacent unknown and the
+    stencil direction (1=E, 2=W, 3=N, 4=S) from that unknown to the ring node."""
+    m = n - 1
+    ids, pos, adj, dirs = [], [], [], []
+    s = n - 2
+    for rid in range(4 * m):
+        if rid % m == 0:
+            continue  # corners couple to no unknown
+        if rid < m:
+            x, y, ax, ay, d = rid, 0, rid, 1, 4
+        elif rid < 2 * m:
+            x, y, ax, ay, d = m, rid - m, m - 1, rid - m, 1
+        elif rid < 3 * m:
+            x, y, ax, ay, d = m - (rid - 2 * m), m, m - (rid - 2 * m), m - 1, 3
+        else:
+            x, y, ax, ay, d = 0, m - (rid - 3 * m), 1, m - (rid - 3 * m), 2
+        ids.append(rid)
+        pos.append((x, y))
+        adj.append((ay - 1) * s + (ax - 1))
+        dirs.append(d)
+    return np.array(ids), pos, np.array(adj, dtype=np.int64), np.array(dirs)
+
+
+def ring_dtn(sol: "SolutionOperator", op: DiscreteOperator, device: bool = False):
+    """Dirichlet-ring DtN map T = (1/h)(I + P G D_b) on the 4 n_int non-corner
+    ring nodes (SURVEY f-1; derived from A u = -D g, grid.hpp:88-90, since the
+    reference itself stops at G): T g is the one-sided normal derivative
+    (g_i - u_adj(i)) / h of the solution with ring data g. Computed on the GPU
+    from the resident G; returns a host array, or a CUDA tensor with device."""
+    if op.n != sol.n:
+        raise ValueError("ring_dtn: operator and solution sizes differ")
+    _, _, adj_uid, dirs = ring_nodes(op.n)
+    where = np.full(int(sol.boundary.max()) + 1, -1, dtype=np.int64)
+    where[sol.boundary] = np.arange(len(sol.boundary))
+    adj = np.ascontiguousarray(where[adj_uid])
+    coef = np.ascontiguousarray(op.stencil[dirs, adj_uid], dtype=np.float64)
+    m = len(adj)
+    if device:
+        import torch
+        T = torch.empty((m, m), dtype=torch.float64, device="cuda").t()
+        sol.ctx.check(L.lib().dtn_gpu_ring_dtn(sol.h, adj.ctypes.data, coef.ctypes.data, m, op.h, T.data_ptr(), m, 1))
+        return T
+    T = np.zeros((m, m), order="F")
+    sol.ctx.check(L.lib().dtn_gpu_ring_dtn(sol.h, adj.ctypes.data, coef.ctypes.data, m, op.h, T.ctypes.data, m, 0))
+    return T
+
+
+def dump_schur(S: np.ndarray, path: str) -> None:
+    """dense_nd.cpp:227-237: int64 rows, int64 cols, then the matrix row-major."""
+    S = np.asarray(S, dtype=np.float64)
+    with open(path, "wb") as f:
+        np.array([S.shape[0], S.shape[1]], dtype="<i8").tofile(f)
+        np.ascontiguousarray(S, dtype="<f8").tofile(f)
+
+
+def load_schur(path: str) -> np.ndarray:
+    """dense_nd.cpp:239-251 (column-major result, like the Eigen Matrix)."""
+    with open(path, "rb") as f:
+        head = np.fromfile(f, dtype="<i8", count=2)
+        if head.size != 2:
+            raise RuntimeError("load_schur: truncated file " + path)
+        rows, cols = int(head[0]), int(head[1])
+        data = np.fromfile(f, dtype="<f8", count=rows * cols)
+    if data.size != rows * cols:
+        raise RuntimeError("load_schur: truncated file " + path)
+    return np.asfortranarray(data.reshape(rows, cols))
+
+
 def root_boundary(tree: BoxTree) -> np.ndarray:
     """Canonical CCW ring of root unknowns (grid.cpp:185-188)."""
     s = tree.n - 2
