@@ -158,6 +158,31 @@ def run_reference(args, cfg, rank, world):
 
 
 # ------------------------------------------------------------------ B200 arm
+def build_cfg4_dense(dtn, torch, dev, reps=2):
+    """configs[3]'s operator (Laplace, n=4096 interior, 32x32 leaves; 16.8M
+    unknowns) on the DENSE engine on one GPU (the reference compresses these
+    merges; dense is exact): S only (the root inverse needs a > 8192-row
+    panel). Inputs resident in HBM; device time of the build from its events."""
+    n_int = 4096
+    op = dtn.discretize(dtn.baseline_problem(4, n_int))
+    tree = dtn.build_tree_uniform(n_int + 2, 32)
+    st = torch.from_numpy(op.stencil).to(dev)
+    best = None
+    for _ in range(reps + 1):  # first build: plan + graph capture (untimed)
+        s = dtn.build_root_gpu(None, tree, want_G=False, stencil_device_ptr=st.data_ptr())
+        b = s.build_stats
+        s.free()
+        best = b if best is None or b["build_ms"] < best["build_ms"] else best
+    peak_tf, _ = fp64_peak()
+    del st
+    torch.cuda.empty_cache()
+    return {"workload": "config4 operator: laplace n=4096 interior, 32x32 leaves, dense FP64 merges (S only), 1 GPU",
+            "build_ms": best["build_ms"], "grid_points_per_s": n_int ** 2 / (best["build_ms"] * 1e-3),
+            "merge_tflops": best["merge_flops"] / (best["build_ms"] * 1e-3) / 1e12,
+            "merge_frac_fp64_peak": best["merge_flops"] / (best["build_ms"] * 1e-3) / 1e12 / peak_tf,
+            "merge_gflop": best["merge_flops"] / 1e9, "launches": best["launches"]}
+
+
 def solve_cfg5(dtn, torch, ctx, dev, stream, rank, world, steps, warmup):
     """configs[4]: the DtN operator of the Helmholtz kappa=100, n=2048 build
     (dense FP64 here; the compressed engine is the next step) applied to 4096
@@ -377,6 +402,11 @@ def run_b200(args, cfg, rank, world, local):
             line["solve"] = sv
         except Exception as e:  # pragma: no cover
             line["solve"] = {"error": str(e)}
+    if rank == 0 and world == 1 and not args.no_cfg4:
+        try:
+            line["config4_dense"] = build_cfg4_dense(dtn, torch, dev)
+        except Exception as e:  # pragma: no cover
+            line["config4_dense"] = {"error": str(e)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
@@ -409,6 +439,7 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-solve", action="store_true", help="skip the config-5 solve measurement")
+    ap.add_argument("--no-cfg4", action="store_true", help="skip the config-4 dense build measurement")
     args = ap.parse_args()
     rank, world, local = dist_env()
     cfg = CONFIGS[args.config]

@@ -220,7 +220,7 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
     r.s_off = D->lu_off;
     r.piv_off = P.piv_ints;
   }
-  D->root_kb = panel_kb(nb);
+  D->root_kb = 32;  // (the root LU's row limit is checked when G is requested)
   // launch lists
   std::vector<int> lists;
   D->wl.resize(P.waves.size());
@@ -693,6 +693,7 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
   if (prof) prof->wave = int(D.wl.size());
   if (want_G) {
     const int nb = D.nb;
+    panel_kb(nb);  // throws beyond the cluster panel's 8192 rows
     double* LU = D.d_arena + D.lu_off;
     run(K_COPY, 0.0, 16.0 * nb2, [&] { return launch_copy2d(D.d_S, D.lds, LU, D.ldlu, nb, nb, st); });
     const int* rl = D.d_lists + D.root_list_off;
