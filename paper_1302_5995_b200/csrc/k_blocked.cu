@@ -333,13 +333,15 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
   // pivoted loop below -- the result is always that of partial pivoting.
   __shared__ int fast_fail;
   bool fast = false;
+  int jstart = 0;  // the pivoted loop resumes here: steps < jstart needed no interchange
+  __shared__ int jtop_s;
   if (try_fast) {
 #pragma unroll
     for (int a = 0; a < RPT; ++a)
 #pragma unroll
       for (int c = 0; c < PKB; ++c) psave[(a * PNT + tid) * (PKB + 1) + c] = v[a][c];
-    if (tid == 0) fast_fail = 0;
-    bool ok = true;
+    if (tid == 0) fast_fail = PKB;  // first step needing an interchange (PKB: none)
+    int jf = PKB;
     PROCLK(4);
     if (crank == 0 && warp == 0) {  // rows 0..kbe-1 live in lanes 0..kbe-1 (a = 0)
 #pragma unroll
@@ -354,7 +356,7 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
           if (lane > j && lane < kbe) {
             const double l = v[0][j] * rinv;
             v[0][j] = l;
-            ok &= fabs(l) <= 1.0;
+            if (!(fabs(l) <= 1.0) && jf == PKB) jf = j;
 #pragma unroll
             for (int c = j + 1; c < PKB; ++c) v[0][c] = fma(-l, pr[c], v[0][c]);
           }
@@ -363,13 +365,70 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
       // U11 rows for the substitution (row-major, 16-byte aligned)
 #pragma unroll
       for (int c = 0; c < PKB; ++c) ub[lane * PLD + c] = (c >= lane) ? v[0][c] : 0.0;
-      // (ub row j holds U11 row j in columns >= j); the pivot statistics
-      double apiv = 0.0;
+      const int jt = __reduce_min_sync(0xffffffffu, unsigned(jf));
+      if (lane == 0) fast_fail = jt;
+    }
+    if constexpr (CL) {
+      cg::this_cluster().sync();  // rank 0's U11 and first failing step complete
+      if (crank != 0) {
+        const double* rub = cg::this_cluster().map_shared_rank(ub, 0);
+        for (int e = tid; e < PKB * PLD + PKB; e += PNT) ub[e] = rub[e];
+        if (tid == 0) jtop_s = *cg::this_cluster().map_shared_rank(&fast_fail, 0);
+      }
+    }
+    __syncthreads();
+    if (crank == 0 && tid == 0) jtop_s = fast_fail;
+    __syncthreads();
+    const int jtop = jtop_s;  // every row below fails no later than the top block
+    PROCLK(5);
+    // every row below the top block: x U11 = a (forward substitution), the
+    // elimination's own operation order, steps < jmax
+    auto subst = [&](int rlo, int jmax, bool track) {
 #pragma unroll
-      for (int c = 0; c < PKB; ++c)
-        if (c == lane) apiv = fabs(v[0][c]);
-      double lo = lane < kbe ? apiv : DBL_MAX, hi = lane < kbe ? apiv : 0.0;
-      const bool nb_ = lane < kbe && (!(apiv == apiv) || apiv == INFINITY);
+      for (int a = 0; a < RPT; ++a) {
+        const int r = crank * PNT + tid + stride * a;
+        if (r >= rlo && r < Ri) {
+#pragma unroll
+          for (int j = 0; j < PKB; ++j) {
+            if (j < jmax) {
+              const double l = v[a][j] * urinv[j];
+              v[a][j] = l;
+              if (track && !(fabs(l) <= 1.0) && jf == PKB) jf = j;
+              if ((j + 1) & 1) v[a][j + 1] = fma(-l, ub[j * PLD + j + 1], v[a][j + 1]);
+#pragma unroll
+              for (int c = (j + 2) & ~1; c < PKB; c += 2) {
+                const double2 u2 = *reinterpret_cast<const double2*>(&ub[j * PLD + c]);
+                v[a][c] = fma(-l, u2.x, v[a][c]);
+                v[a][c + 1] = fma(-l, u2.y, v[a][c + 1]);
+              }
+            }
+          }
+        }
+      }
+    };
+    subst(kbe, min(kbe, jtop), true);
+    // first failing step over the panel (every CTA of the cluster)
+    if (jf < PKB) atomicMin(&fast_fail, jf);
+    __syncthreads();
+    PROCLK(6);
+    int jstar;
+    if constexpr (CL) {
+      if (tid == 0 && crank != 0 && fast_fail < PKB) atomicMin(cg::this_cluster().map_shared_rank(&fast_fail, 0), fast_fail);
+      cg::this_cluster().sync();
+      jstar = *cg::this_cluster().map_shared_rank(&fast_fail, 0);
+      cg::this_cluster().sync();  // rank 0's value read by all before anything reuses it
+    } else {
+      jstar = fast_fail;
+    }
+    jstar = min(jstar, kbe);
+    fast = jstar >= kbe;
+    PROCLK(7);
+    // pivot statistics of the pivots taken without interchanges (rank 0 warp 0 owns them)
+    if (crank == 0 && warp == 0) {
+      const double apiv = fabs(ub[lane * PLD + lane]);
+      const bool live = lane < jstar;
+      double lo = live ? apiv : DBL_MAX, hi = live ? apiv : 0.0;
+      const bool nb_ = live && (!(apiv == apiv) || apiv == INFINITY);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
@@ -379,54 +438,6 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
       pmax = fmax(pmax, hi);
       bad |= __any_sync(0xffffffffu, nb_);
     }
-    // the top block already interchanges: skip the substitution
-    if (crank == 0 && warp == 0 && __any_sync(0xffffffffu, !ok) && lane == 0) fast_fail = 1;
-    if constexpr (CL) {
-      cg::this_cluster().sync();  // rank 0's U11 complete
-      if (crank != 0) {
-        const double* rub = cg::this_cluster().map_shared_rank(ub, 0);
-        for (int e = tid; e < PKB * PLD + PKB; e += PNT) ub[e] = rub[e];
-        if (tid == 0 && *cg::this_cluster().map_shared_rank(&fast_fail, 0)) ok = false;
-      }
-    }
-    __syncthreads();
-    const bool top_failed = crank == 0 ? fast_fail != 0 : __syncthreads_or(!ok) != 0;
-    if (top_failed) ok = false;
-    PROCLK(5);
-    // every row below the top block: x U11 = a (forward substitution)
-#pragma unroll
-    for (int a = 0; a < RPT; ++a) {
-      const int r = crank * PNT + tid + stride * a;
-      if (!top_failed && r >= kbe && r < Ri) {
-#pragma unroll
-        for (int j = 0; j < PKB; ++j) {
-          if (j < kbe) {
-            const double l = v[a][j] * urinv[j];
-            v[a][j] = l;
-            ok &= fabs(l) <= 1.0;
-            if ((j + 1) & 1) v[a][j + 1] = fma(-l, ub[j * PLD + j + 1], v[a][j + 1]);
-#pragma unroll
-            for (int c = (j + 2) & ~1; c < PKB; c += 2) {
-              const double2 u2 = *reinterpret_cast<const double2*>(&ub[j * PLD + c]);
-              v[a][c] = fma(-l, u2.x, v[a][c]);
-              v[a][c + 1] = fma(-l, u2.y, v[a][c + 1]);
-            }
-          }
-        }
-      }
-    }
-    // all of the panel (every CTA of the cluster) must pass
-    const int cta_fail = __syncthreads_or(!ok);
-    PROCLK(6);
-    if constexpr (CL) {
-      if (tid == 0 && cta_fail) atomicOr(cg::this_cluster().map_shared_rank(&fast_fail, 0), 1);
-      cg::this_cluster().sync();
-      fast = *cg::this_cluster().map_shared_rank(&fast_fail, 0) == 0;
-      cg::this_cluster().sync();  // rank 0's flag read by all before anything reuses it
-    } else {
-      fast = !cta_fail;
-    }
-    PROCLK(7);
     if (fast) {
       // identity placement; the move list moves every pivot row onto itself
 #pragma unroll
@@ -443,17 +454,28 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
         mv[2 * PKB + tid] = tid < kbe ? k0 + tid : -1;
       }
     } else {
+      // steps < jstar are exactly those of partial pivoting (no interchange):
+      // rows >= jstar restart from the saved values with only those steps, rows
+      // < jstar (the top LU's lanes) are the pivot rows of steps 0..jstar-1
       if (crank == 0 && tid == 0) {
         atomicAdd(&g_panel_fallbacks, 1u);
         *pivoting_flag(args, nd) += 1;
       }
 #pragma unroll
-      for (int a = 0; a < RPT; ++a)
+      for (int a = 0; a < RPT; ++a) {
+        const int r = crank * PNT + tid + stride * a;
+        if (r >= jstar)
 #pragma unroll
-        for (int c = 0; c < PKB; ++c) v[a][c] = psave[(a * PNT + tid) * (PKB + 1) + c];
-      pmin = k0 == 0 ? DBL_MAX : args.pivstat[2 * node_id];
-      pmax = k0 == 0 ? 0.0 : args.pivstat[2 * node_id + 1];
-      bad = false;
+          for (int c = 0; c < PKB; ++c) v[a][c] = psave[(a * PNT + tid) * (PKB + 1) + c];
+      }
+      subst(jstar, jstar, false);
+      jstart = jstar;
+#pragma unroll
+      for (int a = 0; a < RPT; ++a) {
+        const int r = crank * PNT + tid + stride * a;
+        if (r < jstart) elim[a] = r;
+      }
+      if (tid < jstart) sp[tid] = tid;
     }
   }
   if (!fast) {
@@ -473,10 +495,12 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
 #pragma unroll
   for (int j = 0; j < PKB; ++j) {
     if (j >= kbe) break;
+    if (j < jstart) continue;
 #ifdef DTN_PANEL_PROFILE
     PCLK(0);
 #endif
-    const int buf = j & 1;
+    const int jr = j - jstart;  // mbarrier phases count the executed steps
+    const int buf = jr & 1;
     // ---- argmax of |column j| over the live rows: 32-bit key = high word of
     // |x| (sign 0, exponent, 20 mantissa bits; NaN ranks highest), low bit
     // set for candidates; hardware warp max + ballot, ties -> lowest lane
@@ -552,7 +576,7 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
           if (lane == 0) st_async_v4_b32(cluster_map(&cinfo[buf][crank][0], d), bkey, blo, unsigned(p), 0u, mb);
         }
       }
-      mbar_wait(&mbar[buf], unsigned(j >> 1) & 1u);
+      mbar_wait(&mbar[buf], unsigned(jr >> 1) & 1u);
       const unsigned ck = lane < csize ? cinfo[buf][lane][0] : 0u;
       const unsigned cl_ = lane < csize ? cinfo[buf][lane][1] : 0u;
       const unsigned gkey = __reduce_max_sync(0xffffffffu, ck);
@@ -778,11 +802,14 @@ unsigned panel_fallbacks_read_reset() {
 size_t panel_dyn_smem(int rpt) { return size_t(PKB * (PKB + 2) + PKB + rpt * PNT * (PKB + 1)) * sizeof(double); }
 
 // no-interchange attempts stop for a node after this many of its panels
-// needed interchanges (DTN_FAST_THRESHOLD; 0 = always run the pivoted loop)
+// needed interchanges (DTN_FAST_THRESHOLD; 0 = always run the pivoted loop).
+// Default: always attempt -- a failed attempt costs the top-block LU and the
+// substitution, and the pivoted loop then resumes at the first step that
+// needs an interchange (config 2: 8.87 ms vs 9.16 ms with threshold 1).
 int panel_fast_threshold() {
   static const int th = [] {
     const char* e = std::getenv("DTN_FAST_THRESHOLD");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : (1 << 30);
   }();
   return th;
 }
