@@ -5,6 +5,7 @@
 // tile in registers (FP64 has no tcgen05/TMEM path on sm_100a).
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -13,12 +14,14 @@ namespace dtnb {
 constexpr int GBM = 128, GBN = 64, GWM = 32, GWN = 32;
 constexpr int GTHREADS = (GBM / GWM) * (GBN / GWN) * 32;  // 256
 constexpr int GPA = 4;                                    // A smem row pad (bank-conflict free frags)
-constexpr int GLDB = 20;                                  // B smem leading dim (== 4 mod 16)
+// B smem leading dim: == 4 mod 16 (bank-conflict-free fragments), >= BK
+template <int BK>
+constexpr int gemm_ldb() { return BK <= 16 ? 20 : BK + 4; }
 
 template <int BK>
 struct GemmSmem {
   double a[2][BK][GBM + GPA];
-  double b[2][GBN][GLDB];
+  double b[2][GBN][gemm_ldb<BK>()];
 };
 
 // One BM x BN tile of C = alpha*A*B + beta*C with alpha, beta in {(1,0), (-1,1)}:
@@ -202,7 +205,9 @@ cudaError_t gemm_init() {
   for (cudaError_t x : {set_desc_attr<16, false, true>(), set_desc_attr<8, false, true>(), set_desc_attr<16, true, true>(),
                         set_desc_attr<8, true, true>(), set_desc_attr<16, false, false>(),
                         set_desc_attr<8, false, false>(), set_desc_attr<16, true, false>(),
-                        set_desc_attr<8, true, false>()})
+                        set_desc_attr<8, true, false>(), set_desc_attr<32, false, true>(),
+                        set_desc_attr<32, true, true>(), set_desc_attr<32, false, false>(),
+                        set_desc_attr<32, true, false>()})
     if (x != cudaSuccess) return x;
   e = cudaFuncSetAttribute(trailing_update_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            sizeof(GemmSmem<16>));
@@ -213,6 +218,17 @@ cudaError_t gemm_init() {
 
 int gemm_tiles(int m, int n) { return ((m + GBM - 1) / GBM) * ((n + GBN - 1) / GBN); }
 
+// K-chunk 32 for long reductions (DTN_GEMM_BK32_MIN, default 2048: +3 % on the
+// config-5 solve, K = 8188; shorter reductions measured faster with 16)
+int gemm_bk32_min() {
+  static const int v = [] {
+    const char* e = std::getenv("DTN_GEMM_BK32_MIN");
+    const int x = e ? std::atoi(e) : 2048;
+    return x <= 0 ? (1 << 30) : x;
+  }();
+  return v;
+}
+
 cudaError_t launch_gemm_desc(const GemmDesc* d_descs, int count, int max_tiles, int kmax, double alpha, double beta,
                              cudaStream_t st, bool a_aligned) {
   if (count <= 0 || max_tiles <= 0) return cudaSuccess;
@@ -220,15 +236,23 @@ cudaError_t launch_gemm_desc(const GemmDesc* d_descs, int count, int max_tiles, 
   const bool upd = alpha == -1.0 && beta == 1.0;
   if (!upd && !(alpha == 1.0 && beta == 0.0)) return cudaErrorInvalidValue;
   const bool bk16 = kmax % 16 == 0 || kmax > 64;
+  const bool bk32 = kmax >= gemm_bk32_min();
 #define DTNB_DESC_LAUNCH(BK, U, AL) \
   gemm_desc_kernel<BK, U, AL><<<grid, GTHREADS, sizeof(GemmSmem<BK>), st>>>(d_descs, alpha, beta)
+#define DTNB_DESC_PICK(U, AL)                           \
+  do {                                                  \
+    if (bk32) DTNB_DESC_LAUNCH(32, U, AL);              \
+    else if (bk16) DTNB_DESC_LAUNCH(16, U, AL);         \
+    else DTNB_DESC_LAUNCH(8, U, AL);                    \
+  } while (0)
   if (a_aligned) {
-    if (upd) { if (bk16) DTNB_DESC_LAUNCH(16, true, true); else DTNB_DESC_LAUNCH(8, true, true); }
-    else { if (bk16) DTNB_DESC_LAUNCH(16, false, true); else DTNB_DESC_LAUNCH(8, false, true); }
+    if (upd) DTNB_DESC_PICK(true, true);
+    else DTNB_DESC_PICK(false, true);
   } else {
-    if (upd) { if (bk16) DTNB_DESC_LAUNCH(16, true, false); else DTNB_DESC_LAUNCH(8, true, false); }
-    else { if (bk16) DTNB_DESC_LAUNCH(16, false, false); else DTNB_DESC_LAUNCH(8, false, false); }
+    if (upd) DTNB_DESC_PICK(true, false);
+    else DTNB_DESC_PICK(false, false);
   }
+#undef DTNB_DESC_PICK
 #undef DTNB_DESC_LAUNCH
   return cudaGetLastError();
 }
