@@ -242,6 +242,14 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
       m_dst[tid] = mvp[tid];
       m_src[tid] = mvp[2 * PKB + tid];
     }
+    // U12 right-hand sides (the top rows moved by step kp; warp w solves
+    // columns 4w..4w+3 with lane = row), loaded speculatively from the
+    // unmoved rows and reloaded below only if step kp interchanged
+    constexpr int QC = PKB / PNW;  // columns per warp
+    double xs[QC];
+#pragma unroll
+    for (int q = 0; q < QC; ++q)
+      xs[q] = (lane < kb && warp * QC + q < kbe) ? Mg[(kp + lane) + (long long)(k0 + warp * QC + q) * ldm] : 0.0;
     cp_async_wait<0>();
     __syncthreads();
     PROCLK(1);
@@ -249,12 +257,12 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
     // 4w..4w+3 with lane = row (slot i moves a row into kp + i), the solved
     // entry of row m broadcast by shuffle at step m
     {
-      constexpr int QC = PKB / PNW;  // columns per warp
       const int i = lane, c0 = warp * QC;
       const int srow = m_src[i];
       double x[QC];
 #pragma unroll
-      for (int q = 0; q < QC; ++q) x[q] = (i < kb && c0 + q < kbe) ? Mg[srow + (long long)(k0 + c0 + q) * ldm] : 0.0;
+      for (int q = 0; q < QC; ++q)
+        x[q] = (srow == kp + i || !(i < kb && c0 + q < kbe)) ? xs[q] : Mg[srow + (long long)(k0 + c0 + q) * ldm];
 #pragma unroll 4
       for (int m = 0; m < kb - 1; ++m) {
         const double lim = (i > m) ? l11[i * PLD + m] : 0.0;
@@ -334,13 +342,13 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
   __shared__ int fast_fail;
   bool fast = false;
   int jstart = 0;  // the pivoted loop resumes here: steps < jstart needed no interchange
-  __shared__ int jtop_s;
+  __shared__ int jtop_s, fail_all;
   if (try_fast) {
 #pragma unroll
     for (int a = 0; a < RPT; ++a)
 #pragma unroll
       for (int c = 0; c < PKB; ++c) psave[(a * PNT + tid) * (PKB + 1) + c] = v[a][c];
-    if (tid == 0) fast_fail = PKB;  // first step needing an interchange (PKB: none)
+    if (tid == 0) fast_fail = fail_all = PKB;  // first step needing an interchange (PKB: none)
     int jf = PKB;
     PROCLK(4);
     if (crank == 0 && warp == 0) {  // rows 0..kbe-1 live in lanes 0..kbe-1 (a = 0)
@@ -413,10 +421,11 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
     PROCLK(6);
     int jstar;
     if constexpr (CL) {
-      if (tid == 0 && crank != 0 && fast_fail < PKB) atomicMin(cg::this_cluster().map_shared_rank(&fast_fail, 0), fast_fail);
+      // every CTA folds its minimum into every CTA's copy: one cluster barrier
+      if (warp == 0 && lane < csize && fast_fail < PKB)
+        atomicMin(cg::this_cluster().map_shared_rank(&fail_all, lane), fast_fail);
       cg::this_cluster().sync();
-      jstar = *cg::this_cluster().map_shared_rank(&fast_fail, 0);
-      cg::this_cluster().sync();  // rank 0's value read by all before anything reuses it
+      jstar = fail_all;
     } else {
       jstar = fast_fail;
     }
