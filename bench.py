@@ -302,7 +302,7 @@ def run_b200(args, cfg, rank, world, local):
 
     def e2e_step():
         if world == 1:
-            s = dtn.build_root_gpu(op_h, tree, ctx=ctx)
+            s = dtn.build_root_gpu(op_h, tree, ctx=ctx, export_S=True)
         else:
             s = SH.build_distributed(eng_host, rank, world)
         if s is not None:

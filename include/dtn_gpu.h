@@ -62,6 +62,9 @@ typedef struct {
   int32_t nshards;     /* subtree sharding: 1, 2 (W|E), 4 (quadrants), 8 (quadrant halves) */
   int32_t shard;       /* >= 0: build only this shard's S; -1: full build (nshards == 1) or the top of
                           the tree from prob.shard_S (nshards > 1) */
+  double* export_S;    /* optional host buffer (page-locked for overlap): receives S (column-major,
+                          leading dimension export_lds) during the build, overlapping the root inverse */
+  int64_t export_lds;
 } dtn_opts;
 
 typedef struct {

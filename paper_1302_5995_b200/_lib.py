@@ -21,7 +21,8 @@ class dtn_problem(C.Structure):
 class dtn_opts(C.Structure):
     _fields_ = [("engine", C.c_int32), ("n_leaf", C.c_int32), ("leaf_side", C.c_int32), ("want_G", C.c_int32),
                 ("micro_max", C.c_int32), ("profile", C.c_int32), ("epsilon", C.c_double),
-                ("crossover", C.c_int64), ("nshards", C.c_int32), ("shard", C.c_int32)]
+                ("crossover", C.c_int64), ("nshards", C.c_int32), ("shard", C.c_int32),
+                ("export_S", C.c_void_p), ("export_lds", C.c_int64)]
 
 
 class dtn_level_stats(C.Structure):

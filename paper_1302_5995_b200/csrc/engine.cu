@@ -152,6 +152,8 @@ struct PlanDev {
   cudaEvent_t ev_start = nullptr, ev_root = nullptr, ev_end = nullptr;
   cudaEvent_t ev_rp = nullptr, ev_rest = nullptr;  // look-ahead dependencies
   cudaEvent_t ev_rest2[2] = {nullptr, nullptr};       // fused look-ahead: side-stream step parity
+  cudaEvent_t ev_S = nullptr;                           // root S complete (external node in the graph)
+  cudaStream_t copy = nullptr;                          // S export overlapping the root inverse
   cudaStream_t side = nullptr;                      // low-priority stream for trailing updates
   cudaGraphExec_t gexec = nullptr;
   int graph_want_G = -1;
@@ -160,9 +162,10 @@ struct PlanDev {
   ~PlanDev() {
     if (gexec) cudaGraphExecDestroy(gexec);
     for (auto e : ev_wave) cudaEventDestroy(e);
-    for (auto e : {ev_start, ev_root, ev_end, ev_rp, ev_rest, ev_rest2[0], ev_rest2[1]})
+    for (auto e : {ev_start, ev_root, ev_end, ev_rp, ev_rest, ev_rest2[0], ev_rest2[1], ev_S})
       if (e) cudaEventDestroy(e);
     if (side) cudaStreamDestroy(side);
+    if (copy) cudaStreamDestroy(copy);
     for (void* p : std::initializer_list<void*>{d_nodes, d_pos, d_arena, d_piv, d_pivstat, d_lists, d_stencil, d_S, d_G,
                                                 d_perm, d_norm, d_inv_descs, d_W, d_LUp, d_tinv, d_root_trs, d_bs_gemm,
                                                 d_bs_copy, d_tri, d_trs})
@@ -459,6 +462,8 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
   CK(cudaEventCreateWithFlags(&D->ev_rest, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&D->ev_rest2[0], cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&D->ev_rest2[1], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&D->ev_S, cudaEventDisableTiming));
+  CK(cudaStreamCreateWithFlags(&D->copy, cudaStreamNonBlocking));
   int lo = 0, hi = 0;
   CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   CK(cudaStreamCreateWithPriority(&D->side, cudaStreamNonBlocking, lo));
@@ -689,6 +694,13 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
   const double* Sview = D.d_arena + root.s_off;
   const double nb2 = double(D.nb) * D.nb;
   run(K_COPY, 0.0, 16.0 * nb2, [&] { return launch_copy2d(Sview, root.ld, D.d_S, D.lds, D.nb, D.nb, st); });
+  // (external event: a host-side export of S can overlap the root inverse)
+  {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(st, &cs));
+    CK(cudaEventRecordWithFlags(D.ev_S, st,
+                                cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault));
+  }
   if (events) CK(cudaEventRecord(D.ev_root, st));
   if (prof) prof->wave = int(D.wl.size());
   if (want_G) {
@@ -934,10 +946,17 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
     } else {
       enqueue_build(*D, st, want_G);
     }
+    if (opts->export_S) {  // S to the caller while the root inverse runs
+      if (opts->export_lds < D->nb) throw std::invalid_argument("dtn_gpu_build: export_lds < nb");
+      CK(cudaStreamWaitEvent(D->copy, D->ev_S, 0));
+      CK(cudaMemcpy2DAsync(opts->export_S, size_t(opts->export_lds) * 8, D->d_S, size_t(D->lds) * 8,
+                           size_t(D->nb) * 8, size_t(D->nb), cudaMemcpyDeviceToHost, D->copy));
+    }
     const size_t nstat = D->h_nodes.size();
     CK(cudaMemcpyAsync(D->h_pivstat, D->d_pivstat, 2 * nstat * sizeof(double), cudaMemcpyDeviceToHost, st));
     if (want_G) CK(cudaMemcpyAsync(D->h_norm, D->d_norm, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (opts->export_S) CK(cudaStreamSynchronize(D->copy));
     CK(cudaGetLastError());
     // singular blocks, first failing node in build order (dense_nd.cpp:93-96, 175-180)
     const Plan& P = D->P;

@@ -436,8 +436,11 @@ def shard_info(tree: BoxTree, nshards: int, shard: int) -> dict:
 
 def build_root_gpu(op: DiscreteOperator | None, tree: BoxTree, want_G: bool = True, micro_max: int = 0,
                    ctx: Context | None = None, stencil_device_ptr: int | None = None,
-                   profile: bool = False, nshards: int = 1, shard: int = -1, shard_S=None) -> SolutionOperator:
-    """The B200 build: leaf elimination + merges + root inverse, through dtn_gpu_build."""
+                   profile: bool = False, nshards: int = 1, shard: int = -1, shard_S=None,
+                   export_S: bool = False) -> SolutionOperator:
+    """The B200 build: leaf elimination + merges + root inverse, through dtn_gpu_build.
+    export_S: S arrives in a page-locked host array during the build (the copy
+    overlaps the root inverse); SolutionOperator.S_dense then costs nothing."""
     ctx = ctx or default_context()
     if stencil_device_ptr:
         prob = L.dtn_problem(tree.n, stencil_device_ptr, 1)
@@ -473,9 +476,17 @@ def build_root_gpu(op: DiscreteOperator | None, tree: BoxTree, want_G: bool = Tr
         prob.shard_S_on_device = 1 if on_dev else 0
     opts = L.dtn_opts(0, tree.n_leaf, tree.leaf_side, 1 if want_G else 0, micro_max, 1 if profile else 0, 0.0, 0,
                       nshards, shard)
+    S_host = None
+    if export_S and shard < 0 and nshards == 1:
+        S_host = SolutionOperator._host_matrix(len(root_boundary(tree)))
+        opts.export_S = S_host.ctypes.data
+        opts.export_lds = S_host.shape[0]
     h = C.c_void_p()
     ctx.check(L.lib().dtn_gpu_build(ctx.h, C.byref(prob), C.byref(opts), C.byref(h)))
-    return SolutionOperator(ctx, h, tree.n, want_G)
+    sol = SolutionOperator(ctx, h, tree.n, want_G)
+    if S_host is not None:
+        sol._S = S_host
+    return sol
 
 
 def build_root_dense_op(op: DiscreteOperator, tree: BoxTree, loads=None) -> SolutionOperator:

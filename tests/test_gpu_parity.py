@@ -209,3 +209,16 @@ def test_dense_n2048_helmholtz_properties():
     G = torch.from_numpy(sol.G_dense).cuda()
     R = Sd @ G - torch.eye(nb, dtype=torch.float64, device="cuda")
     assert float(torch.linalg.matrix_norm(R)) / np.sqrt(nb) <= 1e-11 * max(1.0, sol.cond_estimate)
+
+
+@pytest.mark.gpu
+def test_export_S_during_build_matches_export():
+    """opts.export_S: S copied to the host while the root inverse runs equals
+    the S exported after the build (and G is unaffected)."""
+    n = 66
+    op = dtn.discretize(dtn.baseline_problem(2, n - 2))
+    tree = dtn.build_tree_uniform(n, 16)
+    a = dtn.build_root_gpu(op, tree, export_S=True)
+    b = dtn.build_root_gpu(op, tree)
+    assert np.array_equal(a.S_dense, b.S_dense)
+    assert np.array_equal(a.G_dense, b.G_dense)
