@@ -72,7 +72,7 @@ struct Singular : std::runtime_error {
 int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
 constexpr int kSmallMax = 160;
-constexpr int kDefaultMicro = 64;
+constexpr int kDefaultMicro = 16;  // measured best on configs 1-2 (tools/sweep.py)
 
 // Panel width; the register-resident panel spans up to 16 CTAs x 512 rows.
 int panel_kb(int rows) {

@@ -12,9 +12,9 @@ n = n_int + 2
 op = dtn.discretize(dtn.baseline_problem(cfg, n_int))
 tree = dtn.build_tree_uniform(n, 16)
 st = torch.from_numpy(op.stencil).cuda()
-for mm in [16, 36, 64, 100, 128, 160]:
+for mm in [int(x) for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["16", "36", "64", "100", "128", "160"])]:
     ts = []
-    for it in range(4):
+    for it in range(8):
         s = dtn.build_root_gpu(None, tree, stencil_device_ptr=st.data_ptr(), micro_max=mm)
         ts.append(s.build_stats["build_ms"])
         s.free()
