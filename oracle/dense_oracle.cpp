@@ -719,4 +719,30 @@ int orc_merge_given(void* p, const int* ra, const double* Sa, const int* rb, con
   });
 }
 int orc_blas_threads() { return scipy_openblas_get_num_threads64_(); }
+
+// Probe vectors of error_metrics (reference.cpp:139-161): seeded random unit
+// boundary vector (mt19937_64, Box-Muller on explicit uniforms) and the smooth one.
+void orc_random_unit_boundary(int64_t size, uint64_t seed, double* r) {
+  std::mt19937_64 rng(seed ^ 0x9e3779b97f4a7c15ull);
+  for (int64_t i = 0; i < size; i += 2) {
+    const double u1 = (double(rng() >> 11) + 0.5) * 0x1.0p-53;
+    const double u2 = double(rng() >> 11) * 0x1.0p-53;
+    const double rad = std::sqrt(-2.0 * std::log(u1));
+    r[i] = rad * std::cos(2.0 * std::numbers::pi * u2);
+    if (i + 1 < size) r[i + 1] = rad * std::sin(2.0 * std::numbers::pi * u2);
+  }
+  double nrm = 0.0;
+  for (int64_t i = 0; i < size; ++i) nrm += r[i] * r[i];
+  nrm = std::sqrt(nrm);
+  for (int64_t i = 0; i < size; ++i) r[i] /= nrm;
+}
+void orc_smooth_boundary(int64_t size, double* r) {
+  double nrm = 0.0;
+  for (int64_t i = 0; i < size; ++i) {
+    r[i] = std::sin(2.0 * std::numbers::pi * double(i) / double(size));
+    nrm += r[i] * r[i];
+  }
+  nrm = std::sqrt(nrm);
+  for (int64_t i = 0; i < size; ++i) r[i] /= nrm;
+}
 }

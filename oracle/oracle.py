@@ -57,6 +57,8 @@ def lib():
         L.orc_leaf_rect.argtypes = [vp, i32, i32, i32, i32, P(f64), P(i64)]
         L.orc_merge_rects.argtypes = [vp, P(i32), P(i32), P(f64), P(i64)]
         L.orc_merge_given.argtypes = [vp, P(i32), P(f64), P(i32), P(f64), P(f64), P(i64)]
+        L.orc_random_unit_boundary.argtypes = [i64, C.c_uint64, P(f64)]
+        L.orc_smooth_boundary.argtypes = [i64, P(f64)]
         _lib = L
     return _lib
 
@@ -294,3 +296,59 @@ def ring_dtn(problem: Problem, result: DenseResult) -> np.ndarray:
     adj = np.array(adj)
     coef = np.array(coef)
     return (np.eye(len(adj)) + result.G[np.ix_(adj, adj)] * coef[None, :]) / h
+
+
+
+def random_unit_boundary(size: int, seed: int) -> np.ndarray:
+    """reference.cpp:139-152 (restated in dense_oracle.cpp with std::mt19937_64)."""
+    r = np.zeros(size)
+    lib().orc_random_unit_boundary(size, seed, _dp(r))
+    return r
+
+
+def smooth_boundary(size: int) -> np.ndarray:
+    """reference.cpp:154-161."""
+    r = np.zeros(size)
+    lib().orc_smooth_boundary(size, _dp(r))
+    return r
+
+
+def sparse_system(stencil: np.ndarray, n: int):
+    """The full system matrix A (grid.cpp:128-166) from a 5 x (n-2)^2 stencil."""
+    import scipy.sparse as sp
+    s = n - 2
+    idx = np.arange(s * s)
+    x, y = idx % s, idx // s
+    rows, cols, vals = [idx], [idx], [stencil[0]]
+    for r, (dx, dy) in enumerate([(1, 0), (-1, 0), (0, 1), (0, -1)], start=1):
+        ok = (x + dx >= 0) & (x + dx < s) & (y + dy >= 0) & (y + dy < s)
+        rows.append(idx[ok]); cols.append((idx + dx + dy * s)[ok]); vals.append(stencil[r][ok])
+    return sp.csc_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(s * s, s * s))
+
+
+def error_metrics(apply_dtn, stencil: np.ndarray, n: int, boundary: np.ndarray, seed: int):
+    """error_metrics (reference.cpp:163-177): e1 with the seeded random unit
+    boundary vector, e2 with the smooth one; the exact answer from a sparse
+    direct solve of the full system with boundary right-hand side
+    (reference_dtn_apply, :122-137; SuperLU here in place of Eigen SparseLU,
+    with the reference's residual check and up to 3 refinement steps)."""
+    import scipy.sparse.linalg as spla
+    A = sparse_system(stencil, n)
+    lu = spla.splu(A)
+    out = []
+    for r in (random_unit_boundary(len(boundary), seed), smooth_boundary(len(boundary))):
+        rhs = np.zeros(A.shape[0])
+        rhs[boundary] = r
+        x = lu.solve(rhs)
+        res = np.linalg.norm(A @ x - rhs) / np.linalg.norm(rhs)
+        for _ in range(3):
+            if res <= 1e-6:
+                break
+            x = x + lu.solve(rhs - A @ x)
+            res = np.linalg.norm(A @ x - rhs) / np.linalg.norm(rhs)
+        if res > 1e-6:
+            raise RuntimeError(f"error_metrics: direct solve residual {res:.3g} exceeds 1e-6")
+        exact = x[boundary]
+        approx = apply_dtn(r)
+        out.append(float(np.linalg.norm(approx - exact) / np.linalg.norm(exact)))
+    return tuple(out)
