@@ -65,6 +65,12 @@ typedef struct {
   double* export_S;    /* optional host buffer (page-locked for overlap): receives S (column-major,
                           leading dimension export_lds) during the build, overlapping the root inverse */
   int64_t export_lds;
+  /* body loads (LoadPanel, dense_nd.hpp:29-32; build_with_loads, bodyload.cpp:47-57): unit loads at
+   * these distinct, strictly interior unknown ids are carried through every merge as extra
+   * right-hand-side columns (dense_nd.cpp:98-101, 136-147, 182-184); the result's body map
+   * F = G * rhs_root (accel_nd.cpp:872-875) is read with dtn_gpu_body_map. Needs want_G. */
+  const int64_t* load_ids;
+  int32_t nloads;
 } dtn_opts;
 
 typedef struct {
@@ -121,6 +127,9 @@ int dtn_gpu_export_device(const dtn_op* op, double* S, int64_t lds, double* G, i
  * on_device, in device memory. Requires G (want_G). */
 int dtn_gpu_ring_dtn(const dtn_op* op, const int64_t* adj, const double* coef, int64_t m, double h, double* T,
                      int64_t ldt, int on_device);
+/* Body map F (nb x nloads, column-major, leading dimension ldf) of a build with loads:
+ * solve_with_load (bodyload.cpp:68-77) is v = G g + F fhat. */
+int dtn_gpu_body_map(const dtn_op* op, double* F, int64_t ldf, int on_device);
 int dtn_gpu_apply(const dtn_op* op, int which, const double* X, int64_t ldx, int64_t batch, double* Y, int64_t ldy,
                   int on_device);
 

@@ -5,4 +5,5 @@ from .dtn import (AccelOptions, BoxTree, Context, DiscreteOperator, Engine, Fact
                   ProblemMode, ProblemSpec, SolutionOperator, apply_dtn, apply_schur, baseline_problem,
                   build_root_dense_op, build_root_gpu, build_tree, build_tree_uniform, build_with_loads, catalog, shard_info,
                   catalog_names, default_context, densify_dtn, discrete_eigenvalue, discrete_eigenvalue_kth,
-                  discretize, dump_schur, load_schur, ring_dtn, ring_nodes, root_boundary)
+                  discretize, dump_schur, load_schur, make_load_set, ring_dtn, ring_nodes, root_boundary,
+                  solve_with_load)

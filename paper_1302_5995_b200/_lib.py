@@ -22,7 +22,8 @@ class dtn_opts(C.Structure):
     _fields_ = [("engine", C.c_int32), ("n_leaf", C.c_int32), ("leaf_side", C.c_int32), ("want_G", C.c_int32),
                 ("micro_max", C.c_int32), ("profile", C.c_int32), ("epsilon", C.c_double),
                 ("crossover", C.c_int64), ("nshards", C.c_int32), ("shard", C.c_int32),
-                ("export_S", C.c_void_p), ("export_lds", C.c_int64)]
+                ("export_S", C.c_void_p), ("export_lds", C.c_int64),
+                ("load_ids", C.c_void_p), ("nloads", C.c_int32)]
 
 
 class dtn_level_stats(C.Structure):
@@ -44,7 +45,7 @@ class dtn_kernel_stats(C.Structure):
 EXPORTS = [
     "dtn_gpu_create", "dtn_gpu_destroy", "dtn_gpu_last_error", "dtn_gpu_set_stream", "dtn_gpu_build",
     "dtn_gpu_free", "dtn_gpu_boundary", "dtn_gpu_export", "dtn_gpu_export_device", "dtn_gpu_device_ptrs",
-    "dtn_gpu_apply", "dtn_gpu_ring_dtn",
+    "dtn_gpu_apply", "dtn_gpu_ring_dtn", "dtn_gpu_body_map",
     "dtn_gpu_num_boxes", "dtn_gpu_box_info", "dtn_gpu_box_schur", "dtn_gpu_level_stats", "dtn_gpu_build_stats", "dtn_gpu_kernel_stats",
     "dtn_discretize_continuum", "dtn_discretize_network", "dtn_debug_partial_lu", "dtn_gpu_shard_info",
 ]
@@ -82,6 +83,7 @@ def lib():
     L.dtn_gpu_export_device.argtypes = [vp, vp, i64, vp, i64]
     L.dtn_gpu_apply.argtypes = [vp, C.c_int, vp, i64, i64, vp, i64, C.c_int]
     L.dtn_gpu_ring_dtn.argtypes = [vp, vp, vp, i64, C.c_double, vp, i64, C.c_int]
+    L.dtn_gpu_body_map.argtypes = [vp, vp, i64, C.c_int]
     L.dtn_gpu_num_boxes.argtypes = [vp, P(i32), P(i32)]
     L.dtn_gpu_box_info.argtypes = [vp, i32, P(i32)]
     L.dtn_gpu_box_schur.argtypes = [vp, i32, vp]

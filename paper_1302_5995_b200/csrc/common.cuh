@@ -14,6 +14,9 @@ struct NodeDev {
   int ld;     // leading dimension of this node's S block
   int ldm;    // blocked: leading dimension of the assembled system
   long long s_off, m_off, pos_off, piv_off;
+  long long rhs_off;  // body-load columns (nb x nloads, leading dimension rhs_ld)
+  int rhs_ld;
+  int ncols;          // blocked: columns of the assembled system (total + body-load columns)
 };
 
 struct PosDev {  // == plan.hpp PosEntry
@@ -54,6 +57,8 @@ struct KernelArgs {
   double* arena;
   int* piv;
   double* pivstat;        // 2 per node: min |pivot|, max |pivot|
+  int nl;                 // body-load columns carried through the build (0: none)
+  const int* load_col;    // per unknown: its load column, or -1
 };
 
 // ---------------------------------------------------------------- PTX helpers

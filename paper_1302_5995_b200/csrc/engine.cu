@@ -142,6 +142,13 @@ struct PlanDev {
   TriDesc* d_tri = nullptr;
   double* d_W = nullptr;     // U^{-1} L^{-1} before the column permutation
   double* d_LUp = nullptr;   // L_ik Linv_kk (below) and U_ik Uinv_kk (above the diagonal blocks)
+  int* d_load_col = nullptr;  // body loads: per unknown, its load column or -1
+  double* d_F = nullptr;      // body map F = G * rhs_root (nb x nloads, leading dimension ldf)
+  int ldf = 0;
+  GemmDesc h_F_desc{};
+  GemmDesc* d_F_desc = nullptr;
+  int64_t rhs_root_off = 0;
+  int rhs_root_ld = 0;
   int inv_pre = 0;           // pre-product descriptors at the front of h_inv_descs
   std::vector<TrsmDesc> h_root_trs;
   TrsmDesc* d_root_trs = nullptr;
@@ -167,7 +174,7 @@ struct PlanDev {
     if (side) cudaStreamDestroy(side);
     if (copy) cudaStreamDestroy(copy);
     for (void* p : std::initializer_list<void*>{d_nodes, d_pos, d_arena, d_piv, d_pivstat, d_lists, d_stencil, d_S, d_G,
-                                                d_perm, d_norm, d_inv_descs, d_W, d_LUp, d_tinv, d_root_trs, d_bs_gemm,
+                                                d_perm, d_norm, d_inv_descs, d_W, d_LUp, d_tinv, d_root_trs, d_load_col, d_F, d_F_desc, d_bs_gemm,
                                                 d_bs_copy, d_tri, d_trs})
       if (p) cudaFree(p);
     if (h_pivstat) cudaFreeHost(h_pivstat);
@@ -175,7 +182,8 @@ struct PlanDev {
   }
 
   KernelArgs args() const {
-    return KernelArgs{d_nodes, d_pos, d_stencil, (long long)nu, P.n - 2, d_arena, d_piv, d_pivstat};
+    return KernelArgs{d_nodes, d_pos,    d_stencil, (long long)nu, P.n - 2, d_arena,
+                      d_piv,   d_pivstat, P.key.nloads,  d_load_col};
   }
 };
 
@@ -205,6 +213,9 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
     d.m_off = s.m_off;
     d.pos_off = s.pos_off;
     d.piv_off = s.piv_off;
+    d.rhs_off = s.rhs_off;
+    d.rhs_ld = s.rhs_ld;
+    d.ncols = s.total + (s.blocked ? P.key.nloads : 0);
   }
   D->ldlu = int(align_up(nb, 8));
   D->lu_off = align_up(P.arena_doubles, 32);
@@ -221,6 +232,7 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
     r.ld = D->ldlu;
     r.m_off = D->lu_off;
     r.s_off = D->lu_off;
+    r.ncols = nb;
     r.piv_off = P.piv_ints;
   }
   D->root_kb = 32;  // (the root LU's row limit is checked when G is requested)
@@ -234,13 +246,13 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
     L.micro_cnt = int(wv.micro.size());
     for (int id : wv.micro) {
       lists.push_back(id);
-      L.micro_max = std::max(L.micro_max, P.nodes[id].total);
+      L.micro_max = std::max(L.micro_max, P.nodes[id].total + P.key.nloads);
     }
     L.small_off = int(lists.size());
     L.small_cnt = int(wv.small.size());
     for (int id : wv.small) {
       lists.push_back(id);
-      L.small_max = std::max(L.small_max, P.nodes[id].total);
+      L.small_max = std::max(L.small_max, P.nodes[id].total + P.key.nloads);
     }
     L.blk_off = int(lists.size());
     L.blk_cnt = int(wv.blocked.size());
@@ -300,27 +312,28 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
           if (sblk < 0) continue;
           const int64_t M = nd.m_off, ldm = nd.ldm;
           const int k0 = sblk * 128, k1 = std::min(nd.ni, k0 + 128), bk = k1 - k0;
+          const int ncy = nd.nb + P.key.nloads;  // boundary columns + body-load columns
           // substitution variant: Y_k <- U_kk^{-1} Y_k in place, Y[0:k0] -= U[0:k0, k0:k1] Y_k
           trs.push_back(TrsmDesc{reinterpret_cast<const double*>(M + k0 + int64_t(k0) * ldm),
-                                 reinterpret_cast<double*>(M + k0 + nd.ni * ldm), int(ldm), int(ldm), bk, nd.nb});
+                                 reinterpret_cast<double*>(M + k0 + nd.ni * ldm), int(ldm), int(ldm), bk, ncy});
           gs.push_back(GemmDesc{reinterpret_cast<const double*>(M + int64_t(k0) * ldm),
                                 reinterpret_cast<const double*>(M + k0 + nd.ni * ldm),
-                                reinterpret_cast<double*>(M + nd.ni * ldm), k0, nd.nb, bk, int(ldm), int(ldm), int(ldm)});
+                                reinterpret_cast<double*>(M + nd.ni * ldm), k0, ncy, bk, int(ldm), int(ldm), int(ldm)});
           // default (explicit block inverse): T = Uinv_k Y_k; Y[0:k0] -= U[0:k0, k0:k1] T; Y_k = T
           const int64_t uinv = nd.uinv_off + int64_t(sblk) * 2 * 128 * 128 + 128 * 128;
           gd.push_back(GemmDesc{reinterpret_cast<const double*>(uinv),
                                 reinterpret_cast<const double*>(M + k0 + nd.ni * ldm),
-                                reinterpret_cast<double*>(nd.t_off), bk, nd.nb, bk, 128, int(ldm), 128});
+                                reinterpret_cast<double*>(nd.t_off), bk, ncy, bk, 128, int(ldm), 128});
           g2.push_back(GemmDesc{reinterpret_cast<const double*>(M + int64_t(k0) * ldm),
                                 reinterpret_cast<const double*>(nd.t_off), reinterpret_cast<double*>(M + nd.ni * ldm), k0,
-                                nd.nb, bk, int(ldm), 128, int(ldm)});
+                                ncy, bk, int(ldm), 128, int(ldm)});
           cd.push_back(CopyDesc{reinterpret_cast<const double*>(nd.t_off),
-                                reinterpret_cast<double*>(M + k0 + nd.ni * ldm), 128, int(ldm), bk, nd.nb});
-          t1 = std::max(t1, gemm_tiles(bk, nd.nb));
-          t2 = std::max(t2, gemm_tiles(std::max(k0, 1), nd.nb));
+                                reinterpret_cast<double*>(M + k0 + nd.ni * ldm), 128, int(ldm), bk, ncy});
+          t1 = std::max(t1, gemm_tiles(bk, ncy));
+          t2 = std::max(t2, gemm_tiles(std::max(k0, 1), ncy));
           kk = std::max(kk, bk);
-          mc = std::max(mc, nd.nb);
-          fl += double(bk) * bk * nd.nb + 2.0 * k0 * double(nd.nb) * bk;
+          mc = std::max(mc, ncy);
+          fl += double(bk) * bk * ncy + 2.0 * k0 * double(ncy) * bk;
           ++cnt;
         }
         gd.insert(gd.end(), g2.begin(), g2.end());
@@ -338,10 +351,11 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
       for (int id : wv.blocked) {
         const Node& nd = P.nodes[id];
         const int64_t M = nd.m_off, ldm = nd.ldm;
+        const int ncy = nd.nb + P.key.nloads;  // S and the body-load columns (dense_nd.cpp:181-184)
         gd.push_back(GemmDesc{reinterpret_cast<const double*>(M + nd.ni), reinterpret_cast<const double*>(M + nd.ni * ldm),
-                              reinterpret_cast<double*>(M + nd.ni + nd.ni * ldm), nd.nb, nd.nb, nd.ni, int(ldm), int(ldm),
+                              reinterpret_cast<double*>(M + nd.ni + nd.ni * ldm), nd.nb, ncy, nd.ni, int(ldm), int(ldm),
                               int(ldm)});
-        L.fin_tiles = std::max(L.fin_tiles, gemm_tiles(nd.nb, nd.nb));
+        L.fin_tiles = std::max(L.fin_tiles, gemm_tiles(nd.nb, ncy));
         L.fin_k = std::max(L.fin_k, nd.ni);
         L.fin_aligned = L.fin_aligned && (nd.ni % 2 == 0);
         L.fin_flops += 2.0 * nd.nb * double(nd.nb) * nd.ni;
@@ -367,6 +381,17 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
   CK(cudaMemcpy(D->d_lists, lists.data(), lists.size() * sizeof(int), cudaMemcpyHostToDevice));
   D->d_arena = dalloc<double>(size_t(D->lu_off + int64_t(D->ldlu) * nb));
   D->d_piv = dalloc<int>(size_t(P.piv_ints + align_up(nb, 4) + 260));
+  if (P.key.nloads > 0) {
+    D->d_load_col = dalloc<int>(size_t(D->nu));
+    D->ldf = int(align_up(nb, 8));
+    D->d_F = dalloc<double>(size_t(D->ldf) * P.key.nloads * 2);  // F, then the aligned copy of rhs_root
+    const Node& rt = P.nodes[P.root];
+    D->h_F_desc = GemmDesc{nullptr, D->d_F + size_t(D->ldf) * P.key.nloads, D->d_F, nb, P.key.nloads, nb, 0, D->ldf,
+                           D->ldf};
+    D->rhs_root_off = rt.rhs_off;
+    D->rhs_root_ld = rt.rhs_ld;
+    D->d_F_desc = dalloc<GemmDesc>(1);
+  }
   {  // relocate the Schur-form descriptors (stored as arena offsets) and upload
     double* base = D->d_arena;
     auto rel = [&](auto* p) { return reinterpret_cast<decltype(p)>(base + reinterpret_cast<int64_t>(p)); };
@@ -393,6 +418,11 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
   D->d_S = dalloc<double>(size_t(D->lds) * nb);
   D->ldg = int(align_up(nb, 8));
   D->d_G = dalloc<double>(size_t(D->ldg) * nb);
+  if (P.key.nloads > 0) {
+    D->h_F_desc.A = D->d_G;
+    D->h_F_desc.lda = D->ldg;
+    CK(cudaMemcpy(D->d_F_desc, &D->h_F_desc, sizeof(GemmDesc), cudaMemcpyHostToDevice));
+  }
   D->d_perm = dalloc<int>(nb);
   D->d_norm = dalloc<unsigned long long>(2);
   CK(cudaMallocHost(&D->h_pivstat, 2 * D->h_nodes.size() * sizeof(double)));
@@ -752,6 +782,14 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
     CK(cudaMemsetAsync(D.d_norm, 0, 2 * sizeof(unsigned long long), st));
     run(K_MISC, 0.0, 8.0 * nb2, [&] { return launch_norm1(D.d_S, D.lds, nb, nb, D.d_norm, st); });
     run(K_MISC, 0.0, 8.0 * nb2, [&] { return launch_norm1(D.d_G, D.ldg, nb, nb, D.d_norm + 1, st); });
+    if (P.key.nloads > 0) {  // body map F = G * rhs_root (accel_nd.cpp:872-875)
+      const int nl = P.key.nloads;
+      run(K_COPY, 0.0, 16.0 * nb * nl, [&] {
+        return launch_copy2d(D.d_arena + D.rhs_root_off, D.rhs_root_ld, D.d_F + size_t(D.ldf) * nl, D.ldf, nb, nl, st);
+      });
+      run(K_INV_GEMM, 2.0 * nb2 * nl, 0.0,
+          [&] { return launch_gemm_desc(D.d_F_desc, 1, gemm_tiles(nb, nl), nb, 1.0, 0.0, st, true); });
+    }
   }
   if (events) CK(cudaEventRecord(D.ev_end, st));
   D.launches = launches;
@@ -886,6 +924,13 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
     key.nshards = opts->nshards > 0 ? opts->nshards : 1;
     key.shard = opts->shard;
     if (key.nshards == 1) key.shard = -1;
+    key.nloads = int(opts->nloads);
+    if (opts->nloads < 0 || (opts->nloads > 0 && !opts->load_ids))
+      throw std::invalid_argument("dtn_gpu_build: bad body-load list");
+    if (key.nloads > 0 && key.nshards > 1)
+      throw std::invalid_argument("dtn_gpu_build: body loads are not supported in sharded builds");
+    if (key.nloads > 0 && !opts->want_G)
+      throw std::invalid_argument("dtn_gpu_build: body loads need G (the body map is G * rhs_root)");
     const bool top_mode = key.nshards > 1 && key.shard < 0;
     if (top_mode && !prob->shard_S) throw std::invalid_argument("dtn_gpu_build: top build needs the shard S blocks");
     if (key.leaf_side <= 0 && key.n_leaf < 16) throw std::invalid_argument("build_tree: n_leaf must be >= 16");
@@ -912,6 +957,22 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
     std::unique_ptr<Prof> prof;
     CK(cudaMemcpyAsync(D->d_stencil, prob->stencil, size_t(5 * D->nu) * sizeof(double),
                        prob->stencil_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    if (key.nloads > 0) {  // LoadPanel (dense_nd.hpp:29-32): unit loads, distinct strictly-interior unknowns
+      std::vector<int> col(size_t(D->nu), -1);
+      const int s_ = key.n - 2;
+      for (int j = 0; j < key.nloads; ++j) {
+        const int64_t id = opts->load_ids[j];
+        if (id < 0 || id >= D->nu) throw std::invalid_argument("load node is outside the grid");
+        const int x = int(id % s_) + 1, y = int(id / s_) + 1;
+        if (x == 1 || y == 1 || x == s_ || y == s_)
+          throw std::invalid_argument("load node (" + std::to_string(x) + ", " + std::to_string(y) +
+                                      ") is not strictly interior to the root box");
+        if (col[size_t(id)] >= 0)
+          throw std::invalid_argument("duplicate load node (" + std::to_string(x) + ", " + std::to_string(y) + ")");
+        col[size_t(id)] = j;
+      }
+      CK(cudaMemcpy(D->d_load_col, col.data(), col.size() * sizeof(int), cudaMemcpyHostToDevice));
+    }
     if (profile) {
       prof = std::make_unique<Prof>();
       enqueue_build(*D, st, want_G, prof.get());
@@ -1130,6 +1191,22 @@ int dtn_gpu_device_ptrs(const dtn_op* op, const double** S, const double** G, in
   return DTN_OK;
 }
 
+int dtn_gpu_body_map(const dtn_op* op, double* F, int64_t ldf, int on_device) {
+  if (!op) return DTN_EINVAL;
+  dtn_ctx* ctx = op->ctx;
+  return guarded(ctx, [&] {
+    const PlanDev& D = *op->plan;
+    const int nl = D.P.key.nloads;
+    if (nl == 0) throw std::invalid_argument("dtn_gpu_body_map: the build had no body loads");
+    if (!op->has_G) throw std::invalid_argument("dtn_gpu_body_map: body loads need G (want_G)");
+    if (!F || ldf < op->nb) throw std::invalid_argument("dtn_gpu_body_map: bad output");
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaMemcpy2DAsync(F, size_t(ldf) * 8, D.d_F, size_t(D.ldf) * 8, size_t(op->nb) * 8, size_t(nl),
+                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 int dtn_gpu_ring_dtn(const dtn_op* op, const int64_t* adj, const double* coef, int64_t m, double h, double* T,
                      int64_t ldt, int on_device) {
   if (!op) return DTN_EINVAL;
@@ -1310,6 +1387,7 @@ int dtn_debug_partial_lu(int32_t n, int32_t ni, const double* A, double* out, in
     nd.nb = n - ni;
     nd.ni = ni;
     nd.total = n;
+    nd.ncols = n;
     nd.a = nd.b = -1;
     nd.ld = nd.ldm = ld;
     NodeDev* d_node = dalloc<NodeDev>(1);

@@ -29,7 +29,7 @@ constexpr int RP_COLS = 32;  // trailing columns per rowpanel CTA
 __global__ void __launch_bounds__(256) gather_kernel(KernelArgs args, const int* __restrict__ list) {
   const NodeDev nd = args.nodes[list[blockIdx.y]];
   const int j0 = blockIdx.x * GATHER_COLS;
-  if (j0 >= nd.total) return;
+  if (j0 >= nd.ncols) return;
   const NodeDev ca = args.nodes[nd.a], cb = args.nodes[nd.b];
   const double* A = args.arena + ca.s_off;
   const double* B = args.arena + cb.s_off;
@@ -37,7 +37,17 @@ __global__ void __launch_bounds__(256) gather_kernel(KernelArgs args, const int*
   const PosDev* pos = args.pos + nd.pos_off;
   for (int jj = 0; jj < GATHER_COLS; ++jj) {
     const int j = j0 + jj;
-    if (j >= nd.total) break;
+    if (j >= nd.ncols) break;
+    if (j >= nd.total) {  // body-load column: the children's rhs rows summed into place (dense_nd.cpp:136-146)
+      const int c = j - nd.total;
+      const double* rA = args.arena + ca.rhs_off + (long long)c * ca.rhs_ld;
+      const double* rB = args.arena + cb.rhs_off + (long long)c * cb.rhs_ld;
+      for (int i = threadIdx.x; i < nd.total; i += blockDim.x) {
+        const PosDev pi = pos[i];
+        M[i + (long long)j * nd.ldm] = pi.src >= 0 ? rA[pi.src] : rB[-pi.src - 1];
+      }
+      continue;
+    }
     const PosDev pj = pos[j];
     const double* colA = pj.src >= 0 ? A + (long long)pj.src * ca.ld : nullptr;
     const double* colB = pj.src < 0 ? B + (long long)(-pj.src - 1) * cb.ld : nullptr;
@@ -757,7 +767,7 @@ __global__ void __launch_bounds__(RP_THREADS) rowpanel_kernel(KernelArgs args, c
   // skip_next: the next panel (fused prologue) owns columns [k1, k1 + min(kb, ni - k1))
   const int cs = k1 + (skip_next ? min(kb, max(nd.ni - k1, 0)) : 0);
   const int jbase = left ? (bx - ncoltiles) * RP_COLS : cs + bx * RP_COLS;
-  const int jend = left ? k0 : nd.total;
+  const int jend = left ? k0 : nd.ncols;
   if (jbase >= jend) return;
   const int* mv = move_list(args, nd, k0);
   if (tid < 64) {
@@ -842,7 +852,7 @@ cudaError_t blocked_init() {
 
 cudaError_t launch_gather(const KernelArgs& args, const int* d_list, int count, int max_total, cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
-  dim3 grid((max_total + GATHER_COLS - 1) / GATHER_COLS, count);
+  dim3 grid((max_total + args.nl + GATHER_COLS - 1) / GATHER_COLS, count);
   gather_kernel<<<grid, 256, 0, st>>>(args, d_list);
   return cudaGetLastError();
 }
@@ -902,7 +912,7 @@ cudaError_t launch_panel(const KernelArgs& args, const int* d_list, int count, i
 cudaError_t launch_rowpanel(const KernelArgs& args, const int* d_list, int count, int max_total, int max_nb, int k0,
                             int kb, bool swap_left, cudaStream_t st, bool skip_next) {
   if (count <= 0) return cudaSuccess;
-  const int coltiles = (max_total - k0 + RP_COLS - 1) / RP_COLS;
+  const int coltiles = (max_total + args.nl - k0 + RP_COLS - 1) / RP_COLS;
   const int lefttiles = swap_left ? (k0 + RP_COLS - 1) / RP_COLS : 0;
   const int rowtiles = (max_nb + RP_THREADS - 1) / RP_THREADS;
   if (coltiles + lefttiles + rowtiles <= 0) return cudaSuccess;

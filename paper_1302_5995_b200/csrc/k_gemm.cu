@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(GTHREADS) trailing_update_kernel(KernelArgs ar
   // columns [k1 + c0, min(total, k1 + c1)) (look-ahead split)
   const int m = (iface_rows ? nd.ni : nd.total) - k1;
   // c0 < 0: start after the next panel's interface columns (fused into its prologue)
-  const int cb = k1 + (c0 >= 0 ? c0 : min(kb, max(nd.ni - k1, 0))), n = min(nd.total, k1 + c1) - cb;
+  const int cb = k1 + (c0 >= 0 ? c0 : min(kb, max(nd.ni - k1, 0))), n = min(nd.ncols, k1 + c1) - cb;
   if (m <= 0 || n <= 0) return;
   const int tiles = (m + GBM - 1) / GBM, tiles_n = (n + GBN - 1) / GBN;
   const int t = blockIdx.x;
@@ -261,7 +261,7 @@ cudaError_t launch_gemm_desc(const GemmDesc* d_descs, int count, int max_tiles, 
 cudaError_t launch_trailing_update(const KernelArgs& args, const int* d_list, int count, int max_total, int k0, int kb,
                                    int c0, int c1, cudaStream_t st, int max_rows) {
   const int m = (max_rows > 0 ? max_rows : max_total) - k0 - 1;
-  const int n = std::min(max_total - k0 - 1, c1) - std::max(c0, 0);
+  const int n = std::min(max_total + args.nl - k0 - 1, c1) - std::max(c0, 0);
   if (count <= 0 || m <= 0 || n <= 0) return cudaSuccess;
   dim3 grid(gemm_tiles(m, n), count);
   if (kb % 16 == 0)

@@ -30,6 +30,7 @@ __global__ void __launch_bounds__(TR * TC) small_elim_kernel(KernelArgs args, co
   const int node_id = list[blockIdx.x];
   const NodeDev nd = args.nodes[node_id];
   const int total = nd.total, ni = nd.ni;
+  const int ncol = total + args.nl;  // body-load columns follow the system's columns
   const int tid = threadIdx.x, tr = tid % TR, tc = tid / TR;
 
   for (int p = tid; p < total; p += TR * TC) {
@@ -61,7 +62,17 @@ __global__ void __launch_bounds__(TR * TC) small_elim_kernel(KernelArgs args, co
     for (int b = 0; b < CPT; ++b) {
       const int j = tc + TC * b;
       double v = 0.0;
-      if (i < total && j < total) {
+      if (i < total && j >= total && j < ncol) {  // right-hand sides (dense_nd.cpp:98-101, 136-146)
+        const PosDev pi = spos[i];
+        const int c = j - total;
+        if constexpr (MICRO) {
+          v = args.load_col[pi.gid] == c ? 1.0 : 0.0;
+        } else {
+          const NodeDev ca = args.nodes[nd.a], cb = args.nodes[nd.b];
+          v = pi.src >= 0 ? args.arena[ca.rhs_off + pi.src + (long long)c * ca.rhs_ld]
+                          : args.arena[cb.rhs_off + (-pi.src - 1) + (long long)c * cb.rhs_ld];
+        }
+      } else if (i < total && j < total) {
         const PosDev pi = spos[i], pj = spos[j];
         if constexpr (MICRO) {
           if (i == j) {
@@ -150,7 +161,7 @@ __global__ void __launch_bounds__(TR * TC) small_elim_kernel(KernelArgs args, co
 #pragma unroll
         for (int b = 0; b < CPT; ++b) {
           const int j = tc + TC * b;
-          if (j > k && j < total) m[a][b] = fma(-l, rowp[j], m[a][b]);
+          if (j > k && j < ncol) m[a][b] = fma(-l, rowp[j], m[a][b]);
         }
       }
     }
@@ -165,6 +176,8 @@ __global__ void __launch_bounds__(TR * TC) small_elim_kernel(KernelArgs args, co
     for (int a = 0; a < RPT; ++a) {
       const int i = tr + TR * a;
       if (i >= ni && i < total && j >= ni && j < total) out[(i - ni) + (long long)(j - ni) * nd.ld] = m[a][b];
+      if (i >= ni && i < total && j >= total && j < ncol)
+        args.arena[nd.rhs_off + (i - ni) + (long long)(j - total) * nd.rhs_ld] = m[a][b];
     }
   }
   if (tid == 0) {

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <stdexcept>
+#include <string>
 
 namespace dtnb {
 
@@ -255,6 +256,9 @@ std::vector<int> shard_nodes(const Plan& P, int nshards) {
 }
 
 Plan make_plan(const PlanKey& key) {
+  if (key.nloads < 0 || key.micro_max + key.nloads > key.small_max)
+    throw std::invalid_argument("build: too many body loads for the fused leaf kernel (micro_max + loads > " +
+                                std::to_string(key.small_max) + ")");
   if (key.micro_max < 4 || key.micro_max > key.small_max)
     throw std::invalid_argument("make_plan: bad micro/small thresholds");
   Plan P;
@@ -336,6 +340,7 @@ Plan make_plan(const PlanKey& key) {
     Node& nd = P.nodes[i];
     if (!P.active[i] && !is_input[i]) continue;  // not computed, not read: no storage
     Wave& wv = P.waves[nd.wave];
+    const int nl = key.nloads;
     if (is_input[i]) {  // provided by the caller: compact S storage only
       nd.ld = std::max(nd.nb, 1);
       nd.s_off = off;
@@ -344,7 +349,7 @@ Plan make_plan(const PlanKey& key) {
     }
     if (nd.kind == NodeKind::micro) {
       wv.micro.push_back(i);
-    } else if (nd.total <= key.small_max) {
+    } else if (nd.total + nl <= key.small_max) {  // (load columns ride in the same registers)
       wv.small.push_back(i);
     } else {
       nd.blocked = true;
@@ -354,20 +359,27 @@ Plan make_plan(const PlanKey& key) {
     if (nd.blocked) {
       nd.ldm = int(align_up(nd.total, 8));
       nd.m_off = off;
-      off = align_up(off + int64_t(nd.ldm) * nd.total, 32);
+      off = align_up(off + int64_t(nd.ldm) * (nd.total + nl), 32);
       nd.s_off = nd.m_off + nd.ni + int64_t(nd.ni) * nd.ldm;
       nd.ld = nd.ldm;
+      nd.rhs_off = nd.m_off + nd.ni + int64_t(nd.total) * nd.ldm;
+      nd.rhs_ld = nd.ldm;
       nd.piv_off = poff;
       poff += align_up(std::max(nd.ni, 1), 4) + 260;  // ipiv + two per-panel row-move lists + flags
       const int64_t nblk = (nd.ni + 127) / 128;
       nd.uinv_off = off;
       off = align_up(off + nblk * 2 * 128 * 128, 32);
       nd.t_off = off;
-      off = align_up(off + int64_t(128) * std::max(nd.nb, 1), 32);
+      off = align_up(off + int64_t(128) * std::max(nd.nb + nl, 1), 32);
     } else {
       nd.ld = std::max(nd.nb, 1);
       nd.s_off = off;
       off = align_up(off + int64_t(nd.ld) * nd.nb, 32);
+      if (nl > 0) {
+        nd.rhs_ld = nd.ld;
+        nd.rhs_off = off;
+        off = align_up(off + int64_t(nd.rhs_ld) * nl, 32);
+      }
     }
   }
   P.arena_doubles = std::max<int64_t>(off, 32);

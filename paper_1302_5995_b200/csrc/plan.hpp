@@ -68,6 +68,10 @@ struct Node {
   int64_t piv_off = 0;  // blocked: offset into the int pivot table
   int64_t uinv_off = 0;  // blocked: inverses of the 128 x 128 diagonal blocks of U (back substitution)
   int64_t t_off = 0;     // blocked: 128 x nb staging block of the back substitution
+  // body-load right-hand sides (dense_nd.hpp:18-26 `rhs`, nb x nloads): compact
+  // for micro/small nodes, the view M[ni:total, total:total+nloads] for blocked ones
+  int64_t rhs_off = 0;
+  int rhs_ld = 0;
 };
 
 struct Wave {
@@ -83,9 +87,10 @@ struct Wave {
 struct PlanKey {
   int n = 0, n_leaf = 0, leaf_side = 0, micro_max = 0, small_max = 0;
   int nshards = 1, shard = -1;
+  int nloads = 0;  // body-load columns carried through the merges (LoadPanel, dense_nd.hpp:29-32)
   bool operator==(const PlanKey& o) const {
     return n == o.n && n_leaf == o.n_leaf && leaf_side == o.leaf_side && micro_max == o.micro_max &&
-           small_max == o.small_max && nshards == o.nshards && shard == o.shard;
+           small_max == o.small_max && nshards == o.nshards && shard == o.shard && nloads == o.nloads;
   }
 };
 

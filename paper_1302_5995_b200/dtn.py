@@ -332,6 +332,8 @@ class SolutionOperator:
         self._S = None
         self._G = None
         self.has_G = want_G
+        self.body_map = None  # F (nb x nloads) of a build with body loads (solution_operator.hpp:48)
+        self.load_ids = None
         cond = C.c_double()
         ctx.check(L.lib().dtn_gpu_export(handle, None, None, C.byref(cond)))
         self.cond_estimate = cond.value
@@ -391,9 +393,10 @@ class SolutionOperator:
         return self._G
 
     def memory_bytes(self) -> int:
-        """solution_operator.cpp:5-18 (dense: S and G payloads)."""
+        """solution_operator.cpp:5-18 (dense: S and G payloads, plus the body map)."""
         nb = self.boundary_size()
-        return 8 * nb * nb * (2 if self.has_G else 1)
+        extra = 0 if self.body_map is None else 8 * self.body_map.size
+        return 8 * nb * nb * (2 if self.has_G else 1) + extra
 
     def export_device(self, S_ptr: int | None = None, lds: int = 0, G_ptr: int | None = None, ldg: int = 0):
         """Device-to-device export of S and/or G (column-major, leading dims)."""
@@ -437,7 +440,7 @@ def shard_info(tree: BoxTree, nshards: int, shard: int) -> dict:
 def build_root_gpu(op: DiscreteOperator | None, tree: BoxTree, want_G: bool = True, micro_max: int = 0,
                    ctx: Context | None = None, stencil_device_ptr: int | None = None,
                    profile: bool = False, nshards: int = 1, shard: int = -1, shard_S=None,
-                   export_S: bool = False) -> SolutionOperator:
+                   export_S: bool = False, load_ids=None) -> SolutionOperator:
     """The B200 build: leaf elimination + merges + root inverse, through dtn_gpu_build.
     export_S: S arrives in a page-locked host array during the build (the copy
     overlaps the root inverse); SolutionOperator.S_dense then costs nothing."""
@@ -476,6 +479,11 @@ def build_root_gpu(op: DiscreteOperator | None, tree: BoxTree, want_G: bool = Tr
         prob.shard_S_on_device = 1 if on_dev else 0
     opts = L.dtn_opts(0, tree.n_leaf, tree.leaf_side, 1 if want_G else 0, micro_max, 1 if profile else 0, 0.0, 0,
                       nshards, shard)
+    loads = None
+    if load_ids is not None and len(load_ids):
+        loads = np.ascontiguousarray(load_ids, dtype=np.int64)
+        opts.load_ids = loads.ctypes.data
+        opts.nloads = len(loads)
     S_host = None
     if export_S and shard < 0 and nshards == 1:
         S_host = SolutionOperator._host_matrix(len(root_boundary(tree)))
@@ -486,14 +494,45 @@ def build_root_gpu(op: DiscreteOperator | None, tree: BoxTree, want_G: bool = Tr
     sol = SolutionOperator(ctx, h, tree.n, want_G)
     if S_host is not None:
         sol._S = S_host
+    if loads is not None:
+        F = np.zeros((sol.boundary_size(), len(loads)), order="F")
+        ctx.check(L.lib().dtn_gpu_body_map(h, F.ctypes.data, F.shape[0], 0))
+        sol.body_map = F
+        sol.load_ids = loads
     return sol
 
 
+def make_load_set(lattice: Lattice, points) -> np.ndarray:
+    """make_load_set (bodyload.cpp:9-30): unknown ids of distinct, strictly
+    interior load points (x, y)."""
+    s, seen, ids = lattice.side(), set(), []
+    for x, y in points:
+        if not (1 <= x <= s and 1 <= y <= s) or x == 1 or y == 1 or x == s or y == s:
+            raise ValueError(f"load node ({x}, {y}) is not strictly interior to the root box")
+        i = lattice.unknown_id(x, y)
+        if i in seen:
+            raise ValueError(f"duplicate load node ({x}, {y})")
+        seen.add(i)
+        ids.append(i)
+    return np.array(ids, dtype=np.int64)
+
+
 def build_root_dense_op(op: DiscreteOperator, tree: BoxTree, loads=None) -> SolutionOperator:
-    """accel_nd.hpp:98-100, executed by the B200 engine."""
-    if loads:
-        raise NotImplementedError("body-load panels are not part of the B200 hot path yet")
-    return build_root_gpu(op, tree)
+    """accel_nd.hpp:98-100 (with the LoadPanel of dense_nd.hpp:29-32), executed
+    by the B200 engine; with loads the result carries body_map F (nb x nloads)."""
+    return build_root_gpu(op, tree, load_ids=loads)
+
+
+def solve_with_load(sol: "SolutionOperator", g, fhat):
+    """solve_with_load (bodyload.cpp:68-77): v = G g + F fhat."""
+    v = apply_dtn(sol, g)
+    fhat = np.asarray(fhat, dtype=np.float64)
+    if fhat.size == 0:
+        return v
+    F = getattr(sol, "body_map", None)
+    if F is None or F.shape[1] != fhat.shape[0]:
+        raise ValueError("solve_with_load: load vector does not match the built body map")
+    return v + F @ fhat
 
 
 def build_with_loads(op: DiscreteOperator, tree: BoxTree, loads, engine: Engine, opt: AccelOptions | None = None):

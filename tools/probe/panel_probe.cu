@@ -11,7 +11,7 @@ int main() {
   for (int rows : {256, 512, 1024, 2048, 4096}) {
     const int n = rows, ld = (n + 7) / 8 * 8;
     NodeDev nd{};
-    nd.kind = 2; nd.ni = n; nd.nb = 0; nd.total = n; nd.ld = nd.ldm = ld; nd.a = nd.b = -1;
+    nd.kind = 2; nd.ni = n; nd.nb = 0; nd.total = n; nd.ncols = n; nd.ld = nd.ldm = ld; nd.a = nd.b = -1;
     NodeDev* dn; int* dl; double* da; double* db; int* dp; double* ds;
     cudaMalloc(&dn, sizeof(nd)); cudaMalloc(&dl, 4); cudaMalloc(&da, sizeof(double) * ld * 64);
     cudaMalloc(&db, sizeof(double) * ld * 64); cudaMalloc(&dp, 4 * (n + 200)); cudaMalloc(&ds, 16);
@@ -52,7 +52,7 @@ int main() {
   for (int rows : {256, 512, 1024, 2048, 4096}) {
     const int n = rows, ld = (n + 7) / 8 * 8;
     NodeDev nd{};
-    nd.kind = 2; nd.ni = n; nd.nb = 0; nd.total = n; nd.ld = nd.ldm = ld; nd.a = nd.b = -1;
+    nd.kind = 2; nd.ni = n; nd.nb = 0; nd.total = n; nd.ncols = n; nd.ld = nd.ldm = ld; nd.a = nd.b = -1;
     NodeDev* dn; int* dl; double* da; double* db; int* dp; double* ds;
     cudaMalloc(&dn, sizeof(nd)); cudaMalloc(&dl, 4); cudaMalloc(&da, sizeof(double) * ld * 32);
     cudaMalloc(&db, sizeof(double) * ld * 32); cudaMalloc(&dp, 4 * (n + 300)); cudaMalloc(&ds, 16);
@@ -84,7 +84,7 @@ int main() {
   for (int rows : {256, 512, 1024, 2048, 4096}) {
     const int n = rows, ld = (n + 7) / 8 * 8;
     NodeDev nd{};
-    nd.kind = 2; nd.ni = n; nd.nb = 0; nd.total = n; nd.ld = nd.ldm = ld; nd.a = nd.b = -1;
+    nd.kind = 2; nd.ni = n; nd.nb = 0; nd.total = n; nd.ncols = n; nd.ld = nd.ldm = ld; nd.a = nd.b = -1;
     NodeDev* dn; int* dl; double* da; double* db; int* dp; double* ds;
     cudaMalloc(&dn, sizeof(nd)); cudaMalloc(&dl, 4); cudaMalloc(&da, sizeof(double) * ld * 64);
     cudaMalloc(&db, sizeof(double) * ld * 64); cudaMalloc(&dp, 4 * (n + 300)); cudaMalloc(&ds, 16);
