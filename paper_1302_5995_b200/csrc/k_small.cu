@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(TR * TC) small_elim_kernel(KernelArgs args, co
     B = args.arena + cb.s_off;
     ldb = cb.ld;
   }
+  auto assemble = [&]() {
 #pragma unroll
   for (int a = 0; a < RPT; ++a) {
     const int i = tr + TR * a;
@@ -97,13 +98,83 @@ __global__ void __launch_bounds__(TR * TC) small_elim_kernel(KernelArgs args, co
       m[a][b] = v;
     }
   }
+  };
+  assemble();
 
-  // ---- elimination of rows/columns [0, ni)
-  unsigned elim = 0u;
+  // ---- no-interchange attempt: pivot k = row k, one barrier per step (row
+  // k+1 and column k+1 are published by their owners right after their own
+  // update); accepted iff every interface multiplier has |l| <= 1, i.e. when
+  // partial pivoting would not interchange (then the arithmetic is identical).
+  // Otherwise the system is re-assembled and eliminated with pivoting below.
+  __shared__ double rowq[2][MAXT];
   double pmin = DBL_MAX, pmax = 0.0;
+  bool ok = true;
+  {
+    auto publish = [&](int k, int buf) {
+      const int bk = k / TC, tck = k % TC, ap = k / TR, trk = k % TR;
+      if (tc == tck) {
+#pragma unroll
+        for (int a = 0; a < RPT; ++a) {
+          const int i = tr + TR * a;
+          double v = m[a][0];
+#pragma unroll
+          for (int b = 1; b < CPT; ++b)
+            if (b == bk) v = m[a][b];
+          if (i < total) colk[buf][i] = v;
+        }
+      }
+      if (tr == trk) {
+#pragma unroll
+        for (int a = 0; a < RPT; ++a)
+          if (a == ap) {
+#pragma unroll
+            for (int b = 0; b < CPT; ++b) {
+              const int j = tc + TC * b;
+              if (j < MAXT) rowq[buf][j] = m[a][b];
+            }
+          }
+      }
+    };
+    if (ni > 0) publish(0, 0);
+    __syncthreads();
+    for (int k = 0; k < ni; ++k) {
+      const double* ck = colk[k & 1];
+      const double* rp = rowq[k & 1];
+      const double pv = rp[k];
+      const double apv = fabs(pv);
+      pmin = fmin(pmin, apv);
+      pmax = (apv != apv) ? INFINITY : fmax(pmax, apv);
+      const double rinv = 1.0 / pv;
+#pragma unroll
+      for (int a = 0; a < RPT; ++a) {
+        const int i = tr + TR * a;
+        if (i > k && i < total) {
+          const double l = ck[i] * rinv;
+          if (i < ni) ok &= fabs(l) <= 1.0;
+#pragma unroll
+          for (int b = 0; b < CPT; ++b) {
+            const int j = tc + TC * b;
+            if (j > k && j < ncol) m[a][b] = fma(-l, rp[j], m[a][b]);
+          }
+        }
+      }
+      if (k + 1 < ni) publish(k + 1, (k + 1) & 1);
+      __syncthreads();
+    }
+  }
+  const bool fast = __syncthreads_and(ok) != 0;
+  if (!fast) {
+    assemble();
+    pmin = DBL_MAX;
+    pmax = 0.0;
+  }
+
+  // ---- elimination of rows/columns [0, ni) with partial pivoting among the
+  // interface rows (when the attempt above was rejected)
+  unsigned elim = 0u;
   const unsigned lane = threadIdx.x & 31u;
   const unsigned gmask = (TR == 32) ? 0xffffffffu : (((1u << TR) - 1u) << (lane & ~unsigned(TR - 1)));
-  for (int k = 0; k < ni; ++k) {
+  for (int k = 0; k < (fast ? 0 : ni); ++k) {
     const int bk = k / TC, tck = k % TC;
     double* ck = colk[k & 1];
     if (tc == tck) {
