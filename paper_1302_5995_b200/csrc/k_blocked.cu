@@ -283,10 +283,11 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
       for (int q = 0; q < QC; ++q) pro[i * PLD + c0 + q] = x[q];  // U12[i][c]; written to M after the loop
     }
     // rows displaced by step kp's interchanges (rare) reload from their source
+    const bool displaced = m_dst[PKB] >= 0;  // slots >= PKB list rows moved below the top block
 #pragma unroll
     for (int a = 0; a < RPT; ++a) {
       const int r = crank * PNT + tid + stride * a;
-      if (r < Ri) {
+      if (displaced && r < Ri) {
         const int R = k0 + r;
         int src = R;
 #pragma unroll 4
