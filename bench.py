@@ -372,6 +372,14 @@ def run_b200(args, cfg, rank, world, local):
             roof["traffic"] = json.load(f).get(dom_name)
     except Exception:
         pass
+    if dom_name == "panel":
+        roof["note"] = ("latency-bound pivot chain (32 sequential pivots per launch, a cluster exchange each on the "
+                        "pivoted path); its FLOP/s fraction is small by construction -- see roofline_throughput")
+    # the dominant throughput-bound (GEMM) class, for the tensor-pipe efficiency
+    tname, tk = max(((k, v) for k, v in ks.items() if v["flops"] > 0 and "gemm" in k), key=lambda kv: kv[1]["flops"])
+    t_ach = tk["flops"] / (tk["ms"] * 1e-3) / 1e12
+    roof_t = {"bound": "tensor", "kernel": tname, "achieved": t_ach, "peak": peak_tf, "unit": "TFLOP/s",
+              "frac": t_ach / peak_tf, "launches": tk["launches"], "share_of_build": tk["ms"] / total_prof_ms}
 
     merge_tf = pst["merge_flops"] / (pst["merge_ms"] * 1e-3) / 1e12 if pst["merge_ms"] > 0 else None
     line = {
@@ -390,6 +398,7 @@ def run_b200(args, cfg, rank, world, local):
                 "d2h_bytes_per_step": int(nb * nb * 8 + nb * nvec * 8)},
         "gpu_launches": launches_per_step * args.steps,
         "roofline": roof,
+        "roofline_throughput": roof_t,
         "clocks": clk.summary(),
         "build": {"build_ms": stats["build_ms"], "profiled_build_ms": pst["build_ms"], "leaf_ms": pst["leaf_ms"],
                   "merge_ms": pst["merge_ms"], "inverse_ms": pst["inverse_ms"],
