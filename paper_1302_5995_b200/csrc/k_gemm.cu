@@ -162,6 +162,121 @@ __global__ void __launch_bounds__(GTHREADS) gemm_desc_kernel(const GemmDesc* __r
                           sm);
 }
 
+// ---- large-tile variant: 128 x 128 CTA tile, 8 warps of 64 x 32 (16 DMMA per
+// k-step per warp: fragment loads per DMMA drop from 1 to 0.75), three-stage
+// cp.async pipeline. For large GEMMs (Schur complements, root inverse, solve).
+constexpr int XBM = 128, XBN = 128, XBK = 16, XST = 3, XWM = 64, XWN = 32;
+constexpr int XLDB = XBK + 4;
+struct GemmSmemX {
+  double a[XST][XBK][XBM + GPA];
+  double b[XST][XBN][XLDB];
+};
+
+template <bool UPD>
+__global__ void __launch_bounds__(GTHREADS, 1) gemm_big_kernel(const GemmDesc* __restrict__ descs, double alpha,
+                                                              double beta) {
+  extern __shared__ __align__(16) unsigned char gsm_raw[];
+  GemmSmemX& sm = *reinterpret_cast<GemmSmemX*>(gsm_raw);
+  const GemmDesc d = descs[blockIdx.y];
+  const int m = d.m, n = d.n, k = d.k;
+  const int tiles_m = (m + XBM - 1) / XBM, tiles_n = (n + XBN - 1) / XBN;
+  if (int(blockIdx.x) >= tiles_m * tiles_n) return;
+  const int row0 = (blockIdx.x % tiles_m) * XBM, col0 = (blockIdx.x / tiles_m) * XBN;
+  const double* A = d.A;
+  const double* B = d.B;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, tig = lane & 3;
+  const int wm0 = (warp % (XBM / XWM)) * XWM, wn0 = (warp / (XBM / XWM)) * XWN;
+  const int KT = (k + XBK - 1) / XBK;
+  auto load = [&](int stage, int kt) {
+    const int kb0 = kt * XBK;
+#pragma unroll
+    for (int c = tid; c < XBK * XBM / 2; c += GTHREADS) {  // A: 16-byte chunks along rows
+      const int kk = c / (XBM / 2), rr = (c % (XBM / 2)) * 2;
+      const int gr = row0 + rr, gc = kb0 + kk;
+      int bytes = 0;
+      const double* src = A;
+      if (gc < k && gr < m) {
+        bytes = (m - gr) >= 2 ? 16 : 8;
+        src = A + gr + (long long)gc * d.lda;
+      }
+      cp_async16(&sm.a[stage][kk][rr], src, bytes);
+    }
+#pragma unroll
+    for (int c = tid; c < XBN * XBK / 2; c += GTHREADS) {  // B: 16-byte chunks along k
+      const int nn = c / (XBK / 2), kp = (c % (XBK / 2)) * 2;
+      const int gk = kb0 + kp, gc = col0 + nn;
+      int bytes = 0;
+      const double* src = B;
+      if (gc < n && gk < k) {
+        bytes = (k - gk) >= 2 ? 16 : 8;
+        src = B + gk + (long long)gc * d.ldb;
+      }
+      cp_async16(&sm.b[stage][nn][kp], src, bytes);
+    }
+  };
+  double acc[XWM / 16][XWN / 8][4];
+  if (KT > 0) load(0, 0);
+  cp_async_commit();
+  if (KT > 1) load(1, 1);
+  cp_async_commit();
+#pragma unroll
+  for (int i = 0; i < XWM / 16; ++i)
+#pragma unroll
+    for (int j = 0; j < XWN / 8; ++j)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        double x = 0.0;
+        if constexpr (UPD) {
+          const int r = row0 + wm0 + i * 16 + g + 8 * (v >> 1);
+          const int c = col0 + wn0 + j * 8 + 2 * tig + (v & 1);
+          if (r < m && c < n) x = d.C[r + (long long)c * d.ldc];
+        }
+        acc[i][j][v] = x;
+      }
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<1>();  // stage kt has landed (kt + 1 may still be in flight)
+    __syncthreads();     // ... for every thread, and stage (kt + 2) % 3 is free
+    if (kt + 2 < KT) load((kt + 2) % XST, kt + 2);
+    cp_async_commit();
+    const int s = kt % XST;
+#pragma unroll
+    for (int ks = 0; ks < XBK / 4; ++ks) {
+      double af[XWM / 16][2], bf[XWN / 8];
+#pragma unroll
+      for (int i = 0; i < XWM / 16; ++i) {
+        af[i][0] = sm.a[s][ks * 4 + tig][wm0 + i * 16 + g];
+        af[i][1] = sm.a[s][ks * 4 + tig][wm0 + i * 16 + g + 8];
+        if constexpr (UPD) {
+          af[i][0] = -af[i][0];
+          af[i][1] = -af[i][1];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < XWN / 8; ++j) bf[j] = sm.b[s][wn0 + j * 8 + g][ks * 4 + tig];
+#pragma unroll
+      for (int i = 0; i < XWM / 16; ++i)
+#pragma unroll
+        for (int j = 0; j < XWN / 8; ++j) mma_f64_m16n8k4(acc[i][j], af[i][0], af[i][1], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int i = 0; i < XWM / 16; ++i)
+#pragma unroll
+    for (int j = 0; j < XWN / 8; ++j)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int r = row0 + wm0 + i * 16 + g + 8 * (v >> 1);
+        const int c = col0 + wn0 + j * 8 + 2 * tig + (v & 1);
+        if (r < m && c < n) {
+          double* p = d.C + r + (long long)c * d.ldc;
+          if constexpr (UPD) *p = acc[i][j][v];
+          else *p = beta == 0.0 ? alpha * acc[i][j][v] : fma(alpha, acc[i][j][v], beta * *p);
+        }
+      }
+}
+
 // Trailing update of the blocked partial LU (right-looking, dense_nd.cpp:174-181
 // restated as a blocked elimination): for each merge in the list with
 // ni > k0, M[k1:, k1:] -= M[k1:, k0:k1] * M[k0:k1, k1:], k1 = k0 + min(kb, ni-k0).
@@ -209,6 +324,10 @@ cudaError_t gemm_init() {
                         set_desc_attr<32, true, true>(), set_desc_attr<32, false, false>(),
                         set_desc_attr<32, true, false>()})
     if (x != cudaSuccess) return x;
+  e = cudaFuncSetAttribute(gemm_big_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(GemmSmemX));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(gemm_big_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(GemmSmemX));
+  if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(trailing_update_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            sizeof(GemmSmem<16>));
   if (e != cudaSuccess) return e;
@@ -229,9 +348,28 @@ int gemm_bk32_min() {
   return v;
 }
 
+// Large-tile path (DTN_GEMM_BIG=0 disables): aligned A and enough work (measured: 30 vs 27 TF/s
+// from 4096^2 x 2048 up; at 2044^2 x 1020 the 128 x 64 tile is better, 26 vs 25)
+int gemm_big_min_tiles() {
+  static const int v = [] {
+    const char* e = std::getenv("DTN_GEMM_BIG");
+    if (e && e[0] == '0') return 1 << 30;
+    const char* t = std::getenv("DTN_GEMM_BIG_TILES");
+    return t ? std::atoi(t) : 1184;  // ~4 waves of 128 x 128 tiles: below that the smaller tile balances better
+  }();
+  return v;
+}
+
 cudaError_t launch_gemm_desc(const GemmDesc* d_descs, int count, int max_tiles, int kmax, double alpha, double beta,
                              cudaStream_t st, bool a_aligned) {
   if (count <= 0 || max_tiles <= 0) return cudaSuccess;
+  if (a_aligned && max_tiles * count >= gemm_big_min_tiles() && kmax >= 64) {
+    const bool upd = alpha == -1.0 && beta == 1.0;
+    dim3 grid(max_tiles, count);  // (128 x 64 tile count bounds the 128 x 128 one; extra CTAs exit)
+    if (upd) gemm_big_kernel<true><<<grid, GTHREADS, sizeof(GemmSmemX), st>>>(d_descs, alpha, beta);
+    else gemm_big_kernel<false><<<grid, GTHREADS, sizeof(GemmSmemX), st>>>(d_descs, alpha, beta);
+    return cudaGetLastError();
+  }
   dim3 grid(max_tiles, count);
   const bool upd = alpha == -1.0 && beta == 1.0;
   if (!upd && !(alpha == 1.0 && beta == 0.0)) return cudaErrorInvalidValue;
