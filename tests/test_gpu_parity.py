@@ -222,3 +222,28 @@ def test_export_S_during_build_matches_export():
     b = dtn.build_root_gpu(op, tree)
     assert np.array_equal(a.S_dense, b.S_dense)
     assert np.array_equal(a.G_dense, b.G_dense)
+
+
+@pytest.mark.gpu
+def test_dense_n4096_laplace_properties():
+    # config-4 operator (Laplace, n=4096 interior, 32x32 leaves; 16.8 M unknowns) on
+    # the dense engine, S only (root 16380 x 16380): S of the Laplacian is
+    # symmetric positive definite -- size-independent properties (a Cholesky
+    # factorization of S must succeed), and the merges' largest interface LU
+    # (8190 rows) runs the two-rows-per-thread cluster panel.
+    import torch
+    n_int = 4096
+    op = dtn.discretize(dtn.baseline_problem(4, n_int))
+    st = torch.from_numpy(op.stencil).cuda()
+    sol = dtn.build_root_gpu(None, dtn.build_tree_uniform(n_int + 2, 32), want_G=False,
+                             stencil_device_ptr=st.data_ptr())
+    nb = len(sol.boundary)
+    assert nb == 4 * n_int - 4
+    S = torch.empty((nb, nb), dtype=torch.float64, device="cuda").t()
+    sol.export_device(S.data_ptr(), nb, None, 0)
+    sol.free()
+    del st
+    asym = float(torch.linalg.matrix_norm(S - S.t()) / torch.linalg.matrix_norm(S))
+    assert asym <= 1e-13
+    L, info = torch.linalg.cholesky_ex(0.5 * (S + S.t()))
+    assert int(info) == 0
