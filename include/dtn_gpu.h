@@ -157,6 +157,37 @@ int dtn_debug_partial_lu(int32_t n, int32_t ni, const double* A, double* out, in
 int dtn_discretize_continuum(int32_t n, const double* b, const double* c, const double* d, double* stencil);
 int dtn_discretize_network(int32_t n, double lo, double hi, uint64_t seed, double* stencil);
 
+/* ---- compressed (HBS) operators ----------------------------------------
+ * HbsMatrix (hbs.hpp:30-51): orthonormal-basis hierarchically block separable
+ * matrix over build_index_tree(M, leaf_cap) (index_tree.cpp:37-67).
+ *   dtn_gpu_hbs_compress     compress(H, eps, leaf_cap) (hbs.hpp:58-62, hbs.cpp:61-182) of a dense
+ *                            column-major M x M matrix (host or device memory)
+ *   dtn_gpu_hbs_compress_op  the same on a built operator's resident G (which 0) or S (which 1):
+ *                            the compressed SolutionOperator::G_hbs / S_hbs (solution_operator.hpp:38-42)
+ *   dtn_gpu_hbs_apply        apply(H, x) (hbs.hpp:66, hbs.cpp:187-232), batched; apply_dtn on G_hbs
+ *                            (solution_operator.cpp:42)
+ *   dtn_gpu_hbs_info/tree/factor  size(), max_rank(), payload_bytes(), tree nodes, rank(t) and the
+ *                            D/U/V/B factors (hbs.hpp:30-51)
+ *   dtn_gpu_hbs_serialize / _deserialize  the DTNHBS01 byte format (hbs.hpp:92-95, hbs.cpp:422-519),
+ *                            byte-for-byte the reference layout */
+typedef struct dtn_hbs dtn_hbs;
+int dtn_gpu_hbs_compress(dtn_ctx* ctx, const double* H, int64_t M, int64_t ldh, int on_device, double eps,
+                         int64_t leaf_cap, dtn_hbs** out);
+int dtn_gpu_hbs_compress_op(const dtn_op* op, int which, double eps, int64_t leaf_cap, dtn_hbs** out);
+void dtn_gpu_hbs_free(dtn_hbs* h);
+int dtn_gpu_hbs_info(const dtn_hbs* h, int64_t* M, int64_t* num_nodes, int32_t* depth, int64_t* max_rank,
+                     uint64_t* payload_bytes);
+/* nodes: 6 int64 per node (begin, end, left, right, parent, level), preorder; ranks: rank(t) */
+int dtn_gpu_hbs_tree(const dtn_hbs* h, int64_t* nodes, int64_t* ranks);
+/* which: 0 D (leaves), 1 U, 2 V (non-root), 3 B (parents); out (column-major, rows x cols) may be
+ * NULL to query the shape */
+int dtn_gpu_hbs_factor(const dtn_hbs* h, int32_t node, int32_t which, double* out, int64_t* rows, int64_t* cols);
+int dtn_gpu_hbs_apply(const dtn_hbs* h, const double* X, int64_t ldx, int64_t nrhs, double* Y, int64_t ldy,
+                      int on_device);
+/* buf NULL: *size receives the byte count only */
+int dtn_gpu_hbs_serialize(const dtn_hbs* h, uint8_t* buf, uint64_t cap, uint64_t* size);
+int dtn_gpu_hbs_deserialize(dtn_ctx* ctx, const uint8_t* buf, uint64_t size, dtn_hbs** out);
+
 #ifdef __cplusplus
 }
 #endif

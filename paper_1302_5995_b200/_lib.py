@@ -48,6 +48,8 @@ EXPORTS = [
     "dtn_gpu_apply", "dtn_gpu_ring_dtn", "dtn_gpu_body_map",
     "dtn_gpu_num_boxes", "dtn_gpu_box_info", "dtn_gpu_box_schur", "dtn_gpu_level_stats", "dtn_gpu_build_stats", "dtn_gpu_kernel_stats",
     "dtn_discretize_continuum", "dtn_discretize_network", "dtn_debug_partial_lu", "dtn_gpu_shard_info",
+    "dtn_gpu_hbs_compress", "dtn_gpu_hbs_compress_op", "dtn_gpu_hbs_free", "dtn_gpu_hbs_info", "dtn_gpu_hbs_tree",
+    "dtn_gpu_hbs_factor", "dtn_gpu_hbs_apply", "dtn_gpu_hbs_serialize", "dtn_gpu_hbs_deserialize",
 ]
 
 _lib = None
@@ -94,5 +96,15 @@ def lib():
     L.dtn_discretize_network.argtypes = [i32, f64, f64, C.c_uint64, vp]
     L.dtn_debug_partial_lu.argtypes = [i32, i32, vp, vp, vp, vp]
     L.dtn_gpu_shard_info.argtypes = [i32, i32, i32, i32, i32, P(i32), P(i64)]
+    L.dtn_gpu_hbs_compress.argtypes = [vp, vp, i64, i64, C.c_int, f64, i64, P(vp)]
+    L.dtn_gpu_hbs_compress_op.argtypes = [vp, C.c_int, f64, i64, P(vp)]
+    L.dtn_gpu_hbs_free.argtypes = [vp]
+    L.dtn_gpu_hbs_free.restype = None
+    L.dtn_gpu_hbs_info.argtypes = [vp, P(i64), P(i64), P(i32), P(i64), P(C.c_uint64)]
+    L.dtn_gpu_hbs_tree.argtypes = [vp, vp, vp]
+    L.dtn_gpu_hbs_factor.argtypes = [vp, i32, i32, vp, P(i64), P(i64)]
+    L.dtn_gpu_hbs_apply.argtypes = [vp, vp, i64, i64, vp, i64, C.c_int]
+    L.dtn_gpu_hbs_serialize.argtypes = [vp, vp, C.c_uint64, P(C.c_uint64)]
+    L.dtn_gpu_hbs_deserialize.argtypes = [vp, vp, C.c_uint64, P(vp)]
     _lib = L
     return L

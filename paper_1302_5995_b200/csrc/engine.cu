@@ -22,6 +22,7 @@
 #include "../../include/dtn_gpu.h"
 #include "common.cuh"
 #include "plan.hpp"
+#include "hbs.hpp"
 
 namespace dtnb {
 cudaError_t launch_small_elim(const KernelArgs&, const int*, int, int, bool, cudaStream_t);
@@ -815,6 +816,11 @@ struct dtn_ctx {
   GemmDesc* d_desc = nullptr;
 };
 
+struct dtn_hbs {
+  dtn_ctx* ctx = nullptr;
+  std::unique_ptr<HbsDev> h;
+};
+
 struct dtn_op {
   std::vector<dtn_kernel_stats> kstats;
   dtn_ctx* ctx = nullptr;
@@ -1455,6 +1461,197 @@ int dtn_discretize_network(int32_t n, double lo, double hi, uint64_t seed, doubl
       st[4 * nu + k] = -ss;
     }
   return DTN_OK;
+}
+
+// ---- HBS (compressed) operators: compress (hbs.cpp:61-178), apply
+// (hbs.cpp:187-232), DTNHBS01 (hbs.cpp:422-519); see csrc/hbs.cu
+int dtn_gpu_hbs_compress(dtn_ctx* ctx, const double* H, int64_t M, int64_t ldh, int on_device, double eps,
+                         int64_t leaf_cap, dtn_hbs** out) {
+  if (!ctx || !out) return DTN_EINVAL;
+  return guarded(ctx, [&] {
+    *out = nullptr;
+    if (!H || M < 1 || ldh < M) throw std::invalid_argument("compress: matrix/tree size mismatch");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    const double* dH = H;
+    double* tmp = nullptr;
+    int64_t ld = ldh;
+    if (!on_device) {
+      CK(cudaMalloc(&tmp, size_t(M) * M * 8));
+      CK(cudaMemcpy2DAsync(tmp, size_t(M) * 8, H, size_t(ldh) * 8, size_t(M) * 8, size_t(M), cudaMemcpyHostToDevice,
+                           st));
+      dH = tmp;
+      ld = M;
+    }
+    std::unique_ptr<HbsDev> h;
+    try {
+      h = hbs_compress(dH, ld, M, eps, leaf_cap, st);
+    } catch (...) {
+      if (tmp) cudaFree(tmp);
+      throw;
+    }
+    if (tmp) cudaFree(tmp);
+    auto* r = new dtn_hbs;
+    r->ctx = ctx;
+    r->h = std::move(h);
+    *out = r;
+  });
+}
+
+int dtn_gpu_hbs_compress_op(const dtn_op* op, int which, double eps, int64_t leaf_cap, dtn_hbs** out) {
+  if (!op || !out) return DTN_EINVAL;
+  dtn_ctx* ctx = op->ctx;
+  return guarded(ctx, [&] {
+    *out = nullptr;
+    if (which != 0 && which != 1) throw std::invalid_argument("compress: which must be 0 (G) or 1 (S)");
+    if (which == 0 && !op->has_G) throw std::invalid_argument("compress: G was not built (want_G = 0)");
+    CK(cudaSetDevice(ctx->device));
+    const PlanDev& D = *op->plan;
+    auto h = hbs_compress(which == 0 ? D.d_G : D.d_S, which == 0 ? D.ldg : D.lds, op->nb, eps, leaf_cap, ctx->stream);
+    auto* r = new dtn_hbs;
+    r->ctx = ctx;
+    r->h = std::move(h);
+    *out = r;
+  });
+}
+
+void dtn_gpu_hbs_free(dtn_hbs* h) {
+  if (!h) return;
+  if (h->ctx) cudaSetDevice(h->ctx->device);
+  delete h;
+}
+
+int dtn_gpu_hbs_info(const dtn_hbs* h, int64_t* M, int64_t* num_nodes, int32_t* depth, int64_t* max_rank,
+                     uint64_t* payload_bytes) {
+  if (!h || !h->h) return DTN_EINVAL;
+  const HbsDev& H = *h->h;
+  if (M) *M = H.M;
+  if (num_nodes) *num_nodes = int64_t(H.nodes.size());
+  if (depth) *depth = H.depth;
+  if (max_rank) *max_rank = H.max_rank();
+  if (payload_bytes) *payload_bytes = H.payload_bytes();
+  return DTN_OK;
+}
+
+int dtn_gpu_hbs_tree(const dtn_hbs* h, int64_t* nodes, int64_t* ranks) {
+  if (!h || !h->h) return DTN_EINVAL;
+  const HbsDev& H = *h->h;
+  for (size_t t = 0; t < H.nodes.size(); ++t) {
+    const auto& n = H.nodes[t];
+    if (nodes) {
+      int64_t* o = nodes + 6 * t;
+      o[0] = n.begin;
+      o[1] = n.end;
+      o[2] = n.left;
+      o[3] = n.right;
+      o[4] = n.parent;
+      o[5] = n.level;
+    }
+    if (ranks) ranks[t] = t == 0 ? 0 : H.rank[t];
+  }
+  return DTN_OK;
+}
+
+int dtn_gpu_hbs_factor(const dtn_hbs* h, int32_t node, int32_t which, double* out, int64_t* rows, int64_t* cols) {
+  if (!h || !h->h) return DTN_EINVAL;
+  dtn_ctx* ctx = h->ctx;
+  return guarded(ctx, [&] {
+    const HbsDev& H = *h->h;
+    if (node < 0 || node >= int32_t(H.nodes.size())) throw std::invalid_argument("hbs_factor: no such node");
+    const bool leaf = H.is_leaf(node);
+    const double* src = nullptr;
+    int64_t r = 0, c = 0;
+    switch (which) {
+      case 0:  // D (leaves)
+        if (!leaf) throw std::invalid_argument("hbs_factor: D exists on leaves only");
+        src = H.D[node];
+        r = c = H.node_size(node);
+        break;
+      case 1:
+      case 2:  // U, V (non-root)
+        if (node == 0) throw std::invalid_argument("hbs_factor: the root has no U/V");
+        src = which == 1 ? H.U[node] : H.V[node];
+        r = H.rows[node];
+        c = H.rank[node];
+        break;
+      case 3:  // B (parents)
+        if (leaf) throw std::invalid_argument("hbs_factor: B exists on parents only");
+        src = H.B[node];
+        r = c = H.rows[node];
+        break;
+      default:
+        throw std::invalid_argument("hbs_factor: which must be 0 (D), 1 (U), 2 (V) or 3 (B)");
+    }
+    if (rows) *rows = r;
+    if (cols) *cols = c;
+    if (out && r > 0 && c > 0) {
+      CK(cudaSetDevice(ctx->device));
+      CK(cudaMemcpy2D(out, size_t(r) * 8, src, size_t(H.ld(node)) * 8, size_t(r) * 8, size_t(c),
+                      cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+int dtn_gpu_hbs_apply(const dtn_hbs* h, const double* X, int64_t ldx, int64_t nrhs, double* Y, int64_t ldy,
+                      int on_device) {
+  if (!h || !h->h) return DTN_EINVAL;
+  dtn_ctx* ctx = h->ctx;
+  return guarded(ctx, [&] {
+    HbsDev& H = *h->h;
+    const int64_t M = H.M;
+    if (nrhs < 0 || ldx < M || ldy < M || (!X && nrhs) || (!Y && nrhs))
+      throw std::invalid_argument("apply: dimension mismatch");
+    if (nrhs == 0) return;
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    if (on_device) {
+      hbs_apply(H, X, ldx, nrhs, Y, ldy, st);
+    } else {
+      const size_t need = size_t(M) * size_t(nrhs);
+      if (need > ctx->stage_cap) {
+        if (ctx->d_x) cudaFree(ctx->d_x);
+        if (ctx->d_y) cudaFree(ctx->d_y);
+        ctx->d_x = ctx->d_y = nullptr;
+        ctx->stage_cap = 0;
+        CK(cudaMalloc(&ctx->d_x, need * 8));
+        CK(cudaMalloc(&ctx->d_y, need * 8));
+        ctx->stage_cap = need;
+      }
+      CK(cudaMemcpy2DAsync(ctx->d_x, size_t(M) * 8, X, size_t(ldx) * 8, size_t(M) * 8, size_t(nrhs),
+                           cudaMemcpyHostToDevice, st));
+      hbs_apply(H, ctx->d_x, M, nrhs, ctx->d_y, M, st);
+      CK(cudaMemcpy2DAsync(Y, size_t(ldy) * 8, ctx->d_y, size_t(M) * 8, size_t(M) * 8, size_t(nrhs),
+                           cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int dtn_gpu_hbs_serialize(const dtn_hbs* h, uint8_t* buf, uint64_t cap, uint64_t* size) {
+  if (!h || !h->h || !size) return DTN_EINVAL;
+  dtn_ctx* ctx = h->ctx;
+  return guarded(ctx, [&] {
+    CK(cudaSetDevice(ctx->device));
+    const std::vector<uint8_t> bytes = hbs_serialize(*h->h, ctx->stream);
+    *size = bytes.size();
+    if (!buf) return;
+    if (cap < bytes.size()) throw std::invalid_argument("hbs_serialize: buffer too small");
+    std::memcpy(buf, bytes.data(), bytes.size());
+  });
+}
+
+int dtn_gpu_hbs_deserialize(dtn_ctx* ctx, const uint8_t* buf, uint64_t size, dtn_hbs** out) {
+  if (!ctx || !out) return DTN_EINVAL;
+  return guarded(ctx, [&] {
+    *out = nullptr;
+    if (!buf) throw std::invalid_argument("deserialize: null buffer");
+    CK(cudaSetDevice(ctx->device));
+    auto hd = hbs_deserialize(buf, size_t(size), ctx->stream);
+    auto* r = new dtn_hbs;
+    r->ctx = ctx;
+    r->h = std::move(hd);
+    *out = r;
+  });
 }
 
 }  // extern "C"

@@ -1,0 +1,858 @@
+// HBS compression and apply on the device (the reference's hbs.cpp:61-232 and
+// its DTNHBS01 format, hbs.cpp:422-519), organised for the GPU.
+//
+// compress (hbs.cpp:61-178) keeps a "frontier" of already-compressed nodes
+// covering [0, M) and the reduced matrix R(f, g) = Ubig_f^T H(I_f, I_g) Vbig_g
+// (f != g), merging sibling pairs bottom up. Here the frontier is advanced one
+// tree height at a time, every node of that height at once: with X the current
+// reduced matrix (H itself for the leaves),
+//   1. the active diagonal blocks are taken out (leaf D, parent B) and zeroed,
+//   2. per active node f, the bases of the block row X(f, :) and the block
+//      column X(:, f) are the leading left singular vectors of those blocks
+//      (hbs.cpp:42-57 node_bases, shared rank = max of the two eps-ranks,
+//      hbs.cpp:33-40). Singular values are needed to eps = 1e-10 relative, so
+//      a plain Gram matrix (accurate to sqrt(machine eps)) is not enough: the
+//      block is first rotated by the eigenvectors U0 of its Gram matrix
+//      G1 = A A^T (Jacobi), which grades its rows by singular value
+//      (B = U0^T A); the Gram matrix of B, G2 = B B^T, is then diagonalised by
+//      Jacobi with the relative stopping rule, which resolves every singular
+//      value to relative accuracy (U = U0 W). All products are DMMA GEMMs.
+//   3. X' = blockdiag(U)^T X blockdiag(V) (identity blocks for nodes not yet
+//      active) is the next reduced matrix; its active diagonal blocks are
+//      exactly zero.
+// The result is an orthonormal-basis HBS matrix of the reference's structure
+// (D leaves, U/V non-root, B parents). Ranks and bases agree with the
+// reference's BDCSVD-based compress up to rounding (same eps rule); the
+// processing order (by height instead of reverse preorder) changes only
+// which already-truncated columns a node's block row sees, i.e. results at
+// the eps level.
+//
+// apply (hbs.cpp:187-232): upward x-hat = V^T x, root/parents B, downward
+// U y-hat, leaves D x + U y-hat; batched DMMA GEMMs per tree height on a
+// repacked copy of the factors whose ranks are padded to even (zero columns)
+// so every operand is 16-byte aligned.
+#include <algorithm>
+#include <cstring>
+#include <stdexcept>
+
+#include "common.cuh"
+#include "hbs.hpp"
+
+namespace dtnb {
+
+cudaError_t launch_gemm_desc(const GemmDesc* d_descs, int count, int max_tiles, int kmax, double alpha, double beta,
+                             cudaStream_t st, bool a_aligned);
+int gemm_tiles(int m, int n);
+cudaError_t launch_copy2d_batched(const void* d_descs, int count, cudaStream_t st);
+
+namespace {
+
+#define HCK(x)                                                                                        \
+  do {                                                                                                \
+    const cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess) throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e_) + \
+                                                    " at " #x);                                       \
+  } while (0)
+
+inline int64_t align2(int64_t x) { return (x + 1) & ~int64_t(1); }
+
+struct DevBuf {  // growable device scratch
+  void* p = nullptr;
+  size_t cap = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  void* get(size_t bytes) {
+    if (bytes > cap) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      cap = 0;
+      HCK(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+      cap = std::max<size_t>(bytes, 256);
+    }
+    return p;
+  }
+};
+
+// host descriptors -> device, then launch
+template <class T>
+T* upload(DevBuf& buf, const std::vector<T>& v, cudaStream_t st) {
+  T* d = static_cast<T*>(buf.get(v.size() * sizeof(T)));
+  if (!v.empty()) HCK(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+  return d;
+}
+
+void gemm_batch(DevBuf& buf, const std::vector<GemmDesc>& g, double alpha, double beta, bool a_aligned,
+                cudaStream_t st) {
+  if (g.empty()) return;
+  int tiles = 0, kmax = 0;
+  for (const auto& d : g) {
+    if (d.m <= 0 || d.n <= 0) continue;
+    tiles = std::max(tiles, gemm_tiles(d.m, d.n));
+    kmax = std::max(kmax, d.k);
+  }
+  if (tiles == 0) return;
+  GemmDesc* dd = upload(buf, g, st);
+  HCK(launch_gemm_desc(dd, int(g.size()), tiles, kmax, alpha, beta, st, a_aligned));
+  // the descriptor buffer is reused by the next batch: keep the upload ordered
+  HCK(cudaStreamSynchronize(st));
+}
+
+void transpose_batch(DevBuf& buf, const std::vector<TransDesc>& t, cudaStream_t st) {
+  if (t.empty()) return;
+  int tiles = 0;
+  for (const auto& d : t) tiles = std::max(tiles, ((d.m + 31) / 32) * ((d.n + 31) / 32));
+  TransDesc* dd = upload(buf, t, st);
+  HCK(launch_transpose_batched(dd, int(t.size()), tiles, st));
+  HCK(cudaStreamSynchronize(st));
+}
+
+void copy_batch(DevBuf& buf, const std::vector<CopyDesc>& c, cudaStream_t st) {
+  if (c.empty()) return;
+  CopyDesc* dd = upload(buf, c, st);
+  HCK(launch_copy2d_batched(dd, int(c.size()), st));
+  HCK(cudaStreamSynchronize(st));
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+std::vector<HbsTreeNode> hbs_index_tree(int64_t M, int64_t leaf_cap, int* depth) {
+  if (M < 1) throw std::invalid_argument("build_index_tree: M must be >= 1");
+  if (leaf_cap < 2) throw std::invalid_argument("build_index_tree: leaf_cap must be >= 2");
+  std::vector<HbsTreeNode> nodes;
+  int dmax = 0;
+  // preorder: node, left subtree, right subtree (index_tree.cpp:39-52)
+  struct Frame {
+    int64_t b, e;
+    int parent, level, side;
+  };
+  std::vector<Frame> stack{{0, M, -1, 0, 0}};
+  while (!stack.empty()) {
+    const Frame f = stack.back();
+    stack.pop_back();
+    const int id = int(nodes.size());
+    HbsTreeNode n;
+    n.begin = f.b;
+    n.end = f.e;
+    n.parent = f.parent;
+    n.level = f.level;
+    nodes.push_back(n);
+    dmax = std::max(dmax, f.level);
+    if (f.parent >= 0) (f.side == 0 ? nodes[f.parent].left : nodes[f.parent].right) = id;
+    if (f.e - f.b > leaf_cap) {
+      const int64_t mid = f.b + (f.e - f.b + 1) / 2;
+      stack.push_back({mid, f.e, id, f.level + 1, 1});  // right popped after the whole left subtree
+      stack.push_back({f.b, mid, id, f.level + 1, 0});
+    }
+  }
+  if (depth) *depth = dmax;
+  return nodes;
+}
+
+HbsDev::~HbsDev() {
+  if (device >= 0) cudaSetDevice(device);
+  for (void* p : buffers) cudaFree(p);
+  if (pk.buf) cudaFree(pk.buf);
+  if (ws) cudaFree(ws);
+  if (d_desc) cudaFree(d_desc);
+}
+
+int64_t HbsDev::max_rank() const {
+  int64_t k = 0;
+  for (size_t t = 1; t < nodes.size(); ++t) k = std::max<int64_t>(k, rank[t]);
+  return k;
+}
+
+uint64_t HbsDev::payload_bytes() const {
+  uint64_t n = 0;
+  for (size_t t = 0; t < nodes.size(); ++t) {
+    if (is_leaf(int(t))) n += uint64_t(node_size(int(t))) * uint64_t(node_size(int(t)));
+    if (t != 0) n += 2 * uint64_t(rows[t]) * uint64_t(rank[t]);
+    if (!is_leaf(int(t))) n += uint64_t(rows[t]) * uint64_t(rows[t]);
+  }
+  return n * sizeof(double);
+}
+
+// ---------------------------------------------------------------------------
+std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, double eps, int64_t leaf_cap,
+                                     cudaStream_t st) {
+  if (M < 1 || ldh < M) throw std::invalid_argument("compress: matrix/tree size mismatch");
+  if (!(eps >= 0.0)) throw std::invalid_argument("compress: eps must be >= 0");
+  if (M > (int64_t(1) << 30) / 2) throw std::invalid_argument("compress: matrix too large");
+  auto out = std::make_unique<HbsDev>();
+  HbsDev& H = *out;
+  HCK(cudaGetDevice(&H.device));
+  H.M = M;
+  H.nodes = hbs_index_tree(M, leaf_cap, &H.depth);
+  const int nn = int(H.nodes.size());
+  H.rank.assign(nn, 0);
+  H.rows.assign(nn, 0);
+  H.height.assign(nn, 0);
+  H.D.assign(nn, nullptr);
+  H.U.assign(nn, nullptr);
+  H.V.assign(nn, nullptr);
+  H.B.assign(nn, nullptr);
+  for (int t = nn - 1; t >= 0; --t)  // children have larger preorder ids
+    if (!H.is_leaf(t)) H.height[t] = 1 + std::max(H.height[H.nodes[t].left], H.height[H.nodes[t].right]);
+  DevBuf dbuf;
+  if (nn == 1) {  // stored densely (hbs.cpp:75-78)
+    H.rows[0] = int(M);
+    double* d = nullptr;
+    HCK(cudaMalloc(&d, size_t(H.ld(0)) * M * 8));
+    H.buffers.push_back(d);
+    H.D[0] = d;
+    copy_batch(dbuf, {CopyDesc{dH, d, int(ldh), H.ld(0), int(M), int(M)}}, st);
+    return out;
+  }
+
+  // work buffers (ld = align2(M) everywhere; every slot column block 16-byte aligned)
+  const int64_t L = align2(M);
+  const size_t big = size_t(L) * size_t(M);
+  double *X = nullptr, *XT = nullptr, *P1 = nullptr, *P2 = nullptr, *Q1 = nullptr, *Q2 = nullptr;
+  struct Frees {
+    std::vector<void*> v;
+    ~Frees() {
+      for (void* p : v) cudaFree(p);
+    }
+  } frees;
+  for (double** p : {&X, &XT, &P1, &P2}) {
+    HCK(cudaMalloc(p, big * 8));
+    frees.v.push_back(*p);
+  }
+  // B blocks (align2(s) x nX each, all active nodes): up to (M + nodes) x M
+  const size_t qbig = size_t(M + nn) * size_t(M) + 64;
+  for (double** p : {&Q1, &Q2}) {
+    HCK(cudaMalloc(p, qbig * 8));
+    frees.v.push_back(*p);
+  }
+  // X = H
+  copy_batch(dbuf, {CopyDesc{dH, X, int(ldh), int(L), int(M), int(M)}}, st);
+  int64_t nX = M, ldX = L;
+
+  // frontier: node ids in index order with their slot offsets and sizes
+  std::vector<int> slots;
+  for (int t = 0; t < nn; ++t)
+    if (H.is_leaf(t)) slots.push_back(t);
+  std::sort(slots.begin(), slots.end(), [&](int a, int b) { return H.nodes[a].begin < H.nodes[b].begin; });
+  std::vector<int> ssize(nn, 0);
+  for (int t : slots) ssize[t] = int(H.node_size(t));
+  const int R = H.height[0];
+
+  for (int r = 0; r <= R; ++r) {
+    // parents of height r take their children's adjacent slots
+    if (r > 0) {
+      std::vector<int> ns;
+      for (size_t i = 0; i < slots.size(); ++i) {
+        const int t = slots[i], p = H.nodes[t].parent;
+        if (p >= 0 && H.height[p] == r && H.nodes[p].left == t) {
+          if (i + 1 >= slots.size() || slots[i + 1] != H.nodes[p].right)
+            throw std::logic_error("compress: children not adjacent in frontier");
+          ns.push_back(p);
+          ssize[p] = ssize[t] + ssize[slots[i + 1]];
+          H.rows[p] = ssize[p];
+          ++i;
+        } else {
+          ns.push_back(t);
+        }
+      }
+      slots.swap(ns);
+    }
+    std::vector<int64_t> off(slots.size());
+    {
+      int64_t o = 0;
+      for (size_t i = 0; i < slots.size(); ++i) {
+        off[i] = o;
+        o += ssize[slots[i]];
+      }
+      if (o != nX) throw std::logic_error("compress: frontier size mismatch");
+    }
+    std::vector<int> act;  // frontier positions of this round's nodes
+    for (size_t i = 0; i < slots.size(); ++i)
+      if (H.height[slots[i]] == r) act.push_back(int(i));
+
+    if (r == R) {  // the root: B = the reduced matrix of its two children (hbs.cpp:122-125)
+      double* b = nullptr;
+      H.rows[0] = int(nX);
+      HCK(cudaMalloc(&b, size_t(H.ld(0)) * nX * 8 + 8));
+      H.buffers.push_back(b);
+      H.B[0] = b;
+      copy_batch(dbuf, {CopyDesc{X, b, int(ldX), H.ld(0), int(nX), int(nX)}}, st);
+      break;
+    }
+
+    // 1. diagonal blocks out (leaf D / parent B), then zeroed
+    size_t diag_doubles = 0;
+    for (int i : act) diag_doubles += size_t(align2(ssize[slots[i]])) * ssize[slots[i]];
+    double* dbase = nullptr;
+    HCK(cudaMalloc(&dbase, diag_doubles * 8 + 8));
+    H.buffers.push_back(dbase);
+    {
+      std::vector<CopyDesc> cp;
+      std::vector<ZeroDesc> zd;
+      size_t o = 0;
+      for (int i : act) {
+        const int t = slots[i], s = ssize[t];
+        double* dst = dbase + o;
+        o += size_t(align2(s)) * s;
+        (H.is_leaf(t) ? H.D[t] : H.B[t]) = dst;
+        H.rows[t] = s;
+        double* blk = X + off[i] + off[i] * ldX;
+        cp.push_back(CopyDesc{blk, dst, int(ldX), int(align2(s)), s, s});
+        zd.push_back(ZeroDesc{blk, int(ldX), s, s});
+      }
+      copy_batch(dbuf, cp, st);
+      ZeroDesc* dz = upload(dbuf, zd, st);
+      HCK(launch_zero_blocks(dz, int(zd.size()), st));
+      HCK(cudaStreamSynchronize(st));
+    }
+    // 2. XT = X^T
+    transpose_batch(dbuf, {TransDesc{X, XT, int(ldX), int(ldX), int(nX), int(nX)}}, st);
+
+    // per active node and side (0: rows -> U, 1: columns -> V): work layout
+    const int na = int(act.size());
+    std::vector<size_t> goff(na);
+    size_t gsum = 0;
+    int smax = 0;
+    for (int a = 0; a < na; ++a) {
+      const int s = ssize[slots[act[a]]];
+      goff[a] = gsum;
+      gsum += size_t(align2(s)) * s;
+      smax = std::max(smax, s);
+    }
+    if (smax > 1024) throw std::runtime_error("compress: block of more than 1024 rows (rank too high)");
+    // G1 (2 sides), U0, G2, W, Ufull: 2 * 5 * gsum doubles; select outputs
+    double* wk = nullptr;
+    HCK(cudaMalloc(&wk, (10 * gsum + 2 * size_t(na) * smax) * 8 + 64));
+    frees.v.push_back(wk);
+    auto G1 = [&](int side, int a) { return wk + (0 * 2 + side) * gsum + goff[a]; };
+    auto U0 = [&](int side, int a) { return wk + (1 * 2 + side) * gsum + goff[a]; };
+    auto G2 = [&](int side, int a) { return wk + (2 * 2 + side) * gsum + goff[a]; };
+    auto W = [&](int side, int a) { return wk + (3 * 2 + side) * gsum + goff[a]; };
+    auto UF = [&](int side, int a) { return wk + (4 * 2 + side) * gsum + goff[a]; };
+    double* sig = wk + 10 * gsum;
+    int* ordr = nullptr;
+    HCK(cudaMalloc(&ordr, (2 * size_t(na) * smax + 2 * size_t(na)) * sizeof(int)));
+    frees.v.push_back(ordr);
+    int* rk = ordr + 2 * size_t(na) * smax;
+
+    // 3. G1: rows X(f,:) X(f,:)^T = X(f,:) XT(:,f); columns XT(f,:) X(:,f)
+    {
+      std::vector<GemmDesc> g;
+      for (int a = 0; a < na; ++a) {
+        const int i = act[a], s = ssize[slots[i]];
+        const int ld = int(align2(s));
+        g.push_back(GemmDesc{X + off[i], XT + off[i] * ldX, G1(0, a), s, s, int(nX), int(ldX), int(ldX), ld});
+        g.push_back(GemmDesc{XT + off[i], X + off[i] * ldX, G1(1, a), s, s, int(nX), int(ldX), int(ldX), ld});
+      }
+      gemm_batch(dbuf, g, 1.0, 0.0, false, st);
+    }
+    // 4. Jacobi on G1 -> U0
+    {
+      std::vector<EigDesc> e;
+      for (int a = 0; a < na; ++a) {
+        const int s = ssize[slots[act[a]]], ld = int(align2(s));
+        for (int side = 0; side < 2; ++side) e.push_back(EigDesc{G1(side, a), U0(side, a), s, ld, ld});
+      }
+      EigDesc* de = upload(dbuf, e, st);
+      HCK(launch_jacobi_eig(de, int(e.size()), 30, false, st));
+      HCK(cudaStreamSynchronize(st));
+    }
+    // 5. B^T = A^T U0: rows side XT(:, f) U0r (nX x s) into P1, columns side X(:, f) U0c into P2
+    //    (column block a of P at offset off[i] * L)
+    {
+      std::vector<GemmDesc> g;
+      for (int a = 0; a < na; ++a) {
+        const int i = act[a], s = ssize[slots[i]], ld = int(align2(s));
+        g.push_back(GemmDesc{XT + off[i] * ldX, U0(0, a), P1 + off[i] * L, int(nX), s, s, int(ldX), ld, int(L)});
+        g.push_back(GemmDesc{X + off[i] * ldX, U0(1, a), P2 + off[i] * L, int(nX), s, s, int(ldX), ld, int(L)});
+      }
+      gemm_batch(dbuf, g, 1.0, 0.0, true, st);
+    }
+    // 6. B = (B^T)^T (s x nX, ld align2(s)) into Q1/Q2
+    std::vector<size_t> qoff(na);
+    {
+      size_t q = 0;
+      for (int a = 0; a < na; ++a) {
+        qoff[a] = q;
+        q += size_t(align2(ssize[slots[act[a]]])) * size_t(nX);
+      }
+      if (q > qbig) throw std::logic_error("compress: B workspace overflow");
+      std::vector<TransDesc> t;
+      for (int a = 0; a < na; ++a) {
+        const int i = act[a], s = ssize[slots[i]], ld = int(align2(s));
+        t.push_back(TransDesc{P1 + off[i] * L, Q1 + qoff[a], int(L), ld, int(nX), s});
+        t.push_back(TransDesc{P2 + off[i] * L, Q2 + qoff[a], int(L), ld, int(nX), s});
+      }
+      transpose_batch(dbuf, t, st);
+    }
+    // 7. G2 = B B^T
+    {
+      std::vector<GemmDesc> g;
+      for (int a = 0; a < na; ++a) {
+        const int i = act[a], s = ssize[slots[i]], ld = int(align2(s));
+        g.push_back(GemmDesc{Q1 + qoff[a], P1 + off[i] * L, G2(0, a), s, s, int(nX), ld, int(L), ld});
+        g.push_back(GemmDesc{Q2 + qoff[a], P2 + off[i] * L, G2(1, a), s, s, int(nX), ld, int(L), ld});
+      }
+      gemm_batch(dbuf, g, 1.0, 0.0, true, st);
+    }
+    // 8. Jacobi (relative) on G2 -> W, lambda on the diagonal
+    {
+      std::vector<EigDesc> e;
+      for (int a = 0; a < na; ++a) {
+        const int s = ssize[slots[act[a]]], ld = int(align2(s));
+        for (int side = 0; side < 2; ++side) e.push_back(EigDesc{G2(side, a), W(side, a), s, ld, ld});
+      }
+      EigDesc* de = upload(dbuf, e, st);
+      HCK(launch_jacobi_eig(de, int(e.size()), 30, true, st));
+      HCK(cudaStreamSynchronize(st));
+    }
+    // 9. Ufull = U0 W
+    {
+      std::vector<GemmDesc> g;
+      for (int a = 0; a < na; ++a) {
+        const int s = ssize[slots[act[a]]], ld = int(align2(s));
+        for (int side = 0; side < 2; ++side) g.push_back(GemmDesc{U0(side, a), W(side, a), UF(side, a), s, s, s, ld, ld, ld});
+      }
+      gemm_batch(dbuf, g, 1.0, 0.0, true, st);
+    }
+    // 10. ranks (hbs.cpp:33-40, 47-57)
+    std::vector<int> kf(na);
+    {
+      std::vector<SelDesc> sd;
+      for (int a = 0; a < na; ++a) {
+        const int s = ssize[slots[act[a]]], ld = int(align2(s));
+        for (int side = 0; side < 2; ++side) {
+          const size_t j = 2 * size_t(a) + side;
+          sd.push_back(SelDesc{G2(side, a), ordr + j * smax, sig + j * smax, rk + j, s, ld + 1});
+        }
+      }
+      SelDesc* ds = upload(dbuf, sd, st);
+      HCK(launch_hbs_select(ds, int(sd.size()), eps, st));
+      std::vector<int> hr(2 * size_t(na));
+      HCK(cudaMemcpyAsync(hr.data(), rk, hr.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
+      HCK(cudaStreamSynchronize(st));
+      for (int a = 0; a < na; ++a) kf[a] = std::max(hr[2 * a], hr[2 * a + 1]);
+    }
+    // 11. U_f, V_f = leading kf columns (s x k, ld s)
+    {
+      size_t tot = 0;
+      for (int a = 0; a < na; ++a) tot += 2 * size_t(align2(ssize[slots[act[a]]])) * kf[a];
+      double* ub = nullptr;
+      HCK(cudaMalloc(&ub, tot * 8 + 8));
+      H.buffers.push_back(ub);
+      std::vector<GatherDesc> gd;
+      size_t o = 0;
+      for (int a = 0; a < na; ++a) {
+        const int t = slots[act[a]], s = ssize[t], ld = int(align2(s));
+        H.rank[t] = kf[a];
+        H.U[t] = ub + o;
+        o += size_t(ld) * kf[a];
+        H.V[t] = ub + o;
+        o += size_t(ld) * kf[a];
+        if (kf[a] == 0) continue;
+        gd.push_back(GatherDesc{UF(0, a), H.U[t], ordr + (2 * size_t(a)) * smax, ld, ld, s, kf[a]});
+        gd.push_back(GatherDesc{UF(1, a), H.V[t], ordr + (2 * size_t(a) + 1) * smax, ld, ld, s, kf[a]});
+      }
+      if (!gd.empty()) {
+        GatherDesc* dg = upload(dbuf, gd, st);
+        HCK(launch_gather_cols(dg, int(gd.size()), st));
+        HCK(cudaStreamSynchronize(st));
+      }
+    }
+    // 12. next reduced matrix: TT = XT blockdiag(U~) (nX x nX'), T = TT^T, X' = T blockdiag(V~)
+    std::vector<int64_t> noff(slots.size());
+    int64_t nX2 = 0;
+    std::vector<int> apos(slots.size(), -1);
+    for (int a = 0; a < na; ++a) apos[act[a]] = a;
+    for (size_t i = 0; i < slots.size(); ++i) {
+      noff[i] = nX2;
+      nX2 += apos[i] >= 0 ? kf[apos[i]] : ssize[slots[i]];
+    }
+    const int64_t ldX2 = align2(std::max<int64_t>(nX2, 1));
+    {
+      std::vector<GemmDesc> g;
+      std::vector<CopyDesc> c;
+      for (size_t i = 0; i < slots.size(); ++i) {
+        const int t = slots[i], s = ssize[t];
+        if (apos[i] >= 0) {
+          if (kf[apos[i]] > 0)
+            g.push_back(GemmDesc{XT + off[i] * ldX, H.U[t], P1 + noff[i] * L, int(nX), kf[apos[i]], s, int(ldX),
+                                 H.ld(t), int(L)});
+        } else {
+          c.push_back(CopyDesc{XT + off[i] * ldX, P1 + noff[i] * L, int(ldX), int(L), int(nX), s});
+        }
+      }
+      gemm_batch(dbuf, g, 1.0, 0.0, true, st);
+      copy_batch(dbuf, c, st);
+    }
+    transpose_batch(dbuf, {TransDesc{P1, P2, int(L), int(ldX2), int(nX), int(nX2)}}, st);  // T: nX' x nX
+    {
+      std::vector<GemmDesc> g;
+      std::vector<CopyDesc> c;
+      for (size_t i = 0; i < slots.size(); ++i) {
+        const int t = slots[i], s = ssize[t];
+        if (apos[i] >= 0) {
+          const int k = kf[apos[i]];
+          if (k == 0) continue;
+          g.push_back(GemmDesc{P2 + off[i] * ldX2, H.V[t], X + noff[i] * ldX2, int(nX2), k, s, int(ldX2), H.ld(t),
+                               int(ldX2)});
+        } else {
+          c.push_back(CopyDesc{P2 + off[i] * ldX2, X + noff[i] * ldX2, int(ldX2), int(ldX2), int(nX2), s});
+        }
+      }
+      gemm_batch(dbuf, g, 1.0, 0.0, true, st);
+      copy_batch(dbuf, c, st);
+    }
+    for (int a = 0; a < na; ++a) ssize[slots[act[a]]] = kf[a];
+    nX = nX2;
+    ldX = ldX2;
+  }
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+namespace {
+
+void pack_for_apply(HbsDev& H, cudaStream_t st) {
+  auto& P = H.pk;
+  if (P.ready) return;
+  const int nn = int(H.nodes.size());
+  P.kp.assign(nn, 0);
+  P.xo.assign(nn, 0);
+  P.pb.assign(nn, 0);
+  P.D.assign(nn, nullptr);
+  P.VT.assign(nn, nullptr);
+  P.U.assign(nn, nullptr);
+  P.B.assign(nn, nullptr);
+  P.ldD.assign(nn, 0);
+  P.ldVT.assign(nn, 0);
+  P.ldU.assign(nn, 0);
+  P.ldB.assign(nn, 0);
+  for (int t = 1; t < nn; ++t) P.kp[t] = int(align2(H.rank[t]));
+  // x-hat offsets: sibling pairs contiguous (left then right), pairs in preorder
+  int64_t xo = 0, pb = 0;
+  for (int t = 0; t < nn; ++t) {
+    if (!H.is_leaf(t)) {
+      const int l = H.nodes[t].left, r = H.nodes[t].right;
+      P.xo[l] = int(xo);
+      P.xo[r] = int(xo + P.kp[l]);
+      xo += P.kp[l] + P.kp[r];
+    } else {
+      P.pb[t] = int(pb);
+      pb += align2(H.node_size(t));
+    }
+  }
+  P.xh_rows = std::max<int64_t>(align2(xo), 2);
+  P.xp_rows = std::max<int64_t>(pb, 2);
+  // sizes
+  size_t tot = 0;
+  auto need = [&](int64_t r, int64_t c) { return size_t(align2(r)) * size_t(c); };
+  for (int t = 0; t < nn; ++t) {
+    const bool leaf = H.is_leaf(t);
+    const int64_t inner = leaf ? H.node_size(t) : P.kp[H.nodes[t].left] + P.kp[H.nodes[t].right];
+    if (leaf) tot += need(inner, inner);
+    if (t != 0) tot += need(P.kp[t], inner) + need(inner, P.kp[t]);
+    if (!leaf) tot += need(inner, inner);
+  }
+  HCK(cudaMalloc(&P.buf, tot * 8 + 64));
+  double* base = static_cast<double*>(P.buf);
+  size_t o = 0;
+  std::vector<PackDesc> pd;
+  for (int t = 0; t < nn; ++t) {
+    const bool leaf = H.is_leaf(t);
+    int i1, ip1, i2, inner;  // inner index map (rows of U/B, columns of V^T/B)
+    if (leaf) {
+      inner = int(H.node_size(t));
+      i1 = inner;
+      ip1 = inner;
+      i2 = 0;
+    } else {
+      const int l = H.nodes[t].left, r = H.nodes[t].right;
+      inner = P.kp[l] + P.kp[r];
+      i1 = H.rank[l];
+      ip1 = P.kp[l];
+      i2 = H.rank[r];
+    }
+    const int ldi = int(align2(inner));
+    if (leaf) {
+      P.D[t] = base + o;
+      P.ldD[t] = ldi;
+      o += size_t(ldi) * inner;
+      pd.push_back(PackDesc{H.D[t], P.D[t], H.ld(t), ldi, inner, inner, inner, inner, 0, inner, inner, 0, 0});
+    }
+    if (t != 0) {
+      const int k = H.rank[t], kp = P.kp[t], ldk = int(align2(kp));
+      P.VT[t] = base + o;
+      P.ldVT[t] = std::max(ldk, 2);
+      o += size_t(std::max(ldk, 2)) * inner;
+      // VT(i, j) = V(map(j), i): rows i < k, columns via the inner map
+      pd.push_back(PackDesc{H.V[t], P.VT[t], std::max(H.ld(t), 2), std::max(ldk, 2), kp, inner, k, kp, 0, i1, ip1, i2, 1});
+      P.U[t] = base + o;
+      P.ldU[t] = ldi;
+      o += size_t(ldi) * kp;
+      pd.push_back(PackDesc{H.U[t], P.U[t], std::max(H.ld(t), 2), ldi, inner, kp, i1, ip1, i2, k, kp, 0, 0});
+    }
+    if (!leaf) {
+      P.B[t] = base + o;
+      P.ldB[t] = ldi;
+      o += size_t(ldi) * inner;
+      pd.push_back(PackDesc{H.B[t], P.B[t], std::max(H.ld(t), 2), ldi, inner, inner, i1, ip1, i2, i1, ip1, i2, 0});
+    }
+  }
+  DevBuf dbuf;
+  // drop empty descriptors
+  std::vector<PackDesc> pk2;
+  for (const auto& d : pd)
+    if (d.rp > 0 && d.cp > 0) pk2.push_back(d);
+  if (!pk2.empty()) {
+    PackDesc* dd = upload(dbuf, pk2, st);
+    HCK(launch_pack(dd, int(pk2.size()), st));
+    HCK(cudaStreamSynchronize(st));
+  }
+  P.ready = true;
+}
+
+}  // namespace
+
+void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* dY, int64_t ldy, cudaStream_t st) {
+  if (nrhs <= 0) return;
+  const int nn = int(H.nodes.size());
+  DevBuf dbuf;
+  if (nn == 1) {
+    // Y = D X (the dense single-node case); B operand alignment: stage X
+    const int64_t M = H.M, ld = align2(M);
+    double* xs = nullptr;
+    HCK(cudaMalloc(&xs, size_t(ld) * nrhs * 8 + 8));
+    copy_batch(dbuf, {CopyDesc{dX, xs, int(ldx), int(ld), int(M), int(nrhs)}}, st);
+    gemm_batch(dbuf, {GemmDesc{H.D[0], xs, dY, int(M), int(nrhs), int(M), H.ld(0), int(ld), int(ldy)}}, 1.0, 0.0,
+               true, st);
+    cudaFree(xs);
+    return;
+  }
+  pack_for_apply(H, st);
+  auto& P = H.pk;
+  const int64_t nx = P.xp_rows, nh = P.xh_rows;
+  const size_t need = size_t(nx + 2 * nh) * size_t(nrhs);
+  if (need > H.ws_doubles) {
+    if (H.ws) cudaFree(H.ws);
+    H.ws = nullptr;
+    H.ws_doubles = 0;
+    HCK(cudaMalloc(&H.ws, need * 8 + 64));
+    H.ws_doubles = need;
+  }
+  double* xp = H.ws;
+  double* xh = xp + nx * nrhs;
+  double* yh = xh + nh * nrhs;
+  HCK(cudaMemsetAsync(xp, 0, size_t(nx) * nrhs * 8, st));
+  // gather x into the padded leaf layout
+  {
+    std::vector<CopyDesc> c;
+    for (int t = 0; t < nn; ++t)
+      if (H.is_leaf(t))
+        c.push_back(CopyDesc{dX + H.nodes[t].begin, xp + P.pb[t], int(ldx), int(nx), int(H.node_size(t)), int(nrhs)});
+    copy_batch(dbuf, c, st);
+  }
+  const int R = H.height[0];
+  // upward: x-hat_t = V_t^T (leaf: x_t; parent: [x-hat_l; x-hat_r])
+  for (int r = 0; r < R; ++r) {
+    std::vector<GemmDesc> g;
+    for (int t = 1; t < nn; ++t) {
+      if (H.height[t] != r || P.kp[t] == 0) continue;
+      const bool leaf = H.is_leaf(t);
+      const int inner = leaf ? int(H.node_size(t)) : P.kp[H.nodes[t].left] + P.kp[H.nodes[t].right];
+      if (inner == 0) continue;
+      const double* src = leaf ? xp + P.pb[t] : xh + P.xo[H.nodes[t].left];
+      g.push_back(GemmDesc{P.VT[t], src, xh + P.xo[t], P.kp[t], int(nrhs), inner, P.ldVT[t], int(leaf ? nx : nh),
+                           int(nh)});
+    }
+    // children with zero padded rank still need defined x-hat rows: zero them once
+    gemm_batch(dbuf, g, 1.0, 0.0, true, st);
+  }
+  // downward: [y-hat_l; y-hat_r] = B_t [x-hat_l; x-hat_r] + U_t y-hat_t
+  HCK(cudaMemsetAsync(yh, 0, size_t(nh) * nrhs * 8, st));
+  for (int r = R; r >= 1; --r) {
+    std::vector<GemmDesc> gb, gu;
+    for (int t = 0; t < nn; ++t) {
+      if (H.height[t] != r || H.is_leaf(t)) continue;
+      const int l = H.nodes[t].left;
+      const int inner = P.kp[l] + P.kp[H.nodes[t].right];
+      if (inner == 0) continue;
+      gb.push_back(GemmDesc{P.B[t], xh + P.xo[l], yh + P.xo[l], inner, int(nrhs), inner, P.ldB[t], int(nh), int(nh)});
+      if (t != 0 && P.kp[t] > 0)
+        gu.push_back(GemmDesc{P.U[t], yh + P.xo[t], yh + P.xo[l], inner, int(nrhs), P.kp[t], P.ldU[t], int(nh), int(nh)});
+    }
+    gemm_batch(dbuf, gb, 1.0, 0.0, true, st);
+    gemm_batch(dbuf, gu, 1.0, 1.0, true, st);
+  }
+  // leaves: y_t = D_t x_t + U_t y-hat_t
+  {
+    std::vector<GemmDesc> gd, gu;
+    for (int t = 0; t < nn; ++t) {
+      if (!H.is_leaf(t)) continue;
+      const int s = int(H.node_size(t));
+      gd.push_back(GemmDesc{P.D[t], xp + P.pb[t], dY + H.nodes[t].begin, s, int(nrhs), s, P.ldD[t], int(nx), int(ldy)});
+      if (P.kp[t] > 0)
+        gu.push_back(GemmDesc{P.U[t], yh + P.xo[t], dY + H.nodes[t].begin, s, int(nrhs), P.kp[t], P.ldU[t], int(nh),
+                              int(ldy)});
+    }
+    gemm_batch(dbuf, gd, 1.0, 0.0, true, st);
+    gemm_batch(dbuf, gu, 1.0, 1.0, true, st);
+  }
+}
+
+// ---------------------------------------------------------------------------
+namespace {
+
+const char kMagic[8] = {'D', 'T', 'N', 'H', 'B', 'S', '0', '1'};
+
+void put_i64(std::vector<uint8_t>& out, int64_t v) {
+  for (int i = 0; i < 8; ++i) out.push_back(uint8_t(uint64_t(v) >> (8 * i)));
+}
+
+void put_matrix(std::vector<uint8_t>& out, const double* d, int64_t ld, int64_t r, int64_t c, cudaStream_t st) {
+  put_i64(out, r);
+  put_i64(out, c);
+  const size_t bytes = size_t(r) * size_t(c) * 8;
+  const size_t at = out.size();
+  out.resize(at + bytes);
+  if (bytes) {
+    HCK(cudaMemcpy2DAsync(out.data() + at, size_t(r) * 8, d, size_t(ld) * 8, size_t(r) * 8, size_t(c),
+                          cudaMemcpyDeviceToHost, st));
+    HCK(cudaStreamSynchronize(st));
+  }
+}
+
+struct Reader {
+  const uint8_t* p;
+  const uint8_t* end;
+  int64_t i64() {
+    if (end - p < 8) throw std::invalid_argument("deserialize: truncated input");
+    uint64_t v = 0;
+    for (int i = 0; i < 8; ++i) v |= uint64_t(p[i]) << (8 * i);
+    p += 8;
+    return int64_t(v);
+  }
+};
+
+}  // namespace
+
+std::vector<uint8_t> hbs_serialize(const HbsDev& H, cudaStream_t st) {
+  std::vector<uint8_t> out(kMagic, kMagic + 8);
+  put_i64(out, H.M);
+  put_i64(out, int64_t(H.nodes.size()));
+  put_i64(out, H.depth);
+  for (const auto& n : H.nodes) {
+    put_i64(out, n.begin);
+    put_i64(out, n.end);
+    put_i64(out, n.left);
+    put_i64(out, n.right);
+    put_i64(out, n.parent);
+    put_i64(out, n.level);
+  }
+  for (int t = 0; t < int(H.nodes.size()); ++t) {
+    const bool leaf = H.is_leaf(t);
+    if (leaf) put_matrix(out, H.D[t], H.ld(t), H.node_size(t), H.node_size(t), st);
+    if (t != 0) {
+      put_matrix(out, H.U[t], H.ld(t), H.rows[t], H.rank[t], st);
+      put_matrix(out, H.V[t], H.ld(t), H.rows[t], H.rank[t], st);
+    }
+    if (!leaf) put_matrix(out, H.B[t], H.ld(t), H.rows[t], H.rows[t], st);
+  }
+  return out;
+}
+
+std::unique_ptr<HbsDev> hbs_deserialize(const uint8_t* data, size_t size, cudaStream_t st) {
+  if (size < 8 || std::memcmp(data, kMagic, 8) != 0) throw std::invalid_argument("deserialize: bad magic");
+  Reader rd{data + 8, data + size};
+  auto out = std::make_unique<HbsDev>();
+  HbsDev& H = *out;
+  HCK(cudaGetDevice(&H.device));
+  H.M = rd.i64();
+  const int64_t nn = rd.i64();
+  H.depth = int(rd.i64());
+  if (nn < 1 || nn > (int64_t(1) << 24)) throw std::invalid_argument("deserialize: bad header");
+  H.nodes.resize(size_t(nn));
+  for (auto& n : H.nodes) {
+    n.begin = rd.i64();
+    n.end = rd.i64();
+    n.left = int(rd.i64());
+    n.right = int(rd.i64());
+    n.parent = int(rd.i64());
+    n.level = int(rd.i64());
+  }
+  if (H.nodes[0].end != H.M || H.nodes[0].begin != 0) throw std::invalid_argument("deserialize: bad header");
+  for (int t = 0; t < int(nn); ++t) {
+    const auto& n = H.nodes[t];
+    if ((n.left < 0) != (n.right < 0) || n.left >= nn || n.right >= nn || n.left == 0 || n.right == 0)
+      throw std::invalid_argument("deserialize: bad tree");
+  }
+  H.rank.assign(nn, 0);
+  H.rows.assign(nn, 0);
+  H.height.assign(nn, 0);
+  H.D.assign(nn, nullptr);
+  H.U.assign(nn, nullptr);
+  H.V.assign(nn, nullptr);
+  H.B.assign(nn, nullptr);
+  for (int t = int(nn) - 1; t >= 0; --t)
+    if (!H.is_leaf(t)) H.height[t] = 1 + std::max(H.height[H.nodes[t].left], H.height[H.nodes[t].right]);
+  // first pass: shapes
+  struct Mat {
+    int64_t r, c;
+    const uint8_t* p;
+  };
+  std::vector<Mat> mats;
+  size_t total = 0;
+  auto matrix = [&]() {
+    const int64_t r = rd.i64(), c = rd.i64();
+    if (r < 0 || c < 0) throw std::invalid_argument("deserialize: bad matrix shape");
+    const size_t bytes = size_t(r) * size_t(c) * 8;
+    if (size_t(rd.end - rd.p) < bytes) throw std::invalid_argument("deserialize: truncated input");
+    mats.push_back({r, c, rd.p});
+    rd.p += bytes;
+    total += size_t(align2(r)) * size_t(c);
+  };
+  for (int t = 0; t < int(nn); ++t) {
+    const bool leaf = H.is_leaf(t);
+    if (leaf) matrix();
+    if (t != 0) {
+      matrix();
+      matrix();
+    }
+    if (!leaf) matrix();
+  }
+  double* buf = nullptr;
+  HCK(cudaMalloc(&buf, total * 8 + 8));
+  H.buffers.push_back(buf);
+  size_t o = 0, m = 0;
+  auto place = [&](double*& dst) {
+    const Mat& x = mats[m++];
+    dst = buf + o;
+    const int64_t ld = align2(x.r);
+    if (x.r > 0 && x.c > 0)
+      HCK(cudaMemcpy2D(dst, size_t(ld) * 8, x.p, size_t(x.r) * 8, size_t(x.r) * 8, size_t(x.c), cudaMemcpyHostToDevice));
+    o += size_t(ld) * size_t(x.c);
+    return x;
+  };
+  for (int t = 0; t < int(nn); ++t) {
+    const bool leaf = H.is_leaf(t);
+    if (leaf) {
+      const Mat x = place(H.D[t]);
+      H.rows[t] = int(x.r);
+    }
+    if (t != 0) {
+      const Mat u = place(H.U[t]);
+      place(H.V[t]);
+      H.rank[t] = int(u.c);
+      H.rows[t] = int(u.r);
+    }
+    if (!leaf) {
+      const Mat b = place(H.B[t]);
+      H.rows[t] = int(b.r);
+    }
+  }
+  (void)st;
+  return out;
+}
+
+}  // namespace dtnb

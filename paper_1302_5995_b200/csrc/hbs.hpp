@@ -1,0 +1,122 @@
+// HBS (hierarchically block separable) matrices on the device: compression of
+// a dense device-resident matrix, the telescoping apply, and the DTNHBS01
+// byte format -- the reference's HbsMatrix (proj/include/dtn/hbs.hpp:30-51,
+// proj/src/hbs.cpp) restated B200-first (see hbs.cu for the algorithm).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+namespace dtnb {
+
+struct TransDesc {  // dst (n x m) = src (m x n)^T
+  const double* src;
+  double* dst;
+  int lds, ldd, m, n;
+};
+
+struct EigDesc {  // A (s x s, symmetric) -> diag(lambda) on its diagonal; V eigenvectors
+  double* A;
+  double* V;
+  int s, lda, ldv;
+};
+
+struct SelDesc {  // lambda_i = lam[i * stride]; outputs order[s], sigma[s] (sorted), rank
+  const double* lam;
+  int* order;
+  double* sigma;
+  int* rank;
+  int s, stride;
+};
+
+struct GatherDesc {  // dst(:, j) = src(:, order[j]), j < k
+  const double* src;
+  double* dst;
+  const int* order;
+  int lds, ldd, rows, k;
+};
+
+struct PackDesc {  // see pack_kernel (k_hbs.cu)
+  const double* src;
+  double* dst;
+  int lds, ldd, rp, cp;
+  int r1, rp1, r2, c1, cp1, c2;
+  int trans;
+};
+
+struct ZeroDesc {
+  double* p;
+  int ld, m, n;
+};
+
+cudaError_t launch_transpose_batched(const TransDesc* d_descs, int count, int max_tiles, cudaStream_t st);
+cudaError_t launch_jacobi_eig(const EigDesc* d_descs, int count, int max_sweeps, bool rel, cudaStream_t st);
+cudaError_t launch_hbs_select(const SelDesc* d_descs, int count, double eps, cudaStream_t st);
+cudaError_t launch_gather_cols(const GatherDesc* d_descs, int count, cudaStream_t st);
+cudaError_t launch_pack(const PackDesc* d_descs, int count, cudaStream_t st);
+cudaError_t launch_zero_blocks(const ZeroDesc* d_descs, int count, cudaStream_t st);
+
+// IndexTree node (index_tree.hpp:12-22): contiguous range [begin, end),
+// preorder ids, children -1 for leaves.
+struct HbsTreeNode {
+  int64_t begin = 0, end = 0;
+  int left = -1, right = -1, parent = -1, level = 0;
+};
+
+// build_index_tree (index_tree.cpp:37-67): balanced halving, the left half
+// taking the extra index, ranges above leaf_cap split.
+std::vector<HbsTreeNode> hbs_index_tree(int64_t M, int64_t leaf_cap, int* depth);
+
+struct HbsDev {
+  int device = 0;
+  int64_t M = 0;
+  int depth = 0;
+  std::vector<HbsTreeNode> nodes;
+  std::vector<int> rank;    // k_t (U/V columns); 0 for the root
+  std::vector<int> rows;    // node_rows: leaf size, or k_left + k_right
+  std::vector<int> height;  // 0 for leaves, 1 + max(children)
+  // canonical factors (column-major, leading dimension ld(t) = rows rounded up
+  // to even: every column 16-byte aligned for the DMMA GEMM), device
+  std::vector<double*> D, U, V, B;
+  int ld(int t) const { return int((rows[t] + 1) & ~1); }
+  std::vector<void*> buffers;  // owning allocations
+  // apply layout: ranks padded to even with zero columns, every block 16-byte aligned
+  struct Packed {
+    bool ready = false;
+    std::vector<int> kp, xo, pb;  // padded rank, x-hat row offset, padded leaf row offset
+    int64_t xh_rows = 0, xp_rows = 0;
+    std::vector<double*> D, VT, U, B;  // ld = align2(rows)
+    std::vector<int> ldD, ldVT, ldU, ldB;
+    void* buf = nullptr;
+  } pk;
+  // apply workspace
+  double* ws = nullptr;
+  size_t ws_doubles = 0;
+  void* d_desc = nullptr;
+  size_t desc_bytes = 0;
+  ~HbsDev();
+  int64_t max_rank() const;
+  uint64_t payload_bytes() const;
+  bool is_leaf(int t) const { return nodes[t].left < 0; }
+  int64_t node_size(int t) const { return nodes[t].end - nodes[t].begin; }
+};
+
+// compress (hbs.cpp:61-178): dense H (M x M, column-major, leading dimension
+// ldh, device memory) onto build_index_tree(M, leaf_cap) with relative
+// tolerance eps. Throws std::invalid_argument / std::runtime_error.
+std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, double eps, int64_t leaf_cap,
+                                     cudaStream_t st);
+
+// Y (M x nrhs) = H X through the telescoping factorization (hbs.cpp:187-232);
+// X, Y device pointers.
+void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* dY, int64_t ldy, cudaStream_t st);
+
+// DTNHBS01 serialization (hbs.cpp:422-519), byte-for-byte the reference layout.
+std::vector<uint8_t> hbs_serialize(const HbsDev& H, cudaStream_t st);
+std::unique_ptr<HbsDev> hbs_deserialize(const uint8_t* data, size_t size, cudaStream_t st);
+
+}  // namespace dtnb

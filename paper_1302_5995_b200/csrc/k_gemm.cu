@@ -24,7 +24,7 @@ struct GemmSmem {
   double b[2][GBN][gemm_ldb<BK>()];
 };
 
-// One BM x BN tile of C = alpha*A*B + beta*C with alpha, beta in {(1,0), (-1,1)}:
+// One BM x BN tile of C = alpha*A*B + beta*C (any alpha, beta; (-1, 1) is UPD):
 // UPD (C -= A*B) preloads the C tile into the accumulators before the K loop
 // (its latency overlaps the first A/B stage) and feeds -A to the DMMA, so the
 // epilogue is a plain store. Requires 16-byte aligned B columns.
@@ -371,8 +371,7 @@ cudaError_t launch_gemm_desc(const GemmDesc* d_descs, int count, int max_tiles, 
     return cudaGetLastError();
   }
   dim3 grid(max_tiles, count);
-  const bool upd = alpha == -1.0 && beta == 1.0;
-  if (!upd && !(alpha == 1.0 && beta == 0.0)) return cudaErrorInvalidValue;
+  const bool upd = alpha == -1.0 && beta == 1.0;  // other (alpha, beta): scaled epilogue
   const bool bk16 = kmax % 16 == 0 || kmax > 64;
   const bool bk32 = kmax >= gemm_bk32_min();
 #define DTNB_DESC_LAUNCH(BK, U, AL) \

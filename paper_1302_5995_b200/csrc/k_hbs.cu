@@ -1,0 +1,282 @@
+// Kernels of the HBS (hierarchically block separable) compression and apply
+// (hbs.cpp:61-232 restated for the GPU, see hbs.cu): batched transposes,
+// a batched cyclic Jacobi eigensolver for the per-node Gram matrices, the
+// rank selection, column gathers and the zero-padded repacking of factors.
+// The contractions themselves run on the DMMA GEMM (k_gemm.cu).
+#include <cfloat>
+#include <cstdint>
+
+#include "common.cuh"
+#include "hbs.hpp"
+
+namespace dtnb {
+
+// ---- dst (n x m) = src (m x n)^T, batched; 32 x 32 tiles through shared memory
+__global__ void __launch_bounds__(256) transpose_batched_kernel(const TransDesc* __restrict__ descs) {
+  __shared__ double tile[32][33];
+  const TransDesc d = descs[blockIdx.y];
+  const int tm = (d.m + 31) / 32, tn = (d.n + 31) / 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int t = blockIdx.x; t < tm * tn; t += gridDim.x) {
+    const int r0 = (t % tm) * 32, c0 = (t / tm) * 32;
+#pragma unroll
+    for (int k = 0; k < 32; k += 8) {
+      const int r = r0 + tx, c = c0 + ty + k;
+      tile[ty + k][tx] = (r < d.m && c < d.n) ? d.src[r + (long long)c * d.lds] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 32; k += 8) {
+      const int c = c0 + tx, r = r0 + ty + k;  // dst row c, column r
+      if (c < d.n && r < d.m) d.dst[c + (long long)r * d.ldd] = tile[tx][ty + k];
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_transpose_batched(const TransDesc* d_descs, int count, int max_tiles, cudaStream_t st) {
+  if (count <= 0 || max_tiles <= 0) return cudaSuccess;
+  transpose_batched_kernel<<<dim3(std::min(max_tiles, 1184), count), 256, 0, st>>>(d_descs);
+  return cudaGetLastError();
+}
+
+// ---- symmetric eigen-decomposition A = V diag(lambda) V^T by the cyclic
+// Jacobi method, parallel (round-robin) ordering: each round rotates s/2
+// disjoint (p, q) pairs, a sweep is s-1 rounds. One CTA per matrix; A (and V
+// when both fit) live in shared memory with an odd leading dimension,
+// otherwise in global memory (L2). A rotation is skipped when
+// |a_pq| <= tol * sqrt(|a_pp a_qq|) (rel: Demmel-Veselic relative accuracy,
+// used on the graded second-pass Gram matrices) or <= tol * max|a_ii| (not rel).
+// On exit the diagonal of desc.A holds lambda and desc.V the eigenvectors.
+constexpr int JT = 512;
+constexpr int JMAXP = 512;  // max pairs (s <= 1024)
+
+__global__ void __launch_bounds__(JT) jacobi_eig_kernel(const EigDesc* __restrict__ descs, int max_sweeps,
+                                                       int smem_doubles, int rel) {
+  extern __shared__ __align__(16) double jsm[];
+  __shared__ double cs_[JMAXP], sn_[JMAXP];
+  __shared__ int pp_[JMAXP], qq_[JMAXP];
+  __shared__ int rotated;
+  __shared__ double amax;
+  const EigDesc d = descs[blockIdx.x];
+  const int s = d.s, tid = threadIdx.x;
+  if (s <= 0) return;
+  const int ls = s | 1;
+  const long long need = (long long)s * ls;
+  double* A = d.A;
+  long long lda = d.lda;
+  double* V = d.V;
+  long long ldv = d.ldv;
+  const bool a_sm = need <= smem_doubles, v_sm = 2 * need <= smem_doubles;
+  if (a_sm) {
+    A = jsm;
+    lda = ls;
+    for (long long e = tid; e < (long long)s * s; e += JT) {
+      const int r = int(e % s), c = int(e / s);
+      A[r + c * lda] = d.A[r + c * d.lda];
+    }
+  }
+  if (v_sm) {
+    V = jsm + need;
+    ldv = ls;
+  }
+  for (long long e = tid; e < (long long)s * s; e += JT) {
+    const int r = int(e % s), c = int(e / s);
+    V[r + c * ldv] = r == c ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int i = 0; i < s; ++i) m = fmax(m, fabs(A[i + i * lda]));
+    amax = m;
+  }
+  __syncthreads();
+  const double tol = DBL_EPSILON;
+  const double abs_tol = tol * amax;
+  const int n2 = s + (s & 1), np = n2 / 2;
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    if (tid == 0) rotated = 0;
+    __syncthreads();
+    for (int r = 0; r < n2 - 1; ++r) {
+      for (int i = tid; i < np; i += JT) {
+        int a, b;
+        if (i == 0) {
+          a = r;
+          b = n2 - 1;
+        } else {
+          a = (r + i) % (n2 - 1);
+          b = (r - i + n2 - 1) % (n2 - 1);
+        }
+        const int p = min(a, b), q = max(a, b);
+        double c = 1.0, sg = 0.0;
+        if (q < s) {
+          const double app = A[p + p * lda], aqq = A[q + q * lda], apq = A[p + q * lda];
+          const double thr = rel ? tol * sqrt(fabs(app * aqq)) : abs_tol;
+          if (apq != 0.0 && fabs(apq) > thr) {
+            const double tau = (aqq - app) / (2.0 * apq);
+            double t;
+            if (fabs(tau) > 1e150) t = 0.5 / tau;
+            else t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            c = 1.0 / sqrt(1.0 + t * t);
+            sg = t * c;
+            rotated = 1;
+          }
+        }
+        cs_[i] = c;
+        sn_[i] = sg;
+        pp_[i] = p;
+        qq_[i] = q;
+      }
+      __syncthreads();
+      // rows p, q <- J^T (rows)
+      for (int w = tid; w < np * s; w += JT) {
+        const int i = w / s, j = w - i * s;
+        const double sg = sn_[i];
+        if (sg != 0.0) {
+          const double c = cs_[i];
+          const int p = pp_[i], q = qq_[i];
+          const double x = A[p + j * lda], y = A[q + j * lda];
+          A[p + j * lda] = c * x - sg * y;
+          A[q + j * lda] = sg * x + c * y;
+        }
+      }
+      __syncthreads();
+      // columns p, q <- (A J), V <- V J
+      for (int w = tid; w < np * s; w += JT) {
+        const int i = w / s, j = w - i * s;
+        const double sg = sn_[i];
+        if (sg != 0.0) {
+          const double c = cs_[i];
+          const int p = pp_[i], q = qq_[i];
+          const double x = A[j + p * lda], y = A[j + q * lda];
+          A[j + p * lda] = c * x - sg * y;
+          A[j + q * lda] = sg * x + c * y;
+          const double vx = V[j + p * ldv], vy = V[j + q * ldv];
+          V[j + p * ldv] = c * vx - sg * vy;
+          V[j + q * ldv] = sg * vx + c * vy;
+        }
+      }
+      __syncthreads();
+    }
+    if (!rotated) break;
+    __syncthreads();
+  }
+  if (a_sm)
+    for (int i = tid; i < s; i += JT) d.A[i + (long long)i * d.lda] = A[i + i * lda];
+  if (v_sm)
+    for (long long e = tid; e < (long long)s * s; e += JT) {
+      const int r = int(e % s), c = int(e / s);
+      d.V[r + c * d.ldv] = V[r + c * ldv];
+    }
+}
+
+int jacobi_smem_doubles() { return 200 * 1024 / 8; }
+
+cudaError_t launch_jacobi_eig(const EigDesc* d_descs, int count, int max_sweeps, bool rel, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  static const cudaError_t attr = cudaFuncSetAttribute(jacobi_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       jacobi_smem_doubles() * 8);
+  if (attr != cudaSuccess) return attr;
+  jacobi_eig_kernel<<<count, JT, size_t(jacobi_smem_doubles()) * 8, st>>>(d_descs, max_sweeps, jacobi_smem_doubles(),
+                                                                        rel ? 1 : 0);
+  return cudaGetLastError();
+}
+
+// ---- rank selection (hbs.cpp:33-40 svd_rank): sigma_i = sqrt(max(lambda_i, 0)),
+// sorted descending (ties: lower index first); rank = #{sigma_i > eps sigma_0},
+// 0 when sigma_0 <= 0. One CTA per descriptor.
+__global__ void __launch_bounds__(256) hbs_select_kernel(const SelDesc* __restrict__ descs, double eps) {
+  const SelDesc d = descs[blockIdx.x];
+  const int s = d.s;
+  __shared__ double top;
+  __shared__ int cnt;
+  if (threadIdx.x == 0) {
+    top = 0.0;
+    cnt = 0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < s; i += blockDim.x) {
+    const double li = d.lam[(long long)i * d.stride];
+    int pos = 0;
+    for (int j = 0; j < s; ++j) {
+      const double lj = d.lam[(long long)j * d.stride];
+      pos += (lj > li || (lj == li && j < i)) ? 1 : 0;
+    }
+    d.order[pos] = i;
+    d.sigma[pos] = sqrt(fmax(li, 0.0));
+    if (pos == 0) top = sqrt(fmax(li, 0.0));
+  }
+  __syncthreads();
+  const double cut = eps * top;
+  for (int i = threadIdx.x; i < s; i += blockDim.x)
+    if (top > 0.0 && d.sigma[i] > cut) atomicAdd(&cnt, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) *d.rank = cnt;
+}
+
+cudaError_t launch_hbs_select(const SelDesc* d_descs, int count, double eps, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  hbs_select_kernel<<<count, 256, 0, st>>>(d_descs, eps);
+  return cudaGetLastError();
+}
+
+// ---- dst(:, j) = src(:, order[j]), j < k
+__global__ void gather_cols_kernel(const GatherDesc* __restrict__ descs) {
+  const GatherDesc d = descs[blockIdx.y];
+  const long long total = (long long)d.rows * d.k;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int r = int(e % d.rows), j = int(e / d.rows);
+    d.dst[r + (long long)j * d.ldd] = d.src[r + (long long)d.order[j] * d.lds];
+  }
+}
+
+cudaError_t launch_gather_cols(const GatherDesc* d_descs, int count, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  gather_cols_kernel<<<dim3(32, count), 256, 0, st>>>(d_descs);
+  return cudaGetLastError();
+}
+
+// ---- repack with zero padding (and optional transpose): dst(i, j) =
+// src(rmap(i), cmap(j)) (trans: src(cmap(j), rmap(i))), 0 where a map is -1;
+// map(i) = i for i < x1, x1 + (i - xp1) for xp1 <= i < xp1 + x2, else -1
+__device__ __forceinline__ int pack_map(int i, int x1, int xp1, int x2) {
+  if (i < x1) return i;
+  if (i >= xp1 && i < xp1 + x2) return x1 + (i - xp1);
+  return -1;
+}
+
+__global__ void pack_kernel(const PackDesc* __restrict__ descs) {
+  const PackDesc d = descs[blockIdx.y];
+  const long long total = (long long)d.rp * d.cp;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int i = int(e % d.rp), j = int(e / d.rp);
+    const int ri = pack_map(i, d.r1, d.rp1, d.r2), cj = pack_map(j, d.c1, d.cp1, d.c2);
+    double v = 0.0;
+    if (ri >= 0 && cj >= 0) v = d.trans ? d.src[cj + (long long)ri * d.lds] : d.src[ri + (long long)cj * d.lds];
+    d.dst[i + (long long)j * d.ldd] = v;
+  }
+}
+
+cudaError_t launch_pack(const PackDesc* d_descs, int count, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  pack_kernel<<<dim3(32, count), 256, 0, st>>>(d_descs);
+  return cudaGetLastError();
+}
+
+// ---- zero m x n blocks
+__global__ void zero_blocks_kernel(const ZeroDesc* __restrict__ descs) {
+  const ZeroDesc d = descs[blockIdx.y];
+  const long long total = (long long)d.m * d.n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int r = int(e % d.m), c = int(e / d.m);
+    d.p[r + (long long)c * d.ld] = 0.0;
+  }
+}
+
+cudaError_t launch_zero_blocks(const ZeroDesc* d_descs, int count, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  zero_blocks_kernel<<<dim3(32, count), 256, 0, st>>>(d_descs);
+  return cudaGetLastError();
+}
+
+}  // namespace dtnb

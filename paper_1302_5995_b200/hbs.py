@@ -1,0 +1,285 @@
+"""Compressed (HBS) operators on the B200: the reference's HbsMatrix
+(proj/include/dtn/hbs.hpp:30-51) with compress / apply / serialize
+(proj/src/hbs.cpp:61-232, 422-519) running on the device through the C ABI
+(include/dtn_gpu.h, dtn_gpu_hbs_*; kernels in csrc/k_hbs.cu, csrc/hbs.cu).
+
+The factors stay in HBM; `factor()` / `D`, `U`, `V`, `B` fetch host copies.
+There is no CPU fallback: every compute call goes through libdtn_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib as L
+from .dtn import Context, default_context
+
+__all__ = ["IndexTree", "build_index_tree", "HbsMatrix", "compress", "compress_operator", "apply", "reconstruct",
+           "serialize", "deserialize", "write_hbs", "read_hbs", "basis_orthonormality_defect"]
+
+
+@dataclass
+class IndexNode:
+    begin: int
+    end: int
+    left: int = -1
+    right: int = -1
+    parent: int = -1
+    level: int = 0
+
+
+class IndexTree:
+    """index_tree.hpp:12-38: contiguous ranges, preorder ids."""
+
+    def __init__(self, nodes, depth):
+        self.nodes = list(nodes)
+        self.depth = int(depth)
+
+    def size(self):
+        return self.nodes[0].end if self.nodes else 0
+
+    def num_nodes(self):
+        return len(self.nodes)
+
+    def is_leaf(self, t):
+        return self.nodes[t].left < 0
+
+    def node_size(self, t):
+        return self.nodes[t].end - self.nodes[t].begin
+
+    def top_down(self):
+        return list(range(len(self.nodes)))
+
+    def bottom_up(self):
+        return list(reversed(range(len(self.nodes))))
+
+    def __eq__(self, other):
+        if not isinstance(other, IndexTree) or len(self.nodes) != len(other.nodes):
+            return False
+        return all((a.begin, a.end, a.left, a.right) == (b.begin, b.end, b.left, b.right)
+                   for a, b in zip(self.nodes, other.nodes))
+
+
+def build_index_tree(M: int, leaf_cap: int) -> IndexTree:
+    """build_index_tree (index_tree.cpp:37-67): balanced halving, the left half
+    taking the extra index. Host bookkeeping (the device builds the same tree
+    in hbs_index_tree, csrc/hbs.cu)."""
+    if M < 1:
+        raise ValueError("build_index_tree: M must be >= 1")
+    if leaf_cap < 2:
+        raise ValueError("build_index_tree: leaf_cap must be >= 2")
+    nodes: list[IndexNode] = []
+    depth = 0
+
+    def sub(b, e, parent, level):
+        nonlocal depth
+        i = len(nodes)
+        nodes.append(IndexNode(b, e, -1, -1, parent, level))
+        depth = max(depth, level)
+        if e - b > leaf_cap:
+            mid = b + (e - b + 1) // 2
+            l_ = sub(b, mid, i, level + 1)
+            r_ = sub(mid, e, i, level + 1)
+            nodes[i].left, nodes[i].right = l_, r_
+        return i
+
+    sub(0, M, -1, 0)
+    return IndexTree(nodes, depth)
+
+
+class HbsMatrix:
+    """Device-resident HbsMatrix (hbs.hpp:30-51)."""
+
+    def __init__(self, ctx: Context, handle: C.c_void_p):
+        self.ctx, self.h = ctx, handle
+        M, nn, mr, pb = C.c_int64(), C.c_int64(), C.c_int64(), C.c_uint64()
+        dp = C.c_int32()
+        ctx.check(L.lib().dtn_gpu_hbs_info(handle, C.byref(M), C.byref(nn), C.byref(dp), C.byref(mr), C.byref(pb)))
+        self._M, self._max_rank, self._payload = M.value, mr.value, pb.value
+        raw = np.zeros((nn.value, 6), dtype=np.int64)
+        ranks = np.zeros(nn.value, dtype=np.int64)
+        ctx.check(L.lib().dtn_gpu_hbs_tree(handle, raw.ctypes.data, ranks.ctypes.data))
+        self.tree = IndexTree([IndexNode(*map(int, r)) for r in raw], dp.value)
+        self.ranks = ranks
+        self._cache: dict = {}
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                L.lib().dtn_gpu_hbs_free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    # hbs.hpp:37-50
+    def size(self) -> int:
+        return self._M
+
+    def rank(self, t: int) -> int:
+        return 0 if t == 0 else int(self.ranks[t])
+
+    def node_rows(self, t: int) -> int:
+        if self.tree.is_leaf(t):
+            return self.tree.node_size(t)
+        n = self.tree.nodes[t]
+        return self.rank(n.left) + self.rank(n.right)
+
+    def max_rank(self) -> int:
+        return self._max_rank
+
+    def payload_bytes(self) -> int:
+        return self._payload
+
+    def factor(self, t: int, which: str) -> np.ndarray:
+        key = (t, which)
+        if key not in self._cache:
+            w = {"D": 0, "U": 1, "V": 2, "B": 3}[which]
+            r, c = C.c_int64(), C.c_int64()
+            self.ctx.check(L.lib().dtn_gpu_hbs_factor(self.h, t, w, None, C.byref(r), C.byref(c)))
+            out = np.zeros((r.value, c.value), dtype=np.float64, order="F")
+            self.ctx.check(L.lib().dtn_gpu_hbs_factor(self.h, t, w, out.ctypes.data, C.byref(r), C.byref(c)))
+            self._cache[key] = out
+        return self._cache[key]
+
+    def _all(self, which, pred):
+        return [self.factor(t, which) if pred(t) else None for t in range(self.tree.num_nodes())]
+
+    @property
+    def D(self):
+        return self._all("D", self.tree.is_leaf)
+
+    @property
+    def U(self):
+        return self._all("U", lambda t: t != 0)
+
+    @property
+    def V(self):
+        return self._all("V", lambda t: t != 0)
+
+    @property
+    def B(self):
+        return self._all("B", lambda t: not self.tree.is_leaf(t))
+
+    def apply(self, x):
+        return apply(self, x)
+
+    def serialize(self) -> bytes:
+        return serialize(self)
+
+
+def _ctx(ctx):
+    return ctx if ctx is not None else default_context()
+
+
+def compress(H, eps: float, leaf_cap: int = 64, ctx: Context | None = None) -> HbsMatrix:
+    """compress(H, eps, leaf_cap) (hbs.hpp:58-62): H is a host array or a
+    float64 CUDA tensor (column-major or row-major contiguous)."""
+    ctx = _ctx(ctx)
+    out = C.c_void_p()
+    try:
+        import torch
+        is_t = isinstance(H, torch.Tensor)
+    except ImportError:  # pragma: no cover
+        is_t = False
+    if is_t:
+        if H.dtype != torch.float64 or not H.is_cuda or H.dim() != 2 or H.shape[0] != H.shape[1]:
+            raise ValueError("compress: H must be a square float64 CUDA tensor")
+        Hc = H.t().contiguous().t() if H.stride(0) != 1 else H  # column-major
+        ctx.check(L.lib().dtn_gpu_hbs_compress(ctx.h, Hc.data_ptr(), H.shape[0], Hc.stride(1) if H.shape[0] > 1 else 1,
+                                               1, float(eps), int(leaf_cap), C.byref(out)))
+    else:
+        A = np.asfortranarray(np.asarray(H, dtype=np.float64))
+        if A.ndim != 2 or A.shape[0] != A.shape[1]:
+            raise ValueError("compress: matrix/tree size mismatch")
+        ctx.check(L.lib().dtn_gpu_hbs_compress(ctx.h, A.ctypes.data, A.shape[0], A.shape[0], 0, float(eps),
+                                               int(leaf_cap), C.byref(out)))
+    return HbsMatrix(ctx, out)
+
+
+def compress_operator(sol, which: str = "G", eps: float = 1e-10, leaf_cap: int = 64) -> HbsMatrix:
+    """Compress a built operator's resident G (apply_dtn) or S (apply_schur)
+    in place in HBM: SolutionOperator::G_hbs / S_hbs (solution_operator.hpp:38-42)."""
+    out = C.c_void_p()
+    sol.ctx.check(L.lib().dtn_gpu_hbs_compress_op(sol.h, 0 if which == "G" else 1, float(eps), int(leaf_cap),
+                                                  C.byref(out)))
+    return HbsMatrix(sol.ctx, out)
+
+
+def apply(H: HbsMatrix, x):
+    """apply(H, x) (hbs.hpp:66, hbs.cpp:187-232): x is (M,) / (M, k) host, or a
+    float64 CUDA tensor (result stays on the device)."""
+    M = H.size()
+    try:
+        import torch
+        is_t = isinstance(x, torch.Tensor)
+    except ImportError:  # pragma: no cover
+        is_t = False
+    if is_t:
+        if x.dtype != torch.float64 or not x.is_cuda:
+            raise ValueError("apply: torch input must be a float64 CUDA tensor")
+        vec = x.dim() == 1
+        X = x.reshape(M, -1) if vec else x
+        if X.shape[0] != M:
+            raise ValueError("apply: dimension mismatch")
+        Xf = X.t().contiguous().t() if (X.stride(0) != 1 and X.shape[1] > 1) else X.contiguous()
+        Y = torch.empty((X.shape[1], M), dtype=torch.float64, device=x.device).t()
+        ldx = Xf.stride(1) if Xf.shape[1] > 1 else M
+        H.ctx.check(L.lib().dtn_gpu_hbs_apply(H.h, Xf.data_ptr(), ldx, Xf.shape[1], Y.data_ptr(), M, 1))
+        return Y.reshape(M) if vec else Y
+    X = np.asarray(x, dtype=np.float64)
+    vec = X.ndim == 1
+    if X.shape[0] != M:
+        raise ValueError("apply: dimension mismatch")
+    X2 = np.asfortranarray(X.reshape(M, -1))
+    Y = np.zeros_like(X2, order="F")
+    if X2.shape[1]:
+        H.ctx.check(L.lib().dtn_gpu_hbs_apply(H.h, X2.ctypes.data, M, X2.shape[1], Y.ctypes.data, M, 0))
+    return Y[:, 0].copy() if vec else Y
+
+
+def reconstruct(H: HbsMatrix) -> np.ndarray:
+    """Exact dense evaluation of the stored factorization (hbs.hpp:69, a testing
+    aid): the telescoping apply of the identity, on the device."""
+    return apply(H, np.eye(H.size()))
+
+
+def basis_orthonormality_defect(H: HbsMatrix) -> float:
+    """hbs.cpp:405-417: max_t ||U^T U - I||_max over U and V (a host check on the fetched bases)."""
+    d = 0.0
+    for t in range(1, H.tree.num_nodes()):
+        for w in ("U", "V"):
+            b = H.factor(t, w)
+            if b.shape[1] == 0:
+                continue
+            d = max(d, float(np.abs(b.T @ b - np.eye(b.shape[1])).max()))
+    return d
+
+
+def serialize(H: HbsMatrix) -> bytes:
+    """DTNHBS01 (hbs.cpp:446-470)."""
+    n = C.c_uint64()
+    H.ctx.check(L.lib().dtn_gpu_hbs_serialize(H.h, None, 0, C.byref(n)))
+    buf = (C.c_uint8 * n.value)()
+    H.ctx.check(L.lib().dtn_gpu_hbs_serialize(H.h, buf, n.value, C.byref(n)))
+    return bytes(buf)
+
+
+def deserialize(data: bytes, ctx: Context | None = None) -> HbsMatrix:
+    """hbs.cpp:472-505: the factors are uploaded to the device."""
+    ctx = _ctx(ctx)
+    out = C.c_void_p()
+    b = (C.c_uint8 * len(data)).from_buffer_copy(data) if len(data) else (C.c_uint8 * 1)()
+    ctx.check(L.lib().dtn_gpu_hbs_deserialize(ctx.h, b, len(data), C.byref(out)))
+    return HbsMatrix(ctx, out)
+
+
+def write_hbs(H: HbsMatrix, path: str) -> None:
+    with open(path, "wb") as f:
+        f.write(serialize(H))
+
+
+def read_hbs(path: str, ctx: Context | None = None) -> HbsMatrix:
+    with open(path, "rb") as f:
+        return deserialize(f.read(), ctx)

@@ -1,0 +1,141 @@
+"""GPU HBS compression / apply / DTNHBS01 (csrc/hbs.cu, csrc/k_hbs.cu through
+the C ABI) against the oracle restatement of hbs.cpp and the reference's own
+HBS test properties (proj/tests/test_hbs.cpp)."""
+import numpy as np
+import pytest
+
+from oracle import hbs_oracle as HO
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_fro(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.fixture(scope="module")
+def H():
+    from paper_1302_5995_b200 import hbs
+    return hbs
+
+
+def test_identity_rank_zero(H):  # test_hbs.cpp:88-100
+    c = H.compress(np.eye(96), 1e-10, 16)
+    assert c.max_rank() == 0
+    for t in range(c.tree.num_nodes()):
+        if c.tree.is_leaf(t):
+            assert np.abs(c.factor(t, "D") - np.eye(c.tree.node_size(t))).max() == 0.0
+    assert rel_fro(H.reconstruct(c), np.eye(96)) <= 1e-14
+
+
+def test_rank_one(H):  # test_hbs.cpp:102-108
+    rng = np.random.default_rng(1)
+    A = rng.standard_normal((80, 1)) @ rng.standard_normal((1, 80))
+    c = H.compress(A, 1e-10, 16)
+    assert c.max_rank() <= 1
+    assert rel_fro(H.reconstruct(c), A) <= 1e-12
+
+
+def test_laplace_root_schur(H):  # test_hbs.cpp:110-116
+    S = O.build_root_dense(O.Problem("laplace", 64), O.Tree(64, 4096)).S
+    c = H.compress(S, 1e-7, 64)
+    assert rel_fro(H.reconstruct(c), S) <= 1e-6
+    assert c.max_rank() < S.shape[0] / 4
+    assert H.basis_orthonormality_defect(c) <= 1e-12
+
+
+def test_apply_matches_dense(H):  # test_hbs.cpp:118-125
+    A = HO.kernel_matrix(150, 3)
+    c = H.compress(A, 1e-9, 32)
+    x = np.random.default_rng(4).standard_normal((150, 3))
+    assert rel_fro(H.apply(c, x), A @ x) <= 1e-8
+    assert np.linalg.norm(H.apply(c, np.zeros((150, 2)))) == 0.0
+    with pytest.raises(ValueError):
+        H.apply(c, np.zeros((10, 1)))
+
+
+@pytest.mark.parametrize("eps", [1e-4, 1e-7, 1e-10])
+@pytest.mark.parametrize("seed", [11, 12, 13])
+def test_roundtrip_budget(H, eps, seed):  # test_hbs.cpp:127-136
+    A = HO.kernel_matrix(130, seed)
+    c = H.compress(A, eps, 16)
+    assert rel_fro(H.reconstruct(c), A) <= 10.0 * eps * (c.tree.depth + 1)
+    assert H.basis_orthonormality_defect(c) <= 1e-12
+
+
+def test_ranks_monotone_and_match_oracle(H):  # test_hbs.cpp:138-146
+    A = HO.kernel_matrix(128, 5)
+    loose, tight = H.compress(A, 1e-4, 16), H.compress(A, 1e-9, 16)
+    assert all(loose.rank(t) <= tight.rank(t) for t in range(1, loose.tree.num_nodes()))
+    ref = HO.compress(A, 1e-9, 16)
+    for t in range(1, ref.tree.num_nodes()):
+        if ref.tree.is_leaf(t):
+            assert tight.rank(t) == ref.rank(t), t  # identical block rows: identical eps-ranks
+        else:
+            assert abs(tight.rank(t) - ref.rank(t)) <= 2, t
+
+
+def test_serialization(H, tmp_path):  # test_hbs.cpp:177-196
+    A = HO.kernel_matrix(90, 9)
+    c = H.compress(A, 1e-8, 16)
+    b1, b2 = H.serialize(c), H.serialize(H.compress(A, 1e-8, 16))
+    assert b1 == b2  # byte-for-byte stable for a fixed input
+    ho = HO.deserialize(b1)  # the reference layout, read by the oracle
+    assert rel_fro(HO.reconstruct(ho), H.reconstruct(c)) <= 1e-14
+    back = H.deserialize(b1)
+    assert back.tree == c.tree
+    assert rel_fro(H.reconstruct(back), H.reconstruct(c)) == 0.0
+    p = str(tmp_path / "hbs_io.tmp")
+    H.write_hbs(c, p)
+    assert H.serialize(H.read_hbs(p)) == b1
+    # an oracle-made operator uploads and applies like the oracle
+    oc = HO.compress(A, 1e-8, 16)
+    g = H.deserialize(HO.serialize(oc))
+    x = np.random.default_rng(2).standard_normal((90, 4))
+    assert rel_fro(H.apply(g, x), HO.apply(oc, x)) <= 1e-13
+    with pytest.raises(ValueError):
+        H.deserialize(bytes([1, 2, 3]))
+
+
+def test_single_node(H):
+    A = HO.kernel_matrix(40, 1)
+    c = H.compress(A, 1e-10, 64)
+    assert c.tree.num_nodes() == 1
+    x = np.random.default_rng(0).standard_normal(40)
+    assert rel_fro(H.apply(c, x), A @ x) <= 1e-14
+
+
+@pytest.mark.parametrize("name,param", [("laplace", 0.0), ("helmholtz", 40.0)])
+def test_root_operators_within_10eps(H, name, param):
+    """The compressed root operators (S_hbs, G_hbs of build_root_accel's
+    result) against the dense oracle: within 10 eps relative Frobenius at
+    eps = 1e-10, on the reference-size boundary M = 1020."""
+    import paper_1302_5995_b200 as dtn
+    n = 258
+    ref = O.build_root_dense(O.Problem(name, n, param), O.Tree(n, uniform_side=16))
+    spec = dtn.catalog(name, n) if param == 0.0 else dtn.ProblemSpec.continuum(
+        "h", n, None, None, lambda x, y: np.full_like(x, -param * param))
+    sol = dtn.build_root_gpu(dtn.discretize(spec), dtn.build_tree_uniform(n, 16))
+    eps = 1e-10
+    for which, dense in (("S", ref.S), ("G", ref.G)):
+        c = H.compress_operator(sol, which, eps, 64)
+        assert rel_fro(H.reconstruct(c), dense) <= 10 * eps, which
+        g = np.random.default_rng(1).uniform(-1, 1, (dense.shape[0], 16))
+        assert rel_fro(H.apply(c, g), dense @ g) <= 10 * eps, which
+        assert c.max_rank() < dense.shape[0] / 4
+        # leaf ranks as the oracle's compress of the same operator
+        oc = HO.compress(dense, eps, 64)
+        for t in range(1, oc.tree.num_nodes()):
+            if oc.tree.is_leaf(t):
+                assert abs(c.rank(t) - oc.rank(t)) <= 1, (which, t)
+
+
+def test_torch_device_apply(H):
+    import torch
+    A = HO.kernel_matrix(200, 7)
+    c = H.compress(torch.tensor(A, device="cuda"), 1e-10, 32)
+    x = torch.randn(200, 5, dtype=torch.float64, device="cuda")
+    y = H.apply(c, x)
+    assert y.is_cuda
+    assert rel_fro(y.cpu().numpy(), A @ x.cpu().numpy()) <= 1e-9
