@@ -298,3 +298,100 @@ def kernel_matrix(m: int, seed: int) -> np.ndarray:
     h += 5.0 * np.eye(m)
     h += 0.01 * np.random.default_rng(seed).standard_normal((m, m)) / m
     return h
+
+
+# ---------------------------------------------------------------------------
+# Multi-level inversion (hbs_ops.cpp:148-201) and the inverse's apply
+# (hbs_ops.cpp:203-205): the factors {E, F, G} and the root core inverse are
+# stored in an Hbs of the same tree -- E in U, F in V, G in D (leaves) / B
+# (parents), the core inverse in the root B -- so apply() is the inverse's
+# apply. Eigen's FullPivLU inverse is replaced by LAPACK's partial-pivoting
+# inverse (numpy.linalg.inv); the results agree to rounding on the
+# well-conditioned blocks these tests use.
+
+class FactorizationError(RuntimeError):
+    """errors.hpp:11-21: what + " [" + where + "]"."""
+
+    def __init__(self, what, where):
+        super().__init__(f"{what} [{where}]")
+        self.where = where
+
+
+def _checked_inverse(A, what, where):  # hbs_ops.cpp:27-37
+    if A.size == 0:
+        return A.copy()
+    try:
+        inv = np.linalg.inv(A)
+    except np.linalg.LinAlgError:
+        raise FactorizationError(f"{what} is singular", where) from None
+    if not np.all(np.isfinite(inv)):
+        raise FactorizationError(f"{what} is singular", where)
+    return inv
+
+
+def invert_hbs(h: Hbs) -> Hbs:
+    tree = h.tree
+    rep = Hbs(tree)
+    if tree.num_nodes() == 1:
+        rep.D[0] = _checked_inverse(h.D[0], "D", "root leaf")
+        return rep
+    dhat = [None] * tree.num_nodes()
+    for t in tree.bottom_up():
+        where = f"node {t} level {tree.nodes[t].level}"
+        if tree.is_leaf(t):
+            dtilde = h.D[t].copy()
+        else:
+            c1, c2 = tree.nodes[t].left, tree.nodes[t].right
+            k1, k2 = h.rank(c1), h.rank(c2)
+            dtilde = h.B[t].copy()
+            dtilde[:k1, :k1] += dhat[c1]
+            dtilde[k1:, k1:] += dhat[c2]
+        if t == 0:
+            rep.B[0] = _checked_inverse(dtilde, "root coupling block", where)
+            break
+        dinv = _checked_inverse(dtilde, "Dtilde", where)
+        w = dinv @ h.U[t]
+        dhat[t] = _checked_inverse(h.V[t].T @ w, "reduced block (V^T Dtilde^{-1} U)", where)
+        e = w @ dhat[t]
+        rep.U[t] = e
+        rep.V[t] = dinv.T @ h.V[t] @ dhat[t].T
+        g = dinv - e @ (h.V[t].T @ dinv)
+        if tree.is_leaf(t):
+            rep.D[t] = g
+        else:
+            rep.B[t] = g
+    return rep
+
+
+def apply_inverse(inv: Hbs, x: np.ndarray) -> np.ndarray:
+    return apply(inv, x)
+
+
+def synthetic_hbs(m_total: int, leaf: int, k: int, seed: int) -> Hbs:
+    """test_hbs_ops.cpp:70-105: a well-conditioned HBS matrix with exact rank
+    k everywhere (leaf D = N(0,1) + 20 k I, orthonormal U/V, zero-diagonal B).
+    Gaussian draws from numpy (std::normal_distribution is
+    implementation-defined): same structure and tolerances, other values."""
+    rng = np.random.default_rng(seed)
+    tree = build_index_tree(m_total, leaf)
+    h = Hbs(tree)
+
+    def orth(r, c):
+        q, _ = np.linalg.qr(rng.standard_normal((r, c)))
+        return q[:, :c]
+
+    for t in tree.bottom_up():
+        if tree.is_leaf(t):
+            sz = tree.node_size(t)
+            h.D[t] = rng.standard_normal((sz, sz)) + 20.0 * k * np.eye(sz)
+            if t != 0:
+                h.U[t], h.V[t] = orth(sz, min(k, sz)), orth(sz, min(k, sz))
+            continue
+        k1, k2 = h.U[tree.nodes[t].left].shape[1], h.U[tree.nodes[t].right].shape[1]
+        b = np.zeros((k1 + k2, k1 + k2))
+        b[:k1, k1:] = rng.standard_normal((k1, k2))
+        b[k1:, :k1] = rng.standard_normal((k2, k1))
+        h.B[t] = b
+        if t != 0:
+            h.U[t], h.V[t] = orth(k1 + k2, min(k, k1 + k2)), orth(k1 + k2, min(k, k1 + k2))
+    return h

@@ -110,3 +110,47 @@ def test_exported_hbs_symbols():
                  "dtn_gpu_hbs_deserialize", "dtn_gpu_hbs_info", "dtn_gpu_hbs_tree", "dtn_gpu_hbs_factor",
                  "dtn_gpu_hbs_free"):
         assert hasattr(lib, name), name
+
+
+# ---- multi-level inversion (hbs_ops.cpp:148-205), pinned to test_hbs_ops.cpp:164-216 ----
+
+def test_invert_diagonal_divides_elementwise():  # test_hbs_ops.cpp:164-172
+    d = 1.0 + (np.arange(64) % 7)
+    inv = HO.invert_hbs(HO.compress(np.diag(d), 1e-12, 16))
+    x = np.linspace(-1.0, 2.0, 64)
+    assert np.linalg.norm(HO.apply_inverse(inv, x) - x / d) <= 1e-12
+
+
+def test_invert_two_level_synthetic():  # test_hbs_ops.cpp:174-180
+    h = HO.synthetic_hbs(16, 4, 2, 6)
+    dense = HO.reconstruct(h)
+    g = HO.apply_inverse(HO.invert_hbs(h), np.eye(16))
+    assert rel_fro(g, np.linalg.inv(dense)) <= 1e-9
+
+
+def test_invert_compressed_laplace_schur():  # test_hbs_ops.cpp:182-190
+    S = O.build_root_dense(O.Problem("laplace", 64), O.Tree(64, 4096)).S
+    h = HO.compress(S, 1e-7, 64)
+    x = np.random.default_rng(7).standard_normal((S.shape[0], 2))
+    back = HO.apply(h, HO.apply_inverse(HO.invert_hbs(h), x))
+    assert np.linalg.norm(back - x) / np.linalg.norm(x) <= 1e-5
+
+
+@pytest.mark.parametrize("n", [32, 64])
+def test_invert_residual_within_100_eps(n):  # test_hbs_ops.cpp:192-203
+    eps = 1e-7
+    S = O.build_root_dense(O.Problem("laplace", n), O.Tree(n, 4096)).S
+    h = HO.compress(S, eps, 32)
+    x = np.random.default_rng(8).standard_normal((S.shape[0], 1))
+    back = HO.apply(h, HO.apply_inverse(HO.invert_hbs(h), x))
+    assert np.linalg.norm(back - x) / np.linalg.norm(x) <= 100 * eps
+
+
+def test_invert_names_failing_node():  # test_hbs_ops.cpp:205-216
+    h = HO.synthetic_hbs(16, 4, 2, 9)
+    for t in range(h.tree.num_nodes()):
+        if h.tree.is_leaf(t):
+            h.D[t][:] = 0.0
+            break
+    with pytest.raises(HO.FactorizationError, match="node"):
+        HO.invert_hbs(h)
