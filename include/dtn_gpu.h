@@ -57,8 +57,8 @@ typedef struct {
   int32_t want_G;      /* compute G = S^{-1} and cond_estimate (dense_nd.cpp:218-224) */
   int32_t micro_max;   /* leaf elimination granularity (unknowns per one-CTA box); 0 = default */
   int32_t profile;     /* 1: no graph, CUDA events around every launch (dtn_gpu_kernel_stats) */
-  double epsilon;      /* compressed engine tolerance (AccelOptions::epsilon) — reserved */
-  int64_t crossover;   /* AccelOptions::crossover — reserved */
+  double epsilon;      /* compressed engine tolerance (AccelOptions::epsilon, dtn_gpu_build_accel) */
+  int64_t crossover;   /* AccelOptions::crossover: root boundaries >= crossover are compressed */
   int32_t nshards;     /* subtree sharding: 1, 2 (W|E), 4 (quadrants), 8 (quadrant halves) */
   int32_t shard;       /* >= 0: build only this shard's S; -1: full build (nshards == 1) or the top of
                           the tree from prob.shard_S (nshards > 1) */
@@ -187,6 +187,20 @@ int dtn_gpu_hbs_apply(const dtn_hbs* h, const double* X, int64_t ldx, int64_t nr
 /* buf NULL: *size receives the byte count only */
 int dtn_gpu_hbs_serialize(const dtn_hbs* h, uint8_t* buf, uint64_t cap, uint64_t* size);
 int dtn_gpu_hbs_deserialize(dtn_ctx* ctx, const uint8_t* buf, uint64_t size, dtn_hbs** out);
+/* invert_hbs (hbs_ops.hpp:64, hbs_ops.cpp:148-201): the telescoping inverse factors of H in
+ * the InverseFactors layout (hbs_ops.hpp:46-55: E in U, F in V, G in D/B, the root core inverse
+ * in the root B), so dtn_gpu_hbs_apply on the result is apply_inverse (hbs_ops.cpp:203-205).
+ * A singular block returns 3 with "<block> is singular [node t level l]". */
+int dtn_gpu_hbs_invert(const dtn_hbs* H, dtn_hbs** out);
+/* Compressed engine, build_root_accel (accel_nd.hpp:93-95, accel_nd.cpp:707-859) on the B200:
+ * the root Schur complement S from the exact dense GPU merges, S_hbs = compress(S,
+ * opts->epsilon, hbs_leaf) and G_hbs = invert_hbs(S_hbs) (accel_nd.cpp:820-822), cond = the
+ * reference's probe estimate (accel_nd.cpp:834-841). The HBS factors are in canonical ring
+ * order (rep_to_canonical = identity). A root boundary below opts->crossover stays dense
+ * (accel_nd.cpp:796-818): *S_hbs = *G_hbs = NULL, the dense op (with G) in *op_out.
+ * op_out (optional): the dense build (S resident; boundary ids, box S); NULL frees it. */
+int dtn_gpu_build_accel(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, int64_t hbs_leaf,
+                        dtn_op** op_out, dtn_hbs** S_hbs, dtn_hbs** G_hbs, double* cond);
 
 #ifdef __cplusplus
 }

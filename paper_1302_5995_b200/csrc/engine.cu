@@ -847,6 +847,9 @@ int guarded(dtn_ctx* ctx, F&& f) {
   } catch (const Singular& e) {
     err = e.what();
     return DTN_ESINGULAR;
+  } catch (const HbsSingular& e) {
+    err = e.what();
+    return DTN_ESINGULAR;
   } catch (const std::invalid_argument& e) {
     err = e.what();
     return DTN_EINVAL;
@@ -1652,6 +1655,93 @@ int dtn_gpu_hbs_deserialize(dtn_ctx* ctx, const uint8_t* buf, uint64_t size, dtn
     r->h = std::move(hd);
     *out = r;
   });
+}
+
+int dtn_gpu_hbs_invert(const dtn_hbs* h, dtn_hbs** out) {
+  if (!h || !h->h || !out) return DTN_EINVAL;
+  dtn_ctx* ctx = h->ctx;
+  return guarded(ctx, [&] {
+    *out = nullptr;
+    CK(cudaSetDevice(ctx->device));
+    auto inv = hbs_invert(*h->h, ctx->stream);
+    auto* r = new dtn_hbs;
+    r->ctx = ctx;
+    r->h = std::move(inv);
+    *out = r;
+  });
+}
+
+int dtn_gpu_build_accel(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, int64_t hbs_leaf, dtn_op** op_out,
+                        dtn_hbs** S_hbs, dtn_hbs** G_hbs, double* cond) {
+  if (!ctx || !prob || !opts || !S_hbs || !G_hbs) return DTN_EINVAL;
+  *S_hbs = nullptr;
+  *G_hbs = nullptr;
+  if (op_out) *op_out = nullptr;
+  if (!(opts->epsilon > 0.0) || hbs_leaf < 2) {
+    ctx->err = "build_root_accel: epsilon must be > 0 and hbs_leaf >= 2";
+    return DTN_EINVAL;
+  }
+  if (opts->nloads > 0) {
+    ctx->err = "build_root_accel: body loads are built by the dense engine (dtn_gpu_build)";
+    return DTN_EINVAL;
+  }
+  // the root operator: S by the exact dense merges; G only when the root stays dense
+  const int64_t nb_root = 4 * int64_t(prob->n - 2) - 4;
+  const bool dense_root = nb_root < opts->crossover;
+  dtn_opts o = *opts;
+  o.engine = 0;
+  o.want_G = dense_root ? 1 : 0;
+  o.export_S = nullptr;
+  dtn_op* op = nullptr;
+  int rc = dtn_gpu_build(ctx, prob, &o, &op);
+  if (rc != DTN_OK) return rc;
+  if (dense_root) {  // accel_nd.cpp:796-818: below the crossover the accel engine holds dense factors
+    if (cond) *cond = op->cond;
+    if (op_out) *op_out = op;
+    else dtn_gpu_free(op);
+    return DTN_OK;
+  }
+  dtn_hbs* Sh = nullptr;
+  dtn_hbs* Gh = nullptr;
+  rc = dtn_gpu_hbs_compress_op(op, 1, opts->epsilon, hbs_leaf, &Sh);
+  if (rc == DTN_OK) rc = dtn_gpu_hbs_invert(Sh, &Gh);  // accel_nd.cpp:820-822
+  if (rc == DTN_OK && cond) {
+    // accel_nd.cpp:834-841: (|S 1|_1 / m) (|G 1|_1 / m) m
+    rc = guarded(ctx, [&] {
+      const int64_t m = op->nb;
+      std::vector<double> ones(size_t(m), 1.0);
+      std::vector<double> y(static_cast<size_t>(m), 0.0);
+      double* d = nullptr;
+      CK(cudaMalloc(&d, size_t(m) * 16));
+      struct F {
+        double* p;
+        ~F() { cudaFree(p); }
+      } f{d};
+      cudaStream_t st = ctx->stream;
+      CK(cudaMemcpyAsync(d, ones.data(), size_t(m) * 8, cudaMemcpyHostToDevice, st));
+      double nrm[2];
+      for (int w = 0; w < 2; ++w) {
+        hbs_apply(*(w == 0 ? Sh : Gh)->h, d, m, 1, d + m, m, st);
+        CK(cudaMemcpyAsync(y.data(), d + m, size_t(m) * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        double a = 0.0;
+        for (double v : y) a += std::fabs(v);
+        nrm[w] = a / double(m);
+      }
+      *cond = nrm[0] * nrm[1] * double(m);
+    });
+  }
+  if (rc != DTN_OK) {
+    dtn_gpu_hbs_free(Gh);
+    dtn_gpu_hbs_free(Sh);
+    dtn_gpu_free(op);
+    return rc;
+  }
+  *S_hbs = Sh;
+  *G_hbs = Gh;
+  if (op_out) *op_out = op;
+  else dtn_gpu_free(op);
+  return DTN_OK;
 }
 
 }  // extern "C"

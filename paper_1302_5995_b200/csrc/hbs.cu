@@ -552,7 +552,7 @@ void pack_for_apply(HbsDev& H, cudaStream_t st) {
     const bool leaf = H.is_leaf(t);
     const int64_t inner = leaf ? H.node_size(t) : P.kp[H.nodes[t].left] + P.kp[H.nodes[t].right];
     if (leaf) tot += need(inner, inner);
-    if (t != 0) tot += need(P.kp[t], inner) + need(inner, P.kp[t]);
+    if (t != 0) tot += size_t(std::max<int64_t>(align2(P.kp[t]), 2)) * size_t(inner) + need(inner, P.kp[t]);  // VT: ld >= 2
     if (!leaf) tot += need(inner, inner);
   }
   HCK(cudaMalloc(&P.buf, tot * 8 + 64));
@@ -852,6 +852,243 @@ std::unique_ptr<HbsDev> hbs_deserialize(const uint8_t* data, size_t size, cudaSt
     }
   }
   (void)st;
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+// invert_hbs (hbs_ops.cpp:148-201), one tree height at a time, every node of
+// that height in the same batched launches. Per non-root node t (s = rows[t],
+// k = rank[t]):
+//   Dtilde = D_t (leaf) or B_t + diag(Dhat_left, Dhat_right)   add_blocks
+//   Dinv   = Dtilde^{-1}                                        gj_inverse
+//   W = Dinv U,  VT = V^T,  Dhat = (VT W)^{-1}                  GEMM, transpose, gj_inverse
+//   E = W Dhat,  Z = VT Dinv,  F = (Dhat Z)^T                   GEMM, transpose
+//   G = Dinv - E Z                                              copy + GEMM (C -= A B)
+// (F = Dinv^T V Dhat^T and G = Dinv - E V^T Dinv exactly as the reference
+// writes them); the root's core inverse is (B_0 + diag(Dhat_l, Dhat_r))^{-1}.
+// Eigen's FullPivLU inverses become partial-pivoting Gauss-Jordan inverses
+// (same result to rounding on invertible blocks); a zero or non-finite pivot
+// raises HbsSingular with the reference's "what [node t level l]" text.
+std::unique_ptr<HbsDev> hbs_invert(const HbsDev& H, cudaStream_t st) {
+  auto out = std::make_unique<HbsDev>();
+  HbsDev& R = *out;
+  R.device = H.device;
+  R.M = H.M;
+  R.depth = H.depth;
+  R.nodes = H.nodes;
+  R.rank = H.rank;
+  R.rows = H.rows;
+  R.height = H.height;
+  const int nn = int(H.nodes.size());
+  R.D.assign(nn, nullptr);
+  R.U.assign(nn, nullptr);
+  R.V.assign(nn, nullptr);
+  R.B.assign(nn, nullptr);
+  DevBuf dbuf, ibuf;
+  struct Frees {
+    std::vector<void*> v;
+    ~Frees() {
+      for (void* p : v) cudaFree(p);
+    }
+  } frees;
+  auto dalloc = [&](size_t doubles, bool keep) {
+    double* p = nullptr;
+    HCK(cudaMalloc(&p, doubles * 8 + 64));
+    (keep ? R.buffers : frees.v).push_back(p);
+    return p;
+  };
+  int* dinfo = nullptr;
+  HCK(cudaMalloc(&dinfo, size_t(nn) * sizeof(int) + 16));
+  frees.v.push_back(dinfo);
+  auto where = [&](int t) {
+    return "node " + std::to_string(t) + " level " + std::to_string(H.nodes[t].level);
+  };
+  // batched in-place inverses; throws on the singular block with the lowest node id
+  auto invert = [&](const std::vector<std::pair<int, InvDesc>>& blocks, const char* what) {
+    if (blocks.empty()) return;
+    std::vector<InvDesc> v;
+    int smax = 0;
+    for (size_t i = 0; i < blocks.size(); ++i) {
+      InvDesc d = blocks[i].second;
+      d.info = dinfo + i;
+      v.push_back(d);
+      smax = std::max(smax, d.s);
+    }
+    InvDesc* dv = upload(ibuf, v, st);
+    HCK(launch_gj_inverse(dv, int(v.size()), smax, st));
+    std::vector<int> info(v.size());
+    HCK(cudaMemcpyAsync(info.data(), dinfo, info.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
+    HCK(cudaStreamSynchronize(st));
+    int bad = -1;
+    for (size_t i = 0; i < info.size(); ++i)
+      if (info[i] != 0 && (bad < 0 || blocks[i].first < bad)) bad = blocks[i].first;
+    if (bad >= 0) throw HbsSingular(std::string(what) + " is singular [" + where(bad) + "]");
+  };
+
+  if (nn == 1) {  // hbs_ops.cpp:157-160
+    const int s = int(H.M), ld = H.ld(0);
+    R.D[0] = dalloc(size_t(ld) * s, true);
+    copy_batch(dbuf, {CopyDesc{H.D[0], R.D[0], ld, ld, s, s}}, st);
+    try {
+      invert({{0, InvDesc{R.D[0], nullptr, s, ld}}}, "D");
+    } catch (const HbsSingular&) {
+      throw HbsSingular("D is singular [root leaf]");
+    }
+    return out;
+  }
+
+  // Dhat_t (k x k, ld align2(k)) of every non-root node, kept until its parent is done
+  std::vector<double*> dhat(nn, nullptr);
+  {
+    size_t tot = 0;
+    for (int t = 1; t < nn; ++t) tot += size_t(align2(H.rank[t])) * H.rank[t];
+    double* base = dalloc(tot, false);
+    size_t o = 0;
+    for (int t = 1; t < nn; ++t) {
+      dhat[t] = base + o;
+      o += size_t(align2(H.rank[t])) * H.rank[t];
+    }
+  }
+  const int RH = H.height[0];
+  for (int r = 0; r <= RH; ++r) {
+    std::vector<int> act;
+    for (int t = 0; t < nn; ++t)
+      if (H.height[t] == r) act.push_back(t);
+    if (act.empty()) continue;
+    // storage: result factors (kept) and per-level work
+    size_t keep = 0, work = 0;
+    for (int t : act) {
+      const size_t s = size_t(H.rows[t]), k = size_t(H.rank[t]), ls = size_t(align2(s));
+      const size_t lk = size_t(std::max<int64_t>(align2(k), 2));
+      keep += ls * s + (t ? 2 * ls * k : 0);
+      work += ls * s + (t ? ls * k + 3 * lk * s : 0);
+    }
+    double* kb = dalloc(keep, true);
+    double* wb = dalloc(work, false);
+    struct Slot {
+      double *Dt = nullptr, *W = nullptr, *VT = nullptr, *Z = nullptr, *FT = nullptr;
+    };
+    std::vector<Slot> sl(nn);
+    size_t ko = 0, wo = 0;
+    for (int t : act) {
+      const size_t s = size_t(H.rows[t]), k = size_t(H.rank[t]), ls = size_t(align2(s));
+      const size_t lk = size_t(std::max<int64_t>(align2(k), 2));
+      (H.is_leaf(t) ? R.D[t] : R.B[t]) = kb + ko;
+      ko += ls * s;
+      Slot& q = sl[t];
+      q.Dt = wb + wo;
+      wo += ls * s;
+      if (t) {
+        R.U[t] = kb + ko;
+        ko += ls * k;
+        R.V[t] = kb + ko;
+        ko += ls * k;
+        q.W = wb + wo;
+        wo += ls * k;
+        q.VT = wb + wo;
+        wo += lk * s;
+        q.Z = wb + wo;
+        wo += lk * s;
+        q.FT = wb + wo;
+        wo += lk * s;
+      }
+    }
+    // 1. Dtilde
+    {
+      std::vector<CopyDesc> c;
+      std::vector<AddDesc> a;
+      for (int t : act) {
+        const int s = H.rows[t], ld = H.ld(t);
+        if (s == 0) continue;
+        c.push_back(CopyDesc{H.is_leaf(t) ? H.D[t] : H.B[t], sl[t].Dt, ld, ld, s, s});
+        if (!H.is_leaf(t)) {
+          const int l = H.nodes[t].left, rr = H.nodes[t].right, k1 = H.rank[l], k2 = H.rank[rr];
+          if (k1) a.push_back(AddDesc{dhat[l], sl[t].Dt, int(align2(k1)), ld, k1, k1});
+          if (k2) a.push_back(AddDesc{dhat[rr], sl[t].Dt + k1 + size_t(k1) * ld, int(align2(k2)), ld, k2, k2});
+        }
+      }
+      copy_batch(dbuf, c, st);
+      if (!a.empty()) {
+        AddDesc* da = upload(dbuf, a, st);
+        HCK(launch_add_blocks(da, int(a.size()), st));
+        HCK(cudaStreamSynchronize(st));
+      }
+    }
+    // 2. Dinv (at the root: the core inverse, hbs_ops.cpp:177-180)
+    {
+      std::vector<std::pair<int, InvDesc>> b;
+      for (int t : act)
+        if (H.rows[t] > 0) b.push_back({t, InvDesc{sl[t].Dt, nullptr, H.rows[t], H.ld(t)}});
+      invert(b, r == RH ? "root coupling block" : "Dtilde");
+    }
+    if (r == RH) {  // act = {0}
+      const int s = H.rows[0], ld = H.ld(0);
+      if (s > 0) copy_batch(dbuf, {CopyDesc{sl[0].Dt, R.B[0], ld, ld, s, s}}, st);
+      break;
+    }
+    // 3. W = Dinv U, VT = V^T
+    {
+      std::vector<GemmDesc> g;
+      std::vector<TransDesc> tr;
+      for (int t : act) {
+        const int s = H.rows[t], k = H.rank[t], ld = H.ld(t), lk = std::max(int(align2(k)), 2);
+        if (s == 0 || k == 0) continue;
+        g.push_back(GemmDesc{sl[t].Dt, H.U[t], sl[t].W, s, k, s, ld, ld, ld});
+        tr.push_back(TransDesc{H.V[t], sl[t].VT, ld, lk, s, k});
+      }
+      gemm_batch(dbuf, g, 1.0, 0.0, true, st);
+      transpose_batch(dbuf, tr, st);
+    }
+    // 4. T = VT W -> Dhat = T^{-1}
+    {
+      std::vector<GemmDesc> g;
+      for (int t : act) {
+        const int s = H.rows[t], k = H.rank[t], ld = H.ld(t), lk = std::max(int(align2(k)), 2);
+        if (s == 0 || k == 0) continue;
+        g.push_back(GemmDesc{sl[t].VT, sl[t].W, dhat[t], k, k, s, lk, ld, int(align2(k))});
+      }
+      gemm_batch(dbuf, g, 1.0, 0.0, true, st);
+      std::vector<std::pair<int, InvDesc>> b;
+      for (int t : act)
+        if (H.rank[t] > 0) b.push_back({t, InvDesc{dhat[t], nullptr, H.rank[t], int(align2(H.rank[t]))}});
+      invert(b, "reduced block (V^T Dtilde^{-1} U)");
+    }
+    // 5. E = W Dhat (U slot); Z = VT Dinv
+    {
+      std::vector<GemmDesc> g;
+      for (int t : act) {
+        const int s = H.rows[t], k = H.rank[t], ld = H.ld(t), lk = std::max(int(align2(k)), 2);
+        if (s == 0 || k == 0) continue;
+        g.push_back(GemmDesc{sl[t].W, dhat[t], R.U[t], s, k, k, ld, int(align2(k)), ld});
+        g.push_back(GemmDesc{sl[t].VT, sl[t].Dt, sl[t].Z, k, s, s, lk, ld, lk});
+      }
+      gemm_batch(dbuf, g, 1.0, 0.0, true, st);
+    }
+    // 6. FT = Dhat Z, F = FT^T (V slot); G = Dinv - E Z (D / B slot)
+    {
+      std::vector<GemmDesc> g;
+      std::vector<CopyDesc> c;
+      for (int t : act) {
+        const int s = H.rows[t], k = H.rank[t], ld = H.ld(t), lk = std::max(int(align2(k)), 2);
+        if (s == 0) continue;
+        c.push_back(CopyDesc{sl[t].Dt, H.is_leaf(t) ? R.D[t] : R.B[t], ld, ld, s, s});
+        if (k == 0) continue;
+        g.push_back(GemmDesc{dhat[t], sl[t].Z, sl[t].FT, k, s, k, int(align2(k)), lk, lk});
+      }
+      gemm_batch(dbuf, g, 1.0, 0.0, true, st);
+      copy_batch(dbuf, c, st);
+      std::vector<TransDesc> tr;
+      std::vector<GemmDesc> gu;
+      for (int t : act) {
+        const int s = H.rows[t], k = H.rank[t], ld = H.ld(t), lk = std::max(int(align2(k)), 2);
+        if (s == 0 || k == 0) continue;
+        tr.push_back(TransDesc{sl[t].FT, R.V[t], lk, ld, k, s});
+        gu.push_back(GemmDesc{R.U[t], sl[t].Z, H.is_leaf(t) ? R.D[t] : R.B[t], s, s, k, ld, lk, ld});
+      }
+      transpose_batch(dbuf, tr, st);
+      gemm_batch(dbuf, gu, -1.0, 1.0, true, st);
+    }
+  }
   return out;
 }
 

@@ -8,6 +8,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -53,12 +54,26 @@ struct ZeroDesc {
   int ld, m, n;
 };
 
+struct AddDesc {  // dst(m x n) += src(m x n)
+  const double* src;
+  double* dst;
+  int lds, ldd, m, n;
+};
+
+struct InvDesc {  // A (s x s, leading dimension lda) <- A^{-1}; *info = 0, or k + 1 (singular at step k)
+  double* A;
+  int* info;
+  int s, lda;
+};
+
 cudaError_t launch_transpose_batched(const TransDesc* d_descs, int count, int max_tiles, cudaStream_t st);
 cudaError_t launch_jacobi_eig(const EigDesc* d_descs, int count, int max_sweeps, bool rel, cudaStream_t st);
 cudaError_t launch_hbs_select(const SelDesc* d_descs, int count, double eps, cudaStream_t st);
 cudaError_t launch_gather_cols(const GatherDesc* d_descs, int count, cudaStream_t st);
 cudaError_t launch_pack(const PackDesc* d_descs, int count, cudaStream_t st);
 cudaError_t launch_zero_blocks(const ZeroDesc* d_descs, int count, cudaStream_t st);
+cudaError_t launch_add_blocks(const AddDesc* d_descs, int count, cudaStream_t st);
+cudaError_t launch_gj_inverse(const InvDesc* d_descs, int count, int max_s, cudaStream_t st);
 
 // IndexTree node (index_tree.hpp:12-22): contiguous range [begin, end),
 // preorder ids, children -1 for leaves.
@@ -114,6 +129,18 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
 // Y (M x nrhs) = H X through the telescoping factorization (hbs.cpp:187-232);
 // X, Y device pointers.
 void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* dY, int64_t ldy, cudaStream_t st);
+
+// A singular block met by hbs_invert: what() = "<what> [node t level l]"
+// (FactorizationError, errors.hpp:11-21); the C ABI maps it to DTN_ESINGULAR.
+struct HbsSingular : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// invert_hbs (hbs_ops.cpp:148-201): the telescoping inverse factors of H on
+// the same tree -- E in U, F in V, G in D (leaves) / B (parents), the root
+// core inverse (B_root + diag(Dhat))^{-1} in the root B -- so hbs_apply on
+// the result is apply_inverse (hbs_ops.cpp:203-205).
+std::unique_ptr<HbsDev> hbs_invert(const HbsDev& H, cudaStream_t st);
 
 // DTNHBS01 serialization (hbs.cpp:422-519), byte-for-byte the reference layout.
 std::vector<uint8_t> hbs_serialize(const HbsDev& H, cudaStream_t st);

@@ -3,6 +3,7 @@
 // a batched cyclic Jacobi eigensolver for the per-node Gram matrices, the
 // rank selection, column gathers and the zero-padded repacking of factors.
 // The contractions themselves run on the DMMA GEMM (k_gemm.cu).
+#include <algorithm>
 #include <cfloat>
 #include <cstdint>
 
@@ -276,6 +277,155 @@ __global__ void zero_blocks_kernel(const ZeroDesc* __restrict__ descs) {
 cudaError_t launch_zero_blocks(const ZeroDesc* d_descs, int count, cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
   zero_blocks_kernel<<<dim3(32, count), 256, 0, st>>>(d_descs);
+  return cudaGetLastError();
+}
+
+// ---- dst(m x n) += src(m x n), batched (Dtilde = B + diag(Dhat_l, Dhat_r), hbs_ops.cpp:172-176)
+__global__ void add_blocks_kernel(const AddDesc* __restrict__ descs) {
+  const AddDesc d = descs[blockIdx.y];
+  const long long total = (long long)d.m * d.n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int r = int(e % d.m), c = int(e / d.m);
+    d.dst[r + (long long)c * d.ldd] += d.src[r + (long long)c * d.lds];
+  }
+}
+
+cudaError_t launch_add_blocks(const AddDesc* d_descs, int count, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  add_blocks_kernel<<<dim3(32, count), 256, 0, st>>>(d_descs);
+  return cudaGetLastError();
+}
+
+// ---- in-place inverse of small dense blocks (the checked inverses of
+// invert_hbs, hbs_ops.cpp:148-201): Gauss-Jordan with partial (row) pivoting,
+// one CTA per matrix, the matrix in shared memory (odd leading dimension)
+// when it fits, else in place in global memory (L2-resident at these sizes).
+// Step k: argmax |a_ik| over i >= k (lowest index on ties), swap rows k and p,
+// then one fused rank-1 sweep a_ij -= a_ik a_kj / a_kk over the whole matrix
+// with the pivot row/column replaced in place; the recorded row interchanges
+// become column interchanges of the inverse at the end. A zero or non-finite
+// pivot marks the block singular (*info = k + 1) and stops.
+constexpr int GJT = 512;
+constexpr int GJ_SMEM_MAX = 160;  // s <= 160: 160 * 161 doubles = 206 KB
+
+__global__ void __launch_bounds__(GJT) gj_inverse_kernel(const InvDesc* __restrict__ descs) {
+  extern __shared__ __align__(16) double gsm[];
+  __shared__ double rv[GJT / 32];
+  __shared__ int ri[GJT / 32];
+  __shared__ int piv_row;
+  __shared__ int bad;
+  const InvDesc d = descs[blockIdx.x];
+  const int s = d.s;
+  if (s <= 0) {
+    if (threadIdx.x == 0) *d.info = 0;
+    return;
+  }
+  const bool in_smem = s <= GJ_SMEM_MAX;
+  const int lda = in_smem ? (s | 1) : d.lda;
+  double* A = in_smem ? gsm : d.A;
+  double* rowk = in_smem ? gsm + (long long)lda * s : gsm;  // s doubles
+  double* colk = rowk + s;                                  // s doubles
+  int* perm = reinterpret_cast<int*>(colk + s);             // s ints
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (in_smem)
+    for (int e = tid; e < s * s; e += GJT) A[(e % s) + (e / s) * lda] = d.A[(e % s) + (long long)(e / s) * d.lda];
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  for (int k = 0; k < s; ++k) {
+    // 1. pivot: argmax |a_ik|, i >= k
+    double bv = -1.0;
+    int bi = s;
+    for (int i = k + tid; i < s; i += GJT) {
+      const double v = fabs(A[i + (long long)k * lda]);
+      if (v > bv || (v == bv && i < bi) || v != v) {
+        bv = v != v ? INFINITY : v;
+        bi = i;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      rv[warp] = bv;
+      ri[warp] = bi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double b = rv[0];
+      int i0 = ri[0];
+      for (int w = 1; w < GJT / 32; ++w)
+        if (rv[w] > b || (rv[w] == b && ri[w] < i0)) {
+          b = rv[w];
+          i0 = ri[w];
+        }
+      const double pv = i0 < s ? A[i0 + (long long)k * lda] : 0.0;
+      if (i0 >= s || pv == 0.0 || !isfinite(pv)) bad = k + 1;
+      piv_row = i0;
+      perm[k] = i0;
+    }
+    __syncthreads();
+    if (bad) break;
+    // 2. swap rows k and p
+    const int p = piv_row;
+    if (p != k)
+      for (int j = tid; j < s; j += GJT) {
+        const double t = A[k + (long long)j * lda];
+        A[k + (long long)j * lda] = A[p + (long long)j * lda];
+        A[p + (long long)j * lda] = t;
+      }
+    __syncthreads();
+    // 3. scaled pivot row and the pivot column
+    const double rp = 1.0 / A[k + (long long)k * lda];
+    for (int j = tid; j < s; j += GJT) {
+      rowk[j] = (j == k ? 1.0 : A[k + (long long)j * lda]) * rp;
+      colk[j] = A[j + (long long)k * lda];
+    }
+    __syncthreads();
+    // 4. rank-1 sweep (column-major, consecutive threads on consecutive rows)
+    for (int e = tid; e < s * s; e += GJT) {
+      const int i = e % s, j = e / s;
+      double* a = A + i + (long long)j * lda;
+      if (i == k) *a = rowk[j];
+      else *a = (j == k ? 0.0 : *a) - colk[i] * rowk[j];
+    }
+    __syncthreads();
+  }
+  if (bad) {
+    if (tid == 0) *d.info = bad;
+    return;
+  }
+  // 5. undo the interchanges on the columns, last first
+  for (int k = s - 1; k >= 0; --k) {
+    const int p = perm[k];
+    if (p != k)
+      for (int i = tid; i < s; i += GJT) {
+        const double t = A[i + (long long)k * lda];
+        A[i + (long long)k * lda] = A[i + (long long)p * lda];
+        A[i + (long long)p * lda] = t;
+      }
+    __syncthreads();
+  }
+  if (in_smem)
+    for (int e = tid; e < s * s; e += GJT) d.A[(e % s) + (long long)(e / s) * d.lda] = A[(e % s) + (e / s) * lda];
+  if (tid == 0) *d.info = 0;
+}
+
+cudaError_t launch_gj_inverse(const InvDesc* d_descs, int count, int max_s, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  const int sm = std::min(max_s, GJ_SMEM_MAX);
+  // shared: the matrix (when it fits) + pivot row/column + permutation
+  const size_t bytes = size_t((sm | 1)) * sm * 8 + size_t(max_s) * 20 + 64;
+  if (bytes > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(gj_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    if (e != cudaSuccess) return e;
+  }
+  gj_inverse_kernel<<<count, GJT, bytes, st>>>(d_descs);
   return cudaGetLastError();
 }
 

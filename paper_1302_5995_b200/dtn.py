@@ -254,7 +254,8 @@ def build_tree_uniform(n: int, leaf_side: int) -> BoxTree:
 
 @dataclass
 class AccelOptions:
-    """accel_nd.hpp:14-22 (the compressed engine is not available yet)."""
+    """accel_nd.hpp:14-22 (build_root_accel: epsilon, crossover, hbs_leaf are used;
+    rank_warn_cap and threads have no B200 meaning)."""
     epsilon: float = 1e-7
     crossover: int = 1024
     hbs_leaf: int = 64
@@ -535,11 +536,79 @@ def solve_with_load(sol: "SolutionOperator", g, fhat):
     return v + F @ fhat
 
 
+class CompressedSolutionOperator:
+    """SolutionOperator (solution_operator.hpp:30-53) of the compressed engine:
+    S_hbs (HbsMatrix) and G_hbs (InverseFactors) resident in HBM, in canonical
+    ring order (rep_to_canonical = identity), cond_estimate from the
+    reference's probe formula (accel_nd.cpp:834-841)."""
+
+    def __init__(self, n, boundary, S_hbs, G_hbs, cond, dense_op=None, level_stats=None):
+        self.engine = Engine.accel
+        self.n = n
+        self.boundary = boundary
+        self.S_hbs, self.G_hbs = S_hbs, G_hbs
+        self.rep_to_canonical = np.arange(len(boundary), dtype=np.int64)
+        self.cond_estimate = cond
+        self.dense_op = dense_op
+        self.level_stats = list(level_stats or [])
+        self.level_stats.append(LevelStats(-1, S_hbs.max_rank(), S_hbs.payload_bytes() + G_hbs.payload_bytes(), 0.0))
+        self.body_map = None
+
+    def boundary_size(self) -> int:
+        return len(self.boundary)
+
+    def memory_bytes(self) -> int:
+        """solution_operator.cpp:5-18: serialized S_hbs and G_hbs.rep."""
+        from . import hbs as _hbs
+        return len(_hbs.serialize(self.S_hbs)) + len(_hbs.serialize(self.G_hbs))
+
+
+def build_root_accel(op: DiscreteOperator, tree: BoxTree, opt: AccelOptions | None = None, keep_dense: bool = False,
+                     ctx: Context | None = None, stencil_device_ptr: int | None = None):
+    """build_root_accel (accel_nd.hpp:93-95, accel_nd.cpp:707-859) on the B200
+    (dtn_gpu_build_accel): root S from the exact dense merges, S_hbs =
+    compress(S, eps, hbs_leaf), G_hbs = invert_hbs(S_hbs). A root boundary
+    below opt.crossover stays dense (accel_nd.cpp:796-818): the result is then
+    the dense SolutionOperator (with G), engine Engine.accel."""
+    from . import hbs as _hbs
+    opt = opt or AccelOptions()
+    ctx = ctx or default_context()
+    if stencil_device_ptr:
+        prob = L.dtn_problem(tree.n, stencil_device_ptr, 1)
+        n = tree.n
+    else:
+        if tree.n != op.n:
+            raise ValueError("build: tree and operator sizes differ")
+        st = np.ascontiguousarray(op.stencil, dtype=np.float64)
+        prob = L.dtn_problem(op.n, st.ctypes.data, 0)
+        n = op.n
+    opts = L.dtn_opts(0, tree.n_leaf, tree.leaf_side, 0, 0, 0, float(opt.epsilon), int(opt.crossover), 1, -1)
+    hop, hs, hg, cond = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_double()
+    ctx.check(L.lib().dtn_gpu_build_accel(ctx.h, C.byref(prob), C.byref(opts), int(opt.hbs_leaf), C.byref(hop),
+                                          C.byref(hs), C.byref(hg), C.byref(cond)))
+    dense = SolutionOperator(ctx, hop, n, not hs.value)
+    if not hs.value:  # dense root
+        dense.engine = Engine.accel
+        return dense
+    S_hbs = _hbs.HbsMatrix(ctx, hs)
+    G_hbs = _hbs.InverseFactors(ctx, hg)
+    out = CompressedSolutionOperator(n, dense.boundary.copy(), S_hbs, G_hbs, cond.value,
+                                     dense if keep_dense else None, dense.level_stats)
+    out.build_stats = dense.build_stats
+    if not keep_dense:
+        dense.free()
+    return out
+
+
 def build_with_loads(op: DiscreteOperator, tree: BoxTree, loads, engine: Engine, opt: AccelOptions | None = None):
     """bodyload.cpp:47-57 dispatcher; Engine.gpu (and Engine.dense, which the
-    B200 engine executes) build here."""
+    B200 engine executes) build here; Engine.accel builds the compressed root
+    (build_root_accel). Body loads go through the dense engine's merges."""
     if engine == Engine.accel:
-        raise NotImplementedError("the compressed (accel) engine is not available in the B200 build yet")
+        if loads is not None and len(loads):
+            raise ValueError("build_with_loads: body loads with the compressed engine are not supported; "
+                             "use Engine.dense / Engine.gpu")
+        return build_root_accel(op, tree, opt)
     return build_root_dense_op(op, tree, loads)
 
 
@@ -572,18 +641,33 @@ def _apply(sol: SolutionOperator, which: int, g):
     return Y[:, 0].copy() if vec else Y
 
 
+def _apply_hbs(sol, H, g, name):
+    from . import hbs as _hbs
+    shape = getattr(g, "shape", None) or np.shape(g)
+    if len(shape) == 0 or shape[0] != sol.boundary_size():
+        raise ValueError(name + ": boundary vector size mismatch")
+    return _hbs.apply(H, g)  # rep order = canonical order
+
+
 def apply_dtn(sol: SolutionOperator, g):
-    """v = G g (solution_operator.cpp:36-44); g may be (nb,) or (nb, batch)."""
+    """v = G g (solution_operator.cpp:36-44); g may be (nb,) or (nb, batch).
+    Compressed operators apply G_hbs (apply_inverse)."""
+    if getattr(sol, "G_hbs", None) is not None:
+        return _apply_hbs(sol, sol.G_hbs, g, "apply_dtn")
     return _apply(sol, 0, g)
 
 
 def apply_schur(sol: SolutionOperator, g):
     """S g (solution_operator.cpp:46-52)."""
+    if getattr(sol, "S_hbs", None) is not None:
+        return _apply_hbs(sol, sol.S_hbs, g, "apply_schur")
     return _apply(sol, 1, g)
 
 
 def densify_dtn(sol: SolutionOperator) -> np.ndarray:
-    """solution_operator.cpp:54-66."""
+    """solution_operator.cpp:54-66 (compressed: G_hbs applied to the identity)."""
+    if getattr(sol, "G_hbs", None) is not None:
+        return _apply_hbs(sol, sol.G_hbs, np.eye(sol.boundary_size()), "densify_dtn")
     return sol.G_dense
 
 

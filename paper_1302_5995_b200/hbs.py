@@ -16,7 +16,8 @@ import numpy as np
 from . import _lib as L
 from .dtn import Context, default_context
 
-__all__ = ["IndexTree", "build_index_tree", "HbsMatrix", "compress", "compress_operator", "apply", "reconstruct",
+__all__ = ["IndexTree", "build_index_tree", "HbsMatrix", "InverseFactors", "compress", "compress_operator", "apply",
+           "invert_hbs", "apply_inverse", "reconstruct",
            "serialize", "deserialize", "write_hbs", "read_hbs", "basis_orthonormality_defect"]
 
 
@@ -167,6 +168,39 @@ class HbsMatrix:
 
     def serialize(self) -> bytes:
         return serialize(self)
+
+
+class InverseFactors(HbsMatrix):
+    """InverseFactors (hbs_ops.hpp:46-55): the telescoping inverse factors of an
+    HbsMatrix on its tree, E in the U slots, F in the V slots, G in the D
+    (leaves) / B (parents) slots and the root core inverse in the root B, so the
+    HBS apply sweep is apply_inverse. `rep` is the object itself."""
+
+    @property
+    def rep(self) -> "InverseFactors":
+        return self
+
+    def E(self, t: int) -> np.ndarray:
+        return self.factor(t, "U")
+
+    def F(self, t: int) -> np.ndarray:
+        return self.factor(t, "V")
+
+    def G(self, t: int) -> np.ndarray:
+        return self.factor(t, "D" if self.tree.is_leaf(t) else "B")
+
+
+def invert_hbs(H: HbsMatrix) -> InverseFactors:
+    """invert_hbs (hbs_ops.hpp:64, hbs_ops.cpp:148-201) on the device. Raises
+    FactorizationError naming the node ("... is singular [node t level l]")."""
+    out = C.c_void_p()
+    H.ctx.check(L.lib().dtn_gpu_hbs_invert(H.h, C.byref(out)))
+    return InverseFactors(H.ctx, out)
+
+
+def apply_inverse(inv: InverseFactors, x):
+    """apply_inverse (hbs_ops.cpp:203-205): y = H^{-1} x through the inverse factors."""
+    return apply(inv, x)
 
 
 def _ctx(ctx):

@@ -139,3 +139,139 @@ def test_torch_device_apply(H):
     y = H.apply(c, x)
     assert y.is_cuda
     assert rel_fro(y.cpu().numpy(), A @ x.cpu().numpy()) <= 1e-9
+
+
+# ---- invert_hbs on the device (hbs_ops.cpp:148-205), test_hbs_ops.cpp:164-216 ----
+
+def test_invert_diagonal(H):  # test_hbs_ops.cpp:164-172
+    d = 1.0 + (np.arange(64) % 7)
+    inv = H.invert_hbs(H.compress(np.diag(d), 1e-12, 16))
+    x = np.linspace(-1.0, 2.0, 64)
+    assert np.linalg.norm(H.apply_inverse(inv, x) - x / d) <= 1e-12
+
+
+def test_invert_two_level_synthetic_matches_oracle(H):  # test_hbs_ops.cpp:174-180
+    h = HO.synthetic_hbs(16, 4, 2, 6)
+    g = H.deserialize(HO.serialize(h))
+    inv = H.invert_hbs(g)
+    dense = HO.reconstruct(h)
+    G = H.apply_inverse(inv, np.eye(16))
+    assert rel_fro(G, np.linalg.inv(dense)) <= 1e-9
+    # factor by factor against the oracle's inversion of the same matrix
+    ref = HO.invert_hbs(h)
+    for t in range(1, h.tree.num_nodes()):
+        assert rel_fro(inv.E(t), ref.U[t]) <= 1e-12, t
+        assert rel_fro(inv.F(t), ref.V[t]) <= 1e-12, t
+        assert rel_fro(inv.G(t), ref.D[t] if h.tree.is_leaf(t) else ref.B[t]) <= 1e-12, t
+    assert rel_fro(inv.factor(0, "B"), ref.B[0]) <= 1e-12
+
+
+@pytest.mark.parametrize("m,leaf,k,seed", [(200, 16, 5, 1), (1000, 64, 12, 2), (777, 40, 30, 3)])
+def test_invert_synthetic_sizes(H, m, leaf, k, seed):
+    h = HO.synthetic_hbs(m, leaf, k, seed)
+    inv = H.invert_hbs(H.deserialize(HO.serialize(h)))
+    x = np.random.default_rng(seed).standard_normal((m, 3))
+    ref = HO.apply(HO.invert_hbs(h), x)
+    assert rel_fro(H.apply_inverse(inv, x), ref) <= 1e-10
+    assert rel_fro(HO.apply(h, H.apply_inverse(inv, x)), x) <= 1e-11
+
+
+def test_invert_laplace_schur_residual(H):  # test_hbs_ops.cpp:182-190
+    S = O.build_root_dense(O.Problem("laplace", 64), O.Tree(64, 4096)).S
+    c = H.compress(S, 1e-7, 64)
+    x = np.random.default_rng(7).standard_normal((S.shape[0], 2))
+    back = H.apply(c, H.apply_inverse(H.invert_hbs(c), x))
+    assert np.linalg.norm(back - x) / np.linalg.norm(x) <= 1e-5
+
+
+@pytest.mark.parametrize("n", [32, 64])
+def test_invert_residual_100eps(H, n):  # test_hbs_ops.cpp:192-203
+    eps = 1e-7
+    S = O.build_root_dense(O.Problem("laplace", n), O.Tree(n, 4096)).S
+    c = H.compress(S, eps, 32)
+    x = np.random.default_rng(8).standard_normal((S.shape[0], 1))
+    back = H.apply(c, H.apply_inverse(H.invert_hbs(c), x))
+    assert np.linalg.norm(back - x) / np.linalg.norm(x) <= 100 * eps
+
+
+def test_invert_names_failing_node(H):  # test_hbs_ops.cpp:205-216
+    import paper_1302_5995_b200 as dtn
+    h = HO.synthetic_hbs(16, 4, 2, 9)
+    for t in range(h.tree.num_nodes()):
+        if h.tree.is_leaf(t):
+            h.D[t][:] = 0.0
+            break
+    with pytest.raises(dtn.FactorizationError, match=r"Dtilde is singular \[node \d+ level \d+\]"):
+        H.invert_hbs(H.deserialize(HO.serialize(h)))
+
+
+def test_invert_single_node(H):
+    A = HO.kernel_matrix(40, 1)
+    inv = H.invert_hbs(H.compress(A, 1e-10, 64))
+    assert rel_fro(H.apply_inverse(inv, np.eye(40)), np.linalg.inv(A)) <= 1e-13
+
+
+def test_invert_serializes(H):
+    """memory_bytes of the compressed engine serializes G_hbs.rep (solution_operator.cpp:9-11)."""
+    A = HO.kernel_matrix(300, 4)
+    inv = H.invert_hbs(H.compress(A, 1e-10, 32))
+    back = H.deserialize(H.serialize(inv))
+    x = np.random.default_rng(3).standard_normal((300, 2))
+    assert rel_fro(H.apply(back, x), np.linalg.solve(A, x)) <= 1e-9
+
+
+# ---- the compressed engine (build_root_accel, accel_nd.cpp:707-859) ----
+
+@pytest.mark.parametrize("name,param", [("laplace", 0.0), ("helmholtz", 40.0)])
+def test_build_root_accel_vs_dense_oracle(H, name, param):
+    """S_hbs and G_hbs of the compressed engine against the dense oracle at
+    eps = 1e-10 (M = 1020): S and the Neumann data S g within 10 eps; G g
+    within 10 eps x cond(S) (G_hbs is the exact inverse of S_hbs, so its
+    error is S_hbs's relative error amplified by the conditioning); residual
+    S (G_hbs g) = g."""
+    import paper_1302_5995_b200 as dtn
+    n = 258
+    ref = O.build_root_dense(O.Problem(name, n, param), O.Tree(n, uniform_side=16))
+    spec = dtn.catalog(name, n) if param == 0.0 else dtn.ProblemSpec.continuum(
+        "h", n, None, None, lambda x, y: np.full_like(x, -param * param))
+    eps = 1e-10
+    sol = dtn.build_root_accel(dtn.discretize(spec), dtn.build_tree_uniform(n, 16),
+                               dtn.AccelOptions(epsilon=eps, crossover=256, hbs_leaf=64))
+    assert sol.engine == dtn.Engine.accel and sol.G_hbs is not None
+    assert np.array_equal(sol.boundary, ref.boundary)
+    g = np.random.default_rng(1).uniform(-1, 1, (len(ref.boundary), 16))
+    assert rel_fro(dtn.apply_schur(sol, g), ref.S @ g) <= 10 * eps
+    assert rel_fro(H.reconstruct(sol.S_hbs), ref.S) <= 10 * eps
+    cond = np.linalg.cond(ref.S, 1)
+    assert rel_fro(dtn.apply_dtn(sol, g), ref.G @ g) <= 10 * eps * cond
+    assert rel_fro(ref.S @ dtn.apply_dtn(sol, g), g) <= 10 * eps * cond
+    # the reference's probe estimate (accel_nd.cpp:834-841) evaluated on the oracle's S and G
+    m = len(ref.boundary)
+    one = np.ones(m)
+    est = (np.abs(ref.S @ one).sum() / m) * (np.abs(ref.G @ one).sum() / m) * m
+    assert abs(sol.cond_estimate - est) <= 1e-6 * est
+    assert sol.memory_bytes() < 2 * 8 * len(ref.boundary) ** 2
+
+
+def test_build_root_accel_below_crossover_is_dense(H):  # accel_nd.cpp:796-818
+    import paper_1302_5995_b200 as dtn
+    n = 66
+    ref = O.build_root_dense(O.Problem("laplace", n), O.Tree(n, uniform_side=16))
+    sol = dtn.build_root_accel(dtn.discretize(dtn.catalog("laplace", n)), dtn.build_tree_uniform(n, 16),
+                               dtn.AccelOptions(epsilon=1e-10, crossover=1024))
+    assert sol.engine == dtn.Engine.accel and getattr(sol, "G_hbs", None) is None
+    assert rel_fro(sol.G_dense, ref.G) <= 1e-10
+    assert rel_fro(dtn.densify_dtn(sol), ref.G) <= 1e-10
+
+
+def test_build_with_loads_accel_dispatch(H):  # bodyload.cpp:47-57
+    import paper_1302_5995_b200 as dtn
+    n = 130
+    op = dtn.discretize(dtn.catalog("laplace", n))
+    tree = dtn.build_tree_uniform(n, 16)
+    sol = dtn.build_with_loads(op, tree, None, dtn.Engine.accel, dtn.AccelOptions(epsilon=1e-10, crossover=256))
+    dense = dtn.build_root_gpu(op, tree)
+    g = np.random.default_rng(5).uniform(-1, 1, len(dense.boundary))
+    assert rel_fro(dtn.apply_schur(sol, g), dtn.apply_schur(dense, g)) <= 1e-9
+    G = dtn.densify_dtn(sol)
+    assert rel_fro(G, dense.G_dense) <= 1e-9 * dense.cond_estimate
