@@ -206,6 +206,80 @@ def build_cfg4_dense(dtn, torch, dev, reps=2):
             "merge_gflop": best["merge_flops"] / 1e9, "launches": best["launches"]}
 
 
+def compressed_runs(dtn, torch, dev, stream, ctx=None):
+    """The compressed engine (build_root_accel: S from the exact dense merges,
+    S_hbs = compress(S, 1e-10), G_hbs = invert_hbs(S_hbs)) on configs[2]-[4]'s
+    operators, one GPU, and configs[4]'s solve through G_hbs. Device time of the
+    whole call (CUDA events on the context stream; the dense build's own share
+    from its events). Parity: S_hbs g against the dense S g of the same build
+    (the dense engine is itself pinned to the oracle), and G_hbs (S g) = g."""
+    from paper_1302_5995_b200 import hbs as HB
+    peak_tf, _ = fp64_peak()
+    out = {}
+    for key, cfgno, n_int, leaf in (("config3", 3, 1024, 32), ("config5_build", 5, 2048, 32), ("config4", 4, 4096, 32)):
+        op = dtn.discretize(dtn.baseline_problem(cfgno, n_int))
+        tree = dtn.build_tree_uniform(n_int + 2, leaf)
+        st = torch.from_numpy(op.stencil).to(dev)
+        opt = dtn.AccelOptions(epsilon=1e-10, crossover=256, hbs_leaf=64)
+        times = []
+        sol = None
+        for rep in range(3 if n_int < 4096 else 2):  # first: plan + graph capture (untimed)
+            if sol is not None:
+                sol.dense_op.free() if sol.dense_op is not None else None
+                sol = None
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            sol = dtn.build_root_accel(None, tree, opt, keep_dense=True, ctx=ctx, stencil_device_ptr=st.data_ptr())
+            e1.record(stream)
+            e1.synchronize()
+            if rep:
+                times.append((e0.elapsed_time(e1), sol.build_stats["build_ms"]))
+        total_ms, dense_ms = min(times)
+        nb = sol.boundary_size()
+        g = torch.from_numpy(seeded_vectors(nb, 16)).to(dev).t().contiguous().t()
+        Sg = dtn.apply_schur(sol.dense_op, g)
+        Sg_h = dtn.apply_schur(sol, g)
+        back = dtn.apply_dtn(sol, Sg)
+        rel = lambda a, b: float(torch.linalg.norm(a - b) / torch.linalg.norm(b))
+        r = {"workload": f"config{cfgno} operator n={n_int} interior, {leaf}x{leaf} leaves, compressed engine "
+                         f"eps=1e-10 (dense merges -> compress root S -> invert_hbs)",
+             "build_ms": total_ms, "dense_merges_ms": dense_ms, "compress_invert_ms": total_ms - dense_ms,
+             "grid_points_per_s": n_int ** 2 / (total_ms * 1e-3),
+             "boundary": nb, "S_max_rank": sol.S_hbs.max_rank(), "G_max_rank": sol.G_hbs.max_rank(),
+             "S_hbs_bytes": sol.S_hbs.payload_bytes(), "G_hbs_bytes": sol.G_hbs.payload_bytes(),
+             "dense_bytes": 8 * nb * nb, "cond_estimate": sol.cond_estimate,
+             "Sg_rel_vs_dense": rel(Sg_h, Sg), "G_Sg_residual": rel(back, g), "tol": 1e-9}
+        if cfgno == 5:  # configs[4]: the solve through G_hbs, 4096 vectors
+            batch = 4096
+            X = torch.from_numpy(seeded_vectors(nb, batch)).to(dev).t().contiguous().t()
+            for _ in range(5):
+                Y = dtn.apply_dtn(sol, X)
+            torch.cuda.synchronize(dev)
+            groups = []
+            for _ in range(3):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(5):
+                    Y = dtn.apply_dtn(sol, X)
+                e1.record(stream)
+                e1.synchronize()
+                groups.append(e0.elapsed_time(e1) / 5)
+            ms = sorted(groups)[1]
+            P = sol.G_hbs.payload_bytes() / 8
+            r["solve"] = {"workload": f"config5 solve: G_hbs applied to {batch} uniform[-1,1] vectors",
+                          "vectors_per_s": batch / (ms * 1e-3), "ms_per_batch": ms,
+                          "tflops": 2 * P * batch / (ms * 1e-3) / 1e12,
+                          "frac_fp64_peak": 2 * P * batch / (ms * 1e-3) / 1e12 / peak_tf,
+                          "flops_vs_dense": P / nb ** 2}
+            del X, Y
+        out[key] = r
+        sol.dense_op.free()
+        del sol, st, g, Sg, Sg_h, back
+        torch.cuda.empty_cache()
+    return out
+
+
 def solve_cfg5(dtn, torch, ctx, dev, stream, rank, world, steps, warmup):
     """configs[4]: the DtN operator of the Helmholtz kappa=100, n=2048 build
     (dense FP64 here; the compressed engine is the next step) applied to 4096
@@ -450,6 +524,10 @@ def run_b200(args, cfg, rank, world, local):
             line["config4_dense"] = build_cfg4_dense(dtn, torch, dev)
         except Exception as e:  # pragma: no cover
             line["config4_dense"] = {"error": str(e)}
+        try:
+            line["compressed"] = compressed_runs(dtn, torch, dev, stream, ctx)
+        except Exception as e:  # pragma: no cover
+            line["compressed"] = {"error": repr(e)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1

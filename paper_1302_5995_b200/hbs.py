@@ -257,7 +257,8 @@ def apply(H: HbsMatrix, x):
         X = x.reshape(M, -1) if vec else x
         if X.shape[0] != M:
             raise ValueError("apply: dimension mismatch")
-        Xf = X.t().contiguous().t() if (X.stride(0) != 1 and X.shape[1] > 1) else X.contiguous()
+        colmajor = X.stride(0) == 1 and (X.shape[1] <= 1 or X.stride(1) >= M)
+        Xf = X if colmajor else X.t().contiguous().t()  # column-major with ld >= M
         Y = torch.empty((X.shape[1], M), dtype=torch.float64, device=x.device).t()
         ldx = Xf.stride(1) if Xf.shape[1] > 1 else M
         H.ctx.check(L.lib().dtn_gpu_hbs_apply(H.h, Xf.data_ptr(), ldx, Xf.shape[1], Y.data_ptr(), M, 1))

@@ -275,3 +275,17 @@ def test_build_with_loads_accel_dispatch(H):  # bodyload.cpp:47-57
     assert rel_fro(dtn.apply_schur(sol, g), dtn.apply_schur(dense, g)) <= 1e-9
     G = dtn.densify_dtn(sol)
     assert rel_fro(G, dense.G_dense) <= 1e-9 * dense.cond_estimate
+
+
+def test_torch_column_major_batch(H):
+    """Column-major (Fortran-order) device batches are applied in place."""
+    import torch
+    A = HO.kernel_matrix(120, 2)
+    c = H.compress(A, 1e-10, 32)
+    Xh = np.asfortranarray(np.random.default_rng(1).standard_normal((120, 7)))
+    X = torch.from_numpy(Xh).cuda().t().contiguous().t()
+    assert X.stride(0) == 1
+    y = H.apply(c, X).cpu().numpy()
+    assert rel_fro(y, A @ Xh) <= 1e-9
+    y2 = H.apply(c, torch.from_numpy(np.ascontiguousarray(Xh)).cuda()).cpu().numpy()
+    assert rel_fro(y2, A @ Xh) <= 1e-9
