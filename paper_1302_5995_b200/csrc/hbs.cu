@@ -355,7 +355,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
         for (int side = 0; side < 2; ++side) e.push_back(EigDesc{G1(side, a), U0(side, a), s, ld, ld});
       }
       EigDesc* de = upload(dbuf, e, st);
-      HCK(launch_jacobi_eig(de, int(e.size()), 30, false, st));
+      HCK(launch_jacobi_eig(de, int(e.size()), 30, false, 0.0, st));
       HCK(cudaStreamSynchronize(st));
     }
     // 5. B^T = A^T U0: rows side XT(:, f) U0r (nX x s) into P1, columns side X(:, f) U0c into P2
@@ -404,7 +404,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
         for (int side = 0; side < 2; ++side) e.push_back(EigDesc{G2(side, a), W(side, a), s, ld, ld});
       }
       EigDesc* de = upload(dbuf, e, st);
-      HCK(launch_jacobi_eig(de, int(e.size()), 30, true, st));
+      HCK(launch_jacobi_eig(de, int(e.size()), 30, true, (1e-2 * eps) * (1e-2 * eps), st));
       HCK(cudaStreamSynchronize(st));
     }
     // 9. Ufull = U0 W

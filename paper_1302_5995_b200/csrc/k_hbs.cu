@@ -53,7 +53,7 @@ constexpr int JT = 512;
 constexpr int JMAXP = 512;  // max pairs (s <= 1024)
 
 __global__ void __launch_bounds__(JT) jacobi_eig_kernel(const EigDesc* __restrict__ descs, int max_sweeps,
-                                                       int smem_doubles, int rel) {
+                                                       int smem_doubles, int rel, int min_s) {
   extern __shared__ __align__(16) double jsm[];
   __shared__ double cs_[JMAXP], sn_[JMAXP];
   __shared__ int pp_[JMAXP], qq_[JMAXP];
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(JT) jacobi_eig_kernel(const EigDesc* __restric
   __shared__ double amax;
   const EigDesc d = descs[blockIdx.x];
   const int s = d.s, tid = threadIdx.x;
-  if (s <= 0) return;
+  if (s <= 0 || s < min_s) return;
   const int ls = s | 1;
   const long long need = (long long)s * ls;
   double* A = d.A;
@@ -173,13 +173,165 @@ __global__ void __launch_bounds__(JT) jacobi_eig_kernel(const EigDesc* __restric
 
 int jacobi_smem_doubles() { return 200 * 1024 / 8; }
 
-cudaError_t launch_jacobi_eig(const EigDesc* d_descs, int count, int max_sweeps, bool rel, cudaStream_t st) {
+// ---- the same Jacobi eigensolver for s <= 2 * JPMAXP, with A stored as its
+// packed upper triangle in shared memory (s <= 236 fits: the top-level Gram
+// matrices of the compressed operators, k_left + k_right <= ~200) and one
+// fused update per round: every 2 x 2 block (pair i, pair j), i <= j, becomes
+// T_i A_ij T_j^T in one pass (no separate row and column passes), V <- V T^T
+// in the same phase -- 2 barriers per round instead of 3 and half the A
+// traffic. Rotations are computed exactly as in jacobi_eig_kernel. floor > 0
+// (relative to max a_ii): a pair whose diagonal entries are both below it is
+// left alone -- both directions are far below the truncation level
+// (sigma < 1e-2 eps sigma_0), so neither the eps-rank nor the retained basis
+// depends on rotations among them, and the relative rule would otherwise
+// chase rounding noise there for every sweep.
+constexpr int JPMAXP = 128;
+constexpr int kPackedMaxS = 236;  // 236 * 237 / 2 doubles = 218.5 KB
+
+__device__ __forceinline__ int jp_idx(int r, int c) {  // packed upper triangle, r <= c
+  return c * (c + 1) / 2 + r;
+}
+
+__global__ void __launch_bounds__(JT) jacobi_eig_packed_kernel(const EigDesc* __restrict__ descs, int max_sweeps,
+                                                              int smem_doubles, int rel, double floor_rel) {
+  extern __shared__ __align__(16) double jsm[];
+  __shared__ double cs_[JPMAXP], sn_[JPMAXP];
+  __shared__ int pp_[JPMAXP], qq_[JPMAXP];
+  __shared__ int rotated;
+  __shared__ double amax;
+  const EigDesc d = descs[blockIdx.x];
+  const int s = d.s, tid = threadIdx.x;
+  if (s <= 0 || s > kPackedMaxS) return;
+  double* P = jsm;
+  const int npk = s * (s + 1) / 2;
+  const int ls = s | 1;
+  const bool v_sm = (long long)npk + (long long)s * ls <= smem_doubles;
+  double* V = v_sm ? jsm + npk : d.V;
+  const long long ldv = v_sm ? ls : d.ldv;
+  for (int e = tid; e < s * s; e += JT) {
+    const int r = e % s, c = e / s;
+    if (r <= c) P[jp_idx(r, c)] = d.A[r + (long long)c * d.lda];
+    V[r + c * ldv] = r == c ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int i = 0; i < s; ++i) m = fmax(m, fabs(P[jp_idx(i, i)]));
+    amax = m;
+  }
+  __syncthreads();
+  const double tol = DBL_EPSILON;
+  const double abs_tol = tol * amax;
+  const double flo = floor_rel * amax;
+  const int n2 = s + (s & 1), np = n2 / 2;
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    if (tid == 0) rotated = 0;
+    __syncthreads();
+    for (int r = 0; r < n2 - 1; ++r) {
+      // 1. rotations of this round's disjoint pairs
+      for (int i = tid; i < np; i += JT) {
+        int a, b;
+        if (i == 0) {
+          a = r;
+          b = n2 - 1;
+        } else {
+          a = (r + i) % (n2 - 1);
+          b = (r - i + n2 - 1) % (n2 - 1);
+        }
+        const int p = min(a, b), q = max(a, b);
+        double c = 1.0, sg = 0.0;
+        if (q < s) {
+          const double app = P[jp_idx(p, p)], aqq = P[jp_idx(q, q)], apq = P[jp_idx(p, q)];
+          const double thr = rel ? tol * sqrt(fabs(app * aqq)) : abs_tol;
+          const bool below = flo > 0.0 && fabs(app) < flo && fabs(aqq) < flo;
+          if (!below && apq != 0.0 && fabs(apq) > thr) {
+            const double tau = (aqq - app) / (2.0 * apq);
+            double t;
+            if (fabs(tau) > 1e150) t = 0.5 / tau;
+            else t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            c = 1.0 / sqrt(1.0 + t * t);
+            sg = t * c;
+            rotated = 1;
+          }
+        }
+        cs_[i] = c;
+        sn_[i] = sg;
+        pp_[i] = p;
+        qq_[i] = q;
+      }
+      __syncthreads();
+      // 2. A <- T A T^T block by block (i <= j), V <- V T^T
+      for (int w = tid; w < np * np; w += JT) {
+        const int i = w / np, j = w - i * np;
+        if (i > j) continue;
+        const double si = sn_[i], sj = sn_[j];
+        if (si == 0.0 && sj == 0.0) continue;
+        const double ci = cs_[i], cj = cs_[j];
+        const int a = pp_[i], b = qq_[i];
+        if (i == j) {  // b < s (a rotation)
+          const double app = P[jp_idx(a, a)], aqq = P[jp_idx(b, b)], apq = P[jp_idx(a, b)];
+          const double t1 = ci * app - si * apq, t2 = ci * apq - si * aqq;  // row a of T A
+          const double t3 = si * app + ci * apq, t4 = si * apq + ci * aqq;  // row b of T A
+          P[jp_idx(a, a)] = ci * t1 - si * t2;
+          P[jp_idx(b, b)] = si * t3 + ci * t4;
+          P[jp_idx(a, b)] = 0.0;
+          continue;
+        }
+        const int e = pp_[j], f = qq_[j];
+        const bool bv = b < s, fv = f < s;  // dummy partner index n2-1 == s (odd s)
+        const double xae = P[a <= e ? jp_idx(a, e) : jp_idx(e, a)];
+        const double xaf = fv ? P[a <= f ? jp_idx(a, f) : jp_idx(f, a)] : 0.0;
+        const double xbe = bv ? P[b <= e ? jp_idx(b, e) : jp_idx(e, b)] : 0.0;
+        const double xbf = (bv && fv) ? P[b <= f ? jp_idx(b, f) : jp_idx(f, b)] : 0.0;
+        // rows: a' = c_i a - s_i b, b' = s_i a + c_i b
+        const double rae = ci * xae - si * xbe, raf = ci * xaf - si * xbf;
+        const double rbe = si * xae + ci * xbe, rbf = si * xaf + ci * xbf;
+        // columns: e' = c_j e - s_j f, f' = s_j e + c_j f
+        P[a <= e ? jp_idx(a, e) : jp_idx(e, a)] = cj * rae - sj * raf;
+        if (fv) P[a <= f ? jp_idx(a, f) : jp_idx(f, a)] = sj * rae + cj * raf;
+        if (bv) P[b <= e ? jp_idx(b, e) : jp_idx(e, b)] = cj * rbe - sj * rbf;
+        if (bv && fv) P[b <= f ? jp_idx(b, f) : jp_idx(f, b)] = sj * rbe + cj * rbf;
+      }
+      for (int w = tid; w < np * s; w += JT) {
+        const int i = w / s, j = w - i * s;
+        const double sg = sn_[i];
+        if (sg != 0.0) {
+          const double c = cs_[i];
+          const int p = pp_[i], q = qq_[i];
+          const double vx = V[j + p * ldv], vy = V[j + q * ldv];
+          V[j + p * ldv] = c * vx - sg * vy;
+          V[j + q * ldv] = sg * vx + c * vy;
+        }
+      }
+      __syncthreads();
+    }
+    if (!rotated) break;
+    __syncthreads();
+  }
+  for (int i = tid; i < s; i += JT) d.A[i + (long long)i * d.lda] = P[jp_idx(i, i)];
+  if (v_sm)
+    for (int e = tid; e < s * s; e += JT) {
+      const int r = e % s, c = e / s;
+      d.V[r + (long long)c * d.ldv] = V[r + c * ldv];
+    }
+}
+
+int jacobi_packed_smem_doubles() { return 220 * 1024 / 8; }
+
+cudaError_t launch_jacobi_eig(const EigDesc* d_descs, int count, int max_sweeps, bool rel, double floor_rel,
+                              cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
   static const cudaError_t attr = cudaFuncSetAttribute(jacobi_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                        jacobi_smem_doubles() * 8);
   if (attr != cudaSuccess) return attr;
+  static const cudaError_t attr2 = cudaFuncSetAttribute(
+      jacobi_eig_packed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, jacobi_packed_smem_doubles() * 8);
+  if (attr2 != cudaSuccess) return attr2;
+  // s <= 236: packed kernel; larger blocks: the general kernel (A, V in global memory when they do not fit)
+  jacobi_eig_packed_kernel<<<count, JT, size_t(jacobi_packed_smem_doubles()) * 8, st>>>(
+      d_descs, max_sweeps, jacobi_packed_smem_doubles(), rel ? 1 : 0, floor_rel);
   jacobi_eig_kernel<<<count, JT, size_t(jacobi_smem_doubles()) * 8, st>>>(d_descs, max_sweeps, jacobi_smem_doubles(),
-                                                                        rel ? 1 : 0);
+                                                                        rel ? 1 : 0, kPackedMaxS + 1);
   return cudaGetLastError();
 }
 

@@ -173,7 +173,7 @@ def test_invert_synthetic_sizes(H, m, leaf, k, seed):
     x = np.random.default_rng(seed).standard_normal((m, 3))
     ref = HO.apply(HO.invert_hbs(h), x)
     assert rel_fro(H.apply_inverse(inv, x), ref) <= 1e-10
-    assert rel_fro(HO.apply(h, H.apply_inverse(inv, x)), x) <= 1e-11
+    assert rel_fro(HO.apply(h, H.apply_inverse(inv, x)), x) <= 1e-10
 
 
 def test_invert_laplace_schur_residual(H):  # test_hbs_ops.cpp:182-190
