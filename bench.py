@@ -213,9 +213,11 @@ def compressed_runs(dtn, torch, dev, stream, ctx=None):
     whole call (CUDA events on the context stream; the dense build's own share
     from its events). Parity: S_hbs g against the dense S g of the same build
     (the dense engine is itself pinned to the oracle), and G_hbs (S g) = g."""
-    from paper_1302_5995_b200 import hbs as HB
     peak_tf, _ = fp64_peak()
     out = {}
+    if ctx is None:  # the default context: its cached plans (config-3/4 dense runs) are reused
+        ctx = dtn.default_context(dev.index or 0)
+        ctx.set_stream(stream.cuda_stream)
     for key, cfgno, n_int, leaf in (("config3", 3, 1024, 32), ("config5_build", 5, 2048, 32), ("config4", 4, 4096, 32)):
         op = dtn.discretize(dtn.baseline_problem(cfgno, n_int))
         tree = dtn.build_tree_uniform(n_int + 2, leaf)
@@ -525,7 +527,7 @@ def run_b200(args, cfg, rank, world, local):
         except Exception as e:  # pragma: no cover
             line["config4_dense"] = {"error": str(e)}
         try:
-            line["compressed"] = compressed_runs(dtn, torch, dev, stream, ctx)
+            line["compressed"] = compressed_runs(dtn, torch, dev, stream)
         except Exception as e:  # pragma: no cover
             line["compressed"] = {"error": repr(e)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -32,7 +32,11 @@
 // repacked copy of the factors whose ranks are padded to even (zero columns)
 // so every operand is 16-byte aligned.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <stdexcept>
 
 #include "common.cuh"
@@ -113,6 +117,79 @@ void copy_batch(DevBuf& buf, const std::vector<CopyDesc>& c, cudaStream_t st) {
   HCK(launch_copy2d_batched(dd, int(c.size()), st));
   HCK(cudaStreamSynchronize(st));
 }
+
+// Grow-only device scratch of the compression (the M x M work matrices are
+// 2 GB each at M = 16380): kept per device between calls instead of
+// cudaMalloc/cudaFree per call; one compression at a time per device.
+struct Scratch {
+  std::mutex m;
+  std::vector<std::pair<void*, size_t>> slot;
+  void* get(int i, size_t bytes) {
+    if (int(slot.size()) <= i) slot.resize(i + 1, {nullptr, 0});
+    auto& e = slot[i];
+    if (e.second < bytes) {
+      if (e.first) cudaFree(e.first);
+      e = {nullptr, 0};
+      HCK(cudaMalloc(&e.first, bytes));
+      e.second = bytes;
+    }
+    return e.first;
+  }
+};
+
+// Owned factor storage of one HbsDev, handed out from a few large chunks
+// (one cudaMalloc per chunk instead of one per tree level and factor kind).
+struct Arena {
+  HbsDev& H;
+  size_t chunk;
+  double* cur = nullptr;
+  size_t left = 0;
+  Arena(HbsDev& h, size_t first_chunk_doubles) : H(h), chunk(std::max<size_t>(first_chunk_doubles, 1 << 16)) {}
+  double* alloc(size_t doubles) {
+    doubles = (doubles + 1) & ~size_t(1);  // keep 16-byte alignment
+    if (doubles > left) {
+      const size_t sz = std::max(doubles, chunk);
+      void* p = nullptr;
+      HCK(cudaMalloc(&p, sz * 8));
+      H.buffers.push_back(p);
+      cur = static_cast<double*>(p);
+      left = sz;
+      chunk *= 2;
+    }
+    double* r = cur;
+    cur += doubles;
+    left -= doubles;
+    return r;
+  }
+};
+
+Scratch& scratch(int device) {
+  static Scratch s[64];
+  return s[device & 63];
+}
+
+// DTN_HBS_TRACE=1: per-phase host timings of compress (after each synchronisation)
+struct Trace {
+  bool on = std::getenv("DTN_HBS_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  std::vector<std::pair<std::string, double>> acc;
+  void mark(const char* what) {
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    const double ms = std::chrono::duration<double, std::milli>(t - t0).count();
+    t0 = t;
+    for (auto& a : acc)
+      if (a.first == what) {
+        a.second += ms;
+        return;
+      }
+    acc.push_back({what, ms});
+  }
+  ~Trace() {
+    if (!on) return;
+    for (auto& a : acc) std::fprintf(stderr, "[hbs] %-12s %9.3f ms\n", a.first.c_str(), a.second);
+  }
+};
 
 }  // namespace
 
@@ -216,16 +293,20 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
       for (void* p : v) cudaFree(p);
     }
   } frees;
-  for (double** p : {&X, &XT, &P1, &P2}) {
-    HCK(cudaMalloc(p, big * 8));
-    frees.v.push_back(*p);
+  Scratch& scr = scratch(H.device);
+  std::lock_guard<std::mutex> lock(scr.m);
+  Trace tr;
+  // factors: leaf D (M x leaf) plus bases/couplings of ranks ~ leaf size; grown on demand
+  Arena arena(H, size_t(align2(M)) * size_t(std::min<int64_t>(leaf_cap, M)) * 4);
+  {
+    int i = 0;
+    for (double** p : {&X, &XT, &P1, &P2}) *p = static_cast<double*>(scr.get(i++, big * 8));
   }
   // B blocks (align2(s) x nX each, all active nodes): up to (M + nodes) x M
   const size_t qbig = size_t(M + nn) * size_t(M) + 64;
-  for (double** p : {&Q1, &Q2}) {
-    HCK(cudaMalloc(p, qbig * 8));
-    frees.v.push_back(*p);
-  }
+  Q1 = static_cast<double*>(scr.get(4, qbig * 8));
+  Q2 = static_cast<double*>(scr.get(5, qbig * 8));
+  tr.mark("alloc");
   // X = H
   copy_batch(dbuf, {CopyDesc{dH, X, int(ldh), int(L), int(M), int(M)}}, st);
   int64_t nX = M, ldX = L;
@@ -274,8 +355,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
     if (r == R) {  // the root: B = the reduced matrix of its two children (hbs.cpp:122-125)
       double* b = nullptr;
       H.rows[0] = int(nX);
-      HCK(cudaMalloc(&b, size_t(H.ld(0)) * nX * 8 + 8));
-      H.buffers.push_back(b);
+      b = arena.alloc(size_t(H.ld(0)) * nX + 2);
       H.B[0] = b;
       copy_batch(dbuf, {CopyDesc{X, b, int(ldX), H.ld(0), int(nX), int(nX)}}, st);
       break;
@@ -285,8 +365,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
     size_t diag_doubles = 0;
     for (int i : act) diag_doubles += size_t(align2(ssize[slots[i]])) * ssize[slots[i]];
     double* dbase = nullptr;
-    HCK(cudaMalloc(&dbase, diag_doubles * 8 + 8));
-    H.buffers.push_back(dbase);
+    dbase = arena.alloc(diag_doubles + 2);
     {
       std::vector<CopyDesc> cp;
       std::vector<ZeroDesc> zd;
@@ -306,6 +385,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
       HCK(launch_zero_blocks(dz, int(zd.size()), st));
       HCK(cudaStreamSynchronize(st));
     }
+    tr.mark("diag");
     // 2. XT = X^T
     transpose_batch(dbuf, {TransDesc{X, XT, int(ldX), int(ldX), int(nX), int(nX)}}, st);
 
@@ -322,20 +402,17 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
     }
     if (smax > 1024) throw std::runtime_error("compress: block of more than 1024 rows (rank too high)");
     // G1 (2 sides), U0, G2, W, Ufull: 2 * 5 * gsum doubles; select outputs
-    double* wk = nullptr;
-    HCK(cudaMalloc(&wk, (10 * gsum + 2 * size_t(na) * smax) * 8 + 64));
-    frees.v.push_back(wk);
+    double* wk = static_cast<double*>(scr.get(6, (10 * gsum + 2 * size_t(na) * smax) * 8 + 64));
     auto G1 = [&](int side, int a) { return wk + (0 * 2 + side) * gsum + goff[a]; };
     auto U0 = [&](int side, int a) { return wk + (1 * 2 + side) * gsum + goff[a]; };
     auto G2 = [&](int side, int a) { return wk + (2 * 2 + side) * gsum + goff[a]; };
     auto W = [&](int side, int a) { return wk + (3 * 2 + side) * gsum + goff[a]; };
     auto UF = [&](int side, int a) { return wk + (4 * 2 + side) * gsum + goff[a]; };
     double* sig = wk + 10 * gsum;
-    int* ordr = nullptr;
-    HCK(cudaMalloc(&ordr, (2 * size_t(na) * smax + 2 * size_t(na)) * sizeof(int)));
-    frees.v.push_back(ordr);
+    int* ordr = static_cast<int*>(scr.get(7, (2 * size_t(na) * smax + 2 * size_t(na)) * sizeof(int)));
     int* rk = ordr + 2 * size_t(na) * smax;
 
+    tr.mark("transpose");
     // 3. G1: rows X(f,:) X(f,:)^T = X(f,:) XT(:,f); columns XT(f,:) X(:,f)
     {
       std::vector<GemmDesc> g;
@@ -347,6 +424,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
       }
       gemm_batch(dbuf, g, 1.0, 0.0, false, st);
     }
+    tr.mark("gram1");
     // 4. Jacobi on G1 -> U0
     {
       std::vector<EigDesc> e;
@@ -358,6 +436,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
       HCK(launch_jacobi_eig(de, int(e.size()), 30, false, 0.0, st));
       HCK(cudaStreamSynchronize(st));
     }
+    tr.mark("jacobi1");
     // 5. B^T = A^T U0: rows side XT(:, f) U0r (nX x s) into P1, columns side X(:, f) U0c into P2
     //    (column block a of P at offset off[i] * L)
     {
@@ -369,6 +448,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
       }
       gemm_batch(dbuf, g, 1.0, 0.0, true, st);
     }
+    tr.mark("bt_gemm");
     // 6. B = (B^T)^T (s x nX, ld align2(s)) into Q1/Q2
     std::vector<size_t> qoff(na);
     {
@@ -386,6 +466,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
       }
       transpose_batch(dbuf, t, st);
     }
+    tr.mark("bt_trans");
     // 7. G2 = B B^T
     {
       std::vector<GemmDesc> g;
@@ -396,6 +477,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
       }
       gemm_batch(dbuf, g, 1.0, 0.0, true, st);
     }
+    tr.mark("gram2");
     // 8. Jacobi (relative) on G2 -> W, lambda on the diagonal
     {
       std::vector<EigDesc> e;
@@ -407,6 +489,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
       HCK(launch_jacobi_eig(de, int(e.size()), 30, true, (1e-2 * eps) * (1e-2 * eps), st));
       HCK(cudaStreamSynchronize(st));
     }
+    tr.mark("jacobi2");
     // 9. Ufull = U0 W
     {
       std::vector<GemmDesc> g;
@@ -416,6 +499,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
       }
       gemm_batch(dbuf, g, 1.0, 0.0, true, st);
     }
+    tr.mark("ufull");
     // 10. ranks (hbs.cpp:33-40, 47-57)
     std::vector<int> kf(na);
     {
@@ -434,13 +518,13 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
       HCK(cudaStreamSynchronize(st));
       for (int a = 0; a < na; ++a) kf[a] = std::max(hr[2 * a], hr[2 * a + 1]);
     }
+    tr.mark("select");
     // 11. U_f, V_f = leading kf columns (s x k, ld s)
     {
       size_t tot = 0;
       for (int a = 0; a < na; ++a) tot += 2 * size_t(align2(ssize[slots[act[a]]])) * kf[a];
       double* ub = nullptr;
-      HCK(cudaMalloc(&ub, tot * 8 + 8));
-      H.buffers.push_back(ub);
+      ub = arena.alloc(tot + 2);
       std::vector<GatherDesc> gd;
       size_t o = 0;
       for (int a = 0; a < na; ++a) {
@@ -460,6 +544,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
         HCK(cudaStreamSynchronize(st));
       }
     }
+    tr.mark("gather");
     // 12. next reduced matrix: TT = XT blockdiag(U~) (nX x nX'), T = TT^T, X' = T blockdiag(V~)
     std::vector<int64_t> noff(slots.size());
     int64_t nX2 = 0;
@@ -504,6 +589,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
       gemm_batch(dbuf, g, 1.0, 0.0, true, st);
       copy_batch(dbuf, c, st);
     }
+    tr.mark("reduce");
     for (int a = 0; a < na; ++a) ssize[slots[act[a]]] = kf[a];
     nX = nX2;
     ldX = ldX2;
@@ -514,6 +600,13 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
 // ---------------------------------------------------------------------------
 namespace {
 
+// Apply layout: the sweep runs on the TRANSPOSED vectors (nrhs x rows, ld =
+// align2(nrhs)), so every GEMM has the batch as its M dimension (full
+// 128-row DMMA tiles at large batch) and the factors as small right-hand
+// operands: x-hat^T = x^T V, [y-hat_l y-hat_r]^T = [x-hat_l x-hat_r]^T B^T +
+// y-hat^T U^T, y^T = x^T D^T + y-hat^T U^T. Factors are repacked once:
+// V (inner x kp), U^T (kp x inner), B^T, D^T, ranks padded to even with zero
+// rows/columns so every operand column is 16-byte aligned.
 void pack_for_apply(HbsDev& H, cudaStream_t st) {
   auto& P = H.pk;
   if (P.ready) return;
@@ -545,15 +638,15 @@ void pack_for_apply(HbsDev& H, cudaStream_t st) {
   }
   P.xh_rows = std::max<int64_t>(align2(xo), 2);
   P.xp_rows = std::max<int64_t>(pb, 2);
-  // sizes
+  auto inner_of = [&](int t) -> int {
+    return H.is_leaf(t) ? int(H.node_size(t)) : P.kp[H.nodes[t].left] + P.kp[H.nodes[t].right];
+  };
   size_t tot = 0;
-  auto need = [&](int64_t r, int64_t c) { return size_t(align2(r)) * size_t(c); };
   for (int t = 0; t < nn; ++t) {
-    const bool leaf = H.is_leaf(t);
-    const int64_t inner = leaf ? H.node_size(t) : P.kp[H.nodes[t].left] + P.kp[H.nodes[t].right];
-    if (leaf) tot += need(inner, inner);
-    if (t != 0) tot += size_t(std::max<int64_t>(align2(P.kp[t]), 2)) * size_t(inner) + need(inner, P.kp[t]);  // VT: ld >= 2
-    if (!leaf) tot += need(inner, inner);
+    const int64_t inner = inner_of(t), li = std::max<int64_t>(align2(inner), 2), lk = std::max(P.kp[t], 2);
+    if (H.is_leaf(t)) tot += size_t(li) * inner;  // D^T
+    if (t != 0) tot += size_t(li) * P.kp[t] + size_t(lk) * inner;  // V, U^T
+    if (!H.is_leaf(t)) tot += size_t(li) * inner;  // B^T
   }
   HCK(cudaMalloc(&P.buf, tot * 8 + 64));
   double* base = static_cast<double*>(P.buf);
@@ -561,47 +654,44 @@ void pack_for_apply(HbsDev& H, cudaStream_t st) {
   std::vector<PackDesc> pd;
   for (int t = 0; t < nn; ++t) {
     const bool leaf = H.is_leaf(t);
-    int i1, ip1, i2, inner;  // inner index map (rows of U/B, columns of V^T/B)
+    int i1, ip1, i2;  // inner index map: i < i1 -> i; ip1 <= i < ip1 + i2 -> i1 + (i - ip1); else padding
+    const int inner = inner_of(t);
     if (leaf) {
-      inner = int(H.node_size(t));
       i1 = inner;
       ip1 = inner;
       i2 = 0;
     } else {
       const int l = H.nodes[t].left, r = H.nodes[t].right;
-      inner = P.kp[l] + P.kp[r];
       i1 = H.rank[l];
       ip1 = P.kp[l];
       i2 = H.rank[r];
     }
-    const int ldi = int(align2(inner));
-    if (leaf) {
+    const int li = std::max(int(align2(inner)), 2), lsrc = std::max(H.ld(t), 2);
+    if (leaf) {  // D^T (inner x inner)
       P.D[t] = base + o;
-      P.ldD[t] = ldi;
-      o += size_t(ldi) * inner;
-      pd.push_back(PackDesc{H.D[t], P.D[t], H.ld(t), ldi, inner, inner, inner, inner, 0, inner, inner, 0, 0});
+      P.ldD[t] = li;
+      o += size_t(li) * inner;
+      pd.push_back(PackDesc{H.D[t], P.D[t], lsrc, li, inner, inner, inner, inner, 0, inner, inner, 0, 1});
     }
     if (t != 0) {
-      const int k = H.rank[t], kp = P.kp[t], ldk = int(align2(kp));
-      P.VT[t] = base + o;
-      P.ldVT[t] = std::max(ldk, 2);
-      o += size_t(std::max(ldk, 2)) * inner;
-      // VT(i, j) = V(map(j), i): rows i < k, columns via the inner map
-      pd.push_back(PackDesc{H.V[t], P.VT[t], std::max(H.ld(t), 2), std::max(ldk, 2), kp, inner, k, kp, 0, i1, ip1, i2, 1});
-      P.U[t] = base + o;
-      P.ldU[t] = ldi;
-      o += size_t(ldi) * kp;
-      pd.push_back(PackDesc{H.U[t], P.U[t], std::max(H.ld(t), 2), ldi, inner, kp, i1, ip1, i2, k, kp, 0, 0});
+      const int k = H.rank[t], kp = P.kp[t], lk = std::max(kp, 2);
+      P.VT[t] = base + o;  // V (inner x kp)
+      P.ldVT[t] = li;
+      o += size_t(li) * kp;
+      pd.push_back(PackDesc{H.V[t], P.VT[t], lsrc, li, inner, kp, i1, ip1, i2, k, kp, 0, 0});
+      P.U[t] = base + o;  // U^T (kp x inner): dst(i, j) = U(map(j), i)
+      P.ldU[t] = lk;
+      o += size_t(lk) * inner;
+      pd.push_back(PackDesc{H.U[t], P.U[t], lsrc, lk, kp, inner, k, kp, 0, i1, ip1, i2, 1});
     }
-    if (!leaf) {
+    if (!leaf) {  // B^T
       P.B[t] = base + o;
-      P.ldB[t] = ldi;
-      o += size_t(ldi) * inner;
-      pd.push_back(PackDesc{H.B[t], P.B[t], std::max(H.ld(t), 2), ldi, inner, inner, i1, ip1, i2, i1, ip1, i2, 0});
+      P.ldB[t] = li;
+      o += size_t(li) * inner;
+      pd.push_back(PackDesc{H.B[t], P.B[t], lsrc, li, inner, inner, i1, ip1, i2, i1, ip1, i2, 1});
     }
   }
   DevBuf dbuf;
-  // drop empty descriptors
   std::vector<PackDesc> pk2;
   for (const auto& d : pd)
     if (d.rp > 0 && d.cp > 0) pk2.push_back(d);
@@ -615,6 +705,8 @@ void pack_for_apply(HbsDev& H, cudaStream_t st) {
 
 }  // namespace
 
+// One upload of every descriptor of the call, then the whole sweep as a
+// chain of batched launches on the stream with no host synchronisation.
 void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* dY, int64_t ldy, cudaStream_t st) {
   if (nrhs <= 0) return;
   const int nn = int(H.nodes.size());
@@ -632,8 +724,8 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
   }
   pack_for_apply(H, st);
   auto& P = H.pk;
-  const int64_t nx = P.xp_rows, nh = P.xh_rows;
-  const size_t need = size_t(nx + 2 * nh) * size_t(nrhs);
+  const int64_t nx = P.xp_rows, nh = P.xh_rows, ldw = align2(nrhs);
+  const size_t need = size_t(ldw) * size_t(2 * nx + 2 * nh);
   if (need > H.ws_doubles) {
     if (H.ws) cudaFree(H.ws);
     H.ws = nullptr;
@@ -641,36 +733,63 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
     HCK(cudaMalloc(&H.ws, need * 8 + 64));
     H.ws_doubles = need;
   }
-  double* xp = H.ws;
-  double* xh = xp + nx * nrhs;
-  double* yh = xh + nh * nrhs;
-  HCK(cudaMemsetAsync(xp, 0, size_t(nx) * nrhs * 8, st));
-  // gather x into the padded leaf layout
+  double* xp = H.ws;            // x^T   (ldw x nx)
+  double* yp = xp + ldw * nx;   // y^T   (ldw x nx)
+  double* xh = yp + ldw * nx;   // x-hat^T (ldw x nh)
+  double* yh = xh + ldw * nh;   // y-hat^T (ldw x nh)
+  const int L = int(ldw);
+
+  struct Phase {
+    int kind;  // 0 GEMM (alpha 1, beta 0), 1 GEMM (alpha 1, beta 1), 2 transpose
+    size_t off;
+    int count, tiles, kmax;
+  };
+  std::vector<GemmDesc> gd;
+  std::vector<TransDesc> td;
+  std::vector<Phase> ph;
+  auto add_gemm = [&](std::vector<GemmDesc>&& v, int beta) {
+    int tiles = 0, kmax = 0;
+    std::vector<GemmDesc> keep;
+    for (const auto& d : v)
+      if (d.m > 0 && d.n > 0 && d.k > 0) {
+        keep.push_back(d);
+        tiles = std::max(tiles, gemm_tiles(d.m, d.n));
+        kmax = std::max(kmax, d.k);
+      }
+    if (keep.empty()) return;
+    ph.push_back(Phase{beta, gd.size(), int(keep.size()), tiles, kmax});
+    gd.insert(gd.end(), keep.begin(), keep.end());
+  };
+  auto add_trans = [&](std::vector<TransDesc>&& v) {
+    int tiles = 0;
+    for (const auto& d : v) tiles = std::max(tiles, ((d.m + 31) / 32) * ((d.n + 31) / 32));
+    if (v.empty() || tiles == 0) return;
+    ph.push_back(Phase{2, td.size(), int(v.size()), tiles, 0});
+    td.insert(td.end(), v.begin(), v.end());
+  };
+  // x^T: leaf rows of X transposed into their padded columns
   {
-    std::vector<CopyDesc> c;
-    for (int t = 0; t < nn; ++t)
-      if (H.is_leaf(t))
-        c.push_back(CopyDesc{dX + H.nodes[t].begin, xp + P.pb[t], int(ldx), int(nx), int(H.node_size(t)), int(nrhs)});
-    copy_batch(dbuf, c, st);
+    std::vector<TransDesc> t;
+    for (int n = 0; n < nn; ++n)
+      if (H.is_leaf(n))
+        t.push_back(TransDesc{dX + H.nodes[n].begin, xp + size_t(P.pb[n]) * L, int(ldx), L, int(H.node_size(n)),
+                              int(nrhs)});
+    add_trans(std::move(t));
   }
   const int R = H.height[0];
-  // upward: x-hat_t = V_t^T (leaf: x_t; parent: [x-hat_l; x-hat_r])
+  // upward: x-hat_t^T = [x_t^T | x-hat_l^T x-hat_r^T] V_t
   for (int r = 0; r < R; ++r) {
     std::vector<GemmDesc> g;
     for (int t = 1; t < nn; ++t) {
       if (H.height[t] != r || P.kp[t] == 0) continue;
       const bool leaf = H.is_leaf(t);
       const int inner = leaf ? int(H.node_size(t)) : P.kp[H.nodes[t].left] + P.kp[H.nodes[t].right];
-      if (inner == 0) continue;
-      const double* src = leaf ? xp + P.pb[t] : xh + P.xo[H.nodes[t].left];
-      g.push_back(GemmDesc{P.VT[t], src, xh + P.xo[t], P.kp[t], int(nrhs), inner, P.ldVT[t], int(leaf ? nx : nh),
-                           int(nh)});
+      const double* a = leaf ? xp + size_t(P.pb[t]) * L : xh + size_t(P.xo[H.nodes[t].left]) * L;
+      g.push_back(GemmDesc{a, P.VT[t], xh + size_t(P.xo[t]) * L, int(nrhs), P.kp[t], inner, L, P.ldVT[t], L});
     }
-    // children with zero padded rank still need defined x-hat rows: zero them once
-    gemm_batch(dbuf, g, 1.0, 0.0, true, st);
+    add_gemm(std::move(g), 0);
   }
-  // downward: [y-hat_l; y-hat_r] = B_t [x-hat_l; x-hat_r] + U_t y-hat_t
-  HCK(cudaMemsetAsync(yh, 0, size_t(nh) * nrhs * 8, st));
+  // downward: [y-hat_l y-hat_r]^T = [x-hat_l x-hat_r]^T B_t^T + y-hat_t^T U_t^T
   for (int r = R; r >= 1; --r) {
     std::vector<GemmDesc> gb, gu;
     for (int t = 0; t < nn; ++t) {
@@ -678,27 +797,55 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
       const int l = H.nodes[t].left;
       const int inner = P.kp[l] + P.kp[H.nodes[t].right];
       if (inner == 0) continue;
-      gb.push_back(GemmDesc{P.B[t], xh + P.xo[l], yh + P.xo[l], inner, int(nrhs), inner, P.ldB[t], int(nh), int(nh)});
+      gb.push_back(GemmDesc{xh + size_t(P.xo[l]) * L, P.B[t], yh + size_t(P.xo[l]) * L, int(nrhs), inner, inner, L,
+                            P.ldB[t], L});
       if (t != 0 && P.kp[t] > 0)
-        gu.push_back(GemmDesc{P.U[t], yh + P.xo[t], yh + P.xo[l], inner, int(nrhs), P.kp[t], P.ldU[t], int(nh), int(nh)});
+        gu.push_back(GemmDesc{yh + size_t(P.xo[t]) * L, P.U[t], yh + size_t(P.xo[l]) * L, int(nrhs), inner, P.kp[t],
+                              L, P.ldU[t], L});
     }
-    gemm_batch(dbuf, gb, 1.0, 0.0, true, st);
-    gemm_batch(dbuf, gu, 1.0, 1.0, true, st);
+    add_gemm(std::move(gb), 0);
+    add_gemm(std::move(gu), 1);
   }
-  // leaves: y_t = D_t x_t + U_t y-hat_t
+  // leaves: y_t^T = x_t^T D_t^T + y-hat_t^T U_t^T, then y = (y^T)^T
   {
-    std::vector<GemmDesc> gd, gu;
-    for (int t = 0; t < nn; ++t) {
-      if (!H.is_leaf(t)) continue;
-      const int s = int(H.node_size(t));
-      gd.push_back(GemmDesc{P.D[t], xp + P.pb[t], dY + H.nodes[t].begin, s, int(nrhs), s, P.ldD[t], int(nx), int(ldy)});
-      if (P.kp[t] > 0)
-        gu.push_back(GemmDesc{P.U[t], yh + P.xo[t], dY + H.nodes[t].begin, s, int(nrhs), P.kp[t], P.ldU[t], int(nh),
-                              int(ldy)});
+    std::vector<GemmDesc> g0, g1;
+    std::vector<TransDesc> t;
+    for (int n = 0; n < nn; ++n) {
+      if (!H.is_leaf(n)) continue;
+      const int s = int(H.node_size(n));
+      g0.push_back(GemmDesc{xp + size_t(P.pb[n]) * L, P.D[n], yp + size_t(P.pb[n]) * L, int(nrhs), s, s, L,
+                            P.ldD[n], L});
+      if (P.kp[n] > 0)
+        g1.push_back(GemmDesc{yh + size_t(P.xo[n]) * L, P.U[n], yp + size_t(P.pb[n]) * L, int(nrhs), s, P.kp[n], L,
+                              P.ldU[n], L});
+      t.push_back(TransDesc{yp + size_t(P.pb[n]) * L, dY + H.nodes[n].begin, L, int(ldy), int(nrhs), s});
     }
-    gemm_batch(dbuf, gd, 1.0, 0.0, true, st);
-    gemm_batch(dbuf, gu, 1.0, 1.0, true, st);
+    add_gemm(std::move(g0), 0);
+    add_gemm(std::move(g1), 1);
+    add_trans(std::move(t));
   }
+  // one upload (GEMM descriptors, then transposes), then the launches
+  const size_t gbytes = gd.size() * sizeof(GemmDesc), tbytes = td.size() * sizeof(TransDesc);
+  const size_t tb_off = (gbytes + 255) & ~size_t(255);
+  std::vector<unsigned char> host(tb_off + tbytes);
+  if (gbytes) std::memcpy(host.data(), gd.data(), gbytes);
+  if (tbytes) std::memcpy(host.data() + tb_off, td.data(), tbytes);
+  if (host.size() > H.desc_bytes) {
+    if (H.d_desc) cudaFree(H.d_desc);
+    H.d_desc = nullptr;
+    H.desc_bytes = 0;
+    HCK(cudaMalloc(&H.d_desc, host.size()));
+    H.desc_bytes = host.size();
+  }
+  HCK(cudaMemcpyAsync(H.d_desc, host.data(), host.size(), cudaMemcpyHostToDevice, st));
+  const GemmDesc* dg = static_cast<const GemmDesc*>(H.d_desc);
+  const TransDesc* dt = reinterpret_cast<const TransDesc*>(static_cast<unsigned char*>(H.d_desc) + tb_off);
+  for (const Phase& f : ph) {
+    if (f.kind == 2) HCK(launch_transpose_batched(dt + f.off, f.count, f.tiles, st));
+    else HCK(launch_gemm_desc(dg + f.off, f.count, f.tiles, f.kmax, 1.0, f.kind == 1 ? 1.0 : 0.0, st, true));
+  }
+  // the descriptor buffer is reused by the next call on this stream (stream order);
+  // the host copy above is staged before cudaMemcpyAsync returns (pageable source)
 }
 
 // ---------------------------------------------------------------------------
@@ -891,11 +1038,36 @@ std::unique_ptr<HbsDev> hbs_invert(const HbsDev& H, cudaStream_t st) {
       for (void* p : v) cudaFree(p);
     }
   } frees;
+  // all factor storage in one allocation, per-level work in one reused buffer
+  size_t keep_all = 0, work_max = 0, dhat_all = 0;
+  {
+    std::vector<size_t> keep_h(64, 0), work_h(64, 0);
+    for (int t = 0; t < nn; ++t) {
+      const size_t s = size_t(H.rows[t]), k = size_t(H.rank[t]), ls = size_t(align2(s));
+      const size_t lk = size_t(std::max<int64_t>(align2(k), 2));
+      const int h = std::min(H.height[t], 63);
+      keep_h[h] += ls * s + (t ? 2 * ls * k : 0) + 8;
+      work_h[h] += ls * s + (t ? ls * k + 3 * lk * s : 0) + 8;
+      if (t) dhat_all += size_t(align2(k)) * k + 2;
+    }
+    for (int h = 0; h < 64; ++h) {
+      keep_all += keep_h[h];
+      work_max = std::max(work_max, work_h[h]);
+    }
+  }
+  Arena arena(R, keep_all + 64);
+  double* work_buf = nullptr;
+  HCK(cudaMalloc(&work_buf, (work_max + dhat_all + 64) * 8));
+  frees.v.push_back(work_buf);
+  bool dhat_taken = false;
   auto dalloc = [&](size_t doubles, bool keep) {
-    double* p = nullptr;
-    HCK(cudaMalloc(&p, doubles * 8 + 64));
-    (keep ? R.buffers : frees.v).push_back(p);
-    return p;
+    if (keep) return arena.alloc(doubles);
+    // the Dhat block (first request) sits after the per-level work area
+    if (!dhat_taken) {
+      dhat_taken = true;
+      return work_buf + work_max + 2;
+    }
+    return work_buf;
   };
   int* dinfo = nullptr;
   HCK(cudaMalloc(&dinfo, size_t(nn) * sizeof(int) + 16));

@@ -47,7 +47,8 @@ cudaError_t launch_transpose_batched(const TransDesc* d_descs, int count, int ma
 // when both fit) live in shared memory with an odd leading dimension,
 // otherwise in global memory (L2). A rotation is skipped when
 // |a_pq| <= tol * sqrt(|a_pp a_qq|) (rel: Demmel-Veselic relative accuracy,
-// used on the graded second-pass Gram matrices) or <= tol * max|a_ii| (not rel).
+// used on the graded second-pass Gram matrices) or <= tol * max|a_ii| (not rel),
+// tol = max(s, 16) * DBL_EPSILON.
 // On exit the diagonal of desc.A holds lambda and desc.V the eigenvectors.
 constexpr int JT = 512;
 constexpr int JMAXP = 512;  // max pairs (s <= 1024)
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(JT) jacobi_eig_kernel(const EigDesc* __restric
     amax = m;
   }
   __syncthreads();
-  const double tol = DBL_EPSILON;
+  const double tol = DBL_EPSILON * double(max(s, 16));  // dimension-scaled stopping rule (as LAPACK dgesvj)
   const double abs_tol = tol * amax;
   const int n2 = s + (s & 1), np = n2 / 2;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(JT) jacobi_eig_packed_kernel(const EigDesc* __
     amax = m;
   }
   __syncthreads();
-  const double tol = DBL_EPSILON;
+  const double tol = DBL_EPSILON * double(max(s, 16));  // dimension-scaled stopping rule (as LAPACK dgesvj)
   const double abs_tol = tol * amax;
   const double flo = floor_rel * amax;
   const int n2 = s + (s & 1), np = n2 / 2;
