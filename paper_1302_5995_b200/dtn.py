@@ -438,22 +438,18 @@ def shard_info(tree: BoxTree, nshards: int, shard: int) -> dict:
     return dict(rect=tuple(rect), nb=nb.value)
 
 
-def build_root_gpu(op: DiscreteOperator | None, tree: BoxTree, want_G: bool = True, micro_max: int = 0,
-                   ctx: Context | None = None, stencil_device_ptr: int | None = None,
-                   profile: bool = False, nshards: int = 1, shard: int = -1, shard_S=None,
-                   export_S: bool = False, load_ids=None) -> SolutionOperator:
-    """The B200 build: leaf elimination + merges + root inverse, through dtn_gpu_build.
-    export_S: S arrives in a page-locked host array during the build (the copy
-    overlaps the root inverse); SolutionOperator.S_dense then costs nothing."""
-    ctx = ctx or default_context()
+def _make_problem(op, tree, stencil_device_ptr=None, shard_S=None):
+    """dtn_problem for the C ABI (stencil host or device; the shards' S blocks
+    for a top-of-tree build). Returns (prob, keepalive)."""
     if stencil_device_ptr:
         prob = L.dtn_problem(tree.n, stencil_device_ptr, 1)
+        keep = []
     else:
         if tree.n != op.n:
             raise ValueError("build: tree and operator sizes differ")
         st = np.ascontiguousarray(op.stencil, dtype=np.float64)
         prob = L.dtn_problem(op.n, st.ctypes.data, 0)
-    keep = []
+        keep = [st]
     if shard_S is not None:  # top of a sharded build: the shards' S blocks
         ptrs = (C.c_void_p * len(shard_S))()
         on_dev = None
@@ -478,6 +474,19 @@ def build_root_gpu(op: DiscreteOperator | None, tree: BoxTree, want_G: bool = Tr
             keep.append(S)
         prob.shard_S = ptrs
         prob.shard_S_on_device = 1 if on_dev else 0
+        keep.append(ptrs)
+    return prob, keep
+
+
+def build_root_gpu(op: DiscreteOperator | None, tree: BoxTree, want_G: bool = True, micro_max: int = 0,
+                   ctx: Context | None = None, stencil_device_ptr: int | None = None,
+                   profile: bool = False, nshards: int = 1, shard: int = -1, shard_S=None,
+                   export_S: bool = False, load_ids=None) -> SolutionOperator:
+    """The B200 build: leaf elimination + merges + root inverse, through dtn_gpu_build.
+    export_S: S arrives in a page-locked host array during the build (the copy
+    overlaps the root inverse); SolutionOperator.S_dense then costs nothing."""
+    ctx = ctx or default_context()
+    prob, keep = _make_problem(op, tree, stencil_device_ptr, shard_S)
     opts = L.dtn_opts(0, tree.n_leaf, tree.leaf_side, 1 if want_G else 0, micro_max, 1 if profile else 0, 0.0, 0,
                       nshards, shard)
     loads = None
@@ -564,25 +573,20 @@ class CompressedSolutionOperator:
 
 
 def build_root_accel(op: DiscreteOperator, tree: BoxTree, opt: AccelOptions | None = None, keep_dense: bool = False,
-                     ctx: Context | None = None, stencil_device_ptr: int | None = None):
+                     ctx: Context | None = None, stencil_device_ptr: int | None = None, nshards: int = 1,
+                     shard_S=None):
     """build_root_accel (accel_nd.hpp:93-95, accel_nd.cpp:707-859) on the B200
     (dtn_gpu_build_accel): root S from the exact dense merges, S_hbs =
     compress(S, eps, hbs_leaf), G_hbs = invert_hbs(S_hbs). A root boundary
     below opt.crossover stays dense (accel_nd.cpp:796-818): the result is then
-    the dense SolutionOperator (with G), engine Engine.accel."""
+    the dense SolutionOperator (with G), engine Engine.accel. With nshards > 1
+    and shard_S: the top of a subtree-sharded build (shard.py), compressed."""
     from . import hbs as _hbs
     opt = opt or AccelOptions()
     ctx = ctx or default_context()
-    if stencil_device_ptr:
-        prob = L.dtn_problem(tree.n, stencil_device_ptr, 1)
-        n = tree.n
-    else:
-        if tree.n != op.n:
-            raise ValueError("build: tree and operator sizes differ")
-        st = np.ascontiguousarray(op.stencil, dtype=np.float64)
-        prob = L.dtn_problem(op.n, st.ctypes.data, 0)
-        n = op.n
-    opts = L.dtn_opts(0, tree.n_leaf, tree.leaf_side, 0, 0, 0, float(opt.epsilon), int(opt.crossover), 1, -1)
+    prob, keep = _make_problem(op, tree, stencil_device_ptr, shard_S)
+    n = tree.n
+    opts = L.dtn_opts(0, tree.n_leaf, tree.leaf_side, 0, 0, 0, float(opt.epsilon), int(opt.crossover), nshards, -1)
     hop, hs, hg, cond = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_double()
     ctx.check(L.lib().dtn_gpu_build_accel(ctx.h, C.byref(prob), C.byref(opts), int(opt.hbs_leaf), C.byref(hop),
                                           C.byref(hs), C.byref(hg), C.byref(cond)))

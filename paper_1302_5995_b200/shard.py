@@ -19,8 +19,10 @@ class GpuShardEngine:
     """The B200 engine behind the C ABI (dtn_gpu_build with opts.nshards/shard)."""
 
     def __init__(self, op: dtn.DiscreteOperator, tree: dtn.BoxTree, ctx: dtn.Context | None = None,
-                 stencil_device_ptr: int | None = None, device=None):
+                 stencil_device_ptr: int | None = None, device=None, accel: dtn.AccelOptions | None = None):
+        """accel: build the root in compressed form (build_root_accel) on rank 0."""
         self.op, self.tree, self.ctx = op, tree, ctx
+        self.accel = accel
         self.stencil_device_ptr = stencil_device_ptr
         self.device = device
         self.last_shard_op = None
@@ -29,6 +31,9 @@ class GpuShardEngine:
         return dtn.shard_info(self.tree, nshards, shard)["nb"]
 
     def build_full(self):
+        if self.accel is not None:
+            return dtn.build_root_accel(self.op, self.tree, self.accel, ctx=self.ctx,
+                                        stencil_device_ptr=self.stencil_device_ptr)
         return dtn.build_root_gpu(self.op, self.tree, want_G=True, ctx=self.ctx,
                                   stencil_device_ptr=self.stencil_device_ptr)
 
@@ -44,6 +49,9 @@ class GpuShardEngine:
         return S
 
     def build_top(self, nshards: int, shard_S: list):
+        if self.accel is not None:
+            return dtn.build_root_accel(self.op, self.tree, self.accel, ctx=self.ctx,
+                                        stencil_device_ptr=self.stencil_device_ptr, nshards=nshards, shard_S=shard_S)
         return dtn.build_root_gpu(self.op, self.tree, want_G=True, ctx=self.ctx,
                                   stencil_device_ptr=self.stencil_device_ptr, nshards=nshards, shard=-1,
                                   shard_S=shard_S)
