@@ -38,7 +38,7 @@ cudaError_t launch_block_identity(double*, int, cudaStream_t);
 unsigned panel_fallbacks_read_reset();
 cudaError_t launch_ring_dtn(const double*, int, const int*, const double*, int, double, double*, long long, cudaStream_t);
 cudaError_t launch_trsm_upper_ref(const void*, int, int, cudaStream_t);
-cudaError_t launch_gemm_desc(const GemmDesc*, int, int, int, double, double, cudaStream_t, bool);
+cudaError_t launch_gemm_desc(const GemmDesc*, int, int, int, double, double, cudaStream_t, bool, bool allow_big = true);
 cudaError_t launch_perm_identity(const int*, int, int*, double*, int, cudaStream_t);
 cudaError_t launch_trsm_rows(const double*, int, double*, int, int, int, int, bool, cudaStream_t);
 cudaError_t launch_norm1(const double*, int, int, int, unsigned long long*, cudaStream_t);

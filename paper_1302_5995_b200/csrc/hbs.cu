@@ -45,7 +45,7 @@
 namespace dtnb {
 
 cudaError_t launch_gemm_desc(const GemmDesc* d_descs, int count, int max_tiles, int kmax, double alpha, double beta,
-                             cudaStream_t st, bool a_aligned);
+                             cudaStream_t st, bool a_aligned, bool allow_big = true);
 int gemm_tiles(int m, int n);
 cudaError_t launch_copy2d_batched(const void* d_descs, int count, cudaStream_t st);
 
@@ -600,65 +600,66 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
 // ---------------------------------------------------------------------------
 namespace {
 
-// Apply layout: the sweep runs on the TRANSPOSED vectors (nrhs x rows, ld =
-// align2(nrhs)), so every GEMM has the batch as its M dimension (full
+// Apply layout: the sweep runs on the TRANSPOSED vectors (nrhs x columns,
+// ld = align2(nrhs)), so every GEMM has the batch as its M dimension (full
 // 128-row DMMA tiles at large batch) and the factors as small right-hand
-// operands: x-hat^T = x^T V, [y-hat_l y-hat_r]^T = [x-hat_l x-hat_r]^T B^T +
-// y-hat^T U^T, y^T = x^T D^T + y-hat^T U^T. Factors are repacked once:
-// V (inner x kp), U^T (kp x inner), B^T, D^T, ranks padded to even with zero
-// rows/columns so every operand column is 16-byte aligned.
+// operands. Every node owns a column group of the workspace:
+//   leaf t:   [ x_t (s, padded to even) | y-hat_t (kp_t) ]
+//   parent t: [ x-hat_l (kp_l) | x-hat_r (kp_r) | y-hat_t (kp_t) ]   (root: no y-hat)
+// so that each step of hbs.cpp:187-232 is ONE GEMM with a contiguous A:
+//   up:    x-hat_t^T = group_t[:, :inner] V_t                  (into the parent's group)
+//   down:  y-hat_c^T = group_t [B_t^T; U_t^T][:, cols of c]    (into child c's group)
+//   leaf:  y_t^T     = group_t [D_t^T; U_t^T]
+// Factors are repacked once (ranks padded to even with zero rows/columns, all
+// operand columns 16-byte aligned).
 void pack_for_apply(HbsDev& H, cudaStream_t st) {
   auto& P = H.pk;
   if (P.ready) return;
   const int nn = int(H.nodes.size());
   P.kp.assign(nn, 0);
-  P.xo.assign(nn, 0);
+  P.inner.assign(nn, 0);
+  P.go.assign(nn, 0);
+  P.gw.assign(nn, 0);
   P.pb.assign(nn, 0);
-  P.D.assign(nn, nullptr);
-  P.VT.assign(nn, nullptr);
-  P.U.assign(nn, nullptr);
-  P.B.assign(nn, nullptr);
-  P.ldD.assign(nn, 0);
-  P.ldVT.assign(nn, 0);
-  P.ldU.assign(nn, 0);
-  P.ldB.assign(nn, 0);
+  P.V.assign(nn, nullptr);
+  P.W.assign(nn, nullptr);
+  P.ldV.assign(nn, 0);
+  P.ldW.assign(nn, 0);
   for (int t = 1; t < nn; ++t) P.kp[t] = int(align2(H.rank[t]));
-  // x-hat offsets: sibling pairs contiguous (left then right), pairs in preorder
-  int64_t xo = 0, pb = 0;
+  int64_t cols = 0, outc = 0;
   for (int t = 0; t < nn; ++t) {
-    if (!H.is_leaf(t)) {
-      const int l = H.nodes[t].left, r = H.nodes[t].right;
-      P.xo[l] = int(xo);
-      P.xo[r] = int(xo + P.kp[l]);
-      xo += P.kp[l] + P.kp[r];
+    if (H.is_leaf(t)) {
+      P.inner[t] = int(align2(H.node_size(t)));  // x columns incl. the zero pad column
+      P.pb[t] = int(outc);
+      outc += align2(H.node_size(t));
     } else {
-      P.pb[t] = int(pb);
-      pb += align2(H.node_size(t));
+      P.inner[t] = P.kp[H.nodes[t].left] + P.kp[H.nodes[t].right];
     }
+    P.gw[t] = P.inner[t] + P.kp[t];
+    P.go[t] = int(cols);
+    cols += P.gw[t];
   }
-  P.xh_rows = std::max<int64_t>(align2(xo), 2);
-  P.xp_rows = std::max<int64_t>(pb, 2);
-  auto inner_of = [&](int t) -> int {
-    return H.is_leaf(t) ? int(H.node_size(t)) : P.kp[H.nodes[t].left] + P.kp[H.nodes[t].right];
-  };
+  P.cols = std::max<int64_t>(cols, 2);
+  P.out_cols = std::max<int64_t>(outc, 2);
   size_t tot = 0;
   for (int t = 0; t < nn; ++t) {
-    const int64_t inner = inner_of(t), li = std::max<int64_t>(align2(inner), 2), lk = std::max(P.kp[t], 2);
-    if (H.is_leaf(t)) tot += size_t(li) * inner;  // D^T
-    if (t != 0) tot += size_t(li) * P.kp[t] + size_t(lk) * inner;  // V, U^T
-    if (!H.is_leaf(t)) tot += size_t(li) * inner;  // B^T
+    const int64_t in = P.inner[t], li = std::max<int64_t>(in, 2), lw = std::max<int64_t>(P.gw[t], 2);
+    const int64_t ncol = H.is_leaf(t) ? H.node_size(t) : in;
+    if (t != 0) tot += size_t(li) * P.kp[t];  // V
+    tot += size_t(lw) * ncol;                 // W
   }
   HCK(cudaMalloc(&P.buf, tot * 8 + 64));
+  HCK(cudaMemsetAsync(P.buf, 0, tot * 8 + 64, st));
   double* base = static_cast<double*>(P.buf);
   size_t o = 0;
   std::vector<PackDesc> pd;
   for (int t = 0; t < nn; ++t) {
     const bool leaf = H.is_leaf(t);
-    int i1, ip1, i2;  // inner index map: i < i1 -> i; ip1 <= i < ip1 + i2 -> i1 + (i - ip1); else padding
-    const int inner = inner_of(t);
+    // inner index map (rows of V / U^T columns / B): i < i1 -> i; ip1 <= i < ip1 + i2 -> i1 + (i - ip1)
+    int i1, ip1, i2;
     if (leaf) {
-      i1 = inner;
-      ip1 = inner;
+      i1 = int(H.node_size(t));
+      ip1 = i1;
       i2 = 0;
     } else {
       const int l = H.nodes[t].left, r = H.nodes[t].right;
@@ -666,30 +667,26 @@ void pack_for_apply(HbsDev& H, cudaStream_t st) {
       ip1 = P.kp[l];
       i2 = H.rank[r];
     }
-    const int li = std::max(int(align2(inner)), 2), lsrc = std::max(H.ld(t), 2);
-    if (leaf) {  // D^T (inner x inner)
-      P.D[t] = base + o;
-      P.ldD[t] = li;
-      o += size_t(li) * inner;
-      pd.push_back(PackDesc{H.D[t], P.D[t], lsrc, li, inner, inner, inner, inner, 0, inner, inner, 0, 1});
-    }
+    const int in = P.inner[t], li = std::max(in, 2), lsrc = std::max(H.ld(t), 2);
+    const int k = t ? H.rank[t] : 0, kp = P.kp[t];
+    const int ncol = leaf ? int(H.node_size(t)) : in;  // columns of W (= rows of D, or inner)
     if (t != 0) {
-      const int k = H.rank[t], kp = P.kp[t], lk = std::max(kp, 2);
-      P.VT[t] = base + o;  // V (inner x kp)
-      P.ldVT[t] = li;
+      P.V[t] = base + o;
+      P.ldV[t] = li;
       o += size_t(li) * kp;
-      pd.push_back(PackDesc{H.V[t], P.VT[t], lsrc, li, inner, kp, i1, ip1, i2, k, kp, 0, 0});
-      P.U[t] = base + o;  // U^T (kp x inner): dst(i, j) = U(map(j), i)
-      P.ldU[t] = lk;
-      o += size_t(lk) * inner;
-      pd.push_back(PackDesc{H.U[t], P.U[t], lsrc, lk, kp, inner, k, kp, 0, i1, ip1, i2, 1});
+      pd.push_back(PackDesc{H.V[t], P.V[t], lsrc, li, in, kp, i1, ip1, i2, k, kp, 0, 0});
     }
-    if (!leaf) {  // B^T
-      P.B[t] = base + o;
-      P.ldB[t] = li;
-      o += size_t(li) * inner;
-      pd.push_back(PackDesc{H.B[t], P.B[t], lsrc, li, inner, inner, i1, ip1, i2, i1, ip1, i2, 1});
-    }
+    const int lw = std::max(P.gw[t], 2);
+    P.W[t] = base + o;
+    P.ldW[t] = lw;
+    o += size_t(lw) * ncol;
+    if (leaf)  // D^T in rows [0, s), the pad row stays zero
+      pd.push_back(PackDesc{H.D[t], P.W[t], lsrc, lw, in, ncol, i1, ip1, 0, ncol, ncol, 0, 1});
+    else  // B^T (inner x inner, the inner map on both sides)
+      pd.push_back(PackDesc{H.B[t], P.W[t], lsrc, lw, in, in, i1, ip1, i2, i1, ip1, i2, 1});
+    if (t != 0)  // U^T in rows [inner, inner + kp): dst(i, j) = U(map(j), i)
+      pd.push_back(PackDesc{H.U[t], P.W[t] + in, lsrc, lw, kp, ncol, k, kp, 0, i1, leaf ? ncol : ip1,
+                            leaf ? 0 : i2, 1});
   }
   DevBuf dbuf;
   std::vector<PackDesc> pk2;
@@ -698,8 +695,8 @@ void pack_for_apply(HbsDev& H, cudaStream_t st) {
   if (!pk2.empty()) {
     PackDesc* dd = upload(dbuf, pk2, st);
     HCK(launch_pack(dd, int(pk2.size()), st));
-    HCK(cudaStreamSynchronize(st));
   }
+  HCK(cudaStreamSynchronize(st));
   P.ready = true;
 }
 
@@ -724,30 +721,37 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
   }
   pack_for_apply(H, st);
   auto& P = H.pk;
-  const int64_t nx = P.xp_rows, nh = P.xh_rows, ldw = align2(nrhs);
-  const size_t need = size_t(ldw) * size_t(2 * nx + 2 * nh);
-  if (need > H.ws_doubles) {
+  const int64_t ldw = align2(nrhs);
+  const size_t need = size_t(ldw) * size_t(P.cols + P.out_cols);
+  if (need > H.ws_doubles || ldw != H.ws_ld) {
     if (H.ws) cudaFree(H.ws);
     H.ws = nullptr;
     H.ws_doubles = 0;
     HCK(cudaMalloc(&H.ws, need * 8 + 64));
+    // zero once: the pad columns of odd-sized leaves are read (times a zero
+    // factor row) but never written
+    HCK(cudaMemsetAsync(H.ws, 0, need * 8 + 64, st));
     H.ws_doubles = need;
+    H.ws_ld = ldw;
   }
-  double* xp = H.ws;            // x^T   (ldw x nx)
-  double* yp = xp + ldw * nx;   // y^T   (ldw x nx)
-  double* xh = yp + ldw * nx;   // x-hat^T (ldw x nh)
-  double* yh = xh + ldw * nh;   // y-hat^T (ldw x nh)
   const int L = int(ldw);
+  double* gws = H.ws;                  // the node groups (ldw x cols)
+  double* yp = gws + ldw * P.cols;     // y^T staging (ldw x out_cols)
+  auto col = [&](int64_t c) { return gws + size_t(c) * L; };
+  auto xhat_slot = [&](int c) {  // x-hat_c lives in its parent's group
+    const int p = H.nodes[c].parent;
+    return P.go[p] + (H.nodes[p].left == c ? 0 : P.kp[H.nodes[p].left]);
+  };
 
   struct Phase {
-    int kind;  // 0 GEMM (alpha 1, beta 0), 1 GEMM (alpha 1, beta 1), 2 transpose
+    int kind;  // 0 GEMM (alpha 1, beta 0), 2 transpose
     size_t off;
     int count, tiles, kmax;
   };
   std::vector<GemmDesc> gd;
   std::vector<TransDesc> td;
   std::vector<Phase> ph;
-  auto add_gemm = [&](std::vector<GemmDesc>&& v, int beta) {
+  auto add_gemm = [&](std::vector<GemmDesc>&& v) {
     int tiles = 0, kmax = 0;
     std::vector<GemmDesc> keep;
     for (const auto& d : v)
@@ -757,7 +761,7 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
         kmax = std::max(kmax, d.k);
       }
     if (keep.empty()) return;
-    ph.push_back(Phase{beta, gd.size(), int(keep.size()), tiles, kmax});
+    ph.push_back(Phase{0, gd.size(), int(keep.size()), tiles, kmax});
     gd.insert(gd.end(), keep.begin(), keep.end());
   };
   auto add_trans = [&](std::vector<TransDesc>&& v) {
@@ -767,61 +771,52 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
     ph.push_back(Phase{2, td.size(), int(v.size()), tiles, 0});
     td.insert(td.end(), v.begin(), v.end());
   };
-  // x^T: leaf rows of X transposed into their padded columns
+  // x^T into the leaf groups
   {
     std::vector<TransDesc> t;
     for (int n = 0; n < nn; ++n)
       if (H.is_leaf(n))
-        t.push_back(TransDesc{dX + H.nodes[n].begin, xp + size_t(P.pb[n]) * L, int(ldx), L, int(H.node_size(n)),
-                              int(nrhs)});
+        t.push_back(TransDesc{dX + H.nodes[n].begin, col(P.go[n]), int(ldx), L, int(H.node_size(n)), int(nrhs)});
     add_trans(std::move(t));
   }
   const int R = H.height[0];
-  // upward: x-hat_t^T = [x_t^T | x-hat_l^T x-hat_r^T] V_t
+  // upward: x-hat_t^T = group_t[:, :inner] V_t (leaves: the s real columns)
   for (int r = 0; r < R; ++r) {
     std::vector<GemmDesc> g;
     for (int t = 1; t < nn; ++t) {
       if (H.height[t] != r || P.kp[t] == 0) continue;
-      const bool leaf = H.is_leaf(t);
-      const int inner = leaf ? int(H.node_size(t)) : P.kp[H.nodes[t].left] + P.kp[H.nodes[t].right];
-      const double* a = leaf ? xp + size_t(P.pb[t]) * L : xh + size_t(P.xo[H.nodes[t].left]) * L;
-      g.push_back(GemmDesc{a, P.VT[t], xh + size_t(P.xo[t]) * L, int(nrhs), P.kp[t], inner, L, P.ldVT[t], L});
+      const int K = H.is_leaf(t) ? int(H.node_size(t)) : P.inner[t];
+      g.push_back(GemmDesc{col(P.go[t]), P.V[t], col(xhat_slot(t)), int(nrhs), P.kp[t], K, L, P.ldV[t], L});
     }
-    add_gemm(std::move(g), 0);
+    add_gemm(std::move(g));
   }
-  // downward: [y-hat_l y-hat_r]^T = [x-hat_l x-hat_r]^T B_t^T + y-hat_t^T U_t^T
+  // downward: y-hat_c^T = group_t [B_t^T; U_t^T][:, cols of c], one GEMM per child
   for (int r = R; r >= 1; --r) {
-    std::vector<GemmDesc> gb, gu;
+    std::vector<GemmDesc> g;
     for (int t = 0; t < nn; ++t) {
       if (H.height[t] != r || H.is_leaf(t)) continue;
-      const int l = H.nodes[t].left;
-      const int inner = P.kp[l] + P.kp[H.nodes[t].right];
-      if (inner == 0) continue;
-      gb.push_back(GemmDesc{xh + size_t(P.xo[l]) * L, P.B[t], yh + size_t(P.xo[l]) * L, int(nrhs), inner, inner, L,
-                            P.ldB[t], L});
-      if (t != 0 && P.kp[t] > 0)
-        gu.push_back(GemmDesc{yh + size_t(P.xo[t]) * L, P.U[t], yh + size_t(P.xo[l]) * L, int(nrhs), inner, P.kp[t],
-                              L, P.ldU[t], L});
+      const int l = H.nodes[t].left, rr = H.nodes[t].right;
+      const int K = P.gw[t];
+      if (P.inner[t] == 0) continue;
+      if (P.kp[l] > 0)
+        g.push_back(GemmDesc{col(P.go[t]), P.W[t], col(P.go[l] + P.inner[l]), int(nrhs), P.kp[l], K, L, P.ldW[t], L});
+      if (P.kp[rr] > 0)
+        g.push_back(GemmDesc{col(P.go[t]), P.W[t] + size_t(P.kp[l]) * P.ldW[t], col(P.go[rr] + P.inner[rr]), int(nrhs),
+                             P.kp[rr], K, L, P.ldW[t], L});
     }
-    add_gemm(std::move(gb), 0);
-    add_gemm(std::move(gu), 1);
+    add_gemm(std::move(g));
   }
-  // leaves: y_t^T = x_t^T D_t^T + y-hat_t^T U_t^T, then y = (y^T)^T
+  // leaves: y_t^T = group_t [D_t^T; U_t^T], then y = (y^T)^T
   {
-    std::vector<GemmDesc> g0, g1;
+    std::vector<GemmDesc> g;
     std::vector<TransDesc> t;
     for (int n = 0; n < nn; ++n) {
       if (!H.is_leaf(n)) continue;
       const int s = int(H.node_size(n));
-      g0.push_back(GemmDesc{xp + size_t(P.pb[n]) * L, P.D[n], yp + size_t(P.pb[n]) * L, int(nrhs), s, s, L,
-                            P.ldD[n], L});
-      if (P.kp[n] > 0)
-        g1.push_back(GemmDesc{yh + size_t(P.xo[n]) * L, P.U[n], yp + size_t(P.pb[n]) * L, int(nrhs), s, P.kp[n], L,
-                              P.ldU[n], L});
+      g.push_back(GemmDesc{col(P.go[n]), P.W[n], yp + size_t(P.pb[n]) * L, int(nrhs), s, P.gw[n], L, P.ldW[n], L});
       t.push_back(TransDesc{yp + size_t(P.pb[n]) * L, dY + H.nodes[n].begin, L, int(ldy), int(nrhs), s});
     }
-    add_gemm(std::move(g0), 0);
-    add_gemm(std::move(g1), 1);
+    add_gemm(std::move(g));
     add_trans(std::move(t));
   }
   // one upload (GEMM descriptors, then transposes), then the launches
@@ -842,7 +837,8 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
   const TransDesc* dt = reinterpret_cast<const TransDesc*>(static_cast<unsigned char*>(H.d_desc) + tb_off);
   for (const Phase& f : ph) {
     if (f.kind == 2) HCK(launch_transpose_batched(dt + f.off, f.count, f.tiles, st));
-    else HCK(launch_gemm_desc(dg + f.off, f.count, f.tiles, f.kmax, 1.0, f.kind == 1 ? 1.0 : 0.0, st, true));
+    else  // 128 x 64 tiles: the short reductions (K = leaf or rank) measured 20 % faster than 128 x 128
+      HCK(launch_gemm_desc(dg + f.off, f.count, f.tiles, f.kmax, 1.0, 0.0, st, true, false));
   }
   // the descriptor buffer is reused by the next call on this stream (stream order);
   // the host copy above is staged before cudaMemcpyAsync returns (pageable source)

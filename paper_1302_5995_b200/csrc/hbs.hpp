@@ -101,17 +101,20 @@ struct HbsDev {
   int ld(int t) const { return int((rows[t] + 1) & ~1); }
   std::vector<void*> buffers;  // owning allocations
   // apply layout: ranks padded to even with zero columns, every block 16-byte aligned
+  // apply layout (hbs.cu, pack_for_apply): per node a column group of the
+  // transposed workspace -- leaf [x_t | y-hat_t], parent [x-hat_l x-hat_r | y-hat_t]
   struct Packed {
     bool ready = false;
-    std::vector<int> kp, xo, pb;  // padded rank, x-hat row offset, padded leaf row offset
-    int64_t xh_rows = 0, xp_rows = 0;
-    std::vector<double*> D, VT, U, B;  // ld = align2(rows)
-    std::vector<int> ldD, ldVT, ldU, ldB;
+    std::vector<int> kp, inner, go, gw, pb;  // padded rank, inner size, group offset/width, output offset
+    int64_t cols = 0, out_cols = 0;
+    std::vector<double*> V, W;  // V (inner x kp); W = [D^T; U^T] (leaf) or [B^T; U^T] (parent)
+    std::vector<int> ldV, ldW;
     void* buf = nullptr;
   } pk;
   // apply workspace
   double* ws = nullptr;
   size_t ws_doubles = 0;
+  int64_t ws_ld = 0;
   void* d_desc = nullptr;
   size_t desc_bytes = 0;
   ~HbsDev();

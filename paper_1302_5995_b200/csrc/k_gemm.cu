@@ -361,9 +361,9 @@ int gemm_big_min_tiles() {
 }
 
 cudaError_t launch_gemm_desc(const GemmDesc* d_descs, int count, int max_tiles, int kmax, double alpha, double beta,
-                             cudaStream_t st, bool a_aligned) {
+                             cudaStream_t st, bool a_aligned, bool allow_big) {
   if (count <= 0 || max_tiles <= 0) return cudaSuccess;
-  if (a_aligned && max_tiles * count >= gemm_big_min_tiles() && kmax >= 64) {
+  if (allow_big && a_aligned && max_tiles * count >= gemm_big_min_tiles() && kmax >= 64) {
     const bool upd = alpha == -1.0 && beta == 1.0;
     dim3 grid(max_tiles, count);  // (128 x 64 tile count bounds the 128 x 128 one; extra CTAs exit)
     if (upd) gemm_big_kernel<true><<<grid, GTHREADS, sizeof(GemmSmemX), st>>>(d_descs, alpha, beta);

@@ -75,3 +75,14 @@ def test_no_cpu_fallback_without_device():
         pytest.skip("device present")
     with pytest.raises(RuntimeError):
         dtn.Context(0)
+
+
+def test_library_has_no_unresolved_engine_symbols():
+    """Every dtnb:: function the library calls is defined in it (a stale
+    declaration in one translation unit would leave an undefined symbol that
+    only fails at load/first call on the GPU box)."""
+    import subprocess
+    from paper_1302_5995_b200 import _lib
+    out = subprocess.run(["nm", "-D", "--undefined-only", "-C", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    bad = [ln for ln in out.splitlines() if "dtnb::" in ln]
+    assert not bad, bad
