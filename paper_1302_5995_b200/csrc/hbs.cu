@@ -46,6 +46,8 @@ namespace dtnb {
 
 cudaError_t launch_gemm_desc(const GemmDesc* d_descs, int count, int max_tiles, int kmax, double alpha, double beta,
                              cudaStream_t st, bool a_aligned, bool allow_big = true);
+cudaError_t launch_gemm_desc_tc(const GemmDesc* d_descs, int count, int max_tiles, int kmax, double alpha, double beta,
+                                cudaStream_t st);
 int gemm_tiles(int m, int n);
 cudaError_t launch_copy2d_batched(const void* d_descs, int count, cudaStream_t st);
 
@@ -722,7 +724,7 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
   pack_for_apply(H, st);
   auto& P = H.pk;
   const int64_t ldw = align2(nrhs);
-  const size_t need = size_t(ldw) * size_t(P.cols + P.out_cols);
+  const size_t need = size_t(ldw) * size_t(P.cols);
   if (need > H.ws_doubles || ldw != H.ws_ld) {
     if (H.ws) cudaFree(H.ws);
     H.ws = nullptr;
@@ -735,8 +737,7 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
     H.ws_ld = ldw;
   }
   const int L = int(ldw);
-  double* gws = H.ws;                  // the node groups (ldw x cols)
-  double* yp = gws + ldw * P.cols;     // y^T staging (ldw x out_cols)
+  double* gws = H.ws;  // the node groups (ldw x cols)
   auto col = [&](int64_t c) { return gws + size_t(c) * L; };
   auto xhat_slot = [&](int c) {  // x-hat_c lives in its parent's group
     const int p = H.nodes[c].parent;
@@ -744,14 +745,14 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
   };
 
   struct Phase {
-    int kind;  // 0 GEMM (alpha 1, beta 0), 2 transpose
+    int kind;  // 0 GEMM (alpha 1, beta 0), 2 transpose, 3 GEMM with C stored transposed
     size_t off;
     int count, tiles, kmax;
   };
   std::vector<GemmDesc> gd;
   std::vector<TransDesc> td;
   std::vector<Phase> ph;
-  auto add_gemm = [&](std::vector<GemmDesc>&& v) {
+  auto add_gemm = [&](std::vector<GemmDesc>&& v, int kind = 0) {
     int tiles = 0, kmax = 0;
     std::vector<GemmDesc> keep;
     for (const auto& d : v)
@@ -761,7 +762,7 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
         kmax = std::max(kmax, d.k);
       }
     if (keep.empty()) return;
-    ph.push_back(Phase{0, gd.size(), int(keep.size()), tiles, kmax});
+    ph.push_back(Phase{kind, gd.size(), int(keep.size()), tiles, kmax});
     gd.insert(gd.end(), keep.begin(), keep.end());
   };
   auto add_trans = [&](std::vector<TransDesc>&& v) {
@@ -806,18 +807,15 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
     }
     add_gemm(std::move(g));
   }
-  // leaves: y_t^T = group_t [D_t^T; U_t^T], then y = (y^T)^T
+  // leaves: y_t = (group_t [D_t^T; U_t^T])^T, stored transposed straight into Y
   {
     std::vector<GemmDesc> g;
-    std::vector<TransDesc> t;
     for (int n = 0; n < nn; ++n) {
       if (!H.is_leaf(n)) continue;
       const int s = int(H.node_size(n));
-      g.push_back(GemmDesc{col(P.go[n]), P.W[n], yp + size_t(P.pb[n]) * L, int(nrhs), s, P.gw[n], L, P.ldW[n], L});
-      t.push_back(TransDesc{yp + size_t(P.pb[n]) * L, dY + H.nodes[n].begin, L, int(ldy), int(nrhs), s});
+      g.push_back(GemmDesc{col(P.go[n]), P.W[n], dY + H.nodes[n].begin, int(nrhs), s, P.gw[n], L, P.ldW[n], int(ldy)});
     }
-    add_gemm(std::move(g));
-    add_trans(std::move(t));
+    add_gemm(std::move(g), 3);  // transposed-C GEMM
   }
   // one upload (GEMM descriptors, then transposes), then the launches
   const size_t gbytes = gd.size() * sizeof(GemmDesc), tbytes = td.size() * sizeof(TransDesc);
@@ -837,6 +835,7 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
   const TransDesc* dt = reinterpret_cast<const TransDesc*>(static_cast<unsigned char*>(H.d_desc) + tb_off);
   for (const Phase& f : ph) {
     if (f.kind == 2) HCK(launch_transpose_batched(dt + f.off, f.count, f.tiles, st));
+    else if (f.kind == 3) HCK(launch_gemm_desc_tc(dg + f.off, f.count, f.tiles, f.kmax, 1.0, 0.0, st));
     else  // 128 x 64 tiles: the short reductions (K = leaf or rank) measured 20 % faster than 128 x 128
       HCK(launch_gemm_desc(dg + f.off, f.count, f.tiles, f.kmax, 1.0, 0.0, st, true, false));
   }

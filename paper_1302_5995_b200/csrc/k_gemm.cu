@@ -28,7 +28,7 @@ struct GemmSmem {
 // UPD (C -= A*B) preloads the C tile into the accumulators before the K loop
 // (its latency overlaps the first A/B stage) and feeds -A to the DMMA, so the
 // epilogue is a plain store. Requires 16-byte aligned B columns.
-template <int BK, bool A16 = true, bool UPD = false>
+template <int BK, bool A16 = true, bool UPD = false, bool TC = false>
 __device__ __forceinline__ void gemm_tile(const double* __restrict__ A, int lda, const double* __restrict__ B,
                                           int ldb, double* C, int ldc, int m, int n, int k, int tm, int tn,
                                           double alpha, double beta, GemmSmem<BK>& sm) {
@@ -139,7 +139,8 @@ __device__ __forceinline__ void gemm_tile(const double* __restrict__ A, int lda,
         const int r = row0 + wm0 + i * 16 + g + 8 * (v >> 1);
         const int c = col0 + wn0 + j * 8 + 2 * tig + (v & 1);
         if (r < m && c < n) {
-          double* p = C + r + (long long)c * ldc;
+          // TC: C is stored transposed (element (r, c) at C[c + r * ldc])
+          double* p = TC ? C + c + (long long)r * ldc : C + r + (long long)c * ldc;
           if constexpr (UPD) *p = acc[i][j][v];
           else *p = beta == 0.0 ? alpha * acc[i][j][v] : fma(alpha, acc[i][j][v], beta * *p);
         }
@@ -148,7 +149,7 @@ __device__ __forceinline__ void gemm_tile(const double* __restrict__ A, int lda,
   }
 }
 
-template <int BK, bool UPD, bool A16>
+template <int BK, bool UPD, bool A16, bool TC = false>
 __global__ void __launch_bounds__(GTHREADS) gemm_desc_kernel(const GemmDesc* __restrict__ descs, double alpha,
                                                              double beta) {
   extern __shared__ __align__(16) unsigned char gsm_raw[];
@@ -158,8 +159,8 @@ __global__ void __launch_bounds__(GTHREADS) gemm_desc_kernel(const GemmDesc* __r
   const int t = blockIdx.x;
   if (t >= tiles_m * tiles_n) return;
   // B columns are always 16-byte aligned; A only when the launcher says so
-  gemm_tile<BK, A16, UPD>(d.A, d.lda, d.B, d.ldb, d.C, d.ldc, d.m, d.n, d.k, t % tiles_m, t / tiles_m, alpha, beta,
-                          sm);
+  gemm_tile<BK, A16, UPD, TC>(d.A, d.lda, d.B, d.ldb, d.C, d.ldc, d.m, d.n, d.k, t % tiles_m, t / tiles_m, alpha,
+                              beta, sm);
 }
 
 // ---- large-tile variant: 128 x 128 CTA tile, 8 warps of 64 x 32 (16 DMMA per
@@ -309,9 +310,9 @@ __global__ void __launch_bounds__(GTHREADS) trailing_update_kernel(KernelArgs ar
 
 int gemm_tiles(int m, int n);
 
-template <int BK, bool UPD, bool A16>
+template <int BK, bool UPD, bool A16, bool TC = false>
 cudaError_t set_desc_attr() {
-  return cudaFuncSetAttribute(gemm_desc_kernel<BK, UPD, A16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(gemm_desc_kernel<BK, UPD, A16, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               sizeof(GemmSmem<BK>));
 }
 
@@ -322,7 +323,8 @@ cudaError_t gemm_init() {
                         set_desc_attr<8, false, false>(), set_desc_attr<16, true, false>(),
                         set_desc_attr<8, true, false>(), set_desc_attr<32, false, true>(),
                         set_desc_attr<32, true, true>(), set_desc_attr<32, false, false>(),
-                        set_desc_attr<32, true, false>()})
+                        set_desc_attr<32, true, false>(), set_desc_attr<8, false, true, true>(),
+                        set_desc_attr<16, false, true, true>(), set_desc_attr<32, false, true, true>()})
     if (x != cudaSuccess) return x;
   e = cudaFuncSetAttribute(gemm_big_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(GemmSmemX));
   if (e != cudaSuccess) return e;
@@ -391,6 +393,21 @@ cudaError_t launch_gemm_desc(const GemmDesc* d_descs, int count, int max_tiles, 
   }
 #undef DTNB_DESC_PICK
 #undef DTNB_DESC_LAUNCH
+  return cudaGetLastError();
+}
+
+// C stored transposed (C^T = (A B)^T, element (r, c) at C[c + r ldc]): the
+// HBS apply's leaf step writes y directly from the transposed sweep.
+cudaError_t launch_gemm_desc_tc(const GemmDesc* d_descs, int count, int max_tiles, int kmax, double alpha, double beta,
+                                cudaStream_t st) {
+  if (count <= 0 || max_tiles <= 0) return cudaSuccess;
+  dim3 grid(max_tiles, count);
+  if (kmax >= gemm_bk32_min())
+    gemm_desc_kernel<32, false, true, true><<<grid, GTHREADS, sizeof(GemmSmem<32>), st>>>(d_descs, alpha, beta);
+  else if (kmax % 16 == 0 || kmax > 64)
+    gemm_desc_kernel<16, false, true, true><<<grid, GTHREADS, sizeof(GemmSmem<16>), st>>>(d_descs, alpha, beta);
+  else
+    gemm_desc_kernel<8, false, true, true><<<grid, GTHREADS, sizeof(GemmSmem<8>), st>>>(d_descs, alpha, beta);
   return cudaGetLastError();
 }
 
