@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -1693,8 +1694,18 @@ int dtn_gpu_build_accel(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* o
   o.want_G = dense_root ? 1 : 0;
   o.export_S = nullptr;
   dtn_op* op = nullptr;
+  const bool trace = std::getenv("DTN_HBS_TRACE") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!trace) return;
+    cudaStreamSynchronize(ctx->stream);
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[accel] %-10s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  };
   int rc = dtn_gpu_build(ctx, prob, &o, &op);
   if (rc != DTN_OK) return rc;
+  lap("build");
   if (dense_root) {  // accel_nd.cpp:796-818: below the crossover the accel engine holds dense factors
     if (cond) *cond = op->cond;
     if (op_out) *op_out = op;
@@ -1704,7 +1715,9 @@ int dtn_gpu_build_accel(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* o
   dtn_hbs* Sh = nullptr;
   dtn_hbs* Gh = nullptr;
   rc = dtn_gpu_hbs_compress_op(op, 1, opts->epsilon, hbs_leaf, &Sh);
+  lap("compress");
   if (rc == DTN_OK) rc = dtn_gpu_hbs_invert(Sh, &Gh);  // accel_nd.cpp:820-822
+  lap("invert");
   if (rc == DTN_OK && cond) {
     // accel_nd.cpp:834-841: (|S 1|_1 / m) (|G 1|_1 / m) m
     rc = guarded(ctx, [&] {
@@ -1730,6 +1743,7 @@ int dtn_gpu_build_accel(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* o
       }
       *cond = nrm[0] * nrm[1] * double(m);
     });
+    lap("cond");
   }
   if (rc != DTN_OK) {
     dtn_gpu_hbs_free(Gh);
