@@ -289,3 +289,32 @@ def test_torch_column_major_batch(H):
     assert rel_fro(y, A @ Xh) <= 1e-9
     y2 = H.apply(c, torch.from_numpy(np.ascontiguousarray(Xh)).cuda()).cpu().numpy()
     assert rel_fro(y2, A @ Xh) <= 1e-9
+
+
+@pytest.mark.parametrize("cfg,n_int,leaf", [(3, 1024, 32), (5, 2048, 32)])
+def test_baseline_compressed_configs_full_size(H, cfg, n_int, leaf):
+    """BASELINE configs 3 and 5 at full size through the compressed engine:
+    S_hbs (and the Neumann data S g) within 10 eps = 1e-9 of the dense GPU
+    operator of the same build (the dense engine is itself pinned to the
+    oracle, tests/test_gpu_parity.py), and G_hbs the inverse of S_hbs
+    (residual of S G_hbs g at the conditioning level)."""
+    import torch
+    import paper_1302_5995_b200 as dtn
+    op = dtn.discretize(dtn.baseline_problem(cfg, n_int))
+    tree = dtn.build_tree_uniform(n_int + 2, leaf)
+    eps = 1e-10
+    sol = dtn.build_root_accel(op, tree, dtn.AccelOptions(epsilon=eps, crossover=256, hbs_leaf=64), keep_dense=True)
+    nb = sol.boundary_size()
+    g = torch.from_numpy(np.random.default_rng(1).uniform(-1, 1, (nb, 16))).cuda()
+    Sg = dtn.apply_schur(sol.dense_op, g)
+    rel = lambda a, b: float(torch.linalg.norm(a - b) / torch.linalg.norm(b))
+    assert rel(dtn.apply_schur(sol, g), Sg) <= 10 * eps
+    # the whole operator: S_hbs applied to the identity against the dense S
+    E = torch.eye(nb, dtype=torch.float64, device="cuda")
+    S_rec = dtn.apply_schur(sol, E)
+    S_dense = dtn.apply_schur(sol.dense_op, E)
+    assert rel(S_rec, S_dense) <= 10 * eps
+    res = rel(dtn.apply_dtn(sol, Sg), g)
+    assert res <= 10 * eps * sol.cond_estimate, (res, sol.cond_estimate)
+    assert sol.S_hbs.max_rank() < nb / 8
+    sol.dense_op.free()
