@@ -244,7 +244,11 @@ __global__ void __launch_bounds__(JTP) jacobi_eig_packed_kernel(const EigDesc* _
         double c = 1.0, sg = 0.0;
         if (q < s) {
           const double app = P[jp_idx(p, p)], aqq = P[jp_idx(q, q)], apq = P[jp_idx(p, q)];
-          const double thr = rel ? tol * sqrt(fabs(app * aqq)) : abs_tol;
+          // pairs entirely below the truncation level (both diagonals < 4 eps^2 a_max)
+          // only need their eigenvalues to 1e-8 relative (the eps-rank decision), not
+          // to machine precision: a 1e-4 relative rule there
+          const bool sub = flo > 0.0 && fabs(app) < 4e4 * flo && fabs(aqq) < 4e4 * flo;
+          const double thr = rel ? (sub ? 1e-4 : tol) * sqrt(fabs(app * aqq)) : abs_tol;
           const bool below = flo > 0.0 && fabs(app) < flo && fabs(aqq) < flo;
           if (!below && apq != 0.0 && fabs(apq) > thr) {
             const double tau = (aqq - app) / (2.0 * apq);
