@@ -225,7 +225,7 @@ def compressed_runs(dtn, torch, dev, stream, ctx=None):
         opt = dtn.AccelOptions(epsilon=1e-10, crossover=256, hbs_leaf=64)
         times = []
         sol = None
-        for rep in range(3):  # first: plan + graph capture (untimed); then the best of two
+        for rep in range(4):  # first: plan + graph capture (untimed); then the best of three
             if sol is not None:
                 sol.dense_op.free() if sol.dense_op is not None else None
                 sol = None
