@@ -324,48 +324,81 @@ class SolutionOperator:
     dense copies S_dense / G_dense are fetched on first access."""
 
     def __init__(self, ctx: Context, handle: C.c_void_p, n: int, want_G: bool):
+        # the boundary ids, cond estimate and statistics are fetched on first
+        # access, so a build returns to the caller (and the next launch, e.g. an
+        # apply, is enqueued) without further round trips through the C ABI
         self.ctx, self.h, self.n = ctx, handle, n
         self.engine = Engine.gpu
-        nb = C.c_int64()
-        ctx.check(L.lib().dtn_gpu_boundary(handle, None, C.byref(nb)))
-        self.boundary = np.zeros(nb.value, dtype=np.int64)
-        ctx.check(L.lib().dtn_gpu_boundary(handle, self.boundary.ctypes.data, C.byref(nb)))
         self._S = None
         self._G = None
         self.has_G = want_G
         self.body_map = None  # F (nb x nloads) of a build with body loads (solution_operator.hpp:48)
         self.load_ids = None
-        cond = C.c_double()
-        ctx.check(L.lib().dtn_gpu_export(handle, None, None, C.byref(cond)))
-        self.cond_estimate = cond.value
-        st = L.dtn_build_stats()
-        ctx.check(L.lib().dtn_gpu_build_stats(handle, C.byref(st)))
-        self.build_stats = {f: getattr(st, f) for f, _ in L.dtn_build_stats._fields_}
-        cnt = C.c_int32()
-        ctx.check(L.lib().dtn_gpu_level_stats(handle, None, 0, C.byref(cnt)))
-        arr = (L.dtn_level_stats * cnt.value)()
-        ctx.check(L.lib().dtn_gpu_level_stats(handle, arr, cnt.value, C.byref(cnt)))
-        self.level_stats = [LevelStats(a.level, 0, 8 * a.max_boundary ** 2, a.seconds, a.boxes, a.flops)
-                            for a in arr]
-        ctx.check(L.lib().dtn_gpu_kernel_stats(handle, None, 0, C.byref(cnt)))
-        karr = (L.dtn_kernel_stats * max(cnt.value, 1))()
-        ctx.check(L.lib().dtn_gpu_kernel_stats(handle, karr, cnt.value, C.byref(cnt)))
-        self.kernel_stats = {k.name.decode(): dict(launches=k.launches, ms=k.ms, max_ms=k.max_ms, flops=k.flops,
-                                                   bytes=k.bytes) for k in karr[:cnt.value]}
+        self._lazy: dict = {}
+
+    def _fetch(self, key):
+        if key in self._lazy:
+            return self._lazy[key]
+        if not getattr(self, "h", None):
+            raise RuntimeError("SolutionOperator: the device operator was freed")
+        ctx, handle = self.ctx, self.h
+        if key == "nb":
+            nb = C.c_int64()
+            ctx.check(L.lib().dtn_gpu_boundary(handle, None, C.byref(nb)))
+            v = nb.value
+        elif key == "boundary":
+            nb = C.c_int64(self._fetch("nb"))
+            v = np.zeros(nb.value, dtype=np.int64)
+            ctx.check(L.lib().dtn_gpu_boundary(handle, v.ctypes.data, C.byref(nb)))
+        elif key == "cond_estimate":
+            cond = C.c_double()
+            ctx.check(L.lib().dtn_gpu_export(handle, None, None, C.byref(cond)))
+            v = cond.value
+        elif key == "build_stats":
+            st = L.dtn_build_stats()
+            ctx.check(L.lib().dtn_gpu_build_stats(handle, C.byref(st)))
+            v = {f: getattr(st, f) for f, _ in L.dtn_build_stats._fields_}
+        elif key == "level_stats":
+            cnt = C.c_int32()
+            ctx.check(L.lib().dtn_gpu_level_stats(handle, None, 0, C.byref(cnt)))
+            arr = (L.dtn_level_stats * cnt.value)()
+            ctx.check(L.lib().dtn_gpu_level_stats(handle, arr, cnt.value, C.byref(cnt)))
+            v = [LevelStats(a.level, 0, 8 * a.max_boundary ** 2, a.seconds, a.boxes, a.flops) for a in arr]
+        elif key == "kernel_stats":
+            cnt = C.c_int32()
+            ctx.check(L.lib().dtn_gpu_kernel_stats(handle, None, 0, C.byref(cnt)))
+            karr = (L.dtn_kernel_stats * max(cnt.value, 1))()
+            ctx.check(L.lib().dtn_gpu_kernel_stats(handle, karr, cnt.value, C.byref(cnt)))
+            v = {k.name.decode(): dict(launches=k.launches, ms=k.ms, max_ms=k.max_ms, flops=k.flops, bytes=k.bytes)
+                 for k in karr[:cnt.value]}
+        else:  # pragma: no cover
+            raise KeyError(key)
+        self._lazy[key] = v
+        return v
+
+    boundary = property(lambda self: self._fetch("boundary"))
+    cond_estimate = property(lambda self: self._fetch("cond_estimate"))
+    build_stats = property(lambda self: self._fetch("build_stats"))
+    level_stats = property(lambda self: self._fetch("level_stats"))
+    kernel_stats = property(lambda self: self._fetch("kernel_stats"))
 
     def free(self):
         if getattr(self, "h", None):
+            for key in ("nb", "boundary", "cond_estimate", "build_stats", "level_stats", "kernel_stats"):
+                self._fetch(key)  # host-side copies outlive the device operator
             L.lib().dtn_gpu_free(self.h)
             self.h = None
 
     def __del__(self):
         try:
-            self.free()
+            if getattr(self, "h", None):
+                L.lib().dtn_gpu_free(self.h)
+                self.h = None
         except Exception:
             pass
 
     def boundary_size(self) -> int:
-        return len(self.boundary)
+        return self._fetch("nb")
 
     @staticmethod
     def _host_matrix(nb: int) -> np.ndarray:
