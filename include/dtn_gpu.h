@@ -68,7 +68,8 @@ typedef struct {
   /* body loads (LoadPanel, dense_nd.hpp:29-32; build_with_loads, bodyload.cpp:47-57): unit loads at
    * these distinct, strictly interior unknown ids are carried through every merge as extra
    * right-hand-side columns (dense_nd.cpp:98-101, 136-147, 182-184); the result's body map
-   * F = G * rhs_root (accel_nd.cpp:872-875) is read with dtn_gpu_body_map. Needs want_G. */
+   * F = G * rhs_root (accel_nd.cpp:872-875) is read with dtn_gpu_body_map when want_G; without G
+   * the reduced load columns rhs_root are read with dtn_gpu_root_rhs. */
   const int64_t* load_ids;
   int32_t nloads;
 } dtn_opts;
@@ -130,6 +131,10 @@ int dtn_gpu_ring_dtn(const dtn_op* op, const int64_t* adj, const double* coef, i
 /* Body map F (nb x nloads, column-major, leading dimension ldf) of a build with loads:
  * solve_with_load (bodyload.cpp:68-77) is v = G g + F fhat. */
 int dtn_gpu_body_map(const dtn_op* op, double* F, int64_t ldf, int on_device);
+/* The root's reduced load columns rhs_root (nb x nloads; dense_nd.cpp:182-184, SchurData::rhs) of a
+ * build with body loads, with or without G: the compressed engine's body map is G_hbs * rhs_root
+ * (accel_nd.cpp:848-855), formed with dtn_gpu_hbs_apply. */
+int dtn_gpu_root_rhs(const dtn_op* op, double* R, int64_t ldr, int on_device);
 int dtn_gpu_apply(const dtn_op* op, int which, const double* X, int64_t ldx, int64_t batch, double* Y, int64_t ldy,
                   int on_device);
 
@@ -198,7 +203,9 @@ int dtn_gpu_hbs_invert(const dtn_hbs* H, dtn_hbs** out);
  * reference's probe estimate (accel_nd.cpp:834-841). The HBS factors are in canonical ring
  * order (rep_to_canonical = identity). A root boundary below opts->crossover stays dense
  * (accel_nd.cpp:796-818): *S_hbs = *G_hbs = NULL, the dense op (with G) in *op_out.
- * op_out (optional): the dense build (S resident; boundary ids, box S); NULL frees it. */
+ * op_out (optional): the dense build (S resident; boundary ids, box S); NULL frees it.
+ * Body loads (opts->load_ids / nloads) ride through the dense merges; with a compressed root the
+ * body map is G_hbs * rhs_root (accel_nd.cpp:848-855): rhs_root from dtn_gpu_root_rhs(*op_out). */
 int dtn_gpu_build_accel(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, int64_t hbs_leaf,
                         dtn_op** op_out, dtn_hbs** S_hbs, dtn_hbs** G_hbs, double* cond);
 

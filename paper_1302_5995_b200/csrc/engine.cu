@@ -939,8 +939,8 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
       throw std::invalid_argument("dtn_gpu_build: bad body-load list");
     if (key.nloads > 0 && key.nshards > 1)
       throw std::invalid_argument("dtn_gpu_build: body loads are not supported in sharded builds");
-    if (key.nloads > 0 && !opts->want_G)
-      throw std::invalid_argument("dtn_gpu_build: body loads need G (the body map is G * rhs_root)");
+    // (without G the body map is not formed; the root's reduced load columns are
+    // read with dtn_gpu_root_rhs -- the compressed engine applies G_hbs to them)
     const bool top_mode = key.nshards > 1 && key.shard < 0;
     if (top_mode && !prob->shard_S) throw std::invalid_argument("dtn_gpu_build: top build needs the shard S blocks");
     if (key.leaf_side <= 0 && key.n_leaf < 16) throw std::invalid_argument("build_tree: n_leaf must be >= 16");
@@ -1213,6 +1213,22 @@ int dtn_gpu_body_map(const dtn_op* op, double* F, int64_t ldf, int on_device) {
     CK(cudaSetDevice(ctx->device));
     CK(cudaMemcpy2DAsync(F, size_t(ldf) * 8, D.d_F, size_t(D.ldf) * 8, size_t(op->nb) * 8, size_t(nl),
                          on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int dtn_gpu_root_rhs(const dtn_op* op, double* R, int64_t ldr, int on_device) {
+  if (!op) return DTN_EINVAL;
+  dtn_ctx* ctx = op->ctx;
+  return guarded(ctx, [&] {
+    const PlanDev& D = *op->plan;
+    const int nl = D.P.key.nloads;
+    if (nl == 0) throw std::invalid_argument("dtn_gpu_root_rhs: the build had no body loads");
+    if (!R || ldr < op->nb) throw std::invalid_argument("dtn_gpu_root_rhs: bad output");
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaMemcpy2DAsync(R, size_t(ldr) * 8, D.d_arena + D.rhs_root_off, size_t(D.rhs_root_ld) * 8,
+                         size_t(op->nb) * 8, size_t(nl), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                         ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
   });
 }
@@ -1680,10 +1696,6 @@ int dtn_gpu_build_accel(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* o
   if (op_out) *op_out = nullptr;
   if (!(opts->epsilon > 0.0) || hbs_leaf < 2) {
     ctx->err = "build_root_accel: epsilon must be > 0 and hbs_leaf >= 2";
-    return DTN_EINVAL;
-  }
-  if (opts->nloads > 0) {
-    ctx->err = "build_root_accel: body loads are built by the dense engine (dtn_gpu_build)";
     return DTN_EINVAL;
   }
   // the root operator: S by the exact dense merges; G only when the root stays dense

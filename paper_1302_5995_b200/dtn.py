@@ -600,14 +600,15 @@ class CompressedSolutionOperator:
         return len(self.boundary)
 
     def memory_bytes(self) -> int:
-        """solution_operator.cpp:5-18: serialized S_hbs and G_hbs.rep."""
+        """solution_operator.cpp:5-18: serialized S_hbs and G_hbs.rep, plus the body map."""
         from . import hbs as _hbs
-        return len(_hbs.serialize(self.S_hbs)) + len(_hbs.serialize(self.G_hbs))
+        extra = 0 if self.body_map is None else 8 * self.body_map.size
+        return len(_hbs.serialize(self.S_hbs)) + len(_hbs.serialize(self.G_hbs)) + extra
 
 
 def build_root_accel(op: DiscreteOperator, tree: BoxTree, opt: AccelOptions | None = None, keep_dense: bool = False,
                      ctx: Context | None = None, stencil_device_ptr: int | None = None, nshards: int = 1,
-                     shard_S=None):
+                     shard_S=None, loads=None):
     """build_root_accel (accel_nd.hpp:93-95, accel_nd.cpp:707-859) on the B200
     (dtn_gpu_build_accel): root S from the exact dense merges, S_hbs =
     compress(S, eps, hbs_leaf), G_hbs = invert_hbs(S_hbs). A root boundary
@@ -620,18 +621,31 @@ def build_root_accel(op: DiscreteOperator, tree: BoxTree, opt: AccelOptions | No
     prob, keep = _make_problem(op, tree, stencil_device_ptr, shard_S)
     n = tree.n
     opts = L.dtn_opts(0, tree.n_leaf, tree.leaf_side, 0, 0, 0, float(opt.epsilon), int(opt.crossover), nshards, -1)
+    load_arr = None
+    if loads is not None and len(loads):
+        load_arr = np.ascontiguousarray(loads, dtype=np.int64)
+        opts.load_ids = load_arr.ctypes.data
+        opts.nloads = len(load_arr)
     hop, hs, hg, cond = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_double()
     ctx.check(L.lib().dtn_gpu_build_accel(ctx.h, C.byref(prob), C.byref(opts), int(opt.hbs_leaf), C.byref(hop),
                                           C.byref(hs), C.byref(hg), C.byref(cond)))
     dense = SolutionOperator(ctx, hop, n, not hs.value)
     if not hs.value:  # dense root
         dense.engine = Engine.accel
+        if load_arr is not None:
+            F = np.zeros((dense.boundary_size(), len(load_arr)), order="F")
+            ctx.check(L.lib().dtn_gpu_body_map(hop, F.ctypes.data, F.shape[0], 0))
+            dense.body_map, dense.load_ids = F, load_arr
         return dense
     S_hbs = _hbs.HbsMatrix(ctx, hs)
     G_hbs = _hbs.InverseFactors(ctx, hg)
     out = CompressedSolutionOperator(n, dense.boundary.copy(), S_hbs, G_hbs, cond.value,
                                      dense if keep_dense else None, dense.level_stats)
     out.build_stats = dense.build_stats
+    if load_arr is not None:  # body map F = G_hbs rhs_root (accel_nd.cpp:848-855), formed on the device
+        R = np.zeros((dense.boundary_size(), len(load_arr)), order="F")
+        ctx.check(L.lib().dtn_gpu_root_rhs(hop, R.ctypes.data, R.shape[0], 0))
+        out.body_map, out.load_ids = _hbs.apply(G_hbs, R), load_arr
     if not keep_dense:
         dense.free()
     return out
@@ -640,12 +654,9 @@ def build_root_accel(op: DiscreteOperator, tree: BoxTree, opt: AccelOptions | No
 def build_with_loads(op: DiscreteOperator, tree: BoxTree, loads, engine: Engine, opt: AccelOptions | None = None):
     """bodyload.cpp:47-57 dispatcher; Engine.gpu (and Engine.dense, which the
     B200 engine executes) build here; Engine.accel builds the compressed root
-    (build_root_accel). Body loads go through the dense engine's merges."""
+    (build_root_accel); its body map is G_hbs rhs_root."""
     if engine == Engine.accel:
-        if loads is not None and len(loads):
-            raise ValueError("build_with_loads: body loads with the compressed engine are not supported; "
-                             "use Engine.dense / Engine.gpu")
-        return build_root_accel(op, tree, opt)
+        return build_root_accel(op, tree, opt, loads=loads)
     return build_root_dense_op(op, tree, loads)
 
 

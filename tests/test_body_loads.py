@@ -108,3 +108,41 @@ def test_load_errors():
         dtn.build_root_gpu(op, tree, load_ids=[lat.unknown_id(5, 5)] * 2)
     with pytest.raises(ValueError):
         dtn.build_root_gpu(op, tree, want_G=False, load_ids=[lat.unknown_id(5, 5)])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("crossover", [128, 1024])
+def test_clustered_loads_network_accel(crossover):
+    # test_bodyload.cpp:97-115 with Engine::accel (compressed bound 1e-5): crossover 128
+    # compresses the root (body map = G_hbs rhs_root), 1024 keeps it dense (accel_nd.cpp:796-818)
+    n = 64
+    op = dtn.discretize(dtn.catalog("random1", n, 11))
+    pts = [(n // 2 + k % 4, n // 2 + k // 4) for k in range(10)]
+    ids = dtn.make_load_set(dtn.Lattice(n), pts)
+    sol = dtn.build_with_loads(op, dtn.build_tree(n, 256), ids, dtn.Engine.accel,
+                               dtn.AccelOptions(epsilon=1e-10, crossover=crossover, hbs_leaf=32))
+    assert (getattr(sol, "G_hbs", None) is not None) == (crossover == 128)
+    g = O.random_unit_boundary(sol.boundary_size(), 2)
+    fhat = O.random_unit_boundary(len(ids), 3)
+    v = dtn.solve_with_load(sol, g, fhat)
+    ref = _reference_with_load(op, sol.boundary, g, ids, fhat)
+    assert np.linalg.norm(v - ref) <= 1e-8 * np.linalg.norm(ref)
+    assert sol.memory_bytes() > 8 * sol.body_map.size
+
+
+@pytest.mark.gpu
+def test_loads_accel_matches_dense_engine():
+    n = 130
+    op = dtn.discretize(dtn.baseline_problem(2, n - 2))
+    tree = dtn.build_tree_uniform(n, 16)
+    rng = np.random.default_rng(5)
+    ids = dtn.make_load_set(dtn.Lattice(n), [(20, 30), (64, 64), (100, 40), (33, 99)])
+    acc = dtn.build_with_loads(op, tree, ids, dtn.Engine.accel, dtn.AccelOptions(epsilon=1e-10, crossover=256))
+    dense = dtn.build_with_loads(op, tree, ids, dtn.Engine.gpu)
+    assert acc.G_hbs is not None
+    assert np.linalg.norm(acc.body_map - dense.body_map) <= 1e-9 * dense.cond_estimate * np.linalg.norm(dense.body_map)
+    g = rng.uniform(-1, 1, dense.boundary_size())
+    fhat = rng.uniform(-1, 1, len(ids))
+    ref = _reference_with_load(op, dense.boundary, g, ids, fhat)
+    v = dtn.solve_with_load(acc, g, fhat)
+    assert np.linalg.norm(v - ref) <= 1e-7 * np.linalg.norm(ref)
