@@ -115,8 +115,20 @@ void transpose_batch(DevBuf& buf, const std::vector<TransDesc>& t, cudaStream_t 
 
 void copy_batch(DevBuf& buf, const std::vector<CopyDesc>& c, cudaStream_t st) {
   if (c.empty()) return;
-  CopyDesc* dd = upload(buf, c, st);
-  HCK(launch_copy2d_batched(dd, int(c.size()), st));
+  // large blocks (the M x M working matrix) go through the copy engine; the
+  // batched kernel is for many small blocks
+  std::vector<CopyDesc> small;
+  for (const auto& d : c) {
+    if (int64_t(d.m) * d.n >= (int64_t(1) << 20))
+      HCK(cudaMemcpy2DAsync(d.dst, size_t(d.ldd) * 8, d.src, size_t(d.lds) * 8, size_t(d.m) * 8, size_t(d.n),
+                            cudaMemcpyDeviceToDevice, st));
+    else if (d.m > 0 && d.n > 0)
+      small.push_back(d);
+  }
+  if (!small.empty()) {
+    CopyDesc* dd = upload(buf, small, st);
+    HCK(launch_copy2d_batched(dd, int(small.size()), st));
+  }
   HCK(cudaStreamSynchronize(st));
 }
 

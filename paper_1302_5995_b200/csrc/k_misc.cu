@@ -147,11 +147,14 @@ __global__ void __launch_bounds__(TB) tri_inv_u_batched_kernel(const TriDesc* __
 
 __global__ void copy2d_batched_kernel(const CopyDesc* __restrict__ descs) {
   const CopyDesc d = descs[blockIdx.y];
-  const long long total = (long long)d.m * d.n;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
-    const int r = int(e % d.m), c = int(e / d.m);
-    d.dst[r + (long long)c * d.ldd] = d.src[r + (long long)c * d.lds];
-  }
+  // rows over RT = pow2 >= m (<= blockDim) threads, the CTA's blockDim / RT
+  // thread groups and the grid over columns (no per-element division)
+  int RT = 32;
+  while (RT < d.m && RT < int(blockDim.x)) RT <<= 1;
+  const int groups = int(blockDim.x) / RT, g = int(threadIdx.x) / RT, r0 = int(threadIdx.x) & (RT - 1);
+  for (int c = blockIdx.x * groups + g; c < d.n; c += gridDim.x * groups)
+    for (int r = r0; r < d.m; r += RT)
+      d.dst[r + (long long)c * d.ldd] = d.src[r + (long long)c * d.lds];
 }
 
 cudaError_t launch_tri_inv_u_batched(const void* d_descs, int count, int max_blocks, cudaStream_t st) {
