@@ -30,6 +30,14 @@ struct GemmDesc {  // C(m x n) = beta*C + alpha*A(m x k)*B(k x n), column-major
   int m, n, k, lda, ldb, ldc;
 };
 
+struct GemmDesc2 {  // C = A_cat B, A_cat = [A (row-major, first ka columns) | A2 (column-major)]
+  const double* A;
+  const double* A2;
+  const double* B;
+  double* C;
+  int m, n, k, lda, lda2, ka, ka_valid, ldb, ldc;
+};
+
 struct TriDesc {  // inverses of the 128 x 128 diagonal blocks of U of an n x n LU
   const double* LU;
   double* out;

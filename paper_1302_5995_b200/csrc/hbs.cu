@@ -48,6 +48,7 @@ cudaError_t launch_gemm_desc(const GemmDesc* d_descs, int count, int max_tiles, 
                              cudaStream_t st, bool a_aligned, bool allow_big = true);
 cudaError_t launch_gemm_desc_tc(const GemmDesc* d_descs, int count, int max_tiles, int kmax, double alpha, double beta,
                                 cudaStream_t st);
+cudaError_t launch_gemm_desc2(const GemmDesc2* d_descs, int count, int max_tiles, bool tc, cudaStream_t st);
 int gemm_tiles(int m, int n);
 cudaError_t launch_copy2d_batched(const void* d_descs, int count, cudaStream_t st);
 
@@ -618,12 +619,12 @@ namespace {
 // ld = align2(nrhs)), so every GEMM has the batch as its M dimension (full
 // 128-row DMMA tiles at large batch) and the factors as small right-hand
 // operands. Every node owns a column group of the workspace:
-//   leaf t:   [ x_t (s, padded to even) | y-hat_t (kp_t) ]
+//   leaf t:   [ y-hat_t (kp_t) ]   (x_t is read straight from X, transposed on load)
 //   parent t: [ x-hat_l (kp_l) | x-hat_r (kp_r) | y-hat_t (kp_t) ]   (root: no y-hat)
 // so that each step of hbs.cpp:187-232 is ONE GEMM with a contiguous A:
-//   up:    x-hat_t^T = group_t[:, :inner] V_t                  (into the parent's group)
+//   up:    x-hat_t^T = group_t[:, :inner] V_t   (leaves: x_t^T V_t)  (into the parent's group)
 //   down:  y-hat_c^T = group_t [B_t^T; U_t^T][:, cols of c]    (into child c's group)
-//   leaf:  y_t^T     = group_t [D_t^T; U_t^T]
+//   leaf:  y_t       = ([x_t^T | y-hat_t^T] [D_t^T; U_t^T])^T, stored transposed
 // Factors are repacked once (ranks padded to even with zero rows/columns, all
 // operand columns 16-byte aligned).
 void pack_for_apply(HbsDev& H, cudaStream_t st) {
@@ -643,13 +644,13 @@ void pack_for_apply(HbsDev& H, cudaStream_t st) {
   int64_t cols = 0, outc = 0;
   for (int t = 0; t < nn; ++t) {
     if (H.is_leaf(t)) {
-      P.inner[t] = int(align2(H.node_size(t)));  // x columns incl. the zero pad column
+      P.inner[t] = int((H.node_size(t) + 15) & ~int64_t(15));  // x columns read from X (ka, multiple of 16)
       P.pb[t] = int(outc);
       outc += align2(H.node_size(t));
     } else {
       P.inner[t] = P.kp[H.nodes[t].left] + P.kp[H.nodes[t].right];
     }
-    P.gw[t] = P.inner[t] + P.kp[t];
+    P.gw[t] = H.is_leaf(t) ? P.kp[t] : P.inner[t] + P.kp[t];  // leaves: x is read from X itself
     P.go[t] = int(cols);
     cols += P.gw[t];
   }
@@ -657,7 +658,7 @@ void pack_for_apply(HbsDev& H, cudaStream_t st) {
   P.out_cols = std::max<int64_t>(outc, 2);
   size_t tot = 0;
   for (int t = 0; t < nn; ++t) {
-    const int64_t in = P.inner[t], li = std::max<int64_t>(in, 2), lw = std::max<int64_t>(P.gw[t], 2);
+    const int64_t in = P.inner[t], li = std::max<int64_t>(in, 2), lw = std::max<int64_t>(in + P.kp[t], 2);
     const int64_t ncol = H.is_leaf(t) ? H.node_size(t) : in;
     if (t != 0) tot += size_t(li) * P.kp[t];  // V
     tot += size_t(lw) * ncol;                 // W
@@ -690,7 +691,7 @@ void pack_for_apply(HbsDev& H, cudaStream_t st) {
       o += size_t(li) * kp;
       pd.push_back(PackDesc{H.V[t], P.V[t], lsrc, li, in, kp, i1, ip1, i2, k, kp, 0, 0});
     }
-    const int lw = std::max(P.gw[t], 2);
+    const int lw = std::max(in + kp, 2);  // W rows: [D^T or B^T (inner); U^T (kp)]
     P.W[t] = base + o;
     P.ldW[t] = lw;
     o += size_t(lw) * ncol;
@@ -756,13 +757,16 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
     return P.go[p] + (H.nodes[p].left == c ? 0 : P.kp[H.nodes[p].left]);
   };
 
+  auto yhat_slot = [&](int c) { return P.go[c] + (H.is_leaf(c) ? 0 : P.inner[c]); };
+
   struct Phase {
-    int kind;  // 0 GEMM (alpha 1, beta 0), 2 transpose, 3 GEMM with C stored transposed
+    int kind;  // 0 GEMM, 3 GEMM with C stored transposed, 4 two-source GEMM, 5 two-source with C transposed
     size_t off;
-    int count, tiles, kmax;
+    int count, tiles;
+    int kmax;
   };
   std::vector<GemmDesc> gd;
-  std::vector<TransDesc> td;
+  std::vector<GemmDesc2> gd2;
   std::vector<Phase> ph;
   auto add_gemm = [&](std::vector<GemmDesc>&& v, int kind = 0) {
     int tiles = 0, kmax = 0;
@@ -777,30 +781,36 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
     ph.push_back(Phase{kind, gd.size(), int(keep.size()), tiles, kmax});
     gd.insert(gd.end(), keep.begin(), keep.end());
   };
-  auto add_trans = [&](std::vector<TransDesc>&& v) {
+  auto add_gemm2 = [&](std::vector<GemmDesc2>&& v, int kind) {
     int tiles = 0;
-    for (const auto& d : v) tiles = std::max(tiles, ((d.m + 31) / 32) * ((d.n + 31) / 32));
-    if (v.empty() || tiles == 0) return;
-    ph.push_back(Phase{2, td.size(), int(v.size()), tiles, 0});
-    td.insert(td.end(), v.begin(), v.end());
+    std::vector<GemmDesc2> keep;
+    for (const auto& d : v)
+      if (d.m > 0 && d.n > 0 && d.k > 0) {
+        keep.push_back(d);
+        tiles = std::max(tiles, gemm_tiles(d.m, d.n));
+      }
+    if (keep.empty()) return;
+    ph.push_back(Phase{kind, gd2.size(), int(keep.size()), tiles, 0});
+    gd2.insert(gd2.end(), keep.begin(), keep.end());
   };
-  // x^T into the leaf groups
-  {
-    std::vector<TransDesc> t;
-    for (int n = 0; n < nn; ++n)
-      if (H.is_leaf(n))
-        t.push_back(TransDesc{dX + H.nodes[n].begin, col(P.go[n]), int(ldx), L, int(H.node_size(n)), int(nrhs)});
-    add_trans(std::move(t));
-  }
   const int R = H.height[0];
-  // upward: x-hat_t^T = group_t[:, :inner] V_t (leaves: the s real columns)
+  // upward: x-hat_t^T = group_t[:, :inner] V_t; leaves: x_t^T V_t with x_t read
+  // transposed straight from X (no transpose pass)
   for (int r = 0; r < R; ++r) {
     std::vector<GemmDesc> g;
+    std::vector<GemmDesc2> g2;
     for (int t = 1; t < nn; ++t) {
       if (H.height[t] != r || P.kp[t] == 0) continue;
-      const int K = H.is_leaf(t) ? int(H.node_size(t)) : P.inner[t];
-      g.push_back(GemmDesc{col(P.go[t]), P.V[t], col(xhat_slot(t)), int(nrhs), P.kp[t], K, L, P.ldV[t], L});
+      if (H.is_leaf(t)) {
+        const int s = int(H.node_size(t)), xin = P.inner[t];
+        g2.push_back(GemmDesc2{dX + H.nodes[t].begin, nullptr, P.V[t], col(xhat_slot(t)), int(nrhs), P.kp[t], xin,
+                               int(ldx), 0, xin, s, P.ldV[t], L});
+      } else {
+        g.push_back(GemmDesc{col(P.go[t]), P.V[t], col(xhat_slot(t)), int(nrhs), P.kp[t], P.inner[t], L, P.ldV[t],
+                             L});
+      }
     }
+    add_gemm2(std::move(g2), 4);
     add_gemm(std::move(g));
   }
   // downward: y-hat_c^T = group_t [B_t^T; U_t^T][:, cols of c], one GEMM per child
@@ -812,29 +822,31 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
       const int K = P.gw[t];
       if (P.inner[t] == 0) continue;
       if (P.kp[l] > 0)
-        g.push_back(GemmDesc{col(P.go[t]), P.W[t], col(P.go[l] + P.inner[l]), int(nrhs), P.kp[l], K, L, P.ldW[t], L});
+        g.push_back(GemmDesc{col(P.go[t]), P.W[t], col(yhat_slot(l)), int(nrhs), P.kp[l], K, L, P.ldW[t], L});
       if (P.kp[rr] > 0)
-        g.push_back(GemmDesc{col(P.go[t]), P.W[t] + size_t(P.kp[l]) * P.ldW[t], col(P.go[rr] + P.inner[rr]), int(nrhs),
+        g.push_back(GemmDesc{col(P.go[t]), P.W[t] + size_t(P.kp[l]) * P.ldW[t], col(yhat_slot(rr)), int(nrhs),
                              P.kp[rr], K, L, P.ldW[t], L});
     }
     add_gemm(std::move(g));
   }
-  // leaves: y_t = (group_t [D_t^T; U_t^T])^T, stored transposed straight into Y
+  // leaves: y_t = ([x_t^T | y-hat_t^T] [D_t^T; U_t^T])^T, x_t read transposed from
+  // X, y stored transposed straight into Y
   {
-    std::vector<GemmDesc> g;
+    std::vector<GemmDesc2> g2;
     for (int n = 0; n < nn; ++n) {
       if (!H.is_leaf(n)) continue;
-      const int s = int(H.node_size(n));
-      g.push_back(GemmDesc{col(P.go[n]), P.W[n], dY + H.nodes[n].begin, int(nrhs), s, P.gw[n], L, P.ldW[n], int(ldy)});
+      const int s = int(H.node_size(n)), xin = P.inner[n];
+      g2.push_back(GemmDesc2{dX + H.nodes[n].begin, col(P.go[n]), P.W[n], dY + H.nodes[n].begin, int(nrhs), s,
+                             xin + P.kp[n], int(ldx), L, xin, s, P.ldW[n], int(ldy)});
     }
-    add_gemm(std::move(g), 3);  // transposed-C GEMM
+    add_gemm2(std::move(g2), 5);
   }
-  // one upload (GEMM descriptors, then transposes), then the launches
-  const size_t gbytes = gd.size() * sizeof(GemmDesc), tbytes = td.size() * sizeof(TransDesc);
-  const size_t tb_off = (gbytes + 255) & ~size_t(255);
-  std::vector<unsigned char> host(tb_off + tbytes);
+  // one upload (both descriptor kinds), then the launches
+  const size_t gbytes = gd.size() * sizeof(GemmDesc), g2bytes = gd2.size() * sizeof(GemmDesc2);
+  const size_t g2_off = (gbytes + 255) & ~size_t(255);
+  std::vector<unsigned char> host(g2_off + g2bytes);
   if (gbytes) std::memcpy(host.data(), gd.data(), gbytes);
-  if (tbytes) std::memcpy(host.data() + tb_off, td.data(), tbytes);
+  if (g2bytes) std::memcpy(host.data() + g2_off, gd2.data(), g2bytes);
   if (host.size() > H.desc_bytes) {
     if (H.d_desc) cudaFree(H.d_desc);
     H.d_desc = nullptr;
@@ -844,9 +856,9 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
   }
   HCK(cudaMemcpyAsync(H.d_desc, host.data(), host.size(), cudaMemcpyHostToDevice, st));
   const GemmDesc* dg = static_cast<const GemmDesc*>(H.d_desc);
-  const TransDesc* dt = reinterpret_cast<const TransDesc*>(static_cast<unsigned char*>(H.d_desc) + tb_off);
+  const GemmDesc2* dg2 = reinterpret_cast<const GemmDesc2*>(static_cast<unsigned char*>(H.d_desc) + g2_off);
   for (const Phase& f : ph) {
-    if (f.kind == 2) HCK(launch_transpose_batched(dt + f.off, f.count, f.tiles, st));
+    if (f.kind == 4 || f.kind == 5) HCK(launch_gemm_desc2(dg2 + f.off, f.count, f.tiles, f.kind == 5, st));
     else if (f.kind == 3) HCK(launch_gemm_desc_tc(dg + f.off, f.count, f.tiles, f.kmax, 1.0, 0.0, st));
     else  // 128 x 64 tiles: the short reductions (K = leaf or rank) measured 20 % faster than 128 x 128
       HCK(launch_gemm_desc(dg + f.off, f.count, f.tiles, f.kmax, 1.0, 0.0, st, true, false));

@@ -28,10 +28,16 @@ struct GemmSmem {
 // UPD (C -= A*B) preloads the C tile into the accumulators before the K loop
 // (its latency overlaps the first A/B stage) and feeds -A to the DMMA, so the
 // epilogue is a plain store. Requires 16-byte aligned B columns.
-template <int BK, bool A16 = true, bool UPD = false, bool TC = false>
+// AT (two-source A, the HBS apply's leaf steps): the first ka columns of A
+// come from A stored row-major (A(r, c) = A[c + r lda]: the vectors X read
+// transposed, no transpose pass), the rest from the column-major A2 (lda2);
+// ka must be a multiple of BK.
+template <int BK, bool A16 = true, bool UPD = false, bool TC = false, bool AT = false>
 __device__ __forceinline__ void gemm_tile(const double* __restrict__ A, int lda, const double* __restrict__ B,
                                           int ldb, double* C, int ldc, int m, int n, int k, int tm, int tn,
-                                          double alpha, double beta, GemmSmem<BK>& sm) {
+                                          double alpha, double beta, GemmSmem<BK>& sm,
+                                          const double* __restrict__ A2 = nullptr, int lda2 = 0, int ka = 0,
+                                          int ka_valid = 0) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tig = lane & 3;
   const int wm0 = (warp % (GBM / GWM)) * GWM, wn0 = (warp / (GBM / GWM)) * GWN;
@@ -42,7 +48,32 @@ __device__ __forceinline__ void gemm_tile(const double* __restrict__ A, int lda,
     const int kb0 = kt * BK;
     // A: BK columns x GBM rows, 2-double chunks along rows (1-double chunks
     // when A's columns are only 8-byte aligned)
-    if constexpr (A16) {
+    if (AT && kb0 < ka) {
+      // row-major source: BK consecutive k of one row per BK threads (coalesced),
+      // columns >= ka_valid of the first segment are zero (odd leaf sizes)
+      constexpr int ACH = BK * GBM;
+#pragma unroll
+      for (int c = tid; c < ACH; c += GTHREADS) {
+        const int rr = c / BK, kk = c % BK;
+        const int gr = row0 + rr, gc = kb0 + kk;
+        const bool ok = gc < ka_valid && gr < m;
+        cp_async8(&sm.a[stage][kk][rr], ok ? A + gc + (long long)gr * lda : A, ok ? 8 : 0);
+      }
+    } else if (AT) {
+      constexpr int ACH = BK * GBM / 2;
+#pragma unroll
+      for (int c = tid; c < ACH; c += GTHREADS) {
+        const int kk = c / (GBM / 2), rr = (c % (GBM / 2)) * 2;
+        const int gr = row0 + rr, gc = kb0 + kk;
+        int bytes = 0;
+        const double* src = A2;
+        if (gc < k && gr < m) {
+          bytes = (m - gr) >= 2 ? 16 : 8;
+          src = A2 + gr + (long long)(gc - ka) * lda2;
+        }
+        cp_async16(&sm.a[stage][kk][rr], src, bytes);
+      }
+    } else if constexpr (A16) {
       constexpr int ACH = BK * GBM / 2;
 #pragma unroll
       for (int c = tid; c < ACH; c += GTHREADS) {
@@ -161,6 +192,19 @@ __global__ void __launch_bounds__(GTHREADS) gemm_desc_kernel(const GemmDesc* __r
   // B columns are always 16-byte aligned; A only when the launcher says so
   gemm_tile<BK, A16, UPD, TC>(d.A, d.lda, d.B, d.ldb, d.C, d.ldc, d.m, d.n, d.k, t % tiles_m, t / tiles_m, alpha,
                               beta, sm);
+}
+
+// Two-source A (see gemm_tile AT), C stored transposed or not.
+template <int BK, bool TC>
+__global__ void __launch_bounds__(GTHREADS) gemm_desc2_kernel(const GemmDesc2* __restrict__ descs) {
+  extern __shared__ __align__(16) unsigned char gsm_raw[];
+  GemmSmem<BK>& sm = *reinterpret_cast<GemmSmem<BK>*>(gsm_raw);
+  const GemmDesc2 d = descs[blockIdx.y];
+  const int tiles_m = (d.m + GBM - 1) / GBM, tiles_n = (d.n + GBN - 1) / GBN;
+  const int t = blockIdx.x;
+  if (t >= tiles_m * tiles_n) return;
+  gemm_tile<BK, true, false, TC, true>(d.A, d.lda, d.B, d.ldb, d.C, d.ldc, d.m, d.n, d.k, t % tiles_m, t / tiles_m,
+                                       1.0, 0.0, sm, d.A2, d.lda2, d.ka, d.ka_valid);
 }
 
 // ---- large-tile variant: 128 x 128 CTA tile, 8 warps of 64 x 32 (16 DMMA per
@@ -408,6 +452,22 @@ cudaError_t launch_gemm_desc_tc(const GemmDesc* d_descs, int count, int max_tile
     gemm_desc_kernel<16, false, true, true><<<grid, GTHREADS, sizeof(GemmSmem<16>), st>>>(d_descs, alpha, beta);
   else
     gemm_desc_kernel<8, false, true, true><<<grid, GTHREADS, sizeof(GemmSmem<8>), st>>>(d_descs, alpha, beta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gemm_desc2(const GemmDesc2* d_descs, int count, int max_tiles, bool tc, cudaStream_t st) {
+  if (count <= 0 || max_tiles <= 0) return cudaSuccess;
+  static const cudaError_t attr = [] {
+    cudaError_t e = cudaFuncSetAttribute(gemm_desc2_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         sizeof(GemmSmem<16>));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(gemm_desc2_kernel<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                sizeof(GemmSmem<16>));
+  }();
+  if (attr != cudaSuccess) return attr;
+  dim3 grid(max_tiles, count);
+  if (tc) gemm_desc2_kernel<16, true><<<grid, GTHREADS, sizeof(GemmSmem<16>), st>>>(d_descs);
+  else gemm_desc2_kernel<16, false><<<grid, GTHREADS, sizeof(GemmSmem<16>), st>>>(d_descs);
   return cudaGetLastError();
 }
 
