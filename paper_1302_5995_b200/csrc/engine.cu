@@ -1736,11 +1736,10 @@ int dtn_gpu_build_accel(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* o
       const int64_t m = op->nb;
       std::vector<double> ones(size_t(m), 1.0);
       std::vector<double> y(static_cast<size_t>(m), 0.0);
-      double* d = nullptr;
-      CK(cudaMalloc(&d, size_t(m) * 16));
+      double* d = static_cast<double*>(pool_alloc(size_t(m) * 16));
       struct F {
         double* p;
-        ~F() { cudaFree(p); }
+        ~F() { pool_free(p); }
       } f{d};
       cudaStream_t st = ctx->stream;
       CK(cudaMemcpyAsync(d, ones.data(), size_t(m) * 8, cudaMemcpyHostToDevice, st));

@@ -36,13 +36,84 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <unordered_map>
 #include <stdexcept>
 
 #include "common.cuh"
 #include "hbs.hpp"
 
 namespace dtnb {
+
+// Device memory of the compressed engine comes from a per-device caching pool:
+// cudaMalloc/cudaFree next to a large resident build (a 100+ GB plan arena)
+// were measured to stall for tens of ms at random, and cudaFree synchronises
+// the device. Freed blocks are kept (best fit, at most 2x the request + 1 MB)
+// and returned to the driver only when an allocation fails.
+namespace {
+struct DevPool {
+  std::mutex m;
+  std::multimap<size_t, void*> free_;
+  std::unordered_map<void*, size_t> live_;
+};
+DevPool& dev_pool(int device) {
+  static DevPool pools[64];
+  return pools[device & 63];
+}
+}  // namespace
+
+void* pool_alloc(size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  DevPool& P = dev_pool(dev);
+  bytes = (std::max<size_t>(bytes, 256) + 255) & ~size_t(255);
+  {
+    std::lock_guard<std::mutex> lk(P.m);
+    auto it = P.free_.lower_bound(bytes);
+    if (it != P.free_.end() && it->first <= 2 * bytes + (size_t(1) << 20)) {
+      void* p = it->second;
+      P.live_[p] = it->first;
+      P.free_.erase(it);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) {  // give the cached blocks back and retry once
+    (void)cudaGetLastError();
+    std::lock_guard<std::mutex> lk(P.m);
+    for (auto& kv : P.free_) cudaFree(kv.second);
+    P.free_.clear();
+    e = cudaMalloc(&p, bytes);
+  }
+  if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e) + " (pool_alloc)");
+  std::lock_guard<std::mutex> lk(P.m);
+  P.live_[p] = bytes;
+  return p;
+}
+
+void pool_free(void* p) {
+  if (!p) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  DevPool& P = dev_pool(dev);
+  std::lock_guard<std::mutex> lk(P.m);
+  auto it = P.live_.find(p);
+  if (it == P.live_.end()) {  // not from the pool
+    cudaFree(p);
+    return;
+  }
+  P.free_.insert({it->second, p});
+  P.live_.erase(it);
+}
+
+namespace {
+template <class T>
+void pmalloc(T** p, size_t bytes) {
+  *p = static_cast<T*>(pool_alloc(bytes));
+}
+}  // namespace
 
 cudaError_t launch_gemm_desc(const GemmDesc* d_descs, int count, int max_tiles, int kmax, double alpha, double beta,
                              cudaStream_t st, bool a_aligned, bool allow_big = true);
@@ -67,14 +138,14 @@ struct DevBuf {  // growable device scratch
   void* p = nullptr;
   size_t cap = 0;
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) pool_free(p);
   }
   void* get(size_t bytes) {
     if (bytes > cap) {
-      if (p) cudaFree(p);
+      if (p) pool_free(p);
       p = nullptr;
       cap = 0;
-      HCK(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+      pmalloc(&p, std::max<size_t>(bytes, 256));
       cap = std::max<size_t>(bytes, 256);
     }
     return p;
@@ -143,9 +214,9 @@ struct Scratch {
     if (int(slot.size()) <= i) slot.resize(i + 1, {nullptr, 0});
     auto& e = slot[i];
     if (e.second < bytes) {
-      if (e.first) cudaFree(e.first);
+      if (e.first) pool_free(e.first);
       e = {nullptr, 0};
-      HCK(cudaMalloc(&e.first, bytes));
+      pmalloc(&e.first, bytes);
       e.second = bytes;
     }
     return e.first;
@@ -165,7 +236,7 @@ struct Arena {
     if (doubles > left) {
       const size_t sz = std::max(doubles, chunk);
       void* p = nullptr;
-      HCK(cudaMalloc(&p, sz * 8));
+      pmalloc(&p, sz * 8);
       H.buffers.push_back(p);
       cur = static_cast<double*>(p);
       left = sz;
@@ -244,10 +315,10 @@ std::vector<HbsTreeNode> hbs_index_tree(int64_t M, int64_t leaf_cap, int* depth)
 
 HbsDev::~HbsDev() {
   if (device >= 0) cudaSetDevice(device);
-  for (void* p : buffers) cudaFree(p);
-  if (pk.buf) cudaFree(pk.buf);
-  if (ws) cudaFree(ws);
-  if (d_desc) cudaFree(d_desc);
+  for (void* p : buffers) pool_free(p);
+  if (pk.buf) pool_free(pk.buf);
+  if (ws) pool_free(ws);
+  if (d_desc) pool_free(d_desc);
 }
 
 int64_t HbsDev::max_rank() const {
@@ -291,7 +362,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
   if (nn == 1) {  // stored densely (hbs.cpp:75-78)
     H.rows[0] = int(M);
     double* d = nullptr;
-    HCK(cudaMalloc(&d, size_t(H.ld(0)) * M * 8));
+    pmalloc(&d, size_t(H.ld(0)) * M * 8);
     H.buffers.push_back(d);
     H.D[0] = d;
     copy_batch(dbuf, {CopyDesc{dH, d, int(ldh), H.ld(0), int(M), int(M)}}, st);
@@ -305,7 +376,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
   struct Frees {
     std::vector<void*> v;
     ~Frees() {
-      for (void* p : v) cudaFree(p);
+      for (void* p : v) pool_free(p);
     }
   } frees;
   Scratch& scr = scratch(H.device);
@@ -663,7 +734,7 @@ void pack_for_apply(HbsDev& H, cudaStream_t st) {
     if (t != 0) tot += size_t(li) * P.kp[t];  // V
     tot += size_t(lw) * ncol;                 // W
   }
-  HCK(cudaMalloc(&P.buf, tot * 8 + 64));
+  pmalloc(&P.buf, tot * 8 + 64);
   HCK(cudaMemsetAsync(P.buf, 0, tot * 8 + 64, st));
   double* base = static_cast<double*>(P.buf);
   size_t o = 0;
@@ -727,11 +798,11 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
     // Y = D X (the dense single-node case); B operand alignment: stage X
     const int64_t M = H.M, ld = align2(M);
     double* xs = nullptr;
-    HCK(cudaMalloc(&xs, size_t(ld) * nrhs * 8 + 8));
+    pmalloc(&xs, size_t(ld) * nrhs * 8 + 8);
     copy_batch(dbuf, {CopyDesc{dX, xs, int(ldx), int(ld), int(M), int(nrhs)}}, st);
     gemm_batch(dbuf, {GemmDesc{H.D[0], xs, dY, int(M), int(nrhs), int(M), H.ld(0), int(ld), int(ldy)}}, 1.0, 0.0,
                true, st);
-    cudaFree(xs);
+    pool_free(xs);
     return;
   }
   pack_for_apply(H, st);
@@ -739,10 +810,10 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
   const int64_t ldw = align2(nrhs);
   const size_t need = size_t(ldw) * size_t(P.cols);
   if (need > H.ws_doubles || ldw != H.ws_ld) {
-    if (H.ws) cudaFree(H.ws);
+    if (H.ws) pool_free(H.ws);
     H.ws = nullptr;
     H.ws_doubles = 0;
-    HCK(cudaMalloc(&H.ws, need * 8 + 64));
+    pmalloc(&H.ws, need * 8 + 64);
     // zero once: the pad columns of odd-sized leaves are read (times a zero
     // factor row) but never written
     HCK(cudaMemsetAsync(H.ws, 0, need * 8 + 64, st));
@@ -848,10 +919,10 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
   if (gbytes) std::memcpy(host.data(), gd.data(), gbytes);
   if (g2bytes) std::memcpy(host.data() + g2_off, gd2.data(), g2bytes);
   if (host.size() > H.desc_bytes) {
-    if (H.d_desc) cudaFree(H.d_desc);
+    if (H.d_desc) pool_free(H.d_desc);
     H.d_desc = nullptr;
     H.desc_bytes = 0;
-    HCK(cudaMalloc(&H.d_desc, host.size()));
+    pmalloc(&H.d_desc, host.size());
     H.desc_bytes = host.size();
   }
   HCK(cudaMemcpyAsync(H.d_desc, host.data(), host.size(), cudaMemcpyHostToDevice, st));
@@ -988,7 +1059,7 @@ std::unique_ptr<HbsDev> hbs_deserialize(const uint8_t* data, size_t size, cudaSt
     if (!leaf) matrix();
   }
   double* buf = nullptr;
-  HCK(cudaMalloc(&buf, total * 8 + 8));
+  pmalloc(&buf, total * 8 + 8);
   H.buffers.push_back(buf);
   size_t o = 0, m = 0;
   auto place = [&](double*& dst) {
@@ -1054,7 +1125,7 @@ std::unique_ptr<HbsDev> hbs_invert(const HbsDev& H, cudaStream_t st) {
   struct Frees {
     std::vector<void*> v;
     ~Frees() {
-      for (void* p : v) cudaFree(p);
+      for (void* p : v) pool_free(p);
     }
   } frees;
   // all factor storage in one allocation, per-level work in one reused buffer
@@ -1076,7 +1147,7 @@ std::unique_ptr<HbsDev> hbs_invert(const HbsDev& H, cudaStream_t st) {
   }
   Arena arena(R, keep_all + 64);
   double* work_buf = nullptr;
-  HCK(cudaMalloc(&work_buf, (work_max + dhat_all + 64) * 8));
+  pmalloc(&work_buf, (work_max + dhat_all + 64) * 8);
   frees.v.push_back(work_buf);
   bool dhat_taken = false;
   auto dalloc = [&](size_t doubles, bool keep) {
@@ -1089,7 +1160,7 @@ std::unique_ptr<HbsDev> hbs_invert(const HbsDev& H, cudaStream_t st) {
     return work_buf;
   };
   int* dinfo = nullptr;
-  HCK(cudaMalloc(&dinfo, size_t(nn) * sizeof(int) + 16));
+  pmalloc(&dinfo, size_t(nn) * sizeof(int) + 16);
   frees.v.push_back(dinfo);
   auto where = [&](int t) {
     return "node " + std::to_string(t) + " level " + std::to_string(H.nodes[t].level);

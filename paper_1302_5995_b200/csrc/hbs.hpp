@@ -78,6 +78,10 @@ cudaError_t launch_gj_inverse(const InvDesc* d_descs, int count, int max_s, cuda
 
 // IndexTree node (index_tree.hpp:12-22): contiguous range [begin, end),
 // preorder ids, children -1 for leaves.
+// per-device caching device allocator of the compressed engine (hbs.cu)
+void* pool_alloc(size_t bytes);
+void pool_free(void* p);
+
 struct HbsTreeNode {
   int64_t begin = 0, end = 0;
   int left = -1, right = -1, parent = -1, level = 0;
