@@ -40,6 +40,7 @@ unsigned panel_fallbacks_read_reset();
 cudaError_t launch_ring_dtn(const double*, int, const int*, const double*, int, double, double*, long long, cudaStream_t);
 cudaError_t launch_trsm_upper_ref(const void*, int, int, cudaStream_t);
 cudaError_t launch_gemm_desc(const GemmDesc*, int, int, int, double, double, cudaStream_t, bool, bool allow_big = true);
+cudaError_t launch_pivot_screen(const double*, const int*, int, int, int*, cudaStream_t);
 cudaError_t launch_perm_identity(const int*, int, int*, double*, int, cudaStream_t);
 cudaError_t launch_trsm_rows(const double*, int, double*, int, int, int, int, bool, cudaStream_t);
 cudaError_t launch_norm1(const double*, int, int, int, unsigned long long*, cudaStream_t);
@@ -156,6 +157,9 @@ struct PlanDev {
   TrsmDesc* d_root_trs = nullptr;
   double* d_tinv = nullptr;  // inverses of the 128 x 128 diagonal blocks of L and U
   double* h_pivstat = nullptr;  // pinned
+  int* d_chk = nullptr;         // per node: 1 checked for singular pivots, 2 only when G is built
+  int* d_bad = nullptr;         // lowest failing node id (INT_MAX: none)
+  int* h_bad = nullptr;         // pinned
   unsigned long long* h_norm = nullptr;
   std::vector<cudaEvent_t> ev_wave;
   cudaEvent_t ev_start = nullptr, ev_root = nullptr, ev_end = nullptr;
@@ -177,9 +181,10 @@ struct PlanDev {
     if (copy) cudaStreamDestroy(copy);
     for (void* p : std::initializer_list<void*>{d_nodes, d_pos, d_arena, d_piv, d_pivstat, d_lists, d_stencil, d_S, d_G,
                                                 d_perm, d_norm, d_inv_descs, d_W, d_LUp, d_tinv, d_root_trs, d_load_col, d_F, d_F_desc, d_bs_gemm,
-                                                d_bs_copy, d_tri, d_trs})
+                                                d_bs_copy, d_tri, d_trs, d_chk, d_bad})
       if (p) cudaFree(p);
     if (h_pivstat) cudaFreeHost(h_pivstat);
+    if (h_bad) cudaFreeHost(h_bad);
     if (h_norm) cudaFreeHost(h_norm);
   }
 
@@ -415,6 +420,18 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
       CK(cudaMemcpy(D->d_tri, D->h_tri.data(), D->h_tri.size() * sizeof(TriDesc), cudaMemcpyHostToDevice));
   }
   D->d_pivstat = dalloc<double>(2 * D->h_nodes.size());
+  {
+    std::vector<int> chk(D->h_nodes.size(), 0);
+    for (const Wave& wv : P.waves)
+      for (const auto* lst : {&wv.micro, &wv.small, &wv.blocked})
+        for (int id : *lst)
+          if (P.nodes[id].ni > 0) chk[size_t(id)] = 1;
+    if (size_t(D->root_lu_node) < chk.size()) chk[size_t(D->root_lu_node)] = 2;
+    D->d_chk = dalloc<int>(chk.size());
+    CK(cudaMemcpy(D->d_chk, chk.data(), chk.size() * sizeof(int), cudaMemcpyHostToDevice));
+    D->d_bad = dalloc<int>(1);
+    CK(cudaMallocHost(&D->h_bad, sizeof(int)));
+  }
   D->d_stencil = dalloc<double>(size_t(5 * D->nu));
   D->lds = int(align_up(nb, 8));
   D->d_S = dalloc<double>(size_t(D->lds) * nb);
@@ -1011,9 +1028,13 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
         CK(cudaStreamDestroy(cap));
         D->graph_want_G = int(want_G);
       }
+      const auto hl0 = std::chrono::steady_clock::now();
       CK(cudaEventRecord(D->ev_start, st));
       CK(cudaGraphLaunch(D->gexec, st));
       CK(cudaEventRecord(D->ev_end, st));
+      if (std::getenv("DTN_TRACE_BUILD"))
+        std::fprintf(stderr, "[build] graph launch (host) %.3f ms\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hl0).count());
     } else {
       enqueue_build(*D, st, want_G);
     }
@@ -1024,14 +1045,24 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
                            size_t(D->nb) * 8, size_t(D->nb), cudaMemcpyDeviceToHost, D->copy));
     }
     const size_t nstat = D->h_nodes.size();
-    CK(cudaMemcpyAsync(D->h_pivstat, D->d_pivstat, 2 * nstat * sizeof(double), cudaMemcpyDeviceToHost, st));
+    // screen on the device; the per-node statistics come back only when a block failed
+    CK(cudaMemsetAsync(D->d_bad, 0x7f, sizeof(int), st));
+    CK(launch_pivot_screen(D->d_pivstat, D->d_chk, int(nstat), want_G ? 1 : 0, D->d_bad, st));
+    CK(cudaMemcpyAsync(D->h_bad, D->d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
     if (want_G) CK(cudaMemcpyAsync(D->h_norm, D->d_norm, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    const auto hs0 = std::chrono::steady_clock::now();
     CK(cudaStreamSynchronize(st));
+    if (std::getenv("DTN_TRACE_BUILD"))
+      std::fprintf(stderr, "[build] wait for the device %.3f ms\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hs0).count());
     if (opts->export_S) CK(cudaStreamSynchronize(D->copy));
     CK(cudaGetLastError());
     // singular blocks, first failing node in build order (dense_nd.cpp:93-96, 175-180)
     const Plan& P = D->P;
-    for (const Wave& wv : P.waves)
+    const bool any_bad = *D->h_bad != 0x7f7f7f7f;
+    if (any_bad) CK(cudaMemcpy(D->h_pivstat, D->d_pivstat, 2 * nstat * sizeof(double), cudaMemcpyDeviceToHost));
+    if (any_bad)
+      for (const Wave& wv : P.waves)
       for (const auto* lst : {&wv.micro, &wv.small, &wv.blocked})
         for (int id : *lst) {
           const Node& nd = P.nodes[id];
@@ -1050,7 +1081,7 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
     op->has_G = want_G;
     if (want_G) {
       const int r = D->root_lu_node;
-      if (!pivots_ok(D->h_pivstat[2 * r], D->h_pivstat[2 * r + 1])) {
+      if (any_bad && !pivots_ok(D->h_pivstat[2 * r], D->h_pivstat[2 * r + 1])) {
         delete op;
         throw Singular("root Schur complement is singular [root]");
       }

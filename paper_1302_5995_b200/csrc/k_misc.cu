@@ -519,4 +519,25 @@ cudaError_t launch_copy2d(const double* src, int lds, double* dst, int ldd, int 
   return cudaGetLastError();
 }
 
+// Singular-block screen of a build (dense_nd.cpp:93-96, 175-180): the lowest
+// id of a checked node whose pivots fail pmin > pmax * 1e-300 (or are not
+// finite) -> *first_bad (INT_MAX when none), so the host reads 4 bytes instead
+// of every node's pivot statistics. chk: 1 = check, 2 = check when G is built.
+__global__ void pivot_screen_kernel(const double* __restrict__ pivstat, const int* __restrict__ chk, int n, int want_G,
+                                    int* first_bad) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int c = chk[i];
+    if (c == 0 || (c == 2 && !want_G)) continue;
+    const double pmin = pivstat[2 * i], pmax = pivstat[2 * i + 1];
+    if (!((pmin > pmax * 1e-300) && isfinite(pmax))) atomicMin(first_bad, i);
+  }
+}
+
+cudaError_t launch_pivot_screen(const double* pivstat, const int* chk, int n, int want_G, int* first_bad,
+                                cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  pivot_screen_kernel<<<std::min((n + 255) / 256, 1184), 256, 0, st>>>(pivstat, chk, n, want_G, first_bad);
+  return cudaGetLastError();
+}
+
 }  // namespace dtnb
