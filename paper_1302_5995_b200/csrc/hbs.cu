@@ -319,6 +319,7 @@ HbsDev::~HbsDev() {
   if (pk.buf) pool_free(pk.buf);
   if (ws) pool_free(ws);
   if (d_desc) pool_free(d_desc);
+  if (apply_graph) cudaGraphExecDestroy(apply_graph);
 }
 
 int64_t HbsDev::max_rank() const {
@@ -928,11 +929,40 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
   HCK(cudaMemcpyAsync(H.d_desc, host.data(), host.size(), cudaMemcpyHostToDevice, st));
   const GemmDesc* dg = static_cast<const GemmDesc*>(H.d_desc);
   const GemmDesc2* dg2 = reinterpret_cast<const GemmDesc2*>(static_cast<unsigned char*>(H.d_desc) + g2_off);
-  for (const Phase& f : ph) {
-    if (f.kind == 4 || f.kind == 5) HCK(launch_gemm_desc2(dg2 + f.off, f.count, f.tiles, f.kind == 5, st));
-    else if (f.kind == 3) HCK(launch_gemm_desc_tc(dg + f.off, f.count, f.tiles, f.kmax, 1.0, 0.0, st));
-    else  // 128 x 64 tiles: the short reductions (K = leaf or rank) measured 20 % faster than 128 x 128
-      HCK(launch_gemm_desc(dg + f.off, f.count, f.tiles, f.kmax, 1.0, 0.0, st, true, false));
+  auto launch_all = [&](cudaStream_t s2) {
+    for (const Phase& f : ph) {
+      if (f.kind == 4 || f.kind == 5) HCK(launch_gemm_desc2(dg2 + f.off, f.count, f.tiles, f.kind == 5, s2));
+      else if (f.kind == 3) HCK(launch_gemm_desc_tc(dg + f.off, f.count, f.tiles, f.kmax, 1.0, 0.0, s2));
+      else  // 128 x 64 tiles: the short reductions (K = leaf or rank) measured 20 % faster than 128 x 128
+        HCK(launch_gemm_desc(dg + f.off, f.count, f.tiles, f.kmax, 1.0, 0.0, s2, true, false));
+    }
+  };
+  // the launch sequence depends only on the tree, the ranks and nrhs: replay it as a
+  // graph (one launch instead of ~16) once captured for this batch size
+  static const bool graphs = std::getenv("DTN_HBS_NO_GRAPH") == nullptr;
+  if (graphs && st != nullptr) {
+    if (!(H.apply_graph && H.apply_graph_nrhs == nrhs && H.apply_graph_desc == H.d_desc)) {
+      if (H.apply_graph) cudaGraphExecDestroy(H.apply_graph);
+      H.apply_graph = nullptr;
+      cudaGraph_t g = nullptr;
+      HCK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      try {
+        launch_all(st);
+      } catch (...) {
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      HCK(cudaStreamEndCapture(st, &g));
+      const cudaError_t e = cudaGraphInstantiate(&H.apply_graph, g, 0);
+      cudaGraphDestroy(g);
+      HCK(e);
+      H.apply_graph_nrhs = nrhs;
+      H.apply_graph_desc = H.d_desc;
+    }
+    HCK(cudaGraphLaunch(H.apply_graph, st));
+  } else {
+    launch_all(st);
   }
   // the descriptor buffer is reused by the next call on this stream (stream order);
   // the host copy above is staged before cudaMemcpyAsync returns (pageable source)

@@ -121,6 +121,11 @@ struct HbsDev {
   int64_t ws_ld = 0;
   void* d_desc = nullptr;
   size_t desc_bytes = 0;
+  // the apply's launch sequence as a CUDA graph (valid for one batch size and
+  // descriptor buffer; the descriptors themselves are re-uploaded every call)
+  cudaGraphExec_t apply_graph = nullptr;
+  int64_t apply_graph_nrhs = -1;
+  const void* apply_graph_desc = nullptr;
   ~HbsDev();
   int64_t max_rank() const;
   uint64_t payload_bytes() const;
