@@ -17,6 +17,15 @@ struct NodeDev {
   long long rhs_off;  // body-load columns (nb x nloads, leading dimension rhs_ld)
   int rhs_ld;
   int ncols;          // blocked: columns of the assembled system (total + body-load columns)
+  int defer;          // blocked Schur merge whose boundary columns skip the LU's row moves and rank-kb
+                      // updates: Y = L^{-1} P M_ib is formed after the LU by blocked forward substitution
+};
+
+struct RowGatherDesc {  // dst(i, c) = src(perm[i], c), i < rows, c < cols (perm: arena piv ints)
+  const double* src;
+  double* dst;
+  long long perm_off;
+  int lds, ldd, rows, cols;
 };
 
 struct PosDev {  // == plan.hpp PosEntry

@@ -18,6 +18,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/dtn_gpu.h"
@@ -41,6 +42,7 @@ cudaError_t launch_ring_dtn(const double*, int, const int*, const double*, int, 
 cudaError_t launch_trsm_upper_ref(const void*, int, int, cudaStream_t);
 cudaError_t launch_gemm_desc(const GemmDesc*, int, int, int, double, double, cudaStream_t, bool, bool allow_big = true);
 cudaError_t launch_pivot_screen(const double*, const int*, int, int, int*, cudaStream_t);
+cudaError_t launch_row_gather(const RowGatherDesc*, int, const int*, cudaStream_t);
 cudaError_t launch_perm_identity(const int*, int, int*, double*, int, cudaStream_t);
 cudaError_t launch_trsm_rows(const double*, int, double*, int, int, int, int, bool, cudaStream_t);
 cudaError_t launch_norm1(const double*, int, int, int, unsigned long long*, cudaStream_t);
@@ -95,6 +97,11 @@ struct WaveLaunch {
   std::vector<int> bs_toff, bs_soff, bs_tiles1, bs_tiles2, bs_k, bs_cols;  // launch geometry per step
   std::vector<double> bs_flops;
   int copy_base = 0;                               // first CopyDesc of this wave
+  // deferred boundary columns (NodeDev::defer): copy out, row gather by the LU's
+  // permutation, then Y = L^{-1} (P M_ib) by 128-row blocks (unit-lower substitution + GEMM)
+  int fw_copy_off = 0, fw_cnt = 0, fw_gather_off = 0, fw_max_cols = 0;
+  std::vector<int> fw_toff, fw_goff, fw_n, fw_tiles, fw_k, fw_cols;
+  std::vector<double> fw_flops;
   int fin_off = 0, fin_tiles = 0, fin_k = 0;       // final GEMM S -= M_bi X
   bool fin_aligned = true;
   double fin_flops = 0.0;
@@ -138,6 +145,15 @@ struct PlanDev {
   std::vector<CopyDesc> h_bs_copy;
   std::vector<TriDesc> h_tri;
   std::vector<TrsmDesc> h_trs;
+  std::vector<CopyDesc> h_fw_copy;
+  std::vector<RowGatherDesc> h_fw_gather;
+  std::vector<TrsmDesc> h_fw_trs;
+  std::vector<GemmDesc> h_fw_gemm;
+  CopyDesc* d_fw_copy = nullptr;
+  RowGatherDesc* d_fw_gather = nullptr;
+  TrsmDesc* d_fw_trs = nullptr;
+  GemmDesc* d_fw_gemm = nullptr;
+  int64_t gtmp_off = 0, gtmp_doubles = 0;
   int subst_base = 0;
   TrsmDesc* d_trs = nullptr;
   GemmDesc* d_bs_gemm = nullptr;  // back-substitution / final GEMM descriptors (all waves)
@@ -181,7 +197,8 @@ struct PlanDev {
     if (copy) cudaStreamDestroy(copy);
     for (void* p : std::initializer_list<void*>{d_nodes, d_pos, d_arena, d_piv, d_pivstat, d_lists, d_stencil, d_S, d_G,
                                                 d_perm, d_norm, d_inv_descs, d_W, d_LUp, d_tinv, d_root_trs, d_load_col, d_F, d_F_desc, d_bs_gemm,
-                                                d_bs_copy, d_tri, d_trs, d_chk, d_bad})
+                                                d_bs_copy, d_tri, d_trs, d_chk, d_bad, d_fw_copy, d_fw_gather,
+                                                d_fw_trs, d_fw_gemm})
       if (p) cudaFree(p);
     if (h_pivstat) cudaFreeHost(h_pivstat);
     if (h_bad) cudaFreeHost(h_bad);
@@ -193,6 +210,8 @@ struct PlanDev {
                       d_piv,   d_pivstat, P.key.nloads,  d_load_col};
   }
 };
+
+double defer_min_work();
 
 std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
   auto D = std::make_unique<PlanDev>();
@@ -223,6 +242,7 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
     d.rhs_off = s.rhs_off;
     d.rhs_ld = s.rhs_ld;
     d.ncols = s.total + (s.blocked ? P.key.nloads : 0);
+    d.defer = 0;  // decided per wave below
   }
   D->ldlu = int(align_up(nb, 8));
   D->lu_off = align_up(P.arena_doubles, 32);
@@ -291,6 +311,13 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
     std::vector<TriDesc> td;
     std::vector<TrsmDesc> trs;
     std::vector<GemmDesc> gs;  // substitution variant's updates (appended after gd)
+    std::vector<CopyDesc> fwc;
+    std::vector<RowGatherDesc> fwg;
+    std::vector<TrsmDesc> fwt;
+    std::vector<GemmDesc> fwm;
+    int64_t gtmp_need = 0;
+    // the deferred columns' staging area sits after the root-LU region of the arena
+    D->gtmp_off = align_up(D->lu_off + int64_t(D->ldlu) * nb, 32);
     double* A0 = nullptr;  // descriptors hold absolute pointers into the arena (allocated below)
     (void)A0;
     for (size_t w = 0; w < P.waves.size(); ++w) {
@@ -306,6 +333,68 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
         maxblk = std::max(maxblk, (nd.ni + 127) / 128);
       }
       L.tri_blocks = maxblk;
+      // deferred boundary columns: M_ib -> temp (ni x ncy), gathered back by perm,
+      // then forward substitution by 128-row blocks (top down). Decided per wave by
+      // the boundary-column work of its rank-32 updates, sum of ni (ncols - ni)
+      {
+        double work = 0.0;
+        for (int id : wv.blocked) work += double(P.nodes[id].ni) * double(D->h_nodes[id].ncols - P.nodes[id].ni);
+        if (work >= defer_min_work())
+          for (int id : wv.blocked) D->h_nodes[id].defer = P.nodes[id].ni >= 256 ? 1 : 0;
+      }
+      {
+        int64_t toff = D->gtmp_off;
+        L.fw_copy_off = int(fwc.size());
+        L.fw_gather_off = int(fwg.size());
+        int fmax = 0;
+        for (int id : wv.blocked) {
+          const Node& nd = P.nodes[id];
+          if (!D->h_nodes[id].defer) continue;
+          const int64_t M = nd.m_off, ldm = nd.ldm;
+          const int ncy = nd.nb + P.key.nloads, ldt = int(align_up(nd.ni, 2));
+          fwc.push_back(CopyDesc{reinterpret_cast<const double*>(M + nd.ni * ldm), reinterpret_cast<double*>(toff),
+                                 int(ldm), ldt, nd.ni, ncy});
+          fwg.push_back(RowGatherDesc{reinterpret_cast<const double*>(toff), reinterpret_cast<double*>(M + nd.ni * ldm),
+                                      nd.piv_off, ldt, int(ldm), nd.ni, ncy});
+          toff += int64_t(ldt) * ncy;
+          ++L.fw_cnt;
+          fmax = std::max(fmax, (nd.ni + 127) / 128);
+          L.fw_max_cols = std::max(L.fw_max_cols, ncy);
+        }
+        gtmp_need = std::max(gtmp_need, toff - D->gtmp_off);
+        for (int t = 0; t < fmax; ++t) {
+          int cnt = 0, tiles = 0, kk = 0, mc = 0;
+          double fl = 0.0;
+          L.fw_toff.push_back(int(fwt.size()));
+          L.fw_goff.push_back(int(fwm.size()));
+          for (int id : wv.blocked) {
+            const Node& nd = P.nodes[id];
+            if (!D->h_nodes[id].defer) continue;
+            const int nblk = (nd.ni + 127) / 128;
+            if (t >= nblk) continue;
+            const int64_t M = nd.m_off, ldm = nd.ldm;
+            const int k0 = t * 128, k1 = std::min(nd.ni, k0 + 128), bk = k1 - k0;
+            const int ncy = nd.nb + P.key.nloads;
+            // Y_k <- L_kk^{-1} Y_k (unit lower), Y[k1:ni] -= L[k1:ni, k0:k1] Y_k
+            fwt.push_back(TrsmDesc{reinterpret_cast<const double*>(M + k0 + int64_t(k0) * ldm),
+                                   reinterpret_cast<double*>(M + k0 + nd.ni * ldm), int(ldm), int(ldm), bk, ncy});
+            fwm.push_back(GemmDesc{reinterpret_cast<const double*>(M + k1 + int64_t(k0) * ldm),
+                                   reinterpret_cast<const double*>(M + k0 + nd.ni * ldm),
+                                   reinterpret_cast<double*>(M + k1 + nd.ni * ldm), nd.ni - k1, ncy, bk, int(ldm),
+                                   int(ldm), int(ldm)});
+            tiles = std::max(tiles, gemm_tiles(std::max(nd.ni - k1, 1), ncy));
+            kk = std::max(kk, bk);
+            mc = std::max(mc, ncy);
+            fl += double(bk) * bk * ncy + 2.0 * double(nd.ni - k1) * ncy * bk;
+            ++cnt;
+          }
+          L.fw_n.push_back(cnt);
+          L.fw_tiles.push_back(tiles);
+          L.fw_k.push_back(kk);
+          L.fw_cols.push_back(mc);
+          L.fw_flops.push_back(fl);
+        }
+      }
       L.copy_base = int(cd.size());
       for (int t = 0; t < maxblk; ++t) {
         const int off = int(gd.size()), toff = int(trs.size()), soff = int(gs.size());
@@ -369,6 +458,11 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
       }
     }
     D->h_trs = std::move(trs);
+    D->h_fw_copy = std::move(fwc);
+    D->h_fw_gather = std::move(fwg);
+    D->h_fw_trs = std::move(fwt);
+    D->h_fw_gemm = std::move(fwm);
+    D->gtmp_doubles = gtmp_need;
     D->subst_base = int(gd.size());
     gd.insert(gd.end(), gs.begin(), gs.end());
     D->h_bs_gemm = std::move(gd);
@@ -386,7 +480,8 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
   CK(cudaMemcpy(D->d_pos, P.pos.data(), P.pos.size() * sizeof(PosDev), cudaMemcpyHostToDevice));
   D->d_lists = dalloc<int>(lists.size());
   CK(cudaMemcpy(D->d_lists, lists.data(), lists.size() * sizeof(int), cudaMemcpyHostToDevice));
-  D->d_arena = dalloc<double>(size_t(D->lu_off + int64_t(D->ldlu) * nb));
+  D->d_arena = dalloc<double>(size_t(D->gtmp_doubles > 0 ? D->gtmp_off + D->gtmp_doubles
+                                                           : D->lu_off + int64_t(D->ldlu) * nb));
   D->d_piv = dalloc<int>(size_t(P.piv_ints + align_up(nb, 4) + 260));
   if (P.key.nloads > 0) {
     D->d_load_col = dalloc<int>(size_t(D->nu));
@@ -406,6 +501,19 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
     for (auto& c : D->h_bs_copy) { c.src = rel(c.src); c.dst = rel(c.dst); }
     for (auto& t : D->h_tri) { t.LU = rel(t.LU); t.out = rel(t.out); }
     for (auto& t : D->h_trs) { t.U = rel(t.U); t.Y = rel(t.Y); }
+    for (auto& c : D->h_fw_copy) { c.src = rel(c.src); c.dst = rel(c.dst); }
+    for (auto& g : D->h_fw_gather) { g.src = rel(g.src); g.dst = rel(g.dst); }
+    for (auto& t : D->h_fw_trs) { t.U = rel(t.U); t.Y = rel(t.Y); }
+    for (auto& g : D->h_fw_gemm) { g.A = rel(g.A); g.B = rel(g.B); g.C = rel(g.C); }
+    auto upload_vec = [&](auto& h, auto*& d) {
+      if (h.empty()) return;
+      d = dalloc<std::remove_reference_t<decltype(h[0])>>(h.size());
+      CK(cudaMemcpy(d, h.data(), h.size() * sizeof(h[0]), cudaMemcpyHostToDevice));
+    };
+    upload_vec(D->h_fw_copy, D->d_fw_copy);
+    upload_vec(D->h_fw_gather, D->d_fw_gather);
+    upload_vec(D->h_fw_trs, D->d_fw_trs);
+    upload_vec(D->h_fw_gemm, D->d_fw_gemm);
     D->d_trs = dalloc<TrsmDesc>(D->h_trs.size());
     if (!D->h_trs.empty())
       CK(cudaMemcpy(D->d_trs, D->h_trs.data(), D->h_trs.size() * sizeof(TrsmDesc), cudaMemcpyHostToDevice));
@@ -519,6 +627,23 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
   return D;
 }
 
+// Waves whose rank-32 updates of the boundary columns add up to at least this
+// much work (sum of ni (ncols - ni)) defer those columns (NodeDev::defer): the
+// right-looking updates stream the whole ni x total block from HBM every step;
+// one blocked forward substitution after the LU (rank-128 GEMM updates, the
+// same arithmetic in the same order: bitwise-identical S) cuts that traffic 4x.
+// Lighter waves keep the look-ahead schedule (their boundary updates hide
+// behind the latency-bound panel chain; deferring measured slower there).
+// DTN_DEFER_MIN_WORK (0: never).
+double defer_min_work() {
+  static const double v = [] {
+    const char* e = std::getenv("DTN_DEFER_MIN_WORK");
+    const double x = e ? std::atof(e) : 3.2e7;
+    return x <= 0.0 ? 1e300 : x;
+  }();
+  return v;
+}
+
 bool use_subst() {  // default: substitution (DTN_BACKSUB_SUBST=0 selects the explicit block inverses)
   const char* e = std::getenv("DTN_BACKSUB_SUBST");
   return !(e && e[0] == '0');
@@ -613,7 +738,8 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
         double fp = 0.0, fr = 0.0, ft = 0.0;
         for (int i = 0; i < cnt; ++i) {
           const Node* ndp = hlst ? &P.nodes[hlst[i]] : nullptr;
-          const double ni = ndp ? ndp->ni : max_ni, tot = ndp ? ndp->total : max_total;
+          const double ni = ndp ? ndp->ni : max_ni;
+          const double tot = ndp ? (D.h_nodes[hlst[i]].defer ? ndp->ni : ndp->total) : max_total;
           if (k0 >= ni) continue;
           const double kbe = std::min<double>(kb, ni - k0), mn = tot - k0 - kbe, mr = ni - k0 - kbe;
           fp += (ni - k0) * kbe * kbe;
@@ -640,7 +766,8 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
       double fp = 0.0, fr = 0.0, fn_ = 0.0, fr_ = 0.0;
       for (int i = 0; i < cnt; ++i) {
         const Node* ndp = hlst ? &P.nodes[hlst[i]] : nullptr;
-        const double ni = ndp ? ndp->ni : max_ni, nbn = ndp ? ndp->nb : max_nb, tot = ndp ? ndp->total : max_total;
+        const double ni = ndp ? ndp->ni : max_ni, nbn = ndp ? ndp->nb : max_nb;
+        const double tot = ndp ? (D.h_nodes[hlst[i]].defer ? ndp->ni : ndp->total) : max_total;
         if (k0 >= ni) continue;
         const double kbe = std::min<double>(kb, ni - k0), mn = tot - k0 - kbe;
         const double mr = schur ? ni - k0 - kbe : mn;  // rows of the trailing update
@@ -697,7 +824,23 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
       double gb = 0.0;
       for (int i = 0; i < L.blk_cnt; ++i) gb += 16.0 * double(P.nodes[hlst[i]].total) * P.nodes[hlst[i]].total;
       run(K_GATHER, 0.0, gb, [&] { return launch_gather(a, lst, L.blk_cnt, L.blk_max_total, st); });
-      blocked_lu(lst, hlst, L.blk_cnt, L.blk_max_ni, L.blk_max_total, L.blk_max_nb, L.kb, false, true);
+      // deferred boundary columns need L in the final row order (P A = L U): the row
+      // moves of every step are then also applied to the factored columns (swap_left)
+      blocked_lu(lst, hlst, L.blk_cnt, L.blk_max_ni, L.blk_max_total, L.blk_max_nb, L.kb, L.fw_cnt > 0, true);
+      if (L.fw_cnt > 0) {  // deferred boundary columns: Y = L^{-1} P M_ib
+        run(K_COPY, 0.0, 0.0, [&] { return launch_copy2d_batched(D.d_fw_copy + L.fw_copy_off, L.fw_cnt, st); });
+        run(K_COPY, 0.0, 0.0,
+            [&] { return launch_row_gather(D.d_fw_gather + L.fw_gather_off, L.fw_cnt, D.d_piv, st); });
+        for (size_t t = 0; t < L.fw_n.size(); ++t) {
+          run(K_SUBST, 0.0, 0.0, [&] {
+            return launch_trsm_batched(D.d_fw_trs + L.fw_toff[t], L.fw_n[t], L.fw_cols[t], L.fw_k[t], true, st);
+          });
+          run(K_BACKSUB, L.fw_flops[t], 0.0, [&] {
+            return launch_gemm_desc(D.d_fw_gemm + L.fw_goff[t], L.fw_n[t], L.fw_tiles[t], L.fw_k[t], -1.0, 1.0, st,
+                                    true);
+          });
+        }
+      }
       // X = U^{-1} Y by 128-row blocks from the bottom: dtrsm-style
       // substitution on the diagonal blocks (default; as accurate as the
       // reference on the near-resonant configurations) or explicit block

@@ -768,7 +768,7 @@ __global__ void __launch_bounds__(RP_THREADS) rowpanel_kernel(KernelArgs args, c
   // skip_next: the next panel (fused prologue) owns columns [k1, k1 + min(kb, ni - k1))
   const int cs = k1 + (skip_next ? min(kb, max(nd.ni - k1, 0)) : 0);
   const int jbase = left ? (bx - ncoltiles) * RP_COLS : cs + bx * RP_COLS;
-  const int jend = left ? k0 : nd.ncols;
+  const int jend = left ? k0 : (nd.defer ? nd.ni : nd.ncols);  // deferred: interface columns only
   if (jbase >= jend) return;
   const int* mv = move_list(args, nd, k0);
   if (tid < 64) {

@@ -337,7 +337,8 @@ __global__ void __launch_bounds__(GTHREADS) trailing_update_kernel(KernelArgs ar
   // columns [k1 + c0, min(total, k1 + c1)) (look-ahead split)
   const int m = (iface_rows ? nd.ni : nd.total) - k1;
   // c0 < 0: start after the next panel's interface columns (fused into its prologue)
-  const int cb = k1 + (c0 >= 0 ? c0 : min(kb, max(nd.ni - k1, 0))), n = min(nd.ncols, k1 + c1) - cb;
+  const int cb = k1 + (c0 >= 0 ? c0 : min(kb, max(nd.ni - k1, 0)));
+  const int n = min(nd.defer ? nd.ni : nd.ncols, k1 + c1) - cb;  // deferred: interface columns only
   if (m <= 0 || n <= 0) return;
   const int tiles = (m + GBM - 1) / GBM, tiles_n = (n + GBN - 1) / GBN;
   const int t = blockIdx.x;

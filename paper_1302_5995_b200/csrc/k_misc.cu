@@ -540,4 +540,20 @@ cudaError_t launch_pivot_screen(const double* pivstat, const int* chk, int n, in
   return cudaGetLastError();
 }
 
+// Row permutation of the deferred boundary columns: dst(i, c) = src(perm[i], c)
+// (perm = the interface LU's running permutation, perm[pos] = original row).
+__global__ void row_gather_kernel(const RowGatherDesc* __restrict__ descs, const int* __restrict__ piv) {
+  const RowGatherDesc d = descs[blockIdx.y];
+  const int* perm = piv + d.perm_off;
+  for (int c = blockIdx.x; c < d.cols; c += gridDim.x)
+    for (int i = threadIdx.x; i < d.rows; i += blockDim.x)
+      d.dst[i + (long long)c * d.ldd] = d.src[perm[i] + (long long)c * d.lds];
+}
+
+cudaError_t launch_row_gather(const RowGatherDesc* d_descs, int count, const int* piv, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  row_gather_kernel<<<dim3(592, count), 256, 0, st>>>(d_descs, piv);
+  return cudaGetLastError();
+}
+
 }  // namespace dtnb
