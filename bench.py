@@ -336,6 +336,7 @@ def solve_cfg5(dtn, torch, ctx, dev, stream, rank, world, steps, warmup):
                        f"vectors of length {nb}, batch-sharded x{world}",
            "vectors_per_s": batch / (ms_c * 1e-3), "ms_per_batch": ms_c, "tflops": flops_c / (ms_c * 1e-3) / 1e12,
            "G_hbs_vs_dense_G": rel, "clocks": clk,
+           "hbm_GB_per_s": (8.0 * P + 16.0 * nb * mine) / (ms_c * 1e-3) / 1e9,
            "dense": {"workload": f"the same batch through the dense G ({nb}x{nb}, build {build_ms:.1f} ms untimed)",
                      "vectors_per_s": batch / (ms_d * 1e-3), "ms_per_batch": ms_d,
                      "tflops": flops_d / (ms_d * 1e-3) / 1e12}}
@@ -508,7 +509,14 @@ def run_b200(args, cfg, rank, world, local):
                   "merge_frac_fp64_peak": merge_tf / peak_tf if merge_tf else None,
                   "build_tflops_algorithmic": (stats["merge_flops"] + stats["inverse_flops"]) /
                   (stats["build_ms"] * 1e-3) / 1e12,
-                  "solve_vectors_per_s": None},
+                  "solve_vectors_per_s": None,
+                  # leaf phase against HBM (coefficients in + S out per reference leaf)
+                  "leaf_hbm": (lambda lb: {"bytes": lb, "GB_per_s": lb / (pst["leaf_ms"] * 1e-3) / 1e9,
+                                           "frac_hbm": lb / (pst["leaf_ms"] * 1e-3) / 1e9 / hbm,
+                                           "tflops": pst["leaf_flops"] / (pst["leaf_ms"] * 1e-3) / 1e12,
+                                           "note": "latency-bound chain of in-leaf eliminations (6 waves)"})(
+                      8.0 * (5 * cfg["leaf"] ** 2 + (4 * cfg["leaf"] - 4) ** 2) * (n_int // cfg["leaf"]) ** 2)
+                  if pst["leaf_ms"] > 0 else None},
         "kernels": {k: {"ms": round(v["ms"], 4), "launches": v["launches"],
                         "tflops": (v["flops"] / (v["ms"] * 1e-3) / 1e12) if v["ms"] > 0 and v["flops"] else None}
                     for k, v in ks.items() if v["launches"]},
@@ -526,6 +534,11 @@ def run_b200(args, cfg, rank, world, local):
     e1.record(stream)
     e1.synchronize()
     line["build"]["solve_vectors_per_s"] = reps * nvec / (e0.elapsed_time(e1) * 1e-3)
+    # the small-batch solve is HBM-bound: G (8 nb^2 bytes) streamed once per batch
+    sb = 8.0 * nb * nb + 16.0 * nb * nvec
+    line["build"]["solve_hbm"] = {"bytes_per_batch": sb,
+                                  "GB_per_s": sb / (e0.elapsed_time(e1) * 1e-3 / reps) / 1e9,
+                                  "frac_hbm": sb / (e0.elapsed_time(e1) * 1e-3 / reps) / 1e9 / hbm}
 
     if not args.no_solve:
         try:

@@ -43,6 +43,9 @@ cudaError_t launch_trsm_upper_ref(const void*, int, int, cudaStream_t);
 cudaError_t launch_gemm_desc(const GemmDesc*, int, int, int, double, double, cudaStream_t, bool, bool allow_big = true);
 cudaError_t launch_pivot_screen(const double*, const int*, int, int, int*, cudaStream_t);
 cudaError_t launch_row_gather(const RowGatherDesc*, int, const int*, cudaStream_t);
+cudaError_t launch_skinny_gemm(const double*, int, const double*, int, double*, int, int, int, int, double*,
+                               cudaStream_t);
+size_t skinny_work_doubles(int, int, int);
 cudaError_t launch_perm_identity(const int*, int, int*, double*, int, cudaStream_t);
 cudaError_t launch_trsm_rows(const double*, int, double*, int, int, int, int, bool, cudaStream_t);
 cudaError_t launch_norm1(const double*, int, int, int, unsigned long long*, cudaStream_t);
@@ -974,6 +977,8 @@ struct dtn_ctx {
   double* d_x = nullptr;
   double* d_y = nullptr;
   size_t stage_cap = 0;
+  double* d_skinny = nullptr;  // split-K partials of the small-batch apply
+  size_t skinny_cap = 0;
   GemmDesc* d_desc = nullptr;
 };
 
@@ -1066,6 +1071,7 @@ void dtn_gpu_destroy(dtn_ctx* ctx) {
   if (ctx->d_x) cudaFree(ctx->d_x);
   if (ctx->d_y) cudaFree(ctx->d_y);
   if (ctx->d_desc) cudaFree(ctx->d_desc);
+  if (ctx->d_skinny) pool_free(ctx->d_skinny);
   if (ctx->own) cudaStreamDestroy(ctx->own);
   delete ctx;
 }
@@ -1488,9 +1494,19 @@ int dtn_gpu_apply(const dtn_op* op, int which, const double* X, int64_t ldx, int
       dY = ctx->d_y;
       ldX = ldY = ldp;
     }
-    GemmDesc d{A, dX, dY, nb, int(batch), nb, lda, int(ldX), int(ldY)};
-    CK(cudaMemcpyAsync(ctx->d_desc, &d, sizeof(d), cudaMemcpyHostToDevice, st));
-    CK(launch_gemm_desc(ctx->d_desc, 1, gemm_tiles(nb, int(batch)), nb, 1.0, 0.0, st, true));
+    if (batch <= 32) {  // HBM-bound stream over the operator: split-K skinny product
+      const size_t wd = skinny_work_doubles(nb, nb, int(batch));
+      if (wd > ctx->skinny_cap) {
+        if (ctx->d_skinny) pool_free(ctx->d_skinny);
+        ctx->d_skinny = static_cast<double*>(pool_alloc(wd * 8));
+        ctx->skinny_cap = wd;
+      }
+      CK(launch_skinny_gemm(A, lda, dX, int(ldX), dY, int(ldY), nb, nb, int(batch), ctx->d_skinny, st));
+    } else {
+      GemmDesc d{A, dX, dY, nb, int(batch), nb, lda, int(ldX), int(ldY)};
+      CK(cudaMemcpyAsync(ctx->d_desc, &d, sizeof(d), cudaMemcpyHostToDevice, st));
+      CK(launch_gemm_desc(ctx->d_desc, 1, gemm_tiles(nb, int(batch)), nb, 1.0, 0.0, st, true));
+    }
     if (!aligned)
       CK(cudaMemcpy2DAsync(Y, size_t(ldy) * 8, dY, size_t(ldY) * 8, size_t(nb) * 8, size_t(batch),
                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));

@@ -472,6 +472,71 @@ cudaError_t launch_gemm_desc2(const GemmDesc2* d_descs, int count, int max_tiles
   return cudaGetLastError();
 }
 
+// ---- skinny products Y (m x n) = A (m x k) X (k x n), n <= 32: the small-batch
+// apply_dtn / apply_schur is a stream over A (HBM-bound), which a 128-row GEMM
+// tile grid of ceil(m / 128) CTAs cannot saturate. Split-K instead: CTA (row
+// block, K slice) keeps its rows' partial sums for all n columns in registers
+// (one row per thread, A read coalesced down the columns, the X slice in shared
+// memory), partials go to a workspace and a second kernel adds the slices in a
+// fixed order (deterministic).
+constexpr int SK_ROWS = 128, SK_KC = 64;
+
+template <int N>
+__global__ void __launch_bounds__(SK_ROWS) skinny_partial_kernel(const double* __restrict__ A, int lda,
+                                                                 const double* __restrict__ X, int ldx, int m, int k,
+                                                                 int n, double* __restrict__ work) {
+  __shared__ double xs[SK_KC][N];
+  const int r = blockIdx.x * SK_ROWS + threadIdx.x, s = blockIdx.y;
+  const int c0 = s * SK_KC, c1 = min(k, c0 + SK_KC);
+  for (int e = threadIdx.x; e < SK_KC * N; e += SK_ROWS) {
+    const int c = e / N, j = e % N;
+    xs[c][j] = (c0 + c < c1 && j < n) ? X[(c0 + c) + (long long)j * ldx] : 0.0;
+  }
+  __syncthreads();
+  if (r >= m) return;
+  double acc[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) acc[j] = 0.0;
+  const double* a = A + r + (long long)c0 * lda;
+#pragma unroll 16
+  for (int c = 0; c < c1 - c0; ++c) {
+    const double g = __ldg(a + (long long)c * lda);
+#pragma unroll
+    for (int j = 0; j < N; ++j) acc[j] = fma(g, xs[c][j], acc[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < N; ++j)
+    if (j < n) work[((long long)s * n + j) * m + r] = acc[j];
+}
+
+__global__ void skinny_reduce_kernel(const double* __restrict__ work, int slices, int m, int n, double* Y, int ldy) {
+  const long long total = (long long)m * n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int j = int(e / m), r = int(e - (long long)j * m);
+    double t = 0.0;
+    for (int s = 0; s < slices; ++s) t += work[((long long)s * n + j) * m + r];
+    Y[r + (long long)j * ldy] = t;
+  }
+}
+
+size_t skinny_work_doubles(int m, int k, int n) { return size_t((k + SK_KC - 1) / SK_KC) * size_t(n) * size_t(m); }
+
+cudaError_t launch_skinny_gemm(const double* A, int lda, const double* X, int ldx, double* Y, int ldy, int m, int k,
+                               int n, double* work, cudaStream_t st) {
+  if (m <= 0 || n <= 0) return cudaSuccess;
+  if (n > 32) return cudaErrorInvalidValue;
+  const int slices = (k + SK_KC - 1) / SK_KC;
+  const dim3 grid((m + SK_ROWS - 1) / SK_ROWS, slices);
+  if (n <= 4) skinny_partial_kernel<4><<<grid, SK_ROWS, 0, st>>>(A, lda, X, ldx, m, k, n, work);
+  else if (n <= 8) skinny_partial_kernel<8><<<grid, SK_ROWS, 0, st>>>(A, lda, X, ldx, m, k, n, work);
+  else if (n <= 16) skinny_partial_kernel<16><<<grid, SK_ROWS, 0, st>>>(A, lda, X, ldx, m, k, n, work);
+  else skinny_partial_kernel<32><<<grid, SK_ROWS, 0, st>>>(A, lda, X, ldx, m, k, n, work);
+  const long long total = (long long)m * n;
+  skinny_reduce_kernel<<<int(std::min<long long>((total + 255) / 256, 1184)), 256, 0, st>>>(work, slices, m, n, Y,
+                                                                                              ldy);
+  return cudaGetLastError();
+}
+
 // Columns [k1 + c0, k1 + c1) of the trailing block (c1 = INT_MAX: to the end).
 cudaError_t launch_trailing_update(const KernelArgs& args, const int* d_list, int count, int max_total, int k0, int kb,
                                    int c0, int c1, cudaStream_t st, int max_rows) {
