@@ -415,7 +415,7 @@ def run_b200(args, cfg, rank, world, local):
     value = args.steps * n_int ** 2 / (total_ms * 1e-3)
     if rank != 0:
         stats = {"launches": 0}
-    launches_per_step = stats["launches"] + 1
+    launches_per_step = stats["launches"] + (2 if nvec <= 32 else 1)  # + the apply (split-K: 2 kernels)
 
     # ---- e2e through the public API, host (pinned) buffers
     pin_st = torch.empty(op.stencil.shape, dtype=torch.float64, pin_memory=True).numpy()
