@@ -247,3 +247,20 @@ def test_dense_n4096_laplace_properties():
     assert asym <= 1e-13
     L, info = torch.linalg.cholesky_ex(0.5 * (S + S.t()))
     assert int(info) == 0
+
+
+@pytest.mark.parametrize("n", [4, 5, 6, 7, 9, 13])
+def test_tiny_and_ragged_grids(n):
+    """Smallest grids (n = 4: a 2 x 2 interior, one leaf, the no-interior case
+    of dense_nd.cpp:57-61 at the leaves below it) and odd sizes (ragged
+    partitions, grid.cpp:242-248): S against the brute-force Schur complement,
+    G S = I."""
+    for name in ("laplace", "random1"):
+        sol = gpu_build(name, n, 16, seed=4)
+        p = O.Problem(name, n, seed=4)
+        rb = O.Tree(n, 16).root()
+        assert np.array_equal(sol.boundary, rb["boundary"])
+        brute = O.brute_schur(p.dense_A(), rb["boundary"], rb["interior"])
+        assert O.rel_fro(sol.S_dense, brute) <= TOL, (name, n)
+        nb = len(sol.boundary)
+        assert np.abs(sol.G_dense @ sol.S_dense - np.eye(nb)).max() <= 1e-10, (name, n)
