@@ -378,17 +378,18 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
             const int64_t M = nd.m_off, ldm = nd.ldm;
             const int k0 = t * 128, k1 = std::min(nd.ni, k0 + 128), bk = k1 - k0;
             const int ncy = nd.nb + P.key.nloads;
-            // Y_k <- L_kk^{-1} Y_k (unit lower), Y[k1:ni] -= L[k1:ni, k0:k1] Y_k
+            // left-looking: Y_k -= L[k0:k1, 0:k0] Y[0:k0] (one GEMM, K = k0: the same
+            // subtractions in the same order as the right-looking block updates), then
+            // Y_k <- L_kk^{-1} Y_k (unit lower)
             fwt.push_back(TrsmDesc{reinterpret_cast<const double*>(M + k0 + int64_t(k0) * ldm),
                                    reinterpret_cast<double*>(M + k0 + nd.ni * ldm), int(ldm), int(ldm), bk, ncy});
-            fwm.push_back(GemmDesc{reinterpret_cast<const double*>(M + k1 + int64_t(k0) * ldm),
-                                   reinterpret_cast<const double*>(M + k0 + nd.ni * ldm),
-                                   reinterpret_cast<double*>(M + k1 + nd.ni * ldm), nd.ni - k1, ncy, bk, int(ldm),
-                                   int(ldm), int(ldm)});
-            tiles = std::max(tiles, gemm_tiles(std::max(nd.ni - k1, 1), ncy));
-            kk = std::max(kk, bk);
+            fwm.push_back(GemmDesc{reinterpret_cast<const double*>(M + k0), reinterpret_cast<const double*>(M + nd.ni * ldm),
+                                   reinterpret_cast<double*>(M + k0 + nd.ni * ldm), bk, ncy, k0, int(ldm), int(ldm),
+                                   int(ldm)});
+            tiles = std::max(tiles, gemm_tiles(bk, ncy));
+            kk = std::max(kk, k0);
             mc = std::max(mc, ncy);
-            fl += double(bk) * bk * ncy + 2.0 * double(nd.ni - k1) * ncy * bk;
+            fl += double(bk) * bk * ncy + 2.0 * double(bk) * ncy * k0;
             ++cnt;
           }
           L.fw_n.push_back(cnt);
@@ -835,12 +836,13 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
         run(K_COPY, 0.0, 0.0,
             [&] { return launch_row_gather(D.d_fw_gather + L.fw_gather_off, L.fw_cnt, D.d_piv, st); });
         for (size_t t = 0; t < L.fw_n.size(); ++t) {
+          if (t > 0)  // block 0 has no left part
+            run(K_BACKSUB, L.fw_flops[t], 0.0, [&] {
+              return launch_gemm_desc(D.d_fw_gemm + L.fw_goff[t], L.fw_n[t], L.fw_tiles[t], L.fw_k[t], -1.0, 1.0, st,
+                                      true);
+            });
           run(K_SUBST, 0.0, 0.0, [&] {
-            return launch_trsm_batched(D.d_fw_trs + L.fw_toff[t], L.fw_n[t], L.fw_cols[t], L.fw_k[t], true, st);
-          });
-          run(K_BACKSUB, L.fw_flops[t], 0.0, [&] {
-            return launch_gemm_desc(D.d_fw_gemm + L.fw_goff[t], L.fw_n[t], L.fw_tiles[t], L.fw_k[t], -1.0, 1.0, st,
-                                    true);
+            return launch_trsm_batched(D.d_fw_trs + L.fw_toff[t], L.fw_n[t], L.fw_cols[t], 128, true, st);
           });
         }
       }

@@ -1,6 +1,5 @@
-for t in 1e7 3.2e7 1e8; do
-  DTN_DEFER_MIN_WORK=$t python tools/defer_check.py 4 4096 32 | sed "s/^/thr $t: /"
-done
-for c in "2 512 16" "3 1024 32" "5 2048 32"; do
+for c in "4 4096 32" "5 2048 32"; do
+  DTN_DEFER_MIN_WORK=1 python tools/defer_check.py $c | sed "s/^/forced: /"
   python tools/defer_check.py $c | sed "s/^/default: /"
 done
+DTN_DEFER_MIN_WORK=1 python tools/defer_check.py 2 512 16 | sed "s/^/forced: /"
