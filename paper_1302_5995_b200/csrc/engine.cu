@@ -164,6 +164,9 @@ struct PlanDev {
   TriDesc* d_tri = nullptr;
   double* d_W = nullptr;     // U^{-1} L^{-1} before the column permutation
   double* d_LUp = nullptr;   // L_ik Linv_kk (below) and U_ik Uinv_kk (above the diagonal blocks)
+  double* d_UI = nullptr;    // U^{-1} before its deferred diagonal-block solves, then U^{-1} (d_UI2)
+  double* d_UI2 = nullptr;
+  int inv_ui = 0;            // descriptor ranges: U^{-1} sweep, U^{-1} block solves, final product
   int* d_load_col = nullptr;  // body loads: per unknown, its load column or -1
   double* d_F = nullptr;      // body map F = G * rhs_root (nb x nloads, leading dimension ldf)
   int ldf = 0;
@@ -185,6 +188,7 @@ struct PlanDev {
   cudaEvent_t ev_rp = nullptr, ev_rest = nullptr;  // look-ahead dependencies
   cudaEvent_t ev_rest2[2] = {nullptr, nullptr};       // fused look-ahead: side-stream step parity
   cudaEvent_t ev_S = nullptr;                           // root S complete (external node in the graph)
+  cudaEvent_t ev_inv_fork = nullptr, ev_inv_join = nullptr;  // root inverse: U^{-1} on the side stream
   cudaStream_t copy = nullptr;                          // S export overlapping the root inverse
   cudaStream_t side = nullptr;                      // low-priority stream for trailing updates
   cudaGraphExec_t gexec = nullptr;
@@ -194,12 +198,12 @@ struct PlanDev {
   ~PlanDev() {
     if (gexec) cudaGraphExecDestroy(gexec);
     for (auto e : ev_wave) cudaEventDestroy(e);
-    for (auto e : {ev_start, ev_root, ev_end, ev_rp, ev_rest, ev_rest2[0], ev_rest2[1], ev_S})
+    for (auto e : {ev_start, ev_root, ev_end, ev_rp, ev_rest, ev_rest2[0], ev_rest2[1], ev_S, ev_inv_fork, ev_inv_join})
       if (e) cudaEventDestroy(e);
     if (side) cudaStreamDestroy(side);
     if (copy) cudaStreamDestroy(copy);
     for (void* p : std::initializer_list<void*>{d_nodes, d_pos, d_arena, d_piv, d_pivstat, d_lists, d_stencil, d_S, d_G,
-                                                d_perm, d_norm, d_inv_descs, d_W, d_LUp, d_tinv, d_root_trs, d_load_col, d_F, d_F_desc, d_bs_gemm,
+                                                d_perm, d_norm, d_inv_descs, d_W, d_LUp, d_UI, d_UI2, d_tinv, d_root_trs, d_load_col, d_F, d_F_desc, d_bs_gemm,
                                                 d_bs_copy, d_tri, d_trs, d_chk, d_bad, d_fw_copy, d_fw_gather,
                                                 d_fw_trs, d_fw_gemm})
       if (p) cudaFree(p);
@@ -611,6 +615,28 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
     const int k0 = kb_ * 128, k1 = std::min(nb, k0 + 128), bk = k1 - k0;
     D->h_inv_descs.push_back(GemmDesc{tinv(kb_, 1), D->d_G + k0, D->d_W + k0, bk, nb, bk, 128, D->ldg, D->ldg});
   }
+  // Variant used by the build: U^{-1} formed on the side stream while the forward
+  // sweep runs (the same deferred-solve backward sweep on I, upper-triangular column
+  // ranges only), then W = U^{-1} Z as ONE batched GEMM over the 128-row blocks of
+  // U^{-1} (block row I needs only K >= I) instead of nblk - 1 dependent updates.
+  D->d_UI = dalloc<double>(size_t(D->ldg) * nb);
+  D->d_UI2 = dalloc<double>(size_t(D->ldg) * nb);
+  D->inv_ui = int(D->h_inv_descs.size());
+  for (int kb_ = 1; kb_ < nblk; ++kb_) {  // UI[:k0, k0:] -= U'[:k0, k] UI[k, k0:] (used in reverse order)
+    const int k0 = kb_ * 128, k1 = std::min(nb, k0 + 128), bk = k1 - k0;
+    D->h_inv_descs.push_back(GemmDesc{D->d_LUp + int64_t(k0) * D->ldlu, D->d_UI + k0 + int64_t(k0) * D->ldg,
+                                      D->d_UI + int64_t(k0) * D->ldg, k0, nb - k0, bk, D->ldlu, D->ldg, D->ldg});
+  }
+  for (int kb_ = 0; kb_ < nblk; ++kb_) {  // UI2_k = Uinv_kk UI_k (columns >= k0)
+    const int k0 = kb_ * 128, k1 = std::min(nb, k0 + 128), bk = k1 - k0;
+    D->h_inv_descs.push_back(GemmDesc{tinv(kb_, 1), D->d_UI + k0 + int64_t(k0) * D->ldg,
+                                      D->d_UI2 + k0 + int64_t(k0) * D->ldg, bk, nb - k0, bk, 128, D->ldg, D->ldg});
+  }
+  for (int kb_ = 0; kb_ < nblk; ++kb_) {  // W[I] = UI2[I, I:] Z[I:, :]
+    const int k0 = kb_ * 128, k1 = std::min(nb, k0 + 128), bk = k1 - k0;
+    D->h_inv_descs.push_back(GemmDesc{D->d_UI2 + k0 + int64_t(k0) * D->ldg, D->d_G + k0, D->d_W + k0, bk, nb, nb - k0,
+                                      D->ldg, D->ldg, D->ldg});
+  }
   D->d_inv_descs = dalloc<GemmDesc>(D->h_inv_descs.size());
   CK(cudaMemcpy(D->d_inv_descs, D->h_inv_descs.data(), D->h_inv_descs.size() * sizeof(GemmDesc),
                 cudaMemcpyHostToDevice));
@@ -624,6 +650,8 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
   CK(cudaEventCreateWithFlags(&D->ev_rest2[0], cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&D->ev_rest2[1], cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&D->ev_S, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&D->ev_inv_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&D->ev_inv_join, cudaEventDisableTiming));
   CK(cudaStreamCreateWithFlags(&D->copy, cudaStreamNonBlocking));
   int lo = 0, hi = 0;
   CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -937,14 +965,50 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
     };
     gemm(0, D.inv_pre, 1.0, 0.0);  // L' and U'
     int d = D.inv_pre;
+    const bool ui_side = !env_flag("DTN_INV_SWEEP");
+    if (ui_side) {  // U^{-1} on the side stream, concurrent with the forward sweep
+      CK(cudaEventRecord(D.ev_inv_fork, st));
+      CK(cudaStreamWaitEvent(st2, D.ev_inv_fork, 0));
+      run_on(st2, K_MISC, 0.0, 8.0 * nb2, [&] { return launch_set_identity(D.d_UI, D.ldg, nb, st2); });
+      CK(cudaMemsetAsync(D.d_UI2, 0, size_t(D.ldg) * nb * sizeof(double), st2));
+      auto gemm2 = [&](int d0, int cnt, double alpha, double beta) {
+        int tiles = 0;
+        double f = 0.0;
+        for (int i = d0; i < d0 + cnt; ++i) {
+          const GemmDesc& g = D.h_inv_descs[i];
+          tiles = std::max(tiles, gemm_tiles(g.m, g.n));
+          f += 2.0 * g.m * g.n * g.k;
+        }
+        run_on(st2, K_INV_GEMM, f, 0.0,
+               [&] { return launch_gemm_desc(D.d_inv_descs + d0, cnt, tiles, 128, alpha, beta, st2, true); });
+      };
+      for (int kb_ = nblk - 1; kb_ >= 1; --kb_) gemm2(D.inv_ui + kb_ - 1, 1, -1.0, 1.0);
+      gemm2(D.inv_ui + nblk - 1, nblk, 1.0, 0.0);  // UI2_k = Uinv_kk UI_k
+      CK(cudaEventRecord(D.ev_inv_join, st2));
+    }
     for (int kb_ = 0; kb_ + 1 < nblk; ++kb_) gemm(d + kb_, 1, -1.0, 1.0);  // forward sweep
     d += nblk - 1;
     CK(cudaMemsetAsync(D.d_G, 0, size_t(D.ldg) * nb * sizeof(double), st));
     gemm(d, nblk, 1.0, 0.0);  // Z_k = Linv_kk W_k
     d += nblk;
-    for (int kb_ = nblk - 1; kb_ >= 1; --kb_) gemm(d + kb_ - 1, 1, -1.0, 1.0);  // backward sweep
-    d += nblk - 1;
-    gemm(d, nblk, 1.0, 0.0);  // W_k = Uinv_kk Z_k
+    if (ui_side) {
+      CK(cudaStreamWaitEvent(st, D.ev_inv_join, 0));
+      // W = U^{-1} Z: one batched launch, block row I with K = nb - 128 I
+      int tiles = 0;
+      double f = 0.0;
+      const int f0 = D.inv_ui + (nblk - 1) + nblk;
+      for (int i = f0; i < f0 + nblk; ++i) {
+        const GemmDesc& g = D.h_inv_descs[i];
+        tiles = std::max(tiles, gemm_tiles(g.m, g.n));
+        f += 2.0 * g.m * g.n * g.k;
+      }
+      run(K_INV_GEMM, f, 0.0,
+          [&] { return launch_gemm_desc(D.d_inv_descs + f0, nblk, tiles, nb, 1.0, 0.0, st, true); });
+    } else {
+      for (int kb_ = nblk - 1; kb_ >= 1; --kb_) gemm(d + kb_ - 1, 1, -1.0, 1.0);  // backward sweep
+      d += nblk - 1;
+      gemm(d, nblk, 1.0, 0.0);  // W_k = Uinv_kk Z_k
+    }
     run(K_COPY, 0.0, 16.0 * nb2, [&] { return launch_permute_columns(D.d_W, D.ldg, perm, nb, D.d_G, D.ldg, st); });
     CK(cudaMemsetAsync(D.d_norm, 0, 2 * sizeof(unsigned long long), st));
     run(K_MISC, 0.0, 8.0 * nb2, [&] { return launch_norm1(D.d_S, D.lds, nb, nb, D.d_norm, st); });
