@@ -529,7 +529,8 @@ def build_root_gpu(op: DiscreteOperator | None, tree: BoxTree, want_G: bool = Tr
         opts.nloads = len(loads)
     S_host = None
     if export_S and shard < 0 and nshards == 1:
-        S_host = SolutionOperator._host_matrix(len(root_boundary(tree)))
+        s_ = tree.n - 2
+        S_host = SolutionOperator._host_matrix(4 * s_ - 4 if s_ > 1 else 1)  # len(root_boundary(tree))
         opts.export_S = S_host.ctypes.data
         opts.export_lds = S_host.shape[0]
     h = C.c_void_p()
