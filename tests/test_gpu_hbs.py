@@ -318,3 +318,23 @@ def test_baseline_compressed_configs_full_size(H, cfg, n_int, leaf):
     assert res <= 10 * eps * sol.cond_estimate, (res, sol.cond_estimate)
     assert sol.S_hbs.max_rank() < nb / 8
     sol.dense_op.free()
+
+
+def test_repeated_compressed_builds_keep_memory_flat(H):
+    """Plans are cached per context, the compression scratch and the caching pool are
+    reused and the factors are freed with their operators: device memory in use is
+    flat over repeated build_root_accel + apply rounds."""
+    import torch
+    import paper_1302_5995_b200 as dtn
+    op = dtn.discretize(dtn.baseline_problem(3, 1024))
+    tree = dtn.build_tree_uniform(1026, 32)
+    marks = []
+    for _ in range(4):
+        acc = dtn.build_root_accel(op, tree, dtn.AccelOptions(epsilon=1e-10, crossover=256))
+        X = torch.randn(acc.boundary_size(), 64, dtype=torch.float64, device="cuda")
+        dtn.apply_dtn(acc, X)
+        del acc, X
+        torch.cuda.synchronize()
+        free, total = torch.cuda.mem_get_info()
+        marks.append(total - free)
+    assert marks[-1] <= marks[1] + (64 << 20), marks
