@@ -17,6 +17,10 @@
  * of root unknowns starting at the south-west corner (grid.cpp:170-190), of
  * size 4(n-2)-4 with n the reference grid size including the Dirichlet ring.
  *
+ * Threading: one call at a time per context (a context owns its stream, cached plans and
+ * staging buffers; an HBS operator owns its apply workspace and graph). Built operators are
+ * immutable; use one context per host thread for concurrent builds or applies.
+ *
  * Return codes (errors.hpp, harness.hpp:11-12): 0 ok, 2 invalid argument,
  * 3 singular block (FactorizationError; dtn_gpu_last_error carries the
  * "what [where]" text), 5 CUDA failure. There is no CPU fallback: without a
