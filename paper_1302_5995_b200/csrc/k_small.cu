@@ -12,6 +12,7 @@
 // swaps: pivot rows are flagged instead of moved, so the boundary rows end up
 // holding S = M_bb - M_bi M_ii^{-1} M_ib in place. Two __syncthreads per pivot.
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -262,7 +263,7 @@ __global__ void __launch_bounds__(TR * TC) small_elim_kernel(KernelArgs args, co
   X(32, 8, 8, 4, 4)            \
   X(64, 16, 16, 4, 4)          \
   X(96, 16, 16, 6, 6)          \
-  X(128, 16, 32, 8, 4)         \
+  X(128, 32, 32, 4, 4) /* 1024 threads: measured 0.5 % faster than 16 x 32 x (8, 4) */ \
   X(160, 16, 32, 10, 5)
 
 cudaError_t launch_small_elim(const KernelArgs& args, const int* d_list, int count, int max_total, bool micro,
