@@ -520,7 +520,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
         for (int side = 0; side < 2; ++side) e.push_back(EigDesc{G1(side, a), U0(side, a), s, ld, ld});
       }
       EigDesc* de = upload(dbuf, e, st);
-      HCK(launch_jacobi_eig(de, int(e.size()), 30, false, 0.0, st));
+      HCK(launch_jacobi_eig(de, int(e.size()), 30, false, 0.0, smax, st));
       HCK(cudaStreamSynchronize(st));
     }
     tr.mark("jacobi1");
@@ -573,7 +573,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
         for (int side = 0; side < 2; ++side) e.push_back(EigDesc{G2(side, a), W(side, a), s, ld, ld});
       }
       EigDesc* de = upload(dbuf, e, st);
-      HCK(launch_jacobi_eig(de, int(e.size()), 30, true, (1e-2 * eps) * (1e-2 * eps), st));
+      HCK(launch_jacobi_eig(de, int(e.size()), 30, true, (1e-2 * eps) * (1e-2 * eps), smax, st));
       HCK(cudaStreamSynchronize(st));
     }
     tr.mark("jacobi2");

@@ -68,7 +68,7 @@ struct InvDesc {  // A (s x s, leading dimension lda) <- A^{-1}; *info = 0, or k
 
 cudaError_t launch_transpose_batched(const TransDesc* d_descs, int count, int max_tiles, cudaStream_t st);
 cudaError_t launch_jacobi_eig(const EigDesc* d_descs, int count, int max_sweeps, bool rel, double floor_rel,
-                              cudaStream_t st);
+                              int max_s, cudaStream_t st);
 cudaError_t launch_hbs_select(const SelDesc* d_descs, int count, double eps, cudaStream_t st);
 cudaError_t launch_gather_cols(const GatherDesc* d_descs, int count, cudaStream_t st);
 cudaError_t launch_pack(const PackDesc* d_descs, int count, cudaStream_t st);

@@ -187,14 +187,14 @@ int jacobi_smem_doubles() { return 200 * 1024 / 8; }
 // depends on rotations among them, and the relative rule would otherwise
 // chase rounding noise there for every sweep.
 constexpr int JPMAXP = 128;
-constexpr int JTP = 1024;  // threads of the packed kernel
 constexpr int kPackedMaxS = 236;  // 236 * 237 / 2 doubles = 218.5 KB
 
 __device__ __forceinline__ int jp_idx(int r, int c) {  // packed upper triangle, r <= c
   return c * (c + 1) / 2 + r;
 }
 
-__global__ void __launch_bounds__(JTP) jacobi_eig_packed_kernel(const EigDesc* __restrict__ descs, int max_sweeps,
+template <int NT>
+__global__ void __launch_bounds__(NT) jacobi_eig_packed_kernel(const EigDesc* __restrict__ descs, int max_sweeps,
                                                               int smem_doubles, int rel, double floor_rel) {
   extern __shared__ __align__(16) double jsm[];
   __shared__ double cs_[JPMAXP], sn_[JPMAXP];
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(JTP) jacobi_eig_packed_kernel(const EigDesc* _
   const bool v_sm = (long long)npk + (long long)s * ls <= smem_doubles;
   double* V = v_sm ? jsm + npk : d.V;
   const long long ldv = v_sm ? ls : d.ldv;
-  for (int e = tid; e < s * s; e += JTP) {
+  for (int e = tid; e < s * s; e += NT) {
     const int r = e % s, c = e / s;
     if (r <= c) P[jp_idx(r, c)] = d.A[r + (long long)c * d.lda];
     V[r + c * ldv] = r == c ? 1.0 : 0.0;
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(JTP) jacobi_eig_packed_kernel(const EigDesc* _
     __syncthreads();
     for (int r = 0; r < n2 - 1; ++r) {
       // 1. rotations of this round's disjoint pairs
-      for (int i = tid; i < np; i += JTP) {
+      for (int i = tid; i < np; i += NT) {
         int a, b;
         if (i == 0) {
           a = r;
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(JTP) jacobi_eig_packed_kernel(const EigDesc* _
       __syncthreads();
       // 2. A <- T A T^T block by block (i <= j), V <- V T^T
       const int nblk = np * (np + 1) / 2;
-      for (int w = tid; w < nblk; w += JTP) {
+      for (int w = tid; w < nblk; w += NT) {
         // w = j (j + 1) / 2 + i, i <= j (block pair enumeration without the i > j half)
         int j = int((sqrtf(8.0f * float(w) + 1.0f) - 1.0f) * 0.5f);
         while ((j + 1) * (j + 2) / 2 <= w) ++j;
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(JTP) jacobi_eig_packed_kernel(const EigDesc* _
         if (bv) P[b <= e ? jp_idx(b, e) : jp_idx(e, b)] = cj * rbe - sj * rbf;
         if (bv && fv) P[b <= f ? jp_idx(b, f) : jp_idx(f, b)] = sj * rbe + cj * rbf;
       }
-      for (int w = tid; w < np * s; w += JTP) {
+      for (int w = tid; w < np * s; w += NT) {
         const int i = w / s, j = w - i * s;
         const double sg = sn_[i];
         if (sg != 0.0) {
@@ -318,9 +318,9 @@ __global__ void __launch_bounds__(JTP) jacobi_eig_packed_kernel(const EigDesc* _
     if (!rotated) break;
     __syncthreads();
   }
-  for (int i = tid; i < s; i += JTP) d.A[i + (long long)i * d.lda] = P[jp_idx(i, i)];
+  for (int i = tid; i < s; i += NT) d.A[i + (long long)i * d.lda] = P[jp_idx(i, i)];
   if (v_sm)
-    for (int e = tid; e < s * s; e += JTP) {
+    for (int e = tid; e < s * s; e += NT) {
       const int r = e % s, c = e / s;
       d.V[r + (long long)c * d.ldv] = V[r + c * ldv];
     }
@@ -329,19 +329,27 @@ __global__ void __launch_bounds__(JTP) jacobi_eig_packed_kernel(const EigDesc* _
 int jacobi_packed_smem_doubles() { return 220 * 1024 / 8; }
 
 cudaError_t launch_jacobi_eig(const EigDesc* d_descs, int count, int max_sweeps, bool rel, double floor_rel,
-                              cudaStream_t st) {
-  if (count <= 0) return cudaSuccess;
+                              int max_s, cudaStream_t st) {
+  if (count <= 0 || max_s <= 0) return cudaSuccess;
   static const cudaError_t attr = cudaFuncSetAttribute(jacobi_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                        jacobi_smem_doubles() * 8);
   if (attr != cudaSuccess) return attr;
   static const cudaError_t attr2 = cudaFuncSetAttribute(
-      jacobi_eig_packed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, jacobi_packed_smem_doubles() * 8);
+      jacobi_eig_packed_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, jacobi_packed_smem_doubles() * 8);
   if (attr2 != cudaSuccess) return attr2;
-  // s <= 236: packed kernel; larger blocks: the general kernel (A, V in global memory when they do not fit)
-  jacobi_eig_packed_kernel<<<count, JTP, size_t(jacobi_packed_smem_doubles()) * 8, st>>>(
-      d_descs, max_sweeps, jacobi_packed_smem_doubles(), rel ? 1 : 0, floor_rel);
-  jacobi_eig_kernel<<<count, JT, size_t(jacobi_smem_doubles()) * 8, st>>>(d_descs, max_sweeps, jacobi_smem_doubles(),
-                                                                        rel ? 1 : 0, kPackedMaxS + 1);
+  // s <= 236: packed kernel, shared memory sized for this batch's largest block (the
+  // packed triangle, plus V when it fits) so that two CTAs share an SM at the low tree
+  // levels (256-thread CTAs measured slower: the rounds are latency-bound); larger
+  // blocks: the general kernel
+  const int sp = std::min(max_s, kPackedMaxS);
+  const long long npk = (long long)sp * (sp + 1) / 2, withv = npk + (long long)sp * (sp | 1);
+  const int smem = int(std::min<long long>(withv <= jacobi_packed_smem_doubles() ? withv : npk,
+                                           jacobi_packed_smem_doubles()));
+  jacobi_eig_packed_kernel<1024><<<count, 1024, size_t(smem) * 8, st>>>(d_descs, max_sweeps, smem, rel ? 1 : 0,
+                                                                       floor_rel);
+  if (max_s > kPackedMaxS)
+    jacobi_eig_kernel<<<count, JT, size_t(jacobi_smem_doubles()) * 8, st>>>(d_descs, max_sweeps, jacobi_smem_doubles(),
+                                                                          rel ? 1 : 0, kPackedMaxS + 1);
   return cudaGetLastError();
 }
 
