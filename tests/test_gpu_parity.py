@@ -264,3 +264,19 @@ def test_tiny_and_ragged_grids(n):
         assert O.rel_fro(sol.S_dense, brute) <= TOL, (name, n)
         nb = len(sol.boundary)
         assert np.abs(sol.G_dense @ sol.S_dense - np.eye(nb)).max() <= 1e-10, (name, n)
+
+
+@pytest.mark.parametrize("batch", [1, 2, 7, 31, 32, 33, 64])
+def test_apply_batch_sizes_across_the_skinny_path(batch):
+    """apply_dtn / apply_schur for batch sizes on both sides of the split-K
+    skinny product (<= 32 vectors) and the DMMA GEMM, host and device buffers."""
+    import torch
+    sol = gpu_build("helmholtz1", 66, 64)
+    nb = len(sol.boundary)
+    X = np.asfortranarray(np.random.default_rng(batch).standard_normal((nb, batch)))
+    for which, M in ((dtn.apply_dtn, sol.G_dense), (dtn.apply_schur, sol.S_dense)):
+        ref = M @ X
+        assert O.rel_fro(which(sol, X), ref) <= 1e-13
+        Xd = torch.from_numpy(X).cuda().t().contiguous().t()
+        assert O.rel_fro(which(sol, Xd).cpu().numpy(), ref) <= 1e-13
+        assert O.rel_fro(which(sol, X[:, 0]), ref[:, 0]) <= 1e-13
