@@ -338,3 +338,15 @@ def test_repeated_compressed_builds_keep_memory_flat(H):
         free, total = torch.cuda.mem_get_info()
         marks.append(total - free)
     assert marks[-1] <= marks[1] + (64 << 20), marks
+
+
+@pytest.mark.parametrize("crossover,compressed", [(252, True), (253, False)])
+def test_crossover_gate_is_size_at_least(H, crossover, compressed):
+    """The reference compresses a box whose boundary size is >= crossover
+    (accel_nd.cpp:682, 737); the root boundary here is 4 * 64 - 4 = 252."""
+    import paper_1302_5995_b200 as dtn
+    n = 66
+    sol = dtn.build_root_accel(dtn.discretize(dtn.catalog("laplace", n)), dtn.build_tree_uniform(n, 16),
+                               dtn.AccelOptions(epsilon=1e-10, crossover=crossover, hbs_leaf=32))
+    assert (getattr(sol, "G_hbs", None) is not None) == compressed
+    assert sol.boundary_size() == 252
