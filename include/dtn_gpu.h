@@ -17,9 +17,11 @@
  * of root unknowns starting at the south-west corner (grid.cpp:170-190), of
  * size 4(n-2)-4 with n the reference grid size including the Dirichlet ring.
  *
- * Threading: one call at a time per context (a context owns its stream, cached plans and
- * staging buffers; an HBS operator owns its apply workspace and graph). Built operators are
- * immutable; use one context per host thread for concurrent builds or applies.
+ * Threading: calls on one context -- and on every operator built with it (dense or HBS) --
+ * are serialised by the context's lock (the context owns the stream, cached plans, apply
+ * staging and the HBS apply workspaces), so concurrent applies of one operator are safe
+ * but do not overlap. For concurrent work build one context (and its operators) per host
+ * thread. dtn_gpu_set_stream changes the stream of every later call on the context.
  *
  * Return codes (errors.hpp, harness.hpp:11-12): 0 ok, 2 invalid argument,
  * 3 singular block (FactorizationError; dtn_gpu_last_error carries the

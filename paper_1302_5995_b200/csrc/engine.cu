@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <random>
 #include <stdexcept>
 #include <string>
@@ -57,6 +58,7 @@ cudaError_t launch_set_identity(double*, int, int, cudaStream_t);
 cudaError_t launch_permute_columns(const double*, int, const int*, int, double*, int, cudaStream_t);
 cudaError_t launch_perm_only(const int*, int, int*, cudaStream_t);
 cudaError_t blocked_init();
+cudaError_t hbs_kernels_init();
 int gemm_tiles(int, int);
 }  // namespace dtnb
 
@@ -1034,6 +1036,10 @@ bool use_graphs() {
 }  // namespace
 
 struct dtn_ctx {
+  // every call on a context (and on the operators built with it) runs under this
+  // lock: the stream, cached plans, apply staging and the HBS apply workspaces
+  // are shared state (recursive: the compressed build calls the other entries)
+  std::recursive_mutex mu;
   int device = 0;
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
@@ -1070,6 +1076,8 @@ thread_local std::string g_err;  // errors with no context (dtn_gpu_create)
 
 template <class F>
 int guarded(dtn_ctx* ctx, F&& f) {
+  std::unique_lock<std::recursive_mutex> lock;
+  if (ctx) lock = std::unique_lock<std::recursive_mutex>(ctx->mu);
   std::string& err = ctx ? ctx->err : g_err;
   (void)cudaGetLastError();  // drop stale non-sticky errors from unrelated runtime calls
   try {
@@ -1120,6 +1128,7 @@ int dtn_gpu_create(dtn_ctx** out, int device) {
     CK(gemm_init());
     CK(blocked_init());
     CK(misc_init());
+    CK(hbs_kernels_init());
     auto* c = new dtn_ctx;
     c->device = device;
     CK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
@@ -1954,9 +1963,21 @@ int dtn_gpu_build_accel(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* o
     ctx->err = "build_root_accel: epsilon must be > 0 and hbs_leaf >= 2";
     return DTN_EINVAL;
   }
-  // the root operator: S by the exact dense merges; G only when the root stays dense
-  const int64_t nb_root = 4 * int64_t(prob->n - 2) - 4;
-  const bool dense_root = nb_root < opts->crossover;
+  // the root is structured only when both of its W|E halves are: merge_pair
+  // (accel_nd.cpp:667-689) compresses a merged box (size >= crossover) only when it
+  // has a next merge (out_side != none), and the root's W|E merge has none
+  // (accel_nd.cpp:771-779); a single-leaf tree stays dense
+  bool dense_root = true;
+  {
+    PlanKey hk;
+    hk.n = prob->n;
+    hk.n_leaf = opts->n_leaf;
+    hk.leaf_side = opts->leaf_side;
+    int depth = 0, nb_w = 0, nb_e = 0;
+    const int rc0 = guarded(ctx, [&] { root_halves(hk, &depth, &nb_w, &nb_e); });
+    if (rc0 != DTN_OK) return rc0;
+    dense_root = depth == 0 || nb_w < opts->crossover || nb_e < opts->crossover;
+  }
   dtn_opts o = *opts;
   o.engine = 0;
   o.want_G = dense_root ? 1 : 0;

@@ -1053,6 +1053,14 @@ std::unique_ptr<HbsDev> hbs_deserialize(const uint8_t* data, size_t size, cudaSt
     const auto& n = H.nodes[t];
     if ((n.left < 0) != (n.right < 0) || n.left >= nn || n.right >= nn || n.left == 0 || n.right == 0)
       throw std::invalid_argument("deserialize: bad tree");
+    if (n.begin < 0 || n.end <= n.begin || n.end > H.M) throw std::invalid_argument("deserialize: bad tree");
+    if (n.left >= 0) {  // children partition the parent's range (index_tree.cpp:37-67)
+      const auto& l = H.nodes[n.left];
+      const auto& r = H.nodes[n.right];
+      if (n.left <= t || n.right <= t || l.parent != t || r.parent != t || l.begin != n.begin || l.end != r.begin ||
+          r.end != n.end || l.level != n.level + 1 || r.level != n.level + 1)
+        throw std::invalid_argument("deserialize: bad tree");
+    }
   }
   H.rank.assign(nn, 0);
   H.rows.assign(nn, 0);
@@ -1087,6 +1095,41 @@ std::unique_ptr<HbsDev> hbs_deserialize(const uint8_t* data, size_t size, cudaSt
       matrix();
     }
     if (!leaf) matrix();
+  }
+  {  // every factor's shape against the tree (hbs.hpp:30-51) before anything reaches the device:
+     // leaf D s x s; U, V rows x rank (equal shapes; rows = s on leaves, k_left + k_right on
+     // parents); parent B (k_left + k_right)^2
+    std::vector<int64_t> rk(size_t(nn), 0), rw(size_t(nn), 0);
+    size_t mi = 0;
+    std::vector<size_t> first(static_cast<size_t>(nn), 0);
+    for (int t = 0; t < int(nn); ++t) {
+      first[size_t(t)] = mi;
+      mi += (H.is_leaf(t) ? 1 : 0) + (t != 0 ? 2 : 0) + (H.is_leaf(t) ? 0 : 1);
+    }
+    for (int t = int(nn) - 1; t >= 0; --t) {  // children before parents (preorder: children have larger ids)
+      const auto& n = H.nodes[t];
+      size_t q = first[size_t(t)];
+      const int64_t s = n.end - n.begin;
+      int64_t rows = s;
+      if (H.is_leaf(t)) {
+        const Mat& d = mats[q++];
+        if (d.r != s || d.c != s) throw std::invalid_argument("deserialize: leaf D shape does not match the tree");
+      } else {
+        rows = rk[size_t(n.left)] + rk[size_t(n.right)];
+      }
+      rw[size_t(t)] = rows;
+      if (t != 0) {
+        const Mat& u = mats[q++];
+        const Mat& v = mats[q++];
+        if (u.r != rows || v.r != rows || u.c != v.c || u.c > rows)
+          throw std::invalid_argument("deserialize: U/V shape does not match the tree");
+        rk[size_t(t)] = u.c;
+      }
+      if (!H.is_leaf(t)) {
+        const Mat& b = mats[q++];
+        if (b.r != rows || b.c != rows) throw std::invalid_argument("deserialize: B shape does not match the tree");
+      }
+    }
   }
   double* buf = nullptr;
   pmalloc(&buf, total * 8 + 8);

@@ -378,6 +378,13 @@ cudaError_t gemm_init() {
   e = cudaFuncSetAttribute(trailing_update_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            sizeof(GemmSmem<16>));
   if (e != cudaSuccess) return e;
+  // (function attributes belong to the current device's context: set here, per
+  // device, from dtn_gpu_create -- never cached in a process-wide static)
+  for (cudaError_t x : {cudaFuncSetAttribute(gemm_desc2_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             sizeof(GemmSmem<16>)),
+                        cudaFuncSetAttribute(gemm_desc2_kernel<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             sizeof(GemmSmem<16>))})
+    if (x != cudaSuccess) return x;
   return cudaFuncSetAttribute(trailing_update_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               sizeof(GemmSmem<8>));
 }
@@ -458,14 +465,6 @@ cudaError_t launch_gemm_desc_tc(const GemmDesc* d_descs, int count, int max_tile
 
 cudaError_t launch_gemm_desc2(const GemmDesc2* d_descs, int count, int max_tiles, bool tc, cudaStream_t st) {
   if (count <= 0 || max_tiles <= 0) return cudaSuccess;
-  static const cudaError_t attr = [] {
-    cudaError_t e = cudaFuncSetAttribute(gemm_desc2_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         sizeof(GemmSmem<16>));
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(gemm_desc2_kernel<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                sizeof(GemmSmem<16>));
-  }();
-  if (attr != cudaSuccess) return attr;
   dim3 grid(max_tiles, count);
   if (tc) gemm_desc2_kernel<16, true><<<grid, GTHREADS, sizeof(GemmSmem<16>), st>>>(d_descs);
   else gemm_desc2_kernel<16, false><<<grid, GTHREADS, sizeof(GemmSmem<16>), st>>>(d_descs);

@@ -328,15 +328,19 @@ __global__ void __launch_bounds__(NT) jacobi_eig_packed_kernel(const EigDesc* __
 
 int jacobi_packed_smem_doubles() { return 220 * 1024 / 8; }
 
+// Per-device kernel attributes (called from dtn_gpu_create for every context's
+// device: attributes belong to the current device's context).
+cudaError_t hbs_kernels_init() {
+  cudaError_t e = cudaFuncSetAttribute(jacobi_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       jacobi_smem_doubles() * 8);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(jacobi_eig_packed_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              jacobi_packed_smem_doubles() * 8);
+}
+
 cudaError_t launch_jacobi_eig(const EigDesc* d_descs, int count, int max_sweeps, bool rel, double floor_rel,
                               int max_s, cudaStream_t st) {
   if (count <= 0 || max_s <= 0) return cudaSuccess;
-  static const cudaError_t attr = cudaFuncSetAttribute(jacobi_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                       jacobi_smem_doubles() * 8);
-  if (attr != cudaSuccess) return attr;
-  static const cudaError_t attr2 = cudaFuncSetAttribute(
-      jacobi_eig_packed_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, jacobi_packed_smem_doubles() * 8);
-  if (attr2 != cudaSuccess) return attr2;
   // s <= 236: packed kernel, shared memory sized for this batch's largest block (the
   // packed triangle, plus V when it fits) so that two CTAs share an SM at the low tree
   // levels (256-thread CTAs measured slower: the rounds are latency-bound); larger

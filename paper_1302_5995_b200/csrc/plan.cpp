@@ -222,6 +222,26 @@ int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
 }  // namespace
 
+void root_halves(const PlanKey& key, int* depth, int* nb_w, int* nb_e) {
+  Plan P;
+  build_ref_tree(key, P);
+  *depth = P.depth;
+  *nb_w = *nb_e = 0;
+  if (P.depth == 0) return;
+  const RefBox& rt = P.boxes[0];
+  const Rect& sw = P.boxes[rt.children[0]].r;
+  const Rect& se = P.boxes[rt.children[1]].r;
+  const Rect& nw = P.boxes[rt.children[2]].r;
+  const Rect& ne = P.boxes[rt.children[3]].r;
+  auto uni = [](const Rect& a, const Rect& b) {
+    if (a.empty()) return b;
+    if (b.empty()) return a;
+    return Rect{std::min(a.x0, b.x0), std::max(a.x1, b.x1), std::min(a.y0, b.y0), std::max(a.y1, b.y1)};
+  };
+  *nb_w = perimeter_size(uni(sw, nw));
+  *nb_e = perimeter_size(uni(se, ne));
+}
+
 std::vector<int> shard_nodes(const Plan& P, int nshards) {
   auto need = [&](bool ok) {
     if (!ok) throw std::invalid_argument("shards: the tree is too shallow for this shard count");

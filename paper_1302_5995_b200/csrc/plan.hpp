@@ -117,6 +117,12 @@ struct Plan {
 // else the reference rule with n_leaf. Throws std::invalid_argument.
 Plan make_plan(const PlanKey& key);
 
+// Depth of the reference tree and the boundary sizes of the root's W and E
+// halves (merge_four's (SW,NW) and (SE,NE) merges, dense_nd.cpp:188-194);
+// host-only, no DAG. The compressed engine's root is structured only when both
+// halves are (accel_nd.cpp:667-689, 771-779).
+void root_halves(const PlanKey& key, int* depth, int* nb_w, int* nb_e);
+
 // DAG nodes of the shards of a full plan (see PlanKey), in shard order.
 std::vector<int> shard_nodes(const Plan& P, int nshards);
 

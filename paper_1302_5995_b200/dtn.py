@@ -16,6 +16,7 @@ fallback.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import enum
 import math
@@ -297,7 +298,22 @@ class Context:
             pass
 
     def set_stream(self, stream_handle: int | None):
-        L.lib().dtn_gpu_set_stream(self.h, C.c_void_p(stream_handle or 0) if stream_handle else None)
+        L.lib().dtn_gpu_set_stream(self.h, C.c_void_p(stream_handle) if stream_handle else None)
+
+    @contextlib.contextmanager
+    def torch_stream(self):
+        """Run this context's work on torch's current stream of its device for the
+        duration of the block, so engine calls that read or write torch tensors are
+        ordered with the torch kernels that produce and consume them (and with the
+        caching allocator's reuse of their memory). torch's legacy default stream
+        (handle 0) is passed as cudaStreamLegacy (1)."""
+        import torch
+        h = torch.cuda.current_stream(self.device).cuda_stream or 1
+        self.set_stream(h)
+        try:
+            yield
+        finally:
+            self.set_stream(None)
 
     def check(self, rc: int):
         if rc == 0:
@@ -433,8 +449,10 @@ class SolutionOperator:
         return 8 * nb * nb * (2 if self.has_G else 1) + extra
 
     def export_device(self, S_ptr: int | None = None, lds: int = 0, G_ptr: int | None = None, ldg: int = 0):
-        """Device-to-device export of S and/or G (column-major, leading dims)."""
-        self.ctx.check(L.lib().dtn_gpu_export_device(self.h, S_ptr, lds, G_ptr, ldg))
+        """Device-to-device export of S and/or G (column-major, leading dims) into
+        caller memory, ordered on torch's current stream (torch-allocated targets)."""
+        with self.ctx.torch_stream():
+            self.ctx.check(L.lib().dtn_gpu_export_device(self.h, S_ptr, lds, G_ptr, ldg))
 
     def device_ptrs(self):
         s, g, ld = C.c_void_p(), C.c_void_p(), C.c_int64()
@@ -469,6 +487,14 @@ def shard_info(tree: BoxTree, nshards: int, shard: int) -> dict:
     if rc != 0:
         raise ValueError(L.lib().dtn_gpu_last_error(None).decode())
     return dict(rect=tuple(rect), nb=nb.value)
+
+
+def _device_inputs(stencil_device_ptr, shard_S) -> bool:
+    """Inputs in device memory (a stencil pointer or torch shard blocks): the
+    build is then ordered on torch's current stream (Context.torch_stream)."""
+    if stencil_device_ptr:
+        return True
+    return shard_S is not None and any(getattr(S, "is_cuda", False) for S in shard_S)
 
 
 def _make_problem(op, tree, stencil_device_ptr=None, shard_S=None):
@@ -534,7 +560,8 @@ def build_root_gpu(op: DiscreteOperator | None, tree: BoxTree, want_G: bool = Tr
         opts.export_S = S_host.ctypes.data
         opts.export_lds = S_host.shape[0]
     h = C.c_void_p()
-    ctx.check(L.lib().dtn_gpu_build(ctx.h, C.byref(prob), C.byref(opts), C.byref(h)))
+    with (ctx.torch_stream() if _device_inputs(stencil_device_ptr, shard_S) else contextlib.nullcontext()):
+        ctx.check(L.lib().dtn_gpu_build(ctx.h, C.byref(prob), C.byref(opts), C.byref(h)))
     sol = SolutionOperator(ctx, h, tree.n, want_G)
     if S_host is not None:
         sol._S = S_host
@@ -628,8 +655,9 @@ def build_root_accel(op: DiscreteOperator, tree: BoxTree, opt: AccelOptions | No
         opts.load_ids = load_arr.ctypes.data
         opts.nloads = len(load_arr)
     hop, hs, hg, cond = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_double()
-    ctx.check(L.lib().dtn_gpu_build_accel(ctx.h, C.byref(prob), C.byref(opts), int(opt.hbs_leaf), C.byref(hop),
-                                          C.byref(hs), C.byref(hg), C.byref(cond)))
+    with (ctx.torch_stream() if _device_inputs(stencil_device_ptr, shard_S) else contextlib.nullcontext()):
+        ctx.check(L.lib().dtn_gpu_build_accel(ctx.h, C.byref(prob), C.byref(opts), int(opt.hbs_leaf), C.byref(hop),
+                                              C.byref(hs), C.byref(hg), C.byref(cond)))
     dense = SolutionOperator(ctx, hop, n, not hs.value)
     if not hs.value:  # dense root
         dense.engine = Engine.accel
@@ -677,8 +705,9 @@ def _apply(sol: SolutionOperator, which: int, g):
             raise ValueError("apply_dtn: boundary vector size mismatch")
         Xf = X.t().contiguous().t() if X.stride(0) != 1 else X
         Y = torch.empty((X.shape[1], nb), dtype=torch.float64, device=g.device).t()
-        sol.ctx.check(L.lib().dtn_gpu_apply(sol.h, which, Xf.data_ptr(), Xf.stride(1) if Xf.shape[1] > 1 else nb,
-                                            Xf.shape[1], Y.data_ptr(), nb, 1))
+        with sol.ctx.torch_stream():
+            sol.ctx.check(L.lib().dtn_gpu_apply(sol.h, which, Xf.data_ptr(), Xf.stride(1) if Xf.shape[1] > 1 else nb,
+                                                Xf.shape[1], Y.data_ptr(), nb, 1))
         return Y.reshape(nb) if vec else Y
     X = np.asarray(g, dtype=np.float64)
     vec = X.ndim == 1
@@ -762,7 +791,9 @@ def ring_dtn(sol: "SolutionOperator", op: DiscreteOperator, device: bool = False
     if device:
         import torch
         T = torch.empty((m, m), dtype=torch.float64, device="cuda").t()
-        sol.ctx.check(L.lib().dtn_gpu_ring_dtn(sol.h, adj.ctypes.data, coef.ctypes.data, m, op.h, T.data_ptr(), m, 1))
+        with sol.ctx.torch_stream():
+            sol.ctx.check(L.lib().dtn_gpu_ring_dtn(sol.h, adj.ctypes.data, coef.ctypes.data, m, op.h, T.data_ptr(), m,
+                                                   1))
         return T
     T = np.zeros((m, m), order="F")
     sol.ctx.check(L.lib().dtn_gpu_ring_dtn(sol.h, adj.ctypes.data, coef.ctypes.data, m, op.h, T.ctypes.data, m, 0))

@@ -221,8 +221,10 @@ def compress(H, eps: float, leaf_cap: int = 64, ctx: Context | None = None) -> H
         if H.dtype != torch.float64 or not H.is_cuda or H.dim() != 2 or H.shape[0] != H.shape[1]:
             raise ValueError("compress: H must be a square float64 CUDA tensor")
         Hc = H.t().contiguous().t() if H.stride(0) != 1 else H  # column-major
-        ctx.check(L.lib().dtn_gpu_hbs_compress(ctx.h, Hc.data_ptr(), H.shape[0], Hc.stride(1) if H.shape[0] > 1 else 1,
-                                               1, float(eps), int(leaf_cap), C.byref(out)))
+        with ctx.torch_stream():
+            ctx.check(L.lib().dtn_gpu_hbs_compress(ctx.h, Hc.data_ptr(), H.shape[0],
+                                                   Hc.stride(1) if H.shape[0] > 1 else 1, 1, float(eps),
+                                                   int(leaf_cap), C.byref(out)))
     else:
         A = np.asfortranarray(np.asarray(H, dtype=np.float64))
         if A.ndim != 2 or A.shape[0] != A.shape[1]:
@@ -261,7 +263,8 @@ def apply(H: HbsMatrix, x):
         Xf = X if colmajor else X.t().contiguous().t()  # column-major with ld >= M
         Y = torch.empty((X.shape[1], M), dtype=torch.float64, device=x.device).t()
         ldx = Xf.stride(1) if Xf.shape[1] > 1 else M
-        H.ctx.check(L.lib().dtn_gpu_hbs_apply(H.h, Xf.data_ptr(), ldx, Xf.shape[1], Y.data_ptr(), M, 1))
+        with H.ctx.torch_stream():
+            H.ctx.check(L.lib().dtn_gpu_hbs_apply(H.h, Xf.data_ptr(), ldx, Xf.shape[1], Y.data_ptr(), M, 1))
         return Y.reshape(M) if vec else Y
     X = np.asarray(x, dtype=np.float64)
     vec = X.ndim == 1

@@ -1,0 +1,178 @@
+"""GPU parity at the BASELINE configurations' full sizes, through the C ABI.
+
+* config 5 operator (Helmholtz kappa = 100, n = 2048 interior, 32 x 32 leaves):
+  the dense engine's S and Neumann data S g against the oracle
+  (oracle.build_root_dense, the restated dense_nd.cpp) at 1e-10, and the
+  compressed engine (build_root_accel with the benched defaults, eps = 1e-10)
+  against the SAME oracle S at 10 eps = 1e-9 (BASELINE.json north_star);
+* config 3 operator (variable coefficients, kappa = 60, n = 1024): compressed
+  engine against the oracle S, bounded by the operator's conditioning (two
+  valid FP64 eliminations of this operator differ at ~3e-9, see
+  test_gpu_parity.test_dense_n1024_varcoef_vs_oracle), plus an accuracy check
+  of G_hbs g against a sparse direct solve that must match the oracle's own;
+* config 4 operator (Laplace, n = 4096, 16.8 M unknowns, too large for the
+  oracle) and the config-5 operator: manufactured solutions. For a grid function
+  u with A u = 0 in the interior (u = x y and x^2 - y^2 are discrete-harmonic for
+  the 5-point Laplacian; u = cos(a x + b y) with (4/h^2)(sin^2(a h/2) +
+  sin^2(b h/2)) = kappa^2 is a discrete plane wave of -Delta - kappa^2), the
+  root boundary values satisfy S u_b = -(D g)_b exactly (A u = -D g,
+  grid.hpp:88-90; only boundary unknowns touch the Dirichlet ring), a
+  size-independent check of S and of S_hbs.
+"""
+import numpy as np
+import pytest
+
+import paper_1302_5995_b200 as dtn
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _vectors(nb, nvec, seed=1):
+    rng = np.random.Generator(np.random.MT19937(seed))
+    return np.asfortranarray(rng.uniform(-1.0, 1.0, (nb, nvec)))
+
+
+def manufactured(op, boundary, u):
+    """(u_b, -(D g)_b) for the grid function u(xp, yp) of physical coordinates
+    (x h, y h), h = 1/(n-1) (grid.cpp:138)."""
+    n, st = op.n, op.stencil
+    s, h = n - 2, 1.0 / (n - 1)
+    b = np.asarray(boundary, dtype=np.int64)
+    x, y = b % s + 1, b // s + 1
+    ub = u(x * h, y * h)
+    rhs = np.zeros(len(b))
+    for r, (dx, dy) in enumerate([(1, 0), (-1, 0), (0, 1), (0, -1)], start=1):
+        qx, qy = x + dx, y + dy
+        ring = (qx == 0) | (qx == n - 1) | (qy == 0) | (qy == n - 1)
+        rhs[ring] -= st[r][b[ring]] * u(qx[ring] * h, qy[ring] * h)
+    return ub, rhs
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(b))
+
+
+ACCEL = dict(epsilon=1e-10, crossover=256, hbs_leaf=64)  # bench.py's compressed defaults
+
+
+@pytest.fixture(scope="module")
+def cfg5_oracle():
+    n = 2050
+    return O.build_root_dense(O.Problem("helmholtz", n, 100.0), O.Tree(n, uniform_side=32), threads=16, mode=2)
+
+
+@pytest.fixture(scope="module")
+def cfg5_op():
+    return dtn.discretize(dtn.baseline_problem(5, 2048))
+
+
+def test_config5_dense_S_and_neumann_vs_oracle(cfg5_oracle, cfg5_op):
+    sol = dtn.build_root_gpu(cfg5_op, dtn.build_tree_uniform(2050, 32), want_G=False)
+    ref = cfg5_oracle
+    assert np.array_equal(sol.boundary, ref.boundary)
+    S = sol.S_dense
+    g = _vectors(len(ref.boundary), 16)
+    assert rel(S, ref.S) <= 1e-10
+    assert rel(dtn.apply_schur(sol, g), ref.S @ g) <= 1e-10
+    sol.free()
+
+
+def test_config5_compressed_vs_oracle(cfg5_oracle, cfg5_op):
+    import torch
+    acc = dtn.build_root_accel(cfg5_op, dtn.build_tree_uniform(2050, 32), dtn.AccelOptions(**ACCEL))
+    ref = cfg5_oracle
+    nb = len(ref.boundary)
+    g = _vectors(nb, 16)
+    assert rel(dtn.apply_schur(acc, g), ref.S @ g) <= 1e-9
+    eye = torch.eye(nb, dtype=torch.float64, device="cuda")
+    S_rec = dtn.apply_schur(acc, eye).cpu().numpy()  # reconstruct(S_hbs) on the device
+    assert rel(S_rec, ref.S) <= 1e-9
+    # G_hbs inverts the oracle's S to the operator's conditioning
+    r = dtn.apply_dtn(acc, ref.S @ g)
+    assert rel(r, g) <= 1e-9 * max(1.0, acc.cond_estimate) ** 0.5
+
+
+def test_config5_plane_wave(cfg5_op):
+    """-Delta_h u - kappa^2 u = 0 for the discrete plane wave: S u_b = -(D g)_b."""
+    n, kappa = 2050, 100.0
+    h = 1.0 / (n - 1)
+    a = (2.0 / h) * np.arcsin(kappa * h / np.sqrt(8.0))  # a = b: 2 (4/h^2) sin^2(a h / 2) = kappa^2
+    u = lambda xp, yp: np.cos(a * xp + a * yp + 0.3)
+    sol = dtn.build_root_gpu(cfg5_op, dtn.build_tree_uniform(n, 32), want_G=False)
+    ub, rhs = manufactured(cfg5_op, sol.boundary, u)
+    assert rel(dtn.apply_schur(sol, ub), rhs) <= 1e-10
+    sol.free()
+    acc = dtn.build_root_accel(cfg5_op, dtn.build_tree_uniform(n, 32), dtn.AccelOptions(**ACCEL))
+    assert rel(dtn.apply_schur(acc, ub), rhs) <= 1e-9
+
+
+def test_config3_compressed_vs_oracle():
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spla
+    import torch
+    n, s = 1026, 1024
+    op = dtn.discretize(dtn.baseline_problem(3, s))
+    acc = dtn.build_root_accel(op, dtn.build_tree_uniform(n, 32), dtn.AccelOptions(**ACCEL))
+    ref = O.build_root_dense(O.Problem("varcoef", n, 60.0), O.Tree(n, uniform_side=32), threads=16, mode=2)
+    nb = len(ref.boundary)
+    g = _vectors(nb, 16)
+    eye = torch.eye(nb, dtype=torch.float64, device="cuda")
+    S_rec = dtn.apply_schur(acc, eye).cpu().numpy()
+    # conditioning-limited (oracle vs oracle on two partitions: 3e-9)
+    assert rel(S_rec, ref.S) <= 1e-8
+    assert rel(dtn.apply_schur(acc, g), ref.S @ g) <= 1e-8
+    # accuracy of G_hbs g against a sparse direct solve of the assembled system
+    st = op.stencil
+    idx = np.arange(s * s)
+    x, y = idx % s, idx // s
+    rows, cols, vals = [idx], [idx], [st[0]]
+    for r, (dx, dy) in enumerate([(1, 0), (-1, 0), (0, 1), (0, -1)], start=1):
+        ok = (x + dx >= 0) & (x + dx < s) & (y + dy >= 0) & (y + dy < s)
+        rows.append(idx[ok]); cols.append((idx + dx + dy * s)[ok]); vals.append(st[r][ok])
+    A = sp.csc_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(s * s, s * s))
+    b = ref.boundary
+    v = np.random.default_rng(3).standard_normal(nb)
+    rhs = np.zeros(s * s)
+    rhs[b] = v
+    ub = spla.splu(A).solve(rhs)[b]
+    err_gpu = np.linalg.norm(dtn.apply_dtn(acc, v) - ub) / np.linalg.norm(ub)
+    err_orc = np.linalg.norm(ref.G @ v - ub) / np.linalg.norm(ub)
+    assert err_gpu <= 2.0 * err_orc + 1e-9, (err_gpu, err_orc)
+
+
+def test_config3_dense_benched_defaults_vs_oracle():
+    """The dense engine at its default leaf granularity (micro boxes of 16) on the
+    config-3 operator, against the oracle (conditioning-limited bound)."""
+    n = 1026
+    sol = dtn.build_root_gpu(dtn.discretize(dtn.baseline_problem(3, 1024)), dtn.build_tree_uniform(n, 32),
+                             want_G=False)
+    ref = O.build_root_dense(O.Problem("varcoef", n, 60.0), O.Tree(n, uniform_side=32), threads=16, mode=2)
+    assert rel(sol.S_dense, ref.S) <= 1e-8
+    g = _vectors(len(ref.boundary), 16)
+    assert rel(dtn.apply_schur(sol, g), ref.S @ g) <= 1e-8
+    sol.free()
+
+
+@pytest.mark.parametrize("which", ["dense", "compressed"])
+def test_config4_discrete_harmonic(which):
+    """Config 4 (Laplace, n = 4096 interior, 16.8 M unknowns): S u_b = -(D g)_b for
+    the discrete-harmonic u = x y and u = x^2 - y^2."""
+    import torch
+    n_int = 4096
+    n = n_int + 2
+    op = dtn.discretize(dtn.baseline_problem(4, n_int))
+    tree = dtn.build_tree_uniform(n, 32)
+    st = torch.from_numpy(op.stencil).cuda()
+    if which == "dense":
+        sol = dtn.build_root_gpu(None, tree, want_G=False, stencil_device_ptr=st.data_ptr())
+    else:
+        sol = dtn.build_root_accel(None, tree, dtn.AccelOptions(**ACCEL), stencil_device_ptr=st.data_ptr())
+    del st
+    bnd = dtn.root_boundary(tree)
+    for u in (lambda xp, yp: xp * yp, lambda xp, yp: xp * xp - yp * yp):
+        ub, rhs = manufactured(op, bnd, u)
+        assert rel(dtn.apply_schur(sol, ub), rhs) <= (1e-10 if which == "dense" else 1e-9)
+    if which == "dense":
+        sol.free()
+    torch.cuda.empty_cache()

@@ -340,10 +340,13 @@ def test_repeated_compressed_builds_keep_memory_flat(H):
     assert marks[-1] <= marks[1] + (64 << 20), marks
 
 
-@pytest.mark.parametrize("crossover,compressed", [(252, True), (253, False)])
+@pytest.mark.parametrize("crossover,compressed", [(188, True), (189, False), (252, False)])
 def test_crossover_gate_is_size_at_least(H, crossover, compressed):
-    """The reference compresses a box whose boundary size is >= crossover
-    (accel_nd.cpp:682, 737); the root boundary here is 4 * 64 - 4 = 252."""
+    """The reference compresses a merged box whose boundary size is >= crossover
+    only when it has a next merge (merge_pair, accel_nd.cpp:667-689); the root's
+    W|E merge has none (:771-779), so the root is structured exactly when both
+    halves are. n_int = 64 with 16 x 16 leaves: the W / E halves are 32 x 64 boxes
+    with boundary 2 (32 + 64) - 4 = 188; the root boundary 252 does not matter."""
     import paper_1302_5995_b200 as dtn
     n = 66
     sol = dtn.build_root_accel(dtn.discretize(dtn.catalog("laplace", n)), dtn.build_tree_uniform(n, 16),
