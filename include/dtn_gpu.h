@@ -78,6 +78,15 @@ typedef struct {
    * the reduced load columns rhs_root are read with dtn_gpu_root_rhs. */
   const int64_t* load_ids;
   int32_t nloads;
+  /* 1: keep every box's S resident after the build (dtn_gpu_box_schur); 0 (default): box
+   * storage is reused level by level -- children are dropped once their parent is formed
+   * (dense_nd.cpp:215), so device memory is ~ two tree levels instead of the whole tree */
+  int32_t keep_boxes;
+  /* engine 1 (structured merges, dtn_gpu_build_accel): factor rank ell(j) of a box with a
+   * J edge of j nodes = min(j, rank_base + rank_step * floor(log2(j / 128))), rounded up to
+   * a multiple of 8; 0 = defaults (64, 8) */
+  int32_t rank_base;
+  int32_t rank_step;
 } dtn_opts;
 
 typedef struct {
@@ -86,6 +95,11 @@ typedef struct {
   int64_t max_boundary;
   double seconds;      /* device time of this level's waves */
   double flops;        /* algorithmic merge flops of this level (SURVEY 8d formula) */
+  /* LevelStats (solution_operator.hpp:18-23): the largest numerical rank at epsilon of the
+   * level's off-diagonal factors (structured merges; 0 for dense levels) and the bytes of
+   * the level's box operators (dense S + factors) */
+  int64_t max_rank;
+  uint64_t bytes;
 } dtn_level_stats;
 
 typedef struct {
@@ -98,6 +112,13 @@ typedef struct {
   double inverse_flops;   /* 2 nb^3 */
   int32_t waves;
   int32_t launches;       /* kernels launched by one build */
+  double arena_bytes;     /* device arena of the plan (liveness-packed box storage) */
+  double arena_sum_bytes; /* the same storage without reuse (every box resident) */
+  int32_t structured_merges;
+  int32_t max_rank;       /* largest numerical rank at epsilon of any factor (structured merges) */
+  double sketch_tail;     /* largest |R_ii| / |R_00| over the last 4 sketch columns (range-finder check) */
+  double exec_flops;      /* flops executed by the merge waves (structured: reduced systems + factors) */
+  int32_t rank_attempts;  /* builds run to settle the factor ranks (1 once learned for this problem) */
 } dtn_build_stats;
 
 typedef struct {

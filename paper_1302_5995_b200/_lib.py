@@ -23,18 +23,22 @@ class dtn_opts(C.Structure):
                 ("micro_max", C.c_int32), ("profile", C.c_int32), ("epsilon", C.c_double),
                 ("crossover", C.c_int64), ("nshards", C.c_int32), ("shard", C.c_int32),
                 ("export_S", C.c_void_p), ("export_lds", C.c_int64),
-                ("load_ids", C.c_void_p), ("nloads", C.c_int32)]
+                ("load_ids", C.c_void_p), ("nloads", C.c_int32), ("keep_boxes", C.c_int32),
+                ("rank_base", C.c_int32), ("rank_step", C.c_int32)]
 
 
 class dtn_level_stats(C.Structure):
     _fields_ = [("level", C.c_int32), ("boxes", C.c_int32), ("max_boundary", C.c_int64), ("seconds", C.c_double),
-                ("flops", C.c_double)]
+                ("flops", C.c_double), ("max_rank", C.c_int64), ("bytes", C.c_uint64)]
 
 
 class dtn_build_stats(C.Structure):
     _fields_ = [("build_ms", C.c_double), ("leaf_ms", C.c_double), ("merge_ms", C.c_double),
                 ("inverse_ms", C.c_double), ("merge_flops", C.c_double), ("leaf_flops", C.c_double),
-                ("inverse_flops", C.c_double), ("waves", C.c_int32), ("launches", C.c_int32)]
+                ("inverse_flops", C.c_double), ("waves", C.c_int32), ("launches", C.c_int32),
+                ("arena_bytes", C.c_double), ("arena_sum_bytes", C.c_double), ("structured_merges", C.c_int32),
+                ("max_rank", C.c_int32), ("sketch_tail", C.c_double), ("exec_flops", C.c_double),
+                ("rank_attempts", C.c_int32)]
 
 
 class dtn_kernel_stats(C.Structure):

@@ -19,6 +19,23 @@ struct NodeDev {
   int ncols;          // blocked: columns of the assembled system (total + body-load columns)
   int defer;          // blocked Schur merge whose boundary columns skip the LU's row moves and rank-kb
                       // updates: Y = L^{-1} P M_ib is formed after the LU by blocked forward substitution
+  // compressed engine (plan.hpp Node): structured merge / structured box
+  int smerge;         // 1: M is the reduced interface system [[M_jj, Z], [W, 0]] (total = ni + sys_nb)
+  int sys_nb;        // boundary columns of the blocked system (nb, or ra + rb for a structured merge)
+  int j0, jn, ell;    // J edge range in the CCW boundary and the factor rank
+  int ldq, ldf, ldg, ldr;
+  long long q1_off, q2_off, rt_off, lk_off, om_off, y1_off, y2_off, lkg_off, rkg_off, tg_off;
+};
+
+constexpr int kProbes = 4;  // range-finder probe columns appended to every factor sketch
+
+struct QrDesc {  // Householder QR of the first n columns of Y (m x (n + p), in place), the explicit Q
+                 // (m x n), and the range-finder check of the p probe columns
+  double* Y;
+  double* Q;
+  double* stat;     // [0] = #{|R_ii| > eps scale}, [1] = max over probes of |(I - Q Q^T) y| / scale
+  const double* S;  // the box's S: scale = max_i |S_ii| sqrt(k / 3) (k = sketched columns, uniform[-1,1] probes)
+  int ldy, ldq, m, n, p, lds, nbs, k;
 };
 
 struct RowGatherDesc {  // dst(i, c) = src(perm[i], c), i < rows, c < cols (perm: arena piv ints)

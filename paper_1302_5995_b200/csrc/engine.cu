@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <random>
@@ -59,6 +60,13 @@ cudaError_t launch_permute_columns(const double*, int, const int*, int, double*,
 cudaError_t launch_perm_only(const int*, int, int*, cudaStream_t);
 cudaError_t blocked_init();
 cudaError_t hbs_kernels_init();
+cudaError_t struct_init();
+cudaError_t launch_sgather_red(const KernelArgs&, const int*, int, int, cudaStream_t);
+cudaError_t launch_kk_gather(const KernelArgs&, const int*, int, int, cudaStream_t);
+cudaError_t launch_factor_gather(const KernelArgs&, const int*, int, long long, cudaStream_t);
+cudaError_t launch_omega(const KernelArgs&, const int*, int, long long, cudaStream_t);
+cudaError_t launch_hqr(const QrDesc*, int, int, int, const double*, cudaStream_t);
+cudaError_t launch_gemm_desc2(const GemmDesc2*, int, int, bool, cudaStream_t);
 int gemm_tiles(int, int);
 }  // namespace dtnb
 
@@ -110,6 +118,23 @@ struct WaveLaunch {
   int fin_off = 0, fin_tiles = 0, fin_k = 0;       // final GEMM S -= M_bi X
   bool fin_aligned = true;
   double fin_flops = 0.0;
+  // compressed engine: dense blocked merges (gather) vs structured merges (reduced system)
+  int gd_off = 0, gd_cnt = 0, gd_max_total = 0;
+  int sm_off = 0, sm_cnt = 0, sm_max_total = 0, sm_max_nb = 0;
+  long long sm_max_elems = 0;
+  int sm_copy = 0;                                  // CopyDesc: C -> aligned buffer
+  int sm_t = 0, sm_t_tiles = 0, sm_t_k = 0;         // GemmDesc: T = -L_k C
+  int sm_u = 0, sm_u_tiles = 0, sm_u_k = 0;         // GemmDesc: S -= T R_k
+  double sm_flops = 0.0;
+  int cp_off = 0, cp_cnt = 0;
+  long long cp_max_elems = 0;
+  int cp_y1 = 0, cp_y1_tiles = 0, cp_y1_k = 0;      // GemmDesc:  Y1 = S[J, :] Omega
+  int cp_y2 = 0, cp_y2_tiles = 0;                   // GemmDesc2: Y2 = S[:, J]^T Omega
+  int cp_qr = 0, cp_qr_m = 0, cp_qr_n = 0;          // QrDesc x 2 cp_cnt
+  int cp_rt = 0, cp_rt_tiles = 0;                   // GemmDesc2: R_jk^T = S[J, :]^T Q1
+  int cp_lk = 0, cp_lk_tiles = 0, cp_lk_k = 0;      // GemmDesc:  L_kj = S[:, J] Q2
+  bool cp_lk_aligned = true;
+  double cp_flops = 0.0;
 };
 
 template <class T>
@@ -196,6 +221,19 @@ struct PlanDev {
   cudaGraphExec_t gexec = nullptr;
   int graph_want_G = -1;
   int launches = 0;
+  // compressed engine descriptors (arena offsets relocated at upload) and statistics
+  std::vector<CopyDesc> h_sm_copy;
+  std::vector<GemmDesc> h_sg;
+  std::vector<GemmDesc2> h_sg2;
+  std::vector<QrDesc> h_qr;
+  CopyDesc* d_sm_copy = nullptr;
+  GemmDesc* d_sg = nullptr;
+  GemmDesc2* d_sg2 = nullptr;
+  QrDesc* d_qr = nullptr;
+  double* d_eps = nullptr;     // sketch rank threshold (written before every launch)
+  double* d_qstat = nullptr;   // per QR: numerical rank, tail (QrDesc::stat)
+  double* h_qstat = nullptr;   // pinned
+  std::vector<int> qr_node;    // node of each QR
 
   ~PlanDev() {
     if (gexec) cudaGraphExecDestroy(gexec);
@@ -207,8 +245,9 @@ struct PlanDev {
     for (void* p : std::initializer_list<void*>{d_nodes, d_pos, d_arena, d_piv, d_pivstat, d_lists, d_stencil, d_S, d_G,
                                                 d_perm, d_norm, d_inv_descs, d_W, d_LUp, d_UI, d_UI2, d_tinv, d_root_trs, d_load_col, d_F, d_F_desc, d_bs_gemm,
                                                 d_bs_copy, d_tri, d_trs, d_chk, d_bad, d_fw_copy, d_fw_gather,
-                                                d_fw_trs, d_fw_gemm})
+                                                d_fw_trs, d_fw_gemm, d_sm_copy, d_sg, d_sg2, d_qr, d_eps, d_qstat})
       if (p) cudaFree(p);
+    if (h_qstat) cudaFreeHost(h_qstat);
     if (h_pivstat) cudaFreeHost(h_pivstat);
     if (h_bad) cudaFreeHost(h_bad);
     if (h_norm) cudaFreeHost(h_norm);
@@ -252,6 +291,25 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
     d.rhs_ld = s.rhs_ld;
     d.ncols = s.total + (s.blocked ? P.key.nloads : 0);
     d.defer = 0;  // decided per wave below
+    d.smerge = s.smerge ? 1 : 0;
+    d.sys_nb = s.sys_nb;
+    d.j0 = s.j0;
+    d.jn = s.jn;
+    d.ell = s.ell;
+    d.ldq = s.ldq;
+    d.ldf = s.ldf;
+    d.ldg = s.ldg;
+    d.ldr = s.ldr;
+    d.q1_off = s.q1_off;
+    d.q2_off = s.q2_off;
+    d.rt_off = s.rt_off;
+    d.lk_off = s.lk_off;
+    d.om_off = s.om_off;
+    d.y1_off = s.y1_off;
+    d.y2_off = s.y2_off;
+    d.lkg_off = s.lkg_off;
+    d.rkg_off = s.rkg_off;
+    d.tg_off = s.tg_off;
   }
   D->ldlu = int(align_up(nb, 8));
   D->lu_off = align_up(P.arena_doubles, 32);
@@ -300,6 +358,29 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
       L.blk_max_nb = std::max(L.blk_max_nb, nd.nb);
     }
     if (L.blk_cnt) L.kb = panel_kb(L.blk_max_ni);
+    L.gd_off = int(lists.size());
+    for (int id : wv.blocked)
+      if (!P.nodes[id].smerge) {
+        lists.push_back(id);
+        ++L.gd_cnt;
+        L.gd_max_total = std::max(L.gd_max_total, P.nodes[id].total);
+      }
+    L.sm_off = int(lists.size());
+    for (int id : wv.smerge) {
+      const Node& nd = P.nodes[id];
+      lists.push_back(id);
+      ++L.sm_cnt;
+      L.sm_max_total = std::max(L.sm_max_total, nd.total);
+      L.sm_max_nb = std::max(L.sm_max_nb, nd.nb);
+      L.sm_max_elems = std::max<long long>(L.sm_max_elems, (long long)nd.nb * nd.sys_nb);
+    }
+    L.cp_off = int(lists.size());
+    for (int id : wv.compress) {
+      const Node& nd = P.nodes[id];
+      lists.push_back(id);
+      ++L.cp_cnt;
+      L.cp_max_elems = std::max<long long>(L.cp_max_elems, (long long)nd.nb * (nd.ell + kProbes));
+    }
     for (int id : wv.small) {
       const Node& nd = P.nodes[id];
       if (nd.label_level >= 0) L.level = L.level < 0 ? nd.label_level : std::min(L.level, nd.label_level);
@@ -360,7 +441,7 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
           const Node& nd = P.nodes[id];
           if (!D->h_nodes[id].defer) continue;
           const int64_t M = nd.m_off, ldm = nd.ldm;
-          const int ncy = nd.nb + P.key.nloads, ldt = int(align_up(nd.ni, 2));
+          const int ncy = nd.sys_nb + P.key.nloads, ldt = int(align_up(nd.ni, 2));
           fwc.push_back(CopyDesc{reinterpret_cast<const double*>(M + nd.ni * ldm), reinterpret_cast<double*>(toff),
                                  int(ldm), ldt, nd.ni, ncy});
           fwg.push_back(RowGatherDesc{reinterpret_cast<const double*>(toff), reinterpret_cast<double*>(M + nd.ni * ldm),
@@ -383,7 +464,7 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
             if (t >= nblk) continue;
             const int64_t M = nd.m_off, ldm = nd.ldm;
             const int k0 = t * 128, k1 = std::min(nd.ni, k0 + 128), bk = k1 - k0;
-            const int ncy = nd.nb + P.key.nloads;
+            const int ncy = nd.sys_nb + P.key.nloads;
             // left-looking: Y_k -= L[k0:k1, 0:k0] Y[0:k0] (one GEMM, K = k0: the same
             // subtractions in the same order as the right-looking block updates), then
             // Y_k <- L_kk^{-1} Y_k (unit lower)
@@ -418,7 +499,7 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
           if (sblk < 0) continue;
           const int64_t M = nd.m_off, ldm = nd.ldm;
           const int k0 = sblk * 128, k1 = std::min(nd.ni, k0 + 128), bk = k1 - k0;
-          const int ncy = nd.nb + P.key.nloads;  // boundary columns + body-load columns
+          const int ncy = nd.sys_nb + P.key.nloads;  // boundary columns + body-load columns
           // substitution variant: Y_k <- U_kk^{-1} Y_k in place, Y[0:k0] -= U[0:k0, k0:k1] Y_k
           trs.push_back(TrsmDesc{reinterpret_cast<const double*>(M + k0 + int64_t(k0) * ldm),
                                  reinterpret_cast<double*>(M + k0 + nd.ni * ldm), int(ldm), int(ldm), bk, ncy});
@@ -457,14 +538,14 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
       for (int id : wv.blocked) {
         const Node& nd = P.nodes[id];
         const int64_t M = nd.m_off, ldm = nd.ldm;
-        const int ncy = nd.nb + P.key.nloads;  // S and the body-load columns (dense_nd.cpp:181-184)
+        const int ncy = nd.sys_nb + P.key.nloads;  // S and the body-load columns (dense_nd.cpp:181-184)
         gd.push_back(GemmDesc{reinterpret_cast<const double*>(M + nd.ni), reinterpret_cast<const double*>(M + nd.ni * ldm),
-                              reinterpret_cast<double*>(M + nd.ni + nd.ni * ldm), nd.nb, ncy, nd.ni, int(ldm), int(ldm),
-                              int(ldm)});
-        L.fin_tiles = std::max(L.fin_tiles, gemm_tiles(nd.nb, ncy));
+                              reinterpret_cast<double*>(M + nd.ni + nd.ni * ldm), nd.sys_nb, ncy, nd.ni, int(ldm),
+                              int(ldm), int(ldm)});
+        L.fin_tiles = std::max(L.fin_tiles, gemm_tiles(nd.sys_nb, ncy));
         L.fin_k = std::max(L.fin_k, nd.ni);
         L.fin_aligned = L.fin_aligned && (nd.ni % 2 == 0);
-        L.fin_flops += 2.0 * nd.nb * double(nd.nb) * nd.ni;
+        L.fin_flops += 2.0 * nd.sys_nb * double(nd.sys_nb) * nd.ni;
       }
     }
     D->h_trs = std::move(trs);
@@ -478,6 +559,90 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
     D->h_bs_gemm = std::move(gd);
     D->h_bs_copy = std::move(cd);
     D->h_tri = std::move(td);
+  }
+  // compressed engine descriptors (arena offsets, relocated below)
+  {
+    auto off = [](int64_t o) { return reinterpret_cast<double*>(o); };
+    auto coff = [](int64_t o) { return reinterpret_cast<const double*>(o); };
+    for (size_t w = 0; w < P.waves.size(); ++w) {
+      WaveLaunch& L = D->wl[w];
+      const Wave& wv = P.waves[w];
+      // structured merges: C (the reduced system's Schur complement) -> aligned copy,
+      // T = -L_k C, S -= T R_k
+      L.sm_copy = int(D->h_sm_copy.size());
+      for (int id : wv.smerge) {
+        const Node& nd = P.nodes[id];
+        D->h_sm_copy.push_back(CopyDesc{coff(nd.m_off + nd.ni + int64_t(nd.ni) * nd.ldm), off(nd.cbuf_off), nd.ldm,
+                                        nd.ldr, nd.sys_nb, nd.sys_nb});
+      }
+      L.sm_t = int(D->h_sg.size());
+      for (int id : wv.smerge) {
+        const Node& nd = P.nodes[id];
+        D->h_sg.push_back(GemmDesc{coff(nd.lkg_off), coff(nd.cbuf_off), off(nd.tg_off), nd.nb, nd.sys_nb, nd.sys_nb,
+                                   nd.ldg, nd.ldr, nd.ldg});
+        L.sm_t_tiles = std::max(L.sm_t_tiles, gemm_tiles(nd.nb, nd.sys_nb));
+        L.sm_t_k = std::max(L.sm_t_k, nd.sys_nb);
+        L.sm_flops += 2.0 * nd.nb * double(nd.sys_nb) * nd.sys_nb;
+      }
+      L.sm_u = int(D->h_sg.size());
+      for (int id : wv.smerge) {
+        const Node& nd = P.nodes[id];
+        D->h_sg.push_back(GemmDesc{coff(nd.tg_off), coff(nd.rkg_off), off(nd.s_off), nd.nb, nd.nb, nd.sys_nb, nd.ldg,
+                                   nd.ldr, nd.ld});
+        L.sm_u_tiles = std::max(L.sm_u_tiles, gemm_tiles(nd.nb, nd.nb));
+        L.sm_u_k = std::max(L.sm_u_k, nd.sys_nb);
+        L.sm_flops += 2.0 * nd.nb * double(nd.nb) * nd.sys_nb;
+      }
+      // factors of the wave's structured boxes (randomized range finder + Householder QR)
+      L.cp_y1 = int(D->h_sg.size());
+      for (int id : wv.compress) {
+        const Node& nd = P.nodes[id];
+        D->h_sg.push_back(GemmDesc{coff(nd.s_off + nd.j0), coff(nd.om_off), off(nd.y1_off), nd.jn, nd.ell + kProbes,
+                                   nd.nb, nd.ld, nd.ldf, nd.ldq});
+        L.cp_y1_tiles = std::max(L.cp_y1_tiles, gemm_tiles(nd.jn, nd.ell + kProbes));
+        L.cp_y1_k = std::max(L.cp_y1_k, nd.nb);
+        L.cp_flops += 2.0 * nd.jn * double(nd.nb) * nd.ell;
+      }
+      L.cp_lk = int(D->h_sg.size());
+      for (int id : wv.compress) {
+        const Node& nd = P.nodes[id];
+        D->h_sg.push_back(GemmDesc{coff(nd.s_off + int64_t(nd.j0) * nd.ld), coff(nd.q2_off), off(nd.lk_off), nd.nb,
+                                   nd.ell, nd.jn, nd.ld, nd.ldq, nd.ldf});
+        L.cp_lk_tiles = std::max(L.cp_lk_tiles, gemm_tiles(nd.nb, nd.ell));
+        L.cp_lk_k = std::max(L.cp_lk_k, nd.jn);
+        L.cp_lk_aligned = L.cp_lk_aligned && ((nd.s_off + int64_t(nd.j0) * nd.ld) % 2 == 0) && (nd.ld % 2 == 0);
+        L.cp_flops += 2.0 * nd.jn * double(nd.nb) * nd.ell;
+      }
+      L.cp_y2 = int(D->h_sg2.size());
+      for (int id : wv.compress) {  // S[:, J]^T: row-major view of the J columns
+        const Node& nd = P.nodes[id];
+        D->h_sg2.push_back(GemmDesc2{coff(nd.s_off + int64_t(nd.j0) * nd.ld), nullptr, coff(nd.om_off), off(nd.y2_off),
+                                     nd.jn, nd.ell + kProbes, nd.nb, nd.ld, 0, int(align_up(nd.nb, 16)), nd.nb,
+                                     nd.ldf, nd.ldq});
+        L.cp_y2_tiles = std::max(L.cp_y2_tiles, gemm_tiles(nd.jn, nd.ell + kProbes));
+        L.cp_flops += 2.0 * nd.jn * double(nd.nb) * nd.ell;
+      }
+      L.cp_rt = int(D->h_sg2.size());
+      for (int id : wv.compress) {  // S[J, :]^T: row-major view of the J rows
+        const Node& nd = P.nodes[id];
+        D->h_sg2.push_back(GemmDesc2{coff(nd.s_off + nd.j0), nullptr, coff(nd.q1_off), off(nd.rt_off), nd.nb, nd.ell,
+                                     nd.jn, nd.ld, 0, int(align_up(nd.jn, 16)), nd.jn, nd.ldq, nd.ldf});
+        L.cp_rt_tiles = std::max(L.cp_rt_tiles, gemm_tiles(nd.nb, nd.ell));
+        L.cp_flops += 2.0 * nd.jn * double(nd.nb) * nd.ell;
+      }
+      L.cp_qr = int(D->h_qr.size());
+      for (int q = 0; q < 2; ++q)
+        for (int id : wv.compress) {
+          const Node& nd = P.nodes[id];
+          D->h_qr.push_back(QrDesc{off(q ? nd.y2_off : nd.y1_off), off(q ? nd.q2_off : nd.q1_off),
+                                   reinterpret_cast<double*>(int64_t(2 * D->h_qr.size())), coff(nd.s_off), nd.ldq,
+                                   nd.ldq, nd.jn, nd.ell, kProbes, nd.ld, nd.nb, nd.nb - nd.jn});
+          D->qr_node.push_back(id);
+          L.cp_qr_m = std::max(L.cp_qr_m, nd.jn);
+          L.cp_qr_n = std::max(L.cp_qr_n, nd.ell + kProbes);
+          L.cp_flops += 8.0 * nd.jn * double(nd.ell) * nd.ell;  // factor + form Q
+        }
+    }
   }
   D->root_list_off = int(lists.size());
   lists.push_back(D->root_lu_node);
@@ -515,6 +680,19 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
     for (auto& g : D->h_fw_gather) { g.src = rel(g.src); g.dst = rel(g.dst); }
     for (auto& t : D->h_fw_trs) { t.U = rel(t.U); t.Y = rel(t.Y); }
     for (auto& g : D->h_fw_gemm) { g.A = rel(g.A); g.B = rel(g.B); g.C = rel(g.C); }
+    for (auto& c : D->h_sm_copy) { c.src = rel(c.src); c.dst = rel(c.dst); }
+    for (auto& g : D->h_sg) { g.A = rel(g.A); g.B = rel(g.B); g.C = rel(g.C); }
+    for (auto& g : D->h_sg2) { g.A = rel(g.A); g.B = rel(g.B); g.C = rel(g.C); }
+    if (!D->h_qr.empty()) {
+      D->d_qstat = dalloc<double>(2 * D->h_qr.size());
+      CK(cudaMallocHost(&D->h_qstat, 2 * D->h_qr.size() * sizeof(double)));
+    }
+    for (auto& q : D->h_qr) {
+      q.Y = rel(q.Y);
+      q.Q = rel(q.Q);
+      q.S = rel(q.S);
+      q.stat = D->d_qstat + reinterpret_cast<int64_t>(q.stat);
+    }
     auto upload_vec = [&](auto& h, auto*& d) {
       if (h.empty()) return;
       d = dalloc<std::remove_reference_t<decltype(h[0])>>(h.size());
@@ -524,6 +702,11 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
     upload_vec(D->h_fw_gather, D->d_fw_gather);
     upload_vec(D->h_fw_trs, D->d_fw_trs);
     upload_vec(D->h_fw_gemm, D->d_fw_gemm);
+    upload_vec(D->h_sm_copy, D->d_sm_copy);
+    upload_vec(D->h_sg, D->d_sg);
+    upload_vec(D->h_sg2, D->d_sg2);
+    upload_vec(D->h_qr, D->d_qr);
+    D->d_eps = dalloc<double>(1);
     D->d_trs = dalloc<TrsmDesc>(D->h_trs.size());
     if (!D->h_trs.empty())
       CK(cudaMemcpy(D->d_trs, D->h_trs.data(), D->h_trs.size() * sizeof(TrsmDesc), cudaMemcpyHostToDevice));
@@ -702,11 +885,12 @@ bool use_fused() {  // DTN_NO_FUSED=1: the unfused look-ahead (next-panel update
 // aggregated per kernel class with the algorithmic work of each launch.
 enum KClass {
   K_SMALL = 0, K_GATHER, K_PANEL, K_ROWPANEL, K_TRAILING, K_BACKSUB, K_SCHUR, K_COPY, K_INV_TRSM, K_INV_GEMM, K_MISC,
-  K_SUBST, K_COUNT
+  K_SUBST, K_SGATHER, K_SGEMM, K_COMPRESS, K_COUNT
 };
 const char* kclass_name(int k) {
   static const char* names[K_COUNT] = {"small_elim", "gather",   "panel",    "rowpanel", "trailing_gemm", "backsub_gemm",
-                                       "schur_gemm", "copy",     "inv_trsm", "inv_gemm", "misc", "backsub_subst"};
+                                       "schur_gemm", "copy",     "inv_trsm", "inv_gemm", "misc", "backsub_subst",
+                                       "struct_gather", "struct_gemm", "sketch_qr"};
   return names[k];
 }
 struct Prof {
@@ -857,7 +1041,11 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
       const int* hlst = hl.data() + L.blk_off;
       double gb = 0.0;
       for (int i = 0; i < L.blk_cnt; ++i) gb += 16.0 * double(P.nodes[hlst[i]].total) * P.nodes[hlst[i]].total;
-      run(K_GATHER, 0.0, gb, [&] { return launch_gather(a, lst, L.blk_cnt, L.blk_max_total, st); });
+      run(K_GATHER, 0.0, gb,
+          [&] { return launch_gather(a, D.d_lists + L.gd_off, L.gd_cnt, L.gd_max_total, st); });
+      if (L.sm_cnt)  // structured merges: the reduced interface system (Step 1)
+        run(K_SGATHER, 0.0, 0.0,
+            [&] { return launch_sgather_red(a, D.d_lists + L.sm_off, L.sm_cnt, L.sm_max_total, st); });
       // deferred boundary columns need L in the final row order (P A = L U): the row
       // moves of every step are then also applied to the factored columns (swap_left)
       blocked_lu(lst, hlst, L.blk_cnt, L.blk_max_ni, L.blk_max_total, L.blk_max_nb, L.kb, L.fw_cnt > 0, true);
@@ -912,6 +1100,34 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
       run(K_SCHUR, L.fin_flops, 0.0, [&] {
         return launch_gemm_desc(D.d_bs_gemm + L.fin_off, L.blk_cnt, L.fin_tiles, L.fin_k, -1.0, 1.0, st,
                                 L.fin_aligned);
+      });
+      if (L.sm_cnt) {  // Steps 2-3: S = M_kk + L_k C R_k
+        const int* sl = D.d_lists + L.sm_off;
+        run(K_SGATHER, 0.0, 0.0, [&] { return launch_kk_gather(a, sl, L.sm_cnt, L.sm_max_nb, st); });
+        run(K_SGATHER, 0.0, 0.0, [&] { return launch_factor_gather(a, sl, L.sm_cnt, L.sm_max_elems, st); });
+        run(K_COPY, 0.0, 0.0, [&] { return launch_copy2d_batched(D.d_sm_copy + L.sm_copy, L.sm_cnt, st); });
+        run(K_SGEMM, L.sm_flops * 0.0, 0.0, [&] {
+          return launch_gemm_desc(D.d_sg + L.sm_t, L.sm_cnt, L.sm_t_tiles, L.sm_t_k, -1.0, 0.0, st, true);
+        });
+        run(K_SGEMM, L.sm_flops, 0.0, [&] {
+          return launch_gemm_desc(D.d_sg + L.sm_u, L.sm_cnt, L.sm_u_tiles, L.sm_u_k, -1.0, 1.0, st, true);
+        });
+      }
+    }
+    if (L.cp_cnt) {  // the wave's structured boxes: factors for their next merge
+      const int* cl = D.d_lists + L.cp_off;
+      run(K_COMPRESS, 0.0, 0.0, [&] { return launch_omega(a, cl, L.cp_cnt, L.cp_max_elems, st); });
+      run(K_SGEMM, 0.0, 0.0, [&] {
+        return launch_gemm_desc(D.d_sg + L.cp_y1, L.cp_cnt, L.cp_y1_tiles, L.cp_y1_k, 1.0, 0.0, st, false);
+      });
+      run(K_SGEMM, 0.0, 0.0,
+          [&] { return launch_gemm_desc2(D.d_sg2 + L.cp_y2, L.cp_cnt, L.cp_y2_tiles, false, st); });
+      run(K_COMPRESS, 0.0, 0.0,
+          [&] { return launch_hqr(D.d_qr + L.cp_qr, 2 * L.cp_cnt, L.cp_qr_m, L.cp_qr_n, D.d_eps, st); });
+      run(K_SGEMM, 0.0, 0.0,
+          [&] { return launch_gemm_desc2(D.d_sg2 + L.cp_rt, L.cp_cnt, L.cp_rt_tiles, false, st); });
+      run(K_SGEMM, L.cp_flops, 0.0, [&] {
+        return launch_gemm_desc(D.d_sg + L.cp_lk, L.cp_cnt, L.cp_lk_tiles, L.cp_lk_k, 1.0, 0.0, st, L.cp_lk_aligned);
       });
     }
     if (events) CK(cudaEventRecord(D.ev_wave[w], st));
@@ -1041,6 +1257,8 @@ struct dtn_ctx {
   // are shared state (recursive: the compressed build calls the other entries)
   std::recursive_mutex mu;
   int device = 0;
+  // structured merges: factor ranks learned per problem family (dtn_gpu_build)
+  std::map<std::string, std::vector<std::pair<int, int>>> learned_ranks;
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   std::vector<std::unique_ptr<PlanDev>> plans;
@@ -1129,6 +1347,7 @@ int dtn_gpu_create(dtn_ctx** out, int device) {
     CK(blocked_init());
     CK(misc_init());
     CK(hbs_kernels_init());
+    CK(struct_init());
     auto* c = new dtn_ctx;
     c->device = device;
     CK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
@@ -1159,12 +1378,18 @@ int dtn_gpu_set_stream(dtn_ctx* ctx, void* stream) {
   return DTN_OK;
 }
 
-int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, dtn_op** out) {
+}  // extern "C"
+
+namespace {
+
+int build_impl(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts,
+               const std::vector<std::pair<int, int>>& ell_over, dtn_op** out) {
   return guarded(ctx, [&] {
     if (!ctx || !prob || !opts || !out) throw std::invalid_argument("dtn_gpu_build: null argument");
     if (prob->n < 4) throw std::invalid_argument("discretize: n must be >= 4");
     if (!prob->stencil) throw std::invalid_argument("dtn_gpu_build: null stencil");
-    if (opts->engine != 0) throw std::invalid_argument("dtn_gpu_build: only the dense engine is available");
+    if (opts->engine != 0 && opts->engine != 1)
+      throw std::invalid_argument("dtn_gpu_build: engine must be 0 (dense) or 1 (structured merges)");
     CK(cudaSetDevice(ctx->device));
     PlanKey key;
     key.n = prob->n;
@@ -1176,6 +1401,17 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
     key.shard = opts->shard;
     if (key.nshards == 1) key.shard = -1;
     key.nloads = int(opts->nloads);
+    key.keep = opts->keep_boxes ? 1 : 0;
+    if (opts->engine == 1) {  // compressed engine: structured merges above the crossover
+      if (opts->nloads > 0)
+        throw std::invalid_argument("dtn_gpu_build: body loads ride through the dense merges (engine 0)");
+      if (opts->crossover < 1) throw std::invalid_argument("dtn_gpu_build: crossover must be >= 1");
+      key.structured = 1;
+      key.crossover = opts->crossover;
+      key.ell_base = opts->rank_base > 0 ? opts->rank_base : 64;
+      key.ell_step = opts->rank_step > 0 ? opts->rank_step : 8;
+      key.ell_over = ell_over;
+    }
     if (opts->nloads < 0 || (opts->nloads > 0 && !opts->load_ids))
       throw std::invalid_argument("dtn_gpu_build: bad body-load list");
     if (key.nloads > 0 && key.nshards > 1)
@@ -1208,6 +1444,8 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
     std::unique_ptr<Prof> prof;
     CK(cudaMemcpyAsync(D->d_stencil, prob->stencil, size_t(5 * D->nu) * sizeof(double),
                        prob->stencil_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    const double eps = opts->epsilon > 0.0 ? opts->epsilon : 1e-10;  // numerical-rank threshold of the factors
+    CK(cudaMemcpyAsync(D->d_eps, &eps, sizeof(double), cudaMemcpyHostToDevice, st));
     if (key.nloads > 0) {  // LoadPanel (dense_nd.hpp:29-32): unit loads, distinct strictly-interior unknowns
       std::vector<int> col(size_t(D->nu), -1);
       const int s_ = key.n - 2;
@@ -1274,6 +1512,8 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
     CK(launch_pivot_screen(D->d_pivstat, D->d_chk, int(nstat), want_G ? 1 : 0, D->d_bad, st));
     CK(cudaMemcpyAsync(D->h_bad, D->d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
     if (want_G) CK(cudaMemcpyAsync(D->h_norm, D->d_norm, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    if (!D->h_qr.empty())
+      CK(cudaMemcpyAsync(D->h_qstat, D->d_qstat, 2 * D->h_qr.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
     const auto hs0 = std::chrono::steady_clock::now();
     CK(cudaStreamSynchronize(st));
     if (std::getenv("DTN_TRACE_BUILD"))
@@ -1331,12 +1571,37 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
     s.inverse_flops = want_G ? 2.0 * double(D->nb) * D->nb * D->nb : 0.0;
     s.waves = int(P.waves.size());
     s.launches = D->launches;
+    s.arena_bytes = double(P.arena_peak_bytes);
+    s.arena_sum_bytes = double(P.arena_sum_bytes);
     std::vector<dtn_level_stats> lv(P.depth + 1);
     for (int l = 0; l <= P.depth; ++l) {
       lv[l].level = l;
       lv[l].boxes = int(P.levels[l].size());
-      for (int id : P.levels[l])
+      for (int id : P.levels[l]) {
         lv[l].max_boundary = std::max<int64_t>(lv[l].max_boundary, perimeter_size(P.boxes[id].r));
+        const int v = P.boxes[id].node;
+        if (v < 0 || !P.active[v]) continue;
+        const Node& nd = P.nodes[v];
+        lv[l].bytes += uint64_t(8) * uint64_t(nd.nb) * uint64_t(nd.nb) +
+                       (nd.factors ? uint64_t(8) * uint64_t(nd.ell) * uint64_t(2 * nd.jn + 2 * nd.nb) : 0);
+      }
+    }
+    // structured merges: numerical ranks and the range-finder check per level
+    s.exec_flops = 0.0;
+    for (const WaveLaunch& W : D->wl) s.exec_flops += W.sm_flops + W.cp_flops + W.fin_flops;
+    for (const Node& nd : P.nodes)
+      if (nd.smerge) {
+        ++s.structured_merges;
+        s.exec_flops += merge_flop_count(nd.ni, nd.sys_nb) - 2.0 * nd.sys_nb * double(nd.sys_nb) * nd.ni;
+      }
+    for (size_t q = 0; q < D->h_qr.size(); ++q) {
+      const Node& nd = P.nodes[size_t(D->qr_node[q])];
+      const int rank = int(D->h_qstat[2 * q]);
+      s.max_rank = std::max(s.max_rank, rank);
+      s.sketch_tail = std::max(s.sketch_tail, D->h_qstat[2 * q + 1]);
+      // (a W/E half counts with its merge_four's level, a reference leaf with the leaves)
+      const int l = std::min(std::max(nd.label_level >= 0 ? nd.label_level : P.depth, 0), P.depth);
+      lv[size_t(l)].max_rank = std::max<int64_t>(lv[size_t(l)].max_rank, rank);
     }
     cudaEvent_t prev = D->ev_start;
     for (size_t w = 0; w < D->wl.size(); ++w) {
@@ -1392,6 +1657,87 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
     D->busy = true;
     *out = op;
   });
+}
+
+// Range-finder acceptance: the probe residual |(I - Q Q^T) S[J, K] w| relative to the box
+// operator's scale must be <= factor * eps (DTN_RANK_TOL, default 1: the truncation of a
+// factor then perturbs S by ~eps |S|, the scale of the reference's eps sigma_max cuts).
+double rank_tol_factor() {
+  static const double v = [] {
+    const char* e = std::getenv("DTN_RANK_TOL");
+    return e ? std::atof(e) : 1.0;
+  }();
+  return v;
+}
+
+// Factor ranks that failed the range-finder check of a structured build (tail of the
+// sketch's R diagonal above tol): raise them by half (at least 16), per J edge size.
+bool raise_ranks(const dtn_op* op, double tol, std::vector<std::pair<int, int>>& over) {
+  const PlanDev& D = *op->plan;
+  bool raised = false;
+  for (size_t q = 0; q < D.h_qr.size(); ++q) {
+    if (!(D.h_qstat[2 * q + 1] > tol)) continue;
+    const Node& nd = D.P.nodes[size_t(D.qr_node[q])];
+    if (nd.ell >= nd.jn) continue;  // already exact
+    const int want = std::min({nd.jn, 252, int(align_up(nd.ell + std::max(16, nd.ell / 2), 8))});
+    if (want <= nd.ell) continue;  // at the cap
+    auto it = std::find_if(over.begin(), over.end(), [&](const auto& e) { return e.first == nd.jn; });
+    if (it == over.end()) {
+      over.push_back({nd.jn, want});
+      raised = true;
+    } else if (it->second < want) {
+      it->second = want;
+      raised = true;
+    }
+  }
+  return raised;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, dtn_op** out) {
+  if (!ctx || !opts || opts->engine != 1) return build_impl(ctx, prob, opts, {}, out);
+  // structured merges: the factor ranks adapt to the operator. A build whose sketches
+  // did not resolve a factor to eps (the probe residual relative to the box operator's
+  // scale, cf. lowrank_from_dense's eps sigma_max cut, lowrank.cpp:27-36) is repeated
+  // with those ranks raised; the learned ranks are kept in the context for later builds
+  // of the same problem family.
+  const double eps = opts->epsilon > 0.0 ? opts->epsilon : 1e-10;
+  char fam[256];
+  std::snprintf(fam, sizeof(fam), "%d/%d/%d/%lld/%d/%d/%d/%d/%g", prob ? prob->n : 0, opts->n_leaf, opts->leaf_side,
+                (long long)opts->crossover, opts->nshards, opts->shard, opts->rank_base, opts->rank_step, eps);
+  std::vector<std::pair<int, int>> over;
+  {
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    auto it = ctx->learned_ranks.find(fam);
+    if (it != ctx->learned_ranks.end()) over = it->second;
+  }
+  for (int attempt = 0;; ++attempt) {
+    dtn_op* op = nullptr;
+    const int rc = build_impl(ctx, prob, opts, over, &op);
+    if (rc != DTN_OK) return rc;
+    std::vector<std::pair<int, int>> next = over;
+    if (attempt < 6 && raise_ranks(op, rank_tol_factor() * eps, next)) {
+      PlanDev* stale = op->plan;
+      dtn_gpu_free(op);
+      {  // the failed attempt's plan (arena, graph) is not reused: drop it
+        std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        auto& pl = ctx->plans;
+        pl.erase(std::remove_if(pl.begin(), pl.end(), [&](const auto& p) { return p.get() == stale; }), pl.end());
+      }
+      over = std::move(next);
+      std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+      ctx->learned_ranks[fam] = over;
+      continue;
+    }
+    op->stats.rank_attempts = attempt + 1;
+    *out = op;
+    return DTN_OK;
+  }
 }
 
 void dtn_gpu_free(dtn_op* op) {
@@ -1612,6 +1958,8 @@ int dtn_gpu_box_schur(const dtn_op* op, int32_t box, double* S) {
     const int node = D.P.boxes[box].node;
     if (node < 0) throw std::invalid_argument("dtn_gpu_box_schur: empty box");
     if (!D.P.active[node]) throw std::invalid_argument("dtn_gpu_box_schur: box not computed by this (sharded) build");
+    if (!D.P.key.keep && node != D.P.root)
+      throw std::invalid_argument("dtn_gpu_box_schur: box storage was reused (build with opts.keep_boxes = 1)");
     const Node& nd = D.P.nodes[node];
     CK(cudaSetDevice(op->ctx->device));
     CK(cudaMemcpy2D(S, size_t(nd.nb) * 8, D.d_arena + nd.s_off, size_t(nd.ld) * 8, size_t(nd.nb) * 8, nd.nb,
@@ -1979,7 +2327,9 @@ int dtn_gpu_build_accel(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* o
     dense_root = depth == 0 || nb_w < opts->crossover || nb_e < opts->crossover;
   }
   dtn_opts o = *opts;
-  o.engine = 0;
+  // engine 1: structured merges above the crossover (accel_merge on the B200); engine 0:
+  // exact dense merges with only the root compressed. Body loads ride the dense merges.
+  o.engine = (opts->engine == 1 && opts->nloads == 0) ? 1 : 0;
   o.want_G = dense_root ? 1 : 0;
   o.export_S = nullptr;
   dtn_op* op = nullptr;

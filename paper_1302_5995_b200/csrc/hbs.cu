@@ -945,15 +945,23 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
       if (H.apply_graph) cudaGraphExecDestroy(H.apply_graph);
       H.apply_graph = nullptr;
       cudaGraph_t g = nullptr;
-      HCK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      // captured on a private stream (nothing executes during capture; the caller's
+      // stream may be the legacy default stream, which cannot be captured)
+      cudaStream_t cap = nullptr;
+      HCK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+      struct CapGuard {
+        cudaStream_t s;
+        ~CapGuard() { cudaStreamDestroy(s); }
+      } cap_guard{cap};
+      HCK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
       try {
-        launch_all(st);
+        launch_all(cap);
       } catch (...) {
-        cudaStreamEndCapture(st, &g);
+        cudaStreamEndCapture(cap, &g);
         if (g) cudaGraphDestroy(g);
         throw;
       }
-      HCK(cudaStreamEndCapture(st, &g));
+      HCK(cudaStreamEndCapture(cap, &g));
       const cudaError_t e = cudaGraphInstantiate(&H.apply_graph, g, 0);
       cudaGraphDestroy(g);
       HCK(e);

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <map>
 #include <stdexcept>
 #include <string>
 
@@ -290,6 +291,7 @@ Plan make_plan(const PlanKey& key) {
   for (int lev = P.depth; lev >= 0; --lev) {
     for (int id : P.levels[lev]) {
       RefBox& bx = P.boxes[id];
+      const int before = int(P.nodes.size());
       if (lev == P.depth) {
         bx.node = B.leaf_node(bx.r, id);
       } else {
@@ -297,7 +299,18 @@ Plan make_plan(const PlanKey& key) {
         const int nw = P.boxes[bx.children[2]].node, ne = P.boxes[bx.children[3]].node;
         const int w = B.add_merge(sw, nw, lev, id, true);
         const int e = B.add_merge(se, ne, lev, id, true);
+        // merge_four's halves merge W|E next: their J edges face each other
+        // (build_root_accel's merge_pair(..., JSide::east / west), accel_nd.cpp:771-776)
+        if (w >= before) P.nodes[w].jside = 2;
+        if (e >= before) P.nodes[e].jside = 3;
         bx.node = B.add_merge(w, e, lev, id, true);
+      }
+      // a box's own J edge faces its sibling in the next merge_four: SW / SE merge
+      // upward (north), NW / NE downward (child_j_side, accel_nd.cpp:661-665)
+      if (bx.node >= before && lev > 0) {
+        const RefBox& par = P.boxes[bx.parent];
+        const int ci = int(std::find(par.children, par.children + 4, id) - par.children);
+        P.nodes[bx.node].jside = ci < 2 ? 0 : 1;
       }
       if (bx.node >= 0 && P.nodes[bx.node].ref_box < 0) P.nodes[bx.node].ref_box = id;
     }
@@ -349,59 +362,205 @@ Plan make_plan(const PlanKey& key) {
       (nd.label_level >= 0 ? P.merge_flops : P.micro_flops) += merge_flop_count(nd.ni, nd.nb);
     }
   }
-  // waves and storage
+  // parents (the consumer of each node's S)
+  for (int i = 0; i < int(P.nodes.size()); ++i) {
+    const Node& nd = P.nodes[i];
+    if (nd.kind == NodeKind::merge) {
+      P.nodes[nd.a].parent = i;
+      P.nodes[nd.b].parent = i;
+    }
+  }
+  std::vector<char> is_input(P.nodes.size(), 0);
+  for (int v : P.inputs) is_input[v] = 1;
+  for (auto& nd : P.nodes) {
+    nd.pos_n = nd.kind == NodeKind::merge ? nd.ni + nd.nb : nd.total;
+    nd.sys_nb = nd.nb;
+  }
+  // compressed engine: structured boxes and structured merges, bottom-up in build
+  // order (merge_pair, accel_nd.cpp:667-689; leaves :728-744): a merge of two
+  // structured boxes is structured (accel_merge); otherwise the merge is dense and its
+  // result is compressed (compress_box) when it has a next merge and size >= crossover
+  if (key.structured) {
+    for (int i = 0; i < int(P.nodes.size()); ++i) {
+      Node& nd = P.nodes[i];
+      if (!P.active[i] && !is_input[i]) continue;
+      const bool tree_box = nd.label_level >= 0 || nd.ref_box >= 0;  // a reference box or a W/E half
+      if (!tree_box || is_input[i]) continue;
+      const bool kids = nd.kind == NodeKind::merge && P.active[nd.a] && P.active[nd.b] &&
+                        (P.nodes[nd.a].factors || P.nodes[nd.a].exact) &&
+                        (P.nodes[nd.b].factors || P.nodes[nd.b].exact) && !is_input[nd.a] && !is_input[nd.b];
+      // a structured merge needs both children in factored form; children whose factors
+      // would be full rank ("exact") merge densely -- the same result, fewer flops
+      nd.smerge = kids && P.nodes[nd.a].factors && P.nodes[nd.b].factors;
+      if (nd.jside >= 0 && nd.r.w() >= 3 && nd.r.h() >= 3 && (kids || nd.nb >= key.crossover)) {
+        nd.factors = true;
+        const int w = nd.r.w(), h = nd.r.h();
+        switch (nd.jside) {
+          case 0: nd.j0 = w + h - 1; nd.jn = w - 2; break;       // north, x1-1 .. x0+1
+          case 1: nd.j0 = 1; nd.jn = w - 2; break;               // south, x0+1 .. x1-1
+          case 2: nd.j0 = w; nd.jn = h - 2; break;               // east, y0+1 .. y1-1
+          default: nd.j0 = 2 * w + h - 2; nd.jn = h - 2; break;  // west, y1-1 .. y0+1
+        }
+        int ell = key.ell_base;
+        for (int t = 256; t <= nd.jn; t *= 2) ell += key.ell_step;
+        ell = int(align_up(ell, 8));
+        for (const auto& [jn, e] : key.ell_over)
+          if (jn == nd.jn) ell = std::max(ell, e);
+        nd.ell = std::min({ell, nd.jn, 252});  // (+ 4 probes <= the QR kernel's 256 columns)
+        if (2 * nd.ell >= nd.jn) {  // rank >= half the edge: no compression to gain, keep S exact
+          nd.factors = false;
+          nd.exact = true;
+          nd.ell = nd.jn;
+        }
+      }
+    }
+    for (auto& nd : P.nodes)
+      if (nd.smerge) {
+        const Node& a = P.nodes[nd.a];
+        const Node& b = P.nodes[nd.b];
+        nd.sys_nb = a.ell + b.ell;
+        nd.total = nd.ni + nd.sys_nb;
+        // the interface rows are J_a then J_b, each in its box's CCW order
+        // (interface_coupling's anti-diagonal pairing, accel_nd.cpp:169-215)
+        bool ok = a.jn + b.jn == nd.ni;
+        for (int i = 0; ok && i < nd.ni; ++i) {
+          const int src = P.pos[size_t(nd.pos_off + i)].src;
+          ok = i < a.jn ? src == a.j0 + i : src == -(b.j0 + i - a.jn) - 1;
+        }
+        if (!ok) throw std::logic_error("structured merge: interface is not the children's J edges");
+      }
+  }
+  // waves
   int nw = 0;
   for (auto& nd : P.nodes) nw = std::max(nw, nd.wave + 1);
   P.waves.assign(nw, {});
-  int64_t off = 0, poff = 0;
-  std::vector<char> is_input(P.nodes.size(), 0);
-  for (int v : P.inputs) is_input[v] = 1;
+  const int nl = key.nloads;
   for (int i = 0; i < int(P.nodes.size()); ++i) {
     Node& nd = P.nodes[i];
-    if (!P.active[i] && !is_input[i]) continue;  // not computed, not read: no storage
+    if (!P.active[i] || is_input[i]) continue;
     Wave& wv = P.waves[nd.wave];
-    const int nl = key.nloads;
-    if (is_input[i]) {  // provided by the caller: compact S storage only
-      nd.ld = std::max(nd.nb, 1);
-      nd.s_off = off;
-      off = align_up(off + int64_t(nd.ld) * nd.nb, 32);
-      continue;
-    }
     if (nd.kind == NodeKind::micro) {
       wv.micro.push_back(i);
-    } else if (nd.total + nl <= key.small_max) {  // (load columns ride in the same registers)
+    } else if (!nd.smerge && nd.total + nl <= key.small_max) {  // (load columns ride in the same registers)
       wv.small.push_back(i);
     } else {
       nd.blocked = true;
       wv.blocked.push_back(i);
+      if (nd.smerge) wv.smerge.push_back(i);
       wv.max_ni_blocked = std::max(wv.max_ni_blocked, nd.ni);
     }
-    if (nd.blocked) {
-      nd.ldm = int(align_up(nd.total, 8));
-      nd.m_off = off;
-      off = align_up(off + int64_t(nd.ldm) * (nd.total + nl), 32);
-      nd.s_off = nd.m_off + nd.ni + int64_t(nd.ni) * nd.ldm;
-      nd.ld = nd.ldm;
-      nd.rhs_off = nd.m_off + nd.ni + int64_t(nd.total) * nd.ldm;
-      nd.rhs_ld = nd.ldm;
-      nd.piv_off = poff;
-      poff += align_up(std::max(nd.ni, 1), 4) + 260;  // ipiv + two per-panel row-move lists + flags
-      const int64_t nblk = (nd.ni + 127) / 128;
-      nd.uinv_off = off;
-      off = align_up(off + nblk * 2 * 128 * 128, 32);
-      nd.t_off = off;
-      off = align_up(off + int64_t(128) * std::max(nd.nb + nl, 1), 32);
-    } else {
-      nd.ld = std::max(nd.nb, 1);
-      nd.s_off = off;
-      off = align_up(off + int64_t(nd.ld) * nd.nb, 32);
-      if (nl > 0) {
-        nd.rhs_ld = nd.ld;
-        nd.rhs_off = off;
-        off = align_up(off + int64_t(nd.rhs_ld) * nl, 32);
+    if (nd.factors) wv.compress.push_back(i);
+  }
+  // storage: one arena, packed by liveness -- a node's S (and factors) live from its
+  // wave to its parent's wave (children are dropped level by level,
+  // dense_nd.cpp:215), scratch only during its own wave; key.keep keeps everything
+  struct Arena {
+    std::map<int64_t, int64_t> free;  // offset -> size (doubles), coalesced
+    int64_t end = 0;
+    int64_t get(int64_t n) {
+      n = align_up(std::max<int64_t>(n, 1), 32);
+      for (auto it = free.begin(); it != free.end(); ++it)
+        if (it->second >= n) {
+          const int64_t off = it->first, rest = it->second - n;
+          free.erase(it);
+          if (rest > 0) free[off + n] = rest;
+          return off;
+        }
+      const int64_t off = end;
+      end += n;
+      return off;
+    }
+    void put(int64_t off, int64_t n) {
+      n = align_up(std::max<int64_t>(n, 1), 32);
+      auto it = free.emplace(off, n).first;
+      auto nx = std::next(it);
+      if (nx != free.end() && it->first + it->second == nx->first) {
+        it->second += nx->second;
+        free.erase(nx);
+      }
+      if (it != free.begin()) {
+        auto pv = std::prev(it);
+        if (pv->first + pv->second == it->first) {
+          pv->second += it->second;
+          free.erase(it);
+        }
+      }
+    }
+  } arena;
+  constexpr int kForever = 1 << 30;
+  std::vector<std::vector<std::pair<int64_t, int64_t>>> release(static_cast<size_t>(nw) + 1);
+  int64_t sum = 0;
+  auto take = [&](int64_t n, int death) {
+    const int64_t off = arena.get(n);
+    sum += align_up(std::max<int64_t>(n, 1), 32);
+    if (death < kForever && !key.keep) release[size_t(std::min(death, nw))].push_back({off, n});
+    return off;
+  };
+  int64_t poff = 0;
+  // caller-provided shard S blocks (top mode): compact, resident
+  for (int v : P.inputs) {
+    Node& nd = P.nodes[v];
+    nd.ld = std::max(nd.nb, 1);
+    nd.s_off = take(int64_t(nd.ld) * nd.nb, kForever);
+  }
+  std::vector<std::vector<int>> born(static_cast<size_t>(nw));
+  for (int i = 0; i < int(P.nodes.size()); ++i)
+    if (P.active[i] && !is_input[i]) born[size_t(P.nodes[i].wave)].push_back(i);
+  for (int w = 0; w < nw; ++w) {
+    for (auto [off, n] : release[size_t(w)]) arena.put(off, n);  // dead before this wave
+    for (int i : born[size_t(w)]) {
+      Node& nd = P.nodes[i];
+      const bool top = nd.parent < 0 || !P.active[nd.parent] || i == P.root;
+      const int death = top ? kForever : P.nodes[nd.parent].wave + 1;  // free after the parent's wave
+      if (nd.blocked) {
+        if (nd.smerge) {  // reduced interface system (scratch) + the assembled S (kept)
+          nd.ldm = int(align_up(nd.total, 8));
+          nd.m_off = take(int64_t(nd.ldm) * nd.total, w + 1);
+          nd.ld = int(align_up(nd.nb, 8));
+          nd.s_off = take(int64_t(nd.ld) * nd.nb, death);
+          nd.ldg = int(align_up(nd.nb, 8));
+          nd.ldr = int(align_up(nd.sys_nb, 2));
+          nd.lkg_off = take(int64_t(nd.ldg) * nd.sys_nb, w + 1);
+          nd.rkg_off = take(int64_t(nd.ldr) * nd.nb, w + 1);
+          nd.tg_off = take(int64_t(nd.ldg) * nd.sys_nb, w + 1);
+          nd.cbuf_off = take(int64_t(nd.ldr) * nd.sys_nb, w + 1);
+        } else {
+          nd.ldm = int(align_up(nd.total, 8));
+          nd.m_off = take(int64_t(nd.ldm) * (nd.total + nl), death);
+          nd.s_off = nd.m_off + nd.ni + int64_t(nd.ni) * nd.ldm;
+          nd.ld = nd.ldm;
+          nd.rhs_off = nd.m_off + nd.ni + int64_t(nd.total) * nd.ldm;
+          nd.rhs_ld = nd.ldm;
+        }
+        nd.piv_off = poff;
+        poff += align_up(std::max(nd.ni, 1), 4) + 260;  // ipiv + two per-panel row-move lists + flags
+        const int64_t nblk = (nd.ni + 127) / 128;
+        nd.uinv_off = take(nblk * 2 * 128 * 128, w + 1);
+        nd.t_off = take(int64_t(128) * std::max(nd.sys_nb + nl, 1), w + 1);
+      } else {
+        nd.ld = std::max(nd.nb, 1);
+        nd.s_off = take(int64_t(nd.ld) * nd.nb, death);
+        if (nl > 0) {
+          nd.rhs_ld = nd.ld;
+          nd.rhs_off = take(int64_t(nd.rhs_ld) * nl, death);
+        }
+      }
+      if (nd.factors) {
+        nd.ldq = int(align_up(nd.jn, 8));
+        nd.ldf = int(align_up(nd.nb, 8));
+        nd.q1_off = take(int64_t(nd.ldq) * nd.ell, death);
+        nd.q2_off = take(int64_t(nd.ldq) * nd.ell, death);
+        nd.rt_off = take(int64_t(nd.ldf) * nd.ell, death);
+        nd.lk_off = take(int64_t(nd.ldf) * nd.ell, death);
+        nd.om_off = take(int64_t(nd.ldf) * (nd.ell + 4), w + 1);  // + kProbes range-finder probes
+        nd.y1_off = take(int64_t(nd.ldq) * (nd.ell + 4), w + 1);
+        nd.y2_off = take(int64_t(nd.ldq) * (nd.ell + 4), w + 1);
       }
     }
   }
+  const int64_t off = arena.end;
+  P.arena_peak_bytes = 8 * off;
+  P.arena_sum_bytes = 8 * sum;
   P.arena_doubles = std::max<int64_t>(off, 32);
   P.piv_ints = std::max<int64_t>(poff, 4);
   return P;

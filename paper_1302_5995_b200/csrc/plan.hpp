@@ -72,10 +72,36 @@ struct Node {
   // for micro/small nodes, the view M[ni:total, total:total+nloads] for blocked ones
   int64_t rhs_off = 0;
   int rhs_ld = 0;
+  // ---- compressed engine (build_root_accel, accel_nd.cpp:667-689, 707-859) ----
+  // A structured box keeps its S dense in CCW order plus rank-ell factors of the
+  // off-diagonal blocks of its [J; K] split (StructuredSchur, accel_nd.hpp:31-48;
+  // J = the edge eliminated at the box's next merge, arc_boundary :46-88):
+  //   S[J, K] ~= Q1 (Q1^T S[J, :])  -> L_jk = Q1 (jn x ell), R_jk^T = S[J, :]^T Q1 (nb x ell)
+  //   S[K, J] ~= (S[:, J] Q2) Q2^T  -> L_kj = S[:, J] Q2 (nb x ell), R_kj^T = Q2 (jn x ell)
+  // A structured merge (accel_merge :434-628) factors only the reduced interface
+  // system [[M_jj, Z], [W, 0]] (Z = blockdiag(L_jk), W = blockdiag(R_kj)) and adds
+  // the rank-(ra + rb) product L_k C R_k to the assembled kept block.
+  int parent = -1;       // consumer merge node (-1: the root / a shard root)
+  int jside = -1;        // 0 north, 1 south, 2 east, 3 west; -1: no next merge (root)
+  bool factors = false;  // structured box: factors formed at the end of its wave
+  bool smerge = false;   // structured merge (both children structured)
+  bool exact = false;    // structured box whose factors would be full rank: kept dense (exact)
+  int j0 = 0, jn = 0;    // J edge = positions [j0, j0 + jn) of the CCW boundary
+  int ell = 0;           // factor rank (randomized range-finder sketch width)
+  int sys_nb = 0;        // boundary columns of the blocked system: nb, or ra + rb (smerge)
+  int pos_n = 0;         // rows of the position table (ni + nb)
+  int64_t q1_off = 0, q2_off = 0, rt_off = 0, lk_off = 0;
+  int ldq = 0, ldf = 0;
+  // scratch of the node's own wave: sketch (omega nb x ell, y1 / y2 jn x ell);
+  // structured merge: gathered L_k, R_k^T and T = L_k C (nb x (ra + rb) each)
+  int64_t om_off = 0, y1_off = 0, y2_off = 0, lkg_off = 0, rkg_off = 0, tg_off = 0, cbuf_off = 0;
+  int ldg = 0, ldr = 0;
 };
 
 struct Wave {
-  std::vector<int> micro, small, blocked;  // node ids
+  std::vector<int> micro, small, blocked;  // node ids (blocked: dense blocked merges and structured merges)
+  std::vector<int> smerge;                 // the structured merges among `blocked`
+  std::vector<int> compress;               // structured boxes whose factors are formed at the end of the wave
   int max_ni_blocked = 0;
 };
 
@@ -88,9 +114,21 @@ struct PlanKey {
   int n = 0, n_leaf = 0, leaf_side = 0, micro_max = 0, small_max = 0;
   int nshards = 1, shard = -1;
   int nloads = 0;  // body-load columns carried through the merges (LoadPanel, dense_nd.hpp:29-32)
+  // compressed engine: boxes of boundary >= crossover with a next merge become
+  // structured (accel_nd.cpp:682, 737); factor rank ell(jn) = min(jn, ell_base +
+  // ell_step * floor(log2(jn / 128))) rounded up to a multiple of 8
+  int structured = 0;
+  int64_t crossover = 0;
+  int ell_base = 0, ell_step = 0;
+  int keep = 0;  // keep every box's S resident (dtn_gpu_box_schur); else storage is reused level by level
+  // learned ranks: (J edge size, ell) overrides of the schedule, raised by the engine when a
+  // factor's range-finder check fails (engine.cu, dtn_gpu_build)
+  std::vector<std::pair<int, int>> ell_over;
   bool operator==(const PlanKey& o) const {
     return n == o.n && n_leaf == o.n_leaf && leaf_side == o.leaf_side && micro_max == o.micro_max &&
-           small_max == o.small_max && nshards == o.nshards && shard == o.shard && nloads == o.nloads;
+           small_max == o.small_max && nshards == o.nshards && shard == o.shard && nloads == o.nloads &&
+           structured == o.structured && crossover == o.crossover && ell_base == o.ell_base &&
+           ell_step == o.ell_step && keep == o.keep && ell_over == o.ell_over;
   }
 };
 
@@ -108,6 +146,8 @@ struct Plan {
   int root = -1;  // root node (the shard's node in shard mode)
   std::vector<int> inputs;  // top mode: shard nodes whose S is provided by the caller
   std::vector<char> active;  // nodes computed by this plan
+  int64_t arena_peak_bytes = 0;  // liveness-packed arena (vs the sum of all node storage)
+  int64_t arena_sum_bytes = 0;
   // algorithmic work (reference formulation)
   double merge_flops = 0.0;     // sum of (2/3)ni^3 + 2ni^2nb + 2nb^2ni over reference-tree merges
   double micro_flops = 0.0;     // leaf-interior elimination executed (same formula)

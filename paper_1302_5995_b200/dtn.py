@@ -262,6 +262,10 @@ class AccelOptions:
     hbs_leaf: int = 64
     rank_warn_cap: int = 4096
     threads: int = 1
+    # B200 structured merges: factor rank schedule (0 = engine defaults, dtn_opts.rank_base/step)
+    rank_base: int = 0
+    rank_step: int = 0
+    structured: bool = True  # False: exact dense merges, compress only the root (round-1 engine)
 
 
 @dataclass
@@ -379,7 +383,7 @@ class SolutionOperator:
             ctx.check(L.lib().dtn_gpu_level_stats(handle, None, 0, C.byref(cnt)))
             arr = (L.dtn_level_stats * cnt.value)()
             ctx.check(L.lib().dtn_gpu_level_stats(handle, arr, cnt.value, C.byref(cnt)))
-            v = [LevelStats(a.level, 0, 8 * a.max_boundary ** 2, a.seconds, a.boxes, a.flops) for a in arr]
+            v = [LevelStats(a.level, a.max_rank, a.bytes, a.seconds, a.boxes, a.flops) for a in arr]
         elif key == "kernel_stats":
             cnt = C.c_int32()
             ctx.check(L.lib().dtn_gpu_kernel_stats(handle, None, 0, C.byref(cnt)))
@@ -540,14 +544,22 @@ def _make_problem(op, tree, stencil_device_ptr=None, shard_S=None):
 def build_root_gpu(op: DiscreteOperator | None, tree: BoxTree, want_G: bool = True, micro_max: int = 0,
                    ctx: Context | None = None, stencil_device_ptr: int | None = None,
                    profile: bool = False, nshards: int = 1, shard: int = -1, shard_S=None,
-                   export_S: bool = False, load_ids=None) -> SolutionOperator:
+                   export_S: bool = False, load_ids=None, keep_boxes: bool = False,
+                   accel: "AccelOptions | None" = None) -> SolutionOperator:
     """The B200 build: leaf elimination + merges + root inverse, through dtn_gpu_build.
     export_S: S arrives in a page-locked host array during the build (the copy
-    overlaps the root inverse); SolutionOperator.S_dense then costs nothing."""
+    overlaps the root inverse); SolutionOperator.S_dense then costs nothing.
+    keep_boxes: every box's S stays readable (box_schur); otherwise box storage is
+    reused level by level. accel: structured merges above accel.crossover (engine 1,
+    the compressed engine's merges) with the root S dense."""
     ctx = ctx or default_context()
     prob, keep = _make_problem(op, tree, stencil_device_ptr, shard_S)
     opts = L.dtn_opts(0, tree.n_leaf, tree.leaf_side, 1 if want_G else 0, micro_max, 1 if profile else 0, 0.0, 0,
                       nshards, shard)
+    opts.keep_boxes = 1 if keep_boxes else 0
+    if accel is not None:
+        opts.engine, opts.epsilon, opts.crossover = 1, float(accel.epsilon), int(accel.crossover)
+        opts.rank_base, opts.rank_step = int(accel.rank_base), int(accel.rank_step)
     loads = None
     if load_ids is not None and len(load_ids):
         loads = np.ascontiguousarray(load_ids, dtype=np.int64)
@@ -648,7 +660,9 @@ def build_root_accel(op: DiscreteOperator, tree: BoxTree, opt: AccelOptions | No
     ctx = ctx or default_context()
     prob, keep = _make_problem(op, tree, stencil_device_ptr, shard_S)
     n = tree.n
-    opts = L.dtn_opts(0, tree.n_leaf, tree.leaf_side, 0, 0, 0, float(opt.epsilon), int(opt.crossover), nshards, -1)
+    opts = L.dtn_opts(1 if opt.structured else 0, tree.n_leaf, tree.leaf_side, 0, 0, 0, float(opt.epsilon),
+                      int(opt.crossover), nshards, -1)
+    opts.rank_base, opts.rank_step = int(opt.rank_base), int(opt.rank_step)
     load_arr = None
     if loads is not None and len(loads):
         load_arr = np.ascontiguousarray(loads, dtype=np.int64)

@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-10
 
 
-def gpu_build(name, n, n_leaf=16, leaf_side=0, seed=0, param=None, micro_max=0, want_G=True):
+def gpu_build(name, n, n_leaf=16, leaf_side=0, seed=0, param=None, micro_max=0, want_G=True, keep_boxes=False):
     if param is not None:
         spec = dtn.baseline_problem({"helmholtz": 2, "varcoef": 3}[name], n - 2)
         if name == "helmholtz":
@@ -22,7 +22,7 @@ def gpu_build(name, n, n_leaf=16, leaf_side=0, seed=0, param=None, micro_max=0, 
         spec = dtn.catalog(name, n, seed=seed)
     op = dtn.discretize(spec)
     tree = dtn.build_tree_uniform(n, leaf_side) if leaf_side else dtn.build_tree(n, n_leaf)
-    return dtn.build_root_gpu(op, tree, want_G=want_G, micro_max=micro_max)
+    return dtn.build_root_gpu(op, tree, want_G=want_G, micro_max=micro_max, keep_boxes=keep_boxes)
 
 
 @pytest.mark.parametrize("n", [8, 16, 24, 32])
@@ -51,7 +51,7 @@ def test_acceptance_criterion1_all_catalog(n):  # acceptance.cpp:74-114
 
 @pytest.mark.parametrize("name,n,n_leaf", [("diffconv3", 66, 64), ("helmholtz2", 70, 100), ("random2", 45, 40)])
 def test_every_box_matches_oracle(name, n, n_leaf):
-    sol = gpu_build(name, n, n_leaf, seed=2)
+    sol = gpu_build(name, n, n_leaf, seed=2, keep_boxes=True)
     p = O.Problem(name, n, seed=2)
     t = O.Tree(n, n_leaf)
     ref = O.build_root_dense(p, t, keep_all=True)
