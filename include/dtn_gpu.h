@@ -133,6 +133,8 @@ typedef struct {
 int dtn_gpu_create(dtn_ctx** ctx, int device);
 void dtn_gpu_destroy(dtn_ctx* ctx);
 const char* dtn_gpu_last_error(const dtn_ctx* ctx);
+/* kernel launches issued so far by the HBS code (compress, invert_hbs, apply), process-wide */
+unsigned long long dtn_gpu_hbs_launch_count(void);
 /* Run this context's work on an external CUDA stream (cudaStream_t); NULL restores its own. */
 int dtn_gpu_set_stream(dtn_ctx* ctx, void* stream);
 

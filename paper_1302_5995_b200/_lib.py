@@ -54,7 +54,7 @@ EXPORTS = [
     "dtn_discretize_continuum", "dtn_discretize_network", "dtn_debug_partial_lu", "dtn_gpu_shard_info",
     "dtn_gpu_hbs_compress", "dtn_gpu_hbs_compress_op", "dtn_gpu_hbs_free", "dtn_gpu_hbs_info", "dtn_gpu_hbs_tree",
     "dtn_gpu_hbs_factor", "dtn_gpu_hbs_apply", "dtn_gpu_hbs_serialize", "dtn_gpu_hbs_deserialize",
-    "dtn_gpu_hbs_invert", "dtn_gpu_build_accel", "dtn_gpu_root_rhs",
+    "dtn_gpu_hbs_invert", "dtn_gpu_build_accel", "dtn_gpu_root_rhs", "dtn_gpu_hbs_launch_count",
 ]
 
 _lib = None
@@ -113,6 +113,8 @@ def lib():
     L.dtn_gpu_hbs_deserialize.argtypes = [vp, vp, C.c_uint64, P(vp)]
     L.dtn_gpu_hbs_invert.argtypes = [vp, P(vp)]
     L.dtn_gpu_root_rhs.argtypes = [vp, vp, i64, C.c_int]
+    L.dtn_gpu_hbs_launch_count.argtypes = []
+    L.dtn_gpu_hbs_launch_count.restype = C.c_ulonglong
     L.dtn_gpu_build_accel.argtypes = [vp, vp, vp, i64, P(vp), P(vp), P(vp), P(f64)]
     _lib = L
     return L

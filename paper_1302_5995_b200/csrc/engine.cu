@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -68,6 +69,7 @@ cudaError_t launch_omega(const KernelArgs&, const int*, int, long long, cudaStre
 cudaError_t launch_hqr(const QrDesc*, int, int, int, const double*, cudaStream_t);
 cudaError_t launch_gemm_desc2(const GemmDesc2*, int, int, bool, cudaStream_t);
 int gemm_tiles(int, int);
+extern std::atomic<unsigned long long> g_hbs_launches;
 }  // namespace dtnb
 
 using namespace dtnb;
@@ -1371,6 +1373,8 @@ void dtn_gpu_destroy(dtn_ctx* ctx) {
 }
 
 const char* dtn_gpu_last_error(const dtn_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+unsigned long long dtn_gpu_hbs_launch_count(void) { return g_hbs_launches.load(); }
 
 int dtn_gpu_set_stream(dtn_ctx* ctx, void* stream) {
   if (!ctx) return DTN_EINVAL;

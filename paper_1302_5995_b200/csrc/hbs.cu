@@ -31,6 +31,7 @@
 // U y-hat, leaves D x + U y-hat; batched DMMA GEMMs per tree height on a
 // repacked copy of the factors whose ranks are padded to even (zero columns)
 // so every operand is 16-byte aligned.
+#include <atomic>
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
@@ -123,7 +124,15 @@ cudaError_t launch_gemm_desc2(const GemmDesc2* d_descs, int count, int max_tiles
 int gemm_tiles(int m, int n);
 cudaError_t launch_copy2d_batched(const void* d_descs, int count, cudaStream_t st);
 
+// kernel launches issued by the HBS code (compress, invert, apply), process-wide
+std::atomic<unsigned long long> g_hbs_launches{0};
+
 namespace {
+#define HLK(x)                    \
+  do {                            \
+    HCK(x);                       \
+    g_hbs_launches.fetch_add(1);  \
+  } while (0)
 
 #define HCK(x)                                                                                        \
   do {                                                                                                \
@@ -171,7 +180,7 @@ void gemm_batch(DevBuf& buf, const std::vector<GemmDesc>& g, double alpha, doubl
   }
   if (tiles == 0) return;
   GemmDesc* dd = upload(buf, g, st);
-  HCK(launch_gemm_desc(dd, int(g.size()), tiles, kmax, alpha, beta, st, a_aligned));
+  HLK(launch_gemm_desc(dd, int(g.size()), tiles, kmax, alpha, beta, st, a_aligned));
   // the descriptor buffer is reused by the next batch: keep the upload ordered
   HCK(cudaStreamSynchronize(st));
 }
@@ -181,7 +190,7 @@ void transpose_batch(DevBuf& buf, const std::vector<TransDesc>& t, cudaStream_t 
   int tiles = 0;
   for (const auto& d : t) tiles = std::max(tiles, ((d.m + 31) / 32) * ((d.n + 31) / 32));
   TransDesc* dd = upload(buf, t, st);
-  HCK(launch_transpose_batched(dd, int(t.size()), tiles, st));
+  HLK(launch_transpose_batched(dd, int(t.size()), tiles, st));
   HCK(cudaStreamSynchronize(st));
 }
 
@@ -199,7 +208,7 @@ void copy_batch(DevBuf& buf, const std::vector<CopyDesc>& c, cudaStream_t st) {
   }
   if (!small.empty()) {
     CopyDesc* dd = upload(buf, small, st);
-    HCK(launch_copy2d_batched(dd, int(small.size()), st));
+    HLK(launch_copy2d_batched(dd, int(small.size()), st));
   }
   HCK(cudaStreamSynchronize(st));
 }
@@ -469,7 +478,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
       }
       copy_batch(dbuf, cp, st);
       ZeroDesc* dz = upload(dbuf, zd, st);
-      HCK(launch_zero_blocks(dz, int(zd.size()), st));
+      HLK(launch_zero_blocks(dz, int(zd.size()), st));
       HCK(cudaStreamSynchronize(st));
     }
     tr.mark("diag");
@@ -520,7 +529,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
         for (int side = 0; side < 2; ++side) e.push_back(EigDesc{G1(side, a), U0(side, a), s, ld, ld});
       }
       EigDesc* de = upload(dbuf, e, st);
-      HCK(launch_jacobi_eig(de, int(e.size()), 30, false, 0.0, smax, st));
+      HLK(launch_jacobi_eig(de, int(e.size()), 30, false, 0.0, smax, st));
       HCK(cudaStreamSynchronize(st));
     }
     tr.mark("jacobi1");
@@ -573,7 +582,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
         for (int side = 0; side < 2; ++side) e.push_back(EigDesc{G2(side, a), W(side, a), s, ld, ld});
       }
       EigDesc* de = upload(dbuf, e, st);
-      HCK(launch_jacobi_eig(de, int(e.size()), 30, true, (1e-2 * eps) * (1e-2 * eps), smax, st));
+      HLK(launch_jacobi_eig(de, int(e.size()), 30, true, (1e-2 * eps) * (1e-2 * eps), smax, st));
       HCK(cudaStreamSynchronize(st));
     }
     tr.mark("jacobi2");
@@ -599,7 +608,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
         }
       }
       SelDesc* ds = upload(dbuf, sd, st);
-      HCK(launch_hbs_select(ds, int(sd.size()), eps, st));
+      HLK(launch_hbs_select(ds, int(sd.size()), eps, st));
       std::vector<int> hr(2 * size_t(na));
       HCK(cudaMemcpyAsync(hr.data(), rk, hr.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
       HCK(cudaStreamSynchronize(st));
@@ -627,7 +636,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
       }
       if (!gd.empty()) {
         GatherDesc* dg = upload(dbuf, gd, st);
-        HCK(launch_gather_cols(dg, int(gd.size()), st));
+        HLK(launch_gather_cols(dg, int(gd.size()), st));
         HCK(cudaStreamSynchronize(st));
       }
     }
@@ -781,7 +790,7 @@ void pack_for_apply(HbsDev& H, cudaStream_t st) {
     if (d.rp > 0 && d.cp > 0) pk2.push_back(d);
   if (!pk2.empty()) {
     PackDesc* dd = upload(dbuf, pk2, st);
-    HCK(launch_pack(dd, int(pk2.size()), st));
+    HLK(launch_pack(dd, int(pk2.size()), st));
   }
   HCK(cudaStreamSynchronize(st));
   P.ready = true;
@@ -931,10 +940,10 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
   const GemmDesc2* dg2 = reinterpret_cast<const GemmDesc2*>(static_cast<unsigned char*>(H.d_desc) + g2_off);
   auto launch_all = [&](cudaStream_t s2) {
     for (const Phase& f : ph) {
-      if (f.kind == 4 || f.kind == 5) HCK(launch_gemm_desc2(dg2 + f.off, f.count, f.tiles, f.kind == 5, s2));
-      else if (f.kind == 3) HCK(launch_gemm_desc_tc(dg + f.off, f.count, f.tiles, f.kmax, 1.0, 0.0, s2));
+      if (f.kind == 4 || f.kind == 5) HLK(launch_gemm_desc2(dg2 + f.off, f.count, f.tiles, f.kind == 5, s2));
+      else if (f.kind == 3) HLK(launch_gemm_desc_tc(dg + f.off, f.count, f.tiles, f.kmax, 1.0, 0.0, s2));
       else  // 128 x 64 tiles: the short reductions (K = leaf or rank) measured 20 % faster than 128 x 128
-        HCK(launch_gemm_desc(dg + f.off, f.count, f.tiles, f.kmax, 1.0, 0.0, s2, true, false));
+        HLK(launch_gemm_desc(dg + f.off, f.count, f.tiles, f.kmax, 1.0, 0.0, s2, true, false));
     }
   };
   // the launch sequence depends only on the tree, the ranks and nrhs: replay it as a
@@ -1258,7 +1267,7 @@ std::unique_ptr<HbsDev> hbs_invert(const HbsDev& H, cudaStream_t st) {
       smax = std::max(smax, d.s);
     }
     InvDesc* dv = upload(ibuf, v, st);
-    HCK(launch_gj_inverse(dv, int(v.size()), smax, st));
+    HLK(launch_gj_inverse(dv, int(v.size()), smax, st));
     std::vector<int> info(v.size());
     HCK(cudaMemcpyAsync(info.data(), dinfo, info.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
     HCK(cudaStreamSynchronize(st));
@@ -1353,7 +1362,7 @@ std::unique_ptr<HbsDev> hbs_invert(const HbsDev& H, cudaStream_t st) {
       copy_batch(dbuf, c, st);
       if (!a.empty()) {
         AddDesc* da = upload(dbuf, a, st);
-        HCK(launch_add_blocks(da, int(a.size()), st));
+        HLK(launch_add_blocks(da, int(a.size()), st));
         HCK(cudaStreamSynchronize(st));
       }
     }

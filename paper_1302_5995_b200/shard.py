@@ -39,8 +39,10 @@ class GpuShardEngine:
 
     def build_shard(self, nshards: int, shard: int):
         import torch
+        # with accel: the shard's subtree uses the structured merges above the crossover
         sol = dtn.build_root_gpu(self.op, self.tree, want_G=False, ctx=self.ctx,
-                                 stencil_device_ptr=self.stencil_device_ptr, nshards=nshards, shard=shard)
+                                 stencil_device_ptr=self.stencil_device_ptr, nshards=nshards, shard=shard,
+                                 accel=self.accel)
         nb = len(sol.boundary)
         # device-to-device copy of the shard S into a column-major tensor
         S = torch.empty((nb, nb), dtype=torch.float64, device=self.device or "cuda").t()

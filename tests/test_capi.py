@@ -13,7 +13,7 @@ from oracle import oracle as O
 
 def header_symbols():
     src = open(L.HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+\*?(dtn_\w+)\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*|unsigned long long)\s+\*?(dtn_\w+)\(", src, re.M)))
 
 
 def test_library_exports_header_symbols():
