@@ -994,18 +994,6 @@ void put_i64(std::vector<uint8_t>& out, int64_t v) {
   for (int i = 0; i < 8; ++i) out.push_back(uint8_t(uint64_t(v) >> (8 * i)));
 }
 
-void put_matrix(std::vector<uint8_t>& out, const double* d, int64_t ld, int64_t r, int64_t c, cudaStream_t st) {
-  put_i64(out, r);
-  put_i64(out, c);
-  const size_t bytes = size_t(r) * size_t(c) * 8;
-  const size_t at = out.size();
-  out.resize(at + bytes);
-  if (bytes) {
-    HCK(cudaMemcpy2DAsync(out.data() + at, size_t(r) * 8, d, size_t(ld) * 8, size_t(r) * 8, size_t(c),
-                          cudaMemcpyDeviceToHost, st));
-    HCK(cudaStreamSynchronize(st));
-  }
-}
 
 struct Reader {
   const uint8_t* p;
@@ -1034,14 +1022,56 @@ std::vector<uint8_t> hbs_serialize(const HbsDev& H, cudaStream_t st) {
     put_i64(out, n.parent);
     put_i64(out, n.level);
   }
+  // every factor straight into one page-locked staging buffer (all copies in flight
+  // at once, one synchronisation), then the DTNHBS01 records around them
+  struct Mat {
+    const double* d;
+    int64_t ld, r, c;
+  };
+  std::vector<Mat> mats;
   for (int t = 0; t < int(H.nodes.size()); ++t) {
     const bool leaf = H.is_leaf(t);
-    if (leaf) put_matrix(out, H.D[t], H.ld(t), H.node_size(t), H.node_size(t), st);
+    if (leaf) mats.push_back({H.D[t], H.ld(t), H.node_size(t), H.node_size(t)});
     if (t != 0) {
-      put_matrix(out, H.U[t], H.ld(t), H.rows[t], H.rank[t], st);
-      put_matrix(out, H.V[t], H.ld(t), H.rows[t], H.rank[t], st);
+      mats.push_back({H.U[t], H.ld(t), H.rows[t], H.rank[t]});
+      mats.push_back({H.V[t], H.ld(t), H.rows[t], H.rank[t]});
     }
-    if (!leaf) put_matrix(out, H.B[t], H.ld(t), H.rows[t], H.rows[t], st);
+    if (!leaf) mats.push_back({H.B[t], H.ld(t), H.rows[t], H.rows[t]});
+  }
+  size_t total = 0;
+  for (const Mat& x : mats) total += size_t(x.r) * size_t(x.c) * 8;
+  thread_local struct Pinned {
+    void* p = nullptr;
+    size_t cap = 0;
+    ~Pinned() {
+      if (p) cudaFreeHost(p);
+    }
+  } stage;
+  if (stage.cap < total) {
+    if (stage.p) cudaFreeHost(stage.p);
+    stage.p = nullptr;
+    stage.cap = 0;
+    HCK(cudaMallocHost(&stage.p, total));
+    stage.cap = total;
+  }
+  uint8_t* hs = static_cast<uint8_t*>(stage.p);
+  size_t at = 0;
+  for (const Mat& x : mats) {
+    const size_t bytes = size_t(x.r) * size_t(x.c) * 8;
+    if (bytes)
+      HCK(cudaMemcpy2DAsync(hs + at, size_t(x.r) * 8, x.d, size_t(x.ld) * 8, size_t(x.r) * 8, size_t(x.c),
+                            cudaMemcpyDeviceToHost, st));
+    at += bytes;
+  }
+  HCK(cudaStreamSynchronize(st));
+  out.reserve(out.size() + total + 16 * mats.size());
+  at = 0;
+  for (const Mat& x : mats) {
+    const size_t bytes = size_t(x.r) * size_t(x.c) * 8;
+    put_i64(out, x.r);
+    put_i64(out, x.c);
+    out.insert(out.end(), hs + at, hs + at + bytes);
+    at += bytes;
   }
   return out;
 }

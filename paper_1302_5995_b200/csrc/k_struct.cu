@@ -173,177 +173,196 @@ __global__ void __launch_bounds__(256) omega_kernel(KernelArgs args, const int* 
 }
 
 // Householder QR of the first n columns of Y (m x (n + p)) and the explicit
-// Q = H_0 ... H_{n-1} [I; 0] (m x n) (LAPACK dgeqr2 / dorg2r conventions:
-// H = I - tau v v^T, v_c = 1, beta = -sign(alpha) ||x||), one thread-block
-// cluster of C CTAs per matrix: CTA r owns rows [r R, (r + 1) R) and keeps them in
-// shared memory when they fit (SM) -- the column loop then never touches HBM/L2
-// except through the cluster's DSMEM reductions. Per column: partial norms (one
-// cluster barrier: the pivot column's norm and alpha), then partial dot products
-// of the reflector with every trailing column (a second barrier), each CTA
-// summing the C partials in rank order so every CTA computes bit-identical
-// reflectors. Reduction buffers alternate by column parity (a CTA can run at most
-// one barrier ahead of the slowest reader). The reflectors are applied to the p
-// probe columns too: their rows n..m-1 then hold (I - Q Q^T) y, the randomized
-// range finder's a-posteriori estimate (Halko, Martinsson & Tropp 2011, Sec. 4.3).
-// stat[1] = max_probe |(I - Q Q^T) y| / scale, stat[0] = #{|R_ii| > eps scale},
-// relative to the box operator's scale max_i |S_ii| sqrt(k / 3) (the expected
-// norm of S applied to a k-vector of uniform[-1, 1] entries, S diagonally dominant).
+// Q = H_0 ... H_{n-1} [I; 0] (m x n), LAPACK dgeqr2 / dorg2r conventions
+// (H = I - tau v v^T, v_c = 1, beta = -sign(alpha) ||x||; Q formed in place over
+// the reflectors). One thread-block cluster of C CTAs per matrix: CTA r owns rows
+// [r R, (r + 1) R) and keeps them in shared memory (SM) or works on them in place in
+// global memory (large matrices). A column step is two phases: warp 0 forms the
+// reflector (norm by a warp reduction, scaling by all lanes); then groups of 8
+// lanes own the trailing columns (dot product over the rows, a 3-step shuffle
+// reduction, the update of the same rows). With C > 1 the partial norms and dot
+// products are summed over the cluster through DSMEM in rank order, so every CTA
+// forms bit-identical reflectors; reduction slots alternate by column parity. The
+// reflectors are applied to the p probe columns too: their rows n..m-1 then hold
+// (I - Q Q^T) y, the randomized range finder's a-posteriori estimate (Halko,
+// Martinsson & Tropp 2011, Sec. 4.3). stat[1] = max_probe |(I - Q Q^T) y| / scale,
+// stat[0] = #{|R_ii| > eps scale}, relative to the box operator's scale
+// max_i |S_ii| sqrt(k / 3) (the expected norm of S applied to a k-vector of
+// uniform[-1, 1] entries; S is diagonally dominant).
 constexpr int QR_THREADS = 256, QR_WARPS = QR_THREADS / 32, QR_MAXC = 16, QR_MAXN = 256;
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
+constexpr int QR_GL = 8, QR_NG = QR_THREADS / QR_GL;  // lanes per column group, column groups
 
 struct QrShared {
-  double a[2][2];              // [parity][0: partial sum of squares, 1: alpha (owner)]
+  double a[2][2];              // [parity] partial sum of squares, alpha (the row owner's)
   double w[2][QR_MAXN + 8];    // [parity] partial dot products
   double tau[QR_MAXN], rdiag[QR_MAXN];
   double red[QR_WARPS];
 };
 
-// CL = false: a single CTA per matrix (C == 1), plain block barriers and shared memory
-template <bool SM, bool CL>
-__global__ void __launch_bounds__(QR_THREADS) hqr_cluster_kernel(const QrDesc* __restrict__ descs,
-                                                                 const double* eps_ptr, int C) {
+template <bool CL, bool SM>
+__global__ void __launch_bounds__(QR_THREADS) hqr_kernel(const QrDesc* __restrict__ descs, const double* eps_ptr,
+                                                         int C) {
   extern __shared__ __align__(16) double qdyn[];
   __shared__ QrShared sh;
-  struct Sync {
-    __device__ void sync() const {
-      if constexpr (CL) cg::this_cluster().sync();
-      else __syncthreads();
-    }
-    __device__ double* map(double* p, int q) const {
-      if constexpr (CL) return cg::this_cluster().map_shared_rank(p, q);
-      else return p;
-    }
-  } cl;
   const int rank = CL ? int(cg::this_cluster().block_rank()) : 0;
+  auto csync = [] {
+    if constexpr (CL) cg::this_cluster().sync();
+  };
+  auto remote = [&](double* p, int q) -> double {
+    if constexpr (CL) return *cg::this_cluster().map_shared_rank(p, q);
+    else return *p;
+  };
   const QrDesc d = descs[blockIdx.x / C];
   const int m = d.m, n = d.n, nc = d.n + d.p;
   const int R = (m + C - 1) / C, r0 = rank * R, r1 = min(m, r0 + R), nr = max(r1 - r0, 0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // local rows: shared memory (ld = R) or the matrix itself
-  double* Yl = SM ? qdyn : d.Y + r0;
-  const long long ldl = SM ? R : d.ldy;
-  if (SM) {
+  const int gl = tid & (QR_GL - 1), grp = tid / QR_GL;
+  const long long ld = SM ? (nr | 1) : d.ldy;
+  double* Y = SM ? qdyn : d.Y + r0;  // local rows, column-major
+  if constexpr (SM) {
     for (int j = 0; j < nc; ++j)
-      for (int i = tid; i < nr; i += QR_THREADS) Yl[i + j * ldl] = d.Y[r0 + i + (long long)j * d.ldy];
+      for (int i = tid; i < nr; i += QR_THREADS) Y[i + j * ld] = d.Y[r0 + i + (long long)j * d.ldy];
     __syncthreads();
   }
-  auto remote_sum = [&](double* base) {  // sum over ranks, fixed order
-    double t = 0.0;
-    for (int q = 0; q < C; ++q) t += *cl.map(base, q);
-    return t;
+  // trailing-column phase: every column j in [j0, j1) -> dot with the reflector in
+  // column c (rows >= c; v_c = 1), summed over the cluster, and y_j -= tau (v . y_j) v
+  auto apply_reflector = [&](int c, int j0, int j1, int par) {
+    const double tc = sh.tau[c];
+    const double* yc = Y + c * ld;
+    const bool own_row = c >= r0 && c < r1;
+    const int lv = max(c - r0, 0);
+    for (int jb = j0; jb < j1; jb += QR_NG) {
+      const int j = jb + grp;
+      double dot = 0.0;
+      if (j < j1) {
+        const double* yj = Y + j * ld;
+        double s0 = 0.0, s1 = 0.0;
+        int i = lv + gl;
+        if (own_row && gl == 0) {
+          s0 = yj[lv];
+          i += QR_GL;
+        }
+        for (; i + QR_GL < nr; i += 2 * QR_GL) {
+          s0 = fma(yc[i], yj[i], s0);
+          s1 = fma(yc[i + QR_GL], yj[i + QR_GL], s1);
+        }
+        if (i < nr) s0 = fma(yc[i], yj[i], s0);
+        dot = s0 + s1;
+      }
+#pragma unroll
+      for (int o = QR_GL / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      if constexpr (CL) {
+        if (j < j1 && gl == 0) sh.w[par][j] = dot;
+        csync();
+        if (j < j1) {
+          dot = 0.0;
+          if (gl == 0)
+            for (int q = 0; q < C; ++q) dot += remote(&sh.w[par][j], q);
+        }
+        dot = __shfl_sync(0xffffffffu, dot, (lane / QR_GL) * QR_GL);
+      }
+      if (j < j1 && tc != 0.0) {
+        double* yj = Y + j * ld;
+        const double f = tc * dot;
+        int i = lv + gl;
+        if (own_row && gl == 0) {
+          yj[lv] -= f;
+          i += QR_GL;
+        }
+        for (; i < nr; i += QR_GL) yj[i] = fma(-f, yc[i], yj[i]);
+      }
+      if constexpr (CL) csync();  // (the slots of this column block are reused by the next)
+    }
   };
   for (int c = 0; c < n; ++c) {
     const int par = c & 1;
-    double* yc = Yl + (long long)c * ldl;
-    // rows of this CTA strictly below the diagonal: [max(c + 1, r0), r1)
+    double* yc = Y + c * ld;
+    const bool own_row = c >= r0 && c < r1;
     const int lo = max(c + 1 - r0, 0);
-    double ss = 0.0;
-    for (int i = lo + tid; i < nr; i += QR_THREADS) ss = fma(yc[i], yc[i], ss);
-    ss = warp_sum(ss);
-    if (lane == 0) sh.red[warp] = ss;
-    __syncthreads();
-    if (tid == 0) {
-      double t = 0.0;
-      for (int w = 0; w < QR_WARPS; ++w) t += sh.red[w];
-      sh.a[par][0] = t;
-      sh.a[par][1] = (c >= r0 && c < r1) ? yc[c - r0] : 0.0;
-    }
-    cl.sync();
-    const double sst = remote_sum(&sh.a[par][0]);
-    const double alpha = *cl.map(&sh.a[par][1], c / R);
-    double beta, tc, scal;
-    if (sst == 0.0) {
-      beta = alpha;
-      tc = 0.0;
-      scal = 0.0;
-    } else {
-      beta = -copysign(sqrt(fma(alpha, alpha, sst)), alpha);
-      tc = (beta - alpha) / beta;
-      scal = 1.0 / (alpha - beta);
-    }
-    for (int i = lo + tid; i < nr; i += QR_THREADS) yc[i] *= scal;  // v below the diagonal
-    const bool own = c >= r0 && c < r1;
-    if (own && tid == 0) yc[c - r0] = beta;
-    if (tid == 0) {
-      sh.tau[c] = tc;
-      sh.rdiag[c] = beta;
-    }
-    __syncthreads();
-    // partial dots v^T y_j over the local rows (v_c = 1 on the owner's row c)
-    const int lv = max(c - r0, 0);  // first local row of the reflector
-    for (int j = c + 1 + warp; j < nc; j += QR_WARPS) {
-      const double* yj = Yl + (long long)j * ldl;
-      double s = 0.0;
-      for (int i = lv + lane; i < nr; i += 32) s = fma((own && i == c - r0) ? 1.0 : yc[i], yj[i], s);
-      s = warp_sum(s);
-      if (lane == 0) sh.w[par][j] = s;
-    }
-    cl.sync();
-    if (tc != 0.0) {
-      for (int j = c + 1 + warp; j < nc; j += QR_WARPS) {
-        const double wj = remote_sum(&sh.w[par][j]) * tc;
-        double* yj = Yl + (long long)j * ldl;
-        for (int i = lv + lane; i < nr; i += 32) yj[i] = fma(-wj, (own && i == c - r0) ? 1.0 : yc[i], yj[i]);
+    // reflector of column c (warp 0)
+    if (warp == 0) {
+      double ss = 0.0;
+      for (int i = lo + lane; i < nr; i += 32) ss = fma(yc[i], yc[i], ss);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) {
+        sh.a[par][0] = ss;
+        sh.a[par][1] = own_row ? yc[c - r0] : 0.0;
       }
     }
+    csync();
+    if (warp == 0) {
+      double sst = 0.0, alpha = 0.0;
+      if (lane == 0) {
+        for (int q = 0; q < C; ++q) sst += remote(&sh.a[par][0], q);
+        alpha = remote(&sh.a[par][1], c / R);
+      }
+      sst = __shfl_sync(0xffffffffu, sst, 0);
+      alpha = __shfl_sync(0xffffffffu, alpha, 0);
+      double beta, tc, scal;
+      if (sst == 0.0) {
+        beta = alpha;
+        tc = 0.0;
+        scal = 0.0;
+      } else {
+        beta = -copysign(sqrt(fma(alpha, alpha, sst)), alpha);
+        tc = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      for (int i = lo + lane; i < nr; i += 32) yc[i] *= scal;
+      if (lane == 0) {
+        if (own_row) yc[c - r0] = beta;
+        sh.tau[c] = tc;
+        sh.rdiag[c] = beta;
+      }
+    }
+    __syncthreads();
+    apply_reflector(c, c + 1, nc, par);
     __syncthreads();
   }
   // range-finder check: |(I - Q Q^T) y_probe|^2 = sum of the probe columns' rows >= n
   double pres = 0.0;
   {
     const int lo = max(n - r0, 0);
-    for (int q = 0; q < d.p; ++q) {
-      const double* yq = Yl + (long long)(n + q) * ldl;
+    if (warp < d.p) {
+      const double* yq = Y + (n + warp) * ld;
       double ss = 0.0;
-      for (int i = lo + tid; i < nr; i += QR_THREADS) ss = fma(yq[i], yq[i], ss);
-      ss = warp_sum(ss);
-      if (lane == 0) sh.red[warp] = ss;
-      __syncthreads();
-      if (tid == 0) {
-        double t = 0.0;
-        for (int w = 0; w < QR_WARPS; ++w) t += sh.red[w];
-        sh.w[q & 1][QR_MAXN + (q >> 1)] = t;
-      }
-      __syncthreads();
-    }
-    cl.sync();
-    for (int q = 0; q < d.p; ++q) pres = fmax(pres, sqrt(remote_sum(&sh.w[q & 1][QR_MAXN + (q >> 1)])));
-    cl.sync();  // (the partial buffers are reused below)
-  }
-  // Q = H_0 ... H_{n-1} [I; 0] on the local rows, backward accumulation
-  double* Q = d.Q + r0;
-  const long long ldq = d.ldq;
-  for (int j = 0; j < n; ++j)
-    for (int i = tid; i < nr; i += QR_THREADS) Q[i + j * ldq] = (r0 + i == j) ? 1.0 : 0.0;
-  __syncthreads();
-  for (int c = n - 1; c >= 0; --c) {
-    const int par = c & 1;
-    const double tc = sh.tau[c];
-    const double* yc = Yl + (long long)c * ldl;
-    const bool own = c >= r0 && c < r1;
-    const int lv = max(c - r0, 0);
-    for (int j = c + warp; j < n; j += QR_WARPS) {
-      const double* qj = Q + (long long)j * ldq;
-      double s = 0.0;
-      for (int i = lv + lane; i < nr; i += 32) s = fma((own && i == c - r0) ? 1.0 : yc[i], qj[i], s);
-      s = warp_sum(s);
-      if (lane == 0) sh.w[par][j] = s;
-    }
-    cl.sync();
-    if (tc != 0.0) {
-      for (int j = c + warp; j < n; j += QR_WARPS) {
-        const double wj = remote_sum(&sh.w[par][j]) * tc;
-        double* qj = Q + (long long)j * ldq;
-        for (int i = lv + lane; i < nr; i += 32) qj[i] = fma(-wj, (own && i == c - r0) ? 1.0 : yc[i], qj[i]);
-      }
+      for (int i = lo + lane; i < nr; i += 32) ss = fma(yq[i], yq[i], ss);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) sh.w[0][QR_MAXN + warp] = ss;
     }
     __syncthreads();
+    csync();
+    for (int q = 0; q < d.p; ++q) {
+      double t = 0.0;
+      for (int r = 0; r < C; ++r) t += remote(&sh.w[0][QR_MAXN + q], r);
+      pres = fmax(pres, sqrt(t));
+    }
+    csync();
   }
+  // Q in place (dorg2r): backward over the reflectors; column c + 1 becomes Q's column
+  // (its reflector no longer read) at the start of step c
+  auto finish_col = [&](int c) {
+    double* y = Y + c * ld;
+    const double tc = sh.tau[c];
+    for (int i = tid; i < nr; i += QR_THREADS) {
+      const int gi = r0 + i;
+      y[i] = gi < c ? 0.0 : (gi == c ? 1.0 - tc : -tc * y[i]);
+    }
+  };
+  for (int c = n - 1; c >= 0; --c) {
+    if (c + 1 < n) {
+      finish_col(c + 1);
+      __syncthreads();
+    }
+    apply_reflector(c, c + 1, n, c & 1);
+    __syncthreads();
+  }
+  finish_col(0);
+  __syncthreads();
+  for (int jj = 0; jj < n; ++jj)
+    for (int i = tid; i < nr; i += QR_THREADS) d.Q[r0 + i + (long long)jj * d.ldq] = Y[i + jj * ld];
   if (rank == 0 && d.stat) {
     double dmax = 0.0;
     for (int i = tid; i < d.nbs; i += QR_THREADS) dmax = fmax(dmax, fabs(d.S[i + (long long)i * d.lds]));
@@ -362,7 +381,7 @@ __global__ void __launch_bounds__(QR_THREADS) hqr_cluster_kernel(const QrDesc* _
       d.stat[1] = scale > 0.0 ? pres / scale : 0.0;
     }
   }
-  cl.sync();  // no CTA leaves while others may still read its shared memory
+  csync();  // no CTA leaves while others may still read its shared memory
 }
 
 cudaError_t launch_sgather_red(const KernelArgs& args, const int* d_list, int count, int max_total, cudaStream_t st) {
@@ -394,25 +413,27 @@ cudaError_t launch_omega(const KernelArgs& args, const int* d_list, int count, l
   return cudaGetLastError();
 }
 
-// cluster size for an m x nc matrix: the smallest C whose row blocks fit in shared memory
-// (<= 200 KB), else 16 CTAs working on the matrix in global memory (L1/L2-resident)
-static int qr_cluster(int m, int nc, bool* smem) {
+// cluster size for an m x nc matrix: the smallest C whose row blocks fit in shared
+// memory, else 16 CTAs working on the matrix in place (global memory, L1/L2-resident)
+static int qr_cluster(int m, int nc, bool* sm) {
   for (int C = 1; C <= QR_MAXC; C *= 2) {
     const long long R = (m + C - 1) / C;
-    if (R * nc * 8 <= 200 * 1024) {
-      *smem = true;
+    if ((R | 1) * nc * 8 <= 200 * 1024) {
+      *sm = true;
       return C;
     }
   }
-  *smem = false;
+  *sm = false;
   return QR_MAXC;
 }
 
 cudaError_t struct_init() {
-  for (auto f : {hqr_cluster_kernel<true, true>, hqr_cluster_kernel<false, true>, hqr_cluster_kernel<true, false>}) {
+  for (auto f : {hqr_kernel<true, true>, hqr_kernel<false, true>, hqr_kernel<true, false>}) {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  }
+  for (auto f : {hqr_kernel<true, true>, hqr_kernel<true, false>}) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -421,26 +442,23 @@ cudaError_t struct_init() {
 cudaError_t launch_hqr(const QrDesc* d_descs, int count, int max_m, int max_nc, const double* d_eps, cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
   if (max_nc > QR_MAXN) return cudaErrorInvalidValue;
-  bool sm = false;
+  bool sm = true;
   const int C = qr_cluster(max_m, max_nc, &sm);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(count * C);
   cfg.blockDim = dim3(QR_THREADS);
   cfg.stream = st;
-  cfg.dynamicSmemBytes = sm ? size_t((max_m + C - 1) / C) * max_nc * 8 : 0;
+  cfg.dynamicSmemBytes = sm ? size_t(((max_m + C - 1) / C) | 1) * max_nc * 8 : 0;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = C;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (sm && C == 1) {
-    cfg.numAttrs = 0;
-    return cudaLaunchKernelEx(&cfg, hqr_cluster_kernel<true, false>, d_descs, d_eps, C);
-  }
-  if (sm) return cudaLaunchKernelEx(&cfg, hqr_cluster_kernel<true, true>, d_descs, d_eps, C);
-  return cudaLaunchKernelEx(&cfg, hqr_cluster_kernel<false, true>, d_descs, d_eps, C);
+  cfg.numAttrs = C > 1 ? 1 : 0;
+  if (!sm) return cudaLaunchKernelEx(&cfg, hqr_kernel<true, false>, d_descs, d_eps, C);
+  if (C > 1) return cudaLaunchKernelEx(&cfg, hqr_kernel<true, true>, d_descs, d_eps, C);
+  return cudaLaunchKernelEx(&cfg, hqr_kernel<false, true>, d_descs, d_eps, C);
 }
 
 }  // namespace dtnb
