@@ -320,7 +320,7 @@ def run_b200(args, cfg, rank, world, local):
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    ctx = dtn.Context(local)
+    ctx = dtn.collective_context(local) if world > 1 else dtn.Context(local)
     stream = torch.cuda.current_stream(dev)
     ctx.set_stream(stream.cuda_stream or 1)  # (torch legacy default stream = cudaStreamLegacy)
 
@@ -337,13 +337,12 @@ def run_b200(args, cfg, rank, world, local):
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
 
     from paper_1302_5995_b200 import shard as SH
-    eng_dev = SH.GpuShardEngine(None, tree, ctx=ctx, stencil_device_ptr=stencil_d.data_ptr(), device=dev)
 
     def device_step():
         if world == 1:
             sol = dtn.build_root_gpu(None, tree, ctx=ctx, stencil_device_ptr=stencil_d.data_ptr())
         else:  # subtree-sharded build: shards on every GPU, top merges + inverse on rank 0
-            sol = SH.build_distributed(eng_dev, rank, world)
+            sol = SH.build_collective(None, tree, ctx, stencil_device_ptr=stencil_d.data_ptr())
         Y = dtn.apply_dtn(sol, X_d) if sol is not None else None
         return sol, Y
 
@@ -389,13 +388,12 @@ def run_b200(args, cfg, rank, world, local):
     op_h = dtn.DiscreteOperator(op.n, op.h, op.mode, pin_st)
     pin_x = torch.empty((nvec, nb), dtype=torch.float64, pin_memory=True).numpy().T
     pin_x[...] = X_h
-    eng_host = SH.GpuShardEngine(op_h, tree, ctx=ctx, device=dev)
 
     def e2e_step():
         if world == 1:
             s = dtn.build_root_gpu(op_h, tree, ctx=ctx, export_S=True)
         else:
-            s = SH.build_distributed(eng_host, rank, world)
+            s = SH.build_collective(op_h, tree, ctx)
         if s is not None:
             dtn.apply_dtn(s, pin_x)
             s.S_dense
@@ -458,8 +456,9 @@ def run_b200(args, cfg, rank, world, local):
         "config": {"workload": f"config{args.config}: {cfg['name']} n={n_int} interior (ref n={n}), "
                                f"{cfg['leaf']}x{cfg['leaf']} leaves, dense FP64 merges, G applied to "
                                f"{nvec} uniform[-1,1] vectors",
-                   "parallelism": (f"subtree shards x{world} (NCCL gather of shard S to rank 0, top merges + "
-                                   f"root inverse on rank 0)" if world > 1 else "single GPU"),
+                   "parallelism": (f"collective build x{world}: subtree shards, shard S all-gathered, top merges "
+                                   f"and root inverse column-sharded (NCCL in the engine)" if world > 1
+                                   else "single GPU"),
                    "l2": "flushed between timed steps (256 MB write)"},
         "e2e": {"value": e2e_value, "unit": "grid-points/s",
                 "h2d_bytes_per_step": int(op.stencil.nbytes + X_h.nbytes),
@@ -558,7 +557,7 @@ def run_b200_compressed(args, cfg, rank, world, local):
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    ctx = dtn.Context(local)
+    ctx = dtn.collective_context(local) if world > 1 else dtn.Context(local)
     stream = torch.cuda.current_stream(dev)
     ctx.set_stream(stream.cuda_stream or 1)
     n_int = cfg["n_int"]
@@ -570,12 +569,11 @@ def run_b200_compressed(args, cfg, rank, world, local):
     stencil_d = torch.from_numpy(op.stencil).to(dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
     from paper_1302_5995_b200 import shard as SH
-    eng_dev = SH.GpuShardEngine(None, tree, ctx=ctx, stencil_device_ptr=stencil_d.data_ptr(), device=dev, accel=opt)
 
     def device_step():
         if world == 1:
             return dtn.build_root_accel(None, tree, opt, ctx=ctx, stencil_device_ptr=stencil_d.data_ptr())
-        return SH.build_distributed(eng_dev, rank, world)
+        return SH.build_collective(None, tree, ctx, stencil_device_ptr=stencil_d.data_ptr(), accel=opt)
 
     def barrier():
         if world > 1:
@@ -611,11 +609,10 @@ def run_b200_compressed(args, cfg, rank, world, local):
     pin_st = torch.empty(op.stencil.shape, dtype=torch.float64, pin_memory=True).numpy()
     pin_st[...] = op.stencil
     op_h = dtn.DiscreteOperator(op.n, op.h, op.mode, pin_st)
-    eng_host = SH.GpuShardEngine(op_h, tree, ctx=ctx, device=dev, accel=opt)
     d2h = [0]
 
     def e2e_step():
-        s_ = dtn.build_root_accel(op_h, tree, opt, ctx=ctx) if world == 1 else SH.build_distributed(eng_host, rank, world)
+        s_ = SH.build_collective(op_h, tree, ctx, accel=opt)
         if s_ is not None:
             d2h[0] = len(H.serialize(s_.S_hbs)) + len(H.serialize(s_.G_hbs))
 
@@ -662,8 +659,9 @@ def run_b200_compressed(args, cfg, rank, world, local):
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE config shapes)",
         "config": {"workload": workload_text(args, cfg),
-                   "parallelism": (f"subtree shards x{world} (structured shard builds, NCCL gather of shard S to "
-                                   f"rank 0, top merges + compression on rank 0)" if world > 1 else "single GPU"),
+                   "parallelism": (f"collective build x{world}: structured shard subtrees, shard S all-gathered, "
+                                   f"top merges column-sharded (NCCL in the engine), root compressed on every rank"
+                                   if world > 1 else "single GPU"),
                    "l2": "flushed between timed steps (256 MB write)"},
         "e2e": {"value": e2e_value, "unit": "grid-points/s", "h2d_bytes_per_step": int(op.stencil.nbytes),
                 "d2h_bytes_per_step": int(d2h[0])},

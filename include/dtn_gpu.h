@@ -67,7 +67,12 @@ typedef struct {
   int64_t crossover;   /* AccelOptions::crossover: root boundaries >= crossover are compressed */
   int32_t nshards;     /* subtree sharding: 1, 2 (W|E), 4 (quadrants), 8 (quadrant halves) */
   int32_t shard;       /* >= 0: build only this shard's S; -1: full build (nshards == 1) or the top of
-                          the tree from prob.shard_S (nshards > 1) */
+                          the tree from prob.shard_S (nshards > 1); -2: collective build over the
+                          context's NCCL world (dtn_gpu_create_rank, nshards == world): shard `rank`
+                          locally, shard S gathered to every rank, the top merges column-sharded
+                          (interface LU redundant, boundary columns split, ncclAllGather per wave);
+                          S (and G) on every rank; -3: the same split computed on this one device
+                          (every shard and column chunk in turn, no communication) */
   double* export_S;    /* optional host buffer (page-locked for overlap): receives S (column-major,
                           leading dimension export_lds) during the build, overlapping the root inverse */
   int64_t export_lds;
@@ -131,6 +136,11 @@ typedef struct {
 } dtn_kernel_stats;
 
 int dtn_gpu_create(dtn_ctx** ctx, int device);
+/* Multi-GPU, one process per GPU: rank 0 draws a 128-byte NCCL unique id,
+ * the launcher hands it to every rank, and each rank creates its context on its device;
+ * the context owns the NCCL communicator of the collective builds (opts.shard = -2). */
+int dtn_gpu_nccl_unique_id(uint8_t* id);
+int dtn_gpu_create_rank(dtn_ctx** ctx, int device, int nranks, int rank, const uint8_t* id);
 void dtn_gpu_destroy(dtn_ctx* ctx);
 const char* dtn_gpu_last_error(const dtn_ctx* ctx);
 /* kernel launches issued so far by the HBS code (compress, invert_hbs, apply), process-wide */
@@ -180,6 +190,11 @@ int dtn_gpu_kernel_stats(const dtn_op* op, dtn_kernel_stats* out, int32_t max, i
  * rect = x0, x1, y0, y1 of its unknown rectangle; nb = its boundary size. */
 int dtn_gpu_shard_info(int32_t n, int32_t n_leaf, int32_t leaf_side, int32_t nshards, int32_t shard, int32_t* rect,
                        int64_t* nb);
+
+/* Work (flops) per rank of a collective build over nranks GPUs (opts.shard = -2), host
+ * only: per_rank[r] (nranks entries) and the single-GPU build's algorithmic flops */
+int dtn_gpu_collective_flops(int32_t n, int32_t n_leaf, int32_t leaf_side, int32_t nranks, int32_t want_G,
+                             double* per_rank, double* single_gpu);
 
 /* Test hook: partial LU (pivots among the first ni rows) of a host n x n
  * column-major matrix with the engine's blocked kernels; ni == n is a full LU. */

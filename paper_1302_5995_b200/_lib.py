@@ -47,14 +47,14 @@ class dtn_kernel_stats(C.Structure):
 
 
 EXPORTS = [
-    "dtn_gpu_create", "dtn_gpu_destroy", "dtn_gpu_last_error", "dtn_gpu_set_stream", "dtn_gpu_build",
+    "dtn_gpu_create", "dtn_gpu_nccl_unique_id", "dtn_gpu_create_rank", "dtn_gpu_destroy", "dtn_gpu_last_error", "dtn_gpu_set_stream", "dtn_gpu_build",
     "dtn_gpu_free", "dtn_gpu_boundary", "dtn_gpu_export", "dtn_gpu_export_device", "dtn_gpu_device_ptrs",
     "dtn_gpu_apply", "dtn_gpu_ring_dtn", "dtn_gpu_body_map",
     "dtn_gpu_num_boxes", "dtn_gpu_box_info", "dtn_gpu_box_schur", "dtn_gpu_level_stats", "dtn_gpu_build_stats", "dtn_gpu_kernel_stats",
     "dtn_discretize_continuum", "dtn_discretize_network", "dtn_debug_partial_lu", "dtn_gpu_shard_info",
     "dtn_gpu_hbs_compress", "dtn_gpu_hbs_compress_op", "dtn_gpu_hbs_free", "dtn_gpu_hbs_info", "dtn_gpu_hbs_tree",
     "dtn_gpu_hbs_factor", "dtn_gpu_hbs_apply", "dtn_gpu_hbs_serialize", "dtn_gpu_hbs_deserialize",
-    "dtn_gpu_hbs_invert", "dtn_gpu_build_accel", "dtn_gpu_root_rhs", "dtn_gpu_hbs_launch_count",
+    "dtn_gpu_hbs_invert", "dtn_gpu_build_accel", "dtn_gpu_root_rhs", "dtn_gpu_hbs_launch_count", "dtn_gpu_collective_flops",
 ]
 
 _lib = None
@@ -113,6 +113,9 @@ def lib():
     L.dtn_gpu_hbs_deserialize.argtypes = [vp, vp, C.c_uint64, P(vp)]
     L.dtn_gpu_hbs_invert.argtypes = [vp, P(vp)]
     L.dtn_gpu_root_rhs.argtypes = [vp, vp, i64, C.c_int]
+    L.dtn_gpu_nccl_unique_id.argtypes = [vp]
+    L.dtn_gpu_create_rank.argtypes = [P(vp), C.c_int, C.c_int, C.c_int, vp]
+    L.dtn_gpu_collective_flops.argtypes = [i32, i32, i32, i32, i32, vp, vp]
     L.dtn_gpu_hbs_launch_count.argtypes = []
     L.dtn_gpu_hbs_launch_count.restype = C.c_ulonglong
     L.dtn_gpu_build_accel.argtypes = [vp, vp, vp, i64, P(vp), P(vp), P(vp), P(f64)]

@@ -28,6 +28,7 @@
 #include "common.cuh"
 #include "plan.hpp"
 #include "hbs.hpp"
+#include "nccl_dl.hpp"
 
 namespace dtnb {
 cudaError_t launch_small_elim(const KernelArgs&, const int*, int, int, bool, cudaStream_t);
@@ -62,6 +63,7 @@ cudaError_t launch_perm_only(const int*, int, int*, cudaStream_t);
 cudaError_t blocked_init();
 cudaError_t hbs_kernels_init();
 cudaError_t struct_init();
+cudaError_t launch_perm_identity_cols(const int*, int, int, int, double*, int, cudaStream_t);
 cudaError_t launch_sgather_red(const KernelArgs&, const int*, int, int, cudaStream_t);
 cudaError_t launch_kk_gather(const KernelArgs&, const int*, int, int, cudaStream_t);
 cudaError_t launch_factor_gather(const KernelArgs&, const int*, int, long long, cudaStream_t);
@@ -117,7 +119,8 @@ struct WaveLaunch {
   int fw_copy_off = 0, fw_cnt = 0, fw_gather_off = 0, fw_max_cols = 0;
   std::vector<int> fw_toff, fw_goff, fw_n, fw_tiles, fw_k, fw_cols;
   std::vector<double> fw_flops;
-  int fin_off = 0, fin_tiles = 0, fin_k = 0;       // final GEMM S -= M_bi X
+  int fin_off = 0, fin_tiles = 0, fin_k = 0, fin_cnt = 0;  // final GEMM S -= M_bi X (descriptors)
+  std::vector<int> gather_nodes;                   // column-sharded merges: ncclAllGather after the wave
   bool fin_aligned = true;
   double fin_flops = 0.0;
   // compressed engine: dense blocked merges (gather) vs structured merges (reduced system)
@@ -223,6 +226,16 @@ struct PlanDev {
   cudaGraphExec_t gexec = nullptr;
   int graph_want_G = -1;
   int launches = 0;
+  void* comm = nullptr;  // ncclComm_t of a collective top build (the context's)
+  // collective top build: G by column chunks, G[:, c0:c1] = U^{-1} L^{-1} P[:, c0:c1]
+  // (forward / backward block substitution on the root LU, this rank's chunk)
+  int root_cw = 0;
+  std::vector<std::pair<int, int>> root_chunks;
+  std::vector<GemmDesc> h_rg;  // per block step: forward updates, then backward updates
+  std::vector<TrsmDesc> h_rt;  // per block step: forward (unit lower), then backward (upper)
+  std::vector<int> rg_off, rg_cnt, rt_off, rt_cnt;  // [0, nblk) forward steps, [nblk, 2 nblk) backward
+  GemmDesc* d_rg = nullptr;
+  TrsmDesc* d_rt = nullptr;
   // compressed engine descriptors (arena offsets relocated at upload) and statistics
   std::vector<CopyDesc> h_sm_copy;
   std::vector<GemmDesc> h_sg;
@@ -247,7 +260,7 @@ struct PlanDev {
     for (void* p : std::initializer_list<void*>{d_nodes, d_pos, d_arena, d_piv, d_pivstat, d_lists, d_stencil, d_S, d_G,
                                                 d_perm, d_norm, d_inv_descs, d_W, d_LUp, d_UI, d_UI2, d_tinv, d_root_trs, d_load_col, d_F, d_F_desc, d_bs_gemm,
                                                 d_bs_copy, d_tri, d_trs, d_chk, d_bad, d_fw_copy, d_fw_gather,
-                                                d_fw_trs, d_fw_gemm, d_sm_copy, d_sg, d_sg2, d_qr, d_eps, d_qstat})
+                                                d_fw_trs, d_fw_gemm, d_sm_copy, d_sg, d_sg2, d_qr, d_eps, d_qstat, d_rg, d_rt})
       if (p) cudaFree(p);
     if (h_qstat) cudaFreeHost(h_qstat);
     if (h_pivstat) cudaFreeHost(h_pivstat);
@@ -396,7 +409,10 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
     for (int id : wv.micro) L.flops += merge_flop_count(P.nodes[id].ni, P.nodes[id].nb);
   }
   // Schur-form descriptors: X = U^{-1} Y by 128-row blocks from the bottom
-  // (T = Uinv_k Y_k; Y_top -= U_top,k T; Y_k = T), then S -= M_bi X.
+  // (T = Uinv_k Y_k; Y_top -= U_top,k T; Y_k = T), then S -= M_bi X. Every
+  // descriptor covers one column segment [c0, c1) of a node's boundary columns:
+  // the whole range, or (collective top build, Node::colshard) this rank's chunk
+  // -- or every rank's chunk in turn when the split is checked on one device.
   {
     std::vector<GemmDesc> gd;
     std::vector<CopyDesc> cd;
@@ -410,8 +426,20 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
     int64_t gtmp_need = 0;
     // the deferred columns' staging area sits after the root-LU region of the arena
     D->gtmp_off = align_up(D->lu_off + int64_t(D->ldlu) * nb, 32);
-    double* A0 = nullptr;  // descriptors hold absolute pointers into the arena (allocated below)
-    (void)A0;
+    auto segs = [&](const Node& nd) {
+      std::vector<std::pair<int, int>> out;
+      const int ncy = nd.sys_nb + P.key.nloads;
+      if (!nd.colshard) {
+        out.push_back({0, ncy});
+        return out;
+      }
+      for (int r = 0; r < P.key.world; ++r) {
+        if (P.key.wrank >= 0 && r != P.key.wrank) continue;
+        const int c0 = r * nd.cw, c1 = std::min(ncy, c0 + nd.cw);
+        if (c1 > c0) out.push_back({c0, c1});
+      }
+      return out;
+    };
     for (size_t w = 0; w < P.waves.size(); ++w) {
       WaveLaunch& L = D->wl[w];
       const Wave& wv = P.waves[w];
@@ -427,12 +455,15 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
       L.tri_blocks = maxblk;
       // deferred boundary columns: M_ib -> temp (ni x ncy), gathered back by perm,
       // then forward substitution by 128-row blocks (top down). Decided per wave by
-      // the boundary-column work of its rank-32 updates, sum of ni (ncols - ni)
+      // the boundary-column work of its rank-32 updates, sum of ni (ncols - ni);
+      // always for column-sharded merges (their LU must not touch the boundary columns)
       {
         double work = 0.0;
         for (int id : wv.blocked) work += double(P.nodes[id].ni) * double(D->h_nodes[id].ncols - P.nodes[id].ni);
         if (work >= defer_min_work())
           for (int id : wv.blocked) D->h_nodes[id].defer = P.nodes[id].ni >= 256 ? 1 : 0;
+        for (int id : wv.blocked)
+          if (P.nodes[id].colshard) D->h_nodes[id].defer = 1;
       }
       {
         int64_t toff = D->gtmp_off;
@@ -443,15 +474,19 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
           const Node& nd = P.nodes[id];
           if (!D->h_nodes[id].defer) continue;
           const int64_t M = nd.m_off, ldm = nd.ldm;
-          const int ncy = nd.sys_nb + P.key.nloads, ldt = int(align_up(nd.ni, 2));
-          fwc.push_back(CopyDesc{reinterpret_cast<const double*>(M + nd.ni * ldm), reinterpret_cast<double*>(toff),
-                                 int(ldm), ldt, nd.ni, ncy});
-          fwg.push_back(RowGatherDesc{reinterpret_cast<const double*>(toff), reinterpret_cast<double*>(M + nd.ni * ldm),
-                                      nd.piv_off, ldt, int(ldm), nd.ni, ncy});
-          toff += int64_t(ldt) * ncy;
-          ++L.fw_cnt;
+          const int ldt = int(align_up(nd.ni, 2));
+          for (auto [c0, c1] : segs(nd)) {
+            const int ncy = c1 - c0;
+            const int64_t Yc = M + (int64_t(nd.ni) + c0) * ldm;
+            fwc.push_back(CopyDesc{reinterpret_cast<const double*>(Yc), reinterpret_cast<double*>(toff), int(ldm), ldt,
+                                   nd.ni, ncy});
+            fwg.push_back(RowGatherDesc{reinterpret_cast<const double*>(toff), reinterpret_cast<double*>(Yc),
+                                        nd.piv_off, ldt, int(ldm), nd.ni, ncy});
+            toff += int64_t(ldt) * ncy;
+            ++L.fw_cnt;
+            L.fw_max_cols = std::max(L.fw_max_cols, ncy);
+          }
           fmax = std::max(fmax, (nd.ni + 127) / 128);
-          L.fw_max_cols = std::max(L.fw_max_cols, ncy);
         }
         gtmp_need = std::max(gtmp_need, toff - D->gtmp_off);
         for (int t = 0; t < fmax; ++t) {
@@ -466,20 +501,22 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
             if (t >= nblk) continue;
             const int64_t M = nd.m_off, ldm = nd.ldm;
             const int k0 = t * 128, k1 = std::min(nd.ni, k0 + 128), bk = k1 - k0;
-            const int ncy = nd.sys_nb + P.key.nloads;
-            // left-looking: Y_k -= L[k0:k1, 0:k0] Y[0:k0] (one GEMM, K = k0: the same
-            // subtractions in the same order as the right-looking block updates), then
-            // Y_k <- L_kk^{-1} Y_k (unit lower)
-            fwt.push_back(TrsmDesc{reinterpret_cast<const double*>(M + k0 + int64_t(k0) * ldm),
-                                   reinterpret_cast<double*>(M + k0 + nd.ni * ldm), int(ldm), int(ldm), bk, ncy});
-            fwm.push_back(GemmDesc{reinterpret_cast<const double*>(M + k0), reinterpret_cast<const double*>(M + nd.ni * ldm),
-                                   reinterpret_cast<double*>(M + k0 + nd.ni * ldm), bk, ncy, k0, int(ldm), int(ldm),
-                                   int(ldm)});
-            tiles = std::max(tiles, gemm_tiles(bk, ncy));
+            for (auto [c0, c1] : segs(nd)) {
+              const int ncy = c1 - c0;
+              const int64_t Yc = M + (int64_t(nd.ni) + c0) * ldm;
+              // left-looking: Y_k -= L[k0:k1, 0:k0] Y[0:k0] (one GEMM, K = k0: the same
+              // subtractions in the same order as the right-looking block updates), then
+              // Y_k <- L_kk^{-1} Y_k (unit lower)
+              fwt.push_back(TrsmDesc{reinterpret_cast<const double*>(M + k0 + int64_t(k0) * ldm),
+                                     reinterpret_cast<double*>(Yc + k0), int(ldm), int(ldm), bk, ncy});
+              fwm.push_back(GemmDesc{reinterpret_cast<const double*>(M + k0), reinterpret_cast<const double*>(Yc),
+                                     reinterpret_cast<double*>(Yc + k0), bk, ncy, k0, int(ldm), int(ldm), int(ldm)});
+              tiles = std::max(tiles, gemm_tiles(bk, ncy));
+              mc = std::max(mc, ncy);
+              fl += double(bk) * bk * ncy + 2.0 * double(bk) * ncy * k0;
+              ++cnt;
+            }
             kk = std::max(kk, k0);
-            mc = std::max(mc, ncy);
-            fl += double(bk) * bk * ncy + 2.0 * double(bk) * ncy * k0;
-            ++cnt;
           }
           L.fw_n.push_back(cnt);
           L.fw_tiles.push_back(tiles);
@@ -501,29 +538,31 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
           if (sblk < 0) continue;
           const int64_t M = nd.m_off, ldm = nd.ldm;
           const int k0 = sblk * 128, k1 = std::min(nd.ni, k0 + 128), bk = k1 - k0;
-          const int ncy = nd.sys_nb + P.key.nloads;  // boundary columns + body-load columns
-          // substitution variant: Y_k <- U_kk^{-1} Y_k in place, Y[0:k0] -= U[0:k0, k0:k1] Y_k
-          trs.push_back(TrsmDesc{reinterpret_cast<const double*>(M + k0 + int64_t(k0) * ldm),
-                                 reinterpret_cast<double*>(M + k0 + nd.ni * ldm), int(ldm), int(ldm), bk, ncy});
-          gs.push_back(GemmDesc{reinterpret_cast<const double*>(M + int64_t(k0) * ldm),
-                                reinterpret_cast<const double*>(M + k0 + nd.ni * ldm),
-                                reinterpret_cast<double*>(M + nd.ni * ldm), k0, ncy, bk, int(ldm), int(ldm), int(ldm)});
-          // default (explicit block inverse): T = Uinv_k Y_k; Y[0:k0] -= U[0:k0, k0:k1] T; Y_k = T
-          const int64_t uinv = nd.uinv_off + int64_t(sblk) * 2 * 128 * 128 + 128 * 128;
-          gd.push_back(GemmDesc{reinterpret_cast<const double*>(uinv),
-                                reinterpret_cast<const double*>(M + k0 + nd.ni * ldm),
-                                reinterpret_cast<double*>(nd.t_off), bk, ncy, bk, 128, int(ldm), 128});
-          g2.push_back(GemmDesc{reinterpret_cast<const double*>(M + int64_t(k0) * ldm),
-                                reinterpret_cast<const double*>(nd.t_off), reinterpret_cast<double*>(M + nd.ni * ldm), k0,
-                                ncy, bk, int(ldm), 128, int(ldm)});
-          cd.push_back(CopyDesc{reinterpret_cast<const double*>(nd.t_off),
-                                reinterpret_cast<double*>(M + k0 + nd.ni * ldm), 128, int(ldm), bk, ncy});
-          t1 = std::max(t1, gemm_tiles(bk, ncy));
-          t2 = std::max(t2, gemm_tiles(std::max(k0, 1), ncy));
+          for (auto [c0, c1] : segs(nd)) {
+            const int ncy = c1 - c0;  // boundary columns + body-load columns (this segment)
+            const int64_t Yc = M + (int64_t(nd.ni) + c0) * ldm;
+            // substitution variant: Y_k <- U_kk^{-1} Y_k in place, Y[0:k0] -= U[0:k0, k0:k1] Y_k
+            trs.push_back(TrsmDesc{reinterpret_cast<const double*>(M + k0 + int64_t(k0) * ldm),
+                                   reinterpret_cast<double*>(Yc + k0), int(ldm), int(ldm), bk, ncy});
+            gs.push_back(GemmDesc{reinterpret_cast<const double*>(M + int64_t(k0) * ldm),
+                                  reinterpret_cast<const double*>(Yc + k0), reinterpret_cast<double*>(Yc), k0, ncy, bk,
+                                  int(ldm), int(ldm), int(ldm)});
+            // default (explicit block inverse): T = Uinv_k Y_k; Y[0:k0] -= U[0:k0, k0:k1] T; Y_k = T
+            const int64_t uinv = nd.uinv_off + int64_t(sblk) * 2 * 128 * 128 + 128 * 128;
+            gd.push_back(GemmDesc{reinterpret_cast<const double*>(uinv), reinterpret_cast<const double*>(Yc + k0),
+                                  reinterpret_cast<double*>(nd.t_off), bk, ncy, bk, 128, int(ldm), 128});
+            g2.push_back(GemmDesc{reinterpret_cast<const double*>(M + int64_t(k0) * ldm),
+                                  reinterpret_cast<const double*>(nd.t_off), reinterpret_cast<double*>(Yc), k0, ncy, bk,
+                                  int(ldm), 128, int(ldm)});
+            cd.push_back(CopyDesc{reinterpret_cast<const double*>(nd.t_off), reinterpret_cast<double*>(Yc + k0), 128,
+                                  int(ldm), bk, ncy});
+            t1 = std::max(t1, gemm_tiles(bk, ncy));
+            t2 = std::max(t2, gemm_tiles(std::max(k0, 1), ncy));
+            mc = std::max(mc, ncy);
+            fl += double(bk) * bk * ncy + 2.0 * k0 * double(ncy) * bk;
+            ++cnt;
+          }
           kk = std::max(kk, bk);
-          mc = std::max(mc, ncy);
-          fl += double(bk) * bk * ncy + 2.0 * k0 * double(ncy) * bk;
-          ++cnt;
         }
         gd.insert(gd.end(), g2.begin(), g2.end());
         L.bs_off.push_back(off);
@@ -537,17 +576,23 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
         L.bs_flops.push_back(fl);
       }
       L.fin_off = int(gd.size());
+      L.fin_cnt = 0;
       for (int id : wv.blocked) {
         const Node& nd = P.nodes[id];
         const int64_t M = nd.m_off, ldm = nd.ldm;
-        const int ncy = nd.sys_nb + P.key.nloads;  // S and the body-load columns (dense_nd.cpp:181-184)
-        gd.push_back(GemmDesc{reinterpret_cast<const double*>(M + nd.ni), reinterpret_cast<const double*>(M + nd.ni * ldm),
-                              reinterpret_cast<double*>(M + nd.ni + nd.ni * ldm), nd.sys_nb, ncy, nd.ni, int(ldm),
-                              int(ldm), int(ldm)});
-        L.fin_tiles = std::max(L.fin_tiles, gemm_tiles(nd.sys_nb, ncy));
+        for (auto [c0, c1] : segs(nd)) {  // S and the body-load columns (dense_nd.cpp:181-184)
+          const int ncy = c1 - c0;
+          const int64_t Yc = M + (int64_t(nd.ni) + c0) * ldm;
+          gd.push_back(GemmDesc{reinterpret_cast<const double*>(M + nd.ni), reinterpret_cast<const double*>(Yc),
+                                reinterpret_cast<double*>(Yc + nd.ni), nd.sys_nb, ncy, nd.ni, int(ldm), int(ldm),
+                                int(ldm)});
+          L.fin_tiles = std::max(L.fin_tiles, gemm_tiles(nd.sys_nb, ncy));
+          L.fin_flops += 2.0 * nd.sys_nb * double(ncy) * nd.ni;
+          ++L.fin_cnt;
+        }
         L.fin_k = std::max(L.fin_k, nd.ni);
         L.fin_aligned = L.fin_aligned && (nd.ni % 2 == 0);
-        L.fin_flops += 2.0 * nd.sys_nb * double(nd.sys_nb) * nd.ni;
+        if (nd.colshard) L.gather_nodes.push_back(id);
       }
     }
     D->h_trs = std::move(trs);
@@ -739,7 +784,9 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
   D->lds = int(align_up(nb, 8));
   D->d_S = dalloc<double>(size_t(D->lds) * nb);
   D->ldg = int(align_up(nb, 8));
-  D->d_G = dalloc<double>(size_t(D->ldg) * nb);
+  if (P.key.world > 1) D->root_cw = (nb + P.key.world - 1) / P.key.world;
+  // (collective: room for every rank's column chunk, gathered in place)
+  D->d_G = dalloc<double>(size_t(D->ldg) * std::max<int64_t>(nb, int64_t(P.key.world) * D->root_cw));
   if (P.key.nloads > 0) {
     D->h_F_desc.A = D->d_G;
     D->h_F_desc.lda = D->ldg;
@@ -823,6 +870,49 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
     const int k0 = kb_ * 128, k1 = std::min(nb, k0 + 128), bk = k1 - k0;
     D->h_inv_descs.push_back(GemmDesc{D->d_UI2 + k0 + int64_t(k0) * D->ldg, D->d_G + k0, D->d_W + k0, bk, nb, nb - k0,
                                       D->ldg, D->ldg, D->ldg});
+  }
+  if (P.key.world > 1) {  // collective top build: G column chunks by block substitution
+    const int cw = D->root_cw;
+    for (int r = 0; r < P.key.world; ++r) {
+      if (P.key.wrank >= 0 && r != P.key.wrank) continue;
+      const int c0 = r * cw, c1 = std::min(nb, c0 + cw);
+      if (c1 > c0) D->root_chunks.push_back({c0, c1});
+    }
+    double* G = D->d_G;
+    const int ldg = D->ldg, ldl = D->ldlu;
+    for (int t = 0; t < nblk; ++t) {  // forward, left-looking: G_k -= L[k, :k0] G[:k0]; G_k <- L_kk^{-1} G_k
+      const int k0 = t * 128, k1 = std::min(nb, k0 + 128), bk = k1 - k0;
+      D->rg_off.push_back(int(D->h_rg.size()));
+      D->rt_off.push_back(int(D->h_rt.size()));
+      for (auto [c0, c1] : D->root_chunks) {
+        if (k0 > 0)
+          D->h_rg.push_back(GemmDesc{LU + k0, G + int64_t(c0) * ldg, G + k0 + int64_t(c0) * ldg, bk, c1 - c0, k0, ldl,
+                                     ldg, ldg});
+        D->h_rt.push_back(TrsmDesc{LU + k0 + int64_t(k0) * ldl, G + k0 + int64_t(c0) * ldg, ldl, ldg, bk, c1 - c0});
+      }
+      D->rg_cnt.push_back(int(D->h_rg.size()) - D->rg_off.back());
+      D->rt_cnt.push_back(int(D->h_rt.size()) - D->rt_off.back());
+    }
+    for (int t = nblk - 1; t >= 0; --t) {  // backward: G_k <- U_kk^{-1} G_k; G[:k0] -= U[:k0, k] G_k
+      const int k0 = t * 128, k1 = std::min(nb, k0 + 128), bk = k1 - k0;
+      D->rg_off.push_back(int(D->h_rg.size()));
+      D->rt_off.push_back(int(D->h_rt.size()));
+      for (auto [c0, c1] : D->root_chunks) {
+        D->h_rt.push_back(TrsmDesc{LU + k0 + int64_t(k0) * ldl, G + k0 + int64_t(c0) * ldg, ldl, ldg, bk, c1 - c0});
+        if (k0 > 0)
+          D->h_rg.push_back(GemmDesc{LU + int64_t(k0) * ldl, G + k0 + int64_t(c0) * ldg, G + int64_t(c0) * ldg, k0,
+                                     c1 - c0, bk, ldl, ldg, ldg});
+      }
+      D->rg_cnt.push_back(int(D->h_rg.size()) - D->rg_off.back());
+      D->rt_cnt.push_back(int(D->h_rt.size()) - D->rt_off.back());
+    }
+    if (!D->h_rg.empty()) {
+      D->d_rg = dalloc<GemmDesc>(D->h_rg.size());
+      CK(cudaMemcpy(D->d_rg, D->h_rg.data(), D->h_rg.size() * sizeof(GemmDesc), cudaMemcpyHostToDevice));
+    }
+    D->d_rt = dalloc<TrsmDesc>(std::max<size_t>(D->h_rt.size(), 1));
+    if (!D->h_rt.empty())
+      CK(cudaMemcpy(D->d_rt, D->h_rt.data(), D->h_rt.size() * sizeof(TrsmDesc), cudaMemcpyHostToDevice));
   }
   D->d_inv_descs = dalloc<GemmDesc>(D->h_inv_descs.size());
   CK(cudaMemcpy(D->d_inv_descs, D->h_inv_descs.data(), D->h_inv_descs.size() * sizeof(GemmDesc),
@@ -1100,9 +1190,21 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
         coff += cnt;
       }
       run(K_SCHUR, L.fin_flops, 0.0, [&] {
-        return launch_gemm_desc(D.d_bs_gemm + L.fin_off, L.blk_cnt, L.fin_tiles, L.fin_k, -1.0, 1.0, st,
+        return launch_gemm_desc(D.d_bs_gemm + L.fin_off, L.fin_cnt, L.fin_tiles, L.fin_k, -1.0, 1.0, st,
                                 L.fin_aligned);
       });
+      if (!L.gather_nodes.empty() && D.comm) {  // collective top build: every rank's column chunk to all
+        const NcclApi& nc = nccl();
+        nccl_check(nc.GroupStart(), "ncclGroupStart");
+        for (int id : L.gather_nodes) {
+          const Node& nd = P.nodes[id];
+          double* Mb = D.d_arena + nd.m_off + int64_t(nd.ni) * nd.ldm;
+          const size_t cnt = size_t(nd.ldm) * nd.cw;
+          nccl_check(nc.AllGather(Mb + cnt * P.key.wrank, Mb, cnt, ncclDouble, static_cast<ncclComm_t>(D.comm), st),
+                     "ncclAllGather (merge columns)");
+        }
+        nccl_check(nc.GroupEnd(), "ncclGroupEnd");
+      }
       if (L.sm_cnt) {  // Steps 2-3: S = M_kk + L_k C R_k
         const int* sl = D.d_lists + L.sm_off;
         run(K_SGATHER, 0.0, 0.0, [&] { return launch_kk_gather(a, sl, L.sm_cnt, L.sm_max_nb, st); });
@@ -1157,6 +1259,56 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
     blocked_lu(rl, nullptr, 1, nb, nb, 0, D.root_kb, true, false);
     // the panels maintain perm[pos] = original row of the root LU (P A = L U)
     const int* perm = D.d_piv + D.h_nodes[D.root_lu_node].piv_off;
+    if (P.key.world > 1) {  // collective top build: this rank's column chunk of G, gathered
+      const int nblk = (nb + 127) / 128, mb = std::min(nb, 128);
+      for (auto [c0, c1] : D.root_chunks)
+        run(K_MISC, 0.0, 8.0 * nb * (c1 - c0), [&] {
+          return launch_perm_identity_cols(perm, nb, c0, c1 - c0, D.d_G + int64_t(c0) * D.ldg, D.ldg, st);
+        });
+      int maxc = 0;
+      for (auto [c0, c1] : D.root_chunks) maxc = std::max(maxc, c1 - c0);
+      for (int q = 0; q < 2 * nblk; ++q) {
+        const bool fwd = q < nblk;
+        auto gem = [&] {
+          if (D.rg_cnt[q] == 0) return;
+          int tiles = 0, kmax = 0;
+          double f = 0.0;
+          for (int i = D.rg_off[q]; i < D.rg_off[q] + D.rg_cnt[q]; ++i) {
+            const GemmDesc& g = D.h_rg[i];
+            tiles = std::max(tiles, gemm_tiles(g.m, g.n));
+            kmax = std::max(kmax, g.k);
+            f += 2.0 * g.m * g.n * g.k;
+          }
+          run(K_INV_GEMM, f, 0.0, [&] {
+            return launch_gemm_desc(D.d_rg + D.rg_off[q], D.rg_cnt[q], tiles, kmax, -1.0, 1.0, st, true);
+          });
+        };
+        auto trs = [&] {
+          run(K_INV_TRSM, 0.0, 0.0, [&] {
+            return launch_trsm_batched(D.d_rt + D.rt_off[q], D.rt_cnt[q], maxc, mb, fwd, st);
+          });
+        };
+        if (fwd) {
+          gem();
+          trs();
+        } else {
+          trs();
+          gem();
+        }
+      }
+      if (D.comm) {
+        const size_t cnt = size_t(D.ldg) * D.root_cw;
+        nccl_check(nccl().AllGather(D.d_G + cnt * P.key.wrank, D.d_G, cnt, ncclDouble,
+                                    static_cast<ncclComm_t>(D.comm), st),
+                   "ncclAllGather (G columns)");
+      }
+      CK(cudaMemsetAsync(D.d_norm, 0, 2 * sizeof(unsigned long long), st));
+      run(K_MISC, 0.0, 8.0 * nb2, [&] { return launch_norm1(D.d_S, D.lds, nb, nb, D.d_norm, st); });
+      run(K_MISC, 0.0, 8.0 * nb2, [&] { return launch_norm1(D.d_G, D.ldg, nb, nb, D.d_norm + 1, st); });
+      if (events) CK(cudaEventRecord(D.ev_end, st));
+      D.launches = launches;
+      return;
+    }
     if (env_flag("DTN_TRIINV_REF")) {
       run(K_INV_TRSM, 0.0, 0.0, [&] { return launch_tri_inv_blocks(LU, D.ldlu, nb, D.d_tinv, st); });
     } else {
@@ -1261,6 +1413,11 @@ struct dtn_ctx {
   int device = 0;
   // structured merges: factor ranks learned per problem family (dtn_gpu_build)
   std::map<std::string, std::vector<std::pair<int, int>>> learned_ranks;
+  // multi-GPU (one process per GPU): this rank of `world`, the NCCL communicator
+  int world = 1, rank = 0;
+  ncclComm_t comm = nullptr;
+  double* d_gather = nullptr;  // shard-S gather buffer (world x slot doubles)
+  size_t gather_cap = 0;
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   std::vector<std::unique_ptr<PlanDev>> plans;
@@ -1359,11 +1516,44 @@ int dtn_gpu_create(dtn_ctx** out, int device) {
   });
 }
 
+int dtn_gpu_nccl_unique_id(uint8_t* id) {
+  return guarded(nullptr, [&] {
+    if (!id) throw std::invalid_argument("dtn_gpu_nccl_unique_id: null output");
+    ncclUniqueId u;
+    nccl_check(nccl().GetUniqueId(&u), "ncclGetUniqueId");
+    static_assert(sizeof(u.internal) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(id, u.internal, 128);
+  });
+}
+
+int dtn_gpu_create_rank(dtn_ctx** out, int device, int nranks, int rank, const uint8_t* id) {
+  if (!out) return DTN_EINVAL;
+  int rc = dtn_gpu_create(out, device);
+  if (rc != DTN_OK || nranks <= 1) return rc;
+  dtn_ctx* c = *out;
+  rc = guarded(c, [&] {
+    if (rank < 0 || rank >= nranks || !id) throw std::invalid_argument("dtn_gpu_create_rank: bad rank or id");
+    ncclUniqueId u;
+    std::memcpy(u.internal, id, 128);
+    CK(cudaSetDevice(device));
+    nccl_check(nccl().CommInitRank(&c->comm, nranks, u, rank), "ncclCommInitRank");
+    c->world = nranks;
+    c->rank = rank;
+  });
+  if (rc != DTN_OK) {
+    dtn_gpu_destroy(c);
+    *out = nullptr;
+  }
+  return rc;
+}
+
 void dtn_gpu_destroy(dtn_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   ctx->plans.clear();
+  if (ctx->comm) nccl().CommDestroy(ctx->comm);
+  if (ctx->d_gather) cudaFree(ctx->d_gather);
   if (ctx->d_x) cudaFree(ctx->d_x);
   if (ctx->d_y) cudaFree(ctx->d_y);
   if (ctx->d_desc) cudaFree(ctx->d_desc);
@@ -1386,8 +1576,12 @@ int dtn_gpu_set_stream(dtn_ctx* ctx, void* stream) {
 
 namespace {
 
+// world > 1: the top-of-tree build (opts->shard == -1, nshards == world) with its blocked
+// merges column-sharded (PlanKey::world, wrank; comm != null: this rank's chunk plus
+// ncclAllGather after each wave, comm == null: every chunk on this device)
 int build_impl(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts,
-               const std::vector<std::pair<int, int>>& ell_over, dtn_op** out) {
+               const std::vector<std::pair<int, int>>& ell_over, dtn_op** out, int world = 1, int wrank = -1,
+               void* comm = nullptr) {
   return guarded(ctx, [&] {
     if (!ctx || !prob || !opts || !out) throw std::invalid_argument("dtn_gpu_build: null argument");
     if (prob->n < 4) throw std::invalid_argument("discretize: n must be >= 4");
@@ -1406,6 +1600,11 @@ int build_impl(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts,
     if (key.nshards == 1) key.shard = -1;
     key.nloads = int(opts->nloads);
     key.keep = opts->keep_boxes ? 1 : 0;
+    if (world > 1) {
+      if (key.nshards != world || key.shard != -1) throw std::logic_error("collective top build: bad shard key");
+      key.world = world;
+      key.wrank = wrank;
+    }
     if (opts->engine == 1) {  // compressed engine: structured merges above the crossover
       if (opts->nloads > 0)
         throw std::invalid_argument("dtn_gpu_build: body loads ride through the dense merges (engine 0)");
@@ -1432,6 +1631,7 @@ int build_impl(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts,
       ctx->plans.push_back(make_plandev(key, ctx->device));
       D = ctx->plans.back().get();
     }
+    D->comm = comm;
     cudaStream_t st = ctx->stream;
     const bool want_G = opts->want_G != 0 && key.shard < 0;  // a shard's S is not inverted
     if (top_mode) {
@@ -1469,7 +1669,7 @@ int build_impl(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts,
     if (profile) {
       prof = std::make_unique<Prof>();
       enqueue_build(*D, st, want_G, prof.get());
-    } else if (use_graphs()) {
+    } else if (use_graphs() && !comm) {  // (collective builds enqueue NCCL calls directly)
       if (!D->gexec || D->graph_want_G != int(want_G)) {
         if (D->gexec) {
           CK(cudaGraphExecDestroy(D->gexec));
@@ -1567,7 +1767,7 @@ int build_impl(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts,
       return double(t);
     };
     dtn_build_stats& s = op->stats;
-    const bool graph_run = !profile && use_graphs();
+    const bool graph_run = !profile && use_graphs() && !comm;
     s.build_ms = ms(D->ev_start, D->ev_end);
     s.inverse_ms = graph_run ? 0.0 : ms(D->ev_root, D->ev_end);
     s.merge_flops = P.merge_flops;
@@ -1701,8 +1901,13 @@ bool raise_ranks(const dtn_op* op, double tol, std::vector<std::pair<int, int>>&
 
 extern "C" {
 
-int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, dtn_op** out) {
-  if (!ctx || !opts || opts->engine != 1) return build_impl(ctx, prob, opts, {}, out);
+}  // extern "C"
+
+namespace {
+
+int build_adaptive(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, dtn_op** out, int world = 1,
+                   int wrank = -1, void* comm = nullptr) {
+  if (!ctx || !opts || opts->engine != 1) return build_impl(ctx, prob, opts, {}, out, world, wrank, comm);
   // structured merges: the factor ranks adapt to the operator. A build whose sketches
   // did not resolve a factor to eps (the probe residual relative to the box operator's
   // scale, cf. lowrank_from_dense's eps sigma_max cut, lowrank.cpp:27-36) is repeated
@@ -1720,7 +1925,7 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
   }
   for (int attempt = 0;; ++attempt) {
     dtn_op* op = nullptr;
-    const int rc = build_impl(ctx, prob, opts, over, &op);
+    const int rc = build_impl(ctx, prob, opts, over, &op, world, wrank, comm);
     if (rc != DTN_OK) return rc;
     std::vector<std::pair<int, int>> next = over;
     if (attempt < 6 && raise_ranks(op, rank_tol_factor() * eps, next)) {
@@ -1742,6 +1947,92 @@ int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, d
     *out = op;
     return DTN_OK;
   }
+}
+
+// Collective build over `world` GPUs (one process per GPU, opts->shard == -2):
+// rank r builds shard r's subtree (no communication), the shard S blocks are gathered to
+// every rank (ncclAllGather), then every rank runs the top of the tree with its blocked
+// merges column-sharded -- interface LU redundant, this rank's chunk of the boundary
+// columns' substitutions and Schur GEMM, ncclAllGather of the chunks after each wave --
+// so the root S (and G) ends up on every rank. opts->shard == -3: the same split with
+// every shard and every chunk computed on this device (no communication), which
+// checks the partition on one GPU.
+int build_collective(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, dtn_op** out) {
+  const int N = opts->nshards;
+  const bool real = opts->shard == -2;
+  std::vector<int64_t> nbs(static_cast<size_t>(N), 0);
+  int rc = guarded(ctx, [&] {
+    if (!prob || !out) throw std::invalid_argument("dtn_gpu_build: null argument");
+    if (real && (ctx->world != N || !ctx->comm))
+      throw std::invalid_argument("collective build: nshards must equal the context's NCCL world (dtn_gpu_create_rank)");
+    if (opts->nloads > 0) throw std::invalid_argument("dtn_gpu_build: body loads are not supported in sharded builds");
+    int32_t rect[4];
+    for (int r = 0; r < N; ++r) {
+      const int e = dtn_gpu_shard_info(prob->n, opts->n_leaf, opts->leaf_side, N, r, rect, &nbs[size_t(r)]);
+      if (e != DTN_OK) throw std::invalid_argument(dtn_gpu_last_error(nullptr));
+    }
+  });
+  if (rc != DTN_OK) return rc;
+  int64_t slot = 0;
+  for (int64_t b : nbs) slot = std::max(slot, b * b);
+  slot = align_up(slot, 32);
+  rc = guarded(ctx, [&] {
+    CK(cudaSetDevice(ctx->device));
+    if (ctx->gather_cap < size_t(N) * size_t(slot)) {
+      if (ctx->d_gather) cudaFree(ctx->d_gather);
+      ctx->d_gather = nullptr;
+      ctx->gather_cap = 0;
+      CK(cudaMalloc(&ctx->d_gather, size_t(N) * size_t(slot) * 8));
+      ctx->gather_cap = size_t(N) * size_t(slot);
+    }
+  });
+  if (rc != DTN_OK) return rc;
+  cudaStream_t st = ctx->stream;
+  for (int r = 0; r < N; ++r) {
+    if (real && r != ctx->rank) continue;
+    dtn_opts os = *opts;
+    os.shard = r;
+    os.want_G = 0;
+    os.export_S = nullptr;
+    dtn_op* sop = nullptr;
+    rc = build_adaptive(ctx, prob, &os, &sop);
+    if (rc != DTN_OK) return rc;
+    rc = guarded(ctx, [&] {
+      const PlanDev& D = *sop->plan;
+      CK(cudaMemcpy2DAsync(ctx->d_gather + size_t(r) * slot, size_t(nbs[size_t(r)]) * 8, D.d_S, size_t(D.lds) * 8,
+                           size_t(nbs[size_t(r)]) * 8, size_t(nbs[size_t(r)]), cudaMemcpyDeviceToDevice, st));
+      CK(cudaStreamSynchronize(st));
+    });
+    dtn_gpu_free(sop);
+    if (rc != DTN_OK) return rc;
+  }
+  if (real) {
+    rc = guarded(ctx, [&] {
+      nccl_check(nccl().AllGather(ctx->d_gather + size_t(ctx->rank) * slot, ctx->d_gather, size_t(slot), ncclDouble,
+                                  ctx->comm, st),
+                 "ncclAllGather (shard S)");
+      CK(cudaStreamSynchronize(st));
+    });
+    if (rc != DTN_OK) return rc;
+  }
+  std::vector<const double*> ptrs(static_cast<size_t>(N), nullptr);
+  for (int r = 0; r < N; ++r) ptrs[size_t(r)] = ctx->d_gather + size_t(r) * slot;
+  dtn_problem pt = *prob;
+  pt.shard_S = ptrs.data();
+  pt.shard_S_on_device = 1;
+  dtn_opts ot = *opts;
+  ot.shard = -1;
+  return build_adaptive(ctx, &pt, &ot, out, N, real ? ctx->rank : -1, real ? static_cast<void*>(ctx->comm) : nullptr);
+}
+
+}  // namespace
+
+extern "C" {
+
+int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, dtn_op** out) {
+  if (ctx && opts && opts->nshards > 1 && (opts->shard == -2 || opts->shard == -3))
+    return build_collective(ctx, prob, opts, out);
+  return build_adaptive(ctx, prob, opts, out);
 }
 
 void dtn_gpu_free(dtn_op* op) {
@@ -2013,6 +2304,56 @@ int dtn_gpu_shard_info(int32_t n, int32_t n_leaf, int32_t leaf_side, int32_t nsh
       rect[3] = nd.r.y1;
     }
     if (nb) *nb = nd.nb;
+  });
+}
+
+// Work per rank of a collective build (host only): shard r's subtree, plus the top of
+// the tree with every column-sharded merge's interface LU redundant and its boundary
+// columns' substitutions (2 ni^2 per column) and Schur GEMM (2 nb ni per column) split
+// by chunk, small merges redundant, and (want_G) the root inverse as a redundant LU of
+// S plus this rank's chunk of the substitutions (2 nb^2 per column).
+int dtn_gpu_collective_flops(int32_t n, int32_t n_leaf, int32_t leaf_side, int32_t nranks, int32_t want_G,
+                             double* per_rank, double* single_gpu) {
+  return guarded(nullptr, [&] {
+    if (nranks < 2 || !per_rank) throw std::invalid_argument("dtn_gpu_collective_flops: bad arguments");
+    PlanKey key;
+    key.n = n;
+    key.n_leaf = n_leaf;
+    key.leaf_side = leaf_side;
+    key.micro_max = kDefaultMicro;
+    key.small_max = kSmallMax;
+    const Plan full = make_plan(key);
+    const int nb = full.nodes[full.root].nb;
+    if (single_gpu) *single_gpu = full.merge_flops + full.micro_flops + (want_G ? 2.0 * nb * double(nb) * nb : 0.0);
+    for (int r = 0; r < nranks; ++r) {
+      PlanKey ks = key;
+      ks.nshards = nranks;
+      ks.shard = r;
+      const Plan sp = make_plan(ks);
+      double f = sp.merge_flops + sp.micro_flops;
+      PlanKey kt = key;
+      kt.nshards = nranks;
+      kt.shard = -1;
+      kt.world = nranks;
+      kt.wrank = r;
+      const Plan tp = make_plan(kt);
+      for (size_t v = 0; v < tp.nodes.size(); ++v) {
+        const Node& nd = tp.nodes[v];
+        if (!tp.active[v] || nd.kind != NodeKind::merge) continue;
+        if (!nd.colshard) {
+          f += merge_flop_count(nd.ni, nd.nb);
+          continue;
+        }
+        const int c0 = r * nd.cw, c1 = std::min(nd.nb, c0 + nd.cw);
+        const double cols = std::max(0, c1 - c0);
+        f += (2.0 / 3.0) * nd.ni * double(nd.ni) * nd.ni + cols * (2.0 * nd.ni * double(nd.ni) + 2.0 * nd.nb * double(nd.ni));
+      }
+      if (want_G) {
+        const int cw = (nb + nranks - 1) / nranks, c0 = r * cw, c1 = std::min(nb, c0 + cw);
+        f += (2.0 / 3.0) * nb * double(nb) * nb + 2.0 * nb * double(nb) * std::max(0, c1 - c0);
+      }
+      per_rank[r] = f;
+    }
   });
 }
 

@@ -27,6 +27,22 @@ __global__ void scatter_identity_kernel(const int* __restrict__ perm, int n, dou
   }
 }
 
+// Columns [c0, c0 + w) of P (P A = L U, perm[pos] = original row): X(pos, j) = 1 iff
+// perm[pos] == c0 + j -- the right-hand sides of G's column chunk G = U^{-1} L^{-1} P.
+__global__ void perm_identity_cols_kernel(const int* __restrict__ perm, int n, int c0, int w, double* X, int ldx) {
+  const long long total = (long long)w * n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int r = int(e % n), c = int(e / n);
+    X[r + (long long)c * ldx] = perm[r] == c0 + c ? 1.0 : 0.0;
+  }
+}
+
+cudaError_t launch_perm_identity_cols(const int* perm, int n, int c0, int w, double* X, int ldx, cudaStream_t st) {
+  if (w <= 0 || n <= 0) return cudaSuccess;
+  perm_identity_cols_kernel<<<592, 256, 0, st>>>(perm, n, c0, w, X, ldx);
+  return cudaGetLastError();
+}
+
 // X[k0:k0+kbe, :] <- T^{-1} X[k0:k0+kbe, :] with T the kbe x kbe diagonal block
 // of the LU factors (lower: unit lower L; else upper U). One warp per column.
 __global__ void __launch_bounds__(256) trsm_rows_kernel(const double* __restrict__ LU, int ldlu, double* X, int ldx,

@@ -445,6 +445,11 @@ Plan make_plan(const PlanKey& key) {
       wv.small.push_back(i);
     } else {
       nd.blocked = true;
+      // collective top build: blocked merges above the shards split their columns
+      if (key.world > 1 && !P.inputs.empty() && !nd.smerge) {
+        nd.colshard = true;
+        nd.cw = (nd.nb + key.world - 1) / key.world;
+      }
       wv.blocked.push_back(i);
       if (nd.smerge) wv.smerge.push_back(i);
       wv.max_ni_blocked = std::max(wv.max_ni_blocked, nd.ni);
@@ -526,7 +531,10 @@ Plan make_plan(const PlanKey& key) {
           nd.cbuf_off = take(int64_t(nd.ldr) * nd.sys_nb, w + 1);
         } else {
           nd.ldm = int(align_up(nd.total, 8));
-          nd.m_off = take(int64_t(nd.ldm) * (nd.total + nl), death);
+          // (column-sharded merges: every rank's chunk is ldm x cw, the gather is in place)
+          const int64_t cols = nd.colshard ? std::max<int64_t>(nd.total, nd.ni + int64_t(key.world) * nd.cw)
+                                           : nd.total + nl;
+          nd.m_off = take(int64_t(nd.ldm) * cols, death);
           nd.s_off = nd.m_off + nd.ni + int64_t(nd.ni) * nd.ldm;
           nd.ld = nd.ldm;
           nd.rhs_off = nd.m_off + nd.ni + int64_t(nd.total) * nd.ldm;

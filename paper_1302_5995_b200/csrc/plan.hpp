@@ -86,6 +86,8 @@ struct Node {
   bool factors = false;  // structured box: factors formed at the end of its wave
   bool smerge = false;   // structured merge (both children structured)
   bool exact = false;    // structured box whose factors would be full rank: kept dense (exact)
+  bool colshard = false; // collective top build: boundary columns split over the ranks
+  int cw = 0;            // column chunk per rank (ceil(nb / world))
   int j0 = 0, jn = 0;    // J edge = positions [j0, j0 + jn) of the CCW boundary
   int ell = 0;           // factor rank (randomized range-finder sketch width)
   int sys_nb = 0;        // boundary columns of the blocked system: nb, or ra + rb (smerge)
@@ -124,11 +126,18 @@ struct PlanKey {
   // learned ranks: (J edge size, ell) overrides of the schedule, raised by the engine when a
   // factor's range-finder check fails (engine.cu, dtn_gpu_build)
   std::vector<std::pair<int, int>> ell_over;
+  // collective top build: the blocked merges above the shards are
+  // column-sharded over `world` ranks -- interface LU redundant on every rank, the
+  // boundary columns' substitutions and Schur GEMM split in `world` chunks of
+  // ceil(nb / world) columns, gathered after each wave (ncclAllGather). wrank: this
+  // rank's chunk, or -1: every chunk computed locally (single-device check of the split)
+  int world = 1, wrank = -1;
   bool operator==(const PlanKey& o) const {
     return n == o.n && n_leaf == o.n_leaf && leaf_side == o.leaf_side && micro_max == o.micro_max &&
            small_max == o.small_max && nshards == o.nshards && shard == o.shard && nloads == o.nloads &&
            structured == o.structured && crossover == o.crossover && ell_base == o.ell_base &&
-           ell_step == o.ell_step && keep == o.keep && ell_over == o.ell_over;
+           ell_step == o.ell_step && keep == o.keep && ell_over == o.ell_over && world == o.world &&
+           wrank == o.wrank;
   }
 };
 

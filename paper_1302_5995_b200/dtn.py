@@ -282,13 +282,25 @@ class LevelStats:
 class Context:
     """One engine context (device, stream, cached build plans)."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, world: int = 1, rank: int = 0, nccl_id: bytes | None = None):
+        """world > 1: one rank of a multi-GPU job (one process per GPU); the context owns
+        the NCCL communicator of the collective builds (dtn_gpu_create_rank), built from
+        the 128-byte unique id every rank received from rank 0 (collective_context)."""
         h = C.c_void_p()
-        rc = L.lib().dtn_gpu_create(C.byref(h), device)
+        if world > 1:
+            if nccl_id is None or len(nccl_id) != 128:
+                raise ValueError("Context: a 128-byte NCCL unique id is required for world > 1")
+            buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+            rc = L.lib().dtn_gpu_create_rank(C.byref(h), device, world, rank, buf)
+            what = "dtn_gpu_create_rank"
+        else:
+            rc = L.lib().dtn_gpu_create(C.byref(h), device)
+            what = "dtn_gpu_create"
         if rc != 0:
-            raise RuntimeError(f"dtn_gpu_create failed ({rc}): {L.lib().dtn_gpu_last_error(None).decode()}")
+            raise RuntimeError(f"{what} failed ({rc}): {L.lib().dtn_gpu_last_error(None).decode()}")
         self.h = h
         self.device = device
+        self.world, self.rank = world, rank
 
     def close(self):
         if getattr(self, "h", None):
@@ -328,6 +340,27 @@ class Context:
         if rc == L.DTN_EINVAL:
             raise ValueError(msg)
         raise RuntimeError(f"dtn_gpu error {rc}: {msg}")
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    rc = L.lib().dtn_gpu_nccl_unique_id(buf)
+    if rc != 0:
+        raise RuntimeError(f"dtn_gpu_nccl_unique_id failed ({rc}): {L.lib().dtn_gpu_last_error(None).decode()}")
+    return bytes(buf)
+
+
+def collective_context(device: int) -> Context:
+    """The context of this rank of an initialised torch.distributed job: rank 0 draws the
+    NCCL unique id, torch.distributed hands it to every rank (plumbing only; the build's
+    collectives run in the engine's own communicator)."""
+    import torch.distributed as tdist
+    world, rank = tdist.get_world_size(), tdist.get_rank()
+    if world == 1:
+        return Context(device)
+    box = [nccl_unique_id() if rank == 0 else None]
+    tdist.broadcast_object_list(box, src=0)
+    return Context(device, world, rank, box[0])
 
 
 _contexts: dict[int, Context] = {}
@@ -648,20 +681,22 @@ class CompressedSolutionOperator:
 
 def build_root_accel(op: DiscreteOperator, tree: BoxTree, opt: AccelOptions | None = None, keep_dense: bool = False,
                      ctx: Context | None = None, stencil_device_ptr: int | None = None, nshards: int = 1,
-                     shard_S=None, loads=None):
+                     shard_S=None, loads=None, collective: int = 0):
     """build_root_accel (accel_nd.hpp:93-95, accel_nd.cpp:707-859) on the B200
-    (dtn_gpu_build_accel): root S from the exact dense merges, S_hbs =
-    compress(S, eps, hbs_leaf), G_hbs = invert_hbs(S_hbs). A root boundary
-    below opt.crossover stays dense (accel_nd.cpp:796-818): the result is then
-    the dense SolutionOperator (with G), engine Engine.accel. With nshards > 1
-    and shard_S: the top of a subtree-sharded build (shard.py), compressed."""
+    (dtn_gpu_build_accel): leaf elimination, dense merges below the crossover,
+    structured merges above it (opt.structured), S_hbs = compress(root S, eps,
+    hbs_leaf), G_hbs = invert_hbs(S_hbs). A root below the crossover stays dense
+    (accel_nd.cpp:796-818): the result is then the dense SolutionOperator (with G),
+    engine Engine.accel. With nshards > 1 and shard_S: the top of a subtree-sharded
+    build (shard.py), compressed. collective = -2: the collective multi-GPU build
+    over ctx's NCCL world (nshards = world); -3: the same split on one device."""
     from . import hbs as _hbs
     opt = opt or AccelOptions()
     ctx = ctx or default_context()
     prob, keep = _make_problem(op, tree, stencil_device_ptr, shard_S)
     n = tree.n
     opts = L.dtn_opts(1 if opt.structured else 0, tree.n_leaf, tree.leaf_side, 0, 0, 0, float(opt.epsilon),
-                      int(opt.crossover), nshards, -1)
+                      int(opt.crossover), nshards, collective if collective else -1)
     opts.rank_base, opts.rank_step = int(opt.rank_base), int(opt.rank_step)
     load_arr = None
     if loads is not None and len(loads):

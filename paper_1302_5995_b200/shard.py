@@ -1,14 +1,18 @@
-"""Multi-GPU build by subtree sharding: one process per GPU,
-torch.distributed for the plumbing. Rank r builds the Schur complement of
-shard r (the root's W|E halves for 2 GPUs, its quadrants for 4, the quadrant
-halves for 8) with no communication; the shard S blocks are then sent to rank
-0, which runs the top merges of the tree (the only exchange step of the
-build) and the root inverse. The reference has no distributed path; its own
-top merges are merge_four at the top levels (dense_nd.cpp:188-216).
+"""Multi-GPU build by subtree sharding: one process per GPU.
 
-The driver is written against a small engine interface (`shard_nb`,
-`build_shard`, `build_top`) so the same protocol runs on B200s (GpuShardEngine,
-NCCL over NVLink) and is exercised on CPU with gloo in the tests.
+build_collective -- the production path: the whole sharded build runs in the
+engine (C++ host side, its own NCCL communicator): rank r builds the Schur
+complement of shard r (the root's W|E halves for 2 GPUs, its quadrants for 4,
+the quadrant halves for 8) with no communication, the shard S blocks are
+all-gathered, and the merges above the shards are column-sharded over the
+ranks (interface LU redundant, the boundary columns' substitutions and Schur
+GEMM split, all-gathered per wave), as is the root inverse.
+
+build_distributed -- the same subtree split with the top of the tree on rank 0,
+driven from Python through a small engine interface (`shard_nb`,
+`build_shard`, `build_top`), so the protocol also runs on CPU with gloo in the
+tests. The reference has no distributed path; its own top merges are
+merge_four at the top levels (dense_nd.cpp:188-216).
 """
 from __future__ import annotations
 
@@ -57,6 +61,24 @@ class GpuShardEngine:
         return dtn.build_root_gpu(self.op, self.tree, want_G=True, ctx=self.ctx,
                                   stencil_device_ptr=self.stencil_device_ptr, nshards=nshards, shard=-1,
                                   shard_S=shard_S)
+
+
+def build_collective(op, tree, ctx: dtn.Context, stencil_device_ptr: int | None = None,
+                     accel: dtn.AccelOptions | None = None, want_G: bool = True):
+    """The collective build over ctx's NCCL world (one process per GPU, every rank calls
+    this): shard `rank` built locally, the shard S blocks all-gathered in the engine's
+    communicator, the top merges column-sharded with their chunks all-gathered after
+    each wave, the root inverse column-sharded likewise (dtn_opts.shard = -2, C++ host
+    side). Every rank returns the root operator."""
+    if ctx.world == 1:
+        if accel is not None:
+            return dtn.build_root_accel(op, tree, accel, ctx=ctx, stencil_device_ptr=stencil_device_ptr)
+        return dtn.build_root_gpu(op, tree, want_G=want_G, ctx=ctx, stencil_device_ptr=stencil_device_ptr)
+    if accel is not None:
+        return dtn.build_root_accel(op, tree, accel, ctx=ctx, stencil_device_ptr=stencil_device_ptr,
+                                    nshards=ctx.world, collective=-2)
+    return dtn.build_root_gpu(op, tree, want_G=want_G, ctx=ctx, stencil_device_ptr=stencil_device_ptr,
+                              nshards=ctx.world, shard=-2)
 
 
 def build_distributed(engine, rank: int, world: int):

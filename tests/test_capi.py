@@ -86,3 +86,23 @@ def test_library_has_no_unresolved_engine_symbols():
     out = subprocess.run(["nm", "-D", "--undefined-only", "-C", _lib.LIB_PATH], capture_output=True, text=True).stdout
     bad = [ln for ln in out.splitlines() if "dtnb::" in ln]
     assert not bad, bad
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("n,leaf", [(514, 16), (1026, 32)])
+def test_collective_load_balance(world, n, leaf):
+    """Work per rank of the collective build (dtn_gpu_collective_flops, host only):
+    every rank runs its own shard, the redundant interface LUs of the top merges and
+    of the root, and its chunk of the column work, so no rank carries more than
+    1/N + 10 % of the work all ranks do together (round 1 put the whole top of the
+    tree on rank 0)."""
+    import ctypes as C
+    import numpy as np
+    per = np.zeros(world)
+    single = C.c_double()
+    rc = L.lib().dtn_gpu_collective_flops(n, 0, leaf, world, 1, per.ctypes.data, C.byref(single))
+    assert rc == 0
+    share = per.max() / per.sum()
+    assert share <= 1.0 / world + 0.10, (per, share)
+    # the redundancy (per-rank interface and root LUs) costs less than the split saves
+    assert per.max() < single.value
