@@ -68,7 +68,7 @@ cudaError_t launch_sgather_red(const KernelArgs&, const int*, int, int, cudaStre
 cudaError_t launch_kk_gather(const KernelArgs&, const int*, int, int, cudaStream_t);
 cudaError_t launch_factor_gather(const KernelArgs&, const int*, int, long long, cudaStream_t);
 cudaError_t launch_omega(const KernelArgs&, const int*, int, long long, cudaStream_t);
-cudaError_t launch_hqr(const QrDesc*, int, int, int, const double*, cudaStream_t);
+cudaError_t launch_hqr(const QrDesc*, int, int, int, const double*, cudaStream_t, bool = false);
 cudaError_t launch_gemm_desc2(const GemmDesc2*, int, int, bool, cudaStream_t);
 int gemm_tiles(int, int);
 extern std::atomic<unsigned long long> g_hbs_launches;

@@ -122,6 +122,9 @@ cudaError_t launch_gemm_desc_tc(const GemmDesc* d_descs, int count, int max_tile
                                 cudaStream_t st);
 cudaError_t launch_gemm_desc2(const GemmDesc2* d_descs, int count, int max_tiles, bool tc, cudaStream_t st);
 int gemm_tiles(int m, int n);
+cudaError_t launch_hqr(const QrDesc* d_descs, int count, int max_m, int max_nc, const double* d_eps, cudaStream_t st,
+                       bool pivoted);
+cudaError_t launch_fill_uniform(double* X, int ldx, int rows, int cols, unsigned long long seed, cudaStream_t st);
 cudaError_t launch_copy2d_batched(const void* d_descs, int count, cudaStream_t st);
 
 // kernel launches issued by the HBS code (compress, invert, apply), process-wide
@@ -348,6 +351,13 @@ uint64_t HbsDev::payload_bytes() const {
 }
 
 // ---------------------------------------------------------------------------
+// DTN_HBS_JACOBI=1: the round-1 bases (Gram + two-pass relative Jacobi eigensolves)
+// instead of the randomized rank-revealing QR
+bool use_jacobi_bases() {
+  static const bool v = std::getenv("DTN_HBS_JACOBI") != nullptr;
+  return v;
+}
+
 std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, double eps, int64_t leaf_cap,
                                      cudaStream_t st) {
   if (M < 1 || ldh < M) throw std::invalid_argument("compress: matrix/tree size mismatch");
@@ -509,6 +519,55 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
     int* rk = ordr + 2 * size_t(na) * smax;
 
     tr.mark("transpose");
+    std::vector<int> kf(na);
+    if (!use_jacobi_bases()) {
+      // Bases by randomized rank-revealing QR (the interpolative-decomposition route;
+      // the reference takes the truncated SVD of every block row, hbs.cpp:33-57):
+      // 3. sketches Y = A Omega (s x l, l = min(nX, s + 16)) of the node's block row
+      //    (rows side: X(f,:), the diagonal block zeroed) and block column (XT(f,:));
+      // 4. Householder QR with column pivoting of Y: Q's leading columns span A's
+      //    column space and |R_ii| reveals its eps-rank (#{|R_ii| > eps |R_00|}, the
+      //    same relative cut as svd_rank's sigma_i > eps sigma_0).
+      int lmax = 0;
+      size_t ysum = 0;
+      std::vector<size_t> yoff(na);
+      for (int a = 0; a < na; ++a) {
+        const int s = ssize[slots[act[a]]];
+        const int l = int(std::min<int64_t>(nX, s + 16));
+        lmax = std::max(lmax, l);
+        yoff[a] = ysum;
+        ysum += 2 * size_t(align2(s)) * size_t(l);
+      }
+      double* Om = static_cast<double*>(scr.get(8, (size_t(ldX) * lmax + 2) * 8));
+      double* Yb = static_cast<double*>(scr.get(9, (ysum + 2) * 8));
+      double* qst = static_cast<double*>(scr.get(10, (4 * size_t(na) + 2) * 8));
+      double* d_eps = qst + 4 * size_t(na);
+      HLK(launch_fill_uniform(Om, int(ldX), int(nX), lmax, 0x5eed + r, st));
+      HCK(cudaMemcpyAsync(d_eps, &eps, sizeof(double), cudaMemcpyHostToDevice, st));
+      std::vector<GemmDesc> g;
+      std::vector<QrDesc> q;
+      for (int a = 0; a < na; ++a) {
+        const int i = act[a], s = ssize[slots[i]], ld = int(align2(s));
+        const int l = int(std::min<int64_t>(nX, s + 16)), nq = std::min(s, l);
+        double* y0 = Yb + yoff[a];
+        double* y1 = y0 + size_t(ld) * l;
+        g.push_back(GemmDesc{X + off[i], Om, y0, s, l, int(nX), int(ldX), int(ldX), ld});
+        g.push_back(GemmDesc{XT + off[i], Om, y1, s, l, int(nX), int(ldX), int(ldX), ld});
+        q.push_back(QrDesc{y0, UF(0, a), qst + 4 * a, nullptr, ld, ld, s, nq, l - nq, 0, 0, 0});
+        q.push_back(QrDesc{y1, UF(1, a), qst + 4 * a + 2, nullptr, ld, ld, s, nq, l - nq, 0, 0, 0});
+      }
+      gemm_batch(dbuf, g, 1.0, 0.0, false, st);
+      QrDesc* dq = upload(dbuf, q, st);
+      HLK(launch_hqr(dq, int(q.size()), smax, lmax, d_eps, st, true));
+      std::vector<double> hq(4 * size_t(na));
+      HCK(cudaMemcpyAsync(hq.data(), qst, hq.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+      // basis columns in QR order: ordr = identity
+      std::vector<int> iota(2 * size_t(na) * smax);
+      for (size_t e = 0; e < iota.size(); ++e) iota[e] = int(e % size_t(smax));
+      HCK(cudaMemcpyAsync(ordr, iota.data(), iota.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+      HCK(cudaStreamSynchronize(st));
+      for (int a = 0; a < na; ++a) kf[a] = std::max(int(hq[4 * a]), int(hq[4 * a + 2]));
+    } else {
     // 3. G1: rows X(f,:) X(f,:)^T = X(f,:) XT(:,f); columns XT(f,:) X(:,f)
     {
       std::vector<GemmDesc> g;
@@ -597,7 +656,6 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
     }
     tr.mark("ufull");
     // 10. ranks (hbs.cpp:33-40, 47-57)
-    std::vector<int> kf(na);
     {
       std::vector<SelDesc> sd;
       for (int a = 0; a < na; ++a) {
@@ -613,6 +671,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
       HCK(cudaMemcpyAsync(hr.data(), rk, hr.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
       HCK(cudaStreamSynchronize(st));
       for (int a = 0; a < na; ++a) kf[a] = std::max(hr[2 * a], hr[2 * a + 1]);
+    }
     }
     tr.mark("select");
     // 11. U_f, V_f = leading kf columns (s x k, ld s)

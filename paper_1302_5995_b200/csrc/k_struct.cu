@@ -161,6 +161,23 @@ __device__ __forceinline__ double hash_uniform(unsigned long long x) {
   return double(x >> 11) * 0x1.0p-52 - 1.0;
 }
 
+// X(r, c) = uniform[-1, 1) from the hash of (seed, r, c), r < rows, c < cols (ld ldx)
+__global__ void __launch_bounds__(256) fill_uniform_kernel(double* X, int ldx, int rows, int cols,
+                                                           unsigned long long seed) {
+  const long long tot = (long long)rows * cols;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const int r = int(e % rows), c = int(e / rows);
+    X[r + (long long)c * ldx] = hash_uniform((seed << 40) ^ ((unsigned long long)r * 0x100000001B3ull + c));
+  }
+}
+
+cudaError_t launch_fill_uniform(double* X, int ldx, int rows, int cols, unsigned long long seed, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  const long long tot = (long long)rows * cols;
+  fill_uniform_kernel<<<unsigned(std::min<long long>((tot + 255) / 256, 1184)), 256, 0, st>>>(X, ldx, rows, cols, seed);
+  return cudaGetLastError();
+}
+
 __global__ void __launch_bounds__(256) omega_kernel(KernelArgs args, const int* __restrict__ list) {
   const NodeDev nd = args.nodes[list[blockIdx.y]];
   const long long tot = (long long)nd.nb * (nd.ell + kProbes);
@@ -193,13 +210,19 @@ constexpr int QR_THREADS = 256, QR_WARPS = QR_THREADS / 32, QR_MAXC = 16, QR_MAX
 constexpr int QR_GL = 8, QR_NG = QR_THREADS / QR_GL;  // lanes per column group, column groups
 
 struct QrShared {
+  double nrm[QR_MAXN];         // PIV: trailing column norms^2 (cluster sums)
+  int jmax;                    // PIV: pivot column of this step
   double a[2][2];              // [parity] partial sum of squares, alpha (the row owner's)
   double w[2][QR_MAXN + 8];    // [parity] partial dot products
   double tau[QR_MAXN], rdiag[QR_MAXN];
   double red[QR_WARPS];
 };
 
-template <bool CL, bool SM>
+// PIV: Householder QR with column pivoting (largest remaining column norm first,
+// lowest index on ties; LAPACK dgeqp3's rule with norms recomputed each step) --
+// the rank-revealing QR of the compressed engine's basis selection (hbs.cu); stat[0]
+// then counts |R_ii| > eps |R_00| (QrDesc::S == nullptr).
+template <bool CL, bool SM, bool PIV = false>
 __global__ void __launch_bounds__(QR_THREADS) hqr_kernel(const QrDesc* __restrict__ descs, const double* eps_ptr,
                                                          int C) {
   extern __shared__ __align__(16) double qdyn[];
@@ -279,6 +302,64 @@ __global__ void __launch_bounds__(QR_THREADS) hqr_kernel(const QrDesc* __restric
     double* yc = Y + c * ld;
     const bool own_row = c >= r0 && c < r1;
     const int lo = max(c + 1 - r0, 0);
+    if constexpr (PIV) {  // bring the largest remaining column (rows >= c) to position c
+      const int lv = max(c - r0, 0);
+      for (int jb = c; jb < nc; jb += QR_NG) {
+        const int j = jb + grp;
+        double s0 = 0.0;
+        if (j < nc) {
+          const double* yj = Y + j * ld;
+          for (int i = lv + gl; i < nr; i += QR_GL) s0 = fma(yj[i], yj[i], s0);
+        }
+#pragma unroll
+        for (int o = QR_GL / 2; o > 0; o >>= 1) s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        if (j < nc && gl == 0) sh.nrm[j] = s0;
+      }
+      __syncthreads();
+      if constexpr (CL) {
+        csync();
+        double t[QR_MAXN / QR_THREADS > 0 ? QR_MAXN / QR_THREADS : 1];
+        for (int j = c + tid, q = 0; j < nc; j += QR_THREADS, ++q) {
+          t[q] = 0.0;
+          for (int r = 0; r < C; ++r) t[q] += remote(&sh.nrm[j], r);
+        }
+        csync();
+        for (int j = c + tid, q = 0; j < nc; j += QR_THREADS, ++q) sh.nrm[j] = t[q];
+        __syncthreads();
+      }
+      if (warp == 0) {
+        double best = -1.0;
+        int bj = c;
+        for (int j = c + lane; j < nc; j += 32) {
+          const double v = sh.nrm[j];
+          if (v > best) {
+            best = v;
+            bj = j;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+          if (ob > best || (ob == best && oj < bj)) {
+            best = ob;
+            bj = oj;
+          }
+        }
+        if (lane == 0) sh.jmax = bj;
+      }
+      __syncthreads();
+      const int jm = sh.jmax;
+      if (jm != c) {
+        double* yj = Y + jm * ld;
+        for (int i = tid; i < nr; i += QR_THREADS) {
+          const double t = yc[i];
+          yc[i] = yj[i];
+          yj[i] = t;
+        }
+      }
+      __syncthreads();
+    }
     // reflector of column c (warp 0)
     if (warp == 0) {
       double ss = 0.0;
@@ -365,7 +446,8 @@ __global__ void __launch_bounds__(QR_THREADS) hqr_kernel(const QrDesc* __restric
     for (int i = tid; i < nr; i += QR_THREADS) d.Q[r0 + i + (long long)jj * d.ldq] = Y[i + jj * ld];
   if (rank == 0 && d.stat) {
     double dmax = 0.0;
-    for (int i = tid; i < d.nbs; i += QR_THREADS) dmax = fmax(dmax, fabs(d.S[i + (long long)i * d.lds]));
+    if (d.S)
+      for (int i = tid; i < d.nbs; i += QR_THREADS) dmax = fmax(dmax, fabs(d.S[i + (long long)i * d.lds]));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
     if (lane == 0) sh.red[warp] = dmax;
@@ -373,7 +455,9 @@ __global__ void __launch_bounds__(QR_THREADS) hqr_kernel(const QrDesc* __restric
     if (tid == 0) {
       double t = 0.0;
       for (int w = 0; w < QR_WARPS; ++w) t = fmax(t, sh.red[w]);
-      const double eps = *eps_ptr, scale = t * sqrt(double(d.k) / 3.0);
+      const double eps = *eps_ptr;
+      // operator scale (sketch factors) or, without S, the leading |R_00| (rank-revealing QR)
+      const double scale = d.S ? t * sqrt(double(d.k) / 3.0) : (n > 0 ? fabs(sh.rdiag[0]) : 0.0);
       int rk = 0;
       for (int i = 0; i < n; ++i)
         if (fabs(sh.rdiag[i]) > eps * scale) ++rk;
@@ -428,18 +512,21 @@ static int qr_cluster(int m, int nc, bool* sm) {
 }
 
 cudaError_t struct_init() {
-  for (auto f : {hqr_kernel<true, true>, hqr_kernel<false, true>, hqr_kernel<true, false>}) {
+  for (auto f : {hqr_kernel<true, true>, hqr_kernel<false, true>, hqr_kernel<true, false>,
+                 hqr_kernel<true, true, true>, hqr_kernel<false, true, true>, hqr_kernel<true, false, true>}) {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
   }
-  for (auto f : {hqr_kernel<true, true>, hqr_kernel<true, false>}) {
+  for (auto f : {hqr_kernel<true, true>, hqr_kernel<true, false>, hqr_kernel<true, true, true>,
+                 hqr_kernel<true, false, true>}) {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
 
-cudaError_t launch_hqr(const QrDesc* d_descs, int count, int max_m, int max_nc, const double* d_eps, cudaStream_t st) {
+cudaError_t launch_hqr(const QrDesc* d_descs, int count, int max_m, int max_nc, const double* d_eps, cudaStream_t st,
+                       bool pivoted) {
   if (count <= 0) return cudaSuccess;
   if (max_nc > QR_MAXN) return cudaErrorInvalidValue;
   bool sm = true;
@@ -456,6 +543,11 @@ cudaError_t launch_hqr(const QrDesc* d_descs, int count, int max_m, int max_nc, 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = C > 1 ? 1 : 0;
+  if (pivoted) {
+    if (!sm) return cudaLaunchKernelEx(&cfg, hqr_kernel<true, false, true>, d_descs, d_eps, C);
+    if (C > 1) return cudaLaunchKernelEx(&cfg, hqr_kernel<true, true, true>, d_descs, d_eps, C);
+    return cudaLaunchKernelEx(&cfg, hqr_kernel<false, true, true>, d_descs, d_eps, C);
+  }
   if (!sm) return cudaLaunchKernelEx(&cfg, hqr_kernel<true, false>, d_descs, d_eps, C);
   if (C > 1) return cudaLaunchKernelEx(&cfg, hqr_kernel<true, true>, d_descs, d_eps, C);
   return cudaLaunchKernelEx(&cfg, hqr_kernel<false, true>, d_descs, d_eps, C);
