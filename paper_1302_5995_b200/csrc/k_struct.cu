@@ -211,6 +211,7 @@ constexpr int QR_GL = 8, QR_NG = QR_THREADS / QR_GL;  // lanes per column group,
 
 struct QrShared {
   double nrm[QR_MAXN];         // PIV: trailing column norms^2 (cluster sums)
+  double wsum[QR_MAXN];        // cluster-summed dot products of the current step
   int jmax;                    // PIV: pivot column of this step
   double a[2][2];              // [parity] partial sum of squares, alpha (the row owner's)
   double w[2][QR_MAXN + 8];    // [parity] partial dot products
@@ -254,10 +255,10 @@ __global__ void __launch_bounds__(QR_THREADS) hqr_kernel(const QrDesc* __restric
     const double* yc = Y + c * ld;
     const bool own_row = c >= r0 && c < r1;
     const int lv = max(c - r0, 0);
-    for (int jb = j0; jb < j1; jb += QR_NG) {
-      const int j = jb + grp;
+    // the group's dot product v . y_j (every lane of the warp must call it: it shuffles)
+    auto partial_dot = [&](int j, bool valid) {
       double dot = 0.0;
-      if (j < j1) {
+      if (valid) {
         const double* yj = Y + j * ld;
         double s0 = 0.0, s1 = 0.0;
         int i = lv + gl;
@@ -274,27 +275,47 @@ __global__ void __launch_bounds__(QR_THREADS) hqr_kernel(const QrDesc* __restric
       }
 #pragma unroll
       for (int o = QR_GL / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-      if constexpr (CL) {
+      return dot;
+    };
+    auto update = [&](int j, double dot) {
+      double* yj = Y + j * ld;
+      const double f = tc * dot;
+      int i = lv + gl;
+      if (own_row && gl == 0) {
+        yj[lv] -= f;
+        i += QR_GL;
+      }
+      for (; i < nr; i += QR_GL) yj[i] = fma(-f, yc[i], yj[i]);
+    };
+    if constexpr (CL) {
+      // every trailing column's partial dot (slots indexed by column: one barrier), then
+      // the cluster sums and the updates
+      for (int jb = j0; jb < j1; jb += QR_NG) {
+        const int j = jb + grp;
+        const double dot = partial_dot(j, j < j1);
         if (j < j1 && gl == 0) sh.w[par][j] = dot;
-        csync();
-        if (j < j1) {
-          dot = 0.0;
-          if (gl == 0)
-            for (int q = 0; q < C; ++q) dot += remote(&sh.w[par][j], q);
-        }
-        dot = __shfl_sync(0xffffffffu, dot, (lane / QR_GL) * QR_GL);
       }
-      if (j < j1 && tc != 0.0) {
-        double* yj = Y + j * ld;
-        const double f = tc * dot;
-        int i = lv + gl;
-        if (own_row && gl == 0) {
-          yj[lv] -= f;
-          i += QR_GL;
-        }
-        for (; i < nr; i += QR_GL) yj[i] = fma(-f, yc[i], yj[i]);
+      csync();
+      // one thread per column sums the C partials (independent DSMEM loads, in flight
+      // together), rank order
+      for (int j = j0 + tid; j < j1; j += QR_THREADS) {
+        double t = 0.0;
+        for (int q = 0; q < C; ++q) t += remote(&sh.w[par][j], q);
+        sh.wsum[j] = t;
       }
-      if constexpr (CL) csync();  // (the slots of this column block are reused by the next)
+      __syncthreads();
+      if (tc != 0.0)
+        for (int jb = j0; jb < j1; jb += QR_NG) {
+          const int j = jb + grp;
+          if (j < j1) update(j, sh.wsum[j]);
+        }
+    } else {
+      if (tc != 0.0)
+        for (int jb = j0; jb < j1; jb += QR_NG) {
+          const int j = jb + grp;
+          const double dot = partial_dot(j, j < j1);
+          if (j < j1) update(j, dot);
+        }
     }
   };
   for (int c = 0; c < n; ++c) {
@@ -318,13 +339,13 @@ __global__ void __launch_bounds__(QR_THREADS) hqr_kernel(const QrDesc* __restric
       __syncthreads();
       if constexpr (CL) {
         csync();
-        double t[QR_MAXN / QR_THREADS > 0 ? QR_MAXN / QR_THREADS : 1];
-        for (int j = c + tid, q = 0; j < nc; j += QR_THREADS, ++q) {
-          t[q] = 0.0;
-          for (int r = 0; r < C; ++r) t[q] += remote(&sh.nrm[j], r);
+        for (int j = c + tid; j < nc; j += QR_THREADS) {
+          double t = 0.0;
+          for (int r = 0; r < C; ++r) t += remote(&sh.nrm[j], r);
+          sh.wsum[j] = t;
         }
         csync();
-        for (int j = c + tid, q = 0; j < nc; j += QR_THREADS, ++q) sh.nrm[j] = t[q];
+        for (int j = c + tid; j < nc; j += QR_THREADS) sh.nrm[j] = sh.wsum[j];
         __syncthreads();
       }
       if (warp == 0) {
@@ -373,12 +394,11 @@ __global__ void __launch_bounds__(QR_THREADS) hqr_kernel(const QrDesc* __restric
     }
     csync();
     if (warp == 0) {
-      double sst = 0.0, alpha = 0.0;
-      if (lane == 0) {
-        for (int q = 0; q < C; ++q) sst += remote(&sh.a[par][0], q);
-        alpha = remote(&sh.a[par][1], c / R);
-      }
-      sst = __shfl_sync(0xffffffffu, sst, 0);
+      // lanes q < C load rank q's partial (in flight together), summed in rank order
+      double part = lane < C ? remote(&sh.a[par][0], lane) : 0.0;
+      double sst = 0.0;
+      for (int q = 0; q < C; ++q) sst += __shfl_sync(0xffffffffu, part, q);
+      double alpha = lane == 0 ? remote(&sh.a[par][1], c / R) : 0.0;
       alpha = __shfl_sync(0xffffffffu, alpha, 0);
       double beta, tc, scal;
       if (sst == 0.0) {
