@@ -2610,11 +2610,10 @@ int dtn_gpu_hbs_serialize(const dtn_hbs* h, uint8_t* buf, uint64_t cap, uint64_t
   dtn_ctx* ctx = h->ctx;
   return guarded(ctx, [&] {
     CK(cudaSetDevice(ctx->device));
-    const std::vector<uint8_t> bytes = hbs_serialize(*h->h, ctx->stream);
-    *size = bytes.size();
+    *size = hbs_serialized_size(*h->h);  // a size query copies nothing
     if (!buf) return;
-    if (cap < bytes.size()) throw std::invalid_argument("hbs_serialize: buffer too small");
-    std::memcpy(buf, bytes.data(), bytes.size());
+    if (cap < *size) throw std::invalid_argument("hbs_serialize: buffer too small");
+    hbs_serialize_into(*h->h, buf, ctx->stream);
   });
 }
 
@@ -2707,21 +2706,23 @@ int dtn_gpu_build_accel(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* o
     rc = guarded(ctx, [&] {
       const int64_t m = op->nb;
       std::vector<double> ones(size_t(m), 1.0);
-      std::vector<double> y(static_cast<size_t>(m), 0.0);
-      double* d = static_cast<double*>(pool_alloc(size_t(m) * 16));
+      std::vector<double> y(2 * static_cast<size_t>(m), 0.0);
+      double* d = static_cast<double*>(pool_alloc(size_t(m) * 24));
       struct F {
         double* p;
         ~F() { pool_free(p); }
       } f{d};
       cudaStream_t st = ctx->stream;
       CK(cudaMemcpyAsync(d, ones.data(), size_t(m) * 8, cudaMemcpyHostToDevice, st));
+      // both products enqueued back to back, one copy back, one synchronisation
+      hbs_apply(*Sh->h, d, m, 1, d + m, m, st);
+      hbs_apply(*Gh->h, d, m, 1, d + 2 * m, m, st);
+      CK(cudaMemcpyAsync(y.data(), d + m, size_t(m) * 16, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
       double nrm[2];
       for (int w = 0; w < 2; ++w) {
-        hbs_apply(*(w == 0 ? Sh : Gh)->h, d, m, 1, d + m, m, st);
-        CK(cudaMemcpyAsync(y.data(), d + m, size_t(m) * 8, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
         double a = 0.0;
-        for (double v : y) a += std::fabs(v);
+        for (int64_t i = 0; i < m; ++i) a += std::fabs(y[size_t(w * m + i)]);
         nrm[w] = a / double(m);
       }
       *cond = nrm[0] * nrm[1] * double(m);

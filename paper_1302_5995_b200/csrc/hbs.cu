@@ -1049,10 +1049,6 @@ namespace {
 
 const char kMagic[8] = {'D', 'T', 'N', 'H', 'B', 'S', '0', '1'};
 
-void put_i64(std::vector<uint8_t>& out, int64_t v) {
-  for (int i = 0; i < 8; ++i) out.push_back(uint8_t(uint64_t(v) >> (8 * i)));
-}
-
 
 struct Reader {
   const uint8_t* p;
@@ -1068,26 +1064,15 @@ struct Reader {
 
 }  // namespace
 
-std::vector<uint8_t> hbs_serialize(const HbsDev& H, cudaStream_t st) {
-  std::vector<uint8_t> out(kMagic, kMagic + 8);
-  put_i64(out, H.M);
-  put_i64(out, int64_t(H.nodes.size()));
-  put_i64(out, H.depth);
-  for (const auto& n : H.nodes) {
-    put_i64(out, n.begin);
-    put_i64(out, n.end);
-    put_i64(out, n.left);
-    put_i64(out, n.right);
-    put_i64(out, n.parent);
-    put_i64(out, n.level);
-  }
-  // every factor straight into one page-locked staging buffer (all copies in flight
-  // at once, one synchronisation), then the DTNHBS01 records around them
-  struct Mat {
-    const double* d;
-    int64_t ld, r, c;
-  };
-  std::vector<Mat> mats;
+namespace {
+struct SerMat {
+  const double* d;
+  int64_t ld, r, c;
+};
+// the DTNHBS01 matrix records in file order (hbs.cpp:446-470): per node, D (leaves),
+// U and V (non-root), B (parents)
+std::vector<SerMat> serial_mats(const HbsDev& H) {
+  std::vector<SerMat> mats;
   for (int t = 0; t < int(H.nodes.size()); ++t) {
     const bool leaf = H.is_leaf(t);
     if (leaf) mats.push_back({H.D[t], H.ld(t), H.node_size(t), H.node_size(t)});
@@ -1097,41 +1082,66 @@ std::vector<uint8_t> hbs_serialize(const HbsDev& H, cudaStream_t st) {
     }
     if (!leaf) mats.push_back({H.B[t], H.ld(t), H.rows[t], H.rows[t]});
   }
-  size_t total = 0;
-  for (const Mat& x : mats) total += size_t(x.r) * size_t(x.c) * 8;
-  thread_local struct Pinned {
-    void* p = nullptr;
-    size_t cap = 0;
-    ~Pinned() {
-      if (p) cudaFreeHost(p);
-    }
-  } stage;
-  if (stage.cap < total) {
-    if (stage.p) cudaFreeHost(stage.p);
-    stage.p = nullptr;
-    stage.cap = 0;
-    HCK(cudaMallocHost(&stage.p, total));
-    stage.cap = total;
+  return mats;
+}
+size_t serial_prefix(const HbsDev& H) { return 8 + 3 * 8 + H.nodes.size() * 6 * 8; }
+}  // namespace
+
+uint64_t hbs_serialized_size(const HbsDev& H) {
+  uint64_t n = serial_prefix(H);
+  for (const SerMat& x : serial_mats(H)) n += 16 + uint64_t(x.r) * uint64_t(x.c) * 8;
+  return n;
+}
+
+// Every factor is packed on the device into the byte image of the record stream
+// (one batched copy kernel), the image comes back in ONE device-to-host copy
+// straight into the caller's buffer, and the host writes only the headers.
+void hbs_serialize_into(const HbsDev& H, uint8_t* buf, cudaStream_t st) {
+  const std::vector<SerMat> mats = serial_mats(H);
+  const size_t prefix = serial_prefix(H);
+  size_t body = 0;  // bytes after the prefix: per matrix 16 header bytes + payload
+  for (const SerMat& x : mats) body += 16 + size_t(x.r) * size_t(x.c) * 8;
+  DevBuf img_buf, desc_buf;  // the per-device caching pool
+  double* img = static_cast<double*>(img_buf.get(std::max<size_t>(body, 8)));
+  std::vector<CopyDesc> cp;
+  size_t at = 0;  // in doubles, relative to the image
+  for (const SerMat& x : mats) {
+    at += 2;  // the (rows, cols) header
+    if (x.r > 0 && x.c > 0) cp.push_back(CopyDesc{x.d, img + at, int(x.ld), int(x.r), int(x.r), int(x.c)});
+    at += size_t(x.r) * size_t(x.c);
   }
-  uint8_t* hs = static_cast<uint8_t*>(stage.p);
-  size_t at = 0;
-  for (const Mat& x : mats) {
-    const size_t bytes = size_t(x.r) * size_t(x.c) * 8;
-    if (bytes)
-      HCK(cudaMemcpy2DAsync(hs + at, size_t(x.r) * 8, x.d, size_t(x.ld) * 8, size_t(x.r) * 8, size_t(x.c),
-                            cudaMemcpyDeviceToHost, st));
-    at += bytes;
+  if (!cp.empty()) {
+    CopyDesc* dd = upload(desc_buf, cp, st);
+    HLK(launch_copy2d_batched(dd, int(cp.size()), st));
+  }
+  if (body) HCK(cudaMemcpyAsync(buf + prefix, img, body, cudaMemcpyDeviceToHost, st));
+  // the prefix and the record headers while the copy runs
+  auto put = [](uint8_t* p, int64_t v) {
+    for (int i = 0; i < 8; ++i) p[i] = uint8_t(uint64_t(v) >> (8 * i));
+  };
+  std::memcpy(buf, kMagic, 8);
+  put(buf + 8, H.M);
+  put(buf + 16, int64_t(H.nodes.size()));
+  put(buf + 24, H.depth);
+  uint8_t* q = buf + 32;
+  for (const auto& n : H.nodes) {
+    for (int64_t v : {n.begin, n.end, int64_t(n.left), int64_t(n.right), int64_t(n.parent), int64_t(n.level)}) {
+      put(q, v);
+      q += 8;
+    }
   }
   HCK(cudaStreamSynchronize(st));
-  out.reserve(out.size() + total + 16 * mats.size());
-  at = 0;
-  for (const Mat& x : mats) {
-    const size_t bytes = size_t(x.r) * size_t(x.c) * 8;
-    put_i64(out, x.r);
-    put_i64(out, x.c);
-    out.insert(out.end(), hs + at, hs + at + bytes);
-    at += bytes;
+  uint8_t* h = buf + prefix;
+  for (const SerMat& x : mats) {
+    put(h, x.r);
+    put(h + 8, x.c);
+    h += 16 + size_t(x.r) * size_t(x.c) * 8;
   }
+}
+
+std::vector<uint8_t> hbs_serialize(const HbsDev& H, cudaStream_t st) {
+  std::vector<uint8_t> out(hbs_serialized_size(H));
+  hbs_serialize_into(H, out.data(), st);
   return out;
 }
 

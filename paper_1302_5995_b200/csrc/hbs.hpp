@@ -157,6 +157,8 @@ std::unique_ptr<HbsDev> hbs_invert(const HbsDev& H, cudaStream_t st);
 
 // DTNHBS01 serialization (hbs.cpp:422-519), byte-for-byte the reference layout.
 std::vector<uint8_t> hbs_serialize(const HbsDev& H, cudaStream_t st);
+uint64_t hbs_serialized_size(const HbsDev& H);
+void hbs_serialize_into(const HbsDev& H, uint8_t* buf, cudaStream_t st);  // buf: hbs_serialized_size bytes
 std::unique_ptr<HbsDev> hbs_deserialize(const uint8_t* data, size_t size, cudaStream_t st);
 
 }  // namespace dtnb

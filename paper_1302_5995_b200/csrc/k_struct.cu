@@ -22,6 +22,8 @@
 // four descriptor GEMMs, see engine.cu).
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 
@@ -488,6 +490,215 @@ __global__ void __launch_bounds__(QR_THREADS) hqr_kernel(const QrDesc* __restric
   csync();  // no CTA leaves while others may still read its shared memory
 }
 
+// The sketch factors' Householder QR with ONE cluster reduction per column step
+// (hqr_kernel above needs two, plus one per step of the Q formation): step c
+// reduces, for every trailing column j >= c, s_j = sum_{i > c} y_ic y_ij
+// (s_c = |x(c+1:)|^2) together with row c's entries y_cj; every CTA then forms
+// beta, tau and v = [1; y(c+1:, c) / (alpha - beta)] itself from the same sums in
+// rank order (bit-identical reflectors on every CTA) and
+// v^T y_j = y_cj + s_j / (alpha - beta). The reflector column is scaled lazily
+// at the next step (no CTA reads it there). The explicit Q is formed backward
+// (dorg2r) with the same one-reduction step; the C partials of a sum are loaded
+// together (DSMEM loads in flight at once) and added in rank order.
+template <bool CL, bool SM>
+__global__ void __launch_bounds__(QR_THREADS) hqr1_kernel(const QrDesc* __restrict__ descs,
+                                                          const double* eps_ptr, int C) {
+  extern __shared__ __align__(16) double qdyn[];
+  __shared__ double part[2][QR_MAXN + 8];        // [parity] this CTA's partial sums (+ probe norms)
+  __shared__ double rowc[2][QR_MAXN];            // [parity] row c of the trailing columns (row owner)
+  __shared__ double tot[QR_MAXN], rct[QR_MAXN];  // cluster sums / row c, local copies
+  __shared__ double tau_s[QR_MAXN], rdiag[QR_MAXN];
+  __shared__ double red[QR_WARPS];
+  const int rank = CL ? int(cg::this_cluster().block_rank()) : 0;
+  const QrDesc d = descs[blockIdx.x / C];
+  const int m = d.m, n = d.n, nc = d.n + d.p;
+  const int R = (m + C - 1) / C, r0 = rank * R, r1 = min(m, r0 + R), nr = max(r1 - r0, 0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gl = tid & (QR_GL - 1), grp = tid / QR_GL;
+  const long long ld = SM ? (nr | 1) : d.ldy;
+  double* Y = SM ? qdyn : d.Y + r0;  // local rows, column-major
+  if constexpr (SM) {
+    for (int j = 0; j < nc; ++j)
+      for (int i = tid; i < nr; i += QR_THREADS) Y[i + j * ld] = d.Y[r0 + i + (long long)j * d.ldy];
+    __syncthreads();
+  }
+  auto csync = [] {
+    if constexpr (CL) cg::this_cluster().sync();
+    else __syncthreads();
+  };
+  auto csum = [&](const double* slot) -> double {
+    if constexpr (CL) {
+      double v[QR_MAXC];
+#pragma unroll
+      for (int q = 0; q < QR_MAXC; ++q)
+        v[q] = q < C ? *cg::this_cluster().map_shared_rank(const_cast<double*>(slot), q) : 0.0;
+      double t = v[0];
+#pragma unroll
+      for (int q = 1; q < QR_MAXC; ++q)
+        if (q < C) t += v[q];
+      return t;
+    } else {
+      return *slot;
+    }
+  };
+  // partial dot of local rows [lo, nr) of columns a and b by the 8 lanes of a group
+  auto gdot = [&](const double* ya, const double* yb, int lo, bool valid) {
+    double s0 = 0.0, s1 = 0.0;
+    if (valid) {
+      int i = lo + gl;
+      for (; i + QR_GL < nr; i += 2 * QR_GL) {
+        s0 = fma(ya[i], yb[i], s0);
+        s1 = fma(ya[i + QR_GL], yb[i + QR_GL], s1);
+      }
+      if (i < nr) s0 = fma(ya[i], yb[i], s0);
+    }
+    double dot = s0 + s1;
+#pragma unroll
+    for (int o = QR_GL / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    return dot;
+  };
+  double scal_prev = 0.0, beta_prev = 0.0;
+  auto finish_reflector = [&](int c) {  // column c <- [beta; v(c+1:)]
+    const int lo = max(c + 1 - r0, 0);
+    double* y = Y + c * ld;
+    for (int i = lo + tid; i < nr; i += QR_THREADS) y[i] *= scal_prev;
+    if (tid == 0 && c >= r0 && c < r1) y[c - r0] = beta_prev;
+  };
+  for (int c = 0; c < n; ++c) {
+    const int par = c & 1;
+    const int lo = max(c + 1 - r0, 0);
+    const bool own = c >= r0 && c < r1;
+    const double* yc = Y + c * ld;
+    if (c > 0) finish_reflector(c - 1);
+    for (int jb = c; jb < nc; jb += QR_NG) {
+      const int j = jb + grp;
+      const double dot = gdot(yc, Y + min(j, nc - 1) * ld, lo, j < nc);
+      if (j < nc && gl == 0) part[par][j] = dot;
+    }
+    if (own)
+      for (int j = c + tid; j < nc; j += QR_THREADS) rowc[par][j] = Y[(c - r0) + j * ld];
+    csync();
+    for (int j = c + tid; j < nc; j += QR_THREADS) {
+      tot[j] = csum(&part[par][j]);
+      if constexpr (CL) rct[j] = *cg::this_cluster().map_shared_rank(&rowc[par][j], c / R);
+      else rct[j] = rowc[par][j];
+    }
+    __syncthreads();
+    const double sst = tot[c], alpha = rct[c];
+    double beta, tc, scal;
+    if (sst == 0.0) {
+      beta = alpha;
+      tc = 0.0;
+      scal = 0.0;
+    } else {
+      beta = -copysign(sqrt(fma(alpha, alpha, sst)), alpha);
+      tc = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    if (tid == 0) {
+      tau_s[c] = tc;
+      rdiag[c] = beta;
+    }
+    if (tc != 0.0)
+      for (int jb = c + 1; jb < nc; jb += QR_NG) {
+        const int j = jb + grp;
+        if (j < nc) {
+          const double f = tc * fma(scal, tot[j], rct[j]);  // tau v^T y_j
+          const double g = f * scal;
+          double* yj = Y + j * ld;
+          if (own && gl == 0) yj[c - r0] -= f;
+          for (int i = lo + gl; i < nr; i += QR_GL) yj[i] = fma(-g, yc[i], yj[i]);
+        }
+      }
+    scal_prev = scal;
+    beta_prev = beta;
+    __syncthreads();
+  }
+  if (n > 0) finish_reflector(n - 1);
+  __syncthreads();
+  // range-finder check: |(I - Q Q^T) y_probe|^2 = sum of the probe columns' rows >= n
+  double pres = 0.0;
+  {
+    const int lo = max(n - r0, 0);
+    if (warp < d.p) {
+      const double* yq = Y + (n + warp) * ld;
+      double ss = 0.0;
+      for (int i = lo + lane; i < nr; i += 32) ss = fma(yq[i], yq[i], ss);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) part[0][QR_MAXN + warp] = ss;
+    }
+    csync();
+    for (int q = 0; q < d.p; ++q) pres = fmax(pres, sqrt(csum(&part[0][QR_MAXN + q])));
+    csync();  // the probe slots are free again
+  }
+  // Q in place (dorg2r): backward over the reflectors. Before H_c is applied, the
+  // columns j > c are zero in rows <= c, so v^T q_j = sum_{i > c} v_i q_ij.
+  auto finish_col = [&](int c) {
+    double* y = Y + c * ld;
+    const double tc = tau_s[c];
+    for (int i = tid; i < nr; i += QR_THREADS) {
+      const int gi = r0 + i;
+      y[i] = gi < c ? 0.0 : (gi == c ? 1.0 - tc : -tc * y[i]);
+    }
+  };
+  for (int c = n - 1; c >= 0; --c) {
+    const int par = c & 1;
+    const int lo = max(c + 1 - r0, 0);
+    const bool own = c >= r0 && c < r1;
+    const double* yc = Y + c * ld;
+    const double tc = tau_s[c];
+    if (c + 1 < n) {
+      finish_col(c + 1);
+      __syncthreads();
+    }
+    for (int jb = c + 1; jb < n; jb += QR_NG) {
+      const int j = jb + grp;
+      const double dot = gdot(yc, Y + min(j, n - 1) * ld, lo, j < n);
+      if (j < n && gl == 0) part[par][j] = dot;
+    }
+    csync();
+    for (int j = c + 1 + tid; j < n; j += QR_THREADS) tot[j] = csum(&part[par][j]);
+    __syncthreads();
+    if (tc != 0.0)
+      for (int jb = c + 1; jb < n; jb += QR_NG) {
+        const int j = jb + grp;
+        if (j < n) {
+          const double f = tc * tot[j];
+          double* yj = Y + j * ld;
+          if (own && gl == 0) yj[c - r0] = -f;
+          for (int i = lo + gl; i < nr; i += QR_GL) yj[i] = fma(-f, yc[i], yj[i]);
+        }
+      }
+    __syncthreads();
+  }
+  if (n > 0) finish_col(0);
+  __syncthreads();
+  for (int jj = 0; jj < n; ++jj)
+    for (int i = tid; i < nr; i += QR_THREADS) d.Q[r0 + i + (long long)jj * d.ldq] = Y[i + jj * ld];
+  if (rank == 0 && d.stat) {
+    double dmax = 0.0;
+    if (d.S)
+      for (int i = tid; i < d.nbs; i += QR_THREADS) dmax = fmax(dmax, fabs(d.S[i + (long long)i * d.lds]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    if (lane == 0) red[warp] = dmax;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < QR_WARPS; ++w) t = fmax(t, red[w]);
+      const double eps = *eps_ptr;
+      const double scale = d.S ? t * sqrt(double(d.k) / 3.0) : (n > 0 ? fabs(rdiag[0]) : 0.0);
+      int rk = 0;
+      for (int i = 0; i < n; ++i)
+        if (fabs(rdiag[i]) > eps * scale) ++rk;
+      d.stat[0] = double(rk);
+      d.stat[1] = scale > 0.0 ? pres / scale : 0.0;
+    }
+  }
+  if constexpr (CL) cg::this_cluster().sync();  // no CTA leaves while others may still read its shared memory
+}
+
 cudaError_t launch_sgather_red(const KernelArgs& args, const int* d_list, int count, int max_total, cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
   dim3 grid((max_total + SG_COLS - 1) / SG_COLS, count);
@@ -531,7 +742,23 @@ static int qr_cluster(int m, int nc, bool* sm) {
   return QR_MAXC;
 }
 
+// DTN_HQR_FUSED=1: the sketch QR by hqr1_kernel (one reduction per column step; measured
+// no faster than hqr_kernel: both are bound by the shared-memory traffic of the
+// unblocked column updates, not by the cluster barriers)
+static bool hqr_legacy() {
+  static const bool on = std::getenv("DTN_HQR_FUSED") == nullptr;
+  return on;
+}
+
 cudaError_t struct_init() {
+  for (auto f : {hqr1_kernel<true, true>, hqr1_kernel<false, true>, hqr1_kernel<true, false>}) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+  }
+  for (auto f : {hqr1_kernel<true, true>, hqr1_kernel<true, false>}) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
   for (auto f : {hqr_kernel<true, true>, hqr_kernel<false, true>, hqr_kernel<true, false>,
                  hqr_kernel<true, true, true>, hqr_kernel<false, true, true>, hqr_kernel<true, false, true>}) {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -551,6 +778,9 @@ cudaError_t launch_hqr(const QrDesc* d_descs, int count, int max_m, int max_nc, 
   if (max_nc > QR_MAXN) return cudaErrorInvalidValue;
   bool sm = true;
   const int C = qr_cluster(max_m, max_nc, &sm);
+  if (std::getenv("DTN_DEBUG_QR"))
+    std::fprintf(stderr, "hqr: count %d max_m %d max_nc %d cluster %d smem %d pivoted %d\n", count, max_m, max_nc, C,
+                 int(sm), int(pivoted));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(count * C);
   cfg.blockDim = dim3(QR_THREADS);
@@ -568,9 +798,14 @@ cudaError_t launch_hqr(const QrDesc* d_descs, int count, int max_m, int max_nc, 
     if (C > 1) return cudaLaunchKernelEx(&cfg, hqr_kernel<true, true, true>, d_descs, d_eps, C);
     return cudaLaunchKernelEx(&cfg, hqr_kernel<false, true, true>, d_descs, d_eps, C);
   }
-  if (!sm) return cudaLaunchKernelEx(&cfg, hqr_kernel<true, false>, d_descs, d_eps, C);
-  if (C > 1) return cudaLaunchKernelEx(&cfg, hqr_kernel<true, true>, d_descs, d_eps, C);
-  return cudaLaunchKernelEx(&cfg, hqr_kernel<false, true>, d_descs, d_eps, C);
+  if (hqr_legacy()) {
+    if (!sm) return cudaLaunchKernelEx(&cfg, hqr_kernel<true, false>, d_descs, d_eps, C);
+    if (C > 1) return cudaLaunchKernelEx(&cfg, hqr_kernel<true, true>, d_descs, d_eps, C);
+    return cudaLaunchKernelEx(&cfg, hqr_kernel<false, true>, d_descs, d_eps, C);
+  }
+  if (!sm) return cudaLaunchKernelEx(&cfg, hqr1_kernel<true, false>, d_descs, d_eps, C);
+  if (C > 1) return cudaLaunchKernelEx(&cfg, hqr1_kernel<true, true>, d_descs, d_eps, C);
+  return cudaLaunchKernelEx(&cfg, hqr1_kernel<false, true>, d_descs, d_eps, C);
 }
 
 }  // namespace dtnb

@@ -295,13 +295,16 @@ def basis_orthonormality_defect(H: HbsMatrix) -> float:
     return d
 
 
-def serialize(H: HbsMatrix) -> bytes:
-    """DTNHBS01 (hbs.cpp:446-470)."""
+def serialize(H: HbsMatrix) -> bytearray:
+    """DTNHBS01 (hbs.cpp:446-470), as a bytes-like buffer."""
     n = C.c_uint64()
     H.ctx.check(L.lib().dtn_gpu_hbs_serialize(H.h, None, 0, C.byref(n)))
-    buf = (C.c_uint8 * n.value)()
-    H.ctx.check(L.lib().dtn_gpu_hbs_serialize(H.h, buf, n.value, C.byref(n)))
-    return bytes(buf)
+    out = bytearray(n.value)  # filled in place: one device-to-host copy, no staging copies
+    if n.value:
+        buf = (C.c_uint8 * n.value).from_buffer(out)
+        H.ctx.check(L.lib().dtn_gpu_hbs_serialize(H.h, buf, n.value, C.byref(n)))
+        del buf
+    return out
 
 
 def deserialize(data: bytes, ctx: Context | None = None) -> HbsMatrix:
