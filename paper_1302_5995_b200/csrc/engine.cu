@@ -1874,8 +1874,18 @@ double rank_tol_factor() {
   return v;
 }
 
+// Step of a rank raise: ell / DTN_RANK_RAISE (at least 16).
+int rank_raise_div() {
+  static const int v = [] {
+    const char* e = std::getenv("DTN_RANK_RAISE");
+    return e ? std::max(1, std::atoi(e)) : 4;
+  }();
+  return v;
+}
+
 // Factor ranks that failed the range-finder check of a structured build (tail of the
-// sketch's R diagonal above tol): raise them by half (at least 16), per J edge size.
+// sketch's R diagonal above tol): raise them by ell / DTN_RANK_RAISE (at least 16), per
+// J edge size.
 bool raise_ranks(const dtn_op* op, double tol, std::vector<std::pair<int, int>>& over) {
   const PlanDev& D = *op->plan;
   bool raised = false;
@@ -1883,7 +1893,7 @@ bool raise_ranks(const dtn_op* op, double tol, std::vector<std::pair<int, int>>&
     if (!(D.h_qstat[2 * q + 1] > tol)) continue;
     const Node& nd = D.P.nodes[size_t(D.qr_node[q])];
     if (nd.ell >= nd.jn) continue;  // already exact
-    const int want = std::min({nd.jn, 252, int(align_up(nd.ell + std::max(16, nd.ell / 2), 8))});
+    const int want = std::min({nd.jn, 252, int(align_up(nd.ell + std::max(16, nd.ell / rank_raise_div()), 8))});
     if (want <= nd.ell) continue;  // at the cap
     auto it = std::find_if(over.begin(), over.end(), [&](const auto& e) { return e.first == nd.jn; });
     if (it == over.end()) {

@@ -14,6 +14,7 @@
 // S = M_bb - M_bi M_ii^{-1} M_ib (dense_nd.cpp:181) in place.
 #include <cfloat>
 #include <cstdlib>
+#include <initializer_list>
 
 #include <cooperative_groups.h>
 
@@ -148,6 +149,13 @@ __device__ long long g_pro_clk[8];
 #define PROCLK(slot) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_pro_clk[slot] = clock64(); } while (0)
 #else
 #define PROCLK(slot) do { } while (0)
+#endif
+
+#ifdef DTN_PANEL_PROFILE
+__device__ long long g_p2_clk[16];
+#define P2CLK(slot) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_p2_clk[slot] = clock64(); } while (0)
+#else
+#define P2CLK(slot) do { } while (0)
 #endif
 
 __device__ unsigned g_panel_fallbacks;  // panels whose no-interchange attempt failed (diagnostic)
@@ -726,6 +734,487 @@ __global__ void __launch_bounds__(PNT) panel_kernel(KernelArgs args, const int* 
   if constexpr (CL) cg::this_cluster().sync();  // no CTA exits while others may still write its smem
 }
 
+// ---------------------------------------------------------------------------
+// panel2_kernel: panel_kernel's contract and arithmetic (bit-identical results),
+// loop-ROLLED. panel_kernel unrolls all 32 pivot steps over compile-time register
+// indices (26k SASS instructions, ~415 KB of code executed once per launch: the
+// launch is instruction-fetch bound, ncu "no_instructions" stalls). Here every
+// row lives in a SHIFTING register window: at step j, w[c] holds column j + c,
+// so the step body is the same for every j -- the pivot column is always w[0]
+// and the update w[c - 1] = w[c] - l u[c] shifts the window by one -- and the
+// step loop is rolled (a few KB of code, icache-resident). Multipliers leave the
+// window at their step and go straight to global memory (column-major: a warp's
+// stores are coalesced); a pivot row writes its U row when it is chosen. The
+// final row placement moves only the <= 2 kb rows that change position (rank 0,
+// staged through shared memory after a cluster barrier).
+__device__ __forceinline__ void shift_update(double (&w)[PKB], double l, const double* __restrict__ prow) {
+  const double2* p2 = reinterpret_cast<const double2*>(prow);
+#pragma unroll
+  for (int c2 = 0; c2 < PKB / 2; ++c2) {
+    const double2 u = p2[c2];
+    if (c2 > 0) w[2 * c2 - 1] = fma(-l, u.x, w[2 * c2]);
+    w[2 * c2] = fma(-l, u.y, w[2 * c2 + 1]);
+  }
+  w[PKB - 1] = 0.0;
+}
+
+template <bool CL, int RPT>
+__global__ void __launch_bounds__(PNT) panel2_kernel(KernelArgs args, const int* __restrict__ list, int k0, int kb,
+                                                    int csize, int fused, int use_fast) {
+  constexpr int SC = PNW, NSLOT = PNW + (CL ? PMAXC : 0);
+  __shared__ __align__(16) double rows[2][NSLOT][PKB];
+  __shared__ __align__(16) unsigned sinfo[2][PNW][4];
+  __shared__ int sp[PKB], vac[PKB];
+  __shared__ __align__(16) unsigned cinfo[2][CL ? PMAXC : 1][4];
+  __shared__ __align__(8) unsigned long long mbar[2];
+  constexpr int PLD = PKB + 2;  // 16-byte aligned rows
+  __shared__ __align__(16) double pro[PKB * PLD];  // prologue: U12 of step k0 - kb
+  __shared__ int m_dst[2 * PKB], m_src[2 * PKB];
+  __shared__ int fast_fail, jtop_s, fail_all;
+  __shared__ int mv_dst[2 * PKB], mv_src[2 * PKB];
+  extern __shared__ __align__(16) double pdyn[];
+  double* ub = pdyn;               // [PKB][PLD]: U11 rows SHIFTED, ub[j * PLD + c] = U[j][j + c]
+  double* urinv = ub + PKB * PLD;  // [PKB] reciprocal pivots
+  double* psave = urinv + PKB;     // [RPT * PNT][PKB + 1]: L21 rows (prologue), rows before the panel
+  const int crank = CL ? int(cg::this_cluster().block_rank()) : 0;
+  const int node_id = list[blockIdx.x / csize];
+  const NodeDev nd = args.nodes[node_id];
+  if (k0 >= nd.ni) return;  // uniform over the cluster
+  const int kbe = min(kb, nd.ni - k0);
+  const int Ri = nd.ni - k0;
+  double* M = args.arena + nd.m_off + k0 + (long long)k0 * nd.ldm;
+  const long long ldm = nd.ldm;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int stride = csize * PNT;
+  int* perm = args.piv + nd.piv_off;
+  auto csync = [] {
+    if constexpr (CL) cg::this_cluster().sync();
+    else __syncthreads();
+  };
+
+  P2CLK(0);
+  double v[RPT][PKB];
+  int elim[RPT];
+  const bool try_fast = use_fast && (k0 == 0 || *(volatile int*)pivoting_flag(args, nd) < use_fast);
+  if (k0 == 0 && crank == 0 && tid == 0) *pivoting_flag(args, nd) = 0;
+  if (k0 == 0 || !fused) {
+#pragma unroll
+    for (int a = 0; a < RPT; ++a) {
+      const int r = crank * PNT + tid + stride * a;
+#pragma unroll
+      for (int c = 0; c < PKB; ++c) v[a][c] = (r < Ri && c < kbe) ? M[r + c * ldm] : 0.0;
+      if (k0 == 0 && r < Ri) perm[r] = r;
+    }
+  } else {
+    // fused prologue (as panel_kernel): step kp = k0 - kb applied to this panel's columns
+    const int kp = k0 - kb;
+    double* Mg = args.arena + nd.m_off;
+    double* l11 = ub;  // [PKB][PLD], L11[i][m] at i * PLD + m (unshifted; free until the fast path)
+#pragma unroll
+    for (int a = 0; a < RPT; ++a) {
+      const int r = crank * PNT + tid + stride * a;
+      double* lr = psave + (a * PNT + tid) * (PKB + 1);
+      if (r < Ri) {
+        const long long R = k0 + r;
+        for (int m = 0; m < kb; ++m) cp_async8(lr + m, Mg + R + (long long)(kp + m) * ldm, 8);
+#pragma unroll
+        for (int c = 0; c < PKB; ++c) v[a][c] = c < kbe ? Mg[R + (long long)(k0 + c) * ldm] : 0.0;
+      } else {
+#pragma unroll
+        for (int c = 0; c < PKB; ++c) v[a][c] = 0.0;
+      }
+    }
+    for (int e = tid; e < PKB * PKB; e += PNT) {
+      const int i = e % PKB, m = e / PKB;
+      if (m < i && i < kb) cp_async8(l11 + i * PLD + m, Mg + (kp + i) + (long long)(kp + m) * ldm, 8);
+      else l11[i * PLD + m] = 0.0;
+    }
+    cp_async_commit();
+    const int* mvp = move_list(args, nd, kp);
+    if (tid < 2 * PKB) {
+      m_dst[tid] = mvp[tid];
+      m_src[tid] = mvp[2 * PKB + tid];
+    }
+    constexpr int QC = PKB / PNW;
+    double xs[QC];
+#pragma unroll
+    for (int q = 0; q < QC; ++q)
+      xs[q] = (lane < kb && warp * QC + q < kbe) ? Mg[(kp + lane) + (long long)(k0 + warp * QC + q) * ldm] : 0.0;
+    cp_async_wait<0>();
+    __syncthreads();
+    {
+      const int i = lane, c0 = warp * QC;
+      const int srow = m_src[i];
+      double x[QC];
+#pragma unroll
+      for (int q = 0; q < QC; ++q)
+        x[q] = (srow == kp + i || !(i < kb && c0 + q < kbe)) ? xs[q] : Mg[srow + (long long)(k0 + c0 + q) * ldm];
+#pragma unroll 4
+      for (int m = 0; m < kb - 1; ++m) {
+        const double lim = (i > m) ? l11[i * PLD + m] : 0.0;
+#pragma unroll
+        for (int q = 0; q < QC; ++q) x[q] = fma(-lim, __shfl_sync(0xffffffffu, x[q], m), x[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < QC; ++q) pro[i * PLD + c0 + q] = x[q];
+    }
+    const bool displaced = m_dst[PKB] >= 0;
+#pragma unroll
+    for (int a = 0; a < RPT; ++a) {
+      const int r = crank * PNT + tid + stride * a;
+      if (displaced && r < Ri) {
+        const int R = k0 + r;
+        int src = R;
+#pragma unroll 4
+        for (int t = PKB; t < 2 * PKB; ++t)
+          if (m_dst[t] == R) src = m_src[t];
+        if (src != R)
+#pragma unroll
+          for (int c = 0; c < PKB; ++c) v[a][c] = c < kbe ? Mg[src + (long long)(k0 + c) * ldm] : 0.0;
+      }
+    }
+    __syncthreads();
+    const bool lead = try_fast && crank == 0;
+    if (lead && warp != 0) asm volatile("bar.sync 1, %0;" ::"r"(PNT) : "memory");
+#pragma unroll 2
+    for (int m = 0; m < kb; ++m) {
+      double lm[RPT];
+#pragma unroll
+      for (int a = 0; a < RPT; ++a) lm[a] = psave[(a * PNT + tid) * (PKB + 1) + m];
+      const double2* u2 = reinterpret_cast<const double2*>(pro + m * PLD);
+#pragma unroll
+      for (int c2 = 0; c2 < PKB / 2; ++c2) {
+        const double2 u = u2[c2];
+#pragma unroll
+        for (int a = 0; a < RPT; ++a) {
+          v[a][2 * c2] = fma(-lm[a], u.x, v[a][2 * c2]);
+          v[a][2 * c2 + 1] = fma(-lm[a], u.y, v[a][2 * c2 + 1]);
+        }
+      }
+    }
+    if (lead && warp == 0) asm volatile("bar.arrive 1, %0;" ::"r"(PNT) : "memory");
+#pragma unroll
+    for (int a = 0; a < RPT; ++a) {
+      const int r = crank * PNT + tid + stride * a;
+#pragma unroll
+      for (int c = 0; c < PKB; ++c)
+        if (c >= kbe || r >= Ri) v[a][c] = 0.0;
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < RPT; ++a) {
+    const int r = crank * PNT + tid + stride * a;
+    elim[a] = (r < Ri) ? -1 : PKB;
+  }
+  P2CLK(1);
+  double pmin = k0 == 0 ? DBL_MAX : args.pivstat[2 * node_id];
+  double pmax = k0 == 0 ? 0.0 : args.pivstat[2 * node_id + 1];
+  bool bad = false;
+  bool fast = false;
+  int jstart = 0;
+  if (try_fast) {
+    // ---- no-interchange attempt (see panel_kernel): top block LU by warp 0 of
+    // rank 0, every other row x U11 = a, verified |l| <= 1
+#pragma unroll
+    for (int a = 0; a < RPT; ++a)
+#pragma unroll
+      for (int c = 0; c < PKB; ++c) psave[(a * PNT + tid) * (PKB + 1) + c] = v[a][c];
+    if (tid == 0) fast_fail = fail_all = PKB;
+    int jf = PKB;
+    P2CLK(2);
+    if (crank == 0 && warp == 0) {  // rows 0..kbe-1 in lanes 0..kbe-1 (a = 0)
+      for (int j = 0; j < kbe; ++j) {
+        if (lane == j) {
+#pragma unroll
+          for (int c = 0; c < PKB; c += 2)
+            *reinterpret_cast<double2*>(ub + j * PLD + c) = make_double2(v[0][c], v[0][c + 1]);
+          urinv[j] = __drcp_rn(v[0][0]);
+        }
+        __syncwarp();
+        if (lane > j && lane < kbe) {
+          const double l = v[0][0] * urinv[j];
+          if (!(fabs(l) <= 1.0) && jf == PKB) jf = j;
+          M[lane + (long long)j * ldm] = l;
+          shift_update(v[0], l, ub + j * PLD);
+        }
+      }
+      for (int j = kbe + lane; j < PKB; j += 32) {  // rows past the panel: zero U rows
+#pragma unroll 4
+        for (int c = 0; c < PLD; ++c) ub[j * PLD + c] = 0.0;
+      }
+      const int jt = __reduce_min_sync(0xffffffffu, unsigned(jf));
+      if (lane == 0) fast_fail = jt;
+    }
+    P2CLK(3);
+    if constexpr (CL) {
+      cg::this_cluster().sync();
+      if (crank != 0) {
+        const double* rub = cg::this_cluster().map_shared_rank(ub, 0);
+        for (int e = tid; e < PKB * PLD + PKB; e += PNT) ub[e] = rub[e];
+        if (tid == 0) jtop_s = *cg::this_cluster().map_shared_rank(&fast_fail, 0);
+      }
+    }
+    __syncthreads();
+    if (crank == 0 && tid == 0) jtop_s = fast_fail;
+    __syncthreads();
+    const int jtop = jtop_s;
+    auto subst = [&](int rlo, int jmax, bool track) {
+      for (int j = 0; j < jmax; ++j) {
+#pragma unroll
+        for (int a = 0; a < RPT; ++a) {
+          const int r = crank * PNT + tid + stride * a;
+          if (r >= rlo && r < Ri) {
+            const double l = v[a][0] * urinv[j];
+            if (track && !(fabs(l) <= 1.0) && jf == PKB) jf = j;
+            M[r + (long long)j * ldm] = l;
+            shift_update(v[a], l, ub + j * PLD);
+          }
+        }
+      }
+    };
+    P2CLK(4);
+    subst(kbe, min(kbe, jtop), true);
+    P2CLK(5);
+    if (jf < PKB) atomicMin(&fast_fail, jf);
+    __syncthreads();
+    int jstar;
+    if constexpr (CL) {
+      if (warp == 0 && lane < csize && fast_fail < PKB)
+        atomicMin(cg::this_cluster().map_shared_rank(&fail_all, lane), fast_fail);
+      cg::this_cluster().sync();
+      jstar = fail_all;
+    } else {
+      jstar = fast_fail;
+    }
+    jstar = min(jstar, kbe);
+    fast = jstar >= kbe;
+    P2CLK(6);
+    if (crank == 0 && warp == 0) {
+      const double apiv = fabs(ub[lane * PLD]);
+      const bool live = lane < jstar;
+      double lo = live ? apiv : DBL_MAX, hi = live ? apiv : 0.0;
+      const bool nb_ = live && (!(apiv == apiv) || apiv == INFINITY);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      }
+      pmin = fmin(pmin, lo);
+      pmax = fmax(pmax, hi);
+      bad |= __any_sync(0xffffffffu, nb_);
+    }
+    if (fast) {
+      if (crank == 0) {
+        if (tid < 2 * PKB) {
+          int* mv = move_list(args, nd, k0);
+          mv[tid] = tid < kbe ? k0 + tid : -1;
+          mv[2 * PKB + tid] = tid < kbe ? k0 + tid : -1;
+        }
+        for (int e = tid; e < PKB * PKB; e += PNT) {  // U rows in place
+          const int i = e % PKB, c = e / PKB;
+          if (i < kbe && c >= i && c < kbe) M[i + (long long)c * ldm] = ub[i * PLD + (c - i)];
+        }
+      }
+    } else {
+      if (crank == 0 && tid == 0) {
+        atomicAdd(&g_panel_fallbacks, 1u);
+        *pivoting_flag(args, nd) += 1;
+      }
+      // rows >= jstar restart from the saved values with the steps < jstar (exactly
+      // partial pivoting's); rows < jstar are the pivots of steps 0 .. jstar - 1
+#pragma unroll
+      for (int a = 0; a < RPT; ++a) {
+        const int r = crank * PNT + tid + stride * a;
+        if (r >= jstar)
+#pragma unroll
+          for (int c = 0; c < PKB; ++c) v[a][c] = psave[(a * PNT + tid) * (PKB + 1) + c];
+      }
+      subst(jstar, jstar, false);
+      jstart = jstar;
+#pragma unroll
+      for (int a = 0; a < RPT; ++a) {
+        const int r = crank * PNT + tid + stride * a;
+        if (r < jstart) elim[a] = r;
+      }
+      if (tid < jstart) sp[tid] = tid;
+    }
+  }
+  if (!fast) {
+    const unsigned tx_bytes = unsigned(csize) * (PKB * 8 + 16);
+    if constexpr (CL) {
+      if (tid == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_arm(&mbar[0], tx_bytes);
+        mbar_arm(&mbar[1], tx_bytes);
+      }
+      cg::this_cluster().sync();
+    }
+    for (int j = jstart; j < kbe; ++j) {
+      const int jr = j - jstart;
+      const int buf = jr & 1;
+      unsigned key = 0u, klo = 0u;
+      int ba = 0;
+#pragma unroll
+      for (int a = 0; a < RPT; ++a) {
+        const double ax = fabs(v[a][0]);
+        const unsigned ka = elim[a] < 0 ? (unsigned(__double2hiint(ax)) | 0x80000000u) : 0u;
+        const unsigned kl = unsigned(__double2loint(ax));
+        if (ka > key || (ka == key && kl > klo)) {
+          key = ka;
+          klo = kl;
+          ba = a;
+        }
+      }
+      const unsigned whi = __reduce_max_sync(0xffffffffu, key);
+      const unsigned wlo = __reduce_max_sync(0xffffffffu, key == whi ? klo : 0u);
+      const int wlane = __ffs(__ballot_sync(0xffffffffu, key == whi && klo == wlo)) - 1;
+      {
+        const bool win = lane == wlane;
+#pragma unroll
+        for (int a = 0; a < RPT; ++a) {
+          const bool wa = win && a == ba;
+#pragma unroll
+          for (int c = 0; c < PKB; c += 2) st_shared_v2_pred(&rows[buf][warp][c], v[a][c], v[a][c + 1], wa);
+        }
+        st_shared_v4u_pred(&sinfo[buf][warp][0], whi, wlo, unsigned(crank * PNT + tid + stride * ba), 0u, win);
+      }
+      __syncthreads();
+      const unsigned lk = lane < PNW ? sinfo[buf][lane][0] : 0u;
+      const unsigned ll = lane < PNW ? sinfo[buf][lane][1] : 0u;
+      const unsigned bkey = __reduce_max_sync(0xffffffffu, lk);
+      const unsigned blo = __reduce_max_sync(0xffffffffu, lk == bkey ? ll : 0u);
+      const int bw = __ffs(__ballot_sync(0xffffffffu, lk == bkey && ll == blo && lane < PNW)) - 1;
+      int slot = bw, p = int(sinfo[buf][bw][2]);
+      if constexpr (CL) {
+        {
+          const double rv = rows[buf][bw][lane];
+          for (int d = warp; d < csize; d += PNW) {
+            const unsigned mb = cluster_map(&mbar[buf], d);
+            st_async_b64(cluster_map(&rows[buf][SC + crank][lane], d), __double_as_longlong(rv), mb);
+            if (lane == 0) st_async_v4_b32(cluster_map(&cinfo[buf][crank][0], d), bkey, blo, unsigned(p), 0u, mb);
+          }
+        }
+        mbar_wait(&mbar[buf], unsigned(jr >> 1) & 1u);
+        const unsigned ck = lane < csize ? cinfo[buf][lane][0] : 0u;
+        const unsigned cl_ = lane < csize ? cinfo[buf][lane][1] : 0u;
+        const unsigned gkey = __reduce_max_sync(0xffffffffu, ck);
+        const unsigned glo = __reduce_max_sync(0xffffffffu, ck == gkey ? cl_ : 0u);
+        const int cw = __ffs(__ballot_sync(0xffffffffu, ck == gkey && cl_ == glo && lane < csize)) - 1;
+        slot = SC + cw;
+        p = int(cinfo[buf][cw][2]);
+      }
+      const double* prow = &rows[buf][slot][0];
+      const double piv = prow[0];
+      if (crank == 0 && warp == (j & (PNW - 1))) ub[j * PLD + lane] = prow[lane];  // U row j (shifted)
+      if constexpr (CL) {
+        if (tid == 0) mbar_arm(&mbar[buf], tx_bytes);
+      }
+      const double apiv = fabs(piv);
+      pmin = fmin(pmin, apiv);
+      pmax = fmax(pmax, apiv);
+      bad |= !(apiv == apiv) || apiv == INFINITY;
+      const double rinv = __drcp_rn(piv);
+#pragma unroll
+      for (int a = 0; a < RPT; ++a) {
+        const int r = crank * PNT + tid + stride * a;
+        if (r == p) elim[a] = j;
+        if (elim[a] < 0) {
+          const double l = v[a][0] * rinv;
+          M[r + (long long)j * ldm] = l;
+          shift_update(v[a], l, prow);
+        }
+      }
+      if (tid == 0) sp[j] = p;
+    }
+    // ---- final placement: pivot of step e -> position e; the top rows [0, kbe)
+    // that were not pivots fill, in order, the positions vacated by pivots from
+    // below (also in order). Only those rows move: rank 0 stages them through
+    // shared memory once every CTA's stores are visible.
+    csync();
+    if (crank == 0) {
+      // U row e (ub, shifted) into the pivot row's original position, columns [e, kbe)
+      for (int e = tid; e < PKB * PKB; e += PNT) {
+        const int i = e % PKB, c = e / PKB;
+        if (i < kbe && c >= i && c < kbe) M[sp[i] + (long long)c * ldm] = ub[i * PLD + (c - i)];
+      }
+      __syncthreads();
+      if (warp == 0) {
+        const int x = lane < kbe ? sp[lane] : 0x7fffffff;
+        const int key2 = x >= kbe ? x : 0x7fffffff;
+        int rk = 0;
+        for (int e = 0; e < kbe; ++e) {
+          const int y = sp[e] >= kbe ? sp[e] : 0x7fffffff;
+          rk += (y < key2);
+        }
+        if (lane < kbe && key2 != 0x7fffffff) vac[rk] = key2;
+        unsigned topmask = 0u;
+        for (int e = 0; e < kbe; ++e)
+          if (sp[e] < kbe) topmask |= 1u << sp[e];
+        __syncwarp();
+        // slots: e < kbe -> (dst e, src sp[e]); kbe + i -> (dst vac[i], src i-th displaced top row)
+        for (int sl = lane; sl < 2 * PKB; sl += 32) {
+          int dst = -1, src = -1;
+          if (sl < kbe) {
+            dst = sl;
+            src = sp[sl];
+          } else {
+            const int i = sl - kbe;
+            const int nvac = __popc(~topmask & ((kbe < 32) ? ((1u << kbe) - 1u) : 0xffffffffu));
+            if (i < nvac) {
+              // the i-th top row (ascending) that is not a pivot
+              int t = 0, cnt = -1;
+              for (; t < kbe; ++t)
+                if (!((topmask >> t) & 1u) && ++cnt == i) break;
+              dst = vac[i];
+              src = t;
+            }
+          }
+          mv_dst[sl] = dst;
+          mv_src[sl] = src;
+        }
+      }
+      __syncthreads();
+      int* mv = move_list(args, nd, k0);
+      if (tid < 2 * PKB) {
+        mv[tid] = mv_dst[tid] >= 0 ? k0 + mv_dst[tid] : -1;
+        mv[2 * PKB + tid] = mv_src[tid] >= 0 ? k0 + mv_src[tid] : -1;
+      }
+      // stage the moved rows (panel columns) and their permutation entries
+      double* stage = psave;  // [2 PKB][PKB]
+      for (int e = tid; e < 2 * PKB * PKB; e += PNT) {
+        const int sl = e / PKB, c = e % PKB;
+        const int src = mv_src[sl];
+        if (src >= 0 && mv_dst[sl] != src && c < kbe) stage[sl * PKB + c] = __ldcg(M + src + (long long)c * ldm);
+      }
+      int oldp = 0;
+      if (tid < 2 * PKB && mv_src[tid] >= 0 && mv_dst[tid] != mv_src[tid]) oldp = __ldcg(perm + k0 + mv_src[tid]);
+      __syncthreads();
+      for (int e = tid; e < 2 * PKB * PKB; e += PNT) {
+        const int sl = e / PKB, c = e % PKB;
+        const int src = mv_src[sl];
+        if (src >= 0 && mv_dst[sl] != src && c < kbe) M[mv_dst[sl] + (long long)c * ldm] = stage[sl * PKB + c];
+      }
+      if (tid < 2 * PKB && mv_src[tid] >= 0 && mv_dst[tid] != mv_src[tid]) perm[k0 + mv_dst[tid]] = oldp;
+    }
+  }
+  P2CLK(7);
+  if (fused && k0 > 0 && crank == 0) {  // U12 of the prologue into rows [k0 - kb, k0)
+    double* Mg = args.arena + nd.m_off;
+    for (int e = tid; e < PKB * PKB; e += PNT) {
+      const int i = e % PKB, c = e / PKB;
+      if (i < kb && c < kbe) Mg[(k0 - kb + i) + (long long)(k0 + c) * ldm] = pro[i * PLD + c];
+    }
+  }
+  if (crank == 0 && tid == 0) {
+    args.pivstat[2 * node_id] = pmin;
+    args.pivstat[2 * node_id + 1] = bad ? INFINITY : pmax;
+  }
+  P2CLK(8);
+  if constexpr (CL) cg::this_cluster().sync();  // no CTA exits while others may still read its smem
+}
+
 // Row swaps + U12 = L11^{-1} (P A)[k0:k1, k1:total] for the trailing columns;
 // with swap_left, also the row swaps of the already factored columns [0, k0)
 // (needed only when L itself is reused: the root LU for G = S^{-1}).
@@ -834,7 +1323,25 @@ int panel_fast_threshold() {
   return th;
 }
 
+// DTN_PANEL_LEGACY=1: the fully unrolled panel_kernel instead of panel2_kernel
+bool panel_legacy() {
+  static const bool on = std::getenv("DTN_PANEL_LEGACY") != nullptr;
+  return on;
+}
+
 cudaError_t blocked_init() {
+  for (auto f : {panel2_kernel<true, 1>, panel2_kernel<true, 2>}) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  for (auto f : {panel2_kernel<true, 1>, panel2_kernel<false, 1>}) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(panel_dyn_smem(1)));
+    if (e != cudaSuccess) return e;
+  }
+  for (auto f : {panel2_kernel<true, 2>, panel2_kernel<false, 2>}) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(panel_dyn_smem(2)));
+    if (e != cudaSuccess) return e;
+  }
   cudaError_t e = cudaFuncSetAttribute(panel_kernel<true, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(panel_kernel<true, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -873,6 +1380,7 @@ void panel_shape(int max_rows, int* rpt, int* csize) {
 
 size_t panel_dyn_smem(int rpt);
 int panel_fast_threshold();
+bool panel_legacy();
 
 template <bool CL, int RPT>
 cudaError_t launch_panel_t(const KernelArgs& args, const int* d_list, int count, int k0, int kb, int csize,
@@ -891,7 +1399,10 @@ cudaError_t launch_panel_t(const KernelArgs& args, const int* d_list, int count,
     cfg.numAttrs = 1;
   }
   cfg.dynamicSmemBytes = panel_dyn_smem(RPT);
-  return cudaLaunchKernelEx(&cfg, panel_kernel<CL, RPT>, args, d_list, k0, kb, csize, fused ? 1 : 0,
+  if (panel_legacy())
+    return cudaLaunchKernelEx(&cfg, panel_kernel<CL, RPT>, args, d_list, k0, kb, csize, fused ? 1 : 0,
+                              panel_fast_threshold());
+  return cudaLaunchKernelEx(&cfg, panel2_kernel<CL, RPT>, args, d_list, k0, kb, csize, fused ? 1 : 0,
                             panel_fast_threshold());
 }
 

@@ -699,6 +699,450 @@ __global__ void __launch_bounds__(QR_THREADS) hqr1_kernel(const QrDesc* __restri
   if constexpr (CL) cg::this_cluster().sync();  // no CTA leaves while others may still read its shared memory
 }
 
+// ---------------------------------------------------------------------------
+// hqrb_kernel: the sketch factors' Householder QR BLOCKED (dgeqrf / dorgqr with
+// compact-WY block reflectors, panels of QB = 16 columns). hqr_kernel / hqr1_kernel
+// apply every reflector to every trailing column at once (level-2: each column step
+// streams the whole trailing block through shared memory -- the measured bound);
+// here a column step touches only its panel, and the trailing columns take one
+// rank-16 update per panel: W = V^T Y (partials per CTA, summed over the cluster),
+// Y -= V (T^T W) (dlarft's T). The explicit Q is formed backward per panel as
+// Q[:, c0:] = [E | Q[:, c1:]] - V T (V^T [E | Q[:, c1:]]), E the panel's unit
+// columns. Cluster sums are a reduce-scatter + all-gather through DSMEM (each CTA
+// sums its 1/C share of the entries, then reads the others' shares), added in rank
+// order so every CTA holds bit-identical sums. Results equal dgeqrf/dorgqr's up to
+// rounding (same reflectors, beta = -sign(alpha) |x|, tau = (beta - alpha) / beta).
+constexpr int QB = 16;
+#ifdef HQRB_PROFILE
+__device__ long long g_hqrb_clk[16];
+__device__ unsigned long long g_hqrb_t[2 * 2048];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define HCLK_T(v) long long v = clock64()
+#define HCLK_ADD(slot, t0) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_hqrb_clk[slot] += clock64() - (t0); } while (0)
+#else
+#define HCLK_T(v) do { } while (0)
+#define HCLK_ADD(slot, t0) do { } while (0)
+#endif
+
+struct HqrbSmem {  // dynamic shared-memory carve (doubles), identical for every CTA of a launch
+  int ldl, rmax, ncmax, npan, wcols;
+  __host__ __device__ long long y() const { return 0; }
+  __host__ __device__ long long vr() const { return (long long)ldl * ncmax; }
+  __host__ __device__ long long wp() const { return vr() + (long long)rmax * QB; }
+  __host__ __device__ long long ws() const { return wp(); }  // the sums overwrite the partials (see allreduce_w)
+  __host__ __device__ long long ts() const { return wp() + (long long)QB * wcols; }
+  __host__ __device__ long long total() const { return ts() + (long long)npan * QB * QB; }
+};
+
+template <bool CL>
+__global__ void __launch_bounds__(QR_THREADS) hqrb_kernel(const QrDesc* __restrict__ descs, const double* eps_ptr,
+                                                          int C, HqrbSmem L) {
+#ifdef HQRB_PROFILE
+  if (threadIdx.x == 0) g_hqrb_t[2 * blockIdx.x] = gtimer();
+#endif
+  extern __shared__ __align__(16) double qdyn[];
+  __shared__ double part[2][QB + 8];  // [parity] column-step partials (+ probe norms)
+  __shared__ double rowc[2][QB];
+  __shared__ double tot[QB], rct[QB];
+  __shared__ double tau_s[QR_MAXN], rdiag[QR_MAXN];
+  __shared__ double red[QR_WARPS];
+  const int rank = CL ? int(cg::this_cluster().block_rank()) : 0;
+  const QrDesc d = descs[blockIdx.x / C];
+  const int m = d.m, n = d.n, nc = d.n + d.p;
+  const int R = (m + C - 1) / C, r0 = rank * R, r1 = min(m, r0 + R), nr = max(r1 - r0, 0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ld = L.ldl;
+  double* Y = qdyn + L.y();
+  double* Vr = qdyn + L.vr();  // [rmax][QB] row-major: the panel's reflectors, local rows
+  double* Wp = qdyn + L.wp();  // [QB][wcols] this CTA's partial sums
+  double* Ws = qdyn + L.ws();  // [QB][wcols] cluster sums
+  double* Ts = qdyn + L.ts();  // [npan][QB][QB] T of every panel (upper triangular)
+  for (int j = 0; j < nc; ++j)
+    for (int i = tid; i < nr; i += QR_THREADS) Y[i + j * ld] = d.Y[r0 + i + (long long)j * d.ldy];
+  __syncthreads();
+  auto csync = [] {
+    if constexpr (CL) cg::this_cluster().sync();
+    else __syncthreads();
+  };
+  auto rsum = [&](const double* slot) -> double {  // sum over the cluster's copies of *slot, rank order
+    if constexpr (CL) {
+      double v[QR_MAXC];
+#pragma unroll
+      for (int q = 0; q < QR_MAXC; ++q)
+        v[q] = q < C ? *cg::this_cluster().map_shared_rank(const_cast<double*>(slot), q) : 0.0;
+      double t = v[0];
+#pragma unroll
+      for (int q = 1; q < QR_MAXC; ++q)
+        if (q < C) t += v[q];
+      return t;
+    } else {
+      return *slot;
+    }
+  };
+  // Ws[0 : QB * cols) = cluster sum of Wp, in place (Ws aliases Wp): reduce-scatter (CTA q
+  // sums share q over every CTA's partials and stores it in its own share-q slots, which no
+  // other CTA reads in this phase), barrier, all-gather (CTA q copies every other share
+  // from its owner into its own slots, which no other CTA reads in this phase)
+  auto allreduce_w = [&](int cols) {
+    const int cnt = QB * cols;
+    csync();  // every partial written
+    if constexpr (CL) {
+      const int share = (cnt + C - 1) / C, e0 = rank * share, e1 = min(cnt, e0 + share);
+      for (int e = e0 + tid; e < e1; e += QR_THREADS) {
+        const int k = (e % QB) * L.wcols + e / QB;
+        Ws[k] = rsum(&Wp[k]);  // element k of share `rank`: read (everywhere) and written (here) by this thread only
+      }
+      cg::this_cluster().sync();
+      for (int q = 0; q < C; ++q) {
+        if (q == rank) continue;
+        const int f0 = q * share, f1 = min(cnt, f0 + share);
+        const double* rws = cg::this_cluster().map_shared_rank(Ws, q);
+        for (int e = f0 + tid; e < f1; e += QR_THREADS) {
+          const int k = (e % QB) * L.wcols + e / QB;
+          Ws[k] = rws[k];
+        }
+      }
+    } else {
+      for (int e = tid; e < cnt; e += QR_THREADS) Ws[(e % QB) * L.wcols + e / QB] = Wp[(e % QB) * L.wcols + e / QB];
+    }
+    __syncthreads();
+  };
+  // Vr <- the local rows of panel [c0, c1)'s reflectors (unit diagonal, zeros above)
+  auto stage_v = [&](int c0, int c1) {
+    for (int e = tid; e < nr * QB; e += QR_THREADS) {
+      const int i = e / QB, cc = e % QB, c = c0 + cc, gi = r0 + i;
+      Vr[i * QB + cc] = (c >= c1 || gi < c) ? 0.0 : (gi == c ? 1.0 : Y[i + c * ld]);
+    }
+    __syncthreads();
+  };
+  const int gl = tid & 15, grp = tid >> 4;  // 16 groups of 16 lanes: one panel column per group
+  const int npan = (n + QB - 1) / QB;
+  for (int pn = 0; pn < npan; ++pn) {
+    const int c0 = pn * QB, c1 = min(n, c0 + QB), bw = c1 - c0;
+    double scal_prev = 0.0, beta_prev = 0.0;
+    HCLK_T(tp0);
+    for (int c = c0; c < c1; ++c) {
+      const int par = c & 1;
+      const int lo = max(c + 1 - r0, 0);
+      const bool own = c >= r0 && c < r1;
+      const double* yc = Y + c * ld;
+      if (c > c0) {  // the previous reflector column: [beta; v]
+        const int lp = max(c - r0, 0);
+        double* yp = Y + (c - 1) * ld;
+        for (int i = lp + tid; i < nr; i += QR_THREADS) yp[i] *= scal_prev;
+        if (tid == 0 && c - 1 >= r0 && c - 1 < r1) yp[c - 1 - r0] = beta_prev;
+      }
+      {
+        const int j = c + grp;
+        double s0 = 0.0;
+        if (j < c1) {
+          const double* yj = Y + j * ld;
+          for (int i = lo + gl; i < nr; i += 16) s0 = fma(yc[i], yj[i], s0);
+        }
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        if (j < c1 && gl == 0) part[par][grp] = s0;
+        if (own && tid < c1 - c) rowc[par][tid] = Y[(c - r0) + (c + tid) * ld];
+      }
+      csync();
+      if (tid < c1 - c) {
+        tot[tid] = rsum(&part[par][tid]);
+        if constexpr (CL) rct[tid] = *cg::this_cluster().map_shared_rank(&rowc[par][tid], c / R);
+        else rct[tid] = rowc[par][tid];
+      }
+      __syncthreads();
+      const double sst = tot[0], alpha = rct[0];
+      double beta, tc, scal;
+      if (sst == 0.0) {
+        beta = alpha;
+        tc = 0.0;
+        scal = 0.0;
+      } else {
+        beta = -copysign(sqrt(fma(alpha, alpha, sst)), alpha);
+        tc = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      if (tid == 0) {
+        tau_s[c] = tc;
+        rdiag[c] = beta;
+      }
+      if (tc != 0.0 && grp >= 1 && c + grp < c1) {
+        const int j = c + grp;
+        const double f = tc * fma(scal, tot[grp], rct[grp]);
+        const double g = f * scal;
+        double* yj = Y + j * ld;
+        if (own && gl == 0) yj[c - r0] -= f;
+        for (int i = lo + gl; i < nr; i += 16) yj[i] = fma(-g, yc[i], yj[i]);
+      }
+      scal_prev = scal;
+      beta_prev = beta;
+      __syncthreads();
+    }
+    {  // the panel's last reflector column
+      const int c = c1 - 1, lp = max(c + 1 - r0, 0);
+      double* yp = Y + c * ld;
+      for (int i = lp + tid; i < nr; i += QR_THREADS) yp[i] *= scal_prev;
+      if (tid == 0 && c >= r0 && c < r1) yp[c - r0] = beta_prev;
+    }
+    __syncthreads();
+    // block reflector: G = V^T V and W = V^T Y[:, c1:nc] (one reduction), T (dlarft),
+    // Y[:, c1:nc] -= V (T^T W)
+    HCLK_ADD(1, tp0);
+    HCLK_T(tp1);
+    stage_v(c0, c1);
+    const int nt = nc - c1, ncol = QB + nt;
+    if (tid < ncol) {
+      double acc[QB];
+#pragma unroll
+      for (int cc = 0; cc < QB; ++cc) acc[cc] = 0.0;
+      const bool isv = tid < QB;
+      const double* col = isv ? nullptr : Y + (c1 + tid - QB) * ld;
+      for (int i = 0; i < nr; ++i) {
+        const double y = isv ? Vr[i * QB + tid] : col[i];
+        const double2* v2 = reinterpret_cast<const double2*>(Vr + i * QB);
+#pragma unroll
+        for (int c2 = 0; c2 < QB / 2; ++c2) {
+          const double2 v = v2[c2];
+          acc[2 * c2] = fma(v.x, y, acc[2 * c2]);
+          acc[2 * c2 + 1] = fma(v.y, y, acc[2 * c2 + 1]);
+        }
+      }
+#pragma unroll
+      for (int cc = 0; cc < QB; ++cc) Wp[cc * L.wcols + tid] = acc[cc];
+    }
+    allreduce_w(ncol);
+    HCLK_ADD(2, tp1);
+    HCLK_T(tp2);
+    double* T = Ts + pn * QB * QB;  // T[i * QB + k]
+    if (warp == 0 && lane < QB) {  // dlarft (forward, columnwise): T[0:k, k] = -tau_k T[0:k, 0:k] G[0:k, k]
+      const int i = lane;             // lane i builds row i of T in registers
+      double tr[QB];
+#pragma unroll
+      for (int k = 0; k < QB; ++k) {
+        double g[QB];
+#pragma unroll
+        for (int l = 0; l < k; ++l) g[l] = Ws[l * L.wcols + k];  // G[0:k, k] (broadcast loads)
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int l = 0; l < k; ++l) {
+          const double a = l >= i ? tr[l] : 0.0;
+          if (l & 1) s1 = fma(a, g[l], s1);
+          else s0 = fma(a, g[l], s0);
+        }
+        const double tk = k < bw ? tau_s[c0 + k] : 0.0;
+        tr[k] = i < k ? -tk * (s0 + s1) : (i == k ? tk : 0.0);
+      }
+#pragma unroll
+      for (int k = 0; k < QB; ++k) T[i * QB + k] = tr[k];
+    }
+    __syncthreads();
+    HCLK_ADD(3, tp2);
+    HCLK_T(tp3);
+    if (tid < nt) {
+      double w[QB];
+#pragma unroll
+      for (int cc = 0; cc < QB; ++cc) w[cc] = Ws[cc * L.wcols + QB + tid];
+      double wt[QB];  // T^T w
+#pragma unroll
+      for (int cc = 0; cc < QB; ++cc) {
+        double s = 0.0;
+#pragma unroll
+        for (int l = 0; l <= cc; ++l) s = fma(T[l * QB + cc], w[l], s);
+        wt[cc] = s;
+      }
+      double* col = Y + (c1 + tid) * ld;
+      for (int i = 0; i < nr; ++i) {
+        const double2* v2 = reinterpret_cast<const double2*>(Vr + i * QB);
+        double s = col[i];
+#pragma unroll
+        for (int c2 = 0; c2 < QB / 2; ++c2) {
+          const double2 v = v2[c2];
+          s = fma(-v.x, wt[2 * c2], s);
+          s = fma(-v.y, wt[2 * c2 + 1], s);
+        }
+        col[i] = s;
+      }
+    }
+    __syncthreads();
+    HCLK_ADD(4, tp3);
+  }
+  HCLK_T(tp4);
+  // range-finder check: |(I - Q Q^T) y_probe|^2 = sum of the probe columns' rows >= n
+  double pres = 0.0;
+  {
+    const int lo = max(n - r0, 0);
+    if (warp < d.p) {
+      const double* yq = Y + (n + warp) * ld;
+      double ss = 0.0;
+      for (int i = lo + lane; i < nr; i += 32) ss = fma(yq[i], yq[i], ss);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) part[0][QB + warp] = ss;
+    }
+    csync();
+    for (int q = 0; q < d.p; ++q) pres = fmax(pres, sqrt(rsum(&part[0][QB + q])));
+  }
+  HCLK_ADD(5, tp4);
+  HCLK_T(tp5);
+  // Q, backward over the panels: Q[:, c0:n] = [E | Q[:, c1:n]] - V T (V^T [E | Q[:, c1:n]])
+  for (int pn = npan - 1; pn >= 0; --pn) {
+    const int c0 = pn * QB, c1 = min(n, c0 + QB);
+    stage_v(c0, c1);
+    const int nq = n - c1, ncol = QB + nq;
+    if (tid < ncol) {
+      double acc[QB];
+#pragma unroll
+      for (int cc = 0; cc < QB; ++cc) acc[cc] = 0.0;
+      if (tid < QB) {  // V^T E = V1^T: the owner's rows c0 + tid
+        const int gi = c0 + tid;
+        if (gi >= r0 && gi < r1 && gi < c1)
+#pragma unroll
+          for (int cc = 0; cc < QB; ++cc) acc[cc] = Vr[(gi - r0) * QB + cc];
+      } else {
+        const double* col = Y + (c1 + tid - QB) * ld;
+        for (int i = 0; i < nr; ++i) {
+          const double y = col[i];
+          const double2* v2 = reinterpret_cast<const double2*>(Vr + i * QB);
+#pragma unroll
+          for (int c2 = 0; c2 < QB / 2; ++c2) {
+            const double2 v = v2[c2];
+            acc[2 * c2] = fma(v.x, y, acc[2 * c2]);
+            acc[2 * c2 + 1] = fma(v.y, y, acc[2 * c2 + 1]);
+          }
+        }
+      }
+#pragma unroll
+      for (int cc = 0; cc < QB; ++cc) Wp[cc * L.wcols + tid] = acc[cc];
+    }
+    allreduce_w(ncol);
+    const double* T = Ts + pn * QB * QB;
+    if (tid < ncol && (tid >= QB || c0 + tid < c1)) {
+      double w[QB];
+#pragma unroll
+      for (int cc = 0; cc < QB; ++cc) w[cc] = Ws[cc * L.wcols + tid];
+      double tw[QB];  // T w (T upper)
+#pragma unroll
+      for (int cc = 0; cc < QB; ++cc) {
+        double s = 0.0;
+#pragma unroll
+        for (int l = cc; l < QB; ++l) s = fma(T[cc * QB + l], w[l], s);
+        tw[cc] = s;
+      }
+      const int j = tid < QB ? c0 + tid : c1 + tid - QB;
+      double* col = Y + j * ld;
+      for (int i = 0; i < nr; ++i) {
+        const double2* v2 = reinterpret_cast<const double2*>(Vr + i * QB);
+        double s = tid < QB ? (r0 + i == j ? 1.0 : 0.0) : col[i];
+#pragma unroll
+        for (int c2 = 0; c2 < QB / 2; ++c2) {
+          const double2 v = v2[c2];
+          s = fma(-v.x, tw[2 * c2], s);
+          s = fma(-v.y, tw[2 * c2 + 1], s);
+        }
+        col[i] = s;
+      }
+    }
+    __syncthreads();
+  }
+  HCLK_ADD(6, tp5);
+  for (int jj = 0; jj < n; ++jj)
+    for (int i = tid; i < nr; i += QR_THREADS) d.Q[r0 + i + (long long)jj * d.ldq] = Y[i + jj * ld];
+  if (rank == 0 && d.stat) {
+    double dmax = 0.0;
+    if (d.S)
+      for (int i = tid; i < d.nbs; i += QR_THREADS) dmax = fmax(dmax, fabs(d.S[i + (long long)i * d.lds]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    if (lane == 0) red[warp] = dmax;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < QR_WARPS; ++w) t = fmax(t, red[w]);
+      const double eps = *eps_ptr;
+      const double scale = d.S ? t * sqrt(double(d.k) / 3.0) : (n > 0 ? fabs(rdiag[0]) : 0.0);
+      int rk = 0;
+      for (int i = 0; i < n; ++i)
+        if (fabs(rdiag[i]) > eps * scale) ++rk;
+      d.stat[0] = double(rk);
+      d.stat[1] = scale > 0.0 ? pres / scale : 0.0;
+    }
+  }
+#ifdef HQRB_PROFILE
+  if (threadIdx.x == 0) g_hqrb_t[2 * blockIdx.x + 1] = gtimer();
+#endif
+  if constexpr (CL) cg::this_cluster().sync();  // no CTA leaves while others may still read its shared memory
+}
+
+// launch geometry of hqrb_kernel: the smallest cluster whose row blocks and work
+// buffers fit in shared memory, widened while the launch leaves SMs idle
+template <bool CL>
+__global__ void hqrb_kernel(const QrDesc* __restrict__, const double*, int, HqrbSmem);
+constexpr int HQRB_SMEM_MIN = 120 * 1024;  // one CTA per SM (co-resident CTAs would share its issue slots)
+constexpr int HQRB_SMEM_MAX = 220 * 1024;
+
+// clusters of C CTAs (one per SM) that can be resident at once, per device
+static int hqrb_max_clusters(int C) {
+  static int cache[8][5];
+  static bool init[8][5];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int li = 0;
+  while ((1 << li) < C) ++li;
+  if (dev < 8 && li < 5 && init[dev][li]) return cache[dev][li];
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C * 64);
+  cfg.blockDim = dim3(QR_THREADS);
+  cfg.dynamicSmemBytes = HQRB_SMEM_MIN;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, C > 1 ? (void*)hqrb_kernel<true> : (void*)hqrb_kernel<false>, &cfg) !=
+      cudaSuccess) {
+    (void)cudaGetLastError();
+    n = 0;
+  }
+  if (dev < 8 && li < 5) {
+    cache[dev][li] = n;
+    init[dev][li] = true;
+  }
+  return n;
+}
+
+// launch geometry of hqrb_kernel: the widest cluster (<= 16 CTAs, >= 32 rows each) whose
+// row blocks and work buffers fit in shared memory and whose clusters are all resident at
+// once; else the narrowest that fits
+static bool hqrb_shape(int count, int max_m, int max_nc, int* C_out, HqrbSmem* L) {
+  auto layout = [&](int C) {
+    HqrbSmem s;
+    s.rmax = (max_m + C - 1) / C;
+    s.ldl = s.rmax | 1;
+    s.ncmax = max_nc;
+    s.npan = (max_nc + QB - 1) / QB;
+    s.wcols = max_nc + QB;
+    return s;
+  };
+  int best = 0;
+  for (int C = 1; C <= QR_MAXC; C *= 2) {
+    if (layout(C).total() * 8 > HQRB_SMEM_MAX) continue;
+    if (best == 0) best = C;  // the narrowest that fits
+    if (C > 1 && (max_m + C - 1) / C < 32) break;
+    if (count <= hqrb_max_clusters(C)) best = C;
+  }
+  if (best == 0) return false;
+  *C_out = best;
+  *L = layout(best);
+  return true;
+}
+
 cudaError_t launch_sgather_red(const KernelArgs& args, const int* d_list, int count, int max_total, cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
   dim3 grid((max_total + SG_COLS - 1) / SG_COLS, count);
@@ -750,7 +1194,24 @@ static bool hqr_legacy() {
   return on;
 }
 
+// DTN_HQR_BLOCKED=0: the unblocked sketch QR (hqr_kernel, or hqr1_kernel with DTN_HQR_FUSED)
+static bool hqrb_off() {
+  static const bool off = [] {
+    const char* e = std::getenv("DTN_HQR_BLOCKED");
+    return e && std::atoi(e) == 0;
+  }();
+  return off;
+}
+
 cudaError_t struct_init() {
+  for (auto f : {hqrb_kernel<true>, hqrb_kernel<false>}) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, HQRB_SMEM_MAX);
+    if (e != cudaSuccess) return e;
+  }
+  {
+    cudaError_t e = cudaFuncSetAttribute(hqrb_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
   for (auto f : {hqr1_kernel<true, true>, hqr1_kernel<false, true>, hqr1_kernel<true, false>}) {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
@@ -797,6 +1258,21 @@ cudaError_t launch_hqr(const QrDesc* d_descs, int count, int max_m, int max_nc, 
     if (!sm) return cudaLaunchKernelEx(&cfg, hqr_kernel<true, false, true>, d_descs, d_eps, C);
     if (C > 1) return cudaLaunchKernelEx(&cfg, hqr_kernel<true, true, true>, d_descs, d_eps, C);
     return cudaLaunchKernelEx(&cfg, hqr_kernel<false, true, true>, d_descs, d_eps, C);
+  }
+  if (!hqrb_off()) {
+    int Cb = 1;
+    HqrbSmem Lb;
+    if (hqrb_shape(count, max_m, max_nc, &Cb, &Lb)) {
+      cfg.gridDim = dim3(count * Cb);
+      // >= 120 KB: one CTA per SM (two co-resident clusters would share the SMs' issue slots)
+      cfg.dynamicSmemBytes = std::max<size_t>(size_t(Lb.total()) * 8, HQRB_SMEM_MIN);
+      attr[0].val.clusterDim.x = Cb;
+      cfg.numAttrs = Cb > 1 ? 1 : 0;
+      if (std::getenv("DTN_DEBUG_QR"))
+        std::fprintf(stderr, "hqrb: cluster %d rmax %d smem %lld\n", Cb, Lb.rmax, Lb.total() * 8);
+      if (Cb > 1) return cudaLaunchKernelEx(&cfg, hqrb_kernel<true>, d_descs, d_eps, Cb, Lb);
+      return cudaLaunchKernelEx(&cfg, hqrb_kernel<false>, d_descs, d_eps, Cb, Lb);
+    }
   }
   if (hqr_legacy()) {
     if (!sm) return cudaLaunchKernelEx(&cfg, hqr_kernel<true, false>, d_descs, d_eps, C);

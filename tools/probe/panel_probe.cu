@@ -7,7 +7,23 @@
 #include <random>
 using namespace dtnb;
 int main() {
-  blocked_init();
+  {
+    cudaFuncAttributes fb;
+    printf("getattr panel2<true,1>: %s\n", cudaGetErrorString(cudaFuncGetAttributes(&fb, panel2_kernel<true, 1>)));
+    printf("  regs %d\n", fb.numRegs);
+    printf("set nonport panel2<true,1>: %s\n", cudaGetErrorString(cudaFuncSetAttribute(panel2_kernel<true, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)));
+    printf("set nonport panel2<true,2>: %s\n", cudaGetErrorString(cudaFuncSetAttribute(panel2_kernel<true, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)));
+    printf("set dyn panel2<false,1>: %s\n", cudaGetErrorString(cudaFuncSetAttribute(panel2_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(panel_dyn_smem(1)))));
+    cudaError_t e = blocked_init();
+    printf("blocked_init: %s\n", cudaGetErrorString(e));
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, panel2_kernel<false, 1>);
+    printf("panel2<false,1>: regs %d static smem %zu max dyn %d maxthreads %d\n", fa.numRegs, fa.sharedSizeBytes,
+           fa.maxDynamicSharedSizeBytes, fa.maxThreadsPerBlock);
+    cudaFuncGetAttributes(&fa, panel_kernel<false, 1>);
+    printf("panel<false,1>: regs %d static smem %zu max dyn %d maxthreads %d\n", fa.numRegs, fa.sharedSizeBytes,
+           fa.maxDynamicSharedSizeBytes, fa.maxThreadsPerBlock);
+  }
   for (int kbv : {32})
   for (int rows : {256, 512, 1024, 2048, 4096}) {
     const int n = rows, ld = (n + 7) / 8 * 8;
@@ -77,6 +93,8 @@ int main() {
     }
     int piv[32]; cudaMemcpy(piv, dp, sizeof(piv), cudaMemcpyDeviceToHost);
     int moved = 0; for (int i = 0; i < 32; ++i) moved += piv[i] != i;
+    { long long q[16]; cudaMemcpyFromSymbol(q, g_p2_clk, sizeof(q));
+      printf("  p2 clk: load %lld save %lld topLU %lld ubsync %lld subst %lld check %lld final %lld tail %lld\n", q[1]-q[0], q[2]-q[1], q[3]-q[2], q[4]-q[3], q[5]-q[4], q[6]-q[5], q[7]-q[6], q[8]-q[7]); }
     long long pc[8]; cudaMemcpyFromSymbol(pc, g_pro_clk, sizeof(pc));
     printf("diag-dominant rows %5d: best %.1f us (rows moved %d) %s | start->save %lld topLU %lld subst %lld check %lld\n", n, best * 1e3, moved,
            cudaGetErrorString(cudaGetLastError()), pc[4] - pc[3], pc[5] - pc[4], pc[6] - pc[5], pc[7] - pc[6]);
@@ -111,6 +129,8 @@ int main() {
         float ms; cudaEventElapsedTime(&ms, e0, e1);
         if (r >= 2) best = ms < best ? ms : best;
       }
+      { long long q[16]; cudaMemcpyFromSymbol(q, g_p2_clk, sizeof(q));
+        printf("  p2 clk: load+prologue %lld save %lld topLU %lld ubsync %lld subst %lld check %lld final %lld tail %lld\n", q[1]-q[0], q[2]-q[1], q[3]-q[2], q[4]-q[3], q[5]-q[4], q[6]-q[5], q[7]-q[6], q[8]-q[7]); }
       long long pc[8];
       cudaMemcpyFromSymbol(pc, g_pro_clk, sizeof(pc));
       printf("rows %5d panel(k0=32) fused=%d%s: best %.1f us  prologue clk: loads %lld solve %lld update %lld | save %lld topLU %lld subst %lld check %lld\n", n,
