@@ -42,6 +42,7 @@ cudaError_t launch_trsm_upper_batched(const void*, int, int, cudaStream_t);
 cudaError_t launch_trsm_batched(const void*, int, int, int, bool, cudaStream_t);
 cudaError_t launch_block_identity(double*, int, cudaStream_t);
 unsigned panel_fallbacks_read_reset();
+unsigned small_fallbacks_read_reset();
 cudaError_t launch_ring_dtn(const double*, int, const int*, const double*, int, double, double*, long long, cudaStream_t);
 cudaError_t launch_trsm_upper_ref(const void*, int, int, cudaStream_t);
 cudaError_t launch_gemm_desc(const GemmDesc*, int, int, int, double, double, cudaStream_t, bool, bool allow_big = true);
@@ -1829,7 +1830,8 @@ int build_impl(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts,
       // DTN_PROF_DUMP=1: the launch timeline on stderr (wave, class, start, duration)
       const char* dump = std::getenv("DTN_PROF_DUMP");
       if (dump && dump[0] == '1') {
-        std::fprintf(stderr, "prof panel fallbacks %u\n", panel_fallbacks_read_reset());
+        std::fprintf(stderr, "prof panel fallbacks %u small fallbacks %u\n", panel_fallbacks_read_reset(),
+                     small_fallbacks_read_reset());
         // per wave: blocked merges whose panels needed row interchanges
         for (size_t w = 0; w < P.waves.size(); ++w) {
           int cnt = 0, tot = 0;

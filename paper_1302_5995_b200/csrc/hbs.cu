@@ -126,6 +126,7 @@ cudaError_t launch_hqr(const QrDesc* d_descs, int count, int max_m, int max_nc, 
                        bool pivoted);
 cudaError_t launch_fill_uniform(double* X, int ldx, int rows, int cols, unsigned long long seed, cudaStream_t st);
 cudaError_t launch_copy2d_batched(const void* d_descs, int count, cudaStream_t st);
+cudaError_t launch_sum_slices(double* base, long long stride, int slices, long long count, cudaStream_t st);
 
 // kernel launches issued by the HBS code (compress, invert, apply), process-wide
 std::atomic<unsigned long long> g_hbs_launches{0};
@@ -529,34 +530,47 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
       //    column space and |R_ii| reveals its eps-rank (#{|R_ii| > eps |R_00|}, the
       //    same relative cut as svd_rank's sigma_i > eps sigma_0).
       int lmax = 0;
-      size_t ysum = 0;
-      std::vector<size_t> yoff(na);
-      for (int a = 0; a < na; ++a) {
-        const int s = ssize[slots[act[a]]];
-        const int l = int(std::min<int64_t>(nX, s + 16));
-        lmax = std::max(lmax, l);
-        yoff[a] = ysum;
-        ysum += 2 * size_t(align2(s)) * size_t(l);
-      }
+      for (int a = 0; a < na; ++a) lmax = std::max(lmax, int(std::min<int64_t>(nX, ssize[slots[act[a]]] + 16)));
       double* Om = static_cast<double*>(scr.get(8, (size_t(ldX) * lmax + 2) * 8));
-      double* Yb = static_cast<double*>(scr.get(9, (ysum + 2) * 8));
       double* qst = static_cast<double*>(scr.get(10, (4 * size_t(na) + 2) * 8));
       double* d_eps = qst + 4 * size_t(na);
       HLK(launch_fill_uniform(Om, int(ldX), int(nX), lmax, 0x5eed + r, st));
       HCK(cudaMemcpyAsync(d_eps, &eps, sizeof(double), cudaMemcpyHostToDevice, st));
+      // The active nodes' block rows are row slices of X (block columns: of XT), all
+      // sketched by the same Omega: per side ONE product Y = X Omega (nX x lmax, node a
+      // uses its first l_a columns), split along K so the long reductions (K = nX) fill
+      // the GPU, the K-slices summed afterwards.
+      const int64_t ldY = align2(nX);
+      const size_t side_sz = size_t(ldY) * lmax, slab = 2 * side_sz;
+      const int tiles = std::max(1, gemm_tiles(int(nX), lmax));  // (nX = 0: every block row is zero)
+      int S = std::max(1, std::min<int>(16, (4 * 148 + 2 * tiles - 1) / (2 * tiles)));
+      while (S > 1 && nX / S < 256) --S;
+      double* Yb = static_cast<double*>(scr.get(9, (size_t(S) * slab + 2) * 8));
       std::vector<GemmDesc> g;
+      {
+        const int64_t kc = ((nX + S - 1) / S + 15) / 16 * 16;  // slice boundaries 16-aligned (B columns)
+        int sl = 0;
+        for (int64_t k0 = 0; k0 < nX; k0 += kc, ++sl) {
+          const int kk = int(std::min<int64_t>(kc, nX - k0));
+          for (int side = 0; side < 2; ++side)
+            g.push_back(GemmDesc{(side ? XT : X) + k0 * ldX, Om + k0, Yb + sl * slab + side * side_sz, int(nX), lmax,
+                                 kk, int(ldX), int(ldX), int(ldY)});
+        }
+        S = sl;
+      }
+      if (lmax > 0) {
+        gemm_batch(dbuf, g, 1.0, 0.0, true, st);
+        if (S > 1) HLK(launch_sum_slices(Yb, (long long)slab, S, (long long)slab, st));
+      }
       std::vector<QrDesc> q;
       for (int a = 0; a < na; ++a) {
-        const int i = act[a], s = ssize[slots[i]], ld = int(align2(s));
+        const int i = act[a], s = ssize[slots[i]];
         const int l = int(std::min<int64_t>(nX, s + 16)), nq = std::min(s, l);
-        double* y0 = Yb + yoff[a];
-        double* y1 = y0 + size_t(ld) * l;
-        g.push_back(GemmDesc{X + off[i], Om, y0, s, l, int(nX), int(ldX), int(ldX), ld});
-        g.push_back(GemmDesc{XT + off[i], Om, y1, s, l, int(nX), int(ldX), int(ldX), ld});
-        q.push_back(QrDesc{y0, UF(0, a), qst + 4 * a, nullptr, ld, ld, s, nq, l - nq, 0, 0, 0});
-        q.push_back(QrDesc{y1, UF(1, a), qst + 4 * a + 2, nullptr, ld, ld, s, nq, l - nq, 0, 0, 0});
+        double* y0 = Yb + off[i];
+        double* y1 = Yb + side_sz + off[i];
+        q.push_back(QrDesc{y0, UF(0, a), qst + 4 * a, nullptr, int(ldY), int(align2(s)), s, nq, l - nq, 0, 0, 0});
+        q.push_back(QrDesc{y1, UF(1, a), qst + 4 * a + 2, nullptr, int(ldY), int(align2(s)), s, nq, l - nq, 0, 0, 0});
       }
-      gemm_batch(dbuf, g, 1.0, 0.0, false, st);
       QrDesc* dq = upload(dbuf, q, st);
       HLK(launch_hqr(dq, int(q.size()), smax, lmax, d_eps, st, true));
       std::vector<double> hq(4 * size_t(na));

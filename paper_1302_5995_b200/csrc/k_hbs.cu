@@ -464,6 +464,22 @@ __global__ void add_blocks_kernel(const AddDesc* __restrict__ descs) {
   }
 }
 
+// base[e] = sum_{s < slices} base[e + s stride], e < count (the K-slices of a split product)
+__global__ void __launch_bounds__(256) sum_slices_kernel(double* base, long long stride, int slices, long long count) {
+  for (long long e = blockIdx.x * 256LL + threadIdx.x; e < count; e += (long long)gridDim.x * 256) {
+    double t = base[e];
+    for (int q = 1; q < slices; ++q) t += base[e + q * stride];
+    base[e] = t;
+  }
+}
+
+cudaError_t launch_sum_slices(double* base, long long stride, int slices, long long count, cudaStream_t st) {
+  if (count <= 0 || slices <= 1) return cudaSuccess;
+  const long long blocks = std::min<long long>((count + 255) / 256, 148 * 8);
+  sum_slices_kernel<<<unsigned(blocks), 256, 0, st>>>(base, stride, slices, count);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_add_blocks(const AddDesc* d_descs, int count, cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
   add_blocks_kernel<<<dim3(32, count), 256, 0, st>>>(d_descs);

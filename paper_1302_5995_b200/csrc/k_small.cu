@@ -18,6 +18,14 @@
 
 namespace dtnb {
 
+__device__ unsigned g_small_fallbacks;  // small systems whose no-interchange attempt failed (diagnostic)
+unsigned small_fallbacks_read_reset() {
+  unsigned h = 0, z = 0;
+  cudaMemcpyFromSymbol(&h, g_small_fallbacks, sizeof(h));
+  cudaMemcpyToSymbol(g_small_fallbacks, &z, sizeof(z));
+  return h;
+}
+
 template <int TR, int TC, int RPT, int CPT, bool MICRO>
 __global__ void __launch_bounds__(TR * TC) small_elim_kernel(KernelArgs args, const int* __restrict__ list) {
   constexpr int MAXT = (TR * RPT > TC * CPT) ? TR * RPT : TC * CPT;
@@ -146,24 +154,33 @@ __global__ void __launch_bounds__(TR * TC) small_elim_kernel(KernelArgs args, co
       pmin = fmin(pmin, apv);
       pmax = (apv != apv) ? INFINITY : fmax(pmax, apv);
       const double rinv = 1.0 / pv;
+      // branch-free rank-1 update: rows <= k get l = 0 and columns <= k get u = 0, so
+      // every owned entry takes one unconditional FMA (the predicated form spent ~10
+      // instructions per entry; an FMA with a zero factor leaves finite entries unchanged)
+      double lr[RPT], ur[CPT];
 #pragma unroll
       for (int a = 0; a < RPT; ++a) {
         const int i = tr + TR * a;
-        if (i > k && i < total) {
-          const double l = ck[i] * rinv;
-          if (i < ni) ok &= fabs(l) <= 1.0;
-#pragma unroll
-          for (int b = 0; b < CPT; ++b) {
-            const int j = tc + TC * b;
-            if (j > k && j < ncol) m[a][b] = fma(-l, rp[j], m[a][b]);
-          }
-        }
+        const bool live = i > k && i < total;
+        const double l = live ? ck[i] * rinv : 0.0;
+        if (live && i < ni) ok &= fabs(l) <= 1.0;
+        lr[a] = -l;
       }
+#pragma unroll
+      for (int b = 0; b < CPT; ++b) {
+        const int j = tc + TC * b;
+        ur[b] = (j > k && j < ncol) ? rp[j] : 0.0;
+      }
+#pragma unroll
+      for (int a = 0; a < RPT; ++a)
+#pragma unroll
+        for (int b = 0; b < CPT; ++b) m[a][b] = fma(lr[a], ur[b], m[a][b]);
       if (k + 1 < ni) publish(k + 1, (k + 1) & 1);
       __syncthreads();
     }
   }
   const bool fast = __syncthreads_and(ok) != 0;
+  if (!fast && threadIdx.x == 0) atomicAdd(&g_small_fallbacks, 1u);
   if (!fast) {
     assemble();
     pmin = DBL_MAX;
@@ -225,18 +242,21 @@ __global__ void __launch_bounds__(TR * TC) small_elim_kernel(KernelArgs args, co
     pmax = (apv != apv) ? INFINITY : fmax(pmax, apv);
     __syncthreads();
     const double rinv = 1.0 / pv;
+    double lr[RPT], ur[CPT];  // branch-free update (see the no-interchange loop)
 #pragma unroll
     for (int a = 0; a < RPT; ++a) {
       const int i = tr + TR * a;
-      if (i < total && !((elim >> a) & 1u)) {
-        const double l = ck[i] * rinv;
-#pragma unroll
-        for (int b = 0; b < CPT; ++b) {
-          const int j = tc + TC * b;
-          if (j > k && j < ncol) m[a][b] = fma(-l, rowp[j], m[a][b]);
-        }
-      }
+      lr[a] = (i < total && !((elim >> a) & 1u)) ? -(ck[i] * rinv) : 0.0;
     }
+#pragma unroll
+    for (int b = 0; b < CPT; ++b) {
+      const int j = tc + TC * b;
+      ur[b] = (j > k && j < ncol) ? rowp[j] : 0.0;
+    }
+#pragma unroll
+    for (int a = 0; a < RPT; ++a)
+#pragma unroll
+      for (int b = 0; b < CPT; ++b) m[a][b] = fma(lr[a], ur[b], m[a][b]);
   }
 
   // ---- S = trailing block, written compact (ld = nd.ld)
@@ -259,9 +279,15 @@ __global__ void __launch_bounds__(TR * TC) small_elim_kernel(KernelArgs args, co
 }
 
 // Launch dispatch by the largest system in the batch.
+// (size classes fitted to the systems of the 16 x 16 / 32 x 32 leaf subtrees -- 16, 22,
+// 34, 50, 74, 120 unknowns: the kernel is issue bound, so padding entries cost time)
 #define DTNB_SMALL_VARIANTS(X) \
+  X(24, 8, 8, 3, 3)            \
   X(32, 8, 8, 4, 4)            \
+  X(40, 8, 8, 5, 5)            \
+  X(56, 8, 16, 7, 4)           \
   X(64, 16, 16, 4, 4)          \
+  X(80, 16, 16, 5, 5)          \
   X(96, 16, 16, 6, 6)          \
   X(128, 32, 32, 4, 4) /* 1024 threads: measured 0.5 % faster than 16 x 32 x (8, 4) */ \
   X(160, 16, 32, 10, 5)

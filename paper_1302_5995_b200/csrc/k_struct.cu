@@ -1077,6 +1077,219 @@ __global__ void __launch_bounds__(QR_THREADS) hqrb_kernel(const QrDesc* __restri
   if constexpr (CL) cg::this_cluster().sync();  // no CTA leaves while others may still read its shared memory
 }
 
+// ---------------------------------------------------------------------------
+constexpr int HP_THREADS = 1024, HP_WARPS = HP_THREADS / 32, HP_NG = HP_THREADS / QR_GL;
+// hqrp_kernel: the rank-revealing Householder QR with column pivoting of the HBS
+// compression (hqr_kernel<., ., PIV>'s reflectors, pivot rule and rank count), one
+// CTA per matrix in shared memory. Per column step: one block argmax over the
+// maintained trailing-column norms, the swap, the reflector (every warp forms it
+// from the same column, no barrier), then groups of 8 lanes own the trailing
+// columns: dot product, update and the EXACT new norm of rows > c in one pass (the
+// values are in registers while written: no norm recomputation sweep, no
+// downdating). Q is formed in place (dorg2r).
+__global__ void __launch_bounds__(HP_THREADS) hqrp_kernel(const QrDesc* __restrict__ descs, const double* eps_ptr) {
+  extern __shared__ __align__(16) double qdyn[];
+  __shared__ double nrm[QR_MAXN];
+  __shared__ double tau_s[QR_MAXN], rdiag[QR_MAXN];
+  __shared__ double wbest[HP_WARPS];
+  __shared__ int wj[HP_WARPS];
+  __shared__ int rank_s;
+  HCLK_T(tq0);
+  const QrDesc d = descs[blockIdx.x];
+  const int m = d.m, n = d.n, nc = d.n + d.p;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gl = tid & (QR_GL - 1), grp = tid / QR_GL;  // HP_NG groups of 8 lanes
+  const int ld = m | 1;
+  double* Y = qdyn;
+  for (int j = 0; j < nc; ++j)
+    for (int i = tid; i < m; i += HP_THREADS) Y[i + j * ld] = d.Y[i + (long long)j * d.ldy];
+  __syncthreads();
+  // initial column norms (rows >= 0)
+  for (int jb = 0; jb < nc; jb += HP_NG) {
+    const int j = jb + grp;
+    double s0 = 0.0;
+    if (j < nc)
+      for (int i = gl; i < m; i += QR_GL) s0 = fma(Y[i + j * ld], Y[i + j * ld], s0);
+#pragma unroll
+    for (int o = QR_GL / 2; o > 0; o >>= 1) s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    if (j < nc && gl == 0) nrm[j] = s0;
+  }
+  __syncthreads();
+  HCLK_ADD(7, tq0);
+  double scal_prev = 0.0, beta_prev = 0.0;
+  for (int c = 0; c < n; ++c) {
+    HCLK_T(tqa);
+    // (a) pivot: the largest remaining norm, lowest index on ties
+    {
+      double best = -1.0;
+      int bj = 0x7fffffff;
+      for (int j = c + tid; j < nc; j += HP_THREADS) {
+        const double v = nrm[j];
+        if (v > best) {
+          best = v;
+          bj = j;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+        if (ob > best || (ob == best && oj < bj)) {
+          best = ob;
+          bj = oj;
+        }
+      }
+      if (lane == 0) {
+        wbest[warp] = best;
+        wj[warp] = bj;
+      }
+      // the previous reflector column: [beta; v] (no CTA reads it in this step)
+      if (c > 0) {
+        double* yp = Y + (c - 1) * ld;
+        for (int i = c + tid; i < m; i += HP_THREADS) yp[i] *= scal_prev;
+        if (tid == 0 && c - 1 < m) yp[c - 1] = beta_prev;
+      }
+    }
+    __syncthreads();
+    int jm = wj[0];
+    {
+      double b = wbest[0];
+#pragma unroll
+      for (int w = 1; w < HP_WARPS; ++w)
+        if (wbest[w] > b || (wbest[w] == b && wj[w] < jm)) {
+          b = wbest[w];
+          jm = wj[w];
+        }
+    }
+    HCLK_ADD(8, tqa);
+    HCLK_T(tqb);
+    // (b) swap columns c <-> jm
+    if (jm != c) {
+      double* yc = Y + c * ld;
+      double* yj = Y + jm * ld;
+      for (int i = tid; i < m; i += HP_THREADS) {
+        const double t = yc[i];
+        yc[i] = yj[i];
+        yj[i] = t;
+      }
+    }
+    __syncthreads();
+    if (jm != c && tid == 0) {
+      const double t = nrm[c];
+      nrm[c] = nrm[jm];
+      nrm[jm] = t;
+    }
+    HCLK_ADD(9, tqb);
+    HCLK_T(tqc);
+    // (c) the reflector of column c, formed by every warp (identical sums)
+    const double* yc = Y + c * ld;
+    double ss = 0.0;
+    for (int i = c + 1 + lane; i < m; i += 32) ss = fma(yc[i], yc[i], ss);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const double alpha = c < m ? yc[c] : 0.0;
+    double beta, tc, scal;
+    if (ss == 0.0) {
+      beta = alpha;
+      tc = 0.0;
+      scal = 0.0;
+    } else {
+      beta = -copysign(sqrt(fma(alpha, alpha, ss)), alpha);
+      tc = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    if (tid == 0) {
+      tau_s[c] = tc;
+      rdiag[c] = beta;
+    }
+    // (d) trailing columns: v^T y_j = y_cj + scal sum_{i > c} x_i y_ij; update; new norms
+    for (int jb = c + 1; jb < nc; jb += HP_NG) {
+      const int j = jb + grp;
+      const bool live = j < nc;
+      double* yj = Y + (live ? j : c) * ld;
+      double s0 = 0.0;
+      if (live)
+        for (int i = c + 1 + gl; i < m; i += QR_GL) s0 = fma(yc[i], yj[i], s0);
+#pragma unroll
+      for (int o = QR_GL / 2; o > 0; o >>= 1) s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      double n2 = 0.0;
+      if (live) {
+        const double f = tc * fma(scal, s0, yj[c]);
+        const double g = f * scal;
+        for (int i = c + 1 + gl; i < m; i += QR_GL) {
+          const double y = fma(-g, yc[i], yj[i]);
+          yj[i] = y;
+          n2 = fma(y, y, n2);
+        }
+      }
+#pragma unroll
+      for (int o = QR_GL / 2; o > 0; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+      if (live && gl == 0) {
+        yj[c] -= tc * fma(scal, s0, yj[c]);
+        nrm[j] = n2;
+      }
+    }
+    scal_prev = scal;
+    beta_prev = beta;
+    __syncthreads();
+    HCLK_ADD(10, tqc);
+  }
+  HCLK_T(tqd);
+  if (n > 0) {
+    double* yp = Y + (n - 1) * ld;
+    for (int i = n + tid; i < m; i += HP_THREADS) yp[i] *= scal_prev;
+    if (tid == 0 && n - 1 < m) yp[n - 1] = beta_prev;
+  }
+  if (tid == 0) {
+    const double eps = *eps_ptr;
+    const double scale = n > 0 ? fabs(rdiag[0]) : 0.0;
+    int rk = 0;
+    for (int i = 0; i < n; ++i)
+      if (fabs(rdiag[i]) > eps * scale) ++rk;
+    rank_s = rk;
+    if (d.stat) {
+      d.stat[0] = double(rk);
+      d.stat[1] = 0.0;
+    }
+  }
+  __syncthreads();
+  const int nq = n;  // every column: the caller keeps max(rank of the rows side, of the columns side)
+  auto finish_col = [&](int c) {
+    double* y = Y + c * ld;
+    const double tc = tau_s[c];
+    for (int i = tid; i < m; i += HP_THREADS) y[i] = i < c ? 0.0 : (i == c ? 1.0 - tc : -tc * y[i]);
+  };
+  for (int c = nq - 1; c >= 0; --c) {
+    if (c + 1 < nq) {
+      finish_col(c + 1);
+      __syncthreads();
+    }
+    const double* yc = Y + c * ld;
+    const double tc = tau_s[c];
+    for (int jb = c + 1; jb < nq; jb += HP_NG) {
+      const int j = jb + grp;
+      const bool live = j < nq;
+      double* yj = Y + (live ? j : c) * ld;
+      double s0 = 0.0;
+      if (live)
+        for (int i = c + 1 + gl; i < m; i += QR_GL) s0 = fma(yc[i], yj[i], s0);
+#pragma unroll
+      for (int o = QR_GL / 2; o > 0; o >>= 1) s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      if (live && tc != 0.0) {
+        const double f = tc * s0;
+        if (gl == 0) yj[c] = -f;
+        for (int i = c + 1 + gl; i < m; i += QR_GL) yj[i] = fma(-f, yc[i], yj[i]);
+      }
+    }
+    __syncthreads();
+  }
+  if (nq > 0) finish_col(0);
+  __syncthreads();
+  HCLK_ADD(11, tqd);
+  for (int jj = 0; jj < nq; ++jj)
+    for (int i = tid; i < m; i += HP_THREADS) d.Q[i + (long long)jj * d.ldq] = Y[i + jj * ld];
+}
+
 // launch geometry of hqrb_kernel: the smallest cluster whose row blocks and work
 // buffers fit in shared memory, widened while the launch leaves SMs idle
 template <bool CL>
@@ -1203,7 +1416,20 @@ static bool hqrb_off() {
   return off;
 }
 
+// DTN_HQRP=0: the pivoted QR by hqr_kernel<., ., true>
+static bool hqrp_off() {
+  static const bool off = [] {
+    const char* e = std::getenv("DTN_HQRP");
+    return e && std::atoi(e) == 0;
+  }();
+  return off;
+}
+
 cudaError_t struct_init() {
+  {
+    cudaError_t e = cudaFuncSetAttribute(hqrp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+  }
   for (auto f : {hqrb_kernel<true>, hqrb_kernel<false>}) {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, HQRB_SMEM_MAX);
     if (e != cudaSuccess) return e;
@@ -1255,6 +1481,11 @@ cudaError_t launch_hqr(const QrDesc* d_descs, int count, int max_m, int max_nc, 
   cfg.attrs = attr;
   cfg.numAttrs = C > 1 ? 1 : 0;
   if (pivoted) {
+    if (C == 1 && sm && !hqrp_off()) {
+      cfg.dynamicSmemBytes = size_t(max_m | 1) * max_nc * 8;
+      cfg.blockDim = dim3(HP_THREADS);
+      return cudaLaunchKernelEx(&cfg, hqrp_kernel, d_descs, d_eps);
+    }
     if (!sm) return cudaLaunchKernelEx(&cfg, hqr_kernel<true, false, true>, d_descs, d_eps, C);
     if (C > 1) return cudaLaunchKernelEx(&cfg, hqr_kernel<true, true, true>, d_descs, d_eps, C);
     return cudaLaunchKernelEx(&cfg, hqr_kernel<false, true, true>, d_descs, d_eps, C);

@@ -27,8 +27,10 @@ int main(int argc, char** argv) {
       cudaError_t e = cudaOccupancyMaxActiveClusters(&nclus, C > 1 ? (void*)hqrb_kernel<true> : (void*)hqrb_kernel<false>, &cfg);
       printf("cluster %2d smem %3d KB: max active clusters %d (%s)\n", C, kb, nclus, cudaGetErrorString(e));
     }
-  const int shapes[][4] = {{64, 254, 64, 4}, {16, 510, 152, 4}, {8, 510, 152, 4}, {4, 1022, 80, 4}};
-  for (auto& sh : shapes) {
+  const bool piv = getenv("PIV") != nullptr;
+  const int shapes_t[][4] = {{64, 254, 64, 4}, {16, 510, 152, 4}, {8, 510, 152, 4}, {4, 1022, 80, 4}};
+  const int shapes_p[][4] = {{128, 64, 64, 16}, {64, 49, 49, 16}, {8, 73, 73, 16}, {4, 89, 89, 16}};
+  for (auto& sh : piv ? shapes_p : shapes_t) {
     const int count = sh[0], m = sh[1], n = sh[2], p = sh[3], nc = n + p, ld = m + 2;
     std::vector<double> hY(size_t(ld) * nc * count);
     std::mt19937_64 rng(7);
@@ -65,7 +67,7 @@ int main(int argc, char** argv) {
       for (int r = 0; r < 5; ++r) {
         cudaMemcpy(dY, dY0, hY.size() * 8, cudaMemcpyDeviceToDevice);
         cudaEventRecord(e0);
-        cudaError_t err = launch_hqr(dd, count, m, nc, deps, 0, false);
+        cudaError_t err = launch_hqr(dd, count, m, nc, deps, 0, piv);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         if (err != cudaSuccess || cudaGetLastError() != cudaSuccess) {
@@ -102,7 +104,7 @@ int main(int argc, char** argv) {
 #ifdef HQRB_PROFILE
       cudaMemcpy(dY, dY0, hY.size() * 8, cudaMemcpyDeviceToDevice);
       { long long z[16] = {0}; cudaMemcpyToSymbol(g_hqrb_clk, z, sizeof(z)); }
-      launch_hqr(dd, count, m, nc, deps, 0, false);
+      launch_hqr(dd, count, m, nc, deps, 0, piv);
       cudaDeviceSynchronize();
       long long h[16];
       cudaMemcpyFromSymbol(h, g_hqrb_clk, sizeof(h));
@@ -117,8 +119,8 @@ int main(int argc, char** argv) {
         std::vector<unsigned long long> z(2 * 2048, 0);
         cudaMemcpyToSymbol(g_hqrb_t, z.data(), z.size() * 8);
       }
-      printf("   clk: panel-steps %lld  W+reduce %lld  dlarft %lld  update %lld  probe %lld  Q %lld\n", h[1], h[2], h[3], h[4],
-             h[5], h[6]);
+      printf("   clk: panel-steps %lld  W+reduce %lld  dlarft %lld  update %lld  probe %lld  Q %lld | piv: load %lld argmax %lld swap %lld refl+upd %lld Q %lld\n", h[1], h[2], h[3], h[4],
+             h[5], h[6], h[7], h[8], h[9], h[10], h[11]);
 #endif
     }
   }
