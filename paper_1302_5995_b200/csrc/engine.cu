@@ -2727,8 +2727,8 @@ int dtn_gpu_build_accel(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* o
       cudaStream_t st = ctx->stream;
       CK(cudaMemcpyAsync(d, ones.data(), size_t(m) * 8, cudaMemcpyHostToDevice, st));
       // both products enqueued back to back, one copy back, one synchronisation
-      hbs_apply(*Sh->h, d, m, 1, d + m, m, st);
-      hbs_apply(*Gh->h, d, m, 1, d + 2 * m, m, st);
+      hbs_apply(*Sh->h, d, m, 1, d + m, m, st, false);
+      hbs_apply(*Gh->h, d, m, 1, d + 2 * m, m, st, false);
       CK(cudaMemcpyAsync(y.data(), d + m, size_t(m) * 16, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       double nrm[2];

@@ -147,21 +147,32 @@ namespace {
 
 inline int64_t align2(int64_t x) { return (x + 1) & ~int64_t(1); }
 
-struct DevBuf {  // growable device scratch
-  void* p = nullptr;
-  size_t cap = 0;
+// Device scratch for descriptors and staging: every get() is a FRESH region (a bump
+// allocator over pooled chunks), never reused while the owning call runs, so a launch
+// never waits for the previous one to have read its descriptors (no synchronisation
+// between batches). The owner synchronises its stream before the chunks return to the
+// pool (every user ends with a stream synchronisation).
+struct DevBuf {
+  std::vector<void*> chunks;
+  char* cur = nullptr;
+  size_t cap = 0, off = 0;
   ~DevBuf() {
-    if (p) pool_free(p);
+    for (void* c : chunks) pool_free(c);
   }
   void* get(size_t bytes) {
-    if (bytes > cap) {
-      if (p) pool_free(p);
-      p = nullptr;
-      cap = 0;
-      pmalloc(&p, std::max<size_t>(bytes, 256));
-      cap = std::max<size_t>(bytes, 256);
+    bytes = (std::max<size_t>(bytes, 1) + 255) & ~size_t(255);
+    if (!cur || off + bytes > cap) {
+      const size_t c = std::max<size_t>(bytes, size_t(1) << 20);
+      void* q = nullptr;
+      pmalloc(&q, c);
+      chunks.push_back(q);
+      cur = static_cast<char*>(q);
+      cap = c;
+      off = 0;
     }
-    return p;
+    void* r = cur + off;
+    off += bytes;
+    return r;
   }
 };
 
@@ -185,8 +196,6 @@ void gemm_batch(DevBuf& buf, const std::vector<GemmDesc>& g, double alpha, doubl
   if (tiles == 0) return;
   GemmDesc* dd = upload(buf, g, st);
   HLK(launch_gemm_desc(dd, int(g.size()), tiles, kmax, alpha, beta, st, a_aligned));
-  // the descriptor buffer is reused by the next batch: keep the upload ordered
-  HCK(cudaStreamSynchronize(st));
 }
 
 void transpose_batch(DevBuf& buf, const std::vector<TransDesc>& t, cudaStream_t st) {
@@ -195,7 +204,6 @@ void transpose_batch(DevBuf& buf, const std::vector<TransDesc>& t, cudaStream_t 
   for (const auto& d : t) tiles = std::max(tiles, ((d.m + 31) / 32) * ((d.n + 31) / 32));
   TransDesc* dd = upload(buf, t, st);
   HLK(launch_transpose_batched(dd, int(t.size()), tiles, st));
-  HCK(cudaStreamSynchronize(st));
 }
 
 void copy_batch(DevBuf& buf, const std::vector<CopyDesc>& c, cudaStream_t st) {
@@ -214,7 +222,6 @@ void copy_batch(DevBuf& buf, const std::vector<CopyDesc>& c, cudaStream_t st) {
     CopyDesc* dd = upload(buf, small, st);
     HLK(launch_copy2d_batched(dd, int(small.size()), st));
   }
-  HCK(cudaStreamSynchronize(st));
 }
 
 // Grow-only device scratch of the compression (the M x M work matrices are
@@ -387,6 +394,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
     H.buffers.push_back(d);
     H.D[0] = d;
     copy_batch(dbuf, {CopyDesc{dH, d, int(ldh), H.ld(0), int(M), int(M)}}, st);
+    HCK(cudaStreamSynchronize(st));
     return out;
   }
 
@@ -490,7 +498,6 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
       copy_batch(dbuf, cp, st);
       ZeroDesc* dz = upload(dbuf, zd, st);
       HLK(launch_zero_blocks(dz, int(zd.size()), st));
-      HCK(cudaStreamSynchronize(st));
     }
     tr.mark("diag");
     // 2. XT = X^T
@@ -710,7 +717,6 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
       if (!gd.empty()) {
         GatherDesc* dg = upload(dbuf, gd, st);
         HLK(launch_gather_cols(dg, int(gd.size()), st));
-        HCK(cudaStreamSynchronize(st));
       }
     }
     tr.mark("gather");
@@ -763,6 +769,7 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
     nX = nX2;
     ldX = ldX2;
   }
+  HCK(cudaStreamSynchronize(st));  // before the scratch and descriptor chunks return to the pool
   return out;
 }
 
@@ -873,7 +880,8 @@ void pack_for_apply(HbsDev& H, cudaStream_t st) {
 
 // One upload of every descriptor of the call, then the whole sweep as a
 // chain of batched launches on the stream with no host synchronisation.
-void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* dY, int64_t ldy, cudaStream_t st) {
+void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* dY, int64_t ldy, cudaStream_t st,
+               bool allow_graph) {
   if (nrhs <= 0) return;
   const int nn = int(H.nodes.size());
   DevBuf dbuf;
@@ -885,6 +893,7 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
     copy_batch(dbuf, {CopyDesc{dX, xs, int(ldx), int(ld), int(M), int(nrhs)}}, st);
     gemm_batch(dbuf, {GemmDesc{H.D[0], xs, dY, int(M), int(nrhs), int(M), H.ld(0), int(ld), int(ldy)}}, 1.0, 0.0,
                true, st);
+    HCK(cudaStreamSynchronize(st));  // before the staging and descriptors return to the pool
     pool_free(xs);
     return;
   }
@@ -1022,7 +1031,7 @@ void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* d
   // the launch sequence depends only on the tree, the ranks and nrhs: replay it as a
   // graph (one launch instead of ~16) once captured for this batch size
   static const bool graphs = std::getenv("DTN_HBS_NO_GRAPH") == nullptr;
-  if (graphs && st != nullptr) {
+  if (graphs && allow_graph && st != nullptr) {
     if (!(H.apply_graph && H.apply_graph_nrhs == nrhs && H.apply_graph_desc == H.d_desc)) {
       if (H.apply_graph) cudaGraphExecDestroy(H.apply_graph);
       H.apply_graph = nullptr;
@@ -1363,39 +1372,57 @@ std::unique_ptr<HbsDev> hbs_invert(const HbsDev& H, cudaStream_t st) {
     return work_buf;
   };
   int* dinfo = nullptr;
-  pmalloc(&dinfo, size_t(nn) * sizeof(int) + 16);
+  pmalloc(&dinfo, 2 * size_t(nn) * sizeof(int) + 16);  // every node inverts at most two blocks
   frees.v.push_back(dinfo);
   auto where = [&](int t) {
     return "node " + std::to_string(t) + " level " + std::to_string(H.nodes[t].level);
   };
-  // batched in-place inverses; throws on the singular block with the lowest node id
+  // batched in-place inverses, their singularity flags checked once at the end (no
+  // synchronisation per level): the error names the first failing batch in program
+  // order and its singular block with the lowest node id, as a per-batch check would
+  struct InvCall {
+    std::vector<int> nodes;
+    size_t slot0;
+    const char* what;
+  };
+  std::vector<InvCall> calls;
+  size_t nslots = 0;
   auto invert = [&](const std::vector<std::pair<int, InvDesc>>& blocks, const char* what) {
     if (blocks.empty()) return;
     std::vector<InvDesc> v;
     int smax = 0;
+    InvCall call{{}, nslots, what};
     for (size_t i = 0; i < blocks.size(); ++i) {
       InvDesc d = blocks[i].second;
-      d.info = dinfo + i;
+      d.info = dinfo + nslots + i;
       v.push_back(d);
       smax = std::max(smax, d.s);
+      call.nodes.push_back(blocks[i].first);
     }
+    nslots += blocks.size();
+    calls.push_back(std::move(call));
     InvDesc* dv = upload(ibuf, v, st);
     HLK(launch_gj_inverse(dv, int(v.size()), smax, st));
-    std::vector<int> info(v.size());
-    HCK(cudaMemcpyAsync(info.data(), dinfo, info.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
+  };
+  auto check_singular = [&]() {
+    std::vector<int> info(nslots);
+    if (nslots) HCK(cudaMemcpyAsync(info.data(), dinfo, nslots * sizeof(int), cudaMemcpyDeviceToHost, st));
     HCK(cudaStreamSynchronize(st));
-    int bad = -1;
-    for (size_t i = 0; i < info.size(); ++i)
-      if (info[i] != 0 && (bad < 0 || blocks[i].first < bad)) bad = blocks[i].first;
-    if (bad >= 0) throw HbsSingular(std::string(what) + " is singular [" + where(bad) + "]");
+    for (const InvCall& c : calls) {
+      int bad = -1;
+      for (size_t i = 0; i < c.nodes.size(); ++i)
+        if (info[c.slot0 + i] != 0 && (bad < 0 || c.nodes[i] < bad)) bad = c.nodes[i];
+      if (bad >= 0) throw HbsSingular(std::string(c.what) + " is singular [" + where(bad) + "]");
+    }
   };
 
   if (nn == 1) {  // hbs_ops.cpp:157-160
     const int s = int(H.M), ld = H.ld(0);
     R.D[0] = dalloc(size_t(ld) * s, true);
     copy_batch(dbuf, {CopyDesc{H.D[0], R.D[0], ld, ld, s, s}}, st);
+    invert({{0, InvDesc{R.D[0], nullptr, s, ld}}}, "D");
     try {
-      invert({{0, InvDesc{R.D[0], nullptr, s, ld}}}, "D");
+      check_singular();
     } catch (const HbsSingular&) {
       throw HbsSingular("D is singular [root leaf]");
     }
@@ -1476,7 +1503,6 @@ std::unique_ptr<HbsDev> hbs_invert(const HbsDev& H, cudaStream_t st) {
       if (!a.empty()) {
         AddDesc* da = upload(dbuf, a, st);
         HLK(launch_add_blocks(da, int(a.size()), st));
-        HCK(cudaStreamSynchronize(st));
       }
     }
     // 2. Dinv (at the root: the core inverse, hbs_ops.cpp:177-180)
@@ -1554,6 +1580,7 @@ std::unique_ptr<HbsDev> hbs_invert(const HbsDev& H, cudaStream_t st) {
       gemm_batch(dbuf, gu, -1.0, 1.0, true, st);
     }
   }
+  check_singular();  // (synchronises the stream)
   return out;
 }
 

@@ -141,7 +141,10 @@ std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, d
 
 // Y (M x nrhs) = H X through the telescoping factorization (hbs.cpp:187-232);
 // X, Y device pointers.
-void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* dY, int64_t ldy, cudaStream_t st);
+// allow_graph = false: launch the sweep directly (one-off applies: capturing and
+// instantiating the per-batch-size graph costs more than it saves)
+void hbs_apply(HbsDev& H, const double* dX, int64_t ldx, int64_t nrhs, double* dY, int64_t ldy, cudaStream_t st,
+               bool allow_graph = true);
 
 // A singular block met by hbs_invert: what() = "<what> [node t level l]"
 // (FactorizationError, errors.hpp:11-21); the C ABI maps it to DTN_ESINGULAR.
