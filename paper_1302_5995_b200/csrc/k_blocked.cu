@@ -15,6 +15,7 @@
 #include <cfloat>
 #include <cstdlib>
 #include <initializer_list>
+#include <type_traits>
 
 #include <cooperative_groups.h>
 
@@ -758,6 +759,22 @@ __device__ __forceinline__ void shift_update(double (&w)[PKB], double l, const d
   w[PKB - 1] = 0.0;
 }
 
+// the same step on a window of W live entries (steps j >= 32 - W: columns past the
+// panel are zero, so only w[0 .. W) can change)
+template <int W>
+__device__ __forceinline__ void shift_update_w(double (&w)[PKB], double l, const double* __restrict__ prow) {
+  const double2* p2 = reinterpret_cast<const double2*>(prow);
+#pragma unroll
+  for (int c2 = 0; c2 < W / 2; ++c2) {
+    const double2 u = p2[c2];
+    if (c2 > 0) w[2 * c2 - 1] = fma(-l, u.x, w[2 * c2]);
+    w[2 * c2] = fma(-l, u.y, w[2 * c2 + 1]);
+  }
+  w[W - 1] = 0.0;
+}
+template <int W>
+using WinC = std::integral_constant<int, W>;
+
 template <bool CL, int RPT>
 __global__ void __launch_bounds__(PNT) panel2_kernel(KernelArgs args, const int* __restrict__ list, int k0, int kb,
                                                     int csize, int fused, int use_fast) {
@@ -923,21 +940,34 @@ __global__ void __launch_bounds__(PNT) panel2_kernel(KernelArgs args, const int*
     int jf = PKB;
     P2CLK(2);
     if (crank == 0 && warp == 0) {  // rows 0..kbe-1 in lanes 0..kbe-1 (a = 0)
-      for (int j = 0; j < kbe; ++j) {
-        if (lane == j) {
+      // steps in chunks of 8 on a window narrowing by 8 (32, 24, 16, 8 live entries);
+      // every lane forms the reciprocal of its next pivot candidate as soon as its
+      // window's first entry is updated (lane j + 1's is the next pivot's)
+      double rnext = __drcp_rn(v[0][0]);
+      auto chunk = [&](auto Wc) {
+        constexpr int W = decltype(Wc)::value;
+        const int j0 = PKB - W, j1 = min(kbe, j0 + 8);
+        for (int j = j0; j < j1; ++j) {
+          if (lane == j) {
 #pragma unroll
-          for (int c = 0; c < PKB; c += 2)
-            *reinterpret_cast<double2*>(ub + j * PLD + c) = make_double2(v[0][c], v[0][c + 1]);
-          urinv[j] = __drcp_rn(v[0][0]);
+            for (int c = 0; c < W; c += 2)
+              *reinterpret_cast<double2*>(ub + j * PLD + c) = make_double2(v[0][c], v[0][c + 1]);
+            urinv[j] = rnext;
+          }
+          __syncwarp();
+          if (lane > j && lane < kbe) {
+            const double l = v[0][0] * urinv[j];
+            if (!(fabs(l) <= 1.0) && jf == PKB) jf = j;
+            M[lane + (long long)j * ldm] = l;
+            shift_update_w<W>(v[0], l, ub + j * PLD);
+            rnext = __drcp_rn(v[0][0]);
+          }
         }
-        __syncwarp();
-        if (lane > j && lane < kbe) {
-          const double l = v[0][0] * urinv[j];
-          if (!(fabs(l) <= 1.0) && jf == PKB) jf = j;
-          M[lane + (long long)j * ldm] = l;
-          shift_update(v[0], l, ub + j * PLD);
-        }
-      }
+      };
+      chunk(WinC<32>{});
+      chunk(WinC<24>{});
+      chunk(WinC<16>{});
+      chunk(WinC<8>{});
       for (int j = kbe + lane; j < PKB; j += 32) {  // rows past the panel: zero U rows
 #pragma unroll 4
         for (int c = 0; c < PLD; ++c) ub[j * PLD + c] = 0.0;
@@ -959,18 +989,26 @@ __global__ void __launch_bounds__(PNT) panel2_kernel(KernelArgs args, const int*
     __syncthreads();
     const int jtop = jtop_s;
     auto subst = [&](int rlo, int jmax, bool track) {
-      for (int j = 0; j < jmax; ++j) {
+      auto chunk = [&](auto Wc) {
+        constexpr int W = decltype(Wc)::value;
+        const int j0 = PKB - W, j1 = min(jmax, j0 + 8);
+        for (int j = j0; j < j1; ++j) {
 #pragma unroll
-        for (int a = 0; a < RPT; ++a) {
-          const int r = crank * PNT + tid + stride * a;
-          if (r >= rlo && r < Ri) {
-            const double l = v[a][0] * urinv[j];
-            if (track && !(fabs(l) <= 1.0) && jf == PKB) jf = j;
-            M[r + (long long)j * ldm] = l;
-            shift_update(v[a], l, ub + j * PLD);
+          for (int a = 0; a < RPT; ++a) {
+            const int r = crank * PNT + tid + stride * a;
+            if (r >= rlo && r < Ri) {
+              const double l = v[a][0] * urinv[j];
+              if (track && !(fabs(l) <= 1.0) && jf == PKB) jf = j;
+              M[r + (long long)j * ldm] = l;
+              shift_update_w<W>(v[a], l, ub + j * PLD);
+            }
           }
         }
-      }
+      };
+      chunk(WinC<32>{});
+      chunk(WinC<24>{});
+      chunk(WinC<16>{});
+      chunk(WinC<8>{});
     };
     P2CLK(4);
     subst(kbe, min(kbe, jtop), true);
@@ -1368,12 +1406,23 @@ cudaError_t launch_gather(const KernelArgs& args, const int* d_list, int count, 
 // Panel geometry for systems with up to max_rows rows below k0 (kb <= 32):
 // one row per thread up to 16 CTAs x 256 rows, two rows per thread beyond
 // (clusters of up to 16 CTAs, 8192 rows).
+// DTN_PANEL_ONECTA2=1: systems of 257..512 rows on ONE CTA with 2 rows per thread
+// (the pivoted loop's cheapest exchange) instead of a 2-CTA cluster (half the
+// prologue update and substitution per CTA: the no-interchange path's cost)
+static bool panel_onecta2() {
+  static const bool on = [] {
+    const char* e = std::getenv("DTN_PANEL_ONECTA2");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 void panel_shape(int max_rows, int* rpt, int* csize) {
   // measured per-pivot cost (tools/probe/panel_probe): one CTA 0.9 us (<= 256
   // rows), one CTA with 2 rows/thread 1.14 us (<= 512), clusters with the
   // st.async exchange 1.3-1.6 us (2-16 CTAs x 256 rows), 2 rows/thread beyond
   if (max_rows <= PNT) { *rpt = 1; *csize = 1; }
-  else if (max_rows <= 2 * PNT) { *rpt = 2; *csize = 1; }
+  else if (max_rows <= 2 * PNT && panel_onecta2()) { *rpt = 2; *csize = 1; }
   else if (max_rows <= PMAXC * PNT) { *rpt = 1; *csize = (max_rows + PNT - 1) / PNT; }
   else { *rpt = 2; *csize = (max_rows + 2 * PNT - 1) / (2 * PNT); }
 }

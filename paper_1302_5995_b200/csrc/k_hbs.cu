@@ -498,6 +498,9 @@ cudaError_t launch_add_blocks(const AddDesc* d_descs, int count, cudaStream_t st
 constexpr int GJT = 512;
 constexpr int GJ_SMEM_MAX = 160;  // s <= 160: 160 * 161 doubles = 206 KB
 
+// SM: every block of the launch fits in shared memory (the matrix addressed as shared,
+// not through generic pointers); else every block is inverted in place in global memory
+template <bool SM>
 __global__ void __launch_bounds__(GJT) gj_inverse_kernel(const InvDesc* __restrict__ descs) {
   extern __shared__ __align__(16) double gsm[];
   __shared__ double rv[GJT / 32];
@@ -510,7 +513,7 @@ __global__ void __launch_bounds__(GJT) gj_inverse_kernel(const InvDesc* __restri
     if (threadIdx.x == 0) *d.info = 0;
     return;
   }
-  const bool in_smem = s <= GJ_SMEM_MAX;
+  constexpr bool in_smem = SM;
   const int lda = in_smem ? (s | 1) : d.lda;
   double* A = in_smem ? gsm : d.A;
   double* rowk = in_smem ? gsm + (long long)lda * s : gsm;  // s doubles
@@ -521,68 +524,71 @@ __global__ void __launch_bounds__(GJT) gj_inverse_kernel(const InvDesc* __restri
     for (int e = tid; e < s * s; e += GJT) A[(e % s) + (e / s) * lda] = d.A[(e % s) + (long long)(e / s) * d.lda];
   if (tid == 0) bad = 0;
   __syncthreads();
+  __shared__ double s_piv;
   for (int k = 0; k < s; ++k) {
-    // 1. pivot: argmax |a_ik|, i >= k
-    double bv = -1.0;
-    int bi = s;
-    for (int i = k + tid; i < s; i += GJT) {
-      const double v = fabs(A[i + (long long)k * lda]);
-      if (v > bv || (v == bv && i < bi) || v != v) {
-        bv = v != v ? INFINITY : v;
-        bi = i;
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > bv || (ov == bv && oi < bi)) {
-        bv = ov;
-        bi = oi;
-      }
-    }
-    if (lane == 0) {
-      rv[warp] = bv;
-      ri[warp] = bi;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      double b = rv[0];
-      int i0 = ri[0];
-      for (int w = 1; w < GJT / 32; ++w)
-        if (rv[w] > b || (rv[w] == b && ri[w] < i0)) {
-          b = rv[w];
-          i0 = ri[w];
+    // 1. pivot: argmax |a_ik|, i >= k (warp 0; lowest index on ties, NaN ranks highest)
+    if (warp == 0) {
+      double bv = -1.0;
+      int bi = s;
+      for (int i = k + lane; i < s; i += 32) {
+        double v = fabs(A[i + (long long)k * lda]);
+        if (v != v) v = INFINITY;
+        if (v > bv) {
+          bv = v;
+          bi = i;
         }
-      const double pv = i0 < s ? A[i0 + (long long)k * lda] : 0.0;
-      if (i0 >= s || pv == 0.0 || !isfinite(pv)) bad = k + 1;
-      piv_row = i0;
-      perm[k] = i0;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        const double pv = bi < s ? A[bi + (long long)k * lda] : 0.0;
+        if (bi >= s || pv == 0.0 || !isfinite(pv)) bad = k + 1;
+        piv_row = bi;
+        perm[k] = bi;
+        s_piv = pv;
+      }
     }
     __syncthreads();
     if (bad) break;
-    // 2. swap rows k and p
+    // 2. swap rows k and p (column by column), the scaled pivot row and the pivot
+    //    column, all from the values before the swap
     const int p = piv_row;
-    if (p != k)
-      for (int j = tid; j < s; j += GJT) {
-        const double t = A[k + (long long)j * lda];
-        A[k + (long long)j * lda] = A[p + (long long)j * lda];
-        A[p + (long long)j * lda] = t;
+    const double rp = 1.0 / s_piv;
+    for (int x = tid; x < s; x += GJT) {
+      double* cj = A + (long long)x * lda;
+      const double ak = cj[k], ap = cj[p];
+      if (p != k) {
+        cj[k] = ap;
+        cj[p] = ak;
       }
-    __syncthreads();
-    // 3. scaled pivot row and the pivot column
-    const double rp = 1.0 / A[k + (long long)k * lda];
-    for (int j = tid; j < s; j += GJT) {
-      rowk[j] = (j == k ? 1.0 : A[k + (long long)j * lda]) * rp;
-      colk[j] = A[j + (long long)k * lda];
+      rowk[x] = (x == k ? 1.0 : ap) * rp;  // new row k = old row p
+      // pivot column after the swap: rows k and p from thread k's own (pre-swap)
+      // reads of column k, every other row unaffected by the swap
+      if (x == k) {
+        colk[k] = s_piv;
+        if (p != k) colk[p] = ak;
+      } else if (x != p) {
+        colk[x] = A[x + (long long)k * lda];
+      }
     }
     __syncthreads();
-    // 4. rank-1 sweep (column-major, consecutive threads on consecutive rows)
-    for (int e = tid; e < s * s; e += GJT) {
-      const int i = e % s, j = e / s;
-      double* a = A + i + (long long)j * lda;
-      if (i == k) *a = rowk[j];
-      else *a = (j == k ? 0.0 : *a) - colk[i] * rowk[j];
+    // 3. rank-1 sweep: warp w owns columns w, w + 16, ..., lanes own rows (no division
+    //    per entry); a_kj <- rowk_j, a_ik <- -colk_i rowk_k, a_ij -= colk_i rowk_j
+    for (int j = warp; j < s; j += GJT / 32) {
+      double* cj = A + (long long)j * lda;
+      const double rj = rowk[j];
+      const bool jk = j == k;
+      for (int i = lane; i < s; i += 32) {
+        const double a = jk ? 0.0 : cj[i];
+        cj[i] = i == k ? rj : fma(-colk[i], rj, a);
+      }
     }
     __syncthreads();
   }
@@ -612,10 +618,11 @@ cudaError_t launch_gj_inverse(const InvDesc* d_descs, int count, int max_s, cuda
   // shared: the matrix (when it fits) + pivot row/column + permutation
   const size_t bytes = size_t((sm | 1)) * sm * 8 + size_t(max_s) * 20 + 64;
   if (bytes > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(gj_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    cudaError_t e = cudaFuncSetAttribute(gj_inverse_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
     if (e != cudaSuccess) return e;
   }
-  gj_inverse_kernel<<<count, GJT, bytes, st>>>(d_descs);
+  if (max_s <= GJ_SMEM_MAX) gj_inverse_kernel<true><<<count, GJT, bytes, st>>>(d_descs);
+  else gj_inverse_kernel<false><<<count, GJT, size_t(max_s) * 20 + 64, st>>>(d_descs);
   return cudaGetLastError();
 }
 
