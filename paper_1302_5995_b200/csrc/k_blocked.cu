@@ -1330,12 +1330,25 @@ __global__ void __launch_bounds__(RP_THREADS) rowpanel_kernel(KernelArgs args, c
       continue;
     }
     if (d0 >= 0 && lane >= kbe) col[d0] = g0[q];
-    double x = lane < kbe ? g0[q] : 0.0;
-    for (int c = 0; c < kbe; ++c) {  // unit lower L11
-      const double xc = __shfl_sync(0xffffffffu, x, c);
-      if (lane > c && lane < kbe) x = fma(-T[lane][c], xc, x);
+  }
+  if (left) return;
+  // unit lower L11 solves of the warp's columns, interleaved (independent shuffle/FMA
+  // chains in flight together instead of one column after another)
+  double x[CPW];
+#pragma unroll
+  for (int q = 0; q < CPW; ++q) x[q] = lane < kbe ? g0[q] : 0.0;
+  for (int c = 0; c < kbe; ++c) {
+    const double tl = (lane > c && lane < kbe) ? T[lane][c] : 0.0;
+#pragma unroll
+    for (int q = 0; q < CPW; ++q) {
+      const double xc = __shfl_sync(0xffffffffu, x[q], c);
+      x[q] = fma(-tl, xc, x[q]);
     }
-    if (lane < kbe) col[k0 + lane] = x;
+  }
+#pragma unroll
+  for (int q = 0; q < CPW; ++q) {
+    const int j = jbase + warp * CPW + q;
+    if (j < jend && lane < kbe) M[(long long)j * ld + k0 + lane] = x[q];
   }
 }
 
