@@ -13,10 +13,26 @@
 // holding S = M_bb - M_bi M_ii^{-1} M_ib in place. Two __syncthreads per pivot.
 #include <cfloat>
 #include <cstdlib>
+#include <type_traits>
+#include <utility>
 
 #include "common.cuh"
 
 namespace dtnb {
+
+__device__ __forceinline__ void st_shared_f64_pred(double* p, double v, bool pred) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.shared.f64 [%0], %1;\n}" ::"r"(smem_u32(p)), "d"(v),
+               "r"(int(pred))
+               : "memory");
+}
+template <class F, int... I>
+__device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, I...>) {
+  (f(std::integral_constant<int, I>{}), ...);
+}
+template <int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  static_for_impl(f, std::make_integer_sequence<int, N>{});
+}
 
 __device__ unsigned g_small_fallbacks;  // small systems whose no-interchange attempt failed (diagnostic)
 unsigned small_fallbacks_read_reset() {
@@ -35,6 +51,7 @@ __global__ void __launch_bounds__(TR * TC) small_elim_kernel(KernelArgs args, co
   __shared__ double colk[2][MAXT];
   __shared__ double rowp[MAXT];
   __shared__ int s_piv;
+  __shared__ double s_rinv;
 
   const int node_id = list[blockIdx.x];
   const NodeDev nd = args.nodes[node_id];
@@ -116,60 +133,130 @@ __global__ void __launch_bounds__(TR * TC) small_elim_kernel(KernelArgs args, co
   // partial pivoting would not interchange (then the arithmetic is identical).
   // Otherwise the system is re-assembled and eliminated with pivoting below.
   __shared__ double rowq[2][MAXT];
+  __shared__ double rinvq[2];  // 1 / pivot of the published step (formed once, by the pivot's owner)
   double pmin = DBL_MAX, pmax = 0.0;
   bool ok = true;
   {
+    // per-thread row / column indices (hoisted) and branch-free publishing: every
+    // thread selects its entries of column k and row k and stores them predicated
+    int ii[RPT], jj[CPT];
+#pragma unroll
+    for (int a = 0; a < RPT; ++a) ii[a] = tr + TR * a;
+#pragma unroll
+    for (int b = 0; b < CPT; ++b) jj[b] = tc + TC * b;
     auto publish = [&](int k, int buf) {
       const int bk = k / TC, tck = k % TC, ap = k / TR, trk = k % TR;
-      if (tc == tck) {
+      const bool pc = tc == tck, pr = tr == trk;
 #pragma unroll
-        for (int a = 0; a < RPT; ++a) {
-          const int i = tr + TR * a;
-          double v = m[a][0];
+      for (int a = 0; a < RPT; ++a) {
+        double v = m[a][0];
 #pragma unroll
-          for (int b = 1; b < CPT; ++b)
-            if (b == bk) v = m[a][b];
-          if (i < total) colk[buf][i] = v;
-        }
+        for (int b = 1; b < CPT; ++b) v = b == bk ? m[a][b] : v;
+        if (pc) colk[buf][ii[a]] = v;
       }
-      if (tr == trk) {
+#pragma unroll
+      for (int b = 0; b < CPT; ++b) {
+        double u = m[0][b];
+#pragma unroll
+        for (int a = 1; a < RPT; ++a) u = a == ap ? m[a][b] : u;
+        if (pr) rowq[buf][jj[b]] = u;
+      }
+      if (pc && pr) {  // the pivot's owner: one reciprocal per step for everybody
+        double pv = m[0][0];
 #pragma unroll
         for (int a = 0; a < RPT; ++a)
-          if (a == ap) {
 #pragma unroll
-            for (int b = 0; b < CPT; ++b) {
-              const int j = tc + TC * b;
-              if (j < MAXT) rowq[buf][j] = m[a][b];
-            }
-          }
+          for (int b = 0; b < CPT; ++b) pv = (a == ap && b == bk) ? m[a][b] : pv;
+        rinvq[buf] = 1.0 / pv;
       }
     };
+    bool bad = false;
+    // one elimination step (the pivot row/column of step k are published in colk/rowq)
+    auto step = [&](int k) {
+      const int buf = k & 1;
+      const double* ck = colk[buf];
+      const double* rp = rowq[buf];
+      if (tid == 0) {  // pivot statistics (only thread 0 reports them)
+        const double apv = fabs(rp[k]);
+        pmin = fmin(pmin, apv);
+        pmax = (apv != apv) ? INFINITY : fmax(pmax, apv);
+      }
+      const double rinv = rinvq[buf];
+      double lr[RPT], ur[CPT];
+#pragma unroll
+      for (int a = 0; a < RPT; ++a) {
+        const double l = ck[ii[a]] * rinv;  // (entries past the system are stale: masked)
+        const bool live = ii[a] > k && ii[a] < total;
+        bad |= live && ii[a] < ni && !(fabs(l) <= 1.0);
+        lr[a] = live ? -l : 0.0;
+      }
+#pragma unroll
+      for (int b = 0; b < CPT; ++b) {
+        const double u = rp[jj[b]];
+        ur[b] = (jj[b] > k && jj[b] < ncol) ? u : 0.0;
+      }
+#pragma unroll
+      for (int a = 0; a < RPT; ++a)
+#pragma unroll
+        for (int b = 0; b < CPT; ++b) m[a][b] = fma(lr[a], ur[b], m[a][b]);
+    };
+    if constexpr (TR == TC && RPT == CPT) {
+      // square thread grid: step k's pivot row and column sit in register slot
+      // k / TR of their owners, so with the steps grouped by that slot (compile-time
+      // register indices) publishing is a predicated store per entry, no selects
+      auto publish_c = [&](auto Cc, int k, int buf) {
+        constexpr int C = decltype(Cc)::value;
+        const int kk = k - C * TR;
+        const bool pc = tc == kk, pr = tr == kk;
+#pragma unroll
+        for (int a = 0; a < RPT; ++a) st_shared_f64_pred(&colk[buf][ii[a]], m[a][C], pc);
+#pragma unroll
+        for (int b = 0; b < CPT; ++b) st_shared_f64_pred(&rowq[buf][jj[b]], m[C][b], pr);
+        if (pc && pr) rinvq[buf] = 1.0 / m[C][C];
+      };
+      if (ni > 0) publish_c(std::integral_constant<int, 0>{}, 0, 0);
+      __syncthreads();
+      static_for<RPT>([&](auto Cc) {
+        constexpr int C = decltype(Cc)::value;
+        const int k1 = min(ni, (C + 1) * TR);
+        for (int k = C * TR; k < k1; ++k) {
+          step(k);
+          if (k + 1 < ni) {
+            if (k + 1 < (C + 1) * TR) publish_c(Cc, k + 1, (k + 1) & 1);
+            else publish_c(std::integral_constant<int, (C + 1 < RPT ? C + 1 : C)>{}, k + 1, (k + 1) & 1);
+          }
+          __syncthreads();
+        }
+      });
+      ok = !bad;
+    } else {
     if (ni > 0) publish(0, 0);
     __syncthreads();
     for (int k = 0; k < ni; ++k) {
-      const double* ck = colk[k & 1];
-      const double* rp = rowq[k & 1];
-      const double pv = rp[k];
-      const double apv = fabs(pv);
-      pmin = fmin(pmin, apv);
-      pmax = (apv != apv) ? INFINITY : fmax(pmax, apv);
-      const double rinv = 1.0 / pv;
+      const int buf = k & 1;
+      const double* ck = colk[buf];
+      const double* rp = rowq[buf];
+      if (tid == 0) {  // pivot statistics (only thread 0 reports them)
+        const double apv = fabs(rp[k]);
+        pmin = fmin(pmin, apv);
+        pmax = (apv != apv) ? INFINITY : fmax(pmax, apv);
+      }
+      const double rinv = rinvq[buf];
       // branch-free rank-1 update: rows <= k get l = 0 and columns <= k get u = 0, so
       // every owned entry takes one unconditional FMA (the predicated form spent ~10
       // instructions per entry; an FMA with a zero factor leaves finite entries unchanged)
       double lr[RPT], ur[CPT];
 #pragma unroll
       for (int a = 0; a < RPT; ++a) {
-        const int i = tr + TR * a;
-        const bool live = i > k && i < total;
-        const double l = live ? ck[i] * rinv : 0.0;
-        if (live && i < ni) ok &= fabs(l) <= 1.0;
-        lr[a] = -l;
+        const double l = ck[ii[a]] * rinv;  // (entries past the system are stale: masked)
+        const bool live = ii[a] > k && ii[a] < total;
+        bad |= live && ii[a] < ni && !(fabs(l) <= 1.0);
+        lr[a] = live ? -l : 0.0;
       }
 #pragma unroll
       for (int b = 0; b < CPT; ++b) {
-        const int j = tc + TC * b;
-        ur[b] = (j > k && j < ncol) ? rp[j] : 0.0;
+        const double u = rp[jj[b]];
+        ur[b] = (jj[b] > k && jj[b] < ncol) ? u : 0.0;
       }
 #pragma unroll
       for (int a = 0; a < RPT; ++a)
@@ -177,6 +264,8 @@ __global__ void __launch_bounds__(TR * TC) small_elim_kernel(KernelArgs args, co
         for (int b = 0; b < CPT; ++b) m[a][b] = fma(lr[a], ur[b], m[a][b]);
       if (k + 1 < ni) publish(k + 1, (k + 1) & 1);
       __syncthreads();
+    }
+    ok = !bad;
     }
   }
   const bool fast = __syncthreads_and(ok) != 0;
@@ -219,6 +308,8 @@ __global__ void __launch_bounds__(TR * TC) small_elim_kernel(KernelArgs args, co
         if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
       }
       if (tr == 0) s_piv = bi;
+      __syncwarp(gmask);  // the group's column entries are in ck (same warp)
+      if (tr == 0) s_rinv = 1.0 / ck[bi];
     }
     __syncthreads();
     const int p = s_piv;
@@ -237,11 +328,13 @@ __global__ void __launch_bounds__(TR * TC) small_elim_kernel(KernelArgs args, co
         }
       }
     }
-    const double apv = fabs(pv);
-    pmin = fmin(pmin, apv);
-    pmax = (apv != apv) ? INFINITY : fmax(pmax, apv);
+    if (tid == 0) {
+      const double apv = fabs(pv);
+      pmin = fmin(pmin, apv);
+      pmax = (apv != apv) ? INFINITY : fmax(pmax, apv);
+    }
     __syncthreads();
-    const double rinv = 1.0 / pv;
+    const double rinv = s_rinv;
     double lr[RPT], ur[CPT];  // branch-free update (see the no-interchange loop)
 #pragma unroll
     for (int a = 0; a < RPT; ++a) {
