@@ -775,9 +775,12 @@ __device__ __forceinline__ void shift_update_w(double (&w)[PKB], double l, const
 template <int W>
 using WinC = std::integral_constant<int, W>;
 
-template <bool CL, int RPT>
-__global__ void __launch_bounds__(PNT) panel2_kernel(KernelArgs args, const int* __restrict__ list, int k0, int kb,
-                                                    int csize, int fused, int use_fast) {
+template <bool CL, int RPT, int NT = PNT>
+__global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* __restrict__ list, int k0, int kb,
+                                                   int csize, int fused, int use_fast) {
+  // NT threads per CTA (one row each per RPT): 128-thread CTAs put a 2048-row panel on 16
+  // SMs instead of 8, halving each CTA's prologue update and substitution
+  constexpr int PNT = NT, PNW = NT / 32;
   constexpr int SC = PNW, NSLOT = PNW + (CL ? PMAXC : 0);
   __shared__ __align__(16) double rows[2][NSLOT][PKB];
   __shared__ __align__(16) unsigned sinfo[2][PNW][4];
@@ -1359,7 +1362,8 @@ unsigned panel_fallbacks_read_reset() {
   return h;
 }
 
-size_t panel_dyn_smem(int rpt) { return size_t(PKB * (PKB + 2) + PKB + rpt * PNT * (PKB + 1)) * sizeof(double); }
+size_t panel_dyn_smem(int rpt, int nt) { return size_t(PKB * (PKB + 2) + PKB + rpt * nt * (PKB + 1)) * sizeof(double); }
+size_t panel_dyn_smem(int rpt) { return panel_dyn_smem(rpt, PNT); }
 
 // no-interchange attempts stop for a node after this many of its panels
 // needed interchanges (DTN_FAST_THRESHOLD; 0 = always run the pivoted loop).
@@ -1391,6 +1395,13 @@ cudaError_t blocked_init() {
   }
   for (auto f : {panel2_kernel<true, 2>, panel2_kernel<false, 2>}) {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(panel_dyn_smem(2)));
+    if (e != cudaSuccess) return e;
+  }
+  {
+    cudaError_t e = cudaFuncSetAttribute(panel2_kernel<true, 1, 128>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(panel2_kernel<true, 1, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(panel_dyn_smem(1, 128)));
     if (e != cudaSuccess) return e;
   }
   cudaError_t e = cudaFuncSetAttribute(panel_kernel<true, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -1430,6 +1441,30 @@ static bool panel_onecta2() {
   return on;
 }
 
+void panel_shape(int max_rows, int* rpt, int* csize);
+
+// DTN_PANEL_NT=128: panels of 257..2048 rows on clusters of 128-thread CTAs (twice the
+// SMs per panel; measured 1-2 % slower than the 256-thread default on configs 2, 3, 5: the
+// no-interchange top LU and the per-pivot exchange, not the per-CTA work, set the time)
+static int panel_small_nt() {
+  static const int v = [] {
+    const char* e = std::getenv("DTN_PANEL_NT");
+    return e ? std::atoi(e) : 256;
+  }();
+  return v;
+}
+
+void panel_shape(int max_rows, int* rpt, int* csize, int* nt) {
+  *nt = PNT;
+  if (!panel_legacy() && panel_small_nt() == 128 && max_rows > PNT && max_rows <= PMAXC * 128) {
+    *rpt = 1;
+    *csize = (max_rows + 127) / 128;
+    *nt = 128;
+    return;
+  }
+  panel_shape(max_rows, rpt, csize);
+}
+
 void panel_shape(int max_rows, int* rpt, int* csize) {
   // measured per-pivot cost (tools/probe/panel_probe): one CTA 0.9 us (<= 256
   // rows), one CTA with 2 rows/thread 1.14 us (<= 512), clusters with the
@@ -1444,12 +1479,12 @@ size_t panel_dyn_smem(int rpt);
 int panel_fast_threshold();
 bool panel_legacy();
 
-template <bool CL, int RPT>
+template <bool CL, int RPT, int NT = PNT>
 cudaError_t launch_panel_t(const KernelArgs& args, const int* d_list, int count, int k0, int kb, int csize,
                            cudaStream_t st, bool fused) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(count * csize);
-  cfg.blockDim = dim3(PNT);
+  cfg.blockDim = dim3(NT);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   if (CL) {
@@ -1460,11 +1495,11 @@ cudaError_t launch_panel_t(const KernelArgs& args, const int* d_list, int count,
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  cfg.dynamicSmemBytes = panel_dyn_smem(RPT);
-  if (panel_legacy())
+  cfg.dynamicSmemBytes = panel_dyn_smem(RPT, NT);
+  if (NT == PNT && panel_legacy())
     return cudaLaunchKernelEx(&cfg, panel_kernel<CL, RPT>, args, d_list, k0, kb, csize, fused ? 1 : 0,
                               panel_fast_threshold());
-  return cudaLaunchKernelEx(&cfg, panel2_kernel<CL, RPT>, args, d_list, k0, kb, csize, fused ? 1 : 0,
+  return cudaLaunchKernelEx(&cfg, panel2_kernel<CL, RPT, NT>, args, d_list, k0, kb, csize, fused ? 1 : 0,
                             panel_fast_threshold());
 }
 
@@ -1474,9 +1509,10 @@ cudaError_t launch_panel(const KernelArgs& args, const int* d_list, int count, i
                          cudaStream_t st, bool fused) {
   if (count <= 0) return cudaSuccess;
   if (kb > PKB) return cudaErrorInvalidValue;
-  int rpt, csize;
-  panel_shape(max_rows, &rpt, &csize);
+  int rpt, csize, nt;
+  panel_shape(max_rows, &rpt, &csize, &nt);
   if (csize > PMAXC) return cudaErrorInvalidValue;
+  if (nt == 128) return launch_panel_t<true, 1, 128>(args, d_list, count, k0, kb, csize, st, fused);
   if (csize == 1 && rpt == 2) return launch_panel_t<false, 2>(args, d_list, count, k0, kb, 1, st, fused);
   if (csize == 1) return launch_panel_t<false, 1>(args, d_list, count, k0, kb, 1, st, fused);
   if (rpt == 1) return launch_panel_t<true, 1>(args, d_list, count, k0, kb, csize, st, fused);
