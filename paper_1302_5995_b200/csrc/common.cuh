@@ -56,6 +56,13 @@ struct GemmDesc {  // C(m x n) = beta*C + alpha*A(m x k)*B(k x n), column-major
   int m, n, k, lda, ldb, ldc;
 };
 
+struct SumDesc {  // dst(m x n, ldd) += sum_{s < slices} src + s * stride (m x n, lds each)
+  double* dst;
+  const double* src;
+  long long stride;
+  int ldd, lds, m, n, slices;
+};
+
 struct GemmDesc2 {  // C = A_cat B, A_cat = [A (row-major, first ka columns) | A2 (column-major)]
   const double* A;
   const double* A2;

@@ -69,6 +69,7 @@ cudaError_t launch_sgather_red(const KernelArgs&, const int*, int, int, cudaStre
 cudaError_t launch_kk_gather(const KernelArgs&, const int*, int, int, cudaStream_t);
 cudaError_t launch_factor_gather(const KernelArgs&, const int*, int, long long, cudaStream_t);
 cudaError_t launch_omega(const KernelArgs&, const int*, int, long long, cudaStream_t);
+cudaError_t launch_sum_partials(const SumDesc*, int, long long, cudaStream_t);
 cudaError_t launch_hqr(const QrDesc*, int, int, int, const double*, cudaStream_t, bool = false);
 cudaError_t launch_gemm_desc2(const GemmDesc2*, int, int, bool, cudaStream_t);
 int gemm_tiles(int, int);
@@ -134,8 +135,10 @@ struct WaveLaunch {
   double sm_flops = 0.0;
   int cp_off = 0, cp_cnt = 0;
   long long cp_max_elems = 0;
-  int cp_y1 = 0, cp_y1_tiles = 0, cp_y1_k = 0;      // GemmDesc:  Y1 = S[J, :] Omega
-  int cp_y2 = 0, cp_y2_tiles = 0;                   // GemmDesc2: Y2 = S[:, J]^T Omega
+  int cp_y1 = 0, cp_y1_n = 0, cp_y1_tiles = 0, cp_y1_k = 0;  // GemmDesc:  Y1 = S[J, :] Omega (K-slices)
+  int cp_y2 = 0, cp_y2_n = 0, cp_y2_tiles = 0;                // GemmDesc2: Y2 = S[:, J]^T Omega (K-slices)
+  int cp_sum = 0, cp_sum_n = 0;                               // SumDesc: the slices into Y1 / Y2
+  long long cp_sum_elems = 0;
   int cp_qr = 0, cp_qr_m = 0, cp_qr_n = 0;          // QrDesc x 2 cp_cnt
   int cp_rt = 0, cp_rt_tiles = 0;                   // GemmDesc2: R_jk^T = S[J, :]^T Q1
   int cp_lk = 0, cp_lk_tiles = 0, cp_lk_k = 0;      // GemmDesc:  L_kj = S[:, J] Q2
@@ -241,6 +244,8 @@ struct PlanDev {
   std::vector<CopyDesc> h_sm_copy;
   std::vector<GemmDesc> h_sg;
   std::vector<GemmDesc2> h_sg2;
+  std::vector<SumDesc> h_sum;
+  SumDesc* d_sum = nullptr;
   std::vector<QrDesc> h_qr;
   CopyDesc* d_sm_copy = nullptr;
   GemmDesc* d_sg = nullptr;
@@ -261,7 +266,7 @@ struct PlanDev {
     for (void* p : std::initializer_list<void*>{d_nodes, d_pos, d_arena, d_piv, d_pivstat, d_lists, d_stencil, d_S, d_G,
                                                 d_perm, d_norm, d_inv_descs, d_W, d_LUp, d_UI, d_UI2, d_tinv, d_root_trs, d_load_col, d_F, d_F_desc, d_bs_gemm,
                                                 d_bs_copy, d_tri, d_trs, d_chk, d_bad, d_fw_copy, d_fw_gather,
-                                                d_fw_trs, d_fw_gemm, d_sm_copy, d_sg, d_sg2, d_qr, d_eps, d_qstat, d_rg, d_rt})
+                                                d_fw_trs, d_fw_gemm, d_sm_copy, d_sg, d_sg2, d_sum, d_qr, d_eps, d_qstat, d_rg, d_rt})
       if (p) cudaFree(p);
     if (h_qstat) cudaFreeHost(h_qstat);
     if (h_pivstat) cudaFreeHost(h_pivstat);
@@ -642,15 +647,31 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
         L.sm_flops += 2.0 * nd.nb * double(nd.nb) * nd.sys_nb;
       }
       // factors of the wave's structured boxes (randomized range finder + Householder QR)
+      // K-slice k of the sketches: rows [k0, k1) of Omega (k0 a multiple of 16); slice 0
+      // into Y, slice s > 0 into the node's partials (summed afterwards, in slice order)
+      auto kslice = [](const Node& nd, int sl, int* k0, int* k1) {
+        const int kc = int(align_up((nd.nb + nd.ysplit - 1) / nd.ysplit, 16));
+        *k0 = std::min(nd.nb, sl * kc);
+        *k1 = std::min(nd.nb, *k0 + kc);
+      };
+      auto ypart = [](const Node& nd, int sl, int which) {  // which 0: Y1, 1: Y2
+        if (sl == 0) return which ? nd.y2_off : nd.y1_off;
+        return nd.ysp_off + (int64_t(sl - 1) * 2 + which) * nd.ldq * (nd.ell + kProbes);
+      };
       L.cp_y1 = int(D->h_sg.size());
       for (int id : wv.compress) {
         const Node& nd = P.nodes[id];
-        D->h_sg.push_back(GemmDesc{coff(nd.s_off + nd.j0), coff(nd.om_off), off(nd.y1_off), nd.jn, nd.ell + kProbes,
-                                   nd.nb, nd.ld, nd.ldf, nd.ldq});
+        for (int sl = 0; sl < nd.ysplit; ++sl) {
+          int k0, k1;
+          kslice(nd, sl, &k0, &k1);
+          D->h_sg.push_back(GemmDesc{coff(nd.s_off + nd.j0 + int64_t(k0) * nd.ld), coff(nd.om_off + k0),
+                                     off(ypart(nd, sl, 0)), nd.jn, nd.ell + kProbes, k1 - k0, nd.ld, nd.ldf, nd.ldq});
+          L.cp_y1_k = std::max(L.cp_y1_k, k1 - k0);
+        }
         L.cp_y1_tiles = std::max(L.cp_y1_tiles, gemm_tiles(nd.jn, nd.ell + kProbes));
-        L.cp_y1_k = std::max(L.cp_y1_k, nd.nb);
         L.cp_flops += 2.0 * nd.jn * double(nd.nb) * nd.ell;
       }
+      L.cp_y1_n = int(D->h_sg.size()) - L.cp_y1;
       L.cp_lk = int(D->h_sg.size());
       for (int id : wv.compress) {
         const Node& nd = P.nodes[id];
@@ -664,12 +685,28 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
       L.cp_y2 = int(D->h_sg2.size());
       for (int id : wv.compress) {  // S[:, J]^T: row-major view of the J columns
         const Node& nd = P.nodes[id];
-        D->h_sg2.push_back(GemmDesc2{coff(nd.s_off + int64_t(nd.j0) * nd.ld), nullptr, coff(nd.om_off), off(nd.y2_off),
-                                     nd.jn, nd.ell + kProbes, nd.nb, nd.ld, 0, int(align_up(nd.nb, 16)), nd.nb,
-                                     nd.ldf, nd.ldq});
+        for (int sl = 0; sl < nd.ysplit; ++sl) {
+          int k0, k1;
+          kslice(nd, sl, &k0, &k1);
+          D->h_sg2.push_back(GemmDesc2{coff(nd.s_off + int64_t(nd.j0) * nd.ld + k0), nullptr, coff(nd.om_off + k0),
+                                       off(ypart(nd, sl, 1)), nd.jn, nd.ell + kProbes, k1 - k0, nd.ld, 0,
+                                       int(align_up(k1 - k0, 16)), k1 - k0, nd.ldf, nd.ldq});
+        }
         L.cp_y2_tiles = std::max(L.cp_y2_tiles, gemm_tiles(nd.jn, nd.ell + kProbes));
         L.cp_flops += 2.0 * nd.jn * double(nd.nb) * nd.ell;
       }
+      L.cp_y2_n = int(D->h_sg2.size()) - L.cp_y2;
+      L.cp_sum = int(D->h_sum.size());
+      for (int id : wv.compress) {
+        const Node& nd = P.nodes[id];
+        if (nd.ysplit < 2) continue;
+        for (int which = 0; which < 2; ++which)
+          D->h_sum.push_back(SumDesc{off(which ? nd.y2_off : nd.y1_off), coff(ypart(nd, 1, which)),
+                                     2LL * nd.ldq * (nd.ell + kProbes), nd.ldq, nd.ldq, nd.jn, nd.ell + kProbes,
+                                     nd.ysplit - 1});
+        L.cp_sum_elems = std::max<long long>(L.cp_sum_elems, (long long)nd.jn * (nd.ell + kProbes));
+      }
+      L.cp_sum_n = int(D->h_sum.size()) - L.cp_sum;
       L.cp_rt = int(D->h_sg2.size());
       for (int id : wv.compress) {  // S[J, :]^T: row-major view of the J rows
         const Node& nd = P.nodes[id];
@@ -730,6 +767,7 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
     for (auto& g : D->h_fw_gemm) { g.A = rel(g.A); g.B = rel(g.B); g.C = rel(g.C); }
     for (auto& c : D->h_sm_copy) { c.src = rel(c.src); c.dst = rel(c.dst); }
     for (auto& g : D->h_sg) { g.A = rel(g.A); g.B = rel(g.B); g.C = rel(g.C); }
+    for (auto& g : D->h_sum) { g.dst = rel(g.dst); g.src = rel(g.src); }
     for (auto& g : D->h_sg2) { g.A = rel(g.A); g.B = rel(g.B); g.C = rel(g.C); }
     if (!D->h_qr.empty()) {
       D->d_qstat = dalloc<double>(2 * D->h_qr.size());
@@ -753,6 +791,7 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
     upload_vec(D->h_sm_copy, D->d_sm_copy);
     upload_vec(D->h_sg, D->d_sg);
     upload_vec(D->h_sg2, D->d_sg2);
+    upload_vec(D->h_sum, D->d_sum);
     upload_vec(D->h_qr, D->d_qr);
     D->d_eps = dalloc<double>(1);
     D->d_trs = dalloc<TrsmDesc>(D->h_trs.size());
@@ -1223,10 +1262,13 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
       const int* cl = D.d_lists + L.cp_off;
       run(K_COMPRESS, 0.0, 0.0, [&] { return launch_omega(a, cl, L.cp_cnt, L.cp_max_elems, st); });
       run(K_SGEMM, 0.0, 0.0, [&] {
-        return launch_gemm_desc(D.d_sg + L.cp_y1, L.cp_cnt, L.cp_y1_tiles, L.cp_y1_k, 1.0, 0.0, st, false);
+        return launch_gemm_desc(D.d_sg + L.cp_y1, L.cp_y1_n, L.cp_y1_tiles, L.cp_y1_k, 1.0, 0.0, st, false);
       });
       run(K_SGEMM, 0.0, 0.0,
-          [&] { return launch_gemm_desc2(D.d_sg2 + L.cp_y2, L.cp_cnt, L.cp_y2_tiles, false, st); });
+          [&] { return launch_gemm_desc2(D.d_sg2 + L.cp_y2, L.cp_y2_n, L.cp_y2_tiles, false, st); });
+      if (L.cp_sum_n)
+        run(K_SGATHER, 0.0, 0.0,
+            [&] { return launch_sum_partials(D.d_sum + L.cp_sum, L.cp_sum_n, L.cp_sum_elems, st); });
       run(K_COMPRESS, 0.0, 0.0,
           [&] { return launch_hqr(D.d_qr + L.cp_qr, 2 * L.cp_cnt, L.cp_qr_m, L.cp_qr_n, D.d_eps, st); });
       run(K_SGEMM, 0.0, 0.0,

@@ -1356,6 +1356,25 @@ static bool hqrb_shape(int count, int max_m, int max_nc, int* C_out, HqrbSmem* L
   return true;
 }
 
+// the K-slices of the structured boxes' sketches summed into Y1 / Y2 (slice 0 is Y itself)
+__global__ void __launch_bounds__(256) sum_partials_kernel(const SumDesc* __restrict__ descs) {
+  const SumDesc d = descs[blockIdx.y];
+  const int total = d.m * d.n;
+  for (int e = blockIdx.x * 256 + threadIdx.x; e < total; e += gridDim.x * 256) {
+    const int r = e % d.m, c = e / d.m;
+    double t = d.dst[r + (long long)c * d.ldd];
+    for (int q = 0; q < d.slices; ++q) t += d.src[q * d.stride + r + (long long)c * d.lds];
+    d.dst[r + (long long)c * d.ldd] = t;
+  }
+}
+
+cudaError_t launch_sum_partials(const SumDesc* d_descs, int count, long long max_elems, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  dim3 grid(unsigned(std::min<long long>((max_elems + 255) / 256, 64)), count);
+  sum_partials_kernel<<<grid, 256, 0, st>>>(d_descs);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sgather_red(const KernelArgs& args, const int* d_list, int count, int max_total, cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
   dim3 grid((max_total + SG_COLS - 1) / SG_COLS, count);

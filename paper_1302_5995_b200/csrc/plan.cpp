@@ -6,6 +6,7 @@
 //   merge ordering     dense_nd.cpp:114-131 (union boundary CCW, then the remaining
 //                      child boundary nodes, child a first)
 //   merge_four order   dense_nd.cpp:188-194 (SW+NW, SE+NE, W|E)
+#include <cstdlib>
 #include "plan.hpp"
 
 #include <algorithm>
@@ -15,6 +16,16 @@
 #include <string>
 
 namespace dtnb {
+
+// DTN_SKETCH_SPLIT=0: the structured boxes' sketches as one K = nb product per box
+static bool sketch_split_off() {
+  static const bool off = [] {
+    const char* e = std::getenv("DTN_SKETCH_SPLIT");
+    return e && std::atoi(e) == 0;
+  }();
+  return off;
+}
+
 
 void perimeter_ccw(const Rect& r, std::vector<std::pair<int, int>>& p) {
   p.clear();
@@ -513,6 +524,8 @@ Plan make_plan(const PlanKey& key) {
     if (P.active[i] && !is_input[i]) born[size_t(P.nodes[i].wave)].push_back(i);
   for (int w = 0; w < nw; ++w) {
     for (auto [off, n] : release[size_t(w)]) arena.put(off, n);  // dead before this wave
+    int nfac = 0;  // structured boxes forming factors in this wave (one batched sketch launch)
+    for (int i : born[size_t(w)]) nfac += P.nodes[i].factors ? 1 : 0;
     for (int i : born[size_t(w)]) {
       Node& nd = P.nodes[i];
       const bool top = nd.parent < 0 || !P.active[nd.parent] || i == P.root;
@@ -563,6 +576,13 @@ Plan make_plan(const PlanKey& key) {
         nd.om_off = take(int64_t(nd.ldf) * (nd.ell + 4), w + 1);  // + kProbes range-finder probes
         nd.y1_off = take(int64_t(nd.ldq) * (nd.ell + 4), w + 1);
         nd.y2_off = take(int64_t(nd.ldq) * (nd.ell + 4), w + 1);
+        // K-slices of the sketches (K = nb >> jn): enough CTAs for ~2 per SM, >= 256 per slice
+        const int tiles = ((nd.jn + 127) / 128) * ((nd.ell + 4 + 63) / 64);
+        int S = std::max(1, std::min(8, (2 * 148 + std::max(nfac, 1) * tiles - 1) / (std::max(nfac, 1) * tiles)));
+        while (S > 1 && nd.nb / S < 256) --S;
+        if (sketch_split_off()) S = 1;
+        nd.ysplit = S;
+        if (S > 1) nd.ysp_off = take(int64_t(S - 1) * 2 * nd.ldq * (nd.ell + 4), w + 1);
       }
     }
   }

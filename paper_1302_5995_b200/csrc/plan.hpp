@@ -98,6 +98,10 @@ struct Node {
   // structured merge: gathered L_k, R_k^T and T = L_k C (nb x (ra + rb) each)
   int64_t om_off = 0, y1_off = 0, y2_off = 0, lkg_off = 0, rkg_off = 0, tg_off = 0, cbuf_off = 0;
   int ldg = 0, ldr = 0;
+  // the sketches Y1 / Y2 (K = nb) split into ysplit K-slices: slice 0 into y1 / y2, the
+  // others into partials (ysp_off: per slice [Y1 part | Y2 part], ldq x (ell + 4) each)
+  int ysplit = 1;
+  int64_t ysp_off = 0;
 };
 
 struct Wave {
