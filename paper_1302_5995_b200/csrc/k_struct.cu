@@ -768,6 +768,7 @@ __global__ void __launch_bounds__(QR_THREADS) hqrb_kernel(const QrDesc* __restri
     if constexpr (CL) cg::this_cluster().sync();
     else __syncthreads();
   };
+  auto r0_glob = [&](int r) { return r0 + r; };  // local row -> global row
   auto rsum = [&](const double* slot) -> double {  // sum over the cluster's copies of *slot, rank order
     if constexpr (CL) {
       double v[QR_MAXC];
@@ -806,6 +807,9 @@ __global__ void __launch_bounds__(QR_THREADS) hqrb_kernel(const QrDesc* __restri
           Ws[k] = rws[k];
         }
       }
+      // every CTA has copied every share before anybody overwrites its own (the caller
+      // transforms the sums in place)
+      cg::this_cluster().sync();
     } else {
       for (int e = tid; e < cnt; e += QR_THREADS) Ws[(e % QB) * L.wcols + e / QB] = Wp[(e % QB) * L.wcols + e / QB];
     }
@@ -818,6 +822,60 @@ __global__ void __launch_bounds__(QR_THREADS) hqrb_kernel(const QrDesc* __restri
       Vr[i * QB + cc] = (c >= c1 || gi < c) ? 0.0 : (gi == c ? 1.0 : Y[i + c * ld]);
     }
     __syncthreads();
+  };
+  // ---- the panel products on the FP64 tensor pipe (mma.sync.m16n8k4), warps over 8-column
+  // tiles. W[:, wofs + t] = V^T x_t over the local rows, x_t = column t of Vr (vcols) or of
+  // Y at ycols (ld)
+  const int g8 = lane >> 2, t4 = lane & 3;
+  auto mma_w = [&](const double* ycols, bool vcols, int ncols, int wofs) {
+    const int ntile = (ncols + 7) / 8;
+    for (int tile = warp; tile < ntile; tile += QR_WARPS) {
+      const int cb = tile * 8, col = cb + g8;
+      const bool cv = col < ncols;
+      const double* yc = ycols + (long long)min(col, max(ncols - 1, 0)) * ld;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int k0 = 0; k0 < nr; k0 += 4) {
+        const int r = k0 + t4;
+        const bool rv = r < nr;
+        const double a0 = rv ? Vr[r * QB + g8] : 0.0;
+        const double a1 = rv ? Vr[r * QB + g8 + 8] : 0.0;
+        const double b0 = (rv && cv) ? (vcols ? Vr[r * QB + col] : yc[r]) : 0.0;
+        mma_f64_m16n8k4(acc, a0, a1, b0);
+      }
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int cc = g8 + 8 * (v >> 1), cl = cb + 2 * t4 + (v & 1);
+        if (cl < ncols) Wp[cc * L.wcols + wofs + cl] = acc[v];
+      }
+    }
+  };
+  // out[:, t] = base_t - V Ws[:, wofs + t] over the local rows, base_t = column t of Y at
+  // ycols (in place) or, unit, the unit vector of global row c_unit + t
+  auto mma_upd = [&](double* ycols, int ncols, int wofs, bool unit, int c_unit) {
+    const int rt = (nr + 15) / 16, ct = (ncols + 7) / 8;
+    for (int tile = warp; tile < rt * ct; tile += QR_WARPS) {
+      const int r0 = (tile % rt) * 16, cb = (tile / rt) * 8;
+      double acc[4];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int r = r0 + g8 + 8 * (v >> 1), cl = cb + 2 * t4 + (v & 1);
+        acc[v] = (r < nr && cl < ncols) ? (unit ? (r0_glob(r) == c_unit + cl ? 1.0 : 0.0) : ycols[r + (long long)cl * ld])
+                                        : 0.0;
+      }
+      const int cl = cb + g8;
+#pragma unroll
+      for (int k0 = 0; k0 < QB; k0 += 4) {
+        const double a0 = (r0 + g8 < nr) ? -Vr[(r0 + g8) * QB + k0 + t4] : 0.0;
+        const double a1 = (r0 + g8 + 8 < nr) ? -Vr[(r0 + g8 + 8) * QB + k0 + t4] : 0.0;
+        const double b0 = cl < ncols ? Ws[(k0 + t4) * L.wcols + wofs + cl] : 0.0;
+        mma_f64_m16n8k4(acc, a0, a1, b0);
+      }
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int r = r0 + g8 + 8 * (v >> 1), c2 = cb + 2 * t4 + (v & 1);
+        if (r < nr && c2 < ncols) ycols[r + (long long)c2 * ld] = acc[v];
+      }
+    }
   };
   const int gl = tid & 15, grp = tid >> 4;  // 16 groups of 16 lanes: one panel column per group
   const int npan = (n + QB - 1) / QB;
@@ -895,25 +953,8 @@ __global__ void __launch_bounds__(QR_THREADS) hqrb_kernel(const QrDesc* __restri
     HCLK_T(tp1);
     stage_v(c0, c1);
     const int nt = nc - c1, ncol = QB + nt;
-    if (tid < ncol) {
-      double acc[QB];
-#pragma unroll
-      for (int cc = 0; cc < QB; ++cc) acc[cc] = 0.0;
-      const bool isv = tid < QB;
-      const double* col = isv ? nullptr : Y + (c1 + tid - QB) * ld;
-      for (int i = 0; i < nr; ++i) {
-        const double y = isv ? Vr[i * QB + tid] : col[i];
-        const double2* v2 = reinterpret_cast<const double2*>(Vr + i * QB);
-#pragma unroll
-        for (int c2 = 0; c2 < QB / 2; ++c2) {
-          const double2 v = v2[c2];
-          acc[2 * c2] = fma(v.x, y, acc[2 * c2]);
-          acc[2 * c2 + 1] = fma(v.y, y, acc[2 * c2 + 1]);
-        }
-      }
-#pragma unroll
-      for (int cc = 0; cc < QB; ++cc) Wp[cc * L.wcols + tid] = acc[cc];
-    }
+    mma_w(nullptr, true, QB, 0);         // G = V^T V
+    mma_w(Y + c1 * ld, false, nt, QB);   // W = V^T Y[:, c1:nc]
     allreduce_w(ncol);
     HCLK_ADD(2, tp1);
     HCLK_T(tp2);
@@ -942,31 +983,20 @@ __global__ void __launch_bounds__(QR_THREADS) hqrb_kernel(const QrDesc* __restri
     __syncthreads();
     HCLK_ADD(3, tp2);
     HCLK_T(tp3);
-    if (tid < nt) {
+    for (int t = tid; t < nt; t += QR_THREADS) {  // W <- T^T W in place, column by column
       double w[QB];
 #pragma unroll
-      for (int cc = 0; cc < QB; ++cc) w[cc] = Ws[cc * L.wcols + QB + tid];
-      double wt[QB];  // T^T w
+      for (int cc = 0; cc < QB; ++cc) w[cc] = Ws[cc * L.wcols + QB + t];
 #pragma unroll
       for (int cc = 0; cc < QB; ++cc) {
-        double s = 0.0;
+        double sacc = 0.0;
 #pragma unroll
-        for (int l = 0; l <= cc; ++l) s = fma(T[l * QB + cc], w[l], s);
-        wt[cc] = s;
-      }
-      double* col = Y + (c1 + tid) * ld;
-      for (int i = 0; i < nr; ++i) {
-        const double2* v2 = reinterpret_cast<const double2*>(Vr + i * QB);
-        double s = col[i];
-#pragma unroll
-        for (int c2 = 0; c2 < QB / 2; ++c2) {
-          const double2 v = v2[c2];
-          s = fma(-v.x, wt[2 * c2], s);
-          s = fma(-v.y, wt[2 * c2 + 1], s);
-        }
-        col[i] = s;
+        for (int l = 0; l <= cc; ++l) sacc = fma(T[l * QB + cc], w[l], sacc);
+        Ws[cc * L.wcols + QB + t] = sacc;
       }
     }
+    __syncthreads();
+    mma_upd(Y + c1 * ld, nt, QB, false, 0);
     __syncthreads();
     HCLK_ADD(4, tp3);
   }
@@ -993,59 +1023,30 @@ __global__ void __launch_bounds__(QR_THREADS) hqrb_kernel(const QrDesc* __restri
     const int c0 = pn * QB, c1 = min(n, c0 + QB);
     stage_v(c0, c1);
     const int nq = n - c1, ncol = QB + nq;
-    if (tid < ncol) {
-      double acc[QB];
+    if (tid < QB) {  // V^T E = V1^T: the owner's rows c0 + tid
+      const int gi = c0 + tid;
+      const bool mine = gi >= r0 && gi < r1 && gi < c1;
 #pragma unroll
-      for (int cc = 0; cc < QB; ++cc) acc[cc] = 0.0;
-      if (tid < QB) {  // V^T E = V1^T: the owner's rows c0 + tid
-        const int gi = c0 + tid;
-        if (gi >= r0 && gi < r1 && gi < c1)
-#pragma unroll
-          for (int cc = 0; cc < QB; ++cc) acc[cc] = Vr[(gi - r0) * QB + cc];
-      } else {
-        const double* col = Y + (c1 + tid - QB) * ld;
-        for (int i = 0; i < nr; ++i) {
-          const double y = col[i];
-          const double2* v2 = reinterpret_cast<const double2*>(Vr + i * QB);
-#pragma unroll
-          for (int c2 = 0; c2 < QB / 2; ++c2) {
-            const double2 v = v2[c2];
-            acc[2 * c2] = fma(v.x, y, acc[2 * c2]);
-            acc[2 * c2 + 1] = fma(v.y, y, acc[2 * c2 + 1]);
-          }
-        }
-      }
-#pragma unroll
-      for (int cc = 0; cc < QB; ++cc) Wp[cc * L.wcols + tid] = acc[cc];
+      for (int cc = 0; cc < QB; ++cc) Wp[cc * L.wcols + tid] = mine ? Vr[(gi - r0) * QB + cc] : 0.0;
     }
+    mma_w(Y + c1 * ld, false, nq, QB);  // V^T Q[:, c1:n]
     allreduce_w(ncol);
     const double* T = Ts + pn * QB * QB;
-    if (tid < ncol && (tid >= QB || c0 + tid < c1)) {
+    for (int t = tid; t < ncol; t += QR_THREADS) {  // W <- T W in place (T upper)
       double w[QB];
 #pragma unroll
-      for (int cc = 0; cc < QB; ++cc) w[cc] = Ws[cc * L.wcols + tid];
-      double tw[QB];  // T w (T upper)
+      for (int cc = 0; cc < QB; ++cc) w[cc] = Ws[cc * L.wcols + t];
 #pragma unroll
       for (int cc = 0; cc < QB; ++cc) {
-        double s = 0.0;
+        double sacc = 0.0;
 #pragma unroll
-        for (int l = cc; l < QB; ++l) s = fma(T[cc * QB + l], w[l], s);
-        tw[cc] = s;
-      }
-      const int j = tid < QB ? c0 + tid : c1 + tid - QB;
-      double* col = Y + j * ld;
-      for (int i = 0; i < nr; ++i) {
-        const double2* v2 = reinterpret_cast<const double2*>(Vr + i * QB);
-        double s = tid < QB ? (r0 + i == j ? 1.0 : 0.0) : col[i];
-#pragma unroll
-        for (int c2 = 0; c2 < QB / 2; ++c2) {
-          const double2 v = v2[c2];
-          s = fma(-v.x, tw[2 * c2], s);
-          s = fma(-v.y, tw[2 * c2 + 1], s);
-        }
-        col[i] = s;
+        for (int l = cc; l < QB; ++l) sacc = fma(T[cc * QB + l], w[l], sacc);
+        Ws[cc * L.wcols + t] = sacc;
       }
     }
+    __syncthreads();
+    mma_upd(Y + c1 * ld, nq, QB, false, 0);               // formed columns, in place
+    mma_upd(Y + c0 * ld, c1 - c0, 0, true, c0);           // the panel's own columns from E
     __syncthreads();
   }
   HCLK_ADD(6, tp5);
@@ -1101,8 +1102,10 @@ __global__ void __launch_bounds__(HP_THREADS) hqrp_kernel(const QrDesc* __restri
   const int gl = tid & (QR_GL - 1), grp = tid / QR_GL;  // HP_NG groups of 8 lanes
   const int ld = m | 1;
   double* Y = qdyn;
-  for (int j = 0; j < nc; ++j)
-    for (int i = tid; i < m; i += HP_THREADS) Y[i + j * ld] = d.Y[i + (long long)j * d.ldy];
+  for (int e = tid; e < m * nc; e += HP_THREADS) {  // every thread: one latency round, not one per column
+    const int i = e % m, j = e / m;
+    Y[i + j * ld] = d.Y[i + (long long)j * d.ldy];
+  }
   __syncthreads();
   // initial column norms (rows >= 0)
   for (int jb = 0; jb < nc; jb += HP_NG) {
@@ -1151,15 +1154,20 @@ __global__ void __launch_bounds__(HP_THREADS) hqrp_kernel(const QrDesc* __restri
       }
     }
     __syncthreads();
-    int jm = wj[0];
-    {
-      double b = wbest[0];
+    int jm;
+    {  // every warp reduces the per-warp winners with shuffles (no serial loop over warps)
+      double b = lane < HP_WARPS ? wbest[lane] : -1.0;
+      int bj = lane < HP_WARPS ? wj[lane] : 0x7fffffff;
 #pragma unroll
-      for (int w = 1; w < HP_WARPS; ++w)
-        if (wbest[w] > b || (wbest[w] == b && wj[w] < jm)) {
-          b = wbest[w];
-          jm = wj[w];
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, b, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+        if (ob > b || (ob == b && oj < bj)) {
+          b = ob;
+          bj = oj;
         }
+      }
+      jm = bj;
     }
     HCLK_ADD(8, tqa);
     HCLK_T(tqb);
@@ -1286,8 +1294,10 @@ __global__ void __launch_bounds__(HP_THREADS) hqrp_kernel(const QrDesc* __restri
   if (nq > 0) finish_col(0);
   __syncthreads();
   HCLK_ADD(11, tqd);
-  for (int jj = 0; jj < nq; ++jj)
-    for (int i = tid; i < m; i += HP_THREADS) d.Q[i + (long long)jj * d.ldq] = Y[i + jj * ld];
+  for (int e = tid; e < m * nq; e += HP_THREADS) {
+    const int i = e % m, jj = e / m;
+    d.Q[i + (long long)jj * d.ldq] = Y[i + jj * ld];
+  }
 }
 
 // launch geometry of hqrb_kernel: the smallest cluster whose row blocks and work
