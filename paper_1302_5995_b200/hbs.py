@@ -166,7 +166,7 @@ class HbsMatrix:
     def apply(self, x):
         return apply(self, x)
 
-    def serialize(self) -> bytes:
+    def serialize(self) -> memoryview:
         return serialize(self)
 
 
@@ -295,16 +295,17 @@ def basis_orthonormality_defect(H: HbsMatrix) -> float:
     return d
 
 
-def serialize(H: HbsMatrix) -> bytearray:
-    """DTNHBS01 (hbs.cpp:446-470), as a bytes-like buffer."""
+def serialize(H: HbsMatrix) -> memoryview:
+    """DTNHBS01 (hbs.cpp:446-470), as a read-only bytes-like view (compares equal to the
+    same bytes; `bytes(...)` copies it). The buffer is written in place by ONE device-to-host
+    copy into fresh, unzeroed memory (a bytearray would first zero-fill every page)."""
     n = C.c_uint64()
     H.ctx.check(L.lib().dtn_gpu_hbs_serialize(H.h, None, 0, C.byref(n)))
-    out = bytearray(n.value)  # filled in place: one device-to-host copy, no staging copies
+    out = np.empty(n.value, dtype=np.uint8)
     if n.value:
-        buf = (C.c_uint8 * n.value).from_buffer(out)
-        H.ctx.check(L.lib().dtn_gpu_hbs_serialize(H.h, buf, n.value, C.byref(n)))
-        del buf
-    return out
+        H.ctx.check(L.lib().dtn_gpu_hbs_serialize(H.h, out.ctypes.data, n.value,
+                                                  C.byref(n)))
+    return memoryview(out).toreadonly()
 
 
 def deserialize(data: bytes, ctx: Context | None = None) -> HbsMatrix:
