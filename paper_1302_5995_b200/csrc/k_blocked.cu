@@ -155,8 +155,10 @@ __device__ long long g_pro_clk[8];
 #ifdef DTN_PANEL_PROFILE
 __device__ long long g_p2_clk[16];
 #define P2CLK(slot) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_p2_clk[slot] = clock64(); } while (0)
+#define P2ACC(slot, t) do { if (blockIdx.x == 0 && threadIdx.x == 0) { const long long n_ = clock64(); g_p2_clk[slot] += n_ - (t); (t) = n_; } } while (0)
 #else
 #define P2CLK(slot) do { } while (0)
+#define P2ACC(slot, t) do { } while (0)
 #endif
 
 __device__ unsigned g_panel_fallbacks;  // panels whose no-interchange attempt failed (diagnostic)
@@ -1092,7 +1094,14 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
       }
       cg::this_cluster().sync();
     }
-    for (int j = jstart; j < kbe; ++j) {
+#ifdef DTN_PANEL_PROFILE
+    long long tq = clock64();
+#endif
+    // steps in chunks of 8 on a window narrowing by 8 (see shift_update_w)
+    auto pchunk = [&](auto Wc) {
+    constexpr int W = decltype(Wc)::value;
+    const int jlo = max(jstart, PKB - W), jhi = min(kbe, PKB - W + 8);
+    for (int j = jlo; j < jhi; ++j) {
       const int jr = j - jstart;
       const int buf = jr & 1;
       unsigned key = 0u, klo = 0u;
@@ -1121,7 +1130,9 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
         }
         st_shared_v4u_pred(&sinfo[buf][warp][0], whi, wlo, unsigned(crank * PNT + tid + stride * ba), 0u, win);
       }
+      P2ACC(9, tq);
       __syncthreads();
+      P2ACC(10, tq);
       const unsigned lk = lane < PNW ? sinfo[buf][lane][0] : 0u;
       const unsigned ll = lane < PNW ? sinfo[buf][lane][1] : 0u;
       const unsigned bkey = __reduce_max_sync(0xffffffffu, lk);
@@ -1137,7 +1148,9 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
             if (lane == 0) st_async_v4_b32(cluster_map(&cinfo[buf][crank][0], d), bkey, blo, unsigned(p), 0u, mb);
           }
         }
+        P2ACC(11, tq);
         mbar_wait(&mbar[buf], unsigned(jr >> 1) & 1u);
+        P2ACC(12, tq);
         const unsigned ck = lane < csize ? cinfo[buf][lane][0] : 0u;
         const unsigned cl_ = lane < csize ? cinfo[buf][lane][1] : 0u;
         const unsigned gkey = __reduce_max_sync(0xffffffffu, ck);
@@ -1157,6 +1170,7 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
       pmax = fmax(pmax, apiv);
       bad |= !(apiv == apiv) || apiv == INFINITY;
       const double rinv = __drcp_rn(piv);
+      P2ACC(13, tq);
 #pragma unroll
       for (int a = 0; a < RPT; ++a) {
         const int r = crank * PNT + tid + stride * a;
@@ -1164,11 +1178,17 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
         if (elim[a] < 0) {
           const double l = v[a][0] * rinv;
           M[r + (long long)j * ldm] = l;
-          shift_update(v[a], l, prow);
+          shift_update_w<W>(v[a], l, prow);
         }
       }
       if (tid == 0) sp[j] = p;
+      P2ACC(14, tq);
     }
+    };
+    pchunk(WinC<32>{});
+    pchunk(WinC<24>{});
+    pchunk(WinC<16>{});
+    pchunk(WinC<8>{});
     // ---- final placement: pivot of step e -> position e; the top rows [0, kbe)
     // that were not pivots fill, in order, the positions vacated by pivots from
     // below (also in order). Only those rows move: rank 0 stages them through

@@ -50,6 +50,10 @@ int main() {
       float ms; cudaEventElapsedTime(&ms, e0, e1);
       if (r >= 2) { best = ms < best ? ms : best; tot += ms; }
     }
+    { long long q[16]; cudaMemcpyFromSymbol(q, g_p2_clk, sizeof(q));
+      printf("  pivoted loop (per step, avg over the last launch x reps): argmax+publish %lld sync %lld cta-argmax+push %lld mbar-wait %lld cluster-argmax+rcp %lld update %lld\n",
+             q[9] / (32 * (reps + 2)), q[10] / (32 * (reps + 2)), q[11] / (32 * (reps + 2)), q[12] / (32 * (reps + 2)), q[13] / (32 * (reps + 2)), q[14] / (32 * (reps + 2)));
+      long long z[16] = {0}; cudaMemcpyToSymbol(g_p2_clk, z, sizeof(z)); }
     int rpt, cs; panel_shape(n, &rpt, &cs);
     printf("rpt %d kb %2d rows %5d csize %2d: best %.1f us, mean %.1f us (%.2f us/column)\n", rpt, kbv, n, cs, best * 1e3, tot / reps * 1e3,
            best * 1e3 / kbv);
