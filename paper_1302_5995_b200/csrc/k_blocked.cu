@@ -1279,6 +1279,11 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
 // Row swaps + U12 = L11^{-1} (P A)[k0:k1, k1:total] for the trailing columns;
 // with swap_left, also the row swaps of the already factored columns [0, k0)
 // (needed only when L itself is reused: the root LU for G = S^{-1}).
+// BROWS: the launch includes boundary-row tiles (non-Schur merges). Without them the
+// kernel needs few registers (the boundary rows' 32-entry solve is compiled out), so
+// several CTAs share an SM (with it: 154 registers, one CTA per SM -- the first blocked
+// waves' thousands of column tiles ran one CTA per SM at a time).
+template <bool BROWS>
 __global__ void __launch_bounds__(RP_THREADS) rowpanel_kernel(KernelArgs args, const int* __restrict__ list, int k0,
                                                               int kb, int ncoltiles, int nlefttiles, int skip_next) {
   __shared__ double T[32][33];
@@ -1290,7 +1295,7 @@ __global__ void __launch_bounds__(RP_THREADS) rowpanel_kernel(KernelArgs args, c
   const long long ld = nd.ldm;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int bx = blockIdx.x;
-  if (bx >= ncoltiles + nlefttiles) {
+  if (BROWS && bx >= ncoltiles + nlefttiles) {
     // boundary rows [ni, total): L21 = A[i, k0:k1] U11^{-1}
     const int i = nd.ni + (bx - ncoltiles - nlefttiles) * RP_THREADS + tid;
     if (nd.ni + (bx - ncoltiles - nlefttiles) * RP_THREADS >= nd.total) return;
@@ -1547,7 +1552,10 @@ cudaError_t launch_rowpanel(const KernelArgs& args, const int* d_list, int count
   const int rowtiles = (max_nb + RP_THREADS - 1) / RP_THREADS;
   if (coltiles + lefttiles + rowtiles <= 0) return cudaSuccess;
   dim3 grid(coltiles + lefttiles + rowtiles, count);
-  rowpanel_kernel<<<grid, RP_THREADS, 0, st>>>(args, d_list, k0, kb, coltiles, lefttiles, skip_next ? 1 : 0);
+  if (rowtiles > 0)
+    rowpanel_kernel<true><<<grid, RP_THREADS, 0, st>>>(args, d_list, k0, kb, coltiles, lefttiles, skip_next ? 1 : 0);
+  else
+    rowpanel_kernel<false><<<grid, RP_THREADS, 0, st>>>(args, d_list, k0, kb, coltiles, lefttiles, skip_next ? 1 : 0);
   return cudaGetLastError();
 }
 
