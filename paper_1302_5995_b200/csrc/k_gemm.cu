@@ -181,7 +181,7 @@ __device__ __forceinline__ void gemm_tile(const double* __restrict__ A, int lda,
 }
 
 template <int BK, bool UPD, bool A16, bool TC = false>
-__global__ void __launch_bounds__(GTHREADS) gemm_desc_kernel(const GemmDesc* __restrict__ descs, double alpha,
+__global__ void __launch_bounds__(GTHREADS, 2) gemm_desc_kernel(const GemmDesc* __restrict__ descs, double alpha,
                                                              double beta) {
   extern __shared__ __align__(16) unsigned char gsm_raw[];
   GemmSmem<BK>& sm = *reinterpret_cast<GemmSmem<BK>*>(gsm_raw);

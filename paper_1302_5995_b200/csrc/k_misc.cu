@@ -209,7 +209,7 @@ __device__ long long g_ts_clk[16];
 #endif
 
 template <bool LOWER>
-__global__ void __launch_bounds__(256) trsm_block_kernel(const TrsmDesc* __restrict__ descs) {
+__global__ void __launch_bounds__(256, 2) trsm_block_kernel(const TrsmDesc* __restrict__ descs) {
   extern __shared__ __align__(16) double trsm_smem[];
   const TrsmDesc d = descs[blockIdx.y];
   const int bk = d.bk, bkp = ts_pad(bk), ld = bkp + 2;
