@@ -1428,6 +1428,9 @@ cudaError_t blocked_init() {
     e = cudaFuncSetAttribute(panel2_kernel<true, 1, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(panel_dyn_smem(1, 128)));
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(panel2_kernel<false, 1, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(panel_dyn_smem(1, 128)));
+    if (e != cudaSuccess) return e;
   }
   cudaError_t e = cudaFuncSetAttribute(panel_kernel<true, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
@@ -1468,6 +1471,16 @@ static bool panel_onecta2() {
 
 void panel_shape(int max_rows, int* rpt, int* csize);
 
+// DTN_PANEL_NT1=0: systems of <= 128 rows on 256-thread CTAs (default: 128-thread CTAs, three
+// per SM by registers -- the many-system waves run one panel CTA per system)
+static bool panel_small_nt1() {
+  static const bool on = [] {
+    const char* e = std::getenv("DTN_PANEL_NT1");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
 // DTN_PANEL_NT=128: panels of 257..2048 rows on clusters of 128-thread CTAs (twice the
 // SMs per panel; measured 1-2 % slower than the 256-thread default on configs 2, 3, 5: the
 // no-interchange top LU and the per-pivot exchange, not the per-CTA work, set the time)
@@ -1481,6 +1494,12 @@ static int panel_small_nt() {
 
 void panel_shape(int max_rows, int* rpt, int* csize, int* nt) {
   *nt = PNT;
+  if (!panel_legacy() && max_rows <= 128 && panel_small_nt1()) {  // one 128-thread CTA: 3 per SM
+    *rpt = 1;
+    *csize = 1;
+    *nt = 128;
+    return;
+  }
   if (!panel_legacy() && panel_small_nt() == 128 && max_rows > PNT && max_rows <= PMAXC * 128) {
     *rpt = 1;
     *csize = (max_rows + 127) / 128;
@@ -1537,6 +1556,7 @@ cudaError_t launch_panel(const KernelArgs& args, const int* d_list, int count, i
   int rpt, csize, nt;
   panel_shape(max_rows, &rpt, &csize, &nt);
   if (csize > PMAXC) return cudaErrorInvalidValue;
+  if (nt == 128 && csize == 1) return launch_panel_t<false, 1, 128>(args, d_list, count, k0, kb, 1, st, fused);
   if (nt == 128) return launch_panel_t<true, 1, 128>(args, d_list, count, k0, kb, csize, st, fused);
   if (csize == 1 && rpt == 2) return launch_panel_t<false, 2>(args, d_list, count, k0, kb, 1, st, fused);
   if (csize == 1) return launch_panel_t<false, 1>(args, d_list, count, k0, kb, 1, st, fused);
