@@ -34,6 +34,8 @@ namespace dtnb {
 cudaError_t launch_small_elim(const KernelArgs&, const int*, int, int, bool, cudaStream_t);
 cudaError_t launch_gather(const KernelArgs&, const int*, int, int, cudaStream_t);
 cudaError_t launch_panel(const KernelArgs&, const int*, int, int, int, int, cudaStream_t, bool);
+bool panel_is_tall(int max_rows);
+int panel_tall_max_rows(int count);
 cudaError_t launch_rowpanel(const KernelArgs&, const int*, int, int, int, int, int, bool, cudaStream_t, bool);
 cudaError_t launch_trailing_update(const KernelArgs&, const int*, int, int, int, int, int, int, cudaStream_t, int);
 cudaError_t launch_tri_inv_u_batched(const void*, int, int, cudaStream_t);
@@ -98,9 +100,12 @@ int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 constexpr int kSmallMax = 160;
 constexpr int kDefaultMicro = 16;  // measured best on configs 1-2 (tools/sweep.py)
 
-// Panel width; the register-resident panel spans up to 16 CTAs x 512 rows.
-int panel_kb(int rows) {
-  if (rows > 16 * 512) throw std::invalid_argument("dense merge system too large for the cluster panel (> 8192 rows)");
+// Panel width; the register-resident cluster panel spans up to 16 CTAs x 512 rows, the
+// tall panel (global-memory pivot exchange) up to 512 rows per SM.
+int panel_kb(int rows, int count = 1) {
+  if (rows > 16 * 512 && rows > panel_tall_max_rows(count))
+    throw std::invalid_argument("dense merge system too large for the tall panel (" + std::to_string(rows) +
+                                " rows, " + std::to_string(count) + " systems)");
   return 32;
 }
 
@@ -378,7 +383,7 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
       L.blk_max_ni = std::max(L.blk_max_ni, nd.ni);
       L.blk_max_nb = std::max(L.blk_max_nb, nd.nb);
     }
-    if (L.blk_cnt) L.kb = panel_kb(L.blk_max_ni);
+    if (L.blk_cnt) L.kb = panel_kb(L.blk_max_ni, L.blk_cnt);
     L.gd_off = int(lists.size());
     for (int id : wv.blocked)
       if (!P.nodes[id].smerge) {
@@ -1082,7 +1087,7 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
     // prologue, so the main stream runs only the panel chain; rowpanel(s) and
     // the trailing update of the remaining columns run on the side stream.
     // panel(s) waits for the side stream's step s-2 (its columns' updates).
-    if (nb_rows == 0 && use_fused()) {
+    if (nb_rows == 0 && use_fused() && !panel_is_tall(max_ni)) {
       int s = 0;
       for (int k0 = 0; k0 < max_ni; k0 += kb, ++s) {
         double fp = 0.0, fr = 0.0, ft = 0.0;
@@ -1295,7 +1300,7 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
   if (prof) prof->wave = int(D.wl.size());
   if (want_G) {
     const int nb = D.nb;
-    panel_kb(nb);  // throws beyond the cluster panel's 8192 rows
+    panel_kb(nb);  // throws beyond the tall panel's rows
     double* LU = D.d_arena + D.lu_off;
     run(K_COPY, 0.0, 16.0 * nb2, [&] { return launch_copy2d(D.d_S, D.lds, LU, D.ldlu, nb, nb, st); });
     const int* rl = D.d_lists + D.root_list_off;

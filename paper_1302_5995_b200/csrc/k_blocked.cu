@@ -777,6 +777,78 @@ __device__ __forceinline__ void shift_update_w(double (&w)[PKB], double l, const
 template <int W>
 using WinC = std::integral_constant<int, W>;
 
+// Final row placement of a factored panel (whole CTA): pivot of step e -> position e; the
+// top rows [0, kbe) that were not pivots fill, in order, the positions vacated by pivots
+// from below (also in order). Writes the U rows from ub (shifted), the net move list mv
+// and the moved rows' permutation entries; stage holds 2 PKB x PKB doubles.
+template <int NTH>
+__device__ void place_panel_rows(double* __restrict__ M, long long ldm, int k0, int kbe, const int* sp, int* vac,
+                                 int* mv_dst, int* mv_src, const double* ub, double* stage, int* perm, int* mv) {
+  constexpr int PNT = NTH, PLD = PKB + 2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // U row e (ub, shifted) into the pivot row's original position, columns [e, kbe)
+  for (int e = tid; e < PKB * PKB; e += PNT) {
+    const int i = e % PKB, c = e / PKB;
+    if (i < kbe && c >= i && c < kbe) M[sp[i] + (long long)c * ldm] = ub[i * PLD + (c - i)];
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int x = lane < kbe ? sp[lane] : 0x7fffffff;
+    const int key2 = x >= kbe ? x : 0x7fffffff;
+    int rk = 0;
+    for (int e = 0; e < kbe; ++e) {
+      const int y = sp[e] >= kbe ? sp[e] : 0x7fffffff;
+      rk += (y < key2);
+    }
+    if (lane < kbe && key2 != 0x7fffffff) vac[rk] = key2;
+    unsigned topmask = 0u;
+    for (int e = 0; e < kbe; ++e)
+      if (sp[e] < kbe) topmask |= 1u << sp[e];
+    __syncwarp();
+    // slots: e < kbe -> (dst e, src sp[e]); kbe + i -> (dst vac[i], src i-th displaced top row)
+    for (int sl = lane; sl < 2 * PKB; sl += 32) {
+      int dst = -1, src = -1;
+      if (sl < kbe) {
+        dst = sl;
+        src = sp[sl];
+      } else {
+        const int i = sl - kbe;
+        const int nvac = __popc(~topmask & ((kbe < 32) ? ((1u << kbe) - 1u) : 0xffffffffu));
+        if (i < nvac) {
+          // the i-th top row (ascending) that is not a pivot
+          int t = 0, cnt = -1;
+          for (; t < kbe; ++t)
+            if (!((topmask >> t) & 1u) && ++cnt == i) break;
+          dst = vac[i];
+          src = t;
+        }
+      }
+      mv_dst[sl] = dst;
+      mv_src[sl] = src;
+    }
+  }
+  __syncthreads();
+  if (tid < 2 * PKB) {
+    mv[tid] = mv_dst[tid] >= 0 ? k0 + mv_dst[tid] : -1;
+    mv[2 * PKB + tid] = mv_src[tid] >= 0 ? k0 + mv_src[tid] : -1;
+  }
+  // stage the moved rows (panel columns) and their permutation entries
+  for (int e = tid; e < 2 * PKB * PKB; e += PNT) {
+    const int sl = e / PKB, c = e % PKB;
+    const int src = mv_src[sl];
+    if (src >= 0 && mv_dst[sl] != src && c < kbe) stage[sl * PKB + c] = __ldcg(M + src + (long long)c * ldm);
+  }
+  int oldp = 0;
+  if (tid < 2 * PKB && mv_src[tid] >= 0 && mv_dst[tid] != mv_src[tid]) oldp = __ldcg(perm + k0 + mv_src[tid]);
+  __syncthreads();
+  for (int e = tid; e < 2 * PKB * PKB; e += PNT) {
+    const int sl = e / PKB, c = e % PKB;
+    const int src = mv_src[sl];
+    if (src >= 0 && mv_dst[sl] != src && c < kbe) M[mv_dst[sl] + (long long)c * ldm] = stage[sl * PKB + c];
+  }
+  if (tid < 2 * PKB && mv_src[tid] >= 0 && mv_dst[tid] != mv_src[tid]) perm[k0 + mv_dst[tid]] = oldp;
+}
+
 template <bool CL, int RPT, int NT = PNT>
 __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* __restrict__ list, int k0, int kb,
                                                    int csize, int fused, int use_fast) {
@@ -1194,71 +1266,8 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
     // below (also in order). Only those rows move: rank 0 stages them through
     // shared memory once every CTA's stores are visible.
     csync();
-    if (crank == 0) {
-      // U row e (ub, shifted) into the pivot row's original position, columns [e, kbe)
-      for (int e = tid; e < PKB * PKB; e += PNT) {
-        const int i = e % PKB, c = e / PKB;
-        if (i < kbe && c >= i && c < kbe) M[sp[i] + (long long)c * ldm] = ub[i * PLD + (c - i)];
-      }
-      __syncthreads();
-      if (warp == 0) {
-        const int x = lane < kbe ? sp[lane] : 0x7fffffff;
-        const int key2 = x >= kbe ? x : 0x7fffffff;
-        int rk = 0;
-        for (int e = 0; e < kbe; ++e) {
-          const int y = sp[e] >= kbe ? sp[e] : 0x7fffffff;
-          rk += (y < key2);
-        }
-        if (lane < kbe && key2 != 0x7fffffff) vac[rk] = key2;
-        unsigned topmask = 0u;
-        for (int e = 0; e < kbe; ++e)
-          if (sp[e] < kbe) topmask |= 1u << sp[e];
-        __syncwarp();
-        // slots: e < kbe -> (dst e, src sp[e]); kbe + i -> (dst vac[i], src i-th displaced top row)
-        for (int sl = lane; sl < 2 * PKB; sl += 32) {
-          int dst = -1, src = -1;
-          if (sl < kbe) {
-            dst = sl;
-            src = sp[sl];
-          } else {
-            const int i = sl - kbe;
-            const int nvac = __popc(~topmask & ((kbe < 32) ? ((1u << kbe) - 1u) : 0xffffffffu));
-            if (i < nvac) {
-              // the i-th top row (ascending) that is not a pivot
-              int t = 0, cnt = -1;
-              for (; t < kbe; ++t)
-                if (!((topmask >> t) & 1u) && ++cnt == i) break;
-              dst = vac[i];
-              src = t;
-            }
-          }
-          mv_dst[sl] = dst;
-          mv_src[sl] = src;
-        }
-      }
-      __syncthreads();
-      int* mv = move_list(args, nd, k0);
-      if (tid < 2 * PKB) {
-        mv[tid] = mv_dst[tid] >= 0 ? k0 + mv_dst[tid] : -1;
-        mv[2 * PKB + tid] = mv_src[tid] >= 0 ? k0 + mv_src[tid] : -1;
-      }
-      // stage the moved rows (panel columns) and their permutation entries
-      double* stage = psave;  // [2 PKB][PKB]
-      for (int e = tid; e < 2 * PKB * PKB; e += PNT) {
-        const int sl = e / PKB, c = e % PKB;
-        const int src = mv_src[sl];
-        if (src >= 0 && mv_dst[sl] != src && c < kbe) stage[sl * PKB + c] = __ldcg(M + src + (long long)c * ldm);
-      }
-      int oldp = 0;
-      if (tid < 2 * PKB && mv_src[tid] >= 0 && mv_dst[tid] != mv_src[tid]) oldp = __ldcg(perm + k0 + mv_src[tid]);
-      __syncthreads();
-      for (int e = tid; e < 2 * PKB * PKB; e += PNT) {
-        const int sl = e / PKB, c = e % PKB;
-        const int src = mv_src[sl];
-        if (src >= 0 && mv_dst[sl] != src && c < kbe) M[mv_dst[sl] + (long long)c * ldm] = stage[sl * PKB + c];
-      }
-      if (tid < 2 * PKB && mv_src[tid] >= 0 && mv_dst[tid] != mv_src[tid]) perm[k0 + mv_dst[tid]] = oldp;
-    }
+    if (crank == 0)
+      place_panel_rows<PNT>(M, ldm, k0, kbe, sp, vac, mv_dst, mv_src, ub, psave, perm, move_list(args, nd, k0));
   }
   P2CLK(7);
   if (fused && k0 > 0 && crank == 0) {  // U12 of the prologue into rows [k0 - kb, k0)
@@ -1274,6 +1283,191 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
   }
   P2CLK(8);
   if constexpr (CL) cg::this_cluster().sync();  // no CTA exits while others may still read its smem
+}
+
+// ---------------------------------------------------------------------------
+// tall_panel_kernel: the panel contract of panel2_kernel (non-fused, partial pivoting
+// from the first step) for systems beyond the cluster panel's 16 x 512 rows -- the root
+// LU of G = S^{-1} at config 4 (16380 rows). Rows are spread over TG CTAs per system
+// (gridDim.x = TG, gridDim.y = systems), RPT rows per thread in shifting register windows
+// as in panel2. A cluster cannot span more than 16 SMs, so the pivot exchange goes through
+// global memory: each CTA publishes its best candidate row (key + 32 values), one software
+// barrier over the system's TG CTAs, then every CTA picks the same winner (largest |a|,
+// ties to the lowest row) and applies the step locally. The launcher keeps the whole grid
+// within one CTA per SM, so every CTA of a system is resident together.
+constexpr int TALL_NT = 256;
+constexpr int TALL_MAX_CTAS = 160;
+struct TallCand {
+  double v[PKB];
+  unsigned hi, lo;
+  int row, pad;
+};
+__device__ TallCand g_tall_cand[2][TALL_MAX_CTAS];
+__device__ unsigned g_tall_bar[TALL_MAX_CTAS];
+
+__device__ __forceinline__ void tall_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    unsigned x;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(bar) : "memory");
+    } while (x < target);
+  }
+  __syncthreads();
+}
+
+// (hi, lo, row) candidate order: larger |a| wins, equal |a| goes to the lower row
+__device__ __forceinline__ bool tall_better(unsigned h1, unsigned l1, int r1, unsigned h2, unsigned l2, int r2) {
+  return h1 > h2 || (h1 == h2 && (l1 > l2 || (l1 == l2 && r1 < r2)));
+}
+
+template <int RPT>
+__global__ void __launch_bounds__(TALL_NT) tall_panel_kernel(KernelArgs args, const int* __restrict__ list, int k0,
+                                                             int kb) {
+  constexpr int NW = TALL_NT / 32, PLD = PKB + 2;
+  __shared__ __align__(16) double wrow[NW][PKB];
+  __shared__ unsigned whi[NW], wlo[NW];
+  __shared__ int wr[NW];
+  __shared__ __align__(16) double ub[PKB * PLD];
+  __shared__ __align__(16) double stage[2 * PKB * PKB];
+  __shared__ int sp[PKB], vac[PKB], mv_dst[2 * PKB], mv_src[2 * PKB];
+  __shared__ int s_win;
+  const int TG = gridDim.x, sys = blockIdx.y;
+  const int node_id = list[sys];
+  const NodeDev nd = args.nodes[node_id];
+  if (k0 >= nd.ni) return;  // uniform over the system's CTAs
+  const int kbe = min(kb, nd.ni - k0);
+  const int Ri = nd.ni - k0;
+  double* M = args.arena + nd.m_off + k0 + (long long)k0 * nd.ldm;
+  const long long ldm = nd.ldm;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int stride = TG * TALL_NT;
+  int* perm = args.piv + nd.piv_off;
+  TallCand* cand0 = g_tall_cand[0] + sys * TG;
+  TallCand* cand1 = g_tall_cand[1] + sys * TG;
+  unsigned* bar = g_tall_bar + sys;
+  unsigned nsync = 0;
+
+  double v[RPT][PKB];
+  int elim[RPT];
+#pragma unroll
+  for (int a = 0; a < RPT; ++a) {
+    const int r = blockIdx.x * TALL_NT + tid + stride * a;
+#pragma unroll
+    for (int c = 0; c < PKB; ++c) v[a][c] = (r < Ri && c < kbe) ? M[r + c * ldm] : 0.0;
+    if (k0 == 0 && r < Ri) perm[r] = r;
+    elim[a] = (r < Ri) ? -1 : PKB;
+  }
+  if (k0 == 0 && blockIdx.x == 0 && tid == 0) *pivoting_flag(args, nd) = 0;
+  double pmin = k0 == 0 ? DBL_MAX : args.pivstat[2 * node_id];
+  double pmax = k0 == 0 ? 0.0 : args.pivstat[2 * node_id + 1];
+  bool bad = false;
+  for (int j = 0; j < kbe; ++j) {
+    TallCand* cand = (j & 1) ? cand1 : cand0;
+    // this thread's best live row, then the warp's, then the CTA's
+    unsigned key = 0u, klo = 0u;
+    int br = 0x7fffffff, ba = 0;
+#pragma unroll
+    for (int a = 0; a < RPT; ++a) {
+      const double ax = fabs(v[a][0]);
+      const unsigned ka = elim[a] < 0 ? (unsigned(__double2hiint(ax)) | 0x80000000u) : 0u;
+      const unsigned kl = elim[a] < 0 ? unsigned(__double2loint(ax)) : 0u;
+      const int r = blockIdx.x * TALL_NT + tid + stride * a;
+      if (ka != 0u && tall_better(ka, kl, r, key, klo, br)) {
+        key = ka;
+        klo = kl;
+        br = r;
+        ba = a;
+      }
+    }
+    const unsigned mh = __reduce_max_sync(0xffffffffu, key);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, key == mh ? klo : 0u);
+    const int mr = int(__reduce_min_sync(0xffffffffu, unsigned(key == mh && klo == ml ? br : 0x7fffffff)));
+    if (br == mr && key == mh && mh != 0u) {
+#pragma unroll
+      for (int a = 0; a < RPT; ++a)
+        if (a == ba)
+#pragma unroll
+          for (int c = 0; c < PKB; ++c) wrow[warp][c] = v[a][c];
+    }
+    if (lane == 0) {
+      whi[warp] = mh;
+      wlo[warp] = ml;
+      wr[warp] = mr;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const unsigned h = lane < NW ? whi[lane] : 0u, l = lane < NW ? wlo[lane] : 0u;
+      const int r = lane < NW ? wr[lane] : 0x7fffffff;
+      const unsigned bh = __reduce_max_sync(0xffffffffu, h);
+      const unsigned bl = __reduce_max_sync(0xffffffffu, h == bh ? l : 0u);
+      const int brow = int(__reduce_min_sync(0xffffffffu, unsigned(h == bh && l == bl ? r : 0x7fffffff)));
+      const int bw = __ffs(__ballot_sync(0xffffffffu, lane < NW && h == bh && l == bl && r == brow)) - 1;
+      TallCand& mine = cand[blockIdx.x];
+      mine.v[lane] = bh != 0u ? wrow[bw][lane] : 0.0;
+      if (lane == 0) {
+        mine.hi = bh;
+        mine.lo = bl;
+        mine.row = brow;
+      }
+    }
+    tall_barrier(bar, unsigned(TG) * ++nsync);
+    // every CTA picks the same winner among the TG candidates
+    if (warp == 0) {
+      unsigned h = 0u, l = 0u;
+      int r = 0x7fffffff, w = 0;
+      for (int c = lane; c < TG; c += 32) {
+        const unsigned ch = __ldcg(&cand[c].hi), cl = __ldcg(&cand[c].lo);
+        const int cr = __ldcg(&cand[c].row);
+        if (ch != 0u && tall_better(ch, cl, cr, h, l, r)) {
+          h = ch;
+          l = cl;
+          r = cr;
+          w = c;
+        }
+      }
+      const unsigned bh = __reduce_max_sync(0xffffffffu, h);
+      const unsigned bl = __reduce_max_sync(0xffffffffu, h == bh ? l : 0u);
+      const int brow = int(__reduce_min_sync(0xffffffffu, unsigned(h == bh && l == bl ? r : 0x7fffffff)));
+      const int src = __shfl_sync(0xffffffffu, w, __ffs(__ballot_sync(0xffffffffu, h == bh && l == bl && r == brow)) - 1);
+      ub[j * PLD + lane] = __ldcg(&cand[src].v[lane]);  // U row j, shifted (ub[j][c] = U[j][j + c])
+      if (lane == 0) {
+        s_win = brow;
+        sp[j] = brow;
+      }
+    }
+    __syncthreads();
+    const int p = s_win;
+    const double* prow = ub + j * PLD;
+    const double piv = prow[0];
+    const double apiv = fabs(piv);
+    pmin = fmin(pmin, apiv);
+    pmax = fmax(pmax, apiv);
+    bad |= !(apiv == apiv) || apiv == INFINITY;
+    const double rinv = __drcp_rn(piv);
+#pragma unroll
+    for (int a = 0; a < RPT; ++a) {
+      const int r = blockIdx.x * TALL_NT + tid + stride * a;
+      if (r == p) elim[a] = j;
+      if (elim[a] < 0) {
+        const double l = v[a][0] * rinv;
+        M[r + (long long)j * ldm] = l;
+        shift_update(v[a], l, prow);
+      }
+    }
+  }
+  for (int e = kbe * PLD + tid; e < PKB * PLD; e += TALL_NT) ub[e] = 0.0;
+  // every CTA's multipliers visible before CTA 0 moves rows
+  tall_barrier(bar, unsigned(TG) * ++nsync);
+  if (blockIdx.x == 0) {
+    place_panel_rows<TALL_NT>(M, ldm, k0, kbe, sp, vac, mv_dst, mv_src, ub, stage, perm, move_list(args, nd, k0));
+    if (tid == 0) {
+      args.pivstat[2 * node_id] = pmin;
+      args.pivstat[2 * node_id + 1] = bad ? INFINITY : pmax;
+    }
+  }
 }
 
 // Row swaps + U12 = L11^{-1} (P A)[k0:k1, k1:total] for the trailing columns;
@@ -1549,10 +1743,60 @@ cudaError_t launch_panel_t(const KernelArgs& args, const int* d_list, int count,
 
 // fused: apply step k0 - kb to this panel's columns first (the look-ahead
 // prologue); the matching rowpanel / trailing launches skip those columns.
+// DTN_PANEL_TALL_MIN: panels of at least this many rows take tall_panel_kernel (default:
+// beyond the cluster panel's 16 x 512 rows; smaller values exercise it in the tests)
+// (read per call: a few hundred panel launches per build)
+int panel_tall_min() {
+  const char* e = std::getenv("DTN_PANEL_TALL_MIN");
+  return e ? std::max(1, std::atoi(e)) : PMAXC * 2 * PNT + 1;
+}
+bool panel_is_tall(int max_rows) { return max_rows >= panel_tall_min(); }
+
+static unsigned* g_tall_bar_addr = nullptr;
+
+// grid: TG CTAs per system, TG x count <= one CTA per SM (all resident together)
+cudaError_t launch_tall_panel(const KernelArgs& args, const int* d_list, int count, int max_rows, int k0, int kb,
+                              cudaStream_t st) {
+  int dev = 0, nsm = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return e;
+  if (!g_tall_bar_addr) {
+    e = cudaGetSymbolAddress(reinterpret_cast<void**>(&g_tall_bar_addr), g_tall_bar);
+    if (e != cudaSuccess) return e;
+  }
+  const int slots = std::min(nsm, TALL_MAX_CTAS);
+  for (int rpt = 1; rpt <= 2; ++rpt) {
+    const int tg = (max_rows + rpt * TALL_NT - 1) / (rpt * TALL_NT);
+    if (tg * count > slots) continue;
+    e = cudaMemsetAsync(g_tall_bar_addr, 0, sizeof(unsigned) * count, st);
+    if (e != cudaSuccess) return e;
+    dim3 grid(tg, count);
+    if (rpt == 1) tall_panel_kernel<1><<<grid, TALL_NT, 0, st>>>(args, d_list, k0, kb);
+    else tall_panel_kernel<2><<<grid, TALL_NT, 0, st>>>(args, d_list, k0, kb);
+    return cudaGetLastError();
+  }
+  return cudaErrorNotSupported;  // more rows than two register rows per thread on every SM
+}
+
+// the tall panel's row limit for `count` systems on this device (0 on error)
+int panel_tall_max_rows(int count) {
+  int dev = 0, nsm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return 0;
+  return std::min(nsm, TALL_MAX_CTAS) / std::max(1, count) * 2 * TALL_NT;
+}
+
 cudaError_t launch_panel(const KernelArgs& args, const int* d_list, int count, int max_rows, int k0, int kb,
                          cudaStream_t st, bool fused) {
   if (count <= 0) return cudaSuccess;
   if (kb > PKB) return cudaErrorInvalidValue;
+  if (panel_is_tall(max_rows)) {
+    if (fused) return cudaErrorInvalidValue;  // the engine runs tall systems without the look-ahead
+    const cudaError_t e = launch_tall_panel(args, d_list, count, max_rows, k0, kb, st);
+    if (e != cudaErrorNotSupported || max_rows > PMAXC * 2 * PNT) return e;
+    // (a lowered DTN_PANEL_TALL_MIN on a wave of many systems: the cluster panel, non-fused)
+  }
   int rpt, csize, nt;
   panel_shape(max_rows, &rpt, &csize, &nt);
   if (csize > PMAXC) return cudaErrorInvalidValue;

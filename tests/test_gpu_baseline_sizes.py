@@ -143,25 +143,28 @@ def test_config3_dense_benched_defaults_vs_oracle():
     sol.free()
 
 
-@pytest.mark.parametrize("which", ["dense", "compressed"])
+@pytest.mark.parametrize("which", ["dense", "compressed", "dense_G"])
 def test_config4_discrete_harmonic(which):
     """Config 4 (Laplace, n = 4096 interior, 16.8 M unknowns): S u_b = -(D g)_b for
-    the discrete-harmonic u = x y and u = x^2 - y^2."""
+    the discrete-harmonic u = x y and u = x^2 - y^2; with the dense G = S^{-1}
+    (root LU of 16380 rows: the tall panel), also G (-(D g)_b) = u_b."""
     import torch
     n_int = 4096
     n = n_int + 2
     op = dtn.discretize(dtn.baseline_problem(4, n_int))
     tree = dtn.build_tree_uniform(n, 32)
     st = torch.from_numpy(op.stencil).cuda()
-    if which == "dense":
-        sol = dtn.build_root_gpu(None, tree, want_G=False, stencil_device_ptr=st.data_ptr())
+    if which.startswith("dense"):
+        sol = dtn.build_root_gpu(None, tree, want_G=which == "dense_G", stencil_device_ptr=st.data_ptr())
     else:
         sol = dtn.build_root_accel(None, tree, dtn.AccelOptions(**ACCEL), stencil_device_ptr=st.data_ptr())
     del st
     bnd = dtn.root_boundary(tree)
     for u in (lambda xp, yp: xp * yp, lambda xp, yp: xp * xp - yp * yp):
         ub, rhs = manufactured(op, bnd, u)
-        assert rel(dtn.apply_schur(sol, ub), rhs) <= (1e-10 if which == "dense" else 1e-9)
-    if which == "dense":
+        assert rel(dtn.apply_schur(sol, ub), rhs) <= (1e-9 if which == "compressed" else 1e-10)
+        if which == "dense_G":
+            assert rel(dtn.apply_dtn(sol, rhs), ub) <= 1e-9
+    if which.startswith("dense"):
         sol.free()
     torch.cuda.empty_cache()

@@ -86,3 +86,56 @@ def test_partial_lu_schur(n, ni):
     out, ipiv, ps = gpu_partial_lu(A, ni)
     S = A[ni:, ni:] - A[ni:, :ni] @ np.linalg.solve(A[:ni, :ni], A[:ni, ni:])
     assert np.linalg.norm(out[ni:, ni:] - S) / np.linalg.norm(S) <= 1e-11
+
+
+def _check_lu_by_products(A, out, ipiv, tol):
+    """P A = L U checked through products with random vectors (O(n^2), any size)."""
+    n = A.shape[0]
+    assert sorted(ipiv.tolist()) == list(range(n))
+    Lm = np.tril(out, -1)
+    Um = np.triu(out)
+    assert np.max(np.abs(Lm)) <= 1.0 + 1e-12
+    X = np.random.default_rng(1).standard_normal((n, 4))
+    UX = Um @ X
+    LUX = Lm @ UX + UX
+    r = np.linalg.norm(LUX - A[ipiv] @ X) / (np.linalg.norm(A) * np.linalg.norm(X))
+    assert r <= tol
+
+
+@pytest.mark.parametrize("n", [5, 100, 600, 2100])
+def test_tall_panel_full_lu(n, monkeypatch):
+    """The tall panel (global-memory pivot exchange across TG CTAs, one software grid
+    barrier per pivot), forced at small sizes: a valid partial-pivoting P A = L U whose
+    pivot sequence is LAPACK's (largest |a|, ties to the lowest row) on random data."""
+    monkeypatch.setenv("DTN_PANEL_TALL_MIN", "1")
+    rng = np.random.default_rng(n + 11)
+    A = rng.standard_normal((n, n))
+    out, ipiv, ps = gpu_partial_lu(A, n)
+    _check_lu_by_products(A, out, ipiv, 1e-14)
+    assert ps[0] == pytest.approx(np.min(np.abs(np.diag(out))))
+    # LAPACK getrf's row permutation
+    lu, piv = sla.lu_factor(A)
+    perm = np.arange(n)
+    for i, p in enumerate(piv):
+        perm[[i, p]] = perm[[p, i]]
+    assert np.array_equal(perm, ipiv)
+
+
+@pytest.mark.parametrize("n,ni", [(376, 124), (3064, 1020)])
+def test_tall_panel_schur(n, ni, monkeypatch):
+    monkeypatch.setenv("DTN_PANEL_TALL_MIN", "1")
+    rng = np.random.default_rng(ni + 3)
+    A = rng.standard_normal((n, n))
+    out, ipiv, ps = gpu_partial_lu(A, ni)
+    S = A[ni:, ni:] - A[ni:, :ni] @ np.linalg.solve(A[:ni, :ni], A[:ni, ni:])
+    assert np.linalg.norm(out[ni:, ni:] - S) / np.linalg.norm(S) <= 1e-11
+
+
+@pytest.mark.parametrize("n", [8200, 16380])
+def test_tall_panel_beyond_cluster_limit(n):
+    """Beyond the cluster panel's 8192 rows the tall panel takes over by default
+    (the config-4 root LU for G = S^{-1} is 16380 x 16380)."""
+    rng = np.random.default_rng(n)
+    A = rng.standard_normal((n, n))
+    out, ipiv, ps = gpu_partial_lu(A, n)
+    _check_lu_by_products(A, out, ipiv, 1e-13)

@@ -155,6 +155,17 @@ def test_baseline_config2_full_size():
     assert O.rel_fro(dtn.apply_dtn(sol, g), ref.G @ g) <= 1e-10 * max(1.0, sol.cond_estimate)
 
 
+def test_baseline_config2_tall_panel(monkeypatch):
+    """The tall panel (global-memory pivot exchange, engine without the look-ahead)
+    forced on every interface LU of >= 1000 rows, root LU included: same bar as above."""
+    monkeypatch.setenv("DTN_PANEL_TALL_MIN", "1000")
+    sol, ref, g = _cfg_case(2, 512, 1, 16)
+    assert O.rel_fro(sol.S_dense, ref.S) <= TOL
+    nb = len(ref.boundary)
+    assert np.linalg.norm(ref.S @ sol.G_dense - np.eye(nb)) / np.sqrt(nb) <= 1e-10 * max(1.0, sol.cond_estimate)
+    assert O.rel_fro(dtn.apply_dtn(sol, g), ref.G @ g) <= 1e-10 * max(1.0, sol.cond_estimate)
+
+
 def test_reference_tree_baseline_size():
     # the reference's own 15/16/17-wide partition (build_tree(258, 289)) against the oracle
     n = 258
