@@ -61,12 +61,18 @@ __global__ void toplu(double* M, long long* cyc, int reps) {
         }
       }
     };
+    long long ta = clock64();
     chunk(std::integral_constant<int, 32>{});
+    long long tb = clock64();
     chunk(std::integral_constant<int, 24>{});
+    long long tc = clock64();
     chunk(std::integral_constant<int, 16>{});
+    long long td = clock64();
     chunk(std::integral_constant<int, 8>{});
     __syncwarp();
-    tot += clock64() - t0;
+    long long te = clock64();
+    tot += te - t0;
+    if (lane == 0 && r == reps - 1) { cyc[8 + 4 * V] = tb - ta; cyc[9 + 4 * V] = tc - tb; cyc[10 + 4 * V] = td - tc; cyc[11 + 4 * V] = te - td; }
   }
   double s = 0;
 #pragma unroll
@@ -78,12 +84,13 @@ int main() {
   double* M;
   long long* c;
   cudaMalloc(&M, 8 * 8192);
-  cudaMalloc(&c, 64);
+  cudaMalloc(&c, 8 * 32);
   toplu<0><<<1, 32>>>(M, c, 20);
   toplu<1><<<1, 32>>>(M, c, 20);
   toplu<2><<<1, 32>>>(M, c, 20);
-  long long h[3];
-  cudaMemcpy(h, c, 24, cudaMemcpyDeviceToHost);
+  long long h[32];
+  cudaMemcpy(h, c, sizeof(h), cudaMemcpyDeviceToHost);
+  for (int v = 0; v < 3; ++v) printf("variant %d chunks (8 steps each, W=32/24/16/8): %lld %lld %lld %lld\n", v, h[8 + 4 * v], h[9 + 4 * v], h[10 + 4 * v], h[11 + 4 * v]);
   printf("top LU 32x32, one warp: smem %lld cycles, shuffles %lld, smem without stores %lld (%s)\n", h[0], h[1], h[2],
          cudaGetErrorString(cudaGetLastError()));
   return 0;
