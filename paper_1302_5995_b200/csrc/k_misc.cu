@@ -199,7 +199,7 @@ cudaError_t launch_copy2d_batched(const void* d_descs, int count, cudaStream_t s
 // in register blocks (see update() on the accumulation order). The next group's
 // rows are updated first so its substitution overlaps the update of the rest.
 // bk is padded to a multiple of 32 (zero-filled T and Y rows).
-constexpr int TS_COLS = 64;
+constexpr int TS_COLS_MAX = 64;
 __host__ __device__ constexpr int ts_pad(int bk) { return (bk + 31) & ~31; }
 #ifdef TS_PROFILE
 __device__ long long g_ts_clk[16];
@@ -208,7 +208,7 @@ __device__ long long g_ts_clk[16];
 #define TSCLK(i) do { } while (0)
 #endif
 
-template <bool LOWER>
+template <bool LOWER, int TS_COLS>
 __global__ void __launch_bounds__(256, 2) trsm_block_kernel(const TrsmDesc* __restrict__ descs) {
   extern __shared__ __align__(16) double trsm_smem[];
   const TrsmDesc d = descs[blockIdx.y];
@@ -434,18 +434,33 @@ cudaError_t launch_trsm_upper_ref(const void* d_descs, int count, int max_cols, 
 
 size_t trsm_smem_bytes(int max_bk) {
   const int bkp = ts_pad(std::max(1, std::min(max_bk, TB)));
-  return size_t(bkp * (bkp + 2) + TS_COLS * (bkp + 2) + bkp) * sizeof(double);
+  return size_t(bkp * (bkp + 2) + TS_COLS_MAX * (bkp + 2) + bkp) * sizeof(double);
 }
 
 cudaError_t launch_trsm_batched(const void* d_descs, int count, int max_cols, int max_bk, bool lower,
                                 cudaStream_t st) {
   if (count <= 0 || max_cols <= 0) return cudaSuccess;
   if (max_bk > TB) return cudaErrorInvalidValue;
-  const dim3 grid((max_cols + TS_COLS - 1) / TS_COLS, count);
   const auto* dd = static_cast<const TrsmDesc*>(d_descs);
   const size_t sm = trsm_smem_bytes(max_bk);
-  if (lower) trsm_block_kernel<true><<<grid, 256, sm, st>>>(dd);
-  else trsm_block_kernel<false><<<grid, 256, sm, st>>>(dd);
+  // few CTAs (the tall, narrow back substitutions of the top merges): 32-column CTAs
+  // halve each CTA's serial work; otherwise 64 columns per CTA (the triangle staged once
+  // per 64 columns)
+  static const int narrow_env = [] {
+    const char* e = std::getenv("DTN_TRSM_NARROW");
+    return e ? std::atoi(e) : -1;
+  }();
+  const int tiles64 = (max_cols + 63) / 64 * count;
+  const bool narrow = narrow_env >= 0 ? narrow_env != 0 : tiles64 < 148;
+  if (narrow) {
+    const dim3 grid((max_cols + 31) / 32, count);
+    if (lower) trsm_block_kernel<true, 32><<<grid, 256, sm, st>>>(dd);
+    else trsm_block_kernel<false, 32><<<grid, 256, sm, st>>>(dd);
+  } else {
+    const dim3 grid((max_cols + 63) / 64, count);
+    if (lower) trsm_block_kernel<true, 64><<<grid, 256, sm, st>>>(dd);
+    else trsm_block_kernel<false, 64><<<grid, 256, sm, st>>>(dd);
+  }
   return cudaGetLastError();
 }
 
@@ -481,12 +496,12 @@ cudaError_t misc_init() {
   e = cudaFuncSetAttribute(trsm_upper_block_kernel_ref, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (TB * (TB + 1) + TB) * sizeof(double));
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(trsm_block_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           int(trsm_smem_bytes(TB)));
-
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(trsm_block_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              int(trsm_smem_bytes(TB)));
+  for (auto f : {trsm_block_kernel<false, 64>, trsm_block_kernel<true, 64>, trsm_block_kernel<false, 32>,
+                 trsm_block_kernel<true, 32>}) {
+    e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(trsm_smem_bytes(TB)));
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_tri_inv_blocks(const double* LU, int ldlu, int n, double* out, cudaStream_t st) {
