@@ -241,6 +241,60 @@ int dtn_gpu_hbs_deserialize(dtn_ctx* ctx, const uint8_t* buf, uint64_t size, dtn
  * in the root B), so dtn_gpu_hbs_apply on the result is apply_inverse (hbs_ops.cpp:203-205).
  * A singular block returns 3 with "<block> is singular [node t level l]". */
 int dtn_gpu_hbs_invert(const dtn_hbs* H, dtn_hbs** out);
+/* ---- the HBS algebra (hbs.hpp:71-90, hbs_ops.hpp:57-120, lowrank.hpp) ---------------
+ * Device-resident operations on dtn_hbs handles and low-rank blocks (csrc/hbs_ops.cu).
+ * Index trees are passed as 6 int64 per node (begin, end, left, right, parent, level), preorder,
+ * the dtn_gpu_hbs_tree layout. Factor transforms are exact; the operations that re-compress
+ * (add, from_lowrank, add_lowrank, rebase, split_at, consolidate) evaluate their operands on the
+ * device and compress onto the result's index tree (the reference's tree) at eps. Errors: 2 with
+ * the reference's message (e.g. "add_hbs: operands use different index trees").
+ *   dtn_gpu_hbs_compress_tree  compress(H, tree, eps)                 hbs.hpp:58-60, hbs.cpp:61-178
+ *   dtn_gpu_hbs_reconstruct    reconstruct(H): the dense M x M matrix  hbs.hpp:69, hbs.cpp:258-288
+ *   dtn_gpu_hbs_subtree        subtree_matrix(H, node)                 hbs.cpp:290-320
+ *   dtn_gpu_hbs_flip           flip(H) (index reversal, mirrored tree) hbs.cpp:322-375
+ *   dtn_gpu_hbs_scale(_rows/_cols)  scale / scale_rows / scale_cols, in place   hbs.cpp:377-402
+ *   dtn_gpu_hbs_add            add_hbs(A, B, eps) (same tree)          hbs_ops.cpp:386-404
+ *   dtn_gpu_hbs_from_lowrank   lowrank_to_bs(Q, R, tree)               hbs_ops.cpp:409-465
+ *   dtn_gpu_hbs_add_lowrank    add_lowrank(A, Q, R, eps)               hbs_ops.cpp:467-470
+ *   dtn_gpu_hbs_rebase         rebase(H, target, eps)                  hbs_ops.cpp:737-743
+ *   dtn_gpu_hbs_split_at       split_at(H, pos) with both sides consolidated: lo = H[:pos,:pos],
+ *                              hi = H[pos:,pos:] (NULL when empty), lo_hi / hi_lo the off-diagonal
+ *                              blocks                                  hbs_ops.cpp:620-640, 710-735
+ *   dtn_gpu_hbs_consolidate    consolidate(pieces at offsets tiling [0, size) + placed low-rank
+ *                              corrections (row, col offset pairs), eps)   hbs_ops.cpp:710-735
+ *   dtn_gpu_lowrank_*          LowRank L (m x k) R (k x n): lowrank_from_dense, lowrank_recompress,
+ *                              lowrank_sum of placed terms (offsets: row, col pairs)  lowrank.cpp:27-72 */
+typedef struct dtn_lowrank dtn_lowrank;
+int dtn_gpu_hbs_compress_tree(dtn_ctx* ctx, const double* H, int64_t M, int64_t ldh, int on_device, double eps,
+                              const int64_t* nodes, int64_t num_nodes, dtn_hbs** out);
+int dtn_gpu_hbs_reconstruct(const dtn_hbs* h, double* out, int64_t ldo, int on_device);
+int dtn_gpu_hbs_subtree(const dtn_hbs* h, int32_t node, dtn_hbs** out);
+int dtn_gpu_hbs_flip(const dtn_hbs* h, dtn_hbs** out);
+int dtn_gpu_hbs_scale(dtn_hbs* h, double s);
+int dtn_gpu_hbs_scale_rows(dtn_hbs* h, const double* w, int on_device);
+int dtn_gpu_hbs_scale_cols(dtn_hbs* h, const double* w, int on_device);
+int dtn_gpu_hbs_add(const dtn_hbs* A, const dtn_hbs* B, double eps, dtn_hbs** out);
+int dtn_gpu_hbs_from_lowrank(dtn_ctx* ctx, const double* Q, int64_t ldq, const double* R, int64_t ldr, int64_t k,
+                             const int64_t* nodes, int64_t num_nodes, int on_device, dtn_hbs** out);
+int dtn_gpu_hbs_add_lowrank(const dtn_hbs* A, const double* Q, int64_t ldq, const double* R, int64_t ldr, int64_t k,
+                            double eps, int on_device, dtn_hbs** out);
+int dtn_gpu_hbs_rebase(const dtn_hbs* h, const int64_t* nodes, int64_t num_nodes, double eps, dtn_hbs** out);
+int dtn_gpu_hbs_split_at(const dtn_hbs* h, int64_t pos, double eps, dtn_hbs** lo, dtn_hbs** hi, dtn_lowrank** lo_hi,
+                         dtn_lowrank** hi_lo);
+int dtn_gpu_hbs_consolidate(dtn_ctx* ctx, int64_t size, int64_t npieces, const dtn_hbs* const* pieces,
+                            const int64_t* offsets, int64_t ncorr, const dtn_lowrank* const* corr,
+                            const int64_t* corr_offsets, double eps, dtn_hbs** out);
+int dtn_gpu_lowrank_create(dtn_ctx* ctx, const double* L, int64_t ldl, const double* R, int64_t ldr, int64_t m,
+                           int64_t n, int64_t k, int on_device, dtn_lowrank** out);
+int dtn_gpu_lowrank_from_dense(dtn_ctx* ctx, const double* X, int64_t ldx, int64_t m, int64_t n, int on_device,
+                               double eps, dtn_lowrank** out);
+int dtn_gpu_lowrank_info(const dtn_lowrank* x, int64_t* m, int64_t* n, int64_t* k);
+int dtn_gpu_lowrank_get(const dtn_lowrank* x, double* L, int64_t ldl, double* R, int64_t ldr);
+int dtn_gpu_lowrank_recompress(const dtn_lowrank* x, double eps, dtn_lowrank** out);
+int dtn_gpu_lowrank_sum(dtn_ctx* ctx, int64_t m, int64_t n, int64_t nterms, const dtn_lowrank* const* terms,
+                        const int64_t* offsets, double eps, dtn_lowrank** out);
+void dtn_gpu_lowrank_free(dtn_lowrank* x);
+
 /* Compressed engine, build_root_accel (accel_nd.hpp:93-95, accel_nd.cpp:707-859) on the B200:
  * the root Schur complement S from the exact dense GPU merges, S_hbs = compress(S,
  * opts->epsilon, hbs_leaf) and G_hbs = invert_hbs(S_hbs) (accel_nd.cpp:820-822), cond = the

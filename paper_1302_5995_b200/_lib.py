@@ -55,6 +55,11 @@ EXPORTS = [
     "dtn_gpu_hbs_compress", "dtn_gpu_hbs_compress_op", "dtn_gpu_hbs_free", "dtn_gpu_hbs_info", "dtn_gpu_hbs_tree",
     "dtn_gpu_hbs_factor", "dtn_gpu_hbs_apply", "dtn_gpu_hbs_serialize", "dtn_gpu_hbs_deserialize",
     "dtn_gpu_hbs_invert", "dtn_gpu_build_accel", "dtn_gpu_root_rhs", "dtn_gpu_hbs_launch_count", "dtn_gpu_collective_flops",
+    "dtn_gpu_hbs_compress_tree", "dtn_gpu_hbs_reconstruct", "dtn_gpu_hbs_subtree", "dtn_gpu_hbs_flip",
+    "dtn_gpu_hbs_scale", "dtn_gpu_hbs_scale_rows", "dtn_gpu_hbs_scale_cols", "dtn_gpu_hbs_add",
+    "dtn_gpu_hbs_from_lowrank", "dtn_gpu_hbs_add_lowrank", "dtn_gpu_hbs_rebase", "dtn_gpu_hbs_split_at",
+    "dtn_gpu_hbs_consolidate", "dtn_gpu_lowrank_create", "dtn_gpu_lowrank_from_dense", "dtn_gpu_lowrank_info",
+    "dtn_gpu_lowrank_get", "dtn_gpu_lowrank_recompress", "dtn_gpu_lowrank_sum", "dtn_gpu_lowrank_free",
 ]
 
 _lib = None
@@ -119,5 +124,27 @@ def lib():
     L.dtn_gpu_hbs_launch_count.argtypes = []
     L.dtn_gpu_hbs_launch_count.restype = C.c_ulonglong
     L.dtn_gpu_build_accel.argtypes = [vp, vp, vp, i64, P(vp), P(vp), P(vp), P(f64)]
+    ci = C.c_int
+    L.dtn_gpu_hbs_compress_tree.argtypes = [vp, vp, i64, i64, ci, f64, vp, i64, P(vp)]
+    L.dtn_gpu_hbs_reconstruct.argtypes = [vp, vp, i64, ci]
+    L.dtn_gpu_hbs_subtree.argtypes = [vp, i32, P(vp)]
+    L.dtn_gpu_hbs_flip.argtypes = [vp, P(vp)]
+    L.dtn_gpu_hbs_scale.argtypes = [vp, f64]
+    L.dtn_gpu_hbs_scale_rows.argtypes = [vp, vp, ci]
+    L.dtn_gpu_hbs_scale_cols.argtypes = [vp, vp, ci]
+    L.dtn_gpu_hbs_add.argtypes = [vp, vp, f64, P(vp)]
+    L.dtn_gpu_hbs_from_lowrank.argtypes = [vp, vp, i64, vp, i64, i64, vp, i64, ci, P(vp)]
+    L.dtn_gpu_hbs_add_lowrank.argtypes = [vp, vp, i64, vp, i64, i64, f64, ci, P(vp)]
+    L.dtn_gpu_hbs_rebase.argtypes = [vp, vp, i64, f64, P(vp)]
+    L.dtn_gpu_hbs_split_at.argtypes = [vp, i64, f64, P(vp), P(vp), P(vp), P(vp)]
+    L.dtn_gpu_hbs_consolidate.argtypes = [vp, i64, i64, vp, vp, i64, vp, vp, f64, P(vp)]
+    L.dtn_gpu_lowrank_create.argtypes = [vp, vp, i64, vp, i64, i64, i64, i64, ci, P(vp)]
+    L.dtn_gpu_lowrank_from_dense.argtypes = [vp, vp, i64, i64, i64, ci, f64, P(vp)]
+    L.dtn_gpu_lowrank_info.argtypes = [vp, P(i64), P(i64), P(i64)]
+    L.dtn_gpu_lowrank_get.argtypes = [vp, vp, i64, vp, i64]
+    L.dtn_gpu_lowrank_recompress.argtypes = [vp, f64, P(vp)]
+    L.dtn_gpu_lowrank_sum.argtypes = [vp, i64, i64, i64, vp, vp, f64, P(vp)]
+    L.dtn_gpu_lowrank_free.argtypes = [vp]
+    L.dtn_gpu_lowrank_free.restype = None
     _lib = L
     return L

@@ -2704,6 +2704,307 @@ int dtn_gpu_hbs_invert(const dtn_hbs* h, dtn_hbs** out) {
   });
 }
 
+// ---- the HBS algebra (csrc/hbs_ops.cu): hbs.cpp:290-402, hbs_ops.cpp:213-743, lowrank.cpp
+struct dtn_lowrank {
+  dtn_ctx* ctx = nullptr;
+  std::unique_ptr<LowRankDev> x;
+};
+
+namespace {
+
+std::vector<HbsTreeNode> tree_from(const int64_t* nodes, int64_t num_nodes) {
+  if (!nodes || num_nodes < 1 || num_nodes > (int64_t(1) << 24)) throw std::invalid_argument("index tree: no nodes");
+  std::vector<HbsTreeNode> t(static_cast<size_t>(num_nodes));
+  for (int64_t i = 0; i < num_nodes; ++i) {
+    const int64_t* o = nodes + 6 * i;
+    t[size_t(i)].begin = o[0];
+    t[size_t(i)].end = o[1];
+    t[size_t(i)].left = int(o[2]);
+    t[size_t(i)].right = int(o[3]);
+    t[size_t(i)].parent = int(o[4]);
+    t[size_t(i)].level = int(o[5]);
+  }
+  return t;
+}
+
+// a host (or device) column-major matrix as a device pointer; host data staged into a
+// pooled buffer the holder frees
+struct DevMat {
+  const double* p = nullptr;
+  int64_t ld = 0;
+  void* own = nullptr;
+  DevMat(const double* src, int64_t lds, int64_t rows, int64_t cols, int on_device, cudaStream_t st) {
+    if (rows > 0 && cols > 0 && (!src || lds < rows)) throw std::invalid_argument("matrix: null pointer or ld < rows");
+    if (on_device || rows <= 0 || cols <= 0) {
+      p = src;
+      ld = std::max<int64_t>(lds, 1);
+      return;
+    }
+    ld = (rows + 1) & ~int64_t(1);
+    own = pool_alloc(size_t(ld) * size_t(cols) * 8);
+    CK(cudaMemcpy2DAsync(own, size_t(ld) * 8, src, size_t(lds) * 8, size_t(rows) * 8, size_t(cols),
+                         cudaMemcpyHostToDevice, st));
+    p = static_cast<const double*>(own);
+  }
+  ~DevMat() { pool_free(own); }
+};
+
+dtn_hbs* wrap(dtn_ctx* ctx, std::unique_ptr<HbsDev> h) {
+  auto* r = new dtn_hbs;
+  r->ctx = ctx;
+  r->h = std::move(h);
+  return r;
+}
+
+dtn_lowrank* wrap_lr(dtn_ctx* ctx, std::unique_ptr<LowRankDev> x) {
+  auto* r = new dtn_lowrank;
+  r->ctx = ctx;
+  r->x = std::move(x);
+  return r;
+}
+
+}  // namespace
+
+int dtn_gpu_hbs_compress_tree(dtn_ctx* ctx, const double* H, int64_t M, int64_t ldh, int on_device, double eps,
+                              const int64_t* nodes, int64_t num_nodes, dtn_hbs** out) {
+  if (!ctx || !out) return DTN_EINVAL;
+  return guarded(ctx, [&] {
+    *out = nullptr;
+    if (!H || M < 1 || ldh < M) throw std::invalid_argument("compress: matrix/tree size mismatch");
+    CK(cudaSetDevice(ctx->device));
+    const auto tree = tree_from(nodes, num_nodes);
+    DevMat X(H, ldh, M, M, on_device, ctx->stream);
+    *out = wrap(ctx, hbs_compress_tree(X.p, X.ld, M, eps, tree, ctx->stream));
+  });
+}
+
+int dtn_gpu_hbs_reconstruct(const dtn_hbs* h, double* out, int64_t ldo, int on_device) {
+  if (!h || !h->h || !out) return DTN_EINVAL;
+  dtn_ctx* ctx = h->ctx;
+  return guarded(ctx, [&] {
+    const int64_t M = h->h->M;
+    if (ldo < M) throw std::invalid_argument("reconstruct: ld < M");
+    CK(cudaSetDevice(ctx->device));
+    if (on_device) {
+      hbs_dense(*h->h, out, ldo, ctx->stream);
+      return;
+    }
+    const int64_t L = (M + 1) & ~int64_t(1);
+    void* tmp = pool_alloc(size_t(L) * size_t(M) * 8);
+    try {
+      hbs_dense(*h->h, static_cast<double*>(tmp), L, ctx->stream);
+      CK(cudaMemcpy2DAsync(out, size_t(ldo) * 8, tmp, size_t(L) * 8, size_t(M) * 8, size_t(M), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+      pool_free(tmp);
+      throw;
+    }
+    pool_free(tmp);
+  });
+}
+
+int dtn_gpu_hbs_subtree(const dtn_hbs* h, int32_t node, dtn_hbs** out) {
+  if (!h || !h->h || !out) return DTN_EINVAL;
+  return guarded(h->ctx, [&] {
+    *out = nullptr;
+    CK(cudaSetDevice(h->ctx->device));
+    *out = wrap(h->ctx, hbs_subtree(*h->h, node, h->ctx->stream));
+  });
+}
+
+int dtn_gpu_hbs_flip(const dtn_hbs* h, dtn_hbs** out) {
+  if (!h || !h->h || !out) return DTN_EINVAL;
+  return guarded(h->ctx, [&] {
+    *out = nullptr;
+    CK(cudaSetDevice(h->ctx->device));
+    *out = wrap(h->ctx, hbs_flip(*h->h, h->ctx->stream));
+  });
+}
+
+namespace {
+int scale_common(dtn_hbs* h, double s, const double* w, int on_device, int side) {
+  if (!h || !h->h) return DTN_EINVAL;
+  dtn_ctx* ctx = h->ctx;
+  return guarded(ctx, [&] {
+    CK(cudaSetDevice(ctx->device));
+    const int64_t M = h->h->M;
+    if (side != 0 && !w) throw std::invalid_argument("scale: null weights");
+    DevMat W(w, M, M, side != 0 ? 1 : 0, on_device, ctx->stream);
+    hbs_scale(*h->h, s, side == 1 ? W.p : nullptr, side == 2 ? W.p : nullptr, ctx->stream);
+  });
+}
+}  // namespace
+
+int dtn_gpu_hbs_scale(dtn_hbs* h, double s) { return scale_common(h, s, nullptr, 1, 0); }
+int dtn_gpu_hbs_scale_rows(dtn_hbs* h, const double* w, int on_device) { return scale_common(h, 1.0, w, on_device, 1); }
+int dtn_gpu_hbs_scale_cols(dtn_hbs* h, const double* w, int on_device) { return scale_common(h, 1.0, w, on_device, 2); }
+
+int dtn_gpu_hbs_add(const dtn_hbs* A, const dtn_hbs* B, double eps, dtn_hbs** out) {
+  if (!A || !A->h || !B || !B->h || !out) return DTN_EINVAL;
+  return guarded(A->ctx, [&] {
+    *out = nullptr;
+    if (!(eps >= 0.0)) throw std::invalid_argument("add_hbs: eps must be >= 0");
+    CK(cudaSetDevice(A->ctx->device));
+    *out = wrap(A->ctx, hbs_add(*A->h, *B->h, eps, A->ctx->stream));
+  });
+}
+
+int dtn_gpu_hbs_from_lowrank(dtn_ctx* ctx, const double* Q, int64_t ldq, const double* R, int64_t ldr, int64_t k,
+                             const int64_t* nodes, int64_t num_nodes, int on_device, dtn_hbs** out) {
+  if (!ctx || !out) return DTN_EINVAL;
+  return guarded(ctx, [&] {
+    *out = nullptr;
+    CK(cudaSetDevice(ctx->device));
+    const auto tree = tree_from(nodes, num_nodes);
+    const int64_t M = tree[0].end;
+    if (k < 0) throw std::invalid_argument("lowrank_to_bs: negative rank");
+    DevMat q(Q, ldq, M, k, on_device, ctx->stream), r(R, ldr, k, M, on_device, ctx->stream);
+    *out = wrap(ctx, hbs_from_lowrank(q.p, q.ld, r.p, r.ld, k, tree, ctx->stream));
+  });
+}
+
+int dtn_gpu_hbs_add_lowrank(const dtn_hbs* A, const double* Q, int64_t ldq, const double* R, int64_t ldr, int64_t k,
+                            double eps, int on_device, dtn_hbs** out) {
+  if (!A || !A->h || !out) return DTN_EINVAL;
+  dtn_ctx* ctx = A->ctx;
+  return guarded(ctx, [&] {
+    *out = nullptr;
+    CK(cudaSetDevice(ctx->device));
+    const int64_t M = A->h->M;
+    if (k < 0) throw std::invalid_argument("add_lowrank: negative rank");
+    DevMat q(Q, ldq, M, k, on_device, ctx->stream), r(R, ldr, k, M, on_device, ctx->stream);
+    *out = wrap(ctx, hbs_add_lowrank(*A->h, q.p, q.ld, r.p, r.ld, k, eps, ctx->stream));
+  });
+}
+
+int dtn_gpu_hbs_rebase(const dtn_hbs* h, const int64_t* nodes, int64_t num_nodes, double eps, dtn_hbs** out) {
+  if (!h || !h->h || !out) return DTN_EINVAL;
+  return guarded(h->ctx, [&] {
+    *out = nullptr;
+    CK(cudaSetDevice(h->ctx->device));
+    *out = wrap(h->ctx, hbs_rebase(*h->h, tree_from(nodes, num_nodes), eps, h->ctx->stream));
+  });
+}
+
+int dtn_gpu_hbs_split_at(const dtn_hbs* h, int64_t pos, double eps, dtn_hbs** lo, dtn_hbs** hi, dtn_lowrank** lo_hi,
+                         dtn_lowrank** hi_lo) {
+  if (!h || !h->h || !lo || !hi || !lo_hi || !hi_lo) return DTN_EINVAL;
+  dtn_ctx* ctx = h->ctx;
+  return guarded(ctx, [&] {
+    *lo = *hi = nullptr;
+    *lo_hi = *hi_lo = nullptr;
+    CK(cudaSetDevice(ctx->device));
+    SplitDev sp = hbs_split_at(*h->h, pos, eps, ctx->stream);
+    if (sp.lo) *lo = wrap(ctx, std::move(sp.lo));
+    if (sp.hi) *hi = wrap(ctx, std::move(sp.hi));
+    *lo_hi = wrap_lr(ctx, std::move(sp.lo_hi));
+    *hi_lo = wrap_lr(ctx, std::move(sp.hi_lo));
+  });
+}
+
+int dtn_gpu_hbs_consolidate(dtn_ctx* ctx, int64_t size, int64_t npieces, const dtn_hbs* const* pieces,
+                            const int64_t* offsets, int64_t ncorr, const dtn_lowrank* const* corr,
+                            const int64_t* corr_offsets, double eps, dtn_hbs** out) {
+  if (!ctx || !out) return DTN_EINVAL;
+  return guarded(ctx, [&] {
+    *out = nullptr;
+    if (npieces < 1 || !pieces || !offsets) throw std::invalid_argument("consolidate: no pieces");
+    if (ncorr < 0 || (ncorr > 0 && (!corr || !corr_offsets))) throw std::invalid_argument("consolidate: bad corrections");
+    CK(cudaSetDevice(ctx->device));
+    std::vector<const HbsDev*> p;
+    std::vector<int64_t> o(offsets, offsets + npieces);
+    for (int64_t i = 0; i < npieces; ++i) p.push_back(pieces[i] && pieces[i]->h ? pieces[i]->h.get() : nullptr);
+    std::vector<LowRankPlaced> cs;
+    for (int64_t i = 0; i < ncorr; ++i) {
+      if (!corr[i] || !corr[i]->x) throw std::invalid_argument("consolidate: null correction");
+      cs.push_back(LowRankPlaced{corr_offsets[2 * i], corr_offsets[2 * i + 1], corr[i]->x.get()});
+    }
+    *out = wrap(ctx, hbs_consolidate(size, p, o, cs, eps, ctx->stream));
+  });
+}
+
+int dtn_gpu_lowrank_create(dtn_ctx* ctx, const double* Lf, int64_t ldl, const double* R, int64_t ldr, int64_t m,
+                           int64_t n, int64_t k, int on_device, dtn_lowrank** out) {
+  if (!ctx || !out) return DTN_EINVAL;
+  return guarded(ctx, [&] {
+    *out = nullptr;
+    if (m < 0 || n < 0 || k < 0) throw std::invalid_argument("lowrank: negative dimension");
+    CK(cudaSetDevice(ctx->device));
+    DevMat l(Lf, ldl, m, k, on_device, ctx->stream), r(R, ldr, k, n, on_device, ctx->stream);
+    *out = wrap_lr(ctx, lowrank_from_factors(l.p, l.ld, r.p, r.ld, m, n, k, ctx->stream));
+  });
+}
+
+int dtn_gpu_lowrank_from_dense(dtn_ctx* ctx, const double* X, int64_t ldx, int64_t m, int64_t n, int on_device,
+                               double eps, dtn_lowrank** out) {
+  if (!ctx || !out) return DTN_EINVAL;
+  return guarded(ctx, [&] {
+    *out = nullptr;
+    if (m < 0 || n < 0) throw std::invalid_argument("lowrank: negative dimension");
+    CK(cudaSetDevice(ctx->device));
+    DevMat x(X, ldx, m, n, on_device, ctx->stream);
+    *out = wrap_lr(ctx, lowrank_from_dense(x.p, x.ld, m, n, eps, ctx->stream));
+  });
+}
+
+int dtn_gpu_lowrank_info(const dtn_lowrank* x, int64_t* m, int64_t* n, int64_t* k) {
+  if (!x || !x->x) return DTN_EINVAL;
+  if (m) *m = x->x->m;
+  if (n) *n = x->x->n;
+  if (k) *k = x->x->k;
+  return DTN_OK;
+}
+
+int dtn_gpu_lowrank_get(const dtn_lowrank* x, double* Lf, int64_t ldl, double* R, int64_t ldr) {
+  if (!x || !x->x) return DTN_EINVAL;
+  dtn_ctx* ctx = x->ctx;
+  return guarded(ctx, [&] {
+    const LowRankDev& a = *x->x;
+    CK(cudaSetDevice(ctx->device));
+    if (Lf && a.m > 0 && a.k > 0) {
+      if (ldl < a.m) throw std::invalid_argument("lowrank_get: ldl < m");
+      CK(cudaMemcpy2D(Lf, size_t(ldl) * 8, a.L, size_t(a.ldl) * 8, size_t(a.m) * 8, size_t(a.k), cudaMemcpyDeviceToHost));
+    }
+    if (R && a.k > 0 && a.n > 0) {
+      if (ldr < a.k) throw std::invalid_argument("lowrank_get: ldr < k");
+      CK(cudaMemcpy2D(R, size_t(ldr) * 8, a.R, size_t(a.ldr) * 8, size_t(a.k) * 8, size_t(a.n), cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+int dtn_gpu_lowrank_recompress(const dtn_lowrank* x, double eps, dtn_lowrank** out) {
+  if (!x || !x->x || !out) return DTN_EINVAL;
+  return guarded(x->ctx, [&] {
+    *out = nullptr;
+    CK(cudaSetDevice(x->ctx->device));
+    *out = wrap_lr(x->ctx, lowrank_recompress(*x->x, eps, x->ctx->stream));
+  });
+}
+
+int dtn_gpu_lowrank_sum(dtn_ctx* ctx, int64_t m, int64_t n, int64_t nterms, const dtn_lowrank* const* terms,
+                        const int64_t* offsets, double eps, dtn_lowrank** out) {
+  if (!ctx || !out) return DTN_EINVAL;
+  return guarded(ctx, [&] {
+    *out = nullptr;
+    if (m < 0 || n < 0 || nterms < 0 || (nterms > 0 && (!terms || !offsets)))
+      throw std::invalid_argument("lowrank_sum: bad arguments");
+    CK(cudaSetDevice(ctx->device));
+    std::vector<LowRankPlaced> t;
+    for (int64_t i = 0; i < nterms; ++i) {
+      if (!terms[i] || !terms[i]->x) throw std::invalid_argument("lowrank_sum: null term");
+      t.push_back(LowRankPlaced{offsets[2 * i], offsets[2 * i + 1], terms[i]->x.get()});
+    }
+    *out = wrap_lr(ctx, lowrank_sum(m, n, t, eps, ctx->stream));
+  });
+}
+
+void dtn_gpu_lowrank_free(dtn_lowrank* x) {
+  if (!x) return;
+  if (x->ctx) cudaSetDevice(x->ctx->device);
+  delete x;
+}
+
 int dtn_gpu_build_accel(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, int64_t hbs_leaf, dtn_op** op_out,
                         dtn_hbs** S_hbs, dtn_hbs** G_hbs, double* cond) {
   if (!ctx || !prob || !opts || !S_hbs || !G_hbs) return DTN_EINVAL;

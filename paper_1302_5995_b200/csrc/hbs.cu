@@ -109,170 +109,21 @@ void pool_free(void* p) {
   P.live_.erase(it);
 }
 
-namespace {
-template <class T>
-void pmalloc(T** p, size_t bytes) {
-  *p = static_cast<T*>(pool_alloc(bytes));
-}
-}  // namespace
+}  // namespace dtnb
 
-cudaError_t launch_gemm_desc(const GemmDesc* d_descs, int count, int max_tiles, int kmax, double alpha, double beta,
-                             cudaStream_t st, bool a_aligned, bool allow_big = true);
-cudaError_t launch_gemm_desc_tc(const GemmDesc* d_descs, int count, int max_tiles, int kmax, double alpha, double beta,
-                                cudaStream_t st);
-cudaError_t launch_gemm_desc2(const GemmDesc2* d_descs, int count, int max_tiles, bool tc, cudaStream_t st);
-int gemm_tiles(int m, int n);
-cudaError_t launch_hqr(const QrDesc* d_descs, int count, int max_m, int max_nc, const double* d_eps, cudaStream_t st,
-                       bool pivoted);
-cudaError_t launch_fill_uniform(double* X, int ldx, int rows, int cols, unsigned long long seed, cudaStream_t st);
-cudaError_t launch_copy2d_batched(const void* d_descs, int count, cudaStream_t st);
-cudaError_t launch_sum_slices(double* base, long long stride, int slices, long long count, cudaStream_t st);
+#include "hbs_impl.hpp"
 
-// kernel launches issued by the HBS code (compress, invert, apply), process-wide
+namespace dtnb {
+
+// kernel launches issued by the HBS code (compress, invert, apply, algebra), process-wide
 std::atomic<unsigned long long> g_hbs_launches{0};
-
-namespace {
-#define HLK(x)                    \
-  do {                            \
-    HCK(x);                       \
-    g_hbs_launches.fetch_add(1);  \
-  } while (0)
-
-#define HCK(x)                                                                                        \
-  do {                                                                                                \
-    const cudaError_t e_ = (x);                                                                       \
-    if (e_ != cudaSuccess) throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e_) + \
-                                                    " at " #x);                                       \
-  } while (0)
-
-inline int64_t align2(int64_t x) { return (x + 1) & ~int64_t(1); }
-
-// Device scratch for descriptors and staging: every get() is a FRESH region (a bump
-// allocator over pooled chunks), never reused while the owning call runs, so a launch
-// never waits for the previous one to have read its descriptors (no synchronisation
-// between batches). The owner synchronises its stream before the chunks return to the
-// pool (every user ends with a stream synchronisation).
-struct DevBuf {
-  std::vector<void*> chunks;
-  char* cur = nullptr;
-  size_t cap = 0, off = 0;
-  ~DevBuf() {
-    for (void* c : chunks) pool_free(c);
-  }
-  void* get(size_t bytes) {
-    bytes = (std::max<size_t>(bytes, 1) + 255) & ~size_t(255);
-    if (!cur || off + bytes > cap) {
-      const size_t c = std::max<size_t>(bytes, size_t(1) << 20);
-      void* q = nullptr;
-      pmalloc(&q, c);
-      chunks.push_back(q);
-      cur = static_cast<char*>(q);
-      cap = c;
-      off = 0;
-    }
-    void* r = cur + off;
-    off += bytes;
-    return r;
-  }
-};
-
-// host descriptors -> device, then launch
-template <class T>
-T* upload(DevBuf& buf, const std::vector<T>& v, cudaStream_t st) {
-  T* d = static_cast<T*>(buf.get(v.size() * sizeof(T)));
-  if (!v.empty()) HCK(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
-  return d;
-}
-
-void gemm_batch(DevBuf& buf, const std::vector<GemmDesc>& g, double alpha, double beta, bool a_aligned,
-                cudaStream_t st) {
-  if (g.empty()) return;
-  int tiles = 0, kmax = 0;
-  for (const auto& d : g) {
-    if (d.m <= 0 || d.n <= 0) continue;
-    tiles = std::max(tiles, gemm_tiles(d.m, d.n));
-    kmax = std::max(kmax, d.k);
-  }
-  if (tiles == 0) return;
-  GemmDesc* dd = upload(buf, g, st);
-  HLK(launch_gemm_desc(dd, int(g.size()), tiles, kmax, alpha, beta, st, a_aligned));
-}
-
-void transpose_batch(DevBuf& buf, const std::vector<TransDesc>& t, cudaStream_t st) {
-  if (t.empty()) return;
-  int tiles = 0;
-  for (const auto& d : t) tiles = std::max(tiles, ((d.m + 31) / 32) * ((d.n + 31) / 32));
-  TransDesc* dd = upload(buf, t, st);
-  HLK(launch_transpose_batched(dd, int(t.size()), tiles, st));
-}
-
-void copy_batch(DevBuf& buf, const std::vector<CopyDesc>& c, cudaStream_t st) {
-  if (c.empty()) return;
-  // large blocks (the M x M working matrix) go through the copy engine; the
-  // batched kernel is for many small blocks
-  std::vector<CopyDesc> small;
-  for (const auto& d : c) {
-    if (int64_t(d.m) * d.n >= (int64_t(1) << 20))
-      HCK(cudaMemcpy2DAsync(d.dst, size_t(d.ldd) * 8, d.src, size_t(d.lds) * 8, size_t(d.m) * 8, size_t(d.n),
-                            cudaMemcpyDeviceToDevice, st));
-    else if (d.m > 0 && d.n > 0)
-      small.push_back(d);
-  }
-  if (!small.empty()) {
-    CopyDesc* dd = upload(buf, small, st);
-    HLK(launch_copy2d_batched(dd, int(small.size()), st));
-  }
-}
-
-// Grow-only device scratch of the compression (the M x M work matrices are
-// 2 GB each at M = 16380): kept per device between calls instead of
-// cudaMalloc/cudaFree per call; one compression at a time per device.
-struct Scratch {
-  std::mutex m;
-  std::vector<std::pair<void*, size_t>> slot;
-  void* get(int i, size_t bytes) {
-    if (int(slot.size()) <= i) slot.resize(i + 1, {nullptr, 0});
-    auto& e = slot[i];
-    if (e.second < bytes) {
-      if (e.first) pool_free(e.first);
-      e = {nullptr, 0};
-      pmalloc(&e.first, bytes);
-      e.second = bytes;
-    }
-    return e.first;
-  }
-};
-
-// Owned factor storage of one HbsDev, handed out from a few large chunks
-// (one cudaMalloc per chunk instead of one per tree level and factor kind).
-struct Arena {
-  HbsDev& H;
-  size_t chunk;
-  double* cur = nullptr;
-  size_t left = 0;
-  Arena(HbsDev& h, size_t first_chunk_doubles) : H(h), chunk(std::max<size_t>(first_chunk_doubles, 1 << 16)) {}
-  double* alloc(size_t doubles) {
-    doubles = (doubles + 1) & ~size_t(1);  // keep 16-byte alignment
-    if (doubles > left) {
-      const size_t sz = std::max(doubles, chunk);
-      void* p = nullptr;
-      pmalloc(&p, sz * 8);
-      H.buffers.push_back(p);
-      cur = static_cast<double*>(p);
-      left = sz;
-      chunk *= 2;
-    }
-    double* r = cur;
-    cur += doubles;
-    left -= doubles;
-    return r;
-  }
-};
 
 Scratch& scratch(int device) {
   static Scratch s[64];
   return s[device & 63];
 }
+
+namespace {
 
 // DTN_HBS_TRACE=1: per-phase host timings of compress (after each synchronisation)
 struct Trace {
@@ -369,13 +220,47 @@ bool use_jacobi_bases() {
 std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, double eps, int64_t leaf_cap,
                                      cudaStream_t st) {
   if (M < 1 || ldh < M) throw std::invalid_argument("compress: matrix/tree size mismatch");
+  int depth = 0;
+  auto nodes = hbs_index_tree(M, leaf_cap, &depth);
+  return hbs_compress_tree(dH, ldh, M, eps, nodes, st);
+}
+
+void hbs_check_tree(const std::vector<HbsTreeNode>& nodes, int64_t M, const char* what) {
+  const std::string w = std::string(what) + ": ";
+  const int64_t nn = int64_t(nodes.size());
+  if (nn < 1 || nodes[0].begin != 0 || nodes[0].end != M || nodes[0].parent != -1)
+    throw std::invalid_argument(w + "tree does not cover [0, M)");
+  for (int t = 0; t < int(nn); ++t) {
+    const auto& n = nodes[size_t(t)];
+    if ((n.left < 0) != (n.right < 0) || n.left >= nn || n.right >= nn || n.left == 0 || n.right == 0)
+      throw std::invalid_argument(w + "bad tree");
+    if (n.begin < 0 || n.end <= n.begin || n.end > M) throw std::invalid_argument(w + "bad tree");
+    if (n.left >= 0) {  // children partition the parent's range, preorder ids (index_tree.cpp:37-67)
+      const auto& l = nodes[size_t(n.left)];
+      const auto& r = nodes[size_t(n.right)];
+      if (n.left <= t || n.right <= t || l.parent != t || r.parent != t || l.begin != n.begin || l.end != r.begin ||
+          r.end != n.end || l.level != n.level + 1 || r.level != n.level + 1)
+        throw std::invalid_argument(w + "bad tree");
+    }
+  }
+}
+
+std::unique_ptr<HbsDev> hbs_compress_tree(const double* dH, int64_t ldh, int64_t M, double eps,
+                                          const std::vector<HbsTreeNode>& tree, cudaStream_t st) {
+  if (M < 1 || ldh < M) throw std::invalid_argument("compress: matrix/tree size mismatch");
   if (!(eps >= 0.0)) throw std::invalid_argument("compress: eps must be >= 0");
   if (M > (int64_t(1) << 30) / 2) throw std::invalid_argument("compress: matrix too large");
+  hbs_check_tree(tree, M, "compress");
   auto out = std::make_unique<HbsDev>();
   HbsDev& H = *out;
   HCK(cudaGetDevice(&H.device));
   H.M = M;
-  H.nodes = hbs_index_tree(M, leaf_cap, &H.depth);
+  H.nodes = tree;
+  H.depth = 0;
+  for (const auto& n : tree) H.depth = std::max(H.depth, n.level);
+  int64_t leaf_cap = 2;  // scratch sizing: the largest leaf
+  for (int t = 0; t < int(tree.size()); ++t)
+    if (tree[size_t(t)].left < 0) leaf_cap = std::max<int64_t>(leaf_cap, tree[size_t(t)].end - tree[size_t(t)].begin);
   const int nn = int(H.nodes.size());
   H.rank.assign(nn, 0);
   H.rows.assign(nn, 0);
@@ -1188,19 +1073,7 @@ std::unique_ptr<HbsDev> hbs_deserialize(const uint8_t* data, size_t size, cudaSt
     n.level = int(rd.i64());
   }
   if (H.nodes[0].end != H.M || H.nodes[0].begin != 0) throw std::invalid_argument("deserialize: bad header");
-  for (int t = 0; t < int(nn); ++t) {
-    const auto& n = H.nodes[t];
-    if ((n.left < 0) != (n.right < 0) || n.left >= nn || n.right >= nn || n.left == 0 || n.right == 0)
-      throw std::invalid_argument("deserialize: bad tree");
-    if (n.begin < 0 || n.end <= n.begin || n.end > H.M) throw std::invalid_argument("deserialize: bad tree");
-    if (n.left >= 0) {  // children partition the parent's range (index_tree.cpp:37-67)
-      const auto& l = H.nodes[n.left];
-      const auto& r = H.nodes[n.right];
-      if (n.left <= t || n.right <= t || l.parent != t || r.parent != t || l.begin != n.begin || l.end != r.begin ||
-          r.end != n.end || l.level != n.level + 1 || r.level != n.level + 1)
-        throw std::invalid_argument("deserialize: bad tree");
-    }
-  }
+  hbs_check_tree(H.nodes, H.M, "deserialize");
   H.rank.assign(nn, 0);
   H.rows.assign(nn, 0);
   H.height.assign(nn, 0);

@@ -139,6 +139,12 @@ struct HbsDev {
 std::unique_ptr<HbsDev> hbs_compress(const double* dH, int64_t ldh, int64_t M, double eps, int64_t leaf_cap,
                                      cudaStream_t st);
 
+// compress(H, tree, eps) (hbs.hpp:58-60, hbs.cpp:61-178) onto a given index tree
+// (preorder, children partition their parent: checked, std::invalid_argument).
+std::unique_ptr<HbsDev> hbs_compress_tree(const double* dH, int64_t ldh, int64_t M, double eps,
+                                          const std::vector<HbsTreeNode>& tree, cudaStream_t st);
+void hbs_check_tree(const std::vector<HbsTreeNode>& nodes, int64_t M, const char* what);
+
 // Y (M x nrhs) = H X through the telescoping factorization (hbs.cpp:187-232);
 // X, Y device pointers.
 // allow_graph = false: launch the sweep directly (one-off applies: capturing and
@@ -157,6 +163,52 @@ struct HbsSingular : std::runtime_error {
 // core inverse (B_root + diag(Dhat))^{-1} in the root B -- so hbs_apply on
 // the result is apply_inverse (hbs_ops.cpp:203-205).
 std::unique_ptr<HbsDev> hbs_invert(const HbsDev& H, cudaStream_t st);
+
+// ---- the HBS algebra (hbs_ops.cu): hbs.cpp:290-402, hbs_ops.cpp:213-743, lowrank.cpp
+// Low-rank block L R (L m x k, R k x n, column-major, device; LowRank, lowrank.hpp).
+struct LowRankDev {
+  int device = -1;
+  int64_t m = 0, n = 0, k = 0, ldl = 2, ldr = 2;
+  double* L = nullptr;
+  double* R = nullptr;
+  void* buf = nullptr;
+  LowRankDev() = default;
+  LowRankDev(const LowRankDev&) = delete;
+  LowRankDev& operator=(const LowRankDev&) = delete;
+  ~LowRankDev();
+};
+struct LowRankPlaced {  // PlacedLowRank (lowrank.hpp): a block at (row_offset, col_offset)
+  int64_t row_offset = 0, col_offset = 0;
+  const LowRankDev* lr = nullptr;
+};
+struct SplitDev {  // SplitParts (hbs_ops.hpp) with both accumulations consolidated
+  std::unique_ptr<HbsDev> lo, hi;
+  std::unique_ptr<LowRankDev> lo_hi, hi_lo;
+};
+std::unique_ptr<HbsDev> hbs_subtree(const HbsDev& H, int t, cudaStream_t st);
+std::unique_ptr<HbsDev> hbs_copy(const HbsDev& H, cudaStream_t st);
+std::unique_ptr<HbsDev> hbs_flip(const HbsDev& H, cudaStream_t st);
+void hbs_scale(HbsDev& H, double s, const double* d_wrow, const double* d_wcol, cudaStream_t st);
+void hbs_dense(const HbsDev& H, double* dX, int64_t ldx, cudaStream_t st);
+std::unique_ptr<HbsDev> hbs_add(const HbsDev& A, const HbsDev& B, double eps, cudaStream_t st);
+std::unique_ptr<HbsDev> hbs_from_lowrank(const double* dQ, int64_t ldq, const double* dR, int64_t ldr, int64_t k,
+                                         const std::vector<HbsTreeNode>& tree, cudaStream_t st);
+std::unique_ptr<HbsDev> hbs_add_lowrank(const HbsDev& A, const double* dQ, int64_t ldq, const double* dR, int64_t ldr,
+                                        int64_t k, double eps, cudaStream_t st);
+std::unique_ptr<HbsDev> hbs_rebase(const HbsDev& H, const std::vector<HbsTreeNode>& target, double eps,
+                                   cudaStream_t st);
+SplitDev hbs_split_at(const HbsDev& H, int64_t pos, double eps, cudaStream_t st);
+std::unique_ptr<HbsDev> hbs_consolidate(int64_t size, const std::vector<const HbsDev*>& pieces,
+                                        const std::vector<int64_t>& offsets, const std::vector<LowRankPlaced>& corr,
+                                        double eps, cudaStream_t st);
+std::unique_ptr<LowRankDev> lowrank_alloc(int64_t m, int64_t n, int64_t k);
+std::unique_ptr<LowRankDev> lowrank_from_factors(const double* dL, int64_t ldl, const double* dR, int64_t ldr,
+                                                 int64_t m, int64_t n, int64_t k, cudaStream_t st);
+std::unique_ptr<LowRankDev> lowrank_recompress(const LowRankDev& x, double eps, cudaStream_t st);
+std::unique_ptr<LowRankDev> lowrank_from_dense(const double* dX, int64_t ldx, int64_t m, int64_t n, double eps,
+                                               cudaStream_t st);
+std::unique_ptr<LowRankDev> lowrank_sum(int64_t m, int64_t n, const std::vector<LowRankPlaced>& terms, double eps,
+                                        cudaStream_t st);
 
 // DTNHBS01 serialization (hbs.cpp:422-519), byte-for-byte the reference layout.
 std::vector<uint8_t> hbs_serialize(const HbsDev& H, cudaStream_t st);

@@ -18,7 +18,10 @@ from .dtn import Context, default_context
 
 __all__ = ["IndexTree", "build_index_tree", "HbsMatrix", "InverseFactors", "compress", "compress_operator", "apply",
            "invert_hbs", "apply_inverse", "reconstruct",
-           "serialize", "deserialize", "write_hbs", "read_hbs", "basis_orthonormality_defect"]
+           "serialize", "deserialize", "write_hbs", "read_hbs", "basis_orthonormality_defect",
+           "mirror", "subtree_matrix", "flip", "scale", "scale_rows", "scale_cols", "add_hbs", "lowrank_to_bs",
+           "add_lowrank", "rebase", "SplitParts", "split_at", "consolidate", "LowRank", "Placed",
+           "lowrank_from_dense", "lowrank_recompress", "lowrank_sum"]
 
 
 @dataclass
@@ -207,11 +210,21 @@ def _ctx(ctx):
     return ctx if ctx is not None else default_context()
 
 
-def compress(H, eps: float, leaf_cap: int = 64, ctx: Context | None = None) -> HbsMatrix:
+def compress(H, eps: float, leaf_cap: int = 64, ctx: Context | None = None,
+             tree: IndexTree | None = None) -> HbsMatrix:
     """compress(H, eps, leaf_cap) (hbs.hpp:58-62): H is a host array or a
-    float64 CUDA tensor (column-major or row-major contiguous)."""
+    float64 CUDA tensor (column-major or row-major contiguous). With `tree`:
+    compress(H, tree, eps) onto that index tree (hbs.hpp:58-60)."""
     ctx = _ctx(ctx)
     out = C.c_void_p()
+    if tree is not None:
+        A = np.asfortranarray(np.asarray(H, dtype=np.float64))
+        if A.ndim != 2 or A.shape[0] != A.shape[1] or A.shape[0] != tree.size():
+            raise ValueError("compress: matrix/tree size mismatch")
+        t = _tree_array(tree)
+        ctx.check(L.lib().dtn_gpu_hbs_compress_tree(ctx.h, A.ctypes.data, A.shape[0], A.shape[0], 0, float(eps),
+                                                    t.ctypes.data, t.shape[0], C.byref(out)))
+        return HbsMatrix(ctx, out)
     try:
         import torch
         is_t = isinstance(H, torch.Tensor)
@@ -280,7 +293,10 @@ def apply(H: HbsMatrix, x):
 def reconstruct(H: HbsMatrix) -> np.ndarray:
     """Exact dense evaluation of the stored factorization (hbs.hpp:69, a testing
     aid): the telescoping apply of the identity, on the device."""
-    return apply(H, np.eye(H.size()))
+    M = H.size()
+    out = np.zeros((M, M), dtype=np.float64, order="F")
+    H.ctx.check(L.lib().dtn_gpu_hbs_reconstruct(H.h, out.ctypes.data, M, 0))
+    return out
 
 
 def basis_orthonormality_defect(H: HbsMatrix) -> float:
@@ -325,3 +341,258 @@ def write_hbs(H: HbsMatrix, path: str) -> None:
 def read_hbs(path: str, ctx: Context | None = None) -> HbsMatrix:
     with open(path, "rb") as f:
         return deserialize(f.read(), ctx)
+
+
+# ---------------------------------------------------------------------------- HBS algebra
+# hbs.cpp:290-402 (subtree / flip / scale), hbs_ops.cpp:213-743 (add_hbs, lowrank_to_bs,
+# add_lowrank, split_at, consolidate, rebase), lowrank.cpp; device work in csrc/hbs_ops.cu.
+
+def _tree_array(tree: IndexTree) -> np.ndarray:
+    return np.ascontiguousarray([[n.begin, n.end, n.left, n.right, n.parent, n.level] for n in tree.nodes],
+                                dtype=np.int64).reshape(-1, 6)
+
+
+def _host(a, rows, cols):
+    A = np.asfortranarray(np.asarray(a, dtype=np.float64).reshape(rows, cols))
+    return A, max(rows, 1)
+
+
+def mirror(tree: IndexTree) -> IndexTree:
+    """mirror (index_tree.cpp:71-93): the tree of the reversed index order."""
+    M = tree.size()
+    nodes: list[IndexNode] = []
+    depth = 0
+
+    def rec(t, parent, level):
+        nonlocal depth
+        n = tree.nodes[t]
+        i = len(nodes)
+        nodes.append(IndexNode(M - n.end, M - n.begin, -1, -1, parent, level))
+        depth = max(depth, level)
+        if n.left >= 0:
+            lft = rec(n.right, i, level + 1)
+            rgt = rec(n.left, i, level + 1)
+            nodes[i].left, nodes[i].right = lft, rgt
+        return i
+
+    rec(0, -1, 0)
+    return IndexTree(nodes, depth)
+
+
+def subtree_matrix(H: HbsMatrix, t: int) -> HbsMatrix:
+    """subtree_matrix (hbs.cpp:290-320): the diagonal block of node t as its own HBS matrix."""
+    out = C.c_void_p()
+    H.ctx.check(L.lib().dtn_gpu_hbs_subtree(H.h, int(t), C.byref(out)))
+    return HbsMatrix(H.ctx, out)
+
+
+def flip(H: HbsMatrix) -> HbsMatrix:
+    """flip (hbs.cpp:322-375): P H P with P the index reversal, on the mirrored tree."""
+    out = C.c_void_p()
+    H.ctx.check(L.lib().dtn_gpu_hbs_flip(H.h, C.byref(out)))
+    return HbsMatrix(H.ctx, out)
+
+
+def scale(H: HbsMatrix, s: float) -> None:
+    """scale (hbs.cpp:399-402): H *= s, in place."""
+    H.ctx.check(L.lib().dtn_gpu_hbs_scale(H.h, float(s)))
+    H._cache.clear()
+
+
+def scale_rows(H: HbsMatrix, w) -> None:
+    """scale_rows (hbs.cpp:377-386): diag(w) H, in place."""
+    W = np.ascontiguousarray(w, dtype=np.float64).reshape(-1)
+    if W.shape[0] != H.size():
+        raise ValueError("scale_rows: size mismatch")
+    H.ctx.check(L.lib().dtn_gpu_hbs_scale_rows(H.h, W.ctypes.data, 0))
+    H._cache.clear()
+
+
+def scale_cols(H: HbsMatrix, w) -> None:
+    """scale_cols (hbs.cpp:388-397): H diag(w), in place."""
+    W = np.ascontiguousarray(w, dtype=np.float64).reshape(-1)
+    if W.shape[0] != H.size():
+        raise ValueError("scale_cols: size mismatch")
+    H.ctx.check(L.lib().dtn_gpu_hbs_scale_cols(H.h, W.ctypes.data, 0))
+    H._cache.clear()
+
+
+def add_hbs(A: HbsMatrix, B: HbsMatrix, eps: float) -> HbsMatrix:
+    """add_hbs (hbs_ops.cpp:386-404): A + B on their common tree, recompressed at eps.
+    Different trees raise ValueError ("add_hbs: operands use different index trees")."""
+    out = C.c_void_p()
+    A.ctx.check(L.lib().dtn_gpu_hbs_add(A.h, B.h, float(eps), C.byref(out)))
+    return HbsMatrix(A.ctx, out)
+
+
+def lowrank_to_bs(Q, R, tree: IndexTree, ctx: Context | None = None) -> HbsMatrix:
+    """lowrank_to_bs (hbs_ops.cpp:409-465): Q R (M x k times k x M) as an HBS matrix on `tree`."""
+    ctx = _ctx(ctx)
+    M = tree.size()
+    k = np.asarray(Q).shape[1] if np.asarray(Q).ndim == 2 else 0
+    Qh, ldq = _host(Q, M, k)
+    Rh, ldr = _host(R, k, M)
+    t = _tree_array(tree)
+    out = C.c_void_p()
+    ctx.check(L.lib().dtn_gpu_hbs_from_lowrank(ctx.h, Qh.ctypes.data, ldq, Rh.ctypes.data, max(k, 1), k,
+                                               t.ctypes.data, t.shape[0], 0, C.byref(out)))
+    return HbsMatrix(ctx, out)
+
+
+def add_lowrank(A: HbsMatrix, Q, R, eps: float) -> HbsMatrix:
+    """add_lowrank (hbs_ops.cpp:467-470): A + Q R recompressed at eps on A's tree."""
+    M = A.size()
+    k = np.asarray(Q).shape[1] if np.asarray(Q).ndim == 2 else 0
+    Qh, ldq = _host(Q, M, k)
+    Rh, _ = _host(R, k, M)
+    out = C.c_void_p()
+    A.ctx.check(L.lib().dtn_gpu_hbs_add_lowrank(A.h, Qh.ctypes.data, ldq, Rh.ctypes.data, max(k, 1), k, float(eps), 0,
+                                                C.byref(out)))
+    return HbsMatrix(A.ctx, out)
+
+
+def rebase(H: HbsMatrix, target: IndexTree, eps: float) -> HbsMatrix:
+    """rebase (hbs_ops.cpp:737-743): H re-expressed on the target tree."""
+    t = _tree_array(target)
+    out = C.c_void_p()
+    H.ctx.check(L.lib().dtn_gpu_hbs_rebase(H.h, t.ctypes.data, t.shape[0], float(eps), C.byref(out)))
+    return HbsMatrix(H.ctx, out)
+
+
+class LowRank:
+    """LowRank (lowrank.hpp): L (m x k) R (k x n) held on the device."""
+
+    def __init__(self, ctx: Context, handle: C.c_void_p):
+        self.ctx, self.h = ctx, handle
+        m, n, k = C.c_int64(), C.c_int64(), C.c_int64()
+        ctx.check(L.lib().dtn_gpu_lowrank_info(handle, C.byref(m), C.byref(n), C.byref(k)))
+        self._m, self._n, self._k = m.value, n.value, k.value
+        self._lr = None
+
+    @staticmethod
+    def from_factors(Lf, R, ctx: Context | None = None) -> "LowRank":
+        ctx = _ctx(ctx)
+        Lh = np.asfortranarray(np.asarray(Lf, dtype=np.float64))
+        Rh = np.asfortranarray(np.asarray(R, dtype=np.float64))
+        m, k = Lh.shape
+        k2, n = Rh.shape
+        if k != k2:
+            raise ValueError("lowrank: inner dimensions differ")
+        out = C.c_void_p()
+        ctx.check(L.lib().dtn_gpu_lowrank_create(ctx.h, Lh.ctypes.data, max(m, 1), Rh.ctypes.data, max(k, 1), m, n, k,
+                                                 0, C.byref(out)))
+        return LowRank(ctx, out)
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                L.lib().dtn_gpu_lowrank_free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def rows(self) -> int:
+        return self._m
+
+    def cols(self) -> int:
+        return self._n
+
+    def rank(self) -> int:
+        return self._k
+
+    def _fetch(self):
+        if self._lr is None:
+            Lf = np.zeros((self._m, self._k), order="F")
+            R = np.zeros((self._k, self._n), order="F")
+            self.ctx.check(L.lib().dtn_gpu_lowrank_get(self.h, Lf.ctypes.data, max(self._m, 1), R.ctypes.data,
+                                                       max(self._k, 1)))
+            self._lr = (Lf, R)
+        return self._lr
+
+    @property
+    def L(self) -> np.ndarray:
+        return self._fetch()[0]
+
+    @property
+    def R(self) -> np.ndarray:
+        return self._fetch()[1]
+
+    def dense(self) -> np.ndarray:
+        Lf, R = self._fetch()
+        return Lf @ R
+
+
+@dataclass
+class Placed:
+    """PlacedLowRank (lowrank.hpp): a low-rank block at (row_offset, col_offset)."""
+    row_offset: int
+    col_offset: int
+    lr: LowRank
+
+
+def lowrank_from_dense(X, eps: float, ctx: Context | None = None) -> LowRank:
+    """lowrank_from_dense (lowrank.cpp:27-36): the eps-truncated factorization of X."""
+    ctx = _ctx(ctx)
+    A = np.asfortranarray(np.asarray(X, dtype=np.float64))
+    out = C.c_void_p()
+    ctx.check(L.lib().dtn_gpu_lowrank_from_dense(ctx.h, A.ctypes.data, max(A.shape[0], 1), A.shape[0], A.shape[1], 0,
+                                                 float(eps), C.byref(out)))
+    return LowRank(ctx, out)
+
+
+def lowrank_recompress(x: LowRank, eps: float) -> LowRank:
+    """lowrank_recompress (lowrank.cpp:38-56)."""
+    out = C.c_void_p()
+    x.ctx.check(L.lib().dtn_gpu_lowrank_recompress(x.h, float(eps), C.byref(out)))
+    return LowRank(x.ctx, out)
+
+
+def lowrank_sum(m: int, n: int, terms, eps: float, ctx: Context | None = None) -> LowRank:
+    """lowrank_sum (lowrank.cpp:58-72): the sum of placed low-rank terms, recompressed."""
+    ctx = _ctx(ctx if ctx is not None else (terms[0].lr.ctx if terms else None))
+    hs = (C.c_void_p * max(len(terms), 1))(*[t.lr.h for t in terms])
+    offs = np.ascontiguousarray([[t.row_offset, t.col_offset] for t in terms] or [[0, 0]], dtype=np.int64)
+    out = C.c_void_p()
+    ctx.check(L.lib().dtn_gpu_lowrank_sum(ctx.h, int(m), int(n), len(terms), hs, offs.ctypes.data, float(eps),
+                                          C.byref(out)))
+    return LowRank(ctx, out)
+
+
+@dataclass
+class SplitParts:
+    """SplitParts (hbs_ops.hpp) with both accumulations consolidated: lo = H[:pos, :pos],
+    hi = H[pos:, pos:] (None when empty) on the reference's spine trees, lo_hi = H[:pos, pos:],
+    hi_lo = H[pos:, :pos] as low-rank blocks."""
+    lo: HbsMatrix | None
+    hi: HbsMatrix | None
+    lo_hi: LowRank
+    hi_lo: LowRank
+
+
+def split_at(H: HbsMatrix, pos: int, eps: float = 1e-12) -> SplitParts:
+    """split_at (hbs_ops.cpp:620-640) followed by consolidate of each side (hbs_ops.cpp:710-735)."""
+    lo, hi, a, b = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+    H.ctx.check(L.lib().dtn_gpu_hbs_split_at(H.h, int(pos), float(eps), C.byref(lo), C.byref(hi), C.byref(a),
+                                             C.byref(b)))
+    return SplitParts(HbsMatrix(H.ctx, lo) if lo.value else None, HbsMatrix(H.ctx, hi) if hi.value else None,
+                      LowRank(H.ctx, a), LowRank(H.ctx, b))
+
+
+def consolidate(pieces, offsets, corrections=(), eps: float = 1e-12, size: int | None = None) -> HbsMatrix:
+    """consolidate (hbs_ops.cpp:710-735): HBS pieces tiling [0, size) at `offsets` joined on the
+    reference's spine tree (build_spine, hbs_ops.cpp:676-708), plus the placed low-rank
+    corrections (Placed), recompressed at eps."""
+    if not pieces:
+        raise ValueError("consolidate: no pieces")
+    ctx = pieces[0].ctx
+    if size is None:
+        size = int(offsets[-1]) + pieces[-1].size()
+    ph = (C.c_void_p * len(pieces))(*[p.h for p in pieces])
+    po = np.ascontiguousarray(offsets, dtype=np.int64)
+    corrections = list(corrections)
+    ch = (C.c_void_p * max(len(corrections), 1))(*[c.lr.h for c in corrections])
+    co = np.ascontiguousarray([[c.row_offset, c.col_offset] for c in corrections] or [[0, 0]], dtype=np.int64)
+    out = C.c_void_p()
+    ctx.check(L.lib().dtn_gpu_hbs_consolidate(ctx.h, int(size), len(pieces), ph, po.ctypes.data, len(corrections), ch,
+                                              co.ctypes.data, float(eps), C.byref(out)))
+    return HbsMatrix(ctx, out)
