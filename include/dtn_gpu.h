@@ -200,6 +200,11 @@ int dtn_gpu_collective_flops(int32_t n, int32_t n_leaf, int32_t leaf_side, int32
  * column-major matrix with the engine's blocked kernels; ni == n is a full LU. */
 int dtn_debug_partial_lu(int32_t n, int32_t ni, const double* A, double* out, int32_t* ipiv, double* pivstat);
 
+/* Test hook: C (m x n, in/out) = alpha A B + beta C on host column-major operands through the
+ * engine's FP64 tensor-core GEMMs; path 0 = cp.async-staged kernels, 1 = the TMA-staged kernel. */
+int dtn_debug_gemm(int32_t m, int32_t n, int32_t k, const double* A, const double* B, double* C, double alpha,
+                   double beta, int32_t path);
+
 /* discretize (grid.cpp:106-168) on the host: continuum mode from coefficient
  * samples b, c, d at the unknowns (physical coordinates (x h, y h), h = 1/(n-1),
  * unknown_id order; NULL = 0), network mode from the seeded link conductivities. */

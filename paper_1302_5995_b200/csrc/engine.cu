@@ -58,6 +58,12 @@ cudaError_t launch_trsm_rows(const double*, int, double*, int, int, int, int, bo
 cudaError_t launch_norm1(const double*, int, int, int, unsigned long long*, cudaStream_t);
 cudaError_t launch_copy2d(const double*, int, double*, int, int, int, cudaStream_t);
 cudaError_t gemm_init();
+cudaError_t gemm_tma_init();
+void* tma_build_set(const GemmDesc*, size_t, std::vector<char>&);
+const void* tma_slice(const void*, const std::vector<char>&, size_t, size_t);
+bool tma_encode_one(const GemmDesc&, void*);
+int gemm_tma_min_tiles();
+cudaError_t launch_gemm_tma(const GemmDesc*, const void*, int, int, double, double, cudaStream_t);
 cudaError_t misc_init();
 cudaError_t launch_tri_inv_blocks(const double*, int, int, double*, cudaStream_t);
 cudaError_t launch_set_identity(double*, int, int, cudaStream_t);
@@ -158,7 +164,31 @@ T* dalloc(size_t count) {
   return p;
 }
 
+// Tensor maps of a descriptor array (k_tma.cu): launches whose descriptors all have maps and
+// that are large enough run the TMA-staged kernel, the others the cp.async kernels.
+struct TmaSet {
+  void* d = nullptr;
+  std::vector<char> ok;
+  void build(const std::vector<GemmDesc>& h) {
+    if (d) cudaFree(d);
+    d = tma_build_set(h.data(), h.size(), ok);
+  }
+  const void* slice(size_t off, size_t cnt) const { return tma_slice(d, ok, off, cnt); }
+  ~TmaSet() {
+    if (d) cudaFree(d);
+  }
+};
+
+cudaError_t gemm_go(const GemmDesc* base, const TmaSet& tm, size_t off, int cnt, int max_tiles, int kmax, double alpha,
+                    double beta, cudaStream_t st, bool aligned) {
+  const void* maps =
+      (kmax >= 64 && int64_t(max_tiles) * cnt >= gemm_tma_min_tiles()) ? tm.slice(off, size_t(cnt)) : nullptr;
+  if (maps) return launch_gemm_tma(base + off, maps, cnt, max_tiles, alpha, beta, st);
+  return launch_gemm_desc(base + off, cnt, max_tiles, kmax, alpha, beta, st, aligned);
+}
+
 struct PlanDev {
+  TmaSet tm_bs, tm_sg, tm_rg, tm_inv, tm_fw;
   Plan P;
   bool busy = false;
   int device = 0;
@@ -793,8 +823,10 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
     upload_vec(D->h_fw_gather, D->d_fw_gather);
     upload_vec(D->h_fw_trs, D->d_fw_trs);
     upload_vec(D->h_fw_gemm, D->d_fw_gemm);
+    D->tm_fw.build(D->h_fw_gemm);
     upload_vec(D->h_sm_copy, D->d_sm_copy);
     upload_vec(D->h_sg, D->d_sg);
+    D->tm_sg.build(D->h_sg);
     upload_vec(D->h_sg2, D->d_sg2);
     upload_vec(D->h_sum, D->d_sum);
     upload_vec(D->h_qr, D->d_qr);
@@ -807,6 +839,7 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
     D->d_tri = dalloc<TriDesc>(D->h_tri.size());
     if (!D->h_bs_gemm.empty())
       CK(cudaMemcpy(D->d_bs_gemm, D->h_bs_gemm.data(), D->h_bs_gemm.size() * sizeof(GemmDesc), cudaMemcpyHostToDevice));
+    D->tm_bs.build(D->h_bs_gemm);
     if (!D->h_bs_copy.empty())
       CK(cudaMemcpy(D->d_bs_copy, D->h_bs_copy.data(), D->h_bs_copy.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
     if (!D->h_tri.empty())
@@ -954,6 +987,7 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
     if (!D->h_rg.empty()) {
       D->d_rg = dalloc<GemmDesc>(D->h_rg.size());
       CK(cudaMemcpy(D->d_rg, D->h_rg.data(), D->h_rg.size() * sizeof(GemmDesc), cudaMemcpyHostToDevice));
+      D->tm_rg.build(D->h_rg);
     }
     D->d_rt = dalloc<TrsmDesc>(std::max<size_t>(D->h_rt.size(), 1));
     if (!D->h_rt.empty())
@@ -962,6 +996,7 @@ std::unique_ptr<PlanDev> make_plandev(const PlanKey& key, int device) {
   D->d_inv_descs = dalloc<GemmDesc>(D->h_inv_descs.size());
   CK(cudaMemcpy(D->d_inv_descs, D->h_inv_descs.data(), D->h_inv_descs.size() * sizeof(GemmDesc),
                 cudaMemcpyHostToDevice));
+  D->tm_inv.build(D->h_inv_descs);
   D->ev_wave.resize(P.waves.size());
   for (auto& e : D->ev_wave) CK(cudaEventCreate(&e));
   CK(cudaEventCreate(&D->ev_start));
@@ -1193,8 +1228,7 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
         for (size_t t = 0; t < L.fw_n.size(); ++t) {
           if (t > 0)  // block 0 has no left part
             run(K_BACKSUB, L.fw_flops[t], 0.0, [&] {
-              return launch_gemm_desc(D.d_fw_gemm + L.fw_goff[t], L.fw_n[t], L.fw_tiles[t], L.fw_k[t], -1.0, 1.0, st,
-                                      true);
+              return gemm_go(D.d_fw_gemm, D.tm_fw, size_t(L.fw_goff[t]), L.fw_n[t], L.fw_tiles[t], L.fw_k[t], -1.0, 1.0, st, true);
             });
           run(K_SUBST, 0.0, 0.0, [&] {
             return launch_trsm_batched(D.d_fw_trs + L.fw_toff[t], L.fw_n[t], L.fw_cols[t], 128, true, st);
@@ -1220,23 +1254,23 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
                            : launch_trsm_batched(D.d_trs + L.bs_toff[t], cnt, L.bs_cols[t], L.bs_k[t], false, st);
               });
           run(K_BACKSUB, L.bs_flops[t], 0.0, [&] {
-            return launch_gemm_desc(D.d_bs_gemm + D.subst_base + L.bs_soff[t], cnt, L.bs_tiles2[t], L.bs_k[t], -1.0,
-                                    1.0, st, true);
+            return gemm_go(D.d_bs_gemm, D.tm_bs, size_t(D.subst_base + L.bs_soff[t]), cnt, L.bs_tiles2[t], L.bs_k[t], -1.0, 1.0,
+                           st, true);
           });
         } else {
           run(K_BACKSUB, 0.0, 0.0, [&] {
-            return launch_gemm_desc(D.d_bs_gemm + off, cnt, L.bs_tiles1[t], L.bs_k[t], 1.0, 0.0, st, true);
+            return gemm_go(D.d_bs_gemm, D.tm_bs, size_t(off), cnt, L.bs_tiles1[t], L.bs_k[t], 1.0, 0.0, st, true);
           });
           run(K_BACKSUB, L.bs_flops[t], 0.0, [&] {
-            return launch_gemm_desc(D.d_bs_gemm + off + cnt, cnt, L.bs_tiles2[t], L.bs_k[t], -1.0, 1.0, st, true);
+            return gemm_go(D.d_bs_gemm, D.tm_bs, size_t(off + cnt), cnt, L.bs_tiles2[t], L.bs_k[t], -1.0, 1.0, st, true);
           });
           run(K_COPY, 0.0, 0.0, [&] { return launch_copy2d_batched(D.d_bs_copy + coff, cnt, st); });
         }
         coff += cnt;
       }
       run(K_SCHUR, L.fin_flops, 0.0, [&] {
-        return launch_gemm_desc(D.d_bs_gemm + L.fin_off, L.fin_cnt, L.fin_tiles, L.fin_k, -1.0, 1.0, st,
-                                L.fin_aligned);
+        return gemm_go(D.d_bs_gemm, D.tm_bs, size_t(L.fin_off), L.fin_cnt, L.fin_tiles, L.fin_k, -1.0, 1.0, st,
+                       L.fin_aligned);
       });
       if (!L.gather_nodes.empty() && D.comm) {  // collective top build: every rank's column chunk to all
         const NcclApi& nc = nccl();
@@ -1256,10 +1290,10 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
         run(K_SGATHER, 0.0, 0.0, [&] { return launch_factor_gather(a, sl, L.sm_cnt, L.sm_max_elems, st); });
         run(K_COPY, 0.0, 0.0, [&] { return launch_copy2d_batched(D.d_sm_copy + L.sm_copy, L.sm_cnt, st); });
         run(K_SGEMM, L.sm_flops * 0.0, 0.0, [&] {
-          return launch_gemm_desc(D.d_sg + L.sm_t, L.sm_cnt, L.sm_t_tiles, L.sm_t_k, -1.0, 0.0, st, true);
+          return gemm_go(D.d_sg, D.tm_sg, size_t(L.sm_t), L.sm_cnt, L.sm_t_tiles, L.sm_t_k, -1.0, 0.0, st, true);
         });
         run(K_SGEMM, L.sm_flops, 0.0, [&] {
-          return launch_gemm_desc(D.d_sg + L.sm_u, L.sm_cnt, L.sm_u_tiles, L.sm_u_k, -1.0, 1.0, st, true);
+          return gemm_go(D.d_sg, D.tm_sg, size_t(L.sm_u), L.sm_cnt, L.sm_u_tiles, L.sm_u_k, -1.0, 1.0, st, true);
         });
       }
     }
@@ -1279,7 +1313,7 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
       run(K_SGEMM, 0.0, 0.0,
           [&] { return launch_gemm_desc2(D.d_sg2 + L.cp_rt, L.cp_cnt, L.cp_rt_tiles, false, st); });
       run(K_SGEMM, L.cp_flops, 0.0, [&] {
-        return launch_gemm_desc(D.d_sg + L.cp_lk, L.cp_cnt, L.cp_lk_tiles, L.cp_lk_k, 1.0, 0.0, st, L.cp_lk_aligned);
+        return gemm_go(D.d_sg, D.tm_sg, size_t(L.cp_lk), L.cp_cnt, L.cp_lk_tiles, L.cp_lk_k, 1.0, 0.0, st, L.cp_lk_aligned);
       });
     }
     if (events) CK(cudaEventRecord(D.ev_wave[w], st));
@@ -1328,7 +1362,7 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
             f += 2.0 * g.m * g.n * g.k;
           }
           run(K_INV_GEMM, f, 0.0, [&] {
-            return launch_gemm_desc(D.d_rg + D.rg_off[q], D.rg_cnt[q], tiles, kmax, -1.0, 1.0, st, true);
+            return gemm_go(D.d_rg, D.tm_rg, size_t(D.rg_off[q]), D.rg_cnt[q], tiles, kmax, -1.0, 1.0, st, true);
           });
         };
         auto trs = [&] {
@@ -1380,7 +1414,7 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
         f += 2.0 * g.m * g.n * g.k;
       }
       run(K_INV_GEMM, f, 0.0, [&] {
-        return launch_gemm_desc(D.d_inv_descs + d0, cnt, tiles, 128, alpha, beta, st, true);
+        return gemm_go(D.d_inv_descs, D.tm_inv, size_t(d0), cnt, tiles, 128, alpha, beta, st, true);
       });
     };
     gemm(0, D.inv_pre, 1.0, 0.0);  // L' and U'
@@ -1400,7 +1434,7 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
           f += 2.0 * g.m * g.n * g.k;
         }
         run_on(st2, K_INV_GEMM, f, 0.0,
-               [&] { return launch_gemm_desc(D.d_inv_descs + d0, cnt, tiles, 128, alpha, beta, st2, true); });
+               [&] { return gemm_go(D.d_inv_descs, D.tm_inv, size_t(d0), cnt, tiles, 128, alpha, beta, st2, true); });
       };
       for (int kb_ = nblk - 1; kb_ >= 1; --kb_) gemm2(D.inv_ui + kb_ - 1, 1, -1.0, 1.0);
       gemm2(D.inv_ui + nblk - 1, nblk, 1.0, 0.0);  // UI2_k = Uinv_kk UI_k
@@ -1423,7 +1457,7 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
         f += 2.0 * g.m * g.n * g.k;
       }
       run(K_INV_GEMM, f, 0.0,
-          [&] { return launch_gemm_desc(D.d_inv_descs + f0, nblk, tiles, nb, 1.0, 0.0, st, true); });
+          [&] { return gemm_go(D.d_inv_descs, D.tm_inv, size_t(f0), nblk, tiles, nb, 1.0, 0.0, st, true); });
     } else {
       for (int kb_ = nblk - 1; kb_ >= 1; --kb_) gemm(d + kb_ - 1, 1, -1.0, 1.0);  // backward sweep
       d += nblk - 1;
@@ -1551,6 +1585,7 @@ int dtn_gpu_create(dtn_ctx** out, int device) {
     if (prop.major != 10) throw CudaFail("dtn_gpu_create: sm_100a (B200) device required");
     CK(cudaSetDevice(device));
     CK(gemm_init());
+    CK(gemm_tma_init());
     CK(blocked_init());
     CK(misc_init());
     CK(hbs_kernels_init());
@@ -1559,7 +1594,7 @@ int dtn_gpu_create(dtn_ctx** out, int device) {
     c->device = device;
     CK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
     c->stream = c->own;
-    CK(cudaMalloc(&c->d_desc, sizeof(GemmDesc)));
+    CK(cudaMalloc(&c->d_desc, 512));  // one descriptor + (at byte 256) its two tensor maps
     *out = c;
   });
 }
@@ -2279,8 +2314,15 @@ int dtn_gpu_apply(const dtn_op* op, int which, const double* X, int64_t ldx, int
       CK(launch_skinny_gemm(A, lda, dX, int(ldX), dY, int(ldY), nb, nb, int(batch), ctx->d_skinny, st));
     } else {
       GemmDesc d{A, dX, dY, nb, int(batch), nb, lda, int(ldX), int(ldY)};
-      CK(cudaMemcpyAsync(ctx->d_desc, &d, sizeof(d), cudaMemcpyHostToDevice, st));
-      CK(launch_gemm_desc(ctx->d_desc, 1, gemm_tiles(nb, int(batch)), nb, 1.0, 0.0, st, true));
+      alignas(64) unsigned char img[512] = {0};  // descriptor, and its A / B tensor maps at byte 256
+      std::memcpy(img, &d, sizeof(d));
+      const int tiles = gemm_tiles(nb, int(batch));
+      const bool tma = tiles >= gemm_tma_min_tiles() && tma_encode_one(d, img + 256);
+      CK(cudaMemcpyAsync(ctx->d_desc, img, tma ? 512 : sizeof(d), cudaMemcpyHostToDevice, st));
+      if (tma)
+        CK(launch_gemm_tma(ctx->d_desc, reinterpret_cast<const unsigned char*>(ctx->d_desc) + 256, 1, tiles, 1.0, 0.0, st));
+      else
+        CK(launch_gemm_desc(ctx->d_desc, 1, tiles, nb, 1.0, 0.0, st, true));
     }
     if (!aligned)
       CK(cudaMemcpy2DAsync(Y, size_t(ldy) * 8, dY, size_t(ldY) * 8, size_t(nb) * 8, size_t(batch),
@@ -2423,6 +2465,7 @@ int dtn_debug_partial_lu(int32_t n, int32_t ni, const double* A, double* out, in
   return guarded(nullptr, [&] {
     if (n <= 0 || ni <= 0 || ni > n) throw std::invalid_argument("dtn_debug_partial_lu: bad sizes");
     CK(gemm_init());
+    CK(gemm_tma_init());
     CK(blocked_init());
     const int ld = int(align_up(n, 8));
     NodeDev nd{};
@@ -2457,6 +2500,50 @@ int dtn_debug_partial_lu(int32_t n, int32_t ni, const double* A, double* out, in
     CK(cudaMemcpy(ipiv, d_piv, size_t(ni) * sizeof(int), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(pivstat, d_ps, 2 * sizeof(double), cudaMemcpyDeviceToHost));
     for (void* p : std::initializer_list<void*>{d_node, d_list, d_a, d_piv, d_ps}) cudaFree(p);
+  });
+}
+
+// Test hook: C = alpha A B + beta C (host column-major operands, tight leading dimensions
+// rounded up to even) through the engine's GEMM dispatch; path 0 = cp.async kernels,
+// 1 = the TMA-staged kernel (k_tma.cu; fails if the tensor maps cannot be encoded).
+int dtn_debug_gemm(int32_t m, int32_t n, int32_t k, const double* A, const double* B, double* Cio, double alpha,
+                   double beta, int32_t path) {
+  return guarded(nullptr, [&] {
+    if (m <= 0 || n <= 0 || k <= 0 || !A || !B || !Cio) throw std::invalid_argument("dtn_debug_gemm: bad arguments");
+    CK(gemm_init());
+    CK(gemm_tma_init());
+    const int lda = int(align_up(m, 2)), ldb = int(align_up(k, 2)), ldc = lda;
+    double *dA = nullptr, *dB = nullptr, *dC = nullptr;
+    unsigned char* dd = nullptr;
+    CK(cudaMalloc(&dA, size_t(lda) * k * 8));
+    CK(cudaMalloc(&dB, size_t(ldb) * n * 8));
+    CK(cudaMalloc(&dC, size_t(ldc) * n * 8));
+    CK(cudaMalloc(&dd, 512));
+    CK(cudaMemcpy2D(dA, size_t(lda) * 8, A, size_t(m) * 8, size_t(m) * 8, size_t(k), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy2D(dB, size_t(ldb) * 8, B, size_t(k) * 8, size_t(k) * 8, size_t(n), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy2D(dC, size_t(ldc) * 8, Cio, size_t(m) * 8, size_t(m) * 8, size_t(n), cudaMemcpyHostToDevice));
+    GemmDesc d{dA, dB, dC, m, n, k, lda, ldb, ldc};
+    alignas(64) unsigned char img[512] = {0};
+    std::memcpy(img, &d, sizeof(d));
+    const bool tma = path == 1;
+    bool enc = true;
+    if (tma) enc = tma_encode_one(d, img + 256);
+    cudaError_t e = cudaSuccess;
+    if (enc) {
+      CK(cudaMemcpy(dd, img, 512, cudaMemcpyHostToDevice));
+      const GemmDesc* gd = reinterpret_cast<const GemmDesc*>(dd);
+      e = tma ? launch_gemm_tma(gd, dd + 256, 1, gemm_tiles(m, n), alpha, beta, 0)
+              : launch_gemm_desc(gd, 1, gemm_tiles(m, n), k, alpha, beta, 0, true);
+      if (e == cudaSuccess) e = cudaDeviceSynchronize();
+      if (e == cudaSuccess)
+        e = cudaMemcpy2D(Cio, size_t(m) * 8, dC, size_t(ldc) * 8, size_t(m) * 8, size_t(n), cudaMemcpyDeviceToHost);
+    }
+    cudaFree(dA);
+    cudaFree(dB);
+    cudaFree(dC);
+    cudaFree(dd);
+    if (!enc) throw std::runtime_error("dtn_debug_gemm: no tensor maps for this shape (TMA unavailable or disabled)");
+    CK(e);
   });
 }
 
