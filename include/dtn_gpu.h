@@ -72,7 +72,10 @@ typedef struct {
                           locally, shard S gathered to every rank, the top merges column-sharded
                           (interface LU redundant, boundary columns split, ncclAllGather per wave);
                           S (and G) on every rank; -3: the same split computed on this one device
-                          (every shard and column chunk in turn, no communication) */
+                          (every shard and column chunk in turn, no communication); -4: -3 with every
+                          NCCL call of the -2 path issued in place on the context's 1-rank
+                          communicator (dtn_gpu_create_rank with nranks == 1: a one-GPU check of the
+                          communicator and of the collectives captured in the build graph) */
   double* export_S;    /* optional host buffer (page-locked for overlap): receives S (column-major,
                           leading dimension export_lds) during the build, overlapping the root inverse */
   int64_t export_lds;

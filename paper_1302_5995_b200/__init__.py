@@ -6,4 +6,4 @@ from .dtn import (AccelOptions, BoxTree, Context, DiscreteOperator, Engine, Fact
                   build_root_accel, build_root_dense_op, build_root_gpu, CompressedSolutionOperator, build_tree, build_tree_uniform, build_with_loads, catalog, shard_info,
                   catalog_names, default_context, densify_dtn, discrete_eigenvalue, discrete_eigenvalue_kth,
                   discretize, dump_schur, load_schur, make_load_set, ring_dtn, ring_nodes, root_boundary,
-                  solve_with_load)
+                  solve_with_load, nccl_unique_id, collective_context)

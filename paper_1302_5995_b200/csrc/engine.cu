@@ -1279,7 +1279,8 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
           const Node& nd = P.nodes[id];
           double* Mb = D.d_arena + nd.m_off + int64_t(nd.ni) * nd.ldm;
           const size_t cnt = size_t(nd.ldm) * nd.cw;
-          nccl_check(nc.AllGather(Mb + cnt * P.key.wrank, Mb, cnt, ncclDouble, static_cast<ncclComm_t>(D.comm), st),
+          nccl_check(nc.AllGather(Mb + cnt * std::max(P.key.wrank, 0), Mb, cnt, ncclDouble,
+                                  static_cast<ncclComm_t>(D.comm), st),
                      "ncclAllGather (merge columns)");
         }
         nccl_check(nc.GroupEnd(), "ncclGroupEnd");
@@ -1380,7 +1381,7 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
       }
       if (D.comm) {
         const size_t cnt = size_t(D.ldg) * D.root_cw;
-        nccl_check(nccl().AllGather(D.d_G + cnt * P.key.wrank, D.d_G, cnt, ncclDouble,
+        nccl_check(nccl().AllGather(D.d_G + cnt * std::max(P.key.wrank, 0), D.d_G, cnt, ncclDouble,
                                     static_cast<ncclComm_t>(D.comm), st),
                    "ncclAllGather (G columns)");
       }
@@ -1612,7 +1613,7 @@ int dtn_gpu_nccl_unique_id(uint8_t* id) {
 int dtn_gpu_create_rank(dtn_ctx** out, int device, int nranks, int rank, const uint8_t* id) {
   if (!out) return DTN_EINVAL;
   int rc = dtn_gpu_create(out, device);
-  if (rc != DTN_OK || nranks <= 1) return rc;
+  if (rc != DTN_OK || nranks < 1 || (nranks == 1 && !id)) return rc;
   dtn_ctx* c = *out;
   rc = guarded(c, [&] {
     if (rank < 0 || rank >= nranks || !id) throw std::invalid_argument("dtn_gpu_create_rank: bad rank or id");
@@ -2054,9 +2055,15 @@ int build_adaptive(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, 
 int build_collective(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, dtn_op** out) {
   const int N = opts->nshards;
   const bool real = opts->shard == -2;
+  // -4 (loopback): -3's single-device split with every NCCL call of the real path issued on the
+  // context's 1-rank communicator (in place: no data moves) -- exercises the dlopen'ed API, the
+  // communicator and the collectives captured in the build graph on one GPU
+  const bool loop = opts->shard == -4;
   std::vector<int64_t> nbs(static_cast<size_t>(N), 0);
   int rc = guarded(ctx, [&] {
     if (!prob || !out) throw std::invalid_argument("dtn_gpu_build: null argument");
+    if (loop && (ctx->world != 1 || !ctx->comm))
+      throw std::invalid_argument("collective loopback: the context needs a 1-rank communicator (dtn_gpu_create_rank)");
     if (real && (ctx->world != N || !ctx->comm))
       throw std::invalid_argument("collective build: nshards must equal the context's NCCL world (dtn_gpu_create_rank)");
     if (opts->nloads > 0) throw std::invalid_argument("dtn_gpu_build: body loads are not supported in sharded builds");
@@ -2100,7 +2107,7 @@ int build_collective(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts
     dtn_gpu_free(sop);
     if (rc != DTN_OK) return rc;
   }
-  if (real) {
+  if (real || loop) {
     rc = guarded(ctx, [&] {
       nccl_check(nccl().AllGather(ctx->d_gather + size_t(ctx->rank) * slot, ctx->d_gather, size_t(slot), ncclDouble,
                                   ctx->comm, st),
@@ -2116,7 +2123,8 @@ int build_collective(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts
   pt.shard_S_on_device = 1;
   dtn_opts ot = *opts;
   ot.shard = -1;
-  return build_adaptive(ctx, &pt, &ot, out, N, real ? ctx->rank : -1, real ? static_cast<void*>(ctx->comm) : nullptr);
+  return build_adaptive(ctx, &pt, &ot, out, N, real ? ctx->rank : -1,
+                        (real || loop) ? static_cast<void*>(ctx->comm) : nullptr);
 }
 
 }  // namespace
@@ -2124,7 +2132,7 @@ int build_collective(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts
 extern "C" {
 
 int dtn_gpu_build(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, dtn_op** out) {
-  if (ctx && opts && opts->nshards > 1 && (opts->shard == -2 || opts->shard == -3))
+  if (ctx && opts && opts->nshards > 1 && (opts->shard == -2 || opts->shard == -3 || opts->shard == -4))
     return build_collective(ctx, prob, opts, out);
   return build_adaptive(ctx, prob, opts, out);
 }

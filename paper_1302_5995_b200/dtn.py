@@ -287,7 +287,7 @@ class Context:
         the NCCL communicator of the collective builds (dtn_gpu_create_rank), built from
         the 128-byte unique id every rank received from rank 0 (collective_context)."""
         h = C.c_void_p()
-        if world > 1:
+        if world > 1 or nccl_id is not None:  # (world 1 with an id: a 1-rank communicator, loopback checks)
             if nccl_id is None or len(nccl_id) != 128:
                 raise ValueError("Context: a 128-byte NCCL unique id is required for world > 1")
             buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)

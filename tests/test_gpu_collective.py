@@ -57,3 +57,27 @@ def test_collective_structured_shards(world):
     b = dtn.build_root_accel(op, tree, opt, nshards=world, collective=-3)
     g = np.random.Generator(np.random.MT19937(2)).uniform(-1, 1, (a.boundary_size(), 8))
     assert rel(dtn.apply_schur(b, g), dtn.apply_schur(a, g)) <= 1e-9
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_collective_nccl_loopback(world):
+    """shard = -4: the single-device split with every NCCL call of the real collective
+    path (the shard-S all-gather, the grouped per-wave all-gathers captured in the build
+    graph, the G column all-gather) issued in place on a 1-rank communicator the context
+    owns -- checks the dlopen'ed NCCL entry points, ncclCommInitRank from a unique id and
+    graph capture of the collectives on the one GPU available here."""
+    ctx = dtn.Context(0, 1, 0, dtn.nccl_unique_id())
+    n, leaf = 258, 16
+    op = dtn.discretize(dtn.catalog("helmholtz1", n, seed=1))
+    tree = dtn.build_tree_uniform(n, leaf)
+    full = dtn.build_root_gpu(op, tree, ctx=ctx)
+    for _ in range(2):  # second build: the cached plan's graph replays its collectives
+        col = dtn.build_root_gpu(op, tree, nshards=world, shard=-4, ctx=ctx)
+        assert rel(col.S_dense, full.S_dense) <= 1e-12
+        nb = len(full.boundary)
+        assert np.linalg.norm(full.S_dense @ col.G_dense - np.eye(nb)) / np.sqrt(nb) <= 1e-11 * max(1.0, full.cond_estimate)
+        col.free()
+    acc = dtn.build_root_accel(op, tree, dtn.AccelOptions(epsilon=1e-10, crossover=100, hbs_leaf=32), ctx=ctx,
+                               nshards=world, collective=-4)
+    g = np.random.default_rng(1).uniform(-1, 1, (len(full.boundary), 3))
+    assert rel(dtn.apply_schur(acc, g), full.S_dense @ g) <= 1e-8
