@@ -59,6 +59,10 @@ cudaError_t launch_norm1(const double*, int, int, int, unsigned long long*, cuda
 cudaError_t launch_copy2d(const double*, int, double*, int, int, int, cudaStream_t);
 cudaError_t gemm_init();
 cudaError_t gemm_tma_init();
+cudaError_t fused_init();
+void fused_clocks_read(long long*);
+bool fused_merge_fits(int, int, int);
+cudaError_t launch_fused_merge(const KernelArgs&, const int*, int, int, int, int, cudaStream_t);
 void* tma_build_set(const GemmDesc*, size_t, std::vector<char>&);
 const void* tma_slice(const void*, const std::vector<char>&, size_t, size_t);
 bool tma_encode_one(const GemmDesc&, void*);
@@ -1048,6 +1052,13 @@ bool use_lookahead() {
   return !(e && e[0] == '1');
 }
 
+// One-CTA fused merges (k_fused.cu) for waves whose largest system has at least this many
+// unknowns and fits one CTA's shared memory (DTN_FUSED_MERGE_MIN; 0 disables)
+int fused_merge_min() {
+  const char* e = std::getenv("DTN_FUSED_MERGE_MIN");
+  return e ? std::atoi(e) : 0;  // (off by default until the blocked variant lands)
+}
+
 bool use_fused() {  // DTN_NO_FUSED=1: the unfused look-ahead (next-panel update on the main stream)
   const char* e = std::getenv("DTN_NO_FUSED");
   return use_lookahead() && !(e && e[0] == '1');
@@ -1057,12 +1068,12 @@ bool use_fused() {  // DTN_NO_FUSED=1: the unfused look-ahead (next-panel update
 // aggregated per kernel class with the algorithmic work of each launch.
 enum KClass {
   K_SMALL = 0, K_GATHER, K_PANEL, K_ROWPANEL, K_TRAILING, K_BACKSUB, K_SCHUR, K_COPY, K_INV_TRSM, K_INV_GEMM, K_MISC,
-  K_SUBST, K_SGATHER, K_SGEMM, K_COMPRESS, K_COUNT
+  K_SUBST, K_SGATHER, K_SGEMM, K_COMPRESS, K_FUSED, K_COUNT
 };
 const char* kclass_name(int k) {
   static const char* names[K_COUNT] = {"small_elim", "gather",   "panel",    "rowpanel", "trailing_gemm", "backsub_gemm",
                                        "schur_gemm", "copy",     "inv_trsm", "inv_gemm", "misc", "backsub_subst",
-                                       "struct_gather", "struct_gemm", "sketch_qr"};
+                                       "struct_gather", "struct_gemm", "sketch_qr", "fused_merge"};
   return names[k];
 }
 struct Prof {
@@ -1204,11 +1215,36 @@ void enqueue_build(PlanDev& D, cudaStream_t st, bool want_G, Prof* prof = nullpt
       run(K_SMALL, list_flops(hl.data() + L.micro_off, L.micro_cnt), 0.0, [&] {
         return launch_small_elim(a, D.d_lists + L.micro_off, L.micro_cnt, L.micro_max, true, st);
       });
-    if (L.small_cnt)
-      run(K_SMALL, list_flops(hl.data() + L.small_off, L.small_cnt), 0.0, [&] {
-        return launch_small_elim(a, D.d_lists + L.small_off, L.small_cnt, L.small_max, false, st);
+    // waves of many mid-size merges: the whole merge in one CTA's shared memory (k_fused.cu)
+    auto fused_dims = [&](const int* ids, int cnt, int& mni, int& mnb, int& mtot) {
+      mni = mnb = mtot = 0;
+      bool ok = fused_merge_min() > 0 && P.key.nloads == 0;
+      for (int i = 0; i < cnt && ok; ++i) {
+        const Node& nd = P.nodes[ids[i]];
+        ok = nd.kind == NodeKind::merge && !nd.smerge && nd.cw == 0 && nd.ni > 0 && nd.total > nd.ni;
+        mni = std::max(mni, nd.ni);
+        mnb = std::max(mnb, nd.total - nd.ni);
+        mtot = std::max(mtot, nd.total);
+      }
+      return ok && mtot >= fused_merge_min() && fused_merge_fits(mni, mnb, mtot);
+    };
+    int f_ni = 0, f_nb = 0, f_tot = 0;
+    if (L.small_cnt) {
+      if (fused_dims(hl.data() + L.small_off, L.small_cnt, f_ni, f_nb, f_tot))
+        run(K_FUSED, list_flops(hl.data() + L.small_off, L.small_cnt), 0.0, [&] {
+          return launch_fused_merge(a, D.d_lists + L.small_off, L.small_cnt, f_ni, f_nb, f_tot, st);
+        });
+      else
+        run(K_SMALL, list_flops(hl.data() + L.small_off, L.small_cnt), 0.0, [&] {
+          return launch_small_elim(a, D.d_lists + L.small_off, L.small_cnt, L.small_max, false, st);
+        });
+    }
+    if (L.blk_cnt && L.sm_cnt == 0 && L.gather_nodes.empty() && L.blk_cnt >= 16 &&
+        fused_dims(hl.data() + L.blk_off, L.blk_cnt, f_ni, f_nb, f_tot)) {
+      run(K_FUSED, list_flops(hl.data() + L.blk_off, L.blk_cnt), 0.0, [&] {
+        return launch_fused_merge(a, D.d_lists + L.blk_off, L.blk_cnt, f_ni, f_nb, f_tot, st);
       });
-    if (L.blk_cnt) {
+    } else if (L.blk_cnt) {
       const int* lst = D.d_lists + L.blk_off;
       const int* hlst = hl.data() + L.blk_off;
       double gb = 0.0;
@@ -1587,6 +1623,7 @@ int dtn_gpu_create(dtn_ctx** out, int device) {
     CK(cudaSetDevice(device));
     CK(gemm_init());
     CK(gemm_tma_init());
+    CK(fused_init());
     CK(blocked_init());
     CK(misc_init());
     CK(hbs_kernels_init());
@@ -2474,6 +2511,7 @@ int dtn_debug_partial_lu(int32_t n, int32_t ni, const double* A, double* out, in
     if (n <= 0 || ni <= 0 || ni > n) throw std::invalid_argument("dtn_debug_partial_lu: bad sizes");
     CK(gemm_init());
     CK(gemm_tma_init());
+    CK(fused_init());
     CK(blocked_init());
     const int ld = int(align_up(n, 8));
     NodeDev nd{};
@@ -2511,6 +2549,14 @@ int dtn_debug_partial_lu(int32_t n, int32_t ni, const double* A, double* out, in
   });
 }
 
+// Diagnostic: phase clocks of the fused merge kernel (3 size classes x 8 slots)
+int dtn_debug_fused_clocks(int64_t* out24) {
+  return guarded(nullptr, [&] {
+    cudaDeviceSynchronize();
+    fused_clocks_read(reinterpret_cast<long long*>(out24));
+  });
+}
+
 // Test hook: C = alpha A B + beta C (host column-major operands, tight leading dimensions
 // rounded up to even) through the engine's GEMM dispatch; path 0 = cp.async kernels,
 // 1 = the TMA-staged kernel (k_tma.cu; fails if the tensor maps cannot be encoded).
@@ -2520,6 +2566,7 @@ int dtn_debug_gemm(int32_t m, int32_t n, int32_t k, const double* A, const doubl
     if (m <= 0 || n <= 0 || k <= 0 || !A || !B || !Cio) throw std::invalid_argument("dtn_debug_gemm: bad arguments");
     CK(gemm_init());
     CK(gemm_tma_init());
+    CK(fused_init());
     const int lda = int(align_up(m, 2)), ldb = int(align_up(k, 2)), ldc = lda;
     double *dA = nullptr, *dB = nullptr, *dC = nullptr;
     unsigned char* dd = nullptr;
