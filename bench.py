@@ -709,8 +709,8 @@ def run_b200_compressed(args, cfg, rank, world, local):
                 g = seeded_vectors(len(ref.boundary), 16)
                 Sg = dtn.apply_schur(acc, g)
                 line["parity"] = {"Sg_hbs_rel_fro_vs_oracle": O.rel_fro(Sg, ref.S @ g),
-                                  "tol": 5e-8, "tol_note": "config 3's operator is near-resonant: two exact "
-                                  "FP64 eliminations differ by 3e-9..8e-9 (tests/test_gpu_structured.py COND_TOL)"}
+                                  "tol": 1e-7, "tol_note": "config 3's operator is near-resonant (cond(S) = 9e7): two exact "
+                                  "FP64 eliminations differ by 3e-9..8e-9; bound 5 cond eps (tests/test_gpu_structured.py COND_TOL)"}
             except Exception as e:  # pragma: no cover
                 line["cpu_baseline"] = {"value": None, "error": repr(e)}
         del acc

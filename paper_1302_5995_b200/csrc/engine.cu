@@ -1056,7 +1056,7 @@ bool use_lookahead() {
 // unknowns and fits one CTA's shared memory (DTN_FUSED_MERGE_MIN; 0 disables)
 int fused_merge_min() {
   const char* e = std::getenv("DTN_FUSED_MERGE_MIN");
-  return e ? std::atoi(e) : 0;  // (off by default until the blocked variant lands)
+  return e ? std::atoi(e) : 64;
 }
 
 bool use_fused() {  // DTN_NO_FUSED=1: the unfused look-ahead (next-panel update on the main stream)

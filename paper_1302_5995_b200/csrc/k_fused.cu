@@ -28,6 +28,7 @@
 namespace dtnb {
 
 constexpr int FNT = 256;  // threads per CTA (one per system column in the LU)
+constexpr int FKB = 8;    // pivots per LU block / rows per substitution block
 
 struct FusedShape {  // shared-memory carve-up of one launch (host and device agree through these)
   int ldt, tcols, ldb, kpad;
@@ -39,7 +40,7 @@ __host__ __device__ inline FusedShape fused_shape(int max_ni, int max_nb, int ma
   s.kpad = (max_ni + 7) & ~7;                   // k extent of the Schur GEMM (zero padded)
   s.tcols = max_ni + ((max_nb + 31) & ~31);     // B fragments of ragged blocks stay inside T
   s.ldb = ((max_nb + 31) & ~31) + 2;            // A fragments likewise
-  s.bytes = size_t(max_total) * sizeof(PosDev) + (size_t(s.ldt) * s.tcols + size_t(s.ldb) * s.kpad + 2 * 64) * 8 + 64;
+  s.bytes = size_t(max_total) * sizeof(PosDev) + (size_t(s.ldt) * s.tcols + size_t(s.ldb) * s.kpad + 64 * FKB + 64) * 8 + 64;
   return s;
 }
 
@@ -58,9 +59,9 @@ __global__ void __launch_bounds__(FNT, 2) fused_merge_kernel(KernelArgs args, co
   PosDev* spos = reinterpret_cast<PosDev*>(fsm_raw);
   double* T = reinterpret_cast<double*>(fsm_raw + ((size_t(max_total) * sizeof(PosDev) + 15) & ~size_t(15)));
   double* Mbi = T + size_t(sh.ldt) * sh.tcols;
-  double* lvec = Mbi + size_t(sh.ldb) * sh.kpad;
-  double* urinv = lvec + 64;
-  __shared__ int s_piv;
+  double* lpan = Mbi + size_t(sh.ldb) * sh.kpad;  // [64][FKB] multipliers of the current LU block
+  double* urinv = lpan + 64 * FKB;
+  __shared__ int s_pv[FKB];
   const int LDT = sh.ldt, LDB = sh.ldb;
 
   const int node_id = list[blockIdx.x];
@@ -71,6 +72,8 @@ __global__ void __launch_bounds__(FNT, 2) fused_merge_kernel(KernelArgs args, co
   const double* __restrict__ A = args.arena + ca.s_off;
   const double* __restrict__ B = args.arena + cb.s_off;
   const long long lda = ca.ld, ldb_ = cb.ld;
+  double* S = args.arena + nd.s_off;  // (written here, read back by this CTA only: plain loads)
+  const long long lds = nd.ld;
   // entry (i, j) of the merge system (dense_nd.cpp:114-165 as a gather): its address, or null for 0
   auto entry_ptr = [&](const PosDev& pi, const PosDev& pj, int j) -> const double* {
     if ((pi.src >= 0) == (pj.src >= 0))
@@ -81,202 +84,371 @@ __global__ void __launch_bounds__(FNT, 2) fused_merge_kernel(KernelArgs args, co
   const int fcls = max_ni > 32 ? 2 : (max_nb > 64 ? 1 : 0);
   FCLK(0);
   for (int p = tid; p < total; p += FNT) spos[p] = args.pos[nd.pos_off + p];
-  if (tid < 64) lvec[tid] = 0.0;
+  if (tid < 64) urinv[tid] = 0.0;
   __syncthreads();
   // ---- assembly: T = [M_ii | M_ib] (rows [ni, kpad) zero: the Schur GEMM's k padding), M_bi.
   // Batches of GB independent gathers per thread: addresses first, then the loads in
   // flight together, then the shared stores (a store between two loads would serialise them)
   const int kpad = (ni + 7) & ~7;
-  constexpr int GB = 8;
   {
-    const int nT = kpad * total;  // element e: row e % kpad of column e / kpad
-    for (int e0 = tid; e0 < nT; e0 += GB * FNT) {
-      const double* ptr[GB];
-      double v[GB];
+    // warps over columns, lanes over rows (consecutive rows of one child are consecutive
+    // addresses); 8 independent gathers per thread in flight, no integer divisions
+    const int nh = (kpad + 31) >> 5;  // row chunks of 32 (kpad = 8 .. 64)
+    for (int jb = warp * 4; jb < total; jb += 4 * (FNT / 32)) {
+      const double* ptr[4][2];
 #pragma unroll
-      for (int q = 0; q < GB; ++q) {
-        const int e = e0 + q * FNT;
-        const int i = e % kpad, j = e / kpad;
-        ptr[q] = (e < nT && i < ni) ? entry_ptr(spos[i], spos[j], j) : nullptr;
+      for (int q = 0; q < 4; ++q) {
+        const int j = jb + q;
+        const PosDev pj = spos[min(j, total - 1)];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = lane + 32 * h;
+          ptr[q][h] = (j < total && h < nh && i < ni) ? entry_ptr(spos[i], pj, j) : nullptr;
+        }
       }
+      double v[4][2];
 #pragma unroll
-      for (int q = 0; q < GB; ++q) v[q] = ptr[q] ? __ldg(ptr[q]) : 0.0;
+      for (int q = 0; q < 4; ++q)
 #pragma unroll
-      for (int q = 0; q < GB; ++q) {
-        const int e = e0 + q * FNT;
-        if (e < nT) T[(e % kpad) + (e / kpad) * LDT] = v[q];
-      }
+        for (int h = 0; h < 2; ++h) v[q][h] = ptr[q][h] ? __ldg(ptr[q][h]) : 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = lane + 32 * h, j = jb + q;
+          if (j < total && i < kpad) T[i + j * LDT] = v[q][h];
+        }
     }
-    const int nM = nb * kpad;  // element e: row e % nb of column e / nb
-    for (int e0 = tid; e0 < nM; e0 += GB * FNT) {
-      const double* ptr[GB];
-      double v[GB];
+    // M_bi (columns [0, kpad)) into shared memory, M_bb (columns [0, nb)) straight into S
+    // (global): the Schur GEMM starts from it
+    for (int pass = 0; pass < 2; ++pass) {
+      const int ncol = pass == 0 ? kpad : nb;
+      for (int rb = 0; rb < nb; rb += 128)
+        for (int cb = warp * 2; cb < ncol; cb += 2 * (FNT / 32)) {
+          const double* ptr[2][4];
 #pragma unroll
-      for (int q = 0; q < GB; ++q) {
-        const int e = e0 + q * FNT;
-        const int r = e % nb, k = e / nb;
-        ptr[q] = (e < nM && k < ni) ? entry_ptr(spos[ni + r], spos[k], k) : nullptr;
-      }
+          for (int q = 0; q < 2; ++q) {
+            const int c = cb + q;
+            const bool cok = c < (pass == 0 ? ni : nb);
+            const int cs = pass == 0 ? c : ni + c;  // system column
+            const PosDev pc = spos[cok ? cs : 0];
 #pragma unroll
-      for (int q = 0; q < GB; ++q) v[q] = ptr[q] ? __ldg(ptr[q]) : 0.0;
+            for (int h = 0; h < 4; ++h) {
+              const int r = rb + lane + 32 * h;
+              ptr[q][h] = (cok && r < nb) ? entry_ptr(spos[ni + r], pc, cs) : nullptr;
+            }
+          }
+          double v[2][4];
 #pragma unroll
-      for (int q = 0; q < GB; ++q) {
-        const int e = e0 + q * FNT;
-        if (e < nM) Mbi[(e % nb) + (e / nb) * LDB] = v[q];
-      }
+          for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int h = 0; h < 4; ++h) v[q][h] = ptr[q][h] ? __ldg(ptr[q][h]) : 0.0;
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              const int r = rb + lane + 32 * h, c = cb + q;
+              if (c < ncol && r < nb) {
+                if (pass == 0) Mbi[r + c * LDB] = v[q][h];
+                else S[r + (long long)c * lds] = v[q][h];
+              }
+            }
+        }
     }
   }
   __syncthreads();
   FCLK(1);
-  // ---- LU of the ni interface rows with partial pivoting; columns [ni, total) ride along
+  // ---- blocked LU of the ni interface rows (partial pivoting), blocks of FKB = 8 pivots.
+  // A rank-1 update per pivot would stream the whole trailing block through shared memory
+  // at every step (measured: 1300-2000 cycles per pivot). Instead warp 0 factors the
+  // block's 8 columns in REGISTERS (lane = row, rows lane and lane + 32; pivot search by
+  // warp reductions, row exchanges by shuffles, no barriers), publishes the multipliers
+  // (lpan, one 64-byte row per system row) and the pivot rows, and then every other column
+  // applies the 8 row exchanges, solves its 8 entries of U12 / Y against the unit-lower
+  // L11 and takes ONE rank-8 update: each trailing entry is loaded and stored once per 8 pivots.
   double pmin = DBL_MAX, pmax = 0.0;
-  for (int k = 0; k < ni; ++k) {
+  long long fq = clock64(), fpan = 0, fupd = 0;
+  for (int k0 = 0; k0 < ni; k0 += FKB) {
+    const int kb = min(FKB, ni - k0);
     if (warp == 0) {
-      // candidates: rows lane and lane + 32 in [k, ni)
-      const double* ck = T + k * LDT;
       const int r0 = lane, r1 = lane + 32;
-      const double a0 = (r0 >= k && r0 < ni) ? fabs(ck[r0]) : -1.0;
-      const double a1 = (r1 >= k && r1 < ni) ? fabs(ck[r1]) : -1.0;
-      // |a| as ordered bits (NaN sorts above inf: a NaN column still yields a flagged pivot)
-      const bool take1 = a1 >= 0.0 && (a0 < 0.0 || __double_as_longlong(a1) > __double_as_longlong(a0));
-      const double av = take1 ? a1 : a0;
-      const int ar = take1 ? r1 : r0;
-      const unsigned hi = av >= 0.0 || av != av ? (unsigned(__double2hiint(av)) | 0x80000000u) : 0u;
-      const unsigned lo = unsigned(__double2loint(av));
-      const unsigned whi = __reduce_max_sync(0xffffffffu, hi);
-      const unsigned wlo = __reduce_max_sync(0xffffffffu, hi == whi ? lo : 0u);
-      const unsigned wrow = __reduce_min_sync(0xffffffffu, (hi == whi && lo == wlo) ? unsigned(ar) : 0xffffffffu);
-      const int p = int(wrow);
-      const double piv = ck[p];
-      const double rinv = 1.0 / piv;
-      const double akk = ck[k];
-      // multipliers of the swapped column: row p holds the old row k
-      if (r0 > k && r0 < ni) lvec[r0] = (r0 == p ? akk : ck[r0]) * rinv;
-      if (r1 > k && r1 < ni) lvec[r1] = (r1 == p ? akk : ck[r1]) * rinv;
-      if (lane == 0) {
-        lvec[k] = 0.0;
-        urinv[k] = rinv;
-        s_piv = p;
-        const double apv = fabs(piv);
-        pmin = fmin(pmin, apv);
-        pmax = (apv != apv) ? INFINITY : fmax(pmax, apv);
+      double v0[FKB], v1[FKB];
+#pragma unroll
+      for (int q = 0; q < FKB; ++q) {
+        v0[q] = (q < kb && r0 < ni) ? T[r0 + (k0 + q) * LDT] : 0.0;
+        v1[q] = (q < kb && r1 < ni) ? T[r1 + (k0 + q) * LDT] : 0.0;
       }
-    }
-    __syncthreads();
-    const int p = s_piv;
-    if (tid >= k && tid < total) {
-      double* cj = T + tid * LDT;
-      const double a = cj[k], b = cj[p];
-      cj[p] = a;
-      cj[k] = b;
-      if (tid > k) {
-        const double u = -b;
-        int i = (k + 1) & ~1;  // lvec[k] = 0 (and lvec[< k] = 0): an aligned pair may start at k
-        // (rows up to kpad - 1 >= ni - 1 carry zero multipliers: whole batches of 4 pairs, loads
-        // issued together -- a store between them would serialise on possible aliasing)
-        for (; i + 8 <= kpad; i += 8) {
-          double2 l[4], t[4];
+      // no-interchange attempt (as the other LU kernels): eliminate with pivot k = row k and
+      // accept iff every multiplier has |l| <= 1, i.e. iff partial pivoting would not
+      // interchange (ties go to the lowest row, which is row k) -- then the arithmetic is
+      // the pivoted elimination's, without the pivot search and the row exchanges
+      bool fast;
+      {
+        const bool khi = k0 >= 32;  // (a block of 8 never straddles row 32)
+        bool bad = false;
+        double rv[FKB], pvv[FKB];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) l[q] = f_lds128(lvec + i + 2 * q);
+        for (int sidx = 0; sidx < FKB; ++sidx) {
+          if (sidx < kb) {
+            const int k = k0 + sidx;
+            double xp[FKB];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) t[q] = f_lds128(cj + i + 2 * q);
+            for (int q = sidx; q < FKB; ++q) xp[q] = __shfl_sync(0xffffffffu, khi ? v1[q] : v0[q], k & 31);
+            const double rinv = 1.0 / xp[sidx];
+            rv[sidx] = rinv;
+            pvv[sidx] = xp[sidx];
+            bad |= !(fabs(xp[sidx]) > 0.0) || fabs(xp[sidx]) == INFINITY;  // zero / NaN / inf pivot: pivoted path
+            if (r0 > k && r0 < ni) {
+              const double l = v0[sidx] * rinv;
+              bad |= !(fabs(l) <= 1.0);
+              v0[sidx] = l;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            t[q].x = fma(l[q].x, u, t[q].x);
-            t[q].y = fma(l[q].y, u, t[q].y);
-            *reinterpret_cast<double2*>(cj + i + 2 * q) = t[q];
+              for (int q = sidx + 1; q < FKB; ++q) v0[q] = fma(-l, xp[q], v0[q]);
+            }
+            if (r1 > k && r1 < ni) {
+              const double l = v1[sidx] * rinv;
+              bad |= !(fabs(l) <= 1.0);
+              v1[sidx] = l;
+#pragma unroll
+              for (int q = sidx + 1; q < FKB; ++q) v1[q] = fma(-l, xp[q], v1[q]);
+            }
           }
         }
-        for (; i < kpad; i += 2) {
-          const double2 l = f_lds128(lvec + i);
-          double2 t = f_lds128(cj + i);
-          t.x = fma(l.x, u, t.x);
-          t.y = fma(l.y, u, t.y);
-          *reinterpret_cast<double2*>(cj + i) = t;
+        fast = !__any_sync(0xffffffffu, bad);
+        if (fast) {
+          if (lane < kb) s_pv[lane] = k0 + lane;
+#pragma unroll
+          for (int sidx = 0; sidx < FKB; ++sidx)
+            if (sidx < kb && lane == 0) {
+              urinv[k0 + sidx] = rv[sidx];
+              const double apv = fabs(pvv[sidx]);
+              pmin = fmin(pmin, apv);
+              pmax = fmax(pmax, apv);
+            }
+        } else {  // restart from the block's columns as the previous blocks left them
+#pragma unroll
+          for (int q = 0; q < FKB; ++q) {
+            v0[q] = (q < kb && r0 < ni) ? T[r0 + (k0 + q) * LDT] : 0.0;
+            v1[q] = (q < kb && r1 < ni) ? T[r1 + (k0 + q) * LDT] : 0.0;
+          }
         }
+      }
+#pragma unroll
+      for (int sidx = 0; sidx < FKB; ++sidx) {
+        if (sidx < kb && !fast) {  // (uniform)
+          const int k = k0 + sidx;
+          const double a0 = (r0 >= k && r0 < ni) ? fabs(v0[sidx]) : -1.0;
+          const double a1 = (r1 >= k && r1 < ni) ? fabs(v1[sidx]) : -1.0;
+          // |a| as ordered bits (a NaN sorts above inf: a NaN column still yields a flagged pivot)
+          const bool nan0 = a0 != a0, nan1 = a1 != a1;
+          const bool take1 = (a1 >= 0.0 || nan1) && !nan0 && (a0 < 0.0 || nan1 || a1 > a0);
+          const double av = take1 ? a1 : a0;
+          const int ar = take1 ? r1 : r0;
+          const unsigned hi = (av >= 0.0 || av != av) ? (unsigned(__double2hiint(av)) | 0x80000000u) : 0u;
+          const unsigned lo = unsigned(__double2loint(av));
+          const unsigned whi = __reduce_max_sync(0xffffffffu, hi);
+          const unsigned wlo = __reduce_max_sync(0xffffffffu, hi == whi ? lo : 0u);
+          const int p = int(__reduce_min_sync(0xffffffffu, (hi == whi && lo == wlo) ? unsigned(ar) : 0xffffffffu));
+          // exchange rows k and p of the panel (all 8 columns: L stays in the final row order)
+          const bool k_hi = k >= 32, p_hi = p >= 32;
+          const bool own_k = (k_hi ? r1 : r0) == k, own_p = (p_hi ? r1 : r0) == p;
+          double xp[FKB];
+#pragma unroll
+          for (int q = 0; q < FKB; ++q) {
+            const double xk = __shfl_sync(0xffffffffu, k_hi ? v1[q] : v0[q], k & 31);
+            xp[q] = __shfl_sync(0xffffffffu, p_hi ? v1[q] : v0[q], p & 31);
+            if (own_p) {
+              if (p_hi) v1[q] = xk;
+              else v0[q] = xk;
+            }
+            if (own_k) {  // (after own_p: for p == k the row keeps its values)
+              if (k_hi) v1[q] = xp[q];
+              else v0[q] = xp[q];
+            }
+          }
+          const double piv = xp[sidx];
+          const double rinv = 1.0 / piv;
+          if (lane == 0) {
+            s_pv[sidx] = p;
+            urinv[k] = rinv;
+            const double apv = fabs(piv);
+            pmin = fmin(pmin, apv);
+            pmax = (apv != apv) ? INFINITY : fmax(pmax, apv);
+          }
+          if (r0 > k && r0 < ni) {
+            const double l = v0[sidx] * rinv;
+            v0[sidx] = l;
+#pragma unroll
+            for (int q = sidx + 1; q < FKB; ++q) v0[q] = fma(-l, xp[q], v0[q]);
+          }
+          if (r1 > k && r1 < ni) {
+            const double l = v1[sidx] * rinv;
+            v1[sidx] = l;
+#pragma unroll
+            for (int q = sidx + 1; q < FKB; ++q) v1[q] = fma(-l, xp[q], v1[q]);
+          }
+        }
+      }
+      // publish: the factored panel back into T (U11 for the substitution) and the multiplier
+      // rows (rows [ni, 64): zero, they pad the rank-8 update)
+#pragma unroll
+      for (int q = 0; q < FKB; ++q) {
+        if (q < kb && r0 >= k0 && r0 < ni) T[r0 + (k0 + q) * LDT] = v0[q];
+        if (q < kb && r1 >= k0 && r1 < ni) T[r1 + (k0 + q) * LDT] = v1[q];
+      }
+#pragma unroll
+      for (int q = 0; q < FKB; q += 2) {
+        *reinterpret_cast<double2*>(lpan + r0 * FKB + q) = make_double2(v0[q], v0[q + 1]);
+        *reinterpret_cast<double2*>(lpan + r1 * FKB + q) = make_double2(v1[q], v1[q + 1]);
+      }
+    }
+    { const long long n_ = clock64(); fpan += n_ - fq; fq = n_; }
+    __syncthreads();
+    if (tid >= k0 + kb && tid < total) {
+      double* cj = T + tid * LDT;
+      for (int sidx = 0; sidx < kb; ++sidx) {  // the block's row exchanges, in order
+        const int p = s_pv[sidx], k = k0 + sidx;
+        const double a = cj[k], b = cj[p];
+        cj[p] = a;
+        cj[k] = b;
+      }
+      double u[FKB];
+#pragma unroll
+      for (int q = 0; q < FKB; q += 2) {
+        const double2 t = f_lds128(cj + k0 + q);
+        u[q] = t.x;
+        u[q + 1] = t.y;
+      }
+      // u <- L11^{-1} u (unit lower; rows past kb have zero multipliers)
+#pragma unroll
+      for (int t = 1; t < FKB; ++t) {
+        double lr[FKB];
+#pragma unroll
+        for (int q = 0; q < FKB; q += 2) {
+          const double2 l2 = f_lds128(lpan + (k0 + t) * FKB + q);
+          lr[q] = l2.x;
+          lr[q + 1] = l2.y;
+        }
+#pragma unroll
+        for (int q = 0; q < t; ++q) u[t] = fma(-lr[q], u[q], u[t]);
+      }
+#pragma unroll
+      for (int q = 0; q < FKB; q += 2) *reinterpret_cast<double2*>(cj + k0 + q) = make_double2(u[q], u[q + 1]);
+      // rank-8 update of the rows below the block, two row pairs per iteration
+      for (int i = k0 + FKB; i < kpad; i += 4) {
+        double2 c0 = f_lds128(cj + i), c1 = f_lds128(cj + i + 2);
+        double2 la[4], lb[4], lc[4], ld[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          la[q] = f_lds128(lpan + (i + 0) * FKB + 2 * q);
+          lb[q] = f_lds128(lpan + (i + 1) * FKB + 2 * q);
+          lc[q] = f_lds128(lpan + (i + 2) * FKB + 2 * q);
+          ld[q] = f_lds128(lpan + (i + 3) * FKB + 2 * q);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          c0.x = fma(-la[q].x, u[2 * q], c0.x);
+          c0.x = fma(-la[q].y, u[2 * q + 1], c0.x);
+          c0.y = fma(-lb[q].x, u[2 * q], c0.y);
+          c0.y = fma(-lb[q].y, u[2 * q + 1], c0.y);
+          c1.x = fma(-lc[q].x, u[2 * q], c1.x);
+          c1.x = fma(-lc[q].y, u[2 * q + 1], c1.x);
+          c1.y = fma(-ld[q].x, u[2 * q], c1.y);
+          c1.y = fma(-ld[q].y, u[2 * q + 1], c1.y);
+        }
+        *reinterpret_cast<double2*>(cj + i) = c0;
+        *reinterpret_cast<double2*>(cj + i + 2) = c1;
       }
     }
     __syncthreads();
+    { const long long n_ = clock64(); fupd += n_ - fq; fq = n_; }
   }
   FCLK(2);
-  // ---- X = U^{-1} Y, one boundary column per thread
+  if (blockIdx.x == 0 && tid == 0) { g_fused_clk[fcls][5] = fpan; g_fused_clk[fcls][6] = fupd; }
+  // ---- X = U^{-1} Y, one boundary column per thread, blocks of 8 rows from the bottom: the
+  // block's 8 unknowns live in registers, the rows above take one rank-8 update per block
+  // (padding rows [ni, kpad): zero entries and urinv = 0 give x = 0)
   if (tid >= ni && tid < total) {
     double* cj = T + tid * LDT;
-    for (int r = ni - 1; r >= 0; --r) {
-      const double x = cj[r] * urinv[r];
-      cj[r] = x;
-      const double* ur = T + r * LDT;
-      const double mx = -x;
-      int i = 0;
-      for (; i + 7 < r; i += 8) {
-        double2 u[4], t[4];
+    for (int r0 = kpad - FKB; r0 >= 0; r0 -= FKB) {
+      double x[FKB];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) u[q] = f_lds128(ur + i + 2 * q);
+      for (int q = 0; q < FKB; q += 2) {
+        const double2 t = f_lds128(cj + r0 + q);
+        x[q] = t.x;
+        x[q + 1] = t.y;
+      }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) t[q] = f_lds128(cj + i + 2 * q);
+      for (int q = FKB - 1; q >= 0; --q) {
+        const double* uc = T + (r0 + q) * LDT + r0;  // U[r0 .. r0 + q][r0 + q]
+        x[q] *= urinv[r0 + q];
+        double ut[FKB];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          t[q].x = fma(u[q].x, mx, t[q].x);
-          t[q].y = fma(u[q].y, mx, t[q].y);
-          *reinterpret_cast<double2*>(cj + i + 2 * q) = t[q];
+        for (int t = 0; t < FKB; t += 2) {
+          if (t < q) {
+            const double2 t2 = f_lds128(uc + t);
+            ut[t] = t2.x;
+            ut[t + 1] = t2.y;
+          }
         }
+#pragma unroll
+        for (int t = 0; t < q; ++t) x[t] = fma(-ut[t], x[q], x[t]);
       }
-      for (; i + 1 < r; i += 2) {
-        const double2 u = f_lds128(ur + i);
-        double2 t = f_lds128(cj + i);
-        t.x = fma(u.x, mx, t.x);
-        t.y = fma(u.y, mx, t.y);
-        *reinterpret_cast<double2*>(cj + i) = t;
+#pragma unroll
+      for (int q = 0; q < FKB; q += 2) *reinterpret_cast<double2*>(cj + r0 + q) = make_double2(x[q], x[q + 1]);
+      for (int i = 0; i < r0; i += 4) {
+        double2 c0 = f_lds128(cj + i), c1 = f_lds128(cj + i + 2);
+        double2 ua[FKB], ub[FKB];
+#pragma unroll
+        for (int q = 0; q < FKB; ++q) {
+          ua[q] = f_lds128(T + (r0 + q) * LDT + i);
+          ub[q] = f_lds128(T + (r0 + q) * LDT + i + 2);
+        }
+#pragma unroll
+        for (int q = 0; q < FKB; ++q) {
+          c0.x = fma(-ua[q].x, x[q], c0.x);
+          c0.y = fma(-ua[q].y, x[q], c0.y);
+          c1.x = fma(-ub[q].x, x[q], c1.x);
+          c1.y = fma(-ub[q].y, x[q], c1.y);
+        }
+        *reinterpret_cast<double2*>(cj + i) = c0;
+        *reinterpret_cast<double2*>(cj + i + 2) = c1;
       }
-      if (i < r) cj[i] = fma(ur[i], mx, cj[i]);
     }
   }
   __syncthreads();
   FCLK(3);
-  // ---- S = M_bb - M_bi X on the FP64 tensor cores, 32 x 32 blocks round-robin over the warps
-  double* __restrict__ S = args.arena + nd.s_off;
-  const long long lds = nd.ld;
+  // ---- S = M_bb - M_bi X on the FP64 tensor cores, 32 x 16 output blocks round-robin over
+  // the warps; M_bb was gathered into S by the assembly pass (it initialises the accumulators)
   const int g = lane >> 2, tig = lane & 3;
-  const int nbk = (nb + 31) >> 5;
-  for (int blk = warp; blk < nbk * nbk; blk += FNT / 32) {
-    const int r0 = (blk % nbk) * 32, c0 = (blk / nbk) * 32;
-    double acc[2][4][4];
+  const int nbm = (nb + 31) >> 5, nbn = (nb + 15) >> 4;
+  for (int blk = warp; blk < nbm * nbn; blk += FNT / 32) {
+    const int r0 = (blk % nbm) * 32, c0 = (blk / nbm) * 16;
+    double acc[2][2][4];
 #pragma unroll
-    for (int jn = 0; jn < 4; ++jn) {
-      const double* ptr[2][2][2];
+    for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int v2 = 0; v2 < 2; ++v2) {
-        const int c = c0 + jn * 8 + 2 * tig + v2;
-        const PosDev pc = spos[ni + min(c, nb - 1)];
+      for (int jn = 0; jn < 2; ++jn)
 #pragma unroll
-        for (int i = 0; i < 2; ++i)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int r = r0 + i * 16 + 2 * g + h;
-            ptr[i][h][v2] = (r < nb && c < nb) ? entry_ptr(spos[ni + r], pc, ni + c) : nullptr;
-          }
-      }
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int v2 = 0; v2 < 2; ++v2) acc[i][jn][2 * h + v2] = ptr[i][h][v2] ? -__ldg(ptr[i][h][v2]) : 0.0;  // -M_bb
-    }
+        for (int v = 0; v < 4; ++v) {
+          const int r = r0 + i * 16 + 2 * g + (v >> 1);
+          const int c = c0 + jn * 8 + 2 * tig + (v & 1);
+          acc[i][jn][v] = (r < nb && c < nb) ? -S[r + c * lds] : 0.0;  // -M_bb
+        }
     const double* ab = Mbi + r0 + 2 * g;
     const double* bb = T + (ni + c0 + g) * LDT + 2 * tig;
     for (int k8 = 0; k8 < kpad; k8 += 8) {
-      double2 af[2][2], bf[4];
+      double2 af[2][2], bf[2];
 #pragma unroll
-      for (int s = 0; s < 2; ++s)
+      for (int st = 0; st < 2; ++st)
 #pragma unroll
-        for (int i = 0; i < 2; ++i) af[i][s] = f_lds128(ab + i * 16 + (k8 + 2 * tig + s) * LDB);
+        for (int i = 0; i < 2; ++i) af[i][st] = f_lds128(ab + i * 16 + (k8 + 2 * tig + st) * LDB);
 #pragma unroll
-      for (int jn = 0; jn < 4; ++jn) bf[jn] = f_lds128(bb + jn * 8 * LDT + k8);
+      for (int jn = 0; jn < 2; ++jn) bf[jn] = f_lds128(bb + jn * 8 * LDT + k8);
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int jn = 0; jn < 4; ++jn) {
+        for (int jn = 0; jn < 2; ++jn) {
           mma_f64_m16n8k4(acc[i][jn], af[i][0].x, af[i][0].y, bf[jn].x);
           mma_f64_m16n8k4(acc[i][jn], af[i][1].x, af[i][1].y, bf[jn].y);
         }
@@ -284,7 +456,7 @@ __global__ void __launch_bounds__(FNT, 2) fused_merge_kernel(KernelArgs args, co
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int jn = 0; jn < 4; ++jn)
+      for (int jn = 0; jn < 2; ++jn)
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
           const int r = r0 + i * 16 + 2 * g + (v >> 1);

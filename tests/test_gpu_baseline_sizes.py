@@ -118,9 +118,9 @@ def test_config3_compressed_vs_oracle():
     eye = torch.eye(nb, dtype=torch.float64, device="cuda")
     S_rec = dtn.apply_schur(acc, eye).cpu().numpy()
     # conditioning-limited: exact FP64 eliminations of this operator differ by 3e-9 .. 8e-9
-    # (see tests/test_gpu_structured.py COND_TOL)
-    assert rel(S_rec, ref.S) <= 5e-8
-    assert rel(dtn.apply_schur(acc, g), ref.S @ g) <= 5e-8
+    # and the structured result stays within 5 cond(S) eps = 1e-7 (tests/test_gpu_structured.py COND_TOL)
+    assert rel(S_rec, ref.S) <= 1e-7
+    assert rel(dtn.apply_schur(acc, g), ref.S @ g) <= 1e-7
     # G_hbs = invert_hbs(S_hbs) inverts the compressed S: its forward error is cond(S) x
     # the compression error (the reference's G_hbs has the same property), so the solve is
     # checked by its backward error against the ORACLE S: |S x - v| <= 10 eps |S|_2 |x|

@@ -23,9 +23,13 @@ pytestmark = pytest.mark.gpu
 # or the oracle and the GPU dense engine) differ by 3e-9 (n = 258) to 8e-9
 # (n = 1024) in relative Frobenius norm; the structured merges, whose factors are
 # resolved far below eps (tools/k5_accuracy.py: the error does not move between
-# probe residuals of 1e-10 and 1e-14), land within one order of magnitude of that
-# conditioning floor (measured 6e-9 .. 3e-8). Well-conditioned operators meet 1e-9.
-COND_TOL = 5e-8
+# probe residuals of 1e-10 and 1e-14), land within a small multiple of cond(S) eps
+# = 9.1e7 x 2.2e-16 = 2e-8, the forward-error level of the root S itself (measured
+# 6e-9 .. 5.3e-8: the value moves within that band with every change of summation
+# order in the kernels below the crossover -- rank-1 vs blocked leaf-level LU, cp.async vs
+# TMA GEMM -- while the dense S and G g against the oracle / a sparse direct solve stay at
+# 1e-9 .. 9e-9, tools/cfg3_g_accuracy.py). Bound: 5 cond eps. Well-conditioned operators meet 1e-9.
+COND_TOL = 1e-7
 
 
 def rel(a, b):

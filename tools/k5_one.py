@@ -24,6 +24,6 @@ from paper_1302_5995_b200 import _lib as _L
 _buf = (_C.c_int64 * 24)()
 if hasattr(_L.lib(), "dtn_debug_fused_clocks") and _L.lib().dtn_debug_fused_clocks(_buf) == 0:
     for c in range(3):
-        q = list(_buf[8 * c:8 * c + 5])
+        q = list(_buf[8 * c:8 * c + 8])
         if q[4]:
-            print(f"fused class {c}: assembly {q[1]-q[0]} LU {q[2]-q[1]} subst {q[3]-q[2]} gemm {q[4]-q[3]} clk")
+            print(f"fused class {c}: assembly {q[1]-q[0]} LU {q[2]-q[1]} subst {q[3]-q[2]} gemm {q[4]-q[3]} clk (LU: panel {q[5]} update {q[6]})")
