@@ -651,7 +651,7 @@ def run_b200_compressed(args, cfg, rank, world, local):
             "launches": dom["launches"], "avg_launch_ms": dom["ms"] / max(1, dom["launches"]),
             "peak_source": peak_src + " (FP64; DMMA and DFMA share the FP64 peak on B200)"}
     try:
-        with open(os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02c_ncu_traffic.json")) as f:
             roof["traffic"] = json.load(f).get(dom_name)
     except Exception:
         pass

@@ -203,6 +203,11 @@ int dtn_gpu_collective_flops(int32_t n, int32_t n_leaf, int32_t leaf_side, int32
  * column-major matrix with the engine's blocked kernels; ni == n is a full LU. */
 int dtn_debug_partial_lu(int32_t n, int32_t ni, const double* A, double* out, int32_t* ipiv, double* pivstat);
 
+/* Diagnostic: phase clocks (SM cycles) of CTA 0 of the last fused-merge launch of each of the three
+ * size classes: out24[8 c + {0..4}] = start, assembled, factored, substituted, done; [5], [6] = the
+ * LU's panel / update shares. */
+int dtn_debug_fused_clocks(int64_t* out24);
+
 /* Test hook: C (m x n, in/out) = alpha A B + beta C on host column-major operands through the
  * engine's FP64 tensor-core GEMMs; path 0 = cp.async-staged kernels, 1 = the TMA-staged kernel. */
 int dtn_debug_gemm(int32_t m, int32_t n, int32_t k, const double* A, const double* B, double* C, double alpha,

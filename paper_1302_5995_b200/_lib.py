@@ -51,7 +51,7 @@ EXPORTS = [
     "dtn_gpu_free", "dtn_gpu_boundary", "dtn_gpu_export", "dtn_gpu_export_device", "dtn_gpu_device_ptrs",
     "dtn_gpu_apply", "dtn_gpu_ring_dtn", "dtn_gpu_body_map",
     "dtn_gpu_num_boxes", "dtn_gpu_box_info", "dtn_gpu_box_schur", "dtn_gpu_level_stats", "dtn_gpu_build_stats", "dtn_gpu_kernel_stats",
-    "dtn_discretize_continuum", "dtn_discretize_network", "dtn_debug_partial_lu", "dtn_debug_gemm", "dtn_gpu_shard_info",
+    "dtn_discretize_continuum", "dtn_discretize_network", "dtn_debug_partial_lu", "dtn_debug_gemm", "dtn_debug_fused_clocks", "dtn_gpu_shard_info",
     "dtn_gpu_hbs_compress", "dtn_gpu_hbs_compress_op", "dtn_gpu_hbs_free", "dtn_gpu_hbs_info", "dtn_gpu_hbs_tree",
     "dtn_gpu_hbs_factor", "dtn_gpu_hbs_apply", "dtn_gpu_hbs_serialize", "dtn_gpu_hbs_deserialize",
     "dtn_gpu_hbs_invert", "dtn_gpu_build_accel", "dtn_gpu_root_rhs", "dtn_gpu_hbs_launch_count", "dtn_gpu_collective_flops",
@@ -106,6 +106,7 @@ def lib():
     L.dtn_discretize_network.argtypes = [i32, f64, f64, C.c_uint64, vp]
     L.dtn_debug_partial_lu.argtypes = [i32, i32, vp, vp, vp, vp]
     L.dtn_debug_gemm.argtypes = [i32, i32, i32, vp, vp, vp, f64, f64, i32]
+    L.dtn_debug_fused_clocks.argtypes = [vp]
     L.dtn_gpu_shard_info.argtypes = [i32, i32, i32, i32, i32, P(i32), P(i64)]
     L.dtn_gpu_hbs_compress.argtypes = [vp, vp, i64, i64, C.c_int, f64, i64, P(vp)]
     L.dtn_gpu_hbs_compress_op.argtypes = [vp, C.c_int, f64, i64, P(vp)]
