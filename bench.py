@@ -211,7 +211,7 @@ def accel_opt(dtn):
     return dtn.AccelOptions(epsilon=EPS, crossover=CROSSOVER, hbs_leaf=64)
 
 
-def compressed_build(dtn, torch, ctx, dev, stream, cfgno, n_int, leaf=32, reps=2):
+def compressed_build(dtn, torch, ctx, dev, stream, cfgno, n_int, leaf=32, reps=2, cpu=None):
     """build_root_accel (structured merges + compress + invert_hbs) of a BASELINE
     operator on one GPU from an HBM-resident stencil: device time of the whole call
     (CUDA events on the context stream), the structured build's own statistics, and
@@ -242,6 +242,24 @@ def compressed_build(dtn, torch, ctx, dev, stream, cfgno, n_int, leaf=32, reps=2
            "S_hbs_max_rank": sol.S_hbs.max_rank(), "G_hbs_max_rank": sol.G_hbs.max_rank(),
            "S_hbs_bytes": sol.S_hbs.payload_bytes(), "G_hbs_bytes": sol.G_hbs.payload_bytes(),
            "level_stats": [{"level": l.level, "max_rank": l.max_rank, "bytes": l.bytes} for l in sol.level_stats]}
+    if cpu is not None:  # the oracle port on the host cores, one full build of the same operator (S and G):
+        # a CPU figure and a parity check beside this configuration too (rank 0, N = 1 only)
+        try:
+            from oracle import oracle as O
+            name, kappa = cpu
+            threads = os.cpu_count() or 1
+            t0 = time.perf_counter()
+            ref = O.build_root_dense(O.Problem(name, n_int + 2, kappa), O.Tree(n_int + 2, uniform_side=leaf),
+                                     threads=threads, mode=2)
+            dt = time.perf_counter() - t0
+            g = seeded_vectors(len(ref.boundary), 16)
+            out["cpu_baseline"] = {"value": n_int ** 2 / dt, "unit": "grid-points/s", "cores": threads, "kind": "port",
+                                   "sample": f"one full config{cfgno} build (S and G), C++ restatement of "
+                                             "dense_nd.cpp (OpenBLAS, all host threads)", "seconds": dt}
+            out["parity"] = {"Sg_hbs_rel_fro_vs_oracle": O.rel_fro(dtn.apply_schur(sol, g), ref.S @ g), "tol": 1e-9}
+            del ref
+        except Exception as e:  # pragma: no cover
+            out["cpu_baseline"] = {"value": None, "error": repr(e)}
     del sol
     d = dtn.build_root_gpu(None, tree, want_G=False, ctx=ctx, stencil_device_ptr=st.data_ptr())
     d.free()
@@ -717,7 +735,8 @@ def run_b200_compressed(args, cfg, rank, world, local):
         if not args.no_cfg4:
             for key, cno, ni_ in (("config4_compressed", 4, 4096), ("config5_compressed_build", 5, 2048)):
                 try:
-                    line[key] = compressed_build(dtn, torch, ctx, dev, stream, cno, ni_)
+                    cpu = ("helmholtz", 100.0) if (cno == 5 and not args.no_cpu_baseline) else None
+                    line[key] = compressed_build(dtn, torch, ctx, dev, stream, cno, ni_, cpu=cpu)
                 except Exception as e:  # pragma: no cover
                     line[key] = {"error": repr(e)}
             try:
