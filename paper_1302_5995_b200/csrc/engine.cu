@@ -2005,6 +2005,14 @@ int rank_raise_div() {
   return v;
 }
 
+int rank_raise_fine() {  // DTN_RANK_RAISE_FINE=0: always the full step
+  static const int v = [] {
+    const char* e = std::getenv("DTN_RANK_RAISE_FINE");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+
 // Factor ranks that failed the range-finder check of a structured build (tail of the
 // sketch's R diagonal above tol): raise them by ell / DTN_RANK_RAISE (at least 16), per
 // J edge size.
@@ -2015,7 +2023,12 @@ bool raise_ranks(const dtn_op* op, double tol, std::vector<std::pair<int, int>>&
     if (!(D.h_qstat[2 * q + 1] > tol)) continue;
     const Node& nd = D.P.nodes[size_t(D.qr_node[q])];
     if (nd.ell >= nd.jn) continue;  // already exact
-    const int want = std::min({nd.jn, 252, int(align_up(nd.ell + std::max(16, nd.ell / rank_raise_div()), 8))});
+    // far from resolved (probe residual > 30 tol): ell / DTN_RANK_RAISE (at least 16); close to it
+    // (the residual falls geometrically with the rank): half that step (at least 8), so that the
+    // learned rank ends near the numerical one instead of a full step above it
+    const bool far = !(D.h_qstat[2 * q + 1] <= 30.0 * tol) || rank_raise_fine() == 0;
+    const int step = far ? std::max(16, nd.ell / rank_raise_div()) : std::max(8, nd.ell / (2 * rank_raise_div()));
+    const int want = std::min({nd.jn, 252, int(align_up(nd.ell + step, 8))});
     if (want <= nd.ell) continue;  // at the cap
     auto it = std::find_if(over.begin(), over.end(), [&](const auto& e) { return e.first == nd.jn; });
     if (it == over.end()) {
@@ -2060,7 +2073,7 @@ int build_adaptive(dtn_ctx* ctx, const dtn_problem* prob, const dtn_opts* opts, 
     const int rc = build_impl(ctx, prob, opts, over, &op, world, wrank, comm);
     if (rc != DTN_OK) return rc;
     std::vector<std::pair<int, int>> next = over;
-    if (attempt < 6 && raise_ranks(op, rank_tol_factor() * eps, next)) {
+    if (attempt < 8 && raise_ranks(op, rank_tol_factor() * eps, next)) {
       PlanDev* stale = op->plan;
       dtn_gpu_free(op);
       {  // the failed attempt's plan (arena, graph) is not reused: drop it
