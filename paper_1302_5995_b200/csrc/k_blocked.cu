@@ -154,7 +154,8 @@ __device__ long long g_pro_clk[8];
 
 #ifdef DTN_PANEL_PROFILE
 __device__ long long g_p2_clk[16];
-#define P2CLK(slot) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_p2_clk[slot] = clock64(); } while (0)
+__device__ long long g_p2b_clk[16];  // the same points seen by the LAST thread of the last CTA (a row that works)
+#define P2CLK(slot) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_p2_clk[slot] = clock64(); if (blockIdx.x == gridDim.x - 1 && threadIdx.x == blockDim.x / 2) g_p2b_clk[slot] = clock64(); } while (0)
 #define P2ACC(slot, t) do { if (blockIdx.x == 0 && threadIdx.x == 0) { const long long n_ = clock64(); g_p2_clk[slot] += n_ - (t); (t) = n_; } } while (0)
 #else
 #define P2CLK(slot) do { } while (0)
@@ -1076,7 +1077,9 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
             if (r >= rlo && r < Ri) {
               const double l = v[a][0] * urinv[j];
               if (track && !(fabs(l) <= 1.0) && jf == PKB) jf = j;
+#ifndef DTN_PROBE_NOSTORE
               M[r + (long long)j * ldm] = l;
+#endif
               shift_update_w<W>(v[a], l, ub + j * PLD);
             }
           }
@@ -1626,6 +1629,16 @@ cudaError_t blocked_init() {
                              int(panel_dyn_smem(1, 128)));
     if (e != cudaSuccess) return e;
   }
+  {
+    cudaError_t e = cudaFuncSetAttribute(panel2_kernel<true, 2, 128>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(panel2_kernel<true, 2, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(panel_dyn_smem(2, 128)));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(panel2_kernel<false, 2, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(panel_dyn_smem(2, 128)));
+    if (e != cudaSuccess) return e;
+  }
   cudaError_t e = cudaFuncSetAttribute(panel_kernel<true, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(panel_kernel<true, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -1686,11 +1699,29 @@ static int panel_small_nt() {
   return v;
 }
 
+static bool panel_r2() {
+  static const bool on = [] {
+    const char* e = std::getenv("DTN_PANEL_R2");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 void panel_shape(int max_rows, int* rpt, int* csize, int* nt) {
   *nt = PNT;
   if (!panel_legacy() && max_rows <= 128 && panel_small_nt1()) {  // one 128-thread CTA: 3 per SM
     *rpt = 1;
     *csize = 1;
+    *nt = 128;
+    return;
+  }
+  // DTN_PANEL_R2=1: 128-thread CTAs with TWO rows per thread (the cluster size of the default,
+  // half the warps per SM): the substitution, the prologue update and the pivoted update all
+  // re-read the 32-entry pivot / U row from shared memory in every lane, 8 warps x 256 B x 4
+  // quarter-warp passes per step -- shared-memory bandwidth, not FP64 issue, bounds them
+  if (!panel_legacy() && panel_r2() && max_rows > PNT && max_rows <= PMAXC * PNT) {
+    *rpt = 2;
+    *csize = (max_rows + PNT - 1) / PNT;
     *nt = 128;
     return;
   }
@@ -1800,6 +1831,8 @@ cudaError_t launch_panel(const KernelArgs& args, const int* d_list, int count, i
   int rpt, csize, nt;
   panel_shape(max_rows, &rpt, &csize, &nt);
   if (csize > PMAXC) return cudaErrorInvalidValue;
+  if (nt == 128 && rpt == 2 && csize == 1) return launch_panel_t<false, 2, 128>(args, d_list, count, k0, kb, 1, st, fused);
+  if (nt == 128 && rpt == 2) return launch_panel_t<true, 2, 128>(args, d_list, count, k0, kb, csize, st, fused);
   if (nt == 128 && csize == 1) return launch_panel_t<false, 1, 128>(args, d_list, count, k0, kb, 1, st, fused);
   if (nt == 128) return launch_panel_t<true, 1, 128>(args, d_list, count, k0, kb, csize, st, fused);
   if (csize == 1 && rpt == 2) return launch_panel_t<false, 2>(args, d_list, count, k0, kb, 1, st, fused);

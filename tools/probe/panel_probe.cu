@@ -134,7 +134,9 @@ int main() {
         if (r >= 2) best = ms < best ? ms : best;
       }
       { long long q[16]; cudaMemcpyFromSymbol(q, g_p2_clk, sizeof(q));
-        printf("  p2 clk: load+prologue %lld save %lld topLU %lld ubsync %lld subst %lld check %lld final %lld tail %lld\n", q[1]-q[0], q[2]-q[1], q[3]-q[2], q[4]-q[3], q[5]-q[4], q[6]-q[5], q[7]-q[6], q[8]-q[7]); }
+        printf("  p2 clk: load+prologue %lld save %lld topLU %lld ubsync %lld subst %lld check %lld final %lld tail %lld\n", q[1]-q[0], q[2]-q[1], q[3]-q[2], q[4]-q[3], q[5]-q[4], q[6]-q[5], q[7]-q[6], q[8]-q[7]);
+        long long w[16]; cudaMemcpyFromSymbol(w, g_p2b_clk, sizeof(w));
+        printf("  last thread of the last CTA: load+prologue %lld save %lld (wait for top LU) %lld ubsync %lld subst %lld check %lld final %lld tail %lld | vs thread 0: start %+lld end %+lld\n", w[1]-w[0], w[2]-w[1], w[3]-w[2], w[4]-w[3], w[5]-w[4], w[6]-w[5], w[7]-w[6], w[8]-w[7], w[0]-q[0], w[8]-q[8]); }
       long long pc[8];
       cudaMemcpyFromSymbol(pc, g_pro_clk, sizeof(pc));
       printf("rows %5d panel(k0=32) fused=%d%s: best %.1f us  prologue clk: loads %lld solve %lld update %lld | save %lld topLU %lld subst %lld check %lld\n", n,
