@@ -867,6 +867,7 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
   __shared__ int m_dst[2 * PKB], m_src[2 * PKB];
   __shared__ int fast_fail, jtop_s, fail_all;
   __shared__ int mv_dst[2 * PKB], mv_src[2 * PKB];
+  __shared__ __align__(8) unsigned long long mbar_u[PKB];  // pipelined substitution: one per U row
   extern __shared__ __align__(16) double pdyn[];
   double* ub = pdyn;               // [PKB][PLD]: U11 rows SHIFTED, ub[j * PLD + c] = U[j][j + c]
   double* urinv = ub + PKB * PLD;  // [PKB] reciprocal pivots
@@ -890,12 +891,38 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
   P2CLK(0);
   double v[RPT][PKB];
   int elim[RPT];
+  const bool pipe_req = (use_fast & 0x20000000) != 0;  // launcher flag (DTN_PANEL_PIPE)
+  use_fast &= ~0x20000000;
   const bool try_fast = use_fast && (k0 == 0 || *(volatile int*)pivoting_flag(args, nd) < use_fast);
   if (k0 == 0 && crank == 0 && tid == 0) *pivoting_flag(args, nd) = 0;
+  // Pipelined substitution (clusters): rank 0's warp 0 pushes every U row of the top block to all
+  // CTAs as it is formed (st.async + one mbarrier per row), and the rows below run substitution
+  // step j as soon as row j has landed -- they trail the top LU by one step instead of
+  // starting after it.
+  // (pipelined launches use the LIGHT LEAD row map: rank 0 holds only the 32 top rows, so its warp 0
+  // factors the top block with no other warp of its SM computing; warp 1 forwards the rows)
+  const bool lead32 = CL && pipe_req;
+  const bool piped = lead32 && try_fast;
+  auto rowof = [&](int a_) -> int {
+    if (!lead32) return crank * PNT + tid + stride * a_;
+    if (crank == 0) return (a_ == 0 && tid < PKB) ? tid : (1 << 28);
+    return PKB + (crank - 1) * PNT + tid + (csize - 1) * PNT * a_;
+  };
+  const bool idle_warp = lead32 && crank == 0 && warp != 0;  // no rows: skips the prologue update
+  if constexpr (CL) {
+    if (piped) {
+      if (tid == 0) fast_fail = fail_all = PKB;
+      if (tid < PKB) mbar_init(&mbar_u[tid], 1);
+      if (tid < PKB) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      __syncthreads();
+      if (tid < kbe && crank != 0) mbar_arm(&mbar_u[tid], (PKB + 1) * 8);  // (rank 0: a plain arrive by warp 0)
+      cg::this_cluster().sync();  // every CTA's barriers are armed before the first push
+    }
+  }
   if (k0 == 0 || !fused) {
 #pragma unroll
     for (int a = 0; a < RPT; ++a) {
-      const int r = crank * PNT + tid + stride * a;
+      const int r = rowof(a);
 #pragma unroll
       for (int c = 0; c < PKB; ++c) v[a][c] = (r < Ri && c < kbe) ? M[r + c * ldm] : 0.0;
       if (k0 == 0 && r < Ri) perm[r] = r;
@@ -904,10 +931,13 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
     // fused prologue (as panel_kernel): step kp = k0 - kb applied to this panel's columns
     const int kp = k0 - kb;
     double* Mg = args.arena + nd.m_off;
-    double* l11 = ub;  // [PKB][PLD], L11[i][m] at i * PLD + m (unshifted; free until the fast path)
+    // [PKB][PLD], L11[i][m] at i * PLD + m (unshifted). ub is free until the fast path -- unless rows
+    // are pushed into it by rank 0 while this CTA is still here (pipelined): then the pivoted loop's
+    // exchange buffer, idle until that loop, holds it
+    double* l11 = piped ? &rows[0][0][0] : ub;
 #pragma unroll
     for (int a = 0; a < RPT; ++a) {
-      const int r = crank * PNT + tid + stride * a;
+      const int r = rowof(a);
       double* lr = psave + (a * PNT + tid) * (PKB + 1);
       if (r < Ri) {
         const long long R = k0 + r;
@@ -956,7 +986,7 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
     const bool displaced = m_dst[PKB] >= 0;
 #pragma unroll
     for (int a = 0; a < RPT; ++a) {
-      const int r = crank * PNT + tid + stride * a;
+      const int r = rowof(a);
       if (displaced && r < Ri) {
         const int R = k0 + r;
         int src = R;
@@ -969,10 +999,10 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
       }
     }
     __syncthreads();
-    const bool lead = try_fast && crank == 0;
+    const bool lead = try_fast && crank == 0 && !lead32;
     if (lead && warp != 0) asm volatile("bar.sync 1, %0;" ::"r"(PNT) : "memory");
 #pragma unroll 2
-    for (int m = 0; m < kb; ++m) {
+    for (int m = 0; m < (idle_warp ? 0 : kb); ++m) {
       double lm[RPT];
 #pragma unroll
       for (int a = 0; a < RPT; ++a) lm[a] = psave[(a * PNT + tid) * (PKB + 1) + m];
@@ -990,7 +1020,7 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
     if (lead && warp == 0) asm volatile("bar.arrive 1, %0;" ::"r"(PNT) : "memory");
 #pragma unroll
     for (int a = 0; a < RPT; ++a) {
-      const int r = crank * PNT + tid + stride * a;
+      const int r = rowof(a);
 #pragma unroll
       for (int c = 0; c < PKB; ++c)
         if (c >= kbe || r >= Ri) v[a][c] = 0.0;
@@ -998,7 +1028,7 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
   }
 #pragma unroll
   for (int a = 0; a < RPT; ++a) {
-    const int r = crank * PNT + tid + stride * a;
+    const int r = rowof(a);
     elim[a] = (r < Ri) ? -1 : PKB;
   }
   P2CLK(1);
@@ -1014,7 +1044,7 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
     for (int a = 0; a < RPT; ++a)
 #pragma unroll
       for (int c = 0; c < PKB; ++c) psave[(a * PNT + tid) * (PKB + 1) + c] = v[a][c];
-    if (tid == 0) fast_fail = fail_all = PKB;
+    if (!piped && tid == 0) fast_fail = fail_all = PKB;
     int jf = PKB;
     P2CLK(2);
     if (crank == 0 && warp == 0) {  // rows 0..kbe-1 in lanes 0..kbe-1 (a = 0)
@@ -1033,6 +1063,11 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
             urinv[j] = rnext;
           }
           __syncwarp();
+          if constexpr (CL) {
+            if (piped && lane == 0) {  // row j is in ub: release it to the forwarding warp
+              asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&mbar_u[j])) : "memory");
+            }
+          }
           if (lane > j && lane < kbe) {
             const double l = v[0][0] * urinv[j];
             if (!(fabs(l) <= 1.0) && jf == PKB) jf = j;
@@ -1051,29 +1086,53 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
         for (int c = 0; c < PLD; ++c) ub[j * PLD + c] = 0.0;
       }
       const int jt = __reduce_min_sync(0xffffffffu, unsigned(jf));
-      if (lane == 0) fast_fail = jt;
+      if (lane == 0) {
+        if (piped) atomicMin(&fast_fail, jt);  // (the other warps may already have recorded theirs)
+        else fast_fail = jt;
+      }
+    }
+    if constexpr (CL) {
+      if (piped && crank == 0 && warp == 1) {
+        // forwarding warp: U row j (shifted) and 1 / u_jj to every other CTA as soon as warp 0 has
+        // formed it (st.async, completing that CTA's barrier of row j)
+        for (int j = 0; j < kbe; ++j) {
+          mbar_wait(&mbar_u[j], 0u);
+          const double val = ub[j * PLD + lane];
+          const double rj = urinv[j];
+          for (int d = 1; d < csize; ++d) {
+            const unsigned mb = cluster_map(&mbar_u[j], d);
+            st_async_b64(cluster_map(ub + j * PLD + lane, d), __double_as_longlong(val), mb);
+            if (lane == 0) st_async_b64(cluster_map(urinv + j, d), __double_as_longlong(rj), mb);
+          }
+        }
+      }
     }
     P2CLK(3);
     if constexpr (CL) {
+      if (!piped) {
       cg::this_cluster().sync();
       if (crank != 0) {
         const double* rub = cg::this_cluster().map_shared_rank(ub, 0);
         for (int e = tid; e < PKB * PLD + PKB; e += PNT) ub[e] = rub[e];
         if (tid == 0) jtop_s = *cg::this_cluster().map_shared_rank(&fast_fail, 0);
       }
+      }
     }
-    __syncthreads();
-    if (crank == 0 && tid == 0) jtop_s = fast_fail;
-    __syncthreads();
-    const int jtop = jtop_s;
-    auto subst = [&](int rlo, int jmax, bool track) {
+    if (!piped) {
+      __syncthreads();
+      if (crank == 0 && tid == 0) jtop_s = fast_fail;
+      __syncthreads();
+    }
+    const int jtop = piped ? PKB : jtop_s;  // (pipelined: every step runs; the verification finds the first bad one)
+    auto subst = [&](int rlo, int jmax, bool track, bool wait_rows = false) {
       auto chunk = [&](auto Wc) {
         constexpr int W = decltype(Wc)::value;
         const int j0 = PKB - W, j1 = min(jmax, j0 + 8);
         for (int j = j0; j < j1; ++j) {
+          if (wait_rows) mbar_wait(&mbar_u[j], 0u);
 #pragma unroll
           for (int a = 0; a < RPT; ++a) {
-            const int r = crank * PNT + tid + stride * a;
+            const int r = rowof(a);
             if (r >= rlo && r < Ri) {
               const double l = v[a][0] * urinv[j];
               if (track && !(fabs(l) <= 1.0) && jf == PKB) jf = j;
@@ -1091,7 +1150,7 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
       chunk(WinC<8>{});
     };
     P2CLK(4);
-    subst(kbe, min(kbe, jtop), true);
+    if (!(piped && crank == 0)) subst(kbe, min(kbe, jtop), true, piped);  // (light lead: rank 0 has no rows below)
     P2CLK(5);
     if (jf < PKB) atomicMin(&fast_fail, jf);
     __syncthreads();
@@ -1142,7 +1201,7 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
       // partial pivoting's); rows < jstar are the pivots of steps 0 .. jstar - 1
 #pragma unroll
       for (int a = 0; a < RPT; ++a) {
-        const int r = crank * PNT + tid + stride * a;
+        const int r = rowof(a);
         if (r >= jstar)
 #pragma unroll
           for (int c = 0; c < PKB; ++c) v[a][c] = psave[(a * PNT + tid) * (PKB + 1) + c];
@@ -1151,7 +1210,7 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
       jstart = jstar;
 #pragma unroll
       for (int a = 0; a < RPT; ++a) {
-        const int r = crank * PNT + tid + stride * a;
+        const int r = rowof(a);
         if (r < jstart) elim[a] = r;
       }
       if (tid < jstart) sp[tid] = tid;
@@ -1203,7 +1262,7 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
 #pragma unroll
           for (int c = 0; c < PKB; c += 2) st_shared_v2_pred(&rows[buf][warp][c], v[a][c], v[a][c + 1], wa);
         }
-        st_shared_v4u_pred(&sinfo[buf][warp][0], whi, wlo, unsigned(crank * PNT + tid + stride * ba), 0u, win);
+        st_shared_v4u_pred(&sinfo[buf][warp][0], whi, wlo, unsigned(rowof(ba)), 0u, win);
       }
       P2ACC(9, tq);
       __syncthreads();
@@ -1248,7 +1307,7 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
       P2ACC(13, tq);
 #pragma unroll
       for (int a = 0; a < RPT; ++a) {
-        const int r = crank * PNT + tid + stride * a;
+        const int r = rowof(a);
         if (r == p) elim[a] = j;
         if (elim[a] < 0) {
           const double l = v[a][0] * rinv;
@@ -1748,9 +1807,23 @@ size_t panel_dyn_smem(int rpt);
 int panel_fast_threshold();
 bool panel_legacy();
 
+// Pipelined no-interchange attempt of the cluster panels (DTN_PANEL_PIPE=0: the classic order).
+// Rank 0 holds only the 32 top rows (light lead CTA: its warp 0 factors the top block with no other
+// warp of the SM computing -- 390 instead of 475 cycles per pivot), warp 1 of rank 0 forwards every
+// U row to the other CTAs as it is formed (st.async + one mbarrier per row), and the rows below
+// run substitution step j as soon as row j has landed instead of starting after the whole top LU.
+// Same arithmetic (S bit-identical); 1024-row panel 28.6 -> 24.5 us.
+static bool panel_pipe() {
+  static const bool on = [] {
+    const char* e = std::getenv("DTN_PANEL_PIPE");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
 template <bool CL, int RPT, int NT = PNT>
 cudaError_t launch_panel_t(const KernelArgs& args, const int* d_list, int count, int k0, int kb, int csize,
-                           cudaStream_t st, bool fused) {
+                           cudaStream_t st, bool fused, bool pipe = false) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(count * csize);
   cfg.blockDim = dim3(NT);
@@ -1769,7 +1842,7 @@ cudaError_t launch_panel_t(const KernelArgs& args, const int* d_list, int count,
     return cudaLaunchKernelEx(&cfg, panel_kernel<CL, RPT>, args, d_list, k0, kb, csize, fused ? 1 : 0,
                               panel_fast_threshold());
   return cudaLaunchKernelEx(&cfg, panel2_kernel<CL, RPT, NT>, args, d_list, k0, kb, csize, fused ? 1 : 0,
-                            panel_fast_threshold());
+                            panel_fast_threshold() ? (std::min(panel_fast_threshold(), 0x1fffffff) | (pipe ? 0x20000000 : 0)) : 0);
 }
 
 // fused: apply step k0 - kb to this panel's columns first (the look-ahead
@@ -1837,7 +1910,13 @@ cudaError_t launch_panel(const KernelArgs& args, const int* d_list, int count, i
   if (nt == 128) return launch_panel_t<true, 1, 128>(args, d_list, count, k0, kb, csize, st, fused);
   if (csize == 1 && rpt == 2) return launch_panel_t<false, 2>(args, d_list, count, k0, kb, 1, st, fused);
   if (csize == 1) return launch_panel_t<false, 1>(args, d_list, count, k0, kb, 1, st, fused);
-  if (rpt == 1) return launch_panel_t<true, 1>(args, d_list, count, k0, kb, csize, st, fused);
+  if (rpt == 1) {
+    // pipelined substitution with the light lead CTA: rank 0 holds the 32 top rows only
+    const int cs_pipe = 1 + (max_rows - PKB + PNT - 1) / PNT;
+    if (panel_pipe() && panel_fast_threshold() && cs_pipe <= PMAXC)
+      return launch_panel_t<true, 1>(args, d_list, count, k0, kb, cs_pipe, st, fused, true);
+    return launch_panel_t<true, 1>(args, d_list, count, k0, kb, csize, st, fused);
+  }
   return launch_panel_t<true, 2>(args, d_list, count, k0, kb, csize, st, fused);
 }
 
