@@ -1092,14 +1092,17 @@ __global__ void __launch_bounds__(NT) panel2_kernel(KernelArgs args, const int* 
       }
     }
     if constexpr (CL) {
-      if (piped && crank == 0 && warp == 1) {
-        // forwarding warp: U row j (shifted) and 1 / u_jj to every other CTA as soon as warp 0 has
-        // formed it (st.async, completing that CTA's barrier of row j)
+      const int nfw = min(PNW - 1, (csize - 1 + 3) / 4);  // one forwarding warp per 4 destinations
+      if (piped && crank == 0 && warp >= 1 && warp <= nfw) {
+        // forwarding warps (1 .. nfw, the destinations dealt round-robin; more warps would compete
+        // with warp 0's top LU on this SM): U row j (shifted) and
+        // 1 / u_jj to the other CTAs as soon as warp 0 has formed it (st.async, completing the
+        // destination's barrier of row j)
         for (int j = 0; j < kbe; ++j) {
           mbar_wait(&mbar_u[j], 0u);
           const double val = ub[j * PLD + lane];
           const double rj = urinv[j];
-          for (int d = 1; d < csize; ++d) {
+          for (int d = warp; d < csize; d += nfw) {
             const unsigned mb = cluster_map(&mbar_u[j], d);
             st_async_b64(cluster_map(ub + j * PLD + lane, d), __double_as_longlong(val), mb);
             if (lane == 0) st_async_b64(cluster_map(urinv + j, d), __double_as_longlong(rj), mb);
@@ -1907,7 +1910,12 @@ cudaError_t launch_panel(const KernelArgs& args, const int* d_list, int count, i
   if (nt == 128 && rpt == 2 && csize == 1) return launch_panel_t<false, 2, 128>(args, d_list, count, k0, kb, 1, st, fused);
   if (nt == 128 && rpt == 2) return launch_panel_t<true, 2, 128>(args, d_list, count, k0, kb, csize, st, fused);
   if (nt == 128 && csize == 1) return launch_panel_t<false, 1, 128>(args, d_list, count, k0, kb, 1, st, fused);
-  if (nt == 128) return launch_panel_t<true, 1, 128>(args, d_list, count, k0, kb, csize, st, fused);
+  if (nt == 128) {
+    const int cs_pipe = 1 + (max_rows - PKB + 127) / 128;
+    if (panel_pipe() && panel_fast_threshold() && cs_pipe <= PMAXC)
+      return launch_panel_t<true, 1, 128>(args, d_list, count, k0, kb, cs_pipe, st, fused, true);
+    return launch_panel_t<true, 1, 128>(args, d_list, count, k0, kb, csize, st, fused);
+  }
   if (csize == 1 && rpt == 2) return launch_panel_t<false, 2>(args, d_list, count, k0, kb, 1, st, fused);
   if (csize == 1) return launch_panel_t<false, 1>(args, d_list, count, k0, kb, 1, st, fused);
   if (rpt == 1) {
