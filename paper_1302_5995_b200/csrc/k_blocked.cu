@@ -1787,7 +1787,7 @@ void panel_shape(int max_rows, int* rpt, int* csize, int* nt) {
     *nt = 128;
     return;
   }
-  if (!panel_legacy() && panel_small_nt() == 128 && max_rows > PNT && max_rows <= PMAXC * 128) {
+  if (!panel_legacy() && panel_small_nt() == 128 && max_rows > PNT && max_rows <= PKB + (PMAXC - 1) * 128) {
     *rpt = 1;
     *csize = (max_rows + 127) / 128;
     *nt = 128;
